@@ -1,0 +1,273 @@
+/*
+ * pdlp_b200.h — C-ABI of the B200-native PDLP/PDHG solver (libpdlp_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (`pdhglp`, header-only C++20) has no FFI of its own; its entry point is
+ *
+ *     pdhglp::SolveResult pdhglp::solve(const LpProblem&, const SolverOptions&)
+ *         (reference: proj/include/pdhglp/solver.hpp:535-608)
+ *
+ * and every struct below mirrors one of the reference's structs field for
+ * field, with plain pointers and sizes instead of std::vector:
+ *
+ *   pdlp_csr_view            <- pdhglp::CompressedLayout      sparse.hpp:21-28
+ *   pdlp_problem_view        <- pdhglp::LpProblem + SparseMatrix problem.hpp:15-25, sparse.hpp:33-42
+ *   pdlp_options             <- pdhglp::SolverOptions          solver.hpp:69-90
+ *                               (+ TerminationTolerances residuals.hpp:187-191,
+ *                                  RestartThresholds restarts.hpp:235-239)
+ *   pdlp_iteration_record    <- pdhglp::IterationRecord        solver.hpp:59-65
+ *   pdlp_residual_summary    <- pdhglp::ResidualSummary        residuals.hpp:66-73
+ *   pdlp_result              <- pdhglp::SolveResult            solver.hpp:92-108
+ *                               (+ InfeasibilityCertificate residuals.hpp:202-210)
+ *
+ * The C++ drop-in (include/pdhglp_b200/solver.hpp) marshals the reference's
+ * own structs onto these and calls pdlp_solve(); see INTEGRATION.md.
+ *
+ * Conventions: 0 = OK, negative = error (pdlp_last_error() has the text).
+ * No C++ exception crosses this boundary.  Host arrays are borrowed for the
+ * duration of the call only.  All indices are int64 on the host side (as in
+ * the reference); the device copy uses int32 column indices.
+ *
+ * There is NO CPU fallback: every entry point that computes runs CUDA
+ * kernels on the selected device and fails with PDLP_ERR_CUDA when no
+ * device is usable.
+ */
+#ifndef PDLP_B200_H_
+#define PDLP_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDLP_ABI_VERSION 1
+
+/* Error codes. */
+#define PDLP_OK 0
+#define PDLP_ERR_INVALID_PROBLEM -1 /* reference: std::invalid_argument, solver.hpp:538-541 */
+#define PDLP_ERR_INVALID_ARGUMENT -2
+#define PDLP_ERR_CUDA -3
+#define PDLP_ERR_OUT_OF_MEMORY -4
+#define PDLP_ERR_INTERNAL -5
+
+/* SolveStatus, same order as reference solver.hpp:35-42. */
+#define PDLP_STATUS_OPTIMAL 0
+#define PDLP_STATUS_PRIMAL_INFEASIBLE 1
+#define PDLP_STATUS_DUAL_INFEASIBLE 2
+#define PDLP_STATUS_ITERATION_LIMIT 3
+#define PDLP_STATUS_TIME_LIMIT 4
+#define PDLP_STATUS_NUMERICAL_ERROR 5
+
+/* CertificateKind, reference residuals.hpp:200. */
+#define PDLP_CERT_PRIMAL_INFEASIBLE 0
+#define PDLP_CERT_DUAL_INFEASIBLE 1
+
+/* Execution modes (B200 extension, additive to SolverOptions). */
+#define PDLP_MODE_PERF 0   /* load-balanced SpMV + tree reductions (deterministic) */
+#define PDLP_MODE_PARITY 1 /* bit-exact emulation of the reference's shard plan   */
+
+/* One compressed orientation (reference CompressedLayout, sparse.hpp:21-28). */
+typedef struct pdlp_csr_view {
+  int64_t primary_dim; /* rows for by_row, cols for by_col */
+  int64_t nnz;
+  const int64_t* start; /* primary_dim + 1 */
+  const int64_t* index; /* nnz, sorted within each line */
+  const double* value;  /* nnz */
+} pdlp_csr_view;
+
+/* min c'x  s.t.  con_lower <= A x <= con_upper, var_lower <= x <= var_upper
+ * (reference LpProblem, problem.hpp:15-25; matrix held in both layouts as in
+ * SparseMatrix, sparse.hpp:33-42). */
+typedef struct pdlp_problem_view {
+  int64_t rows;
+  int64_t cols;
+  pdlp_csr_view by_row;
+  pdlp_csr_view by_col;
+  const double* objective; /* cols */
+  const double* con_lower; /* rows */
+  const double* con_upper; /* rows */
+  const double* var_lower; /* cols */
+  const double* var_upper; /* cols */
+} pdlp_problem_view;
+
+/* Reference IterationRecord (solver.hpp:59-65).  x/y are host copies of the
+ * scaled-space iterate, valid only during the callback. */
+typedef struct pdlp_iteration_record {
+  int64_t iteration;
+  const double* x;
+  int64_t x_len;
+  const double* y;
+  int64_t y_len;
+  double eta;
+  double omega;
+} pdlp_iteration_record;
+
+typedef void (*pdlp_observer_fn)(void* user, const pdlp_iteration_record* rec);
+
+/* Reference SolverOptions (solver.hpp:69-90) flattened; defaults via
+ * pdlp_default_options(). */
+typedef struct pdlp_options {
+  /* TerminationTolerances, residuals.hpp:187-191 */
+  double eps_primal;
+  double eps_dual;
+  double eps_rel_gap;
+  int64_t iteration_limit;
+  double time_limit_seconds; /* +inf = none */
+  int32_t threads;
+  int32_t shards_per_thread;
+  int32_t enable_scaling;
+  int32_t ruiz_passes;
+  int32_t pock_chambolle;
+  int32_t enable_polish;
+  int32_t enable_restarts;
+  int32_t detect_infeasibility;
+  double eps_ray;
+  int64_t check_interval;
+  /* RestartThresholds, restarts.hpp:235-239 */
+  double restart_sufficient;
+  double restart_necessary;
+  double restart_artificial;
+  int32_t has_fixed_step_size;
+  int32_t has_fixed_primal_weight;
+  double fixed_step_size;
+  double fixed_primal_weight;
+  int32_t logging;
+  int32_t _pad0;
+  pdlp_observer_fn observer;
+  void* observer_user;
+  /* ---- B200 extensions (additive; the reference fields above are unchanged) */
+  int32_t mode;   /* PDLP_MODE_PERF (default) or PDLP_MODE_PARITY */
+  int32_t device; /* CUDA device ordinal */
+  int32_t use_graphs; /* capture the 64-step attempt block in a CUDA graph */
+  int32_t profile_kernels; /* CUDA events around every step kernel (bench roofline) */
+  /* Timed region of the main loop starts once this many iterations are done
+   * (right after that cadence); see pdlp_result.timed_*.  0 = whole loop. */
+  int64_t timing_warmup_iterations;
+} pdlp_options;
+
+/* Reference ResidualSummary, residuals.hpp:66-73. */
+typedef struct pdlp_residual_summary {
+  double primal_residual_inf;
+  double dual_residual_inf;
+  double primal_objective;
+  double dual_objective;
+  double abs_gap;
+  double rel_gap;
+} pdlp_residual_summary;
+
+/* Reference SolveResult (solver.hpp:92-108) + InfeasibilityCertificate
+ * (residuals.hpp:202-210).  Vector outputs go to caller-owned buffers; any of
+ * them may be NULL to skip the copy. */
+typedef struct pdlp_result {
+  int32_t status;
+  int32_t has_certificate;
+  double* x;             /* cols */
+  double* y;             /* rows */
+  double* reduced_costs; /* cols */
+  pdlp_residual_summary summary;
+  /* certificate */
+  int32_t cert_kind;
+  int32_t _pad0;
+  double* cert_ray_x; /* cols (dual infeasible) */
+  double* cert_ray_y; /* rows (primal infeasible) */
+  double* cert_ray_r; /* cols (primal infeasible) */
+  double cert_residual_inf;
+  double cert_objective;
+  char cert_source[32];
+  /* statistics */
+  int64_t iterations;
+  int64_t polish_iterations;
+  int64_t restarts;
+  int64_t step_retries;
+  double final_step_size;
+  double final_primal_weight;
+  double min_step_size_limit;
+  double solve_seconds;
+  char termination_detail[256];
+  /* B200 extensions: timing breakdown */
+  int64_t attempts;           /* step attempts (accepted + retries), main + polish */
+  double upload_seconds;      /* host->device copy of the problem */
+  double precondition_seconds;
+  double loop_seconds;        /* wall time inside run_inner (main loop) */
+  double step_seconds;        /* device time of the step kernels only (CUDA events) */
+  double timed_seconds;       /* CUDA-event time of the timed region (main loop) */
+  int64_t timed_iterations;   /* accepted main-loop steps inside it */
+  int64_t timed_attempts;     /* step attempts inside it */
+  /* profile_kernels: summed device time and launch count per step kernel:
+   * [0] primal pass, [1] row pass (+dual update), [2] column pass (+decision),
+   * [3] parity-mode reductions/decision */
+  double kernel_seconds[4];
+  int64_t kernel_launches[4];
+} pdlp_result;
+
+/* ---------------------------------------------------------------- solve --- */
+
+/* Defaults equal to the reference's SolverOptions{} (solver.hpp:69-90). */
+void pdlp_default_options(pdlp_options* opt);
+
+/* The drop-in: reference pdhglp::solve (solver.hpp:535-608). */
+int pdlp_solve(const pdlp_problem_view* problem, const pdlp_options* options,
+               pdlp_result* result);
+
+const char* pdlp_last_error(void);
+int pdlp_abi_version(void);
+/* Number of CUDA devices visible, or a negative error code. */
+int pdlp_device_count(void);
+
+/* ------------------------------------------------------ component entry --- *
+ * Single-component entry points used by the parity tests (each runs the same
+ * device kernels the solver uses; host arrays in, host arrays out). */
+
+/* reference pdhg_step (step.hpp:100-115): one step at (omega, eta) from (x, y)
+ * with aty = A'y computed on device.  Returns 1 in *finite when every output
+ * entry is finite. */
+int pdlp_pdhg_step(const pdlp_problem_view* problem, const double* x, const double* y,
+                   double omega, double eta, int32_t mode, int32_t shards, double* x_out,
+                   double* y_out, int32_t* finite);
+
+/* reference adaptive_step (step.hpp:161-193) on the iterate (x, y, aty).
+ * io_state = {eta_hat, k, max_retries(as double), omega}; on return the
+ * iterate arrays hold the new iterate, prev_* the previous one (the trial
+ * buffers), stats = {accepted, retries, min_eta_bar, eta_used}.
+ * Returns outcome 0 = accepted, 1 = numerical error in *outcome. */
+int pdlp_adaptive_step(const pdlp_problem_view* problem, double* x, double* y, double* aty,
+                       double* io_state, int32_t mode, int32_t shards, double* prev_x,
+                       double* prev_y, double* stats, int32_t* outcome);
+
+/* kernels::spmv / spmv_transpose (kernels.hpp:30-59). */
+int pdlp_spmv(const pdlp_problem_view* problem, const double* x, double* out, int32_t mode);
+int pdlp_spmv_transpose(const pdlp_problem_view* problem, const double* y, double* out,
+                        int32_t mode);
+
+/* apply_rescaling (rescaling.hpp:137-143).  Outputs: scaled by_row/by_col
+ * values (nnz each), scaled objective/bounds, row_scale (rows), col_scale
+ * (cols). */
+int pdlp_apply_rescaling(const pdlp_problem_view* problem, int32_t ruiz_passes,
+                         int32_t pock_chambolle, double* row_values, double* col_values,
+                         double* objective, double* con_lower, double* con_upper,
+                         double* var_lower, double* var_upper, double* row_scale,
+                         double* col_scale);
+
+/* normalized_duality_gap (restarts.hpp:107-220) with ax = A x, aty = A'y. */
+int pdlp_normalized_duality_gap(const pdlp_problem_view* problem, const double* x,
+                                const double* y, const double* ax, const double* aty,
+                                double omega, double r, int32_t mode, double* gap);
+
+/* recover_reduced_costs (residuals.hpp:49-64) + kkt_residuals
+ * (residuals.hpp:135-158) on the given problem.  rc_mode 0 = Natural,
+ * 1 = BoundRobust.  r_out may be NULL. */
+int pdlp_kkt_residuals(const pdlp_problem_view* problem, const double* x, const double* y,
+                       int32_t rc_mode, int32_t mode, double* r_out,
+                       pdlp_residual_summary* summary);
+
+/* Scalar step-size rules (step.hpp:126-141), evaluated by the same device code
+ * the decision kernel uses (schedule factors from the host table). */
+int pdlp_step_size_rules(double movement, double curvature, double eta_bar, double eta,
+                         int64_t k, double* limit_out, double* next_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PDLP_B200_H_ */

@@ -1,0 +1,92 @@
+/*
+ * pdlp_gen.h — seeded synthetic LP instances for the BASELINE.json configs
+ * (libpdlp_gen.so; host-only data plumbing, not part of the solve path).
+ *
+ * The reference's own generator (proj/include/pdhglp/generator.hpp:96-104)
+ * samples an m×n Bernoulli mask and cannot build the BASELINE configs, so
+ * these are new recipes in the same splitmix64 style (generator.hpp:75-94),
+ * restated from BASELINE.json configs[0..4] / SURVEY.md §8(d):
+ *
+ *   C0  pdlp_gen_random_lp with params from pdlp_gen_c0_params()
+ *   C1  pdlp_gen_transport(2000, 2000, seed)
+ *   C2  pdlp_gen_random_lp with params from pdlp_gen_c2_params()
+ *   C3  pdlp_gen_unit_commitment(8760, 1000, seed)
+ *   C4  pdlp_gen_random_lp with params from pdlp_gen_c4_params()
+ *
+ * Instances own their arrays; pdlp_instance_view() exposes them as the
+ * solver's pdlp_problem_view.
+ */
+#ifndef PDLP_GEN_H_
+#define PDLP_GEN_H_
+
+#include <stdint.h>
+
+#include "pdlp_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pdlp_instance pdlp_instance;
+
+typedef struct pdlp_gen_params {
+  int64_t rows;
+  int64_t cols;
+  /* per-column entry counts: 0 = fixed (count_fixed), 1 = discrete power law
+   * P(k) ~ k^-alpha on [kmin, kmax] (inverse-CDF sampling, rejection above kmax) */
+  int32_t count_kind;
+  int32_t value_kind; /* 0 = magnitude uniform [lo, hi], 1 = log-uniform [lo, hi]; random sign */
+  int64_t count_fixed;
+  double alpha;
+  int64_t kmin;
+  int64_t kmax;
+  double value_lo;
+  double value_hi;
+  /* row types: the first round(eq_frac*rows) rows are equalities when
+   * eq_rows_first != 0, else each row is an equality with prob. eq_frac;
+   * the others are <= rows with slack U[0, slack_hi]. */
+  double eq_frac;
+  int32_t eq_rows_first;
+  /* variable bounds: 0 = all [0, box_hi] (C0); 1 = mix [0,inf) 60 % / [l,u] 30 % / free 10 % (C2) */
+  int32_t bound_kind;
+  double box_hi;
+  double slack_hi;
+  uint64_t seed;
+} pdlp_gen_params;
+
+void pdlp_gen_c0_params(pdlp_gen_params* p, uint64_t seed);
+void pdlp_gen_c2_params(pdlp_gen_params* p, uint64_t seed);
+void pdlp_gen_c4_params(pdlp_gen_params* p, uint64_t seed);
+
+/* Random sparse LP constructed feasible and bounded (C0/C2/C4 recipes). */
+pdlp_instance* pdlp_gen_random_lp(const pdlp_gen_params* params);
+
+/* Transportation LP (C1): `sources` supply rows sum_d x_sd <= s_s (s integer
+ * U[50,150]), `sinks` demand rows sum_s x_sd >= d_d (d scaled to 95 % of total
+ * supply), n = sources*sinks flows x >= 0, all coefficients +1, costs U[1,100]. */
+pdlp_instance* pdlp_gen_transport(int64_t sources, int64_t sinks, uint64_t seed);
+
+/* Unit-commitment-style staircase LP relaxation (C3).  Variables p_gt >= 0,
+ * u_gt in [0,1]; rows: demand balance per period, ramp rows linking adjacent
+ * periods, capacity rows p_gt - P_g u_gt <= 0. */
+pdlp_instance* pdlp_gen_unit_commitment(int64_t periods, int64_t generators, uint64_t seed);
+
+/* Build an instance from triplets with the reference's from_triplets
+ * semantics (sparse.hpp:48-115): counting sort by line, stable sort by
+ * secondary index, duplicates summed in input order.  Vectors are copied. */
+pdlp_instance* pdlp_instance_from_triplets(int64_t rows, int64_t cols, int64_t count,
+                                           const int64_t* r, const int64_t* c,
+                                           const double* v, const double* objective,
+                                           const double* con_lower, const double* con_upper,
+                                           const double* var_lower, const double* var_upper);
+
+void pdlp_instance_view(const pdlp_instance* inst, pdlp_problem_view* view);
+/* Known feasible primal point (length cols) or NULL. */
+const double* pdlp_instance_feasible_point(const pdlp_instance* inst);
+void pdlp_instance_free(pdlp_instance* inst);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PDLP_GEN_H_ */

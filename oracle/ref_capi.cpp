@@ -1,0 +1,400 @@
+// oracle/ref_capi.cpp — TEST INFRASTRUCTURE ONLY (never linked into the
+// product).  A thin C-ABI over the UNMODIFIED reference library compiled from
+// /root/reference/proj/include (header-only C++20), so that Python tests and
+// bench.py's cpu_baseline / --impl reference arm can call the reference
+// implementation of the PDHG path through the same plain-pointer structs the
+// product exposes (include/pdlp_b200.h).  Built by oracle/Makefile into
+// oracle/_ref/libpdhglp_ref.so with  g++ -std=c++20 -O2 -ffp-contract=off
+// (no -march: FMA contraction breaks the reference, SURVEY.md §0 finding 6).
+//
+// Only marshalling lives here; every number comes from the reference code.
+
+#include <pdhglp/generator.hpp>
+#include <pdhglp/rescaling.hpp>
+#include <pdhglp/residuals.hpp>
+#include <pdhglp/restarts.hpp>
+#include <pdhglp/solver.hpp>
+#include <pdhglp/step.hpp>
+
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "pdlp_b200.h"
+
+using namespace pdhglp;
+
+namespace {
+
+thread_local std::string g_err;
+
+CompressedLayout to_layout(const pdlp_csr_view& v) {
+  CompressedLayout out;
+  out.start.assign(v.start, v.start + v.primary_dim + 1);
+  out.index.assign(v.index, v.index + v.nnz);
+  out.value.assign(v.value, v.value + v.nnz);
+  return out;
+}
+
+LpProblem to_problem(const pdlp_problem_view* pv) {
+  LpProblem p;
+  p.a.rows = pv->rows;
+  p.a.cols = pv->cols;
+  p.a.by_row = to_layout(pv->by_row);
+  p.a.by_col = to_layout(pv->by_col);
+  p.objective.assign(pv->objective, pv->objective + pv->cols);
+  p.con_lower.assign(pv->con_lower, pv->con_lower + pv->rows);
+  p.con_upper.assign(pv->con_upper, pv->con_upper + pv->rows);
+  p.var_lower.assign(pv->var_lower, pv->var_lower + pv->cols);
+  p.var_upper.assign(pv->var_upper, pv->var_upper + pv->cols);
+  return p;
+}
+
+void copy_out(const Vector& v, double* dst) {
+  if (dst != nullptr && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+}
+
+SolverOptions to_options(const pdlp_options* o) {
+  SolverOptions s;
+  s.tolerances.eps_primal = o->eps_primal;
+  s.tolerances.eps_dual = o->eps_dual;
+  s.tolerances.eps_rel_gap = o->eps_rel_gap;
+  s.iteration_limit = o->iteration_limit;
+  s.time_limit_seconds = o->time_limit_seconds;
+  s.threads = o->threads;
+  s.shards_per_thread = o->shards_per_thread;
+  s.enable_scaling = o->enable_scaling != 0;
+  s.ruiz_passes = o->ruiz_passes;
+  s.pock_chambolle = o->pock_chambolle != 0;
+  s.enable_polish = o->enable_polish != 0;
+  s.enable_restarts = o->enable_restarts != 0;
+  s.detect_infeasibility = o->detect_infeasibility != 0;
+  s.eps_ray = o->eps_ray;
+  s.check_interval = o->check_interval;
+  s.restart_thresholds.sufficient = o->restart_sufficient;
+  s.restart_thresholds.necessary = o->restart_necessary;
+  s.restart_thresholds.artificial = o->restart_artificial;
+  if (o->has_fixed_step_size) s.fixed_step_size = o->fixed_step_size;
+  if (o->has_fixed_primal_weight) s.fixed_primal_weight = o->fixed_primal_weight;
+  s.logging = o->logging != 0;
+  if (o->observer != nullptr) {
+    pdlp_observer_fn fn = o->observer;
+    void* user = o->observer_user;
+    s.observer = [fn, user](const IterationRecord& rec) {
+      pdlp_iteration_record r;
+      r.iteration = rec.iteration;
+      r.x = rec.x->data();
+      r.x_len = static_cast<int64_t>(rec.x->size());
+      r.y = rec.y->data();
+      r.y_len = static_cast<int64_t>(rec.y->size());
+      r.eta = rec.eta;
+      r.omega = rec.omega;
+      fn(user, &r);
+    };
+  }
+  return s;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return PDLP_ERR_INVALID_PROBLEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PDLP_ERR_INTERNAL;
+  }
+}
+
+struct RefInstance {
+  GeneratedInstance inst;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+void ref_default_options(pdlp_options* o) {
+  const SolverOptions s{};
+  std::memset(o, 0, sizeof(*o));
+  o->eps_primal = s.tolerances.eps_primal;
+  o->eps_dual = s.tolerances.eps_dual;
+  o->eps_rel_gap = s.tolerances.eps_rel_gap;
+  o->iteration_limit = s.iteration_limit;
+  o->time_limit_seconds = s.time_limit_seconds;
+  o->threads = s.threads;
+  o->shards_per_thread = s.shards_per_thread;
+  o->enable_scaling = s.enable_scaling;
+  o->ruiz_passes = s.ruiz_passes;
+  o->pock_chambolle = s.pock_chambolle;
+  o->enable_polish = s.enable_polish;
+  o->enable_restarts = s.enable_restarts;
+  o->detect_infeasibility = s.detect_infeasibility;
+  o->eps_ray = s.eps_ray;
+  o->check_interval = s.check_interval;
+  o->restart_sufficient = s.restart_thresholds.sufficient;
+  o->restart_necessary = s.restart_thresholds.necessary;
+  o->restart_artificial = s.restart_thresholds.artificial;
+  o->logging = s.logging;
+}
+
+int ref_solve(const pdlp_problem_view* pv, const pdlp_options* o, pdlp_result* res) {
+  return guarded([&] {
+    const LpProblem p = to_problem(pv);
+    const SolverOptions s = to_options(o);
+    SolveResult r = solve(p, s);
+    res->status = static_cast<int32_t>(r.status);
+    copy_out(r.x, res->x);
+    copy_out(r.y, res->y);
+    copy_out(r.reduced_costs, res->reduced_costs);
+    res->summary.primal_residual_inf = r.summary.primal_residual_inf;
+    res->summary.dual_residual_inf = r.summary.dual_residual_inf;
+    res->summary.primal_objective = r.summary.primal_objective;
+    res->summary.dual_objective = r.summary.dual_objective;
+    res->summary.abs_gap = r.summary.abs_gap;
+    res->summary.rel_gap = r.summary.rel_gap;
+    res->has_certificate = r.certificate.has_value() ? 1 : 0;
+    if (r.certificate) {
+      res->cert_kind = static_cast<int32_t>(r.certificate->kind);
+      copy_out(r.certificate->ray_x, res->cert_ray_x);
+      copy_out(r.certificate->ray_y, res->cert_ray_y);
+      copy_out(r.certificate->ray_r, res->cert_ray_r);
+      res->cert_residual_inf = r.certificate->residual_inf;
+      res->cert_objective = r.certificate->objective;
+      std::strncpy(res->cert_source, r.certificate->source, sizeof(res->cert_source) - 1);
+    }
+    res->iterations = r.iterations;
+    res->polish_iterations = r.polish_iterations;
+    res->restarts = r.restarts;
+    res->step_retries = r.step_retries;
+    res->final_step_size = r.final_step_size;
+    res->final_primal_weight = r.final_primal_weight;
+    res->min_step_size_limit = r.min_step_size_limit;
+    res->solve_seconds = r.solve_seconds;
+    std::strncpy(res->termination_detail, r.termination_detail.c_str(),
+                 sizeof(res->termination_detail) - 1);
+    return PDLP_OK;
+  });
+}
+
+int ref_pdhg_step(const pdlp_problem_view* pv, const double* x, const double* y, double omega,
+                  double eta, double* x_out, double* y_out, int32_t* finite) {
+  return guarded([&] {
+    const LpProblem p = to_problem(pv);
+    PrimalDualIterate z{Vector(x, x + pv->cols), Vector(y, y + pv->rows)};
+    auto next = pdhg_step(p, z, omega, eta);
+    *finite = next.has_value() ? 1 : 0;
+    if (next) {
+      copy_out(next->x, x_out);
+      copy_out(next->y, y_out);
+    }
+    return PDLP_OK;
+  });
+}
+
+// io_state = {eta_hat, k, max_retries, omega}; stats = {accepted, retries,
+// min_eta_bar, eta_used}.
+int ref_adaptive_step(const pdlp_problem_view* pv, double* x, double* y, double* aty,
+                      double* io_state, int32_t threads, int32_t spt, double* prev_x,
+                      double* prev_y, double* stats, int32_t* outcome) {
+  return guarded([&] {
+    const LpProblem p = to_problem(pv);
+    Executor ex(p.cols(), p.rows(), threads, spt);
+    PdhgIterate z{Vector(x, x + pv->cols), Vector(y, y + pv->rows),
+                  Vector(aty, aty + pv->cols)};
+    PdhgWorkspace ws;
+    ws.resize(p.cols(), p.rows());
+    StepSizeControl ctrl;
+    ctrl.eta_hat = io_state[0];
+    ctrl.k = static_cast<Index>(io_state[1]);
+    ctrl.max_retries = static_cast<int>(io_state[2]);
+    const double omega = io_state[3];
+    StepStats st;
+    Scalar eta_used = 0.0;
+    const StepOutcome out = adaptive_step(p, ex, z, omega, ctrl, ws, st, eta_used);
+    *outcome = out == StepOutcome::Accepted ? 0 : 1;
+    copy_out(z.x, x);
+    copy_out(z.y, y);
+    copy_out(z.aty, aty);
+    copy_out(ws.x_trial, prev_x);
+    copy_out(ws.y_trial, prev_y);
+    io_state[0] = ctrl.eta_hat;
+    io_state[1] = static_cast<double>(ctrl.k);
+    stats[0] = static_cast<double>(st.accepted_steps);
+    stats[1] = static_cast<double>(st.retries);
+    stats[2] = st.min_eta_bar;
+    stats[3] = eta_used;
+    return PDLP_OK;
+  });
+}
+
+int ref_spmv(const pdlp_problem_view* pv, const double* x, double* out, int32_t threads,
+             int32_t spt) {
+  return guarded([&] {
+    const LpProblem p = to_problem(pv);
+    Executor ex(p.cols(), p.rows(), threads, spt);
+    Vector xv(x, x + pv->cols), o(static_cast<size_t>(pv->rows));
+    kernels::spmv(ex.pool, ex.y_plan, p.a, xv, o);
+    copy_out(o, out);
+    return PDLP_OK;
+  });
+}
+
+int ref_spmv_transpose(const pdlp_problem_view* pv, const double* y, double* out,
+                       int32_t threads, int32_t spt) {
+  return guarded([&] {
+    const LpProblem p = to_problem(pv);
+    Executor ex(p.cols(), p.rows(), threads, spt);
+    Vector yv(y, y + pv->rows), o(static_cast<size_t>(pv->cols));
+    kernels::spmv_transpose(ex.pool, ex.x_plan, p.a, yv, o);
+    copy_out(o, out);
+    return PDLP_OK;
+  });
+}
+
+int ref_apply_rescaling(const pdlp_problem_view* pv, int32_t ruiz, int32_t pc,
+                        double* row_values, double* col_values, double* objective,
+                        double* con_lower, double* con_upper, double* var_lower,
+                        double* var_upper, double* row_scale, double* col_scale) {
+  return guarded([&] {
+    const LpProblem p = to_problem(pv);
+    ScaledProblem sp = apply_rescaling(p, ruiz, pc != 0);
+    copy_out(sp.problem.a.by_row.value, row_values);
+    copy_out(sp.problem.a.by_col.value, col_values);
+    copy_out(sp.problem.objective, objective);
+    copy_out(sp.problem.con_lower, con_lower);
+    copy_out(sp.problem.con_upper, con_upper);
+    copy_out(sp.problem.var_lower, var_lower);
+    copy_out(sp.problem.var_upper, var_upper);
+    copy_out(sp.info.row_scale, row_scale);
+    copy_out(sp.info.col_scale, col_scale);
+    return PDLP_OK;
+  });
+}
+
+int ref_normalized_duality_gap(const pdlp_problem_view* pv, const double* x, const double* y,
+                               const double* ax, const double* aty, double omega, double r,
+                               double* gap) {
+  return guarded([&] {
+    const LpProblem p = to_problem(pv);
+    GapWorkspace ws;
+    *gap = normalized_duality_gap(p, Vector(x, x + pv->cols), Vector(y, y + pv->rows),
+                                  Vector(ax, ax + pv->rows), Vector(aty, aty + pv->cols), omega,
+                                  r, ws);
+    return PDLP_OK;
+  });
+}
+
+int ref_kkt_residuals(const pdlp_problem_view* pv, const double* x, const double* y,
+                      int32_t rc_mode, double* r_out, pdlp_residual_summary* s) {
+  return guarded([&] {
+    const LpProblem p = to_problem(pv);
+    const Vector xv(x, x + pv->cols), yv(y, y + pv->rows);
+    const Vector r = recover_reduced_costs(
+        p, xv, yv, rc_mode == 0 ? ReducedCostMode::Natural : ReducedCostMode::BoundRobust);
+    const ResidualSummary rs = kkt_residuals(p, xv, yv, r);
+    copy_out(r, r_out);
+    s->primal_residual_inf = rs.primal_residual_inf;
+    s->dual_residual_inf = rs.dual_residual_inf;
+    s->primal_objective = rs.primal_objective;
+    s->dual_objective = rs.dual_objective;
+    s->abs_gap = rs.abs_gap;
+    s->rel_gap = rs.rel_gap;
+    return PDLP_OK;
+  });
+}
+
+int ref_step_size_rules(double movement, double curvature, double eta_bar, double eta,
+                        int64_t k, double* limit_out, double* next_out) {
+  *limit_out = step_size_limit(movement, curvature);
+  *next_out = next_step_size(eta_bar, eta, k);
+  return PDLP_OK;
+}
+
+double ref_initialize_primal_weight(const pdlp_problem_view* pv) {
+  return initialize_primal_weight(to_problem(pv));
+}
+
+double ref_initial_step_size(const pdlp_problem_view* pv) {
+  return initial_step_size(to_problem(pv));
+}
+
+// ---- instances from the reference generator (generator.hpp:347-374) ------
+
+void* ref_generate(int32_t kind, int64_t rows, int64_t cols, double density, uint64_t seed) {
+  try {
+    GeneratorSpec spec;
+    spec.kind = static_cast<InstanceKind>(kind);
+    spec.rows = rows;
+    spec.cols = cols;
+    spec.density = density;
+    spec.seed = seed;
+    auto* h = new RefInstance{generate_instance(spec)};
+    return h;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// Builds an instance from triplets with the reference's from_triplets
+// (sparse.hpp:107-115); bounds/objective copied from the given arrays.
+void* ref_from_triplets(int64_t rows, int64_t cols, int64_t count, const int64_t* r,
+                        const int64_t* c, const double* v, const double* objective,
+                        const double* con_lower, const double* con_upper,
+                        const double* var_lower, const double* var_upper) {
+  try {
+    std::vector<Triplet> t(static_cast<size_t>(count));
+    for (int64_t k = 0; k < count; ++k) t[static_cast<size_t>(k)] = {r[k], c[k], v[k]};
+    auto* h = new RefInstance{};
+    LpProblem& p = h->inst.problem;
+    p.a = SparseMatrix::from_triplets(rows, cols, t);
+    p.objective.assign(objective, objective + cols);
+    p.con_lower.assign(con_lower, con_lower + rows);
+    p.con_upper.assign(con_upper, con_upper + rows);
+    p.var_lower.assign(var_lower, var_lower + cols);
+    p.var_upper.assign(var_upper, var_upper + cols);
+    return h;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_instance_view(void* h, pdlp_problem_view* pv) {
+  const LpProblem& p = static_cast<RefInstance*>(h)->inst.problem;
+  pv->rows = p.rows();
+  pv->cols = p.cols();
+  pv->by_row = {p.a.by_row.primary_dim(), p.a.by_row.nonzeros(), p.a.by_row.start.data(),
+                p.a.by_row.index.data(), p.a.by_row.value.data()};
+  pv->by_col = {p.a.by_col.primary_dim(), p.a.by_col.nonzeros(), p.a.by_col.start.data(),
+                p.a.by_col.index.data(), p.a.by_col.value.data()};
+  pv->objective = p.objective.data();
+  pv->con_lower = p.con_lower.data();
+  pv->con_upper = p.con_upper.data();
+  pv->var_lower = p.var_lower.data();
+  pv->var_upper = p.var_upper.data();
+}
+
+// Optimal objective of a random-feasible instance (NaN when unknown).
+double ref_instance_optimal_objective(void* h) {
+  const auto& inst = static_cast<RefInstance*>(h)->inst;
+  return inst.optimal_objective.has_value() ? *inst.optimal_objective : std::nan("");
+}
+
+void ref_instance_free(void* h) { delete static_cast<RefInstance*>(h); }
+
+int ref_validate(const pdlp_problem_view* pv, char* msg, int32_t msg_len) {
+  const LpProblem p = to_problem(pv);
+  auto issue = validate(p);
+  if (!issue) return 0;
+  std::snprintf(msg, static_cast<size_t>(msg_len), "%s (index %lld)", issue->message.c_str(),
+                static_cast<long long>(issue->index));
+  return 1;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+"""In-tree build of the native libraries (no JIT cache, no pip install).
+
+    libpdlp_b200.so  — the solver: sm_100a CUDA kernels (k_*.cu) + the host C++
+                       driver and public C-ABI (solver.cpp), static cudart
+    libpdlp_gen.so   — seeded BASELINE instance generators (host C++)
+
+Every .cu file is compiled with ``-gencode arch=compute_100a,code=sm_100a
+-lineinfo -fmad=false`` (FMA contraction breaks the reference's exact dual
+cancellation, SURVEY.md §0 finding 6; wanted FMAs are explicit fma() calls).
+Rebuilds only what changed.  ``python -m paper_2501_07018_b200.build``.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "_build")
+INCLUDE = os.path.join(ROOT, "include")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CU_FLAGS = ARCH + [
+    "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--extended-lambda",
+    "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
+    f"-I{INCLUDE}", f"-I{CSRC}",
+]
+CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-ffp-contract=off",
+             f"-I{INCLUDE}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
+
+CU_SOURCES = ["k_step.cu", "k_vec.cu", "k_gap.cu"]
+CPP_SOURCES = ["solver.cpp"]
+HEADERS = ["common.cuh", "spmv.cuh", "reduce.cuh", "kernels.h", "device.hpp"]
+
+LIB = os.path.join(HERE, "libpdlp_b200.so")
+GEN_LIB = os.path.join(HERE, "libpdlp_gen.so")
+
+
+def _mtime(p: str) -> float:
+    return os.path.getmtime(p) if os.path.exists(p) else -1.0
+
+
+def _run(cmd: list[str]) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("build failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+    if r.stderr.strip():
+        sys.stderr.write(r.stderr)
+
+
+def build(verbose: bool = False) -> list[str]:
+    os.makedirs(OBJ, exist_ok=True)
+    hdr_time = max(_mtime(os.path.join(CSRC, h)) for h in HEADERS)
+    hdr_time = max(hdr_time, _mtime(os.path.join(INCLUDE, "pdlp_b200.h")))
+    jobs, objs = [], []
+    for src in CU_SOURCES + CPP_SOURCES:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(OBJ, src + ".o")
+        objs.append(obj)
+        if _mtime(obj) >= max(_mtime(path), hdr_time):
+            continue
+        if src.endswith(".cu"):
+            cmd = [NVCC] + CU_FLAGS + ["-c", path, "-o", obj]
+        else:
+            cmd = ["g++"] + CXX_FLAGS + ["-c", path, "-o", obj]
+        jobs.append(cmd)
+    if jobs:
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            for cmd in jobs:
+                if verbose:
+                    print(" ".join(cmd))
+            list(ex.map(_run, jobs))
+    if jobs or _mtime(LIB) < max(_mtime(o) for o in objs):
+        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs)
+    gen_src = os.path.join(CSRC, "gen", "instances.cpp")
+    if _mtime(GEN_LIB) < max(_mtime(gen_src), _mtime(os.path.join(INCLUDE, "pdlp_gen.h"))):
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-Wextra",
+              f"-I{INCLUDE}", "-o", GEN_LIB, gen_src])
+    return [LIB, GEN_LIB]
+
+
+if __name__ == "__main__":
+    for p in build(verbose="-v" in sys.argv):
+        print(p)

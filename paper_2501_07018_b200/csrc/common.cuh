@@ -1,0 +1,133 @@
+// Device-side scalar helpers shared by every kernel.
+//
+// All translation units are compiled with -fmad=false: the reference's dual
+// update  y' = yhat - sigma*proj  (proj/include/pdhglp/step.hpp:85) relies on
+// exact cancellation to keep y' in its sign cone, and FMA contraction breaks
+// that (SURVEY.md §0 finding 6).  Where contraction is wanted (perf-mode SpMV
+// accumulation) it is written explicitly as fma().
+#pragma once
+
+#include <cstdint>
+#include <math_constants.h>
+
+namespace pdlp {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ bool finite_d(double v) { return isfinite(v); }
+
+// reference core.hpp:18-21 — product with 0 * (+-inf) = 0.
+__device__ __forceinline__ double mul_zero_inf(double a, double b) {
+  if (a == 0.0 || b == 0.0) return 0.0;
+  return a * b;
+}
+
+// reference core.hpp:26-28 (NaN passes through, as in the reference).
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+// reference core.hpp:31-35.
+__device__ __forceinline__ double interval_distance(double v, double lo, double hi) {
+  if (v < lo) return lo - v;
+  if (v > hi) return v - hi;
+  return 0.0;
+}
+
+// std::max(acc, v) semantics: (acc < v) ? v : acc — NaN never wins.
+__device__ __forceinline__ double max_keep(double acc, double v) {
+  return (acc < v) ? v : acc;
+}
+
+// SignCone (problem.hpp:36-57): 0 Zero, 1 NonPos, 2 NonNeg, 3 Free.
+enum Cone : int { kZero = 0, kNonPos = 1, kNonNeg = 2, kFree = 3 };
+
+__device__ __forceinline__ int cone_of_bounds(double lo, double hi) {
+  const bool lo_f = lo > -CUDART_INF;
+  const bool hi_f = hi < CUDART_INF;
+  if (lo_f && hi_f) return kFree;
+  if (lo_f) return kNonNeg;
+  if (hi_f) return kNonPos;
+  return kZero;
+}
+
+// recession_cone (residuals.hpp:15-22): the opposite classification.
+__device__ __forceinline__ int recession_cone(double lo, double hi) {
+  const bool lo_f = lo > -CUDART_INF;
+  const bool hi_f = hi < CUDART_INF;
+  if (lo_f && hi_f) return kZero;
+  if (lo_f) return kNonNeg;
+  if (hi_f) return kNonPos;
+  return kFree;
+}
+
+__device__ __forceinline__ double cone_project(double v, int cone) {
+  switch (cone) {
+    case kZero: return 0.0;
+    case kNonPos: return v < 0.0 ? v : 0.0;
+    case kNonNeg: return v > 0.0 ? v : 0.0;
+    default: return v;
+  }
+}
+
+// ----------------------------------------------------------- reductions ---
+// Deterministic block reductions: fixed shuffle tree, fixed smem tree.
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max_keep(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sum over a group of `width` consecutive lanes (width a power of two <= 32);
+// the group's first lane holds the result.
+template <int W>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, W);
+  return v;
+}
+
+// Block-wide sum (blockDim.x a multiple of 32, <= 1024); result valid in
+// thread 0.  `smem` needs blockDim.x/32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < nw ? smem[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+__device__ __forceinline__ double block_max(double v, double* smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < nw ? smem[lane] : 0.0;
+    r = warp_max(r);
+  }
+  return r;
+}
+
+// Streaming loads for data touched once per pass (matrix entries): evict
+// first so the gathered dense operand keeps its L2 residency.
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
+__device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs(p); }
+
+}  // namespace pdlp

@@ -1,0 +1,117 @@
+// Host-side RAII helpers for device memory, streams and events.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+namespace pdlp_host {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaError(std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                    cudaGetErrorString(e) + ")");
+  }
+}
+
+// Launchers in kernels.h return the cudaError_t of the launch (0 = success).
+inline void check_launch(int rc, const char* what) {
+  if (rc != 0) check_cuda(rc < 0 ? cudaErrorUnknown : static_cast<cudaError_t>(rc), what);
+}
+
+#define PDLP_CK(expr) ::pdlp_host::check_cuda((expr), #expr)
+#define PDLP_LAUNCH(expr) ::pdlp_host::check_launch((expr), #expr)
+
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { alloc(n); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t n) {
+    release();
+    n_ = n;
+    if (n == 0) return;
+    void* p = nullptr;
+    PDLP_CK(cudaMalloc(&p, n * sizeof(T)));
+    p_ = static_cast<T*>(p);
+  }
+  void release() {
+    if (p_ != nullptr) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  void swap(DevBuf& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+  }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+class Stream {
+ public:
+  Stream() { PDLP_CK(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking)); }
+  ~Stream() {
+    if (s_ != nullptr) cudaStreamDestroy(s_);
+  }
+  Stream(const Stream&) = delete;
+  Stream& operator=(const Stream&) = delete;
+  cudaStream_t get() const { return s_; }
+  void sync() const { PDLP_CK(cudaStreamSynchronize(s_)); }
+
+ private:
+  cudaStream_t s_ = nullptr;
+};
+
+class Event {
+ public:
+  Event() { PDLP_CK(cudaEventCreate(&e_)); }
+  ~Event() {
+    if (e_ != nullptr) cudaEventDestroy(e_);
+  }
+  Event(const Event&) = delete;
+  Event& operator=(const Event&) = delete;
+  cudaEvent_t get() const { return e_; }
+  void record(cudaStream_t s) { PDLP_CK(cudaEventRecord(e_, s)); }
+
+ private:
+  cudaEvent_t e_ = nullptr;
+};
+
+inline double elapsed_seconds(const Event& a, const Event& b) {
+  float ms = 0.0f;
+  PDLP_CK(cudaEventSynchronize(b.get()));
+  PDLP_CK(cudaEventElapsedTime(&ms, a.get(), b.get()));
+  return static_cast<double>(ms) * 1e-3;
+}
+
+}  // namespace pdlp_host

@@ -1,0 +1,498 @@
+// Exact normalized duality gap on device (reference
+// proj/include/pdhglp/restarts.hpp:107-220):
+//
+//   1. breakpoint events: <= 1 per primal coordinate (slot i), <= 2 per dual
+//      coordinate (slots n+2j, n+2j+1), so slot order == the reference's
+//      push order; plus the lam->inf masses b_inf, c_inf (SEQ in parity)
+//   2. stable radix sort of the events by lambda, descending (order-preserving
+//      uint64 transform; invalid slots get key 0 and sort last)
+//   3. sweep to the first group with phi(lam) = C + B/lam^2 >= r^2:
+//      parity — the reference's sequential loop on one thread;
+//      perf   — exclusive scans of the event masses + a parallel first-hit
+//   4. closed-form lambda*, candidate assembly (assemble_candidate :73-101)
+//      and the gap value (gap_value_at :50-71), SEQ in parity.
+//
+// Parity caveat: std::sort is not stable, so events with EQUAL lambda may be
+// visited in a different order than the reference's introsort puts them,
+// which can change the last bit of the running masses.  Exact ties need
+// bitwise-equal breakpoints; DESIGN.md records this.
+//
+// CUB (part of the CUDA toolkit) provides the radix sort and scans; this is
+// cadence work (2-3 evaluations per 64 steps), not the per-step hot loop.
+//
+// Translation unit compiled with -fmad=false (see common.cuh).
+
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "reduce.cuh"
+
+namespace pdlp {
+namespace {
+
+constexpr int kT = 256;
+
+inline int ew_blocks(int64_t n) {
+  int64_t b = (n + kT - 1) / kT;
+  if (b > 148 * 8) b = 148 * 8;
+  return b < 1 ? 1 : static_cast<int>(b);
+}
+
+#define GRID_STRIDE(i, n)                                                                   \
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); \
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+
+struct GapScalars {
+  double sums[2];  // b_inf, c_inf
+  double count;    // number of valid events
+  double lambda_star;
+  double value;
+  unsigned long long first;  // first crossing group index (perf)
+};
+
+struct Work {
+  uint64_t *keys_in, *keys_out;
+  int32_t *vals_in, *vals_out;
+  double *lam, *dc, *di, *cs, *bs;
+  GapScalars* sc;
+  void* cub_tmp;
+  size_t cub_bytes;
+};
+
+__host__ __device__ inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+size_t cub_bytes_for(int64_t N) {
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, a, static_cast<uint64_t*>(nullptr),
+                                            static_cast<uint64_t*>(nullptr),
+                                            static_cast<int32_t*>(nullptr),
+                                            static_cast<int32_t*>(nullptr), static_cast<int>(N));
+  cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<double*>(nullptr),
+                                static_cast<double*>(nullptr), static_cast<int>(N));
+  return a > b ? a : b;
+}
+
+Work carve(void* base, int64_t n, int64_t m) {
+  const int64_t N = n + 2 * m;
+  char* p = static_cast<char*>(base);
+  Work w;
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += align_up(bytes);
+    return r;
+  };
+  w.keys_in = reinterpret_cast<uint64_t*>(take(8 * N));
+  w.keys_out = reinterpret_cast<uint64_t*>(take(8 * N));
+  w.vals_in = reinterpret_cast<int32_t*>(take(4 * N));
+  w.vals_out = reinterpret_cast<int32_t*>(take(4 * N));
+  w.lam = reinterpret_cast<double*>(take(8 * N));
+  w.dc = reinterpret_cast<double*>(take(8 * N));
+  w.di = reinterpret_cast<double*>(take(8 * N));
+  w.cs = reinterpret_cast<double*>(take(8 * N));
+  w.bs = reinterpret_cast<double*>(take(8 * N));
+  w.sc = reinterpret_cast<GapScalars*>(take(sizeof(GapScalars)));
+  w.cub_bytes = cub_bytes_for(N);
+  w.cub_tmp = take(w.cub_bytes);
+  return w;
+}
+
+// Order-preserving map double -> uint64 (larger double, larger key); key 0 is
+// reserved for "no event" (only reachable by an all-ones negative NaN).
+__device__ __forceinline__ uint64_t order_key(double d) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(d));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+struct GapIn {
+  const double *c, *lv, *uv, *lc, *uc;
+  const double *x, *y, *ax, *aty;
+  int64_t n, m;
+  double omega;
+};
+
+// Per-coordinate logic of restarts.hpp:117-170.  Returns the b_inf / c_inf
+// contributions (flags bit0 / bit1) and up to two events.
+struct Coord {
+  unsigned mass_use = 0;
+  double b = 0.0, c = 0.0;
+  int ne = 0;
+  double lam[2], dc[2], di[2];
+};
+
+__device__ __forceinline__ Coord gap_coord(const GapIn& g, int64_t t) {
+  Coord o;
+  const double omega = g.omega;
+  if (t < g.n) {
+    const int64_t i = t;
+    const double gg = g.aty[i] - g.c[i];
+    if (gg == 0.0) return o;
+    const double off = (gg > 0.0 ? g.uv[i] : g.lv[i]) - g.x[i];
+    if (off == 0.0) return o;
+    o.b = gg * gg / omega;
+    o.mass_use |= 1u;
+    if (finite_d(off)) {
+      o.lam[0] = gg / (omega * off);
+      o.dc[0] = omega * off * off;
+      o.di[0] = -gg * gg / omega;
+      o.ne = 1;
+    }
+    return o;
+  }
+  const int64_t j = t - g.n;
+  const double yj = g.y[j];
+  const double bm = g.ax[j] - g.uc[j];
+  const double bp = g.ax[j] - g.lc[j];
+  const double im = yj * yj / omega;
+  if (yj > 0.0) {
+    if (bp <= 0.0) {
+      if (bp < 0.0) {
+        o.b = omega * bp * bp;
+        o.mass_use |= 1u;
+      }
+      return o;
+    }
+    if (finite_d(bp)) {
+      o.b = omega * bp * bp;
+      o.mass_use |= 1u;
+      o.lam[o.ne] = omega * bp / yj;
+      o.dc[o.ne] = im;
+      o.di[o.ne] = -omega * bp * bp;
+      ++o.ne;
+    } else {
+      o.c = im;
+      o.mass_use |= 2u;
+    }
+    if (bm > 0.0) {
+      o.lam[o.ne] = omega * bm / yj;
+      o.dc[o.ne] = -im;
+      o.di[o.ne] = omega * bm * bm;
+      ++o.ne;
+    }
+  } else if (yj < 0.0) {
+    if (bm >= 0.0) {
+      if (bm > 0.0) {
+        o.b = omega * bm * bm;
+        o.mass_use |= 1u;
+      }
+      return o;
+    }
+    if (finite_d(bm)) {
+      o.b = omega * bm * bm;
+      o.mass_use |= 1u;
+      o.lam[o.ne] = omega * bm / yj;
+      o.dc[o.ne] = im;
+      o.di[o.ne] = -omega * bm * bm;
+      ++o.ne;
+    } else {
+      o.c = im;
+      o.mass_use |= 2u;
+    }
+    if (bp < 0.0) {
+      o.lam[o.ne] = omega * bp / yj;
+      o.dc[o.ne] = -im;
+      o.di[o.ne] = omega * bp * bp;
+      ++o.ne;
+    }
+  } else {
+    if (bm > 0.0) {
+      o.b = omega * bm * bm;
+      o.mass_use |= 1u;
+    } else if (bp < 0.0) {
+      o.b = omega * bp * bp;
+      o.mass_use |= 1u;
+    }
+  }
+  return o;
+}
+
+__global__ void events_kernel(GapIn g, Work w) {
+  GRID_STRIDE(t, g.n + g.m) {
+    const Coord o = gap_coord(g, t);
+    const int64_t s0 = t < g.n ? t : g.n + 2 * (t - g.n);
+    const int slots = t < g.n ? 1 : 2;
+    for (int e = 0; e < slots; ++e) {
+      const int64_t s = s0 + e;
+      if (e < o.ne) {
+        w.keys_in[s] = order_key(o.lam[e]);
+        w.lam[s] = o.lam[e];
+        w.dc[s] = o.dc[e];
+        w.di[s] = o.di[e];
+      } else {
+        w.keys_in[s] = 0;
+        w.lam[s] = 0.0;
+        w.dc[s] = 0.0;
+        w.di[s] = 0.0;
+      }
+      w.vals_in[s] = static_cast<int32_t>(s);
+    }
+  }
+}
+
+__device__ double finish_lambda(double lambda_star) {
+  if (!finite_d(lambda_star)) lambda_star = 1e300;
+  if (lambda_star <= 0.0) lambda_star = 1e-300;
+  return lambda_star;
+}
+
+// Reference sweep (restarts.hpp:175-212), one thread, sorted order.
+__global__ void sweep_seq_kernel(Work w, const double* r_slot, double r_value) {
+  const double r = r_slot ? *r_slot : r_value;
+  const double r2 = r * r;
+  const int64_t E = static_cast<int64_t>(w.sc->count);
+  double c_sum = w.sc->sums[1];
+  double b_sum = w.sc->sums[0];
+  double hi = CUDART_INF;
+  double ls = -1.0;
+  int64_t idx = 0;
+  while (idx < E) {
+    const double lam = w.lam[w.vals_out[idx]];
+    const double phi_lo = c_sum + b_sum / (lam * lam);
+    if (phi_lo >= r2) {
+      if (b_sum > 0.0 && r2 > c_sum) {
+        ls = sqrt(b_sum / (r2 - c_sum));
+      } else {
+        ls = lam;
+      }
+      ls = clampd(ls, lam, hi);
+      break;
+    }
+    while (idx < E && w.lam[w.vals_out[idx]] == lam) {
+      const int32_t s = w.vals_out[idx];
+      c_sum += w.dc[s];
+      b_sum += w.di[s];
+      ++idx;
+    }
+    hi = lam;
+  }
+  if (ls < 0.0) {
+    if (b_sum > 0.0 && r2 > c_sum) {
+      ls = sqrt(b_sum / (r2 - c_sum));
+      ls = ls < hi ? ls : hi;  // std::min(ls, hi)
+    } else if (b_sum > 0.0) {
+      ls = hi;
+    } else {
+      ls = finite_d(hi) ? hi / 2.0 : 1.0;
+    }
+  }
+  w.sc->lambda_star = finish_lambda(ls);
+}
+
+__global__ void gather_masses_kernel(Work w, int64_t N) {
+  GRID_STRIDE(idx, N) {
+    const int32_t s = w.vals_out[idx];
+    w.cs[idx] = w.dc[s];
+    w.bs[idx] = w.di[s];
+  }
+}
+
+__global__ void init_first_kernel(Work w) { w.sc->first = ~0ull; }
+
+// Parallel sweep: scans hold exclusive prefix masses in sorted order.
+__global__ void first_hit_kernel(Work w, const double* r_slot, double r_value, int64_t N) {
+  const double r = r_slot ? *r_slot : r_value;
+  const double r2 = r * r;
+  const int64_t E = static_cast<int64_t>(w.sc->count);
+  const double c0 = w.sc->sums[1], b0 = w.sc->sums[0];
+  GRID_STRIDE(idx, E) {
+    const double lam = w.lam[w.vals_out[idx]];
+    if (idx > 0 && w.lam[w.vals_out[idx - 1]] == lam) continue;  // not a group head
+    const double c_sum = c0 + w.cs[idx];
+    const double b_sum = b0 + w.bs[idx];
+    if (c_sum + b_sum / (lam * lam) >= r2) atomicMin(&w.sc->first, static_cast<unsigned long long>(idx));
+  }
+  (void)N;
+}
+
+__global__ void finalize_perf_kernel(Work w, const double* r_slot, double r_value) {
+  const double r = r_slot ? *r_slot : r_value;
+  const double r2 = r * r;
+  const int64_t E = static_cast<int64_t>(w.sc->count);
+  const double c0 = w.sc->sums[1], b0 = w.sc->sums[0];
+  double ls;
+  const unsigned long long f = w.sc->first;
+  if (f != ~0ull) {
+    const int64_t idx = static_cast<int64_t>(f);
+    const double lam = w.lam[w.vals_out[idx]];
+    const double hi = idx > 0 ? w.lam[w.vals_out[idx - 1]] : CUDART_INF;
+    const double c_sum = c0 + w.cs[idx], b_sum = b0 + w.bs[idx];
+    if (b_sum > 0.0 && r2 > c_sum) {
+      ls = sqrt(b_sum / (r2 - c_sum));
+    } else {
+      ls = lam;
+    }
+    ls = clampd(ls, lam, hi);
+  } else {
+    double c_sum = c0, b_sum = b0, hi = CUDART_INF;
+    if (E > 0) {
+      c_sum = c0 + (w.cs[E - 1] + w.dc[w.vals_out[E - 1]]);
+      b_sum = b0 + (w.bs[E - 1] + w.di[w.vals_out[E - 1]]);
+      hi = w.lam[w.vals_out[E - 1]];
+    }
+    if (b_sum > 0.0 && r2 > c_sum) {
+      ls = sqrt(b_sum / (r2 - c_sum));
+      ls = ls < hi ? ls : hi;
+    } else if (b_sum > 0.0) {
+      ls = hi;
+    } else {
+      ls = finite_d(hi) ? hi / 2.0 : 1.0;
+    }
+  }
+  w.sc->lambda_star = finish_lambda(ls);
+}
+
+// Candidate coordinate (assemble_candidate, restarts.hpp:73-101).
+__device__ __forceinline__ double cand_x(const GapIn& g, int64_t i, double lambda) {
+  const double gg = g.aty[i] - g.c[i];
+  return clampd(g.x[i] + gg / (lambda * g.omega), g.lv[i], g.uv[i]);
+}
+
+__device__ __forceinline__ double cand_y(const GapIn& g, int64_t j, double lambda) {
+  const double nu = lambda / g.omega;
+  const double bm = g.ax[j] - g.uc[j];
+  const double bp = g.ax[j] - g.lc[j];
+  const double t = nu * g.y[j];
+  double v;
+  if (t >= bp) {
+    v = g.y[j] - bp / nu;
+  } else if (t <= bm) {
+    v = g.y[j] - bm / nu;
+  } else {
+    v = 0.0;
+  }
+  return cone_project(v, cone_of_bounds(g.lc[j], g.uc[j]));
+}
+
+// gap_value_at (restarts.hpp:50-71) in the reference's exact order.
+__global__ void value_seq_kernel(GapIn g, Work w, const double* r_slot, double r_value,
+                                 double* out) {
+  const double r = r_slot ? *r_slot : r_value;
+  if (!(r > 0.0)) {
+    *out = 0.0;
+    return;
+  }
+  const double lambda = w.sc->lambda_star;
+  double value = 0.0;
+  for (int64_t i = 0; i < g.n; ++i) {
+    const double xh = cand_x(g, i, lambda);
+    value += g.c[i] * (g.x[i] - xh) + g.aty[i] * xh;
+  }
+  for (int64_t j = 0; j < g.m; ++j) {
+    const double yh = cand_y(g, j, lambda);
+    const double yj = g.y[j];
+    value -= yh * g.ax[j];
+    if (yh > 0.0) {
+      value -= mul_zero_inf(-g.lc[j], yh);
+    } else if (yh < 0.0) {
+      value -= mul_zero_inf(-g.uc[j], yh);
+    }
+    if (yj > 0.0) {
+      value += mul_zero_inf(-g.lc[j], yj);
+    } else if (yj < 0.0) {
+      value += mul_zero_inf(-g.uc[j], yj);
+    }
+  }
+  *out = (value > 0.0) ? value / r : 0.0;
+}
+
+__global__ void value_finish_kernel(const double* sum, const double* r_slot, double r_value,
+                                    double* out) {
+  const double r = r_slot ? *r_slot : r_value;
+  const double value = *sum;
+  *out = (r > 0.0 && value > 0.0) ? value / r : 0.0;
+}
+
+}  // namespace
+}  // namespace pdlp
+
+using namespace pdlp;
+
+extern "C" size_t pdlpk_gap_work_bytes(int64_t n, int64_t m) {
+  const int64_t N = n + 2 * m;
+  return align_up(8 * N) * 2 + align_up(4 * N) * 2 + align_up(8 * N) * 5 +
+         align_up(sizeof(GapScalars)) + align_up(cub_bytes_for(N)) + 256;
+}
+
+extern "C" int pdlpk_gap(const pdlpk_problem* P, const double* x, const double* y,
+                         const double* ax, const double* aty, double omega, const double* r_slot,
+                         double r_value, const pdlpk_red* red, void* work, double* gap_slot,
+                         cudaStream_t s) {
+  const int64_t n = P->n, m = P->m, N = n + 2 * m;
+  Work w = carve(work, n, m);
+  GapIn g{P->c, P->lv, P->uv, P->lc, P->uc, x, y, ax, aty, n, m, omega};
+  const bool parity = red->parity != 0;
+  // lam -> inf masses in the reference's accumulation order
+  auto fm = [g] __device__(int64_t t, double* v) -> unsigned {
+    const Coord o = gap_coord(g, t);
+    v[0] = o.b;
+    v[1] = o.c;
+    return o.mass_use;
+  };
+  if (multi_reduce<2>(fm, n + m, parity ? PDLPK_RED_SEQ : PDLPK_RED_TREE, red->shards, 0u,
+                      red->scratch, w.sc->sums, s) != 0) {
+    return -1;
+  }
+  if (N > 0) {
+    events_kernel<<<ew_blocks(n + m), kT, 0, s>>>(g, w);
+    auto fc = [w] __device__(int64_t idx, double* v) -> unsigned {
+      v[0] = 1.0;
+      return w.keys_in[idx] != 0 ? 1u : 0u;
+    };
+    if (multi_reduce<1>(fc, N, PDLPK_RED_TREE, red->shards, 0u, red->scratch, &w.sc->count, s) != 0)
+      return -1;
+    size_t bytes = w.cub_bytes;
+    if (cub::DeviceRadixSort::SortPairsDescending(w.cub_tmp, bytes, w.keys_in, w.keys_out,
+                                                  w.vals_in, w.vals_out, static_cast<int>(N), 0,
+                                                  64, s) != cudaSuccess) {
+      return -1;
+    }
+  } else {
+    cudaMemsetAsync(&w.sc->count, 0, sizeof(double), s);
+  }
+  if (parity) {
+    sweep_seq_kernel<<<1, 1, 0, s>>>(w, r_slot, r_value);
+    value_seq_kernel<<<1, 1, 0, s>>>(g, w, r_slot, r_value, gap_slot);
+  } else {
+    if (N > 0) {
+      gather_masses_kernel<<<ew_blocks(N), kT, 0, s>>>(w, N);
+      size_t bytes = w.cub_bytes;
+      cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.cs, w.cs, static_cast<int>(N), s);
+      bytes = w.cub_bytes;
+      cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.bs, w.bs, static_cast<int>(N), s);
+    }
+    init_first_kernel<<<1, 1, 0, s>>>(w);
+    if (N > 0) first_hit_kernel<<<ew_blocks(N), kT, 0, s>>>(w, r_slot, r_value, N);
+    finalize_perf_kernel<<<1, 1, 0, s>>>(w, r_slot, r_value);
+    const double* lam_star = &w.sc->lambda_star;
+    auto fv = [g, lam_star] __device__(int64_t t, double* v) -> unsigned {
+      const double lambda = *lam_star;
+      if (t < g.n) {
+        const double xh = cand_x(g, t, lambda);
+        v[0] = g.c[t] * (g.x[t] - xh) + g.aty[t] * xh;
+        return 1u;
+      }
+      const int64_t j = t - g.n;
+      const double yh = cand_y(g, j, lambda);
+      const double yj = g.y[j];
+      double d = -(yh * g.ax[j]);
+      if (yh > 0.0) {
+        d -= mul_zero_inf(-g.lc[j], yh);
+      } else if (yh < 0.0) {
+        d -= mul_zero_inf(-g.uc[j], yh);
+      }
+      if (yj > 0.0) {
+        d += mul_zero_inf(-g.lc[j], yj);
+      } else if (yj < 0.0) {
+        d += mul_zero_inf(-g.uc[j], yj);
+      }
+      v[0] = d;
+      return 1u;
+    };
+    if (multi_reduce<1>(fv, n + m, PDLPK_RED_TREE, red->shards, 0u, red->scratch, &w.sc->value,
+                        s) != 0) {
+      return -1;
+    }
+    value_finish_kernel<<<1, 1, 0, s>>>(&w.sc->value, r_slot, r_value, gap_slot);
+  }
+  return static_cast<int>(cudaGetLastError());
+}

@@ -1,0 +1,506 @@
+// The PDHG step attempt on device: pdhg_step_into + the adaptive step-size
+// decision of the reference (proj/include/pdhglp/step.hpp:60-95, 126-193),
+// with the deferred running-average update (step.hpp:209-216).
+//
+// PERF mode, three launches per attempt:
+//   primal_pass   x' = clamp(x - tau (c - aty)), xbar = 2x' - x      (n, elementwise)
+//                 [+ pending  sum_x += w x  of the previously accepted step]
+//   row_pass      a_ext = K xbar (load-balanced CSR), fused dual update
+//                 y' = yhat - sigma clamp(yhat/sigma, -u_c, -l_c), dy = y' - y,
+//                 per-CTA partials of |dy|^2 and |y'|_inf
+//                 [+ pending  sum_y += w y]
+//   col_pass      aty' = aty + K^T dy (load-balanced CSR of K^T), per-CTA
+//                 partials of |dx|^2, dy^T K dx and |x'|_inf; the last CTA
+//                 combines all partials in a fixed order and runs the
+//                 accept/reject rule, flipping the ping-pong buffers on
+//                 acceptance.  No host round trip per attempt.
+// PARITY mode reproduces the reference's arithmetic order bit for bit:
+// thread-per-line sequential products, per-shard sequential reductions over
+// make_shard_plan(dim, 1, S) and an ascending combine (kernels.hpp:69-97).
+//
+// Translation unit compiled with -fmad=false (see common.cuh).
+
+#include "common.cuh"
+#include "kernels.h"
+#include "spmv.cuh"
+
+namespace pdlp {
+namespace {
+
+constexpr int kEwThreads = 256;
+
+inline int ew_blocks(int64_t n) {
+  int64_t b = (n + kEwThreads - 1) / kEwThreads;
+  if (b > 148 * 8) b = 148 * 8;
+  return b < 1 ? 1 : static_cast<int>(b);
+}
+
+// ------------------------------------------------------------ primal pass ---
+__global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const double eta = st->eta;
+  if (!st->fixed && (!(eta > 0.0) || !finite_d(eta))) {  // step.hpp:166
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->status = 1;
+      st->halt = 1;
+    }
+    return;
+  }
+  const double tau = eta / st->omega;
+  const int cur = st->cur;
+  const double* __restrict__ x = a.x[cur];
+  const double* __restrict__ aty = a.aty[cur];
+  double* __restrict__ xn = a.x[cur ^ 1];
+  const double* __restrict__ c = a.P.c;
+  const double* __restrict__ lv = a.P.lv;
+  const double* __restrict__ uv = a.P.uv;
+  double* __restrict__ xbar = a.xbar;
+  const bool pend = st->avg_pending != 0;
+  const double w = st->avg_w;
+  double* __restrict__ sx = a.sum_x;
+  const int64_t n = a.P.n;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const double xi = x[i];
+    const double step = xi - tau * (c[i] - aty[i]);
+    const double xp = clampd(step, lv[i], uv[i]);
+    xn[i] = xp;
+    xbar[i] = 2.0 * xp - xi;
+    if (pend) sx[i] = sx[i] + w * xi;
+  }
+}
+
+// ---------------------------------------------------------- decision rule ---
+__device__ void decide(pdlpk_step_state* s, double dx2, double dy2, double curv, double infx,
+                       double infy, const double* f_down, const double* f_up,
+                       int64_t table_len) {
+  s->attempts += 1;
+  s->avg_pending = 0;
+  s->dx2 = dx2;
+  s->dy2 = dy2;
+  s->curv = curv;
+  s->inf_x = infx;
+  s->inf_y = infy;
+  const double eta = s->eta;
+  if (s->fixed) {  // solver.hpp:477-491
+    if (!finite_d(infx) || !finite_d(infy)) {
+      s->status = 1;
+      s->halt = 1;
+      return;
+    }
+    s->cur ^= 1;
+    s->k += 1;
+    s->accepted += 1;
+    s->eta_used = eta;
+    s->avg_pending = 1;
+    s->avg_w = eta;
+    s->avg_weight += eta;
+    s->avg_count += 1;
+    if (s->k >= s->k_target) s->halt = 1;
+    return;
+  }
+  const double omega = s->omega;
+  const double movement = omega * dx2 + dy2 / omega;
+  if (!finite_d(movement) || !finite_d(curv)) {  // step.hpp:175
+    s->status = 1;
+    s->halt = 1;
+    return;
+  }
+  // step_size_limit (step.hpp:126-130)
+  const double denom = 2.0 * fabs(curv);
+  const double eta_bar = (denom > 0.0) ? movement / denom : CUDART_INF;
+  s->eta_bar = eta_bar;
+  if (finite_d(eta_bar)) s->min_eta_bar = (eta_bar < s->min_eta_bar) ? eta_bar : s->min_eta_bar;
+  // next_step_size (step.hpp:136-141); factors from the host-libm table.
+  const int64_t k = s->k;
+  if (k >= table_len) {
+    s->table_short = 1;
+    s->status = 1;
+    s->halt = 1;
+    return;
+  }
+  const double down = f_down[k] * eta_bar;
+  const double up = f_up[k] * eta;
+  const double eta_next = (up < down) ? up : down;
+  if (eta <= eta_bar) {
+    s->cur ^= 1;
+    s->eta = eta_next;
+    s->k = k + 1;
+    s->accepted += 1;
+    s->eta_used = eta;
+    s->attempt_in_step = 0;
+    s->avg_pending = 1;
+    s->avg_w = eta;
+    s->avg_weight += eta;
+    s->avg_count += 1;
+    if (s->k >= s->k_target) s->halt = 1;
+    return;
+  }
+  s->retries += 1;
+  s->eta = eta_next;
+  s->attempt_in_step += 1;
+  if (s->attempt_in_step > s->max_retries) {  // step.hpp:165,192
+    s->status = 1;
+    s->halt = 1;
+  }
+}
+
+// --------------------------------------------------------- perf row pass ---
+struct RowEpi {
+  const double* __restrict__ y;
+  double* __restrict__ yn;
+  double* __restrict__ dy;
+  const double* __restrict__ lc;
+  const double* __restrict__ uc;
+  double* __restrict__ sy;
+  double sigma, w;
+  bool pend;
+  double dy2 = 0.0, infy = 0.0;
+  __device__ __forceinline__ void line(int64_t r, double acc) {
+    const double yr = y[r];
+    const double yhat = yr - sigma * acc;
+    const double proj = clampd(yhat / sigma, -uc[r], -lc[r]);
+    const double yp = yhat - sigma * proj;  // exact cancellation: no FMA (step.hpp:85)
+    yn[r] = yp;
+    const double d = yp - yr;
+    dy[r] = d;
+    if (pend) sy[r] = sy[r] + w * yr;
+    dy2 += d * d;
+    infy = max_keep(infy, fabs(yp));
+  }
+};
+
+template <class P, int V>
+__global__ void __launch_bounds__(kSpmvThreads) row_pass(pdlpk_step_args a) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int cur = st->cur;
+  RowEpi e;
+  e.y = a.y[cur];
+  e.yn = a.y[cur ^ 1];
+  e.dy = a.dy;
+  e.lc = a.P.lc;
+  e.uc = a.P.uc;
+  e.sy = a.sum_y;
+  e.sigma = st->eta * st->omega;
+  e.pend = st->avg_pending != 0;
+  e.w = st->avg_w;
+  sched_spmv<P, V>(a.P.K, a.P.K.value, a.xbar, e);
+  __shared__ double red[32];
+  const double s1 = block_sum(e.dy2, red);
+  __syncthreads();
+  const double s2 = block_max(e.infy, red);
+  if (threadIdx.x == 0) {
+    a.part2[blockIdx.x] = s1;
+    a.part2[gridDim.x + blockIdx.x] = s2;
+  }
+}
+
+// ------------------------------------------------------ perf column pass ---
+struct ColEpi {
+  const double* __restrict__ aty;
+  double* __restrict__ atyn;
+  const double* __restrict__ x;
+  const double* __restrict__ xn;
+  double dx2 = 0.0, curv = 0.0, infx = 0.0;
+  __device__ __forceinline__ void line(int64_t i, double d) {
+    atyn[i] = aty[i] + d;
+    const double xp = xn[i];
+    const double dxi = xp - x[i];
+    dx2 += dxi * dxi;
+    curv += d * dxi;
+    infx = max_keep(infx, fabs(xp));
+  }
+};
+
+template <class P, int V>
+__global__ void __launch_bounds__(kSpmvThreads) col_pass(pdlpk_step_args a) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int cur = st->cur;
+  ColEpi e;
+  e.aty = a.aty[cur];
+  e.atyn = a.aty[cur ^ 1];
+  e.x = a.x[cur];
+  e.xn = a.x[cur ^ 1];
+  sched_spmv<P, V>(a.P.KT, a.P.KT.value, a.dy, e);
+  __shared__ double red[32];
+  __shared__ bool last;
+  const double s1 = block_sum(e.dx2, red);
+  __syncthreads();
+  const double s2 = block_sum(e.curv, red);
+  __syncthreads();
+  const double s3 = block_max(e.infx, red);
+  const int64_t g3 = gridDim.x;
+  if (threadIdx.x == 0) {
+    a.part3[blockIdx.x] = s1;
+    a.part3[g3 + blockIdx.x] = s2;
+    a.part3[2 * g3 + blockIdx.x] = s3;
+    __threadfence();
+    const unsigned t = atomicAdd(&st->ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // Last CTA: combine every partial in a fixed order, then decide.
+  const int64_t g2 = sched_blocks(a.P.K);
+  double dy2 = 0.0, infy = 0.0, dx2 = 0.0, curv = 0.0, infx = 0.0;
+  for (int64_t b = threadIdx.x; b < g2; b += blockDim.x) {
+    dy2 += __ldcg(a.part2 + b);
+    infy = max_keep(infy, __ldcg(a.part2 + g2 + b));
+  }
+  for (int64_t b = threadIdx.x; b < g3; b += blockDim.x) {
+    dx2 += __ldcg(a.part3 + b);
+    curv += __ldcg(a.part3 + g3 + b);
+    infx = max_keep(infx, __ldcg(a.part3 + 2 * g3 + b));
+  }
+  dy2 = block_sum(dy2, red);
+  __syncthreads();
+  infy = block_max(infy, red);
+  __syncthreads();
+  dx2 = block_sum(dx2, red);
+  __syncthreads();
+  curv = block_sum(curv, red);
+  __syncthreads();
+  infx = block_max(infx, red);
+  if (threadIdx.x == 0) {
+    st->ticket = 0;
+    decide(st, dx2, dy2, curv, infx, infy, a.f_down, a.f_up, a.table_len);
+  }
+}
+
+// ------------------------------------------------------------ parity path ---
+template <class P>
+__global__ void __launch_bounds__(kEwThreads) parity_row_pass(pdlpk_step_args a) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int cur = st->cur;
+  const double* __restrict__ y = a.y[cur];
+  double* __restrict__ yn = a.y[cur ^ 1];
+  const double sigma = st->eta * st->omega;
+  const bool pend = st->avg_pending != 0;
+  const double w = st->avg_w;
+  const P* __restrict__ start = static_cast<const P*>(a.P.K.start);
+  const int32_t* __restrict__ idx = a.P.K.index;
+  const double* __restrict__ val = a.P.K.value;
+  const double* __restrict__ xbar = a.xbar;
+  const int64_t m = a.P.m;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < m;
+       r += stride) {
+    double acc = 0.0;
+    for (int64_t k = start[r]; k < start[r + 1]; ++k) acc = acc + val[k] * xbar[idx[k]];
+    const double yr = y[r];
+    const double yhat = yr - sigma * acc;
+    const double proj = clampd(yhat / sigma, -a.P.uc[r], -a.P.lc[r]);
+    const double yp = yhat - sigma * proj;
+    yn[r] = yp;
+    a.dy[r] = yp - yr;
+    if (pend) a.sum_y[r] = a.sum_y[r] + w * yr;
+  }
+}
+
+template <class P>
+__global__ void __launch_bounds__(kEwThreads) parity_col_pass(pdlpk_step_args a) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int cur = st->cur;
+  const double* __restrict__ aty = a.aty[cur];
+  double* __restrict__ atyn = a.aty[cur ^ 1];
+  const P* __restrict__ start = static_cast<const P*>(a.P.KT.start);
+  const int32_t* __restrict__ idx = a.P.KT.index;
+  const double* __restrict__ val = a.P.KT.value;
+  const double* __restrict__ dy = a.dy;
+  const int64_t n = a.P.n;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    double acc = 0.0;
+    for (int64_t k = start[i]; k < start[i + 1]; ++k) acc = acc + val[k] * dy[idx[k]];
+    a.aty_diff[i] = acc;
+    atyn[i] = aty[i] + acc;
+  }
+}
+
+__device__ __forceinline__ void shard_range(int64_t dim, int s, int S, int64_t& lo, int64_t& hi) {
+  const int64_t base = dim / S, rem = dim % S;
+  lo = s * base + (s < rem ? s : rem);
+  hi = lo + base + (s < rem ? 1 : 0);
+}
+
+// One thread per shard: x-plan shards [0,S) and y-plan shards [S,2S).
+__global__ void parity_shard_reduce(pdlpk_step_args a) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int S = a.shards;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * S) return;
+  const int cur = st->cur;
+  double* part = a.shard_part;
+  int64_t lo, hi;
+  if (t < S) {
+    const double* x = a.x[cur];
+    const double* xn = a.x[cur ^ 1];
+    shard_range(a.P.n, t, S, lo, hi);
+    double dx2 = 0.0, curv = 0.0, infx = 0.0;
+    for (int64_t i = lo; i < hi; ++i) {
+      const double d = xn[i] - x[i];
+      dx2 += d * d;
+    }
+    for (int64_t i = lo; i < hi; ++i) curv += a.aty_diff[i] * (xn[i] - x[i]);
+    if (st->fixed) {
+      for (int64_t i = lo; i < hi; ++i) infx = max_keep(infx, fabs(xn[i]));
+    }
+    part[t] = dx2;
+    part[S + t] = curv;
+    part[2 * S + t] = infx;
+  } else {
+    const int s = t - S;
+    const double* yn = a.y[cur ^ 1];
+    shard_range(a.P.m, s, S, lo, hi);
+    double dy2 = 0.0, infy = 0.0;
+    for (int64_t j = lo; j < hi; ++j) {
+      const double d = a.dy[j];
+      dy2 += d * d;
+    }
+    if (st->fixed) {
+      for (int64_t j = lo; j < hi; ++j) infy = max_keep(infy, fabs(yn[j]));
+    }
+    part[3 * S + s] = dy2;
+    part[4 * S + s] = infy;
+  }
+}
+
+__global__ void parity_decide(pdlpk_step_args a) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int S = a.shards;
+  const double* part = a.shard_part;
+  double dx2 = 0.0, curv = 0.0, infx = 0.0, dy2 = 0.0, infy = 0.0;
+  for (int s = 0; s < S; ++s) dx2 += part[s];
+  for (int s = 0; s < S; ++s) curv += part[S + s];
+  for (int s = 0; s < S; ++s) infx = max_keep(infx, part[2 * S + s]);
+  for (int s = 0; s < S; ++s) dy2 += part[3 * S + s];
+  for (int s = 0; s < S; ++s) infy = max_keep(infy, part[4 * S + s]);
+  decide(st, dx2, dy2, curv, infx, infy, a.f_down, a.f_up, a.table_len);
+}
+
+// ---------------------------------------------------------- bookkeeping ---
+__global__ void arm_kernel(pdlpk_step_state* st, int64_t k_target) {
+  st->k_target = k_target;
+  st->halt = (st->status != 0 || st->k >= k_target) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kEwThreads) flush_average_kernel(pdlpk_step_args a) {
+  const pdlpk_step_state* st = a.state;
+  if (!st->avg_pending) return;
+  const int cur = st->cur;
+  const double w = st->avg_w;
+  const double* x = a.x[cur];
+  const double* y = a.y[cur];
+  const int64_t n = a.P.n, m = a.P.m;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n + m;
+       i += stride) {
+    if (i < n) {
+      a.sum_x[i] = a.sum_x[i] + w * x[i];
+    } else {
+      const int64_t j = i - n;
+      a.sum_y[j] = a.sum_y[j] + w * y[j];
+    }
+  }
+}
+
+__global__ void clear_pending_kernel(pdlpk_step_state* st) { st->avg_pending = 0; }
+
+struct LaunchRowCol {
+  const pdlpk_step_args* a;
+  cudaStream_t s;
+  bool row;
+  template <class P, int V>
+  int go() {
+    const pdlpk_csr& A = row ? a->P.K : a->P.KT;
+    const int64_t g = sched_blocks(A);
+    if (g <= 0) return 0;
+    if (row) {
+      row_pass<P, V><<<static_cast<unsigned>(g), kSpmvThreads, 0, s>>>(*a);
+    } else {
+      col_pass<P, V><<<static_cast<unsigned>(g), kSpmvThreads, 0, s>>>(*a);
+    }
+    return 0;
+  }
+};
+
+}  // namespace
+}  // namespace pdlp
+
+using namespace pdlp;
+
+extern "C" int64_t pdlpk_step_partials(const pdlpk_problem* P) {
+  const int64_t g2 = sched_blocks(P->K), g3 = sched_blocks(P->KT);
+  return (2 * g2 > 3 * g3 ? 2 * g2 : 3 * g3) + 64;
+}
+
+extern "C" int pdlpk_arm(pdlpk_step_state* st, int64_t k_target, cudaStream_t s) {
+  arm_kernel<<<1, 1, 0, s>>>(st, k_target);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
+  primal_pass<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a);
+  if (a->mode == 0) {
+    // Degenerate shapes (an empty side) still need the decision, which the
+    // column pass performs: it always has >= 1 CTA (short_blocks >= 1).
+    dispatch_pv(a->P.K, LaunchRowCol{a, s, true});
+    dispatch_pv(a->P.KT, LaunchRowCol{a, s, false});
+  } else {
+    const int gm = ew_blocks(a->P.m), gn = ew_blocks(a->P.n);
+    if (a->P.K.wide) {
+      parity_row_pass<int64_t><<<gm, kEwThreads, 0, s>>>(*a);
+      parity_col_pass<int64_t><<<gn, kEwThreads, 0, s>>>(*a);
+    } else {
+      parity_row_pass<int32_t><<<gm, kEwThreads, 0, s>>>(*a);
+      parity_col_pass<int32_t><<<gn, kEwThreads, 0, s>>>(*a);
+    }
+    const int t = 2 * a->shards;
+    parity_shard_reduce<<<(t + 127) / 128, 128, 0, s>>>(*a);
+    parity_decide<<<1, 1, 0, s>>>(*a);
+  }
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_attempt_timed(const pdlpk_step_args* a, cudaEvent_t* ev, cudaStream_t s) {
+  cudaEventRecord(ev[0], s);
+  primal_pass<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a);
+  cudaEventRecord(ev[1], s);
+  if (a->mode == 0) {
+    dispatch_pv(a->P.K, LaunchRowCol{a, s, true});
+    cudaEventRecord(ev[2], s);
+    dispatch_pv(a->P.KT, LaunchRowCol{a, s, false});
+  } else {
+    const int gm = ew_blocks(a->P.m), gn = ew_blocks(a->P.n);
+    if (a->P.K.wide) {
+      parity_row_pass<int64_t><<<gm, kEwThreads, 0, s>>>(*a);
+      cudaEventRecord(ev[2], s);
+      parity_col_pass<int64_t><<<gn, kEwThreads, 0, s>>>(*a);
+    } else {
+      parity_row_pass<int32_t><<<gm, kEwThreads, 0, s>>>(*a);
+      cudaEventRecord(ev[2], s);
+      parity_col_pass<int32_t><<<gn, kEwThreads, 0, s>>>(*a);
+    }
+    const int t = 2 * a->shards;
+    parity_shard_reduce<<<(t + 127) / 128, 128, 0, s>>>(*a);
+    parity_decide<<<1, 1, 0, s>>>(*a);
+  }
+  cudaEventRecord(ev[3], s);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_flush_average(const pdlpk_step_args* a, cudaStream_t s) {
+  flush_average_kernel<<<ew_blocks(a->P.n + a->P.m), kEwThreads, 0, s>>>(*a);
+  clear_pending_kernel<<<1, 1, 0, s>>>(a->state);
+  return static_cast<int>(cudaGetLastError());
+}

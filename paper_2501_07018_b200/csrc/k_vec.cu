@@ -1,0 +1,469 @@
+// Cadence-time device operations: plain products, residual screens, ray
+// tests, averages, preconditioning and setup conversions.  Each operation
+// cites the reference function whose arithmetic it reproduces; in parity
+// mode every sum runs in the reference's order (SEQ / SHARD, reduce.cuh).
+//
+// Translation unit compiled with -fmad=false (see common.cuh).
+
+#include "common.cuh"
+#include "kernels.h"
+#include "reduce.cuh"
+#include "spmv.cuh"
+
+namespace pdlp {
+namespace {
+
+constexpr int kT = 256;
+
+inline int ew_blocks(int64_t n) {
+  int64_t b = (n + kT - 1) / kT;
+  if (b > 148 * 8) b = 148 * 8;
+  return b < 1 ? 1 : static_cast<int>(b);
+}
+
+#define GRID_STRIDE(i, n)                                                                   \
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); \
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+
+inline int ok() { return static_cast<int>(cudaGetLastError()); }
+
+// -------------------------------------------------------------- products ---
+template <class P>
+__global__ void __launch_bounds__(kT) seq_spmv_kernel(const P* __restrict__ start,
+                                                      const int32_t* __restrict__ idx,
+                                                      const double* __restrict__ val,
+                                                      const double* __restrict__ v,
+                                                      double* __restrict__ out, int64_t dim) {
+  GRID_STRIDE(r, dim) {
+    double acc = 0.0;
+    for (int64_t k = start[r]; k < start[r + 1]; ++k) acc = acc + val[k] * v[idx[k]];
+    out[r] = acc;
+  }
+}
+
+struct StoreEpi {
+  double* out;
+  __device__ __forceinline__ void line(int64_t r, double acc) { out[r] = acc; }
+};
+
+template <class P, int V>
+__global__ void __launch_bounds__(kSpmvThreads) sched_spmv_kernel(pdlpk_csr A,
+                                                                  const double* vals,
+                                                                  const double* v, double* out) {
+  StoreEpi e{out};
+  sched_spmv<P, V>(A, vals, v, e);
+}
+
+struct LaunchSpmv {
+  const pdlpk_csr* A;
+  const double* vals;
+  const double* v;
+  double* out;
+  cudaStream_t s;
+  template <class P, int V>
+  int go() {
+    const int64_t g = sched_blocks(*A);
+    if (g > 0) sched_spmv_kernel<P, V><<<static_cast<unsigned>(g), kSpmvThreads, 0, s>>>(*A, vals, v, out);
+    return ok();
+  }
+};
+
+// ------------------------------------------------------------ elementwise ---
+__global__ void sub_kernel(const double* a, const double* b, double* out, int64_t n) {
+  GRID_STRIDE(i, n) out[i] = a[i] - b[i];
+}
+
+__global__ void scale_mul_kernel(const double* scale, const double* v, double* out, int64_t n) {
+  GRID_STRIDE(i, n) out[i] = scale[i] * v[i];
+}
+
+__global__ void average_into_kernel(const pdlpk_step_state* st, const double* sx,
+                                    const double* sy, double* x, double* y, int64_t n,
+                                    int64_t m) {
+  const double inv = 1.0 / st->avg_weight;
+  GRID_STRIDE(i, n + m) {
+    if (i < n) {
+      x[i] = inv * sx[i];
+    } else {
+      y[i - n] = inv * sy[i - n];
+    }
+  }
+}
+
+__global__ void initial_point_kernel(const double* lv, const double* uv, double* x, int64_t n) {
+  GRID_STRIDE(i, n) x[i] = clampd(0.0, lv[i], uv[i]);
+}
+
+__global__ void dual_feas_bounds_kernel(const double* c, const double* lv, const double* uv,
+                                        int64_t n, const double* lc, const double* uc,
+                                        int64_t m, double* slc, double* suc, double* slv,
+                                        double* suv) {
+  GRID_STRIDE(t, n + m) {
+    if (t < n) {
+      const int64_t i = t;
+      const double ci = c[i];
+      switch (cone_of_bounds(lv[i], uv[i])) {
+        case kZero: slc[i] = ci; suc[i] = ci; break;
+        case kNonNeg: slc[i] = -CUDART_INF; suc[i] = ci; break;
+        case kNonPos: slc[i] = ci; suc[i] = CUDART_INF; break;
+        default: slc[i] = -CUDART_INF; suc[i] = CUDART_INF; break;
+      }
+    } else {
+      const int64_t j = t - n;
+      switch (cone_of_bounds(lc[j], uc[j])) {
+        case kZero: slv[j] = 0.0; suv[j] = 0.0; break;
+        case kNonNeg: slv[j] = 0.0; suv[j] = CUDART_INF; break;
+        case kNonPos: slv[j] = -CUDART_INF; suv[j] = 0.0; break;
+        default: slv[j] = -CUDART_INF; suv[j] = CUDART_INF; break;
+      }
+    }
+  }
+}
+
+__global__ void i64_to_i32_kernel(const int64_t* src, int32_t* dst, int64_t n) {
+  GRID_STRIDE(i, n) dst[i] = static_cast<int32_t>(src[i]);
+}
+
+__global__ void radius_kernel(const double* dx2, const double* dy2, double omega, double* out) {
+  *out = sqrt(omega * (*dx2) + (*dy2) / omega);
+}
+
+// ------------------------------------------------------ preconditioning ---
+template <class P>
+__global__ void line_factor_kernel(const P* __restrict__ start, const double* __restrict__ val,
+                                   int64_t dim, int one_norm, double* __restrict__ f) {
+  GRID_STRIDE(r, dim) {
+    double a = 0.0;
+    if (one_norm) {
+      for (int64_t k = start[r]; k < start[r + 1]; ++k) a += fabs(val[k]);  // rescaling.hpp:111-116
+    } else {
+      for (int64_t k = start[r]; k < start[r + 1]; ++k) a = max_keep(a, fabs(val[k]));
+    }
+    f[r] = a > 0.0 ? sqrt(a) : 1.0;
+  }
+}
+
+template <class P>
+__global__ void apply_factor_kernel(const P* __restrict__ start, const int32_t* __restrict__ idx,
+                                    double* __restrict__ val, int64_t dim,
+                                    const double* __restrict__ fp, const double* __restrict__ fs) {
+  GRID_STRIDE(r, dim) {
+    const double a = fp[r];
+    for (int64_t k = start[r]; k < start[r + 1]; ++k) val[k] = val[k] / (a * fs[idx[k]]);
+  }
+}
+
+__global__ void apply_vec_factor_kernel(double* lc, double* uc, double* rs, const double* fr,
+                                        int64_t m, double* c, double* lv, double* uv,
+                                        double* cs, const double* fc, int64_t n) {
+  GRID_STRIDE(t, m + n) {
+    if (t < m) {
+      const double f = fr[t];
+      lc[t] = lc[t] / f;
+      uc[t] = uc[t] / f;
+      rs[t] = rs[t] / f;
+    } else {
+      const int64_t i = t - m;
+      const double f = fc[i];
+      c[i] = c[i] / f;
+      lv[i] = lv[i] * f;
+      uv[i] = uv[i] * f;
+      cs[i] = cs[i] / f;
+    }
+  }
+}
+
+__global__ void find_nonfinite_kernel(const double* v, int64_t n, int32_t code, int32_t* first) {
+  GRID_STRIDE(i, n) {
+    if (!finite_d(v[i])) atomicMin(reinterpret_cast<int*>(first + 1), static_cast<int>(i));
+  }
+  (void)code;
+}
+
+// Reduced cost of coordinate i (recover_reduced_costs_from, residuals.hpp:29-47).
+__device__ __forceinline__ double reduced_cost(double c, double aty, double x, double lv,
+                                               double uv, int rc_mode) {
+  const double v = c - aty;
+  if (rc_mode == 0) return cone_project(v, cone_of_bounds(lv, uv));
+  if (v > 0.0 && x - lv <= fabs(x)) return v;
+  if (v < 0.0 && uv - x <= fabs(x)) return v;
+  return 0.0;
+}
+
+// Penalty term of dual_objective_value (residuals.hpp:77-96) for multiplier
+// value w against bounds (lo, hi): v = -w; hi*v if v > 0, lo*v if v < 0.
+__device__ __forceinline__ bool penalty_term(double w, double lo, double hi, double& out) {
+  const double v = -w;
+  if (v > 0.0) {
+    out = mul_zero_inf(hi, v);
+    return true;
+  }
+  if (v < 0.0) {
+    out = mul_zero_inf(lo, v);
+    return true;
+  }
+  return false;
+}
+
+}  // namespace
+}  // namespace pdlp
+
+using namespace pdlp;
+
+extern "C" {
+
+int64_t pdlpk_red_scratch_doubles(void) { return 8 * kRedMaxBlocks; }
+
+int pdlpk_index_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s) {
+  if (n > 0) i64_to_i32_kernel<<<ew_blocks(n), kT, 0, s>>>(src, dst, n);
+  return ok();
+}
+
+int pdlpk_start_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s) {
+  return pdlpk_index_to_i32(src, dst, n, s);
+}
+
+int pdlpk_spmv(const pdlpk_csr* A, int32_t orig, const double* v, double* out, int32_t parity,
+               cudaStream_t s) {
+  if (A->dim == 0) return 0;
+  const double* vals = orig ? A->value_orig : A->value;
+  if (parity) {
+    const int g = ew_blocks(A->dim);
+    if (A->wide) {
+      seq_spmv_kernel<int64_t><<<g, kT, 0, s>>>(static_cast<const int64_t*>(A->start), A->index,
+                                                vals, v, out, A->dim);
+    } else {
+      seq_spmv_kernel<int32_t><<<g, kT, 0, s>>>(static_cast<const int32_t*>(A->start), A->index,
+                                                vals, v, out, A->dim);
+    }
+    return ok();
+  }
+  return dispatch_pv(*A, LaunchSpmv{A, vals, v, out, s});
+}
+
+int pdlpk_diff_norm_sq(const double* a, const double* b, int64_t n, const pdlpk_red* red,
+                       double* slot, cudaStream_t s) {
+  auto f = [a, b] __device__(int64_t i, double* v) -> unsigned {
+    const double d = a[i] - b[i];
+    v[0] = d * d;
+    return 1u;
+  };
+  return multi_reduce<1>(f, n, red->parity ? PDLPK_RED_SHARD : PDLPK_RED_TREE, red->shards, 0u,
+                         red->scratch, slot, s);
+}
+
+int pdlpk_sub(const double* a, const double* b, double* out, int64_t n, cudaStream_t s) {
+  if (n > 0) sub_kernel<<<ew_blocks(n), kT, 0, s>>>(a, b, out, n);
+  return ok();
+}
+
+int pdlpk_average_into(const pdlpk_step_state* st, const double* sum_x, const double* sum_y,
+                       double* x, double* y, int64_t n, int64_t m, cudaStream_t s) {
+  if (n + m > 0) average_into_kernel<<<ew_blocks(n + m), kT, 0, s>>>(st, sum_x, sum_y, x, y, n, m);
+  return ok();
+}
+
+int pdlpk_scale_mul(const double* scale, const double* v, double* out, int64_t n,
+                    cudaStream_t s) {
+  if (n > 0) scale_mul_kernel<<<ew_blocks(n), kT, 0, s>>>(scale, v, out, n);
+  return ok();
+}
+
+int pdlpk_screen(const pdlpk_problem* P, int32_t orig, const double* x, const double* y,
+                 const double* ax, const double* aty, int32_t rc_mode, const pdlpk_red* red,
+                 double* r_out, double* slots, cudaStream_t s) {
+  const int64_t m = P->m, n = P->n;
+  const double* c = orig ? P->c_o : P->c;
+  const double* lc = orig ? P->lc_o : P->lc;
+  const double* uc = orig ? P->uc_o : P->uc;
+  const double* lv = orig ? P->lv_o : P->lv;
+  const double* uv = orig ? P->uv_o : P->uv;
+  const double* rs = orig ? nullptr : P->row_scale;
+  const double* cs = orig ? nullptr : P->col_scale;
+  // values: 0 primal_inf (max), 1 dual_inf (max), 2 pobj (sum), 3 penalty (sum)
+  auto f = [=] __device__(int64_t t, double* v) -> unsigned {
+    if (t < m) {
+      const int64_t j = t;
+      const double d = interval_distance(ax[j], lc[j], uc[j]);
+      v[0] = rs ? d / rs[j] : d;
+      unsigned use = 1u;
+      if (penalty_term(y[j], lc[j], uc[j], v[3])) use |= 8u;
+      return use;
+    }
+    const int64_t i = t - m;
+    const double xi = x[i];
+    const double d = interval_distance(xi, lv[i], uv[i]);
+    v[0] = cs ? d * cs[i] : d;
+    const double ri = reduced_cost(c[i], aty[i], xi, lv[i], uv[i], rc_mode);
+    if (r_out) r_out[i] = ri;
+    const double dd = fabs(c[i] - aty[i] - ri);
+    v[1] = cs ? dd / cs[i] : dd;
+    v[2] = c[i] * xi;
+    unsigned use = 7u;
+    if (penalty_term(ri, lv[i], uv[i], v[3])) use |= 8u;
+    return use;
+  };
+  return multi_reduce<4>(f, m + n, red->parity ? PDLPK_RED_SEQ : PDLPK_RED_TREE, red->shards,
+                         0x3u, red->scratch, slots, s);
+}
+
+int pdlpk_ray_primal_prep(const pdlpk_problem* P, int32_t orig, const double* yc, double* ray,
+                          const pdlpk_red* red, double* slots, cudaStream_t s) {
+  const double* lc = orig ? P->lc_o : P->lc;
+  const double* uc = orig ? P->uc_o : P->uc;
+  auto f = [=] __device__(int64_t j, double* v) -> unsigned {
+    const double r = cone_project(yc[j], cone_of_bounds(lc[j], uc[j]));
+    ray[j] = r;
+    v[0] = fabs(r);
+    return 1u;
+  };
+  return multi_reduce<1>(f, P->m, PDLPK_RED_TREE, red->shards, 0x1u, red->scratch, slots, s);
+}
+
+int pdlpk_ray_primal_finish(const pdlpk_problem* P, int32_t orig, const double* ray,
+                            const double* aty, double* rhat, const pdlpk_red* red,
+                            double* slots, cudaStream_t s) {
+  const int64_t m = P->m, n = P->n;
+  const double* lc = orig ? P->lc_o : P->lc;
+  const double* uc = orig ? P->uc_o : P->uc;
+  const double* lv = orig ? P->lv_o : P->lv;
+  const double* uv = orig ? P->uv_o : P->uv;
+  // values: 0 residual (max), 1 penalty (sum; dual_objective_value(ray, rhat))
+  auto f = [=] __device__(int64_t t, double* v) -> unsigned {
+    if (t < m) return penalty_term(ray[t], lc[t], uc[t], v[1]) ? 2u : 0u;
+    const int64_t i = t - m;
+    const double a = aty[i];
+    const double rh = cone_project(-a, cone_of_bounds(lv[i], uv[i]));
+    rhat[i] = rh;
+    v[0] = fabs(a + rh);
+    unsigned use = 1u;
+    if (penalty_term(rh, lv[i], uv[i], v[1])) use |= 2u;
+    return use;
+  };
+  return multi_reduce<2>(f, m + n, red->parity ? PDLPK_RED_SEQ : PDLPK_RED_TREE, red->shards,
+                         0x1u, red->scratch, slots, s);
+}
+
+int pdlpk_ray_dual_prep(const pdlpk_problem* P, int32_t orig, const double* xc,
+                        const pdlpk_red* red, double* slots, cudaStream_t s) {
+  const double* c = orig ? P->c_o : P->c;
+  const double* lv = orig ? P->lv_o : P->lv;
+  const double* uv = orig ? P->uv_o : P->uv;
+  // values: 0 |xc|_inf (max), 1 box residual (max), 2 c'xc (sum)
+  auto f = [=] __device__(int64_t i, double* v) -> unsigned {
+    const double xi = xc[i];
+    v[0] = fabs(xi);
+    v[1] = fabs(xi - cone_project(xi, recession_cone(lv[i], uv[i])));
+    v[2] = c[i] * xi;
+    return 7u;
+  };
+  return multi_reduce<3>(f, P->n, red->parity ? PDLPK_RED_SEQ : PDLPK_RED_TREE, red->shards,
+                         0x3u, red->scratch, slots, s);
+}
+
+int pdlpk_ray_dual_finish(const pdlpk_problem* P, int32_t orig, const double* ax,
+                          const pdlpk_red* red, double* slots, cudaStream_t s) {
+  const double* lc = orig ? P->lc_o : P->lc;
+  const double* uc = orig ? P->uc_o : P->uc;
+  auto f = [=] __device__(int64_t j, double* v) -> unsigned {
+    const double a = ax[j];
+    v[0] = fabs(a - cone_project(a, recession_cone(lc[j], uc[j])));
+    return 1u;
+  };
+  return multi_reduce<1>(f, P->m, PDLPK_RED_TREE, red->shards, 0x1u, red->scratch, slots, s);
+}
+
+int pdlpk_radius(const double* dx2, const double* dy2, double omega, double* out,
+                 cudaStream_t s) {
+  radius_kernel<<<1, 1, 0, s>>>(dx2, dy2, omega, out);
+  return ok();
+}
+
+int pdlpk_line_factors(const pdlpk_csr* A, int32_t one_norm, double* f, cudaStream_t s) {
+  if (A->dim == 0) return 0;
+  const int g = ew_blocks(A->dim);
+  if (A->wide) {
+    line_factor_kernel<int64_t><<<g, kT, 0, s>>>(static_cast<const int64_t*>(A->start), A->value,
+                                                 A->dim, one_norm, f);
+  } else {
+    line_factor_kernel<int32_t><<<g, kT, 0, s>>>(static_cast<const int32_t*>(A->start), A->value,
+                                                 A->dim, one_norm, f);
+  }
+  return ok();
+}
+
+int pdlpk_apply_factors(const pdlpk_csr* A, double* value, const double* f_primary,
+                        const double* f_secondary, cudaStream_t s) {
+  if (A->dim == 0) return 0;
+  const int g = ew_blocks(A->dim);
+  if (A->wide) {
+    apply_factor_kernel<int64_t><<<g, kT, 0, s>>>(static_cast<const int64_t*>(A->start), A->index,
+                                                  value, A->dim, f_primary, f_secondary);
+  } else {
+    apply_factor_kernel<int32_t><<<g, kT, 0, s>>>(static_cast<const int32_t*>(A->start), A->index,
+                                                  value, A->dim, f_primary, f_secondary);
+  }
+  return ok();
+}
+
+int pdlpk_apply_vec_factors(double* lc, double* uc, double* row_scale, const double* fr,
+                            int64_t m, double* c, double* lv, double* uv, double* col_scale,
+                            const double* fc, int64_t n, cudaStream_t s) {
+  if (m + n > 0) {
+    apply_vec_factor_kernel<<<ew_blocks(m + n), kT, 0, s>>>(lc, uc, row_scale, fr, m, c, lv, uv,
+                                                           col_scale, fc, n);
+  }
+  return ok();
+}
+
+int pdlpk_abs_max(const double* v, int64_t n, const pdlpk_red* red, double* slot,
+                  cudaStream_t s) {
+  auto f = [v] __device__(int64_t i, double* o) -> unsigned {
+    o[0] = fabs(v[i]);
+    return 1u;
+  };
+  return multi_reduce<1>(f, n, PDLPK_RED_TREE, 1, 0x1u, red->scratch, slot, s);
+}
+
+int pdlpk_primal_weight_sums(const double* c, int64_t n, const double* lc, const double* uc,
+                             int64_t m, const pdlpk_red* red, double* slots, cudaStream_t s) {
+  auto f = [=] __device__(int64_t t, double* v) -> unsigned {
+    if (t < n) {
+      v[0] = c[t] * c[t];
+      return 1u;
+    }
+    const int64_t j = t - n;
+    const double lo = lc[j], hi = uc[j];
+    double mag = 0.0;
+    if (finite_d(lo)) mag = max_keep(mag, fabs(lo));
+    if (finite_d(hi)) mag = max_keep(mag, fabs(hi));
+    v[1] = mag * mag;
+    return 2u;
+  };
+  return multi_reduce<2>(f, n + m, red->parity ? PDLPK_RED_SEQ : PDLPK_RED_TREE, red->shards, 0u,
+                         red->scratch, slots, s);
+}
+
+int pdlpk_initial_point(const double* lv, const double* uv, double* x, int64_t n,
+                        cudaStream_t s) {
+  if (n > 0) initial_point_kernel<<<ew_blocks(n), kT, 0, s>>>(lv, uv, x, n);
+  return ok();
+}
+
+int pdlpk_dual_feas_bounds(const double* c, const double* lv, const double* uv, int64_t n,
+                           const double* lc, const double* uc, int64_t m, double* sub_lc,
+                           double* sub_uc, double* sub_lv, double* sub_uv, cudaStream_t s) {
+  if (n + m > 0) {
+    dual_feas_bounds_kernel<<<ew_blocks(n + m), kT, 0, s>>>(c, lv, uv, n, lc, uc, m, sub_lc,
+                                                           sub_uc, sub_lv, sub_uv);
+  }
+  return ok();
+}
+
+int pdlpk_check_finite(const double* v, int64_t n, int32_t code, int32_t* first,
+                       cudaStream_t s) {
+  if (n > 0) find_nonfinite_kernel<<<ew_blocks(n), kT, 0, s>>>(v, n, code, first);
+  return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+// kernels.h — the thin internal C-ABI between the host C++ driver
+// (solver.cpp) and the hand-written sm_100a kernels (k_*.cu).
+//
+// Plain structs of device pointers and sizes; every launcher is extern "C",
+// enqueues on the given stream and never synchronises.  Scalars that the
+// host needs come back through a small device "slot" array that the driver
+// copies in one batch (pdlpk_slots_*).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Reduction orders.  PARITY reproduces the reference's arithmetic order:
+ *   SEQ   — one sequential chain in index order (the reference's plain loops)
+ *   SHARD — make_shard_plan(dim, 1, S) chains + ascending combine
+ *           (kernels.hpp:69-97, shard.hpp:24-40)
+ * PERF maps both onto TREE (fixed block tree; deterministic run to run). */
+#define PDLPK_RED_TREE 0
+#define PDLPK_RED_SEQ 1
+#define PDLPK_RED_SHARD 2
+
+/* Device CSR for one orientation (int32 secondary indices, fp64 values;
+ * row pointers int32 when nnz < 2^31, else int64) plus the perf-mode
+ * load-balancing schedule built at upload time. */
+typedef struct pdlpk_csr {
+  int64_t dim;
+  int64_t nnz;
+  const void* start; /* dim+1 entries, int32 or int64 */
+  int32_t wide;      /* 1: start is int64 */
+  int32_t vec;       /* lanes per short row (power of two, 1..32) */
+  const int32_t* index;
+  const double* value;      /* scaled values (the iteration matrix) */
+  const double* value_orig; /* original values (verification products) */
+  const int32_t* long_rows; /* rows with len > t_med, one CTA each */
+  int64_t n_long;
+  const int32_t* med_rows; /* rows with t_short < len <= t_med, one warp each */
+  int64_t n_med;
+  int32_t t_short;
+  int32_t t_med;
+  int32_t short_blocks; /* CTAs for the short-row segment */
+  int32_t _pad;
+} pdlpk_csr;
+
+/* Device-resident step controller: one per inner loop (main / polish). */
+typedef struct pdlpk_step_state {
+  double eta;      /* trial step size for the next attempt */
+  double omega;    /* primal weight */
+  double eta_used; /* step size of the last accepted attempt */
+  double min_eta_bar;
+  double avg_weight; /* AverageState::weight */
+  double avg_w;      /* pending average weight (deferred add) */
+  double dx2, dy2, curv, eta_bar, inf_x, inf_y; /* last attempt */
+  int64_t k;        /* accepted steps in this inner loop (st.k == ctrl.k) */
+  int64_t k_target; /* halt when k reaches this */
+  int64_t accepted;
+  int64_t retries;
+  int64_t attempts;
+  int64_t avg_count;
+  int32_t cur;    /* ping-pong index of the current iterate */
+  int32_t halt;   /* 1: every step kernel returns immediately */
+  int32_t status; /* 0 running, 1 numerical error */
+  int32_t attempt_in_step;
+  int32_t max_retries;
+  int32_t avg_pending;
+  int32_t fixed; /* fixed-step mode (solver.hpp:477-491) */
+  int32_t table_short; /* schedule table exhausted */
+  uint32_t ticket;     /* last-CTA election */
+  uint32_t _pad;
+} pdlpk_step_state;
+
+typedef struct pdlpk_problem {
+  int64_t m;
+  int64_t n;
+  pdlpk_csr K;  /* row layout of A   */
+  pdlpk_csr KT; /* column layout of A */
+  const double *c, *lc, *uc, *lv, *uv;           /* scaled */
+  const double *c_o, *lc_o, *uc_o, *lv_o, *uv_o; /* original */
+  const double *row_scale, *col_scale;           /* m, n */
+} pdlpk_problem;
+
+typedef struct pdlpk_step_args {
+  pdlpk_problem P;
+  double* x[2];
+  double* y[2];
+  double* aty[2];
+  double* xbar;     /* n: 2x' - x */
+  double* dy;       /* m: y' - y */
+  double* aty_diff; /* n: A'(y'-y) (parity path) */
+  double* sum_x;    /* n */
+  double* sum_y;    /* m */
+  pdlpk_step_state* state;
+  const double* f_down; /* 1 - (max(k,1)+1)^-0.3, host libm */
+  const double* f_up;   /* 1 + (max(k,1)+1)^-0.6 */
+  int64_t table_len;
+  double* part2; /* per-CTA partials of the row pass */
+  double* part3; /* per-CTA partials of the column pass */
+  int32_t mode;  /* PDLP_MODE_PERF / PDLP_MODE_PARITY */
+  int32_t shards;
+  double* shard_part; /* parity: 4*shards partials */
+} pdlpk_step_args;
+
+/* Reduction context for cadence operations. */
+typedef struct pdlpk_red {
+  int32_t order;  /* PDLPK_RED_* for sequential-loop sums (SEQ in parity, TREE in perf) */
+  int32_t shards; /* S for sharded reductions (parity) */
+  int32_t parity;
+  int32_t _pad;
+  double* scratch; /* >= pdlpk_red_scratch_doubles() */
+} pdlpk_red;
+
+int64_t pdlpk_red_scratch_doubles(void);
+int64_t pdlpk_step_partials(const pdlpk_problem* P);
+
+/* ---------------------------------------------------------------- setup --- */
+int pdlpk_index_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s);
+int pdlpk_start_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s);
+
+/* ----------------------------------------------------------------- step --- */
+/* Arm the controller for a run: k_target, halt = 0. */
+int pdlpk_arm(pdlpk_step_state* st, int64_t k_target, cudaStream_t s);
+/* One step attempt (primal pass, row pass + dual update, column pass +
+ * decision).  Every kernel is a no-op once state->halt is set. */
+int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s);
+/* Same, recording ev[0..3] around the launches (primal | row | column[+reduce]). */
+int pdlpk_attempt_timed(const pdlpk_step_args* a, cudaEvent_t* ev, cudaStream_t s);
+/* Apply a pending deferred average add (AverageState::add, step.hpp:209-216). */
+int pdlpk_flush_average(const pdlpk_step_args* a, cudaStream_t s);
+
+/* ------------------------------------------------------------- cadence --- */
+/* out = A v with the given layout; orig != 0 uses the original values. */
+int pdlpk_spmv(const pdlpk_csr* A, int32_t orig, const double* v, double* out, int32_t parity,
+               cudaStream_t s);
+
+/* slot = sum_i (a_i - b_i)^2 over dim n (sharded in parity). */
+int pdlpk_diff_norm_sq(const double* a, const double* b, int64_t n, const pdlpk_red* red,
+                       double* slot, cudaStream_t s);
+/* out = a - b */
+int pdlpk_sub(const double* a, const double* b, double* out, int64_t n, cudaStream_t s);
+/* out = sum * (1/weight), weight read from the state (average_into, step.hpp:219-227). */
+int pdlpk_average_into(const pdlpk_step_state* st, const double* sum_x, const double* sum_y,
+                       double* x, double* y, int64_t n, int64_t m, cudaStream_t s);
+/* out = scale .* v (unscale_primal / unscale_dual, rescaling.hpp:145-153). */
+int pdlpk_scale_mul(const double* scale, const double* v, double* out, int64_t n,
+                    cudaStream_t s);
+
+/* Residual screen (recover_reduced_costs_from + residuals_from_scaled /
+ * kkt_residuals_from, residuals.hpp:29-47, 98-133, 165-185).  Uses the scaled
+ * (orig = 0) or original (orig = 1, unit scales) data.  slots[0..3] =
+ * primal_inf, dual_inf, pobj, penalty (dobj = -penalty).  r_out (n) may be NULL. */
+int pdlpk_screen(const pdlpk_problem* P, int32_t orig, const double* x, const double* y,
+                 const double* ax, const double* aty, int32_t rc_mode, const pdlpk_red* red,
+                 double* r_out, double* slots, cudaStream_t s);
+
+/* Ray tests (residuals.hpp:222-299), split around their matrix product:
+ *  primal: prep writes ray = proj_cone(yc), slot0 = |ray|_inf;
+ *          finish (after aty = A'ray) writes rhat, slot1 = residual,
+ *          slot2 = penalty of (ray, rhat) (objective = -slot2).
+ *  dual:   prep: slot0 = |xc|_inf, slot1 = box residual, slot2 = c'xc;
+ *          finish (after ax = A xc): slot3 = row residual. */
+int pdlpk_ray_primal_prep(const pdlpk_problem* P, int32_t orig, const double* yc, double* ray,
+                          const pdlpk_red* red, double* slots, cudaStream_t s);
+int pdlpk_ray_primal_finish(const pdlpk_problem* P, int32_t orig, const double* ray,
+                            const double* aty, double* rhat, const pdlpk_red* red,
+                            double* slots, cudaStream_t s);
+int pdlpk_ray_dual_prep(const pdlpk_problem* P, int32_t orig, const double* xc,
+                        const pdlpk_red* red, double* slots, cudaStream_t s);
+int pdlpk_ray_dual_finish(const pdlpk_problem* P, int32_t orig, const double* ax,
+                          const pdlpk_red* red, double* slots, cudaStream_t s);
+
+/* Normalized duality gap (restarts.hpp:107-220).  r read from slot r_slot
+ * (radius) unless r_slot == NULL, in which case r_value is used.  Result in
+ * *gap_slot.  work must hold pdlpk_gap_work_bytes(n, m) bytes. */
+size_t pdlpk_gap_work_bytes(int64_t n, int64_t m);
+int pdlpk_gap(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
+              const double* aty, double omega, const double* r_slot, double r_value,
+              const pdlpk_red* red, void* work, double* gap_slot, cudaStream_t s);
+/* slot = sqrt(omega*dx2 + dy2/omega) from two slots (restart_progress_metric). */
+int pdlpk_radius(const double* dx2, const double* dy2, double omega, double* out,
+                 cudaStream_t s);
+
+/* ------------------------------------------------------- preconditioning --- */
+/* f[line] = sqrt(max|v|) or 1 (ruiz) / sqrt(sum|v|) or 1 (pock-chambolle),
+ * per line of the layout (rescaling.hpp:80-127). */
+int pdlpk_line_factors(const pdlpk_csr* A, int32_t one_norm, double* f, cudaStream_t s);
+/* value /= f_primary[line] * f_secondary[index] for one layout. */
+int pdlpk_apply_factors(const pdlpk_csr* A, double* value, const double* f_primary,
+                        const double* f_secondary, cudaStream_t s);
+/* Vector part of apply_factors (rescaling.hpp:61-73). */
+int pdlpk_apply_vec_factors(double* lc, double* uc, double* row_scale, const double* fr,
+                            int64_t m, double* c, double* lv, double* uv, double* col_scale,
+                            const double* fc, int64_t n, cudaStream_t s);
+/* slot = max |v| (initial_step_size, step.hpp:14-18). */
+int pdlpk_abs_max(const double* v, int64_t n, const pdlpk_red* red, double* slot,
+                  cudaStream_t s);
+/* slots[0] = sum c^2, slots[1] = sum mag(lc,uc)^2 (initialize_primal_weight,
+ * restarts.hpp:278-294). */
+int pdlpk_primal_weight_sums(const double* c, int64_t n, const double* lc, const double* uc,
+                             int64_t m, const pdlpk_red* red, double* slots, cudaStream_t s);
+/* x0 = clamp(0, lv, uv) (initial_point, solver.hpp:196-202). */
+int pdlpk_initial_point(const double* lv, const double* uv, double* x, int64_t n,
+                        cudaStream_t s);
+/* Dual-feasibility subproblem bounds (problem.hpp:181-238):
+ * con bounds (n) from the parent objective and variable cones, variable
+ * bounds (m) from the parent constraint cones. */
+int pdlpk_dual_feas_bounds(const double* c, const double* lv, const double* uv, int64_t n,
+                           const double* lc, const double* uc, int64_t m, double* sub_lc,
+                           double* sub_uc, double* sub_lv, double* sub_uv, cudaStream_t s);
+/* Validation scan (problem.hpp:119-154 minus layouts_consistent):
+ * slot[0] = first failing check code (0 = ok), slot[1] = index. */
+int pdlpk_check_finite(const double* v, int64_t n, int32_t code, int32_t* first, cudaStream_t s);
+
+#ifdef __cplusplus
+}
+#endif

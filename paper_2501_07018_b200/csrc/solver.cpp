@@ -1,0 +1,1518 @@
+// Host C++ driver of the B200 PDLP solver and the public C-ABI (pdlp_b200.h).
+//
+// This is a restatement of the reference driver
+//   solve            proj/include/pdhglp/solver.hpp:535-608
+//   run_inner        solver.hpp:350-531  (64-step cadence, restarts, rays, polish gate)
+//   screen_and_verify / capture_current / detect_rays / attempt_polish
+//                    solver.hpp:207-348
+// in which every O(n), O(m) or O(nnz) operation is a device kernel reached
+// through the thin internal C-ABI of kernels.h.  The host holds only scalars
+// (step controller mirror, restart metrics, omega) and makes the branchy
+// decisions on them with the reference's exact formulas; vectors live in HBM
+// for the whole solve and come back once, at the end.  There is no CPU
+// fallback: without a usable device every entry point fails with
+// PDLP_ERR_CUDA.
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "device.hpp"
+#include "kernels.h"
+#include "pdlp_b200.h"
+
+namespace pdlp_host {
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+using Clock = std::chrono::steady_clock;
+
+thread_local std::string g_last_error;
+
+struct InvalidProblem : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+// ------------------------------------------------------------- host types ---
+struct Summary {  // ResidualSummary, residuals.hpp:66-73
+  double primal = kInf, dual = kInf, pobj = 0.0, dobj = 0.0, abs_gap = kInf, rel_gap = kInf;
+};
+
+// finish_summary (residuals.hpp:98-114)
+Summary finish_summary(double primal_inf, double dual_inf, double pobj, double dobj) {
+  Summary s;
+  s.primal = primal_inf;
+  s.dual = dual_inf;
+  s.pobj = pobj;
+  s.dobj = dobj;
+  if (!std::isfinite(dobj)) return s;
+  s.abs_gap = std::abs(pobj - dobj);
+  const double denom = std::max(std::abs(pobj), std::abs(dobj));
+  s.rel_gap = s.abs_gap == 0.0 ? 0.0 : s.abs_gap / denom;
+  return s;
+}
+
+struct Tol {
+  double eps_primal = 1e-8, eps_dual = 1e-8, eps_rel_gap = 1e-2;
+};
+
+bool check_termination(const Summary& s, const Tol& t) {  // residuals.hpp:193-196
+  return s.primal <= t.eps_primal && s.dual <= t.eps_dual && s.rel_gap <= t.eps_rel_gap;
+}
+
+enum Status { kOptimal = 0, kPrimalInf, kDualInf, kIterLimit, kTimeLimit, kNumErr };
+
+const char* status_name(int s) {  // solver.hpp:44-54
+  switch (s) {
+    case kOptimal: return "optimal";
+    case kPrimalInf: return "primal_infeasible";
+    case kDualInf: return "dual_infeasible";
+    case kIterLimit: return "iteration_limit";
+    case kTimeLimit: return "time_limit";
+    default: return "numerical_error";
+  }
+}
+
+enum Reason { kNone = 0, kSufficient, kStalled, kArtificial };
+const char* reason_name(int r) {
+  switch (r) {
+    case kSufficient: return "sufficient";
+    case kStalled: return "stalled";
+    case kArtificial: return "artificial";
+    default: return "none";
+  }
+}
+
+struct Thresholds {
+  double sufficient = 0.1, necessary = 0.9, artificial = 0.5;
+};
+
+// should_restart (restarts.hpp:257-271)
+int should_restart(double cand, double mu_last, double prev_mu, int64_t since, int64_t total,
+                   const Thresholds& th) {
+  if (std::isfinite(mu_last)) {
+    if (cand <= th.sufficient * mu_last) return kSufficient;
+    if (cand <= th.necessary * mu_last && cand > prev_mu) return kStalled;
+  }
+  if (static_cast<double>(since) >= th.artificial * static_cast<double>(total)) return kArtificial;
+  return kNone;
+}
+
+// update_primal_weight (restarts.hpp:298-303)
+double update_primal_weight(double dx, double dy, double omega_prev) {
+  const double theta = 0.5, eps_zero = 1e-12;
+  if (!(dx > eps_zero) || !(dy > eps_zero)) return omega_prev;
+  return std::exp(theta * std::log(dy / dx) + (1.0 - theta) * std::log(omega_prev));
+}
+
+// --------------------------------------------------------- device problem ---
+struct DevLayout {
+  DevBuf<int32_t> start32;
+  DevBuf<int64_t> start64;
+  DevBuf<int32_t> index;
+  DevBuf<double> value, value_orig;
+  DevBuf<int32_t> long_rows, med_rows;
+  pdlpk_csr view{};
+};
+
+// Perf-mode schedule (spmv.cuh): lanes per short line from the mean length,
+// medium lines one warp, long lines one CTA.
+void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
+  const int64_t nnz = dim > 0 ? start[dim] : 0;
+  const double mean = dim > 0 ? static_cast<double>(nnz) / static_cast<double>(dim) : 0.0;
+  int vec = 1;
+  while (vec < 32 && static_cast<double>(vec) * 8.0 < mean) vec *= 2;
+  const int64_t t_short = std::max<int64_t>(16 * vec, 32);
+  const int64_t t_med = 1024;
+  std::vector<int32_t> med, lng;
+  for (int64_t r = 0; r < dim; ++r) {
+    const int64_t len = start[r + 1] - start[r];
+    if (len > t_med) {
+      lng.push_back(static_cast<int32_t>(r));
+    } else if (len > t_short) {
+      med.push_back(static_cast<int32_t>(r));
+    }
+  }
+  L.long_rows.alloc(lng.size());
+  L.med_rows.alloc(med.size());
+  if (!lng.empty()) {
+    PDLP_CK(cudaMemcpy(L.long_rows.get(), lng.data(), lng.size() * 4, cudaMemcpyHostToDevice));
+  }
+  if (!med.empty()) {
+    PDLP_CK(cudaMemcpy(L.med_rows.get(), med.data(), med.size() * 4, cudaMemcpyHostToDevice));
+  }
+  const int64_t groups_per_block = 256 / vec;
+  int64_t sb = (dim + groups_per_block - 1) / groups_per_block;
+  sb = std::min<int64_t>(sb, 148 * 16);
+  sb = std::max<int64_t>(sb, 1);
+  L.view.vec = vec;
+  L.view.t_short = static_cast<int32_t>(t_short);
+  L.view.t_med = static_cast<int32_t>(t_med);
+  L.view.long_rows = L.long_rows.get();
+  L.view.n_long = static_cast<int64_t>(lng.size());
+  L.view.med_rows = L.med_rows.get();
+  L.view.n_med = static_cast<int64_t>(med.size());
+  L.view.short_blocks = static_cast<int32_t>(sb);
+}
+
+void upload_layout(const pdlp_csr_view& v, DevLayout& L, cudaStream_t s) {
+  const int64_t dim = v.primary_dim, nnz = v.nnz;
+  const bool wide = nnz >= (int64_t(1) << 31) - 1;
+  DevBuf<int64_t> tmp;
+  // start
+  if (wide) {
+    L.start64.alloc(dim + 1);
+    PDLP_CK(cudaMemcpyAsync(L.start64.get(), v.start, (dim + 1) * 8, cudaMemcpyHostToDevice, s));
+  } else {
+    tmp.alloc(dim + 1);
+    L.start32.alloc(dim + 1);
+    PDLP_CK(cudaMemcpyAsync(tmp.get(), v.start, (dim + 1) * 8, cudaMemcpyHostToDevice, s));
+    PDLP_LAUNCH(pdlpk_start_to_i32(tmp.get(), L.start32.get(), dim + 1, s));
+  }
+  // index (int64 -> int32) in chunks to bound the staging buffer
+  L.index.alloc(nnz);
+  const int64_t chunk = std::min<int64_t>(nnz, int64_t(1) << 26);
+  if (chunk > 0) {
+    PDLP_CK(cudaStreamSynchronize(s));
+    tmp.alloc(chunk);
+    for (int64_t off = 0; off < nnz; off += chunk) {
+      const int64_t len = std::min(chunk, nnz - off);
+      PDLP_CK(cudaMemcpyAsync(tmp.get(), v.index + off, len * 8, cudaMemcpyHostToDevice, s));
+      PDLP_LAUNCH(pdlpk_index_to_i32(tmp.get(), L.index.get() + off, len, s));
+    }
+  }
+  L.value_orig.alloc(nnz);
+  L.value.alloc(nnz);
+  if (nnz > 0) {
+    PDLP_CK(cudaMemcpyAsync(L.value_orig.get(), v.value, nnz * 8, cudaMemcpyHostToDevice, s));
+    PDLP_CK(cudaMemcpyAsync(L.value.get(), L.value_orig.get(), nnz * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  PDLP_CK(cudaStreamSynchronize(s));
+  L.view.dim = dim;
+  L.view.nnz = nnz;
+  L.view.wide = wide ? 1 : 0;
+  L.view.start = wide ? static_cast<const void*>(L.start64.get())
+                      : static_cast<const void*>(L.start32.get());
+  L.view.index = L.index.get();
+  L.view.value = L.value.get();
+  L.view.value_orig = L.value_orig.get();
+  build_schedule(v.start, dim, L);
+}
+
+DevBuf<double> upload_vec(const double* h, int64_t n, cudaStream_t s) {
+  DevBuf<double> d(n);
+  if (n > 0) PDLP_CK(cudaMemcpyAsync(d.get(), h, n * 8, cudaMemcpyHostToDevice, s));
+  return d;
+}
+
+DevBuf<double> dev_fill(int64_t n, double v, cudaStream_t s) {
+  DevBuf<double> d(n);
+  if (n > 0) {
+    std::vector<double> h(n, v);
+    PDLP_CK(cudaMemcpyAsync(d.get(), h.data(), n * 8, cudaMemcpyHostToDevice, s));
+    PDLP_CK(cudaStreamSynchronize(s));
+  }
+  return d;
+}
+
+void dev_copy(double* dst, const double* src, int64_t n, cudaStream_t s) {
+  if (n > 0) PDLP_CK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, s));
+}
+
+void dev_zero(double* dst, int64_t n, cudaStream_t s) {
+  if (n > 0) PDLP_CK(cudaMemsetAsync(dst, 0, n * 8, s));
+}
+
+struct DevProblem {
+  int64_t m = 0, n = 0;
+  DevLayout row, col;
+  DevBuf<double> c, lc, uc, lv, uv;            // scaled (in place)
+  DevBuf<double> c_o, lc_o, uc_o, lv_o, uv_o;  // original
+  DevBuf<double> row_scale, col_scale;
+
+  pdlpk_problem view() const {
+    pdlpk_problem P{};
+    P.m = m;
+    P.n = n;
+    P.K = row.view;
+    P.KT = col.view;
+    P.c = c.get();
+    P.lc = lc.get();
+    P.uc = uc.get();
+    P.lv = lv.get();
+    P.uv = uv.get();
+    P.c_o = c_o.get();
+    P.lc_o = lc_o.get();
+    P.uc_o = uc_o.get();
+    P.lv_o = lv_o.get();
+    P.uv_o = uv_o.get();
+    P.row_scale = row_scale.get();
+    P.col_scale = col_scale.get();
+    return P;
+  }
+};
+
+// validate (problem.hpp:119-154), including layouts_consistent
+// (sparse.hpp:118-133) as a per-entry lookup instead of a rebuild.
+void validate(const pdlp_problem_view* p) {
+  auto fail = [](const char* msg, int64_t idx) {
+    throw InvalidProblem(std::string("invalid problem: ") + msg + " (index " +
+                         std::to_string(idx) + ")");
+  };
+  const int64_t m = p->rows, n = p->cols;
+  if (m < 0 || n < 0) fail("negative dimension", -1);
+  if (p->by_row.primary_dim != m) fail("row layout dimension != rows", -1);
+  if (p->by_col.primary_dim != n) fail("column layout dimension != cols", -1);
+  for (int64_t i = 0; i < n; ++i) {
+    if (!std::isfinite(p->objective[i])) fail("objective entry not finite", i);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const double lo = p->var_lower[i], hi = p->var_upper[i];
+    if (std::isnan(lo) || std::isnan(hi)) fail("variable bound is NaN", i);
+    if (lo == kInf) fail("variable lower bound is +inf", i);
+    if (hi == -kInf) fail("variable upper bound is -inf", i);
+    if (lo > hi) fail("variable bounds crossed", i);
+  }
+  for (int64_t j = 0; j < m; ++j) {
+    const double lo = p->con_lower[j], hi = p->con_upper[j];
+    if (std::isnan(lo) || std::isnan(hi)) fail("constraint bound is NaN", j);
+    if (lo == kInf) fail("constraint lower bound is +inf", j);
+    if (hi == -kInf) fail("constraint upper bound is -inf", j);
+    if (lo > hi) fail("constraint bounds crossed", j);
+  }
+  const int64_t nnz = p->by_row.nnz;
+  for (int64_t k = 0; k < nnz; ++k) {
+    if (!std::isfinite(p->by_row.value[k])) fail("matrix entry not finite", k);
+  }
+  // layouts_consistent: same nnz, row lines strictly sorted, and every column
+  // entry found with an equal value in its row (a bijection since counts match
+  // and row lines are duplicate free).
+  const pdlp_csr_view& R = p->by_row;
+  const pdlp_csr_view& C = p->by_col;
+  bool consistent = R.nnz == C.nnz && R.start[0] == 0 && C.start[0] == 0 &&
+                    R.start[m] == R.nnz && C.start[n] == C.nnz;
+  std::vector<int64_t> row_count(consistent ? m : 0, 0);
+  for (int64_t r = 0; consistent && r < m; ++r) {
+    if (R.start[r + 1] < R.start[r]) consistent = false;
+    for (int64_t k = R.start[r]; consistent && k < R.start[r + 1]; ++k) {
+      if (R.index[k] < 0 || R.index[k] >= n) consistent = false;
+      if (k > R.start[r] && R.index[k] <= R.index[k - 1]) consistent = false;
+    }
+  }
+  for (int64_t c = 0; consistent && c < n; ++c) {
+    if (C.start[c + 1] < C.start[c]) {
+      consistent = false;
+      break;
+    }
+    for (int64_t k = C.start[c]; consistent && k < C.start[c + 1]; ++k) {
+      const int64_t r = C.index[k];
+      if (r < 0 || r >= m) {
+        consistent = false;
+        break;
+      }
+      const int64_t* lo = R.index + R.start[r];
+      const int64_t* hi = R.index + R.start[r + 1];
+      const int64_t* it = std::lower_bound(lo, hi, c);
+      if (it == hi || *it != c || R.value[it - R.index] != C.value[k]) consistent = false;
+      ++row_count[r];
+    }
+  }
+  for (int64_t r = 0; consistent && r < m; ++r) {
+    if (row_count[r] != R.start[r + 1] - R.start[r]) consistent = false;
+  }
+  if (!consistent) fail("row/column layouts disagree", -1);
+}
+
+// ------------------------------------------------------------ inner state ---
+struct Cert {
+  bool have = false;
+  int kind = 0;
+  DevBuf<double> ray_x, ray_y, ray_r;
+  double residual = kInf, objective = 0.0;
+  std::string source;
+};
+
+struct Inner {  // InnerState (solver.hpp:135-193), vectors on device
+  int64_t n = 0, m = 0;
+  DevBuf<double> x[2], y[2], aty[2];
+  DevBuf<double> xbar, dy, aty_diff, sum_x, sum_y;
+  DevBuf<double> ref_x, ref_y, ax_cur, avg_x, avg_y, ax_avg, aty_avg, diff_x, diff_y, rc_a, rc_b;
+  DevBuf<double> sol_x, sol_y, sol_r, tmp_x, tmp_y, tmp_r, ray_n, ray_m, prod_n, prod_m;
+  DevBuf<pdlpk_step_state> state;
+  DevBuf<double> part2, part3, shard_part;
+  pdlpk_step_state hs{};  // host mirror of the controller
+
+  // Host scalars of InnerState
+  double omega = 1.0;
+  double last_eta = 0.0;
+  double mu_last = kInf, prev_candidate_mu = kInf;
+  int64_t k_last_restart = 0, restarts = 0;
+  int64_t next_polish_trigger = 100, polish_iterations = 0;
+  Summary sol_summary;
+  bool have_sol = false;
+  std::string detail;
+  Cert cert;
+
+  void allocate(int64_t cols, int64_t rows, int64_t partials, int shards) {
+    n = cols;
+    m = rows;
+    for (int b = 0; b < 2; ++b) {
+      x[b].alloc(n);
+      y[b].alloc(m);
+      aty[b].alloc(n);
+    }
+    for (DevBuf<double>* v : {&xbar, &aty_diff, &sum_x, &ref_x, &avg_x, &aty_avg, &diff_x, &rc_a,
+                              &rc_b, &sol_x, &sol_r, &tmp_x, &tmp_r, &ray_n, &prod_n}) {
+      v->alloc(n);
+    }
+    for (DevBuf<double>* v :
+         {&dy, &sum_y, &ref_y, &ax_cur, &avg_y, &ax_avg, &diff_y, &sol_y, &tmp_y, &ray_m, &prod_m}) {
+      v->alloc(m);
+    }
+    cert.ray_x.alloc(n);
+    cert.ray_y.alloc(m);
+    cert.ray_r.alloc(n);
+    state.alloc(1);
+    part2.alloc(partials);
+    part3.alloc(partials);
+    shard_part.alloc(5 * std::max(shards, 1));
+  }
+  int cur() const { return hs.cur; }
+  int64_t k() const { return hs.k; }
+};
+
+struct InnerCfg {  // InnerConfig (solver.hpp:114-133)
+  Tol tol;
+  bool feasibility_only = false;
+  int rc_mode = 0;  // 0 Natural, 1 BoundRobust
+  int64_t budget = 0;
+  Clock::time_point deadline = Clock::time_point::max();
+  bool enable_restarts = true;
+  bool detect_infeasibility = true;
+  bool enable_polish = false;
+  double eps_ray = 1e-12;
+  int64_t check_interval = 64;
+  Thresholds th;
+  std::optional<double> fixed_eta;
+  bool allow_omega_updates = true;
+  pdlp_observer_fn observer = nullptr;
+  void* observer_user = nullptr;
+  bool logging = false;
+  const char* tag = "main";
+};
+
+// ------------------------------------------------------------------ engine ---
+class Engine {
+ public:
+  Engine(const pdlp_problem_view* p, const pdlp_options& o) : opt_(o) {
+    parity_ = o.mode == PDLP_MODE_PARITY;
+    shards_ = std::max(1, o.threads) * std::max(1, o.shards_per_thread);
+    PDLP_CK(cudaSetDevice(o.device));
+    stream_ = std::make_unique<Stream>();
+    load(p);
+  }
+
+  cudaStream_t s() const { return stream_->get(); }
+  const DevProblem& problem() const { return prob_; }
+  bool parity() const { return parity_; }
+
+  // ---- setup -------------------------------------------------------------
+  void load(const pdlp_problem_view* p) {
+    const auto t0 = Clock::now();
+    prob_.m = p->rows;
+    prob_.n = p->cols;
+    const int64_t m = p->rows, n = p->cols;
+    upload_layout(p->by_row, prob_.row, s());
+    upload_layout(p->by_col, prob_.col, s());
+    prob_.c_o = upload_vec(p->objective, n, s());
+    prob_.lc_o = upload_vec(p->con_lower, m, s());
+    prob_.uc_o = upload_vec(p->con_upper, m, s());
+    prob_.lv_o = upload_vec(p->var_lower, n, s());
+    prob_.uv_o = upload_vec(p->var_upper, n, s());
+    prob_.c.alloc(n);
+    prob_.lc.alloc(m);
+    prob_.uc.alloc(m);
+    prob_.lv.alloc(n);
+    prob_.uv.alloc(n);
+    dev_copy(prob_.c.get(), prob_.c_o.get(), n, s());
+    dev_copy(prob_.lc.get(), prob_.lc_o.get(), m, s());
+    dev_copy(prob_.uc.get(), prob_.uc_o.get(), m, s());
+    dev_copy(prob_.lv.get(), prob_.lv_o.get(), n, s());
+    dev_copy(prob_.uv.get(), prob_.uv_o.get(), n, s());
+    prob_.row_scale = dev_fill(m, 1.0, s());
+    prob_.col_scale = dev_fill(n, 1.0, s());
+    slots_.alloc(64);
+    PDLP_CK(cudaMallocHost(&host_slots_, 64 * sizeof(double)));
+    red_scratch_.alloc(std::max<int64_t>(pdlpk_red_scratch_doubles(), 8 * int64_t(shards_) + 64));
+    const int64_t gap_n = std::max(n + 2 * m, m + 2 * n);
+    (void)gap_n;
+    gap_work_.alloc(std::max(pdlpk_gap_work_bytes(n, m), pdlpk_gap_work_bytes(m, n)));
+    zeros_n_ = dev_fill(n, 0.0, s());
+    zeros_m_ = dev_fill(m, 0.0, s());
+    PDLP_CK(cudaStreamSynchronize(s()));
+    upload_seconds_ = std::chrono::duration<double>(Clock::now() - t0).count();
+  }
+
+  ~Engine() {
+    if (host_slots_ != nullptr) cudaFreeHost(host_slots_);
+    for (cudaEvent_t e : prof_ev_) cudaEventDestroy(e);
+  }
+
+  void ensure_prof_events(int64_t attempts) {
+    while (static_cast<int64_t>(prof_ev_.size()) < 4 * attempts) {
+      cudaEvent_t e;
+      PDLP_CK(cudaEventCreate(&e));
+      prof_ev_.push_back(e);
+    }
+  }
+
+  // Timed region of the main loop (bench): opens once k >= warmup.
+  void maybe_start_timer(const Inner& D) {
+    if (timing_started_ || &D != &main_ || D.k() < timing_warmup_) return;
+    timing_started_ = true;
+    timed_k0_ = D.k();
+    timed_att0_ = D.hs.attempts;
+    timed_begin_.record(s());
+  }
+
+  pdlpk_red red() const {
+    pdlpk_red r{};
+    r.order = parity_ ? PDLPK_RED_SEQ : PDLPK_RED_TREE;
+    r.shards = shards_;
+    r.parity = parity_ ? 1 : 0;
+    r.scratch = red_scratch_.get();
+    return r;
+  }
+
+  double* slot(int i) { return slots_.get() + i; }
+  // Copies slots [0, count) to the host (one sync).
+  const double* read_slots(int count) {
+    PDLP_CK(cudaMemcpyAsync(host_slots_, slots_.get(), count * sizeof(double),
+                            cudaMemcpyDeviceToHost, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));
+    return host_slots_;
+  }
+
+  // apply_rescaling (rescaling.hpp:137-143) on device, both layouts in place.
+  void precondition(int ruiz_passes, bool pock_chambolle) {
+    const auto t0 = Clock::now();
+    const int64_t m = prob_.m, n = prob_.n;
+    DevBuf<double> fr(m), fc(n);
+    auto pass = [&](int one_norm) {
+      PDLP_LAUNCH(pdlpk_line_factors(&prob_.row.view, one_norm, fr.get(), s()));
+      PDLP_LAUNCH(pdlpk_line_factors(&prob_.col.view, one_norm, fc.get(), s()));
+      PDLP_LAUNCH(pdlpk_apply_factors(&prob_.row.view, prob_.row.value.get(), fr.get(), fc.get(), s()));
+      PDLP_LAUNCH(pdlpk_apply_factors(&prob_.col.view, prob_.col.value.get(), fc.get(), fr.get(), s()));
+      PDLP_LAUNCH(pdlpk_apply_vec_factors(prob_.lc.get(), prob_.uc.get(), prob_.row_scale.get(),
+                                          fr.get(), m, prob_.c.get(), prob_.lv.get(),
+                                          prob_.uv.get(), prob_.col_scale.get(), fc.get(), n, s()));
+    };
+    for (int p = 0; p < ruiz_passes; ++p) pass(0);
+    if (pock_chambolle) pass(1);
+    PDLP_CK(cudaStreamSynchronize(s()));
+    precondition_seconds_ = std::chrono::duration<double>(Clock::now() - t0).count();
+  }
+
+  // initial_step_size (step.hpp:14-18)
+  double initial_step_size() {
+    const pdlpk_red r = red();
+    PDLP_LAUNCH(pdlpk_abs_max(prob_.row.value.get(), prob_.row.view.nnz, &r, slot(0), s()));
+    const double mx = read_slots(1)[0];
+    return mx > 0.0 ? 1.0 / mx : 1.0;
+  }
+
+  // initialize_primal_weight (restarts.hpp:278-294)
+  double initialize_primal_weight() {
+    const pdlpk_red r = red();
+    PDLP_LAUNCH(pdlpk_primal_weight_sums(prob_.c.get(), prob_.n, prob_.lc.get(), prob_.uc.get(),
+                                         prob_.m, &r, slot(0), s()));
+    const double* h = read_slots(2);
+    const double nc = std::sqrt(h[0]);
+    const double nb = std::sqrt(h[1]);
+    if (nc > 1e-12 && nb > 1e-12) return nc / nb;
+    return 1.0;
+  }
+
+  // Host-libm schedule factors for next_step_size (step.hpp:136-141).
+  void ensure_table(int64_t len) {
+    if (len <= table_len_) return;
+    int64_t want = std::max<int64_t>(len, 4096);
+    want = std::max(want, 2 * table_len_);
+    std::vector<double> down(want), up(want);
+    for (int64_t k = 0; k < want; ++k) {
+      const double kk = static_cast<double>(k < 1 ? 1 : k) + 1.0;
+      down[k] = 1.0 - std::pow(kk, -0.3);
+      up[k] = 1.0 + std::pow(kk, -0.6);
+    }
+    f_down_.alloc(want);
+    f_up_.alloc(want);
+    PDLP_CK(cudaMemcpy(f_down_.get(), down.data(), want * 8, cudaMemcpyHostToDevice));
+    PDLP_CK(cudaMemcpy(f_up_.get(), up.data(), want * 8, cudaMemcpyHostToDevice));
+    table_len_ = want;
+  }
+
+  pdlpk_step_args step_args(const pdlpk_problem& P, Inner& D) {
+    pdlpk_step_args a{};
+    a.P = P;
+    for (int b = 0; b < 2; ++b) {
+      a.x[b] = D.x[b].get();
+      a.y[b] = D.y[b].get();
+      a.aty[b] = D.aty[b].get();
+    }
+    a.xbar = D.xbar.get();
+    a.dy = D.dy.get();
+    a.aty_diff = D.aty_diff.get();
+    a.sum_x = D.sum_x.get();
+    a.sum_y = D.sum_y.get();
+    a.state = D.state.get();
+    a.f_down = f_down_.get();
+    a.f_up = f_up_.get();
+    a.table_len = table_len_;
+    a.part2 = D.part2.get();
+    a.part3 = D.part3.get();
+    a.mode = parity_ ? PDLP_MODE_PARITY : PDLP_MODE_PERF;
+    a.shards = shards_;
+    a.shard_part = D.shard_part.get();
+    return a;
+  }
+
+  void read_state(Inner& D) {
+    PDLP_CK(cudaMemcpyAsync(&D.hs, D.state.get(), sizeof(pdlpk_step_state),
+                            cudaMemcpyDeviceToHost, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));
+  }
+  void write_state(Inner& D) {
+    PDLP_CK(cudaStreamSynchronize(s()));
+    PDLP_CK(cudaMemcpy(D.state.get(), &D.hs, sizeof(pdlpk_step_state), cudaMemcpyHostToDevice));
+  }
+
+  // InnerState::prepare (solver.hpp:167-192); x0 is a device vector.
+  void prepare(Inner& D, const pdlpk_problem& P, const double* x0, double eta0, double omega0,
+               bool fixed) {
+    const int64_t partials = pdlpk_step_partials(&P);
+    if (D.n != P.n || D.m != P.m || static_cast<int64_t>(D.part2.size()) < partials) {
+      D.allocate(P.n, P.m, partials, shards_);
+    }
+    dev_copy(D.x[0].get(), x0, P.n, s());
+    dev_zero(D.y[0].get(), P.m, s());
+    dev_zero(D.aty[0].get(), P.n, s());
+    dev_zero(D.sum_x.get(), P.n, s());
+    dev_zero(D.sum_y.get(), P.m, s());
+    dev_copy(D.ref_x.get(), x0, P.n, s());
+    dev_zero(D.ref_y.get(), P.m, s());
+    std::memset(&D.hs, 0, sizeof(D.hs));
+    D.hs.eta = eta0;
+    D.hs.omega = omega0;
+    D.hs.min_eta_bar = kInf;
+    D.hs.max_retries = 60;
+    D.hs.halt = 1;
+    D.hs.fixed = fixed ? 1 : 0;
+    D.omega = omega0;
+    D.last_eta = eta0;
+    D.mu_last = kInf;
+    D.prev_candidate_mu = kInf;
+    D.k_last_restart = 0;
+    D.restarts = 0;
+    D.next_polish_trigger = 100;
+    D.polish_iterations = 0;
+    D.have_sol = false;
+    D.detail.clear();
+    D.cert.have = false;
+    write_state(D);
+  }
+
+  // Runs step attempts until k reaches target or the controller halts.
+  void run_steps(const pdlpk_problem& P, Inner& D, int64_t target) {
+    ensure_table(target + 1);
+    pdlpk_step_args a = step_args(P, D);
+    PDLP_LAUNCH(pdlpk_arm(D.state.get(), target, s()));
+    step_begin_.record(s());
+    int64_t known_k = D.hs.k;
+    while (true) {
+      const int64_t need = target - known_k;
+      if (need <= 0) break;
+      if (profile_) {
+        const int64_t attempts0 = D.hs.attempts;
+        ensure_prof_events(need);
+        for (int64_t t = 0; t < need; ++t) {
+          PDLP_LAUNCH(pdlpk_attempt_timed(&a, prof_ev_.data() + 4 * t, s()));
+        }
+        read_state(D);
+        const int64_t ran = std::min(need, D.hs.attempts - attempts0);
+        for (int64_t t = 0; t < ran; ++t) {
+          for (int q = 0; q < 3; ++q) {
+            float ms = 0.0f;
+            PDLP_CK(cudaEventElapsedTime(&ms, prof_ev_[4 * t + q], prof_ev_[4 * t + q + 1]));
+            kernel_seconds_[q] += 1e-3 * ms;
+            kernel_launches_[q] += 1;
+          }
+        }
+      } else {
+        for (int64_t t = 0; t < need; ++t) PDLP_LAUNCH(pdlpk_attempt(&a, s()));
+        read_state(D);
+      }
+      if (D.hs.status != 0 || D.hs.k >= target) break;
+      known_k = D.hs.k;
+    }
+    step_end_.record(s());
+    step_seconds_ += elapsed_seconds(step_begin_, step_end_);
+    read_state(D);
+  }
+
+  void flush_average(const pdlpk_problem& P, Inner& D) {
+    pdlpk_step_args a = step_args(P, D);
+    PDLP_LAUNCH(pdlpk_flush_average(&a, s()));
+    D.hs.avg_pending = 0;
+  }
+
+  // --- residual screens ----------------------------------------------------
+  Summary screen(const pdlpk_problem& P, int orig, const double* x, const double* y,
+                 const double* ax, const double* aty, int rc_mode, double* r_out) {
+    const pdlpk_red r = red();
+    PDLP_LAUNCH(pdlpk_screen(&P, orig, x, y, ax, aty, rc_mode, &r, r_out, slot(0), s()));
+    const double* h = read_slots(4);
+    return finish_summary(h[0], h[1], h[2], -h[3]);
+  }
+
+  // recover_reduced_costs + kkt_residuals on the original data
+  // (residuals.hpp:49-64, 135-158): genuine original-space products.
+  Summary original_kkt(const pdlpk_problem& P, const double* x, const double* y, int rc_mode,
+                       double* r_out, Inner& D) {
+    PDLP_LAUNCH(pdlpk_spmv(&P.K, 1, x, D.prod_m.get(), parity_, s()));
+    PDLP_LAUNCH(pdlpk_spmv(&P.KT, 1, y, D.prod_n.get(), parity_, s()));
+    return screen(P, 1, x, y, D.prod_m.get(), D.prod_n.get(), rc_mode, r_out);
+  }
+
+  // screen_and_verify (solver.hpp:207-232)
+  bool screen_and_verify(const pdlpk_problem& P, const InnerCfg& cfg, const double* xs,
+                         const double* ys, const double* ax_s, const double* aty_s, double* rc,
+                         Summary& screened, Inner& D, const char* which) {
+    screened = screen(P, 0, xs, ys, ax_s, aty_s, cfg.rc_mode, rc);
+    const bool pass = cfg.feasibility_only ? screened.primal <= cfg.tol.eps_primal
+                                           : check_termination(screened, cfg.tol);
+    if (!pass) return false;
+    PDLP_LAUNCH(pdlpk_scale_mul(P.col_scale, xs, D.tmp_x.get(), P.n, s()));
+    PDLP_LAUNCH(pdlpk_scale_mul(P.row_scale, ys, D.tmp_y.get(), P.m, s()));
+    const Summary truth = original_kkt(P, D.tmp_x.get(), D.tmp_y.get(), cfg.rc_mode, D.tmp_r.get(), D);
+    const bool verified = cfg.feasibility_only ? truth.primal <= cfg.tol.eps_primal
+                                               : check_termination(truth, cfg.tol);
+    if (!verified) return false;
+    D.sol_x.swap(D.tmp_x);
+    D.sol_y.swap(D.tmp_y);
+    D.sol_r.swap(D.tmp_r);
+    D.sol_summary = truth;
+    D.have_sol = true;
+    D.detail = std::string("converged at the ") + which;
+    return true;
+  }
+
+  // capture_current (solver.hpp:236-242)
+  void capture_current(const pdlpk_problem& P, const InnerCfg& cfg, Inner& D) {
+    const int c = D.cur();
+    PDLP_LAUNCH(pdlpk_scale_mul(P.col_scale, D.x[c].get(), D.sol_x.get(), P.n, s()));
+    PDLP_LAUNCH(pdlpk_scale_mul(P.row_scale, D.y[c].get(), D.sol_y.get(), P.m, s()));
+    D.sol_summary = original_kkt(P, D.sol_x.get(), D.sol_y.get(), cfg.rc_mode, D.sol_r.get(), D);
+    D.have_sol = true;
+  }
+
+  // --- infeasibility rays (residuals.hpp:222-316) ---------------------------
+  // Primal test on dual candidate yc; on success the ray and its completion
+  // are left in ray_m / ray_n.
+  bool try_primal(const pdlpk_problem& P, int orig, const double* yc, double eps_ray, Inner& D,
+                  double& residual, double& objective) {
+    const pdlpk_red r = red();
+    PDLP_LAUNCH(pdlpk_ray_primal_prep(&P, orig, yc, D.ray_m.get(), &r, slot(0), s()));
+    const double norm = read_slots(1)[0];
+    if (!(norm > 0.0)) return false;
+    PDLP_LAUNCH(pdlpk_spmv(&P.KT, orig, D.ray_m.get(), D.prod_n.get(), parity_, s()));
+    PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, orig, D.ray_m.get(), D.prod_n.get(), D.ray_n.get(), &r,
+                                        slot(0), s()));
+    const double* h = read_slots(2);
+    residual = h[0];
+    if (residual > eps_ray * norm) return false;
+    objective = -h[1];
+    if (!(objective > 0.0) || !std::isfinite(objective)) return false;
+    return true;
+  }
+
+  bool try_dual(const pdlpk_problem& P, int orig, const double* xc, double eps_ray, Inner& D,
+                double& residual, double& objective) {
+    const pdlpk_red r = red();
+    PDLP_LAUNCH(pdlpk_ray_dual_prep(&P, orig, xc, &r, slot(0), s()));
+    const double* h = read_slots(3);
+    const double norm = h[0], box = h[1], obj = h[2];
+    if (!(norm > 0.0)) return false;
+    // Both conditions below must hold for a certificate; testing the cheap
+    // ones first skips the product without changing the verdict.
+    if (box > eps_ray * norm || !(obj < 0.0)) return false;
+    PDLP_LAUNCH(pdlpk_spmv(&P.K, orig, xc, D.prod_m.get(), parity_, s()));
+    PDLP_LAUNCH(pdlpk_ray_dual_finish(&P, orig, D.prod_m.get(), &r, slot(0), s()));
+    const double row = read_slots(1)[0];
+    residual = (box < row) ? row : box;
+    if (residual > eps_ray * norm) return false;
+    objective = obj;
+    return true;
+  }
+
+  // detect_rays (solver.hpp:246-280)
+  std::optional<int> detect_rays(const pdlpk_problem& P, const InnerCfg& cfg, Inner& D,
+                                 bool have_avg) {
+    struct Cand {
+      const double* x;
+      const double* y;
+      const char* source;
+    };
+    std::vector<Cand> cands;
+    const int c = D.cur();
+    if (D.k() > 0) {
+      PDLP_LAUNCH(pdlpk_sub(D.x[c].get(), D.x[c ^ 1].get(), D.diff_x.get(), P.n, s()));
+      PDLP_LAUNCH(pdlpk_sub(D.y[c].get(), D.y[c ^ 1].get(), D.diff_y.get(), P.m, s()));
+      cands.push_back({D.diff_x.get(), D.diff_y.get(), "difference"});
+    }
+    cands.push_back({D.x[c].get(), D.y[c].get(), "current"});
+    if (have_avg) cands.push_back({D.avg_x.get(), D.avg_y.get(), "average"});
+    int kind = -1;
+    const char* source = "";
+    for (const Cand& cd : cands) {
+      double res = 0.0, obj = 0.0;
+      if (try_primal(P, 0, cd.y, cfg.eps_ray, D, res, obj)) {
+        kind = PDLP_CERT_PRIMAL_INFEASIBLE;
+        source = cd.source;
+        break;
+      }
+      if (try_dual(P, 0, cd.x, cfg.eps_ray, D, res, obj)) {
+        kind = PDLP_CERT_DUAL_INFEASIBLE;
+        source = cd.source;
+        // keep the scaled primal ray for the verification below
+        dev_copy(D.ray_n.get(), cd.x, P.n, s());
+        break;
+      }
+    }
+    if (kind < 0) return std::nullopt;
+    double res = 0.0, obj = 0.0;
+    if (kind == PDLP_CERT_PRIMAL_INFEASIBLE) {
+      PDLP_LAUNCH(pdlpk_scale_mul(P.row_scale, D.ray_m.get(), D.tmp_y.get(), P.m, s()));
+      if (try_primal(P, 1, D.tmp_y.get(), cfg.eps_ray, D, res, obj)) {
+        D.cert.have = true;
+        D.cert.kind = kind;
+        dev_copy(D.cert.ray_y.get(), D.ray_m.get(), P.m, s());
+        dev_copy(D.cert.ray_r.get(), D.ray_n.get(), P.n, s());
+        D.cert.residual = res;
+        D.cert.objective = obj;
+        D.cert.source = source;
+        D.detail = std::string("primal infeasibility certified by the ") + source + " ray";
+        return kPrimalInf;
+      }
+    } else {
+      PDLP_LAUNCH(pdlpk_scale_mul(P.col_scale, D.ray_n.get(), D.tmp_x.get(), P.n, s()));
+      if (try_dual(P, 1, D.tmp_x.get(), cfg.eps_ray, D, res, obj)) {
+        D.cert.have = true;
+        D.cert.kind = kind;
+        dev_copy(D.cert.ray_x.get(), D.tmp_x.get(), P.n, s());
+        D.cert.residual = res;
+        D.cert.objective = obj;
+        D.cert.source = source;
+        D.detail = std::string("dual infeasibility certified by the ") + source + " ray";
+        return kDualInf;
+      }
+    }
+    return std::nullopt;
+  }
+
+  // restart_progress_metric (restarts.hpp:223-231)
+  double restart_metric(const pdlpk_problem& P, const double* x, const double* y, const double* ax,
+                        const double* aty, Inner& D, double omega) {
+    const pdlpk_red r = red();
+    PDLP_LAUNCH(pdlpk_diff_norm_sq(x, D.ref_x.get(), P.n, &r, slot(0), s()));
+    PDLP_LAUNCH(pdlpk_diff_norm_sq(y, D.ref_y.get(), P.m, &r, slot(1), s()));
+    PDLP_LAUNCH(pdlpk_radius(slot(0), slot(1), omega, slot(2), s()));
+    PDLP_LAUNCH(pdlpk_gap(&P, x, y, ax, aty, omega, slot(2), 0.0, &r, gap_work_.get(), slot(3), s()));
+    return read_slots(4)[3];
+  }
+
+  // ---- the loop ----------------------------------------------------------
+  int run_inner(const pdlpk_problem& P, const pdlpk_problem& parent_for_polish,
+                const InnerCfg& cfg, Inner& D);
+
+  bool attempt_polish(const pdlpk_problem& P, const InnerCfg& cfg, Inner& D);
+
+  pdlpk_problem primal_feas_view(const pdlpk_problem& P) {
+    pdlpk_problem Q = P;
+    Q.c = zeros_n_.get();
+    Q.c_o = zeros_n_.get();
+    return Q;
+  }
+
+  pdlpk_problem dual_feas_view(const pdlpk_problem& P) {
+    // build_dual_feasibility (problem.hpp:181-238) + swapped RescalingInfo
+    // (solver.hpp:323-325): layouts swap roles, no matrix copy.
+    if (sub_lc_.size() != static_cast<size_t>(P.n)) {
+      sub_lc_.alloc(P.n);
+      sub_uc_.alloc(P.n);
+      sub_lv_.alloc(P.m);
+      sub_uv_.alloc(P.m);
+      sub_lc_o_.alloc(P.n);
+      sub_uc_o_.alloc(P.n);
+      sub_lv_o_.alloc(P.m);
+      sub_uv_o_.alloc(P.m);
+    }
+    PDLP_LAUNCH(pdlpk_dual_feas_bounds(P.c, P.lv, P.uv, P.n, P.lc, P.uc, P.m, sub_lc_.get(),
+                                       sub_uc_.get(), sub_lv_.get(), sub_uv_.get(), s()));
+    PDLP_LAUNCH(pdlpk_dual_feas_bounds(P.c_o, P.lv_o, P.uv_o, P.n, P.lc_o, P.uc_o, P.m,
+                                       sub_lc_o_.get(), sub_uc_o_.get(), sub_lv_o_.get(),
+                                       sub_uv_o_.get(), s()));
+    pdlpk_problem Q{};
+    Q.m = P.n;
+    Q.n = P.m;
+    Q.K = P.KT;
+    Q.KT = P.K;
+    Q.c = zeros_m_.get();
+    Q.c_o = zeros_m_.get();
+    Q.lc = sub_lc_.get();
+    Q.uc = sub_uc_.get();
+    Q.lv = sub_lv_.get();
+    Q.uv = sub_uv_.get();
+    Q.lc_o = sub_lc_o_.get();
+    Q.uc_o = sub_uc_o_.get();
+    Q.lv_o = sub_lv_o_.get();
+    Q.uv_o = sub_uv_o_.get();
+    Q.row_scale = P.col_scale;
+    Q.col_scale = P.row_scale;
+    return Q;
+  }
+
+  // public solve state
+  pdlp_options opt_;
+  bool parity_ = false;
+  int shards_ = 4;
+  std::unique_ptr<Stream> stream_;
+  DevProblem prob_;
+  DevBuf<double> slots_;
+  double* host_slots_ = nullptr;
+  DevBuf<double> red_scratch_;
+  DevBuf<char> gap_work_;
+  DevBuf<double> zeros_n_, zeros_m_;
+  DevBuf<double> sub_lc_, sub_uc_, sub_lv_, sub_uv_, sub_lc_o_, sub_uc_o_, sub_lv_o_, sub_uv_o_;
+  DevBuf<double> f_down_, f_up_;
+  int64_t table_len_ = 0;
+  Event step_begin_, step_end_;
+  double step_seconds_ = 0.0;
+  double upload_seconds_ = 0.0;
+  double precondition_seconds_ = 0.0;
+  int64_t attempts_total_ = 0;
+  bool profile_ = false;
+  std::vector<cudaEvent_t> prof_ev_;
+  double kernel_seconds_[4] = {0, 0, 0, 0};
+  int64_t kernel_launches_[4] = {0, 0, 0, 0};
+  int64_t timing_warmup_ = 0;
+  bool timing_started_ = false;
+  int64_t timed_k0_ = 0, timed_att0_ = 0;
+  Event timed_begin_, timed_end_;
+  Inner main_, polish_primal_, polish_dual_;
+};
+
+bool Engine::attempt_polish(const pdlpk_problem& P, const InnerCfg& cfg, Inner& D) {
+  // solver.hpp:290-348
+  const int64_t remaining = cfg.budget - D.k() - D.polish_iterations;
+  const int64_t budget = std::min(D.k() / 8, remaining);
+  if (budget <= 0) return false;
+  InnerCfg sub = cfg;
+  sub.feasibility_only = true;
+  sub.rc_mode = 0;
+  sub.budget = budget;
+  sub.detect_infeasibility = false;
+  sub.enable_polish = false;
+  sub.observer = nullptr;
+
+  const pdlpk_problem P2 = primal_feas_view(P);
+  Inner& D2 = polish_primal_;
+  prepare(D2, P2, D.avg_x.get(), D.hs.eta, D.omega, cfg.fixed_eta.has_value());
+  sub.tag = "polish_primal";
+  const int s2 = run_inner(P2, P2, sub, D2);
+  D.polish_iterations += D2.k();
+  attempts_total_ += D2.hs.attempts;
+  if (s2 != kOptimal) return false;
+
+  const pdlpk_problem P3 = dual_feas_view(P);
+  Inner& D3 = polish_dual_;
+  prepare(D3, P3, D.avg_y.get(), D.hs.eta, D.omega, cfg.fixed_eta.has_value());
+  sub.budget = std::min(D.k() / 8, remaining - D2.k());
+  if (sub.budget <= 0) return false;
+  sub.tol.eps_primal = cfg.tol.eps_dual;
+  sub.tag = "polish_dual";
+  const int s3 = run_inner(P3, P3, sub, D3);
+  D.polish_iterations += D3.k();
+  attempts_total_ += D3.hs.attempts;
+  if (s3 != kOptimal) return false;
+
+  // Stitch (x from the primal polish, y from the dual polish) and re-check.
+  const Summary truth = original_kkt(P, D2.sol_x.get(), D3.sol_x.get(), 0, D.tmp_r.get(), D);
+  if (!check_termination(truth, cfg.tol)) return false;
+  dev_copy(D.sol_x.get(), D2.sol_x.get(), P.n, s());
+  dev_copy(D.sol_y.get(), D3.sol_x.get(), P.m, s());
+  D.sol_r.swap(D.tmp_r);
+  D.sol_summary = truth;
+  D.have_sol = true;
+  D.detail = "converged at the polished point";
+  return true;
+}
+
+int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerCfg& cfg,
+                      Inner& D) {
+  Summary screen_cur;
+  while (true) {
+    const bool budget_hit = D.k() >= cfg.budget;
+    const bool at_cadence = budget_hit || (D.k() % cfg.check_interval == 0);
+    if (at_cadence) {
+      const bool timed_out = Clock::now() >= cfg.deadline;
+      const int c = D.cur();
+      flush_average(P, D);
+      PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.x[c].get(), D.ax_cur.get(), parity_, s()));
+      PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.y[c].get(), D.aty[c].get(), parity_, s()));
+      const bool have_avg = D.hs.avg_count > 0;
+      if (have_avg) {
+        PDLP_LAUNCH(pdlpk_average_into(D.state.get(), D.sum_x.get(), D.sum_y.get(), D.avg_x.get(),
+                                       D.avg_y.get(), P.n, P.m, s()));
+        PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.avg_x.get(), D.ax_avg.get(), parity_, s()));
+        PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.avg_y.get(), D.aty_avg.get(), parity_, s()));
+      }
+      if (screen_and_verify(P, cfg, D.x[c].get(), D.y[c].get(), D.ax_cur.get(), D.aty[c].get(),
+                            D.rc_a.get(), screen_cur, D, "current iterate")) {
+        return kOptimal;
+      }
+      Summary screen_avg;
+      if (have_avg && screen_and_verify(P, cfg, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
+                                        D.aty_avg.get(), D.rc_b.get(), screen_avg, D,
+                                        "window average")) {
+        return kOptimal;
+      }
+      if (cfg.detect_infeasibility) {
+        auto st = detect_rays(P, cfg, D, have_avg);
+        if (st.has_value()) {
+          const std::string keep = D.detail;
+          capture_current(P, cfg, D);
+          D.detail = keep;
+          return *st;
+        }
+      }
+      if (cfg.enable_polish && have_avg && D.k() >= D.next_polish_trigger && !timed_out &&
+          !budget_hit) {
+        if (screen_avg.rel_gap <= cfg.tol.eps_rel_gap) {
+          if (attempt_polish(P, cfg, D)) return kOptimal;
+          while (D.next_polish_trigger <= D.k()) D.next_polish_trigger *= 2;
+        }
+      }
+      if (cfg.enable_restarts && D.k() > D.k_last_restart) {
+        const double mu_cur = restart_metric(P, D.x[c].get(), D.y[c].get(), D.ax_cur.get(),
+                                             D.aty[c].get(), D, D.omega);
+        const double mu_avg = have_avg ? restart_metric(P, D.avg_x.get(), D.avg_y.get(),
+                                                        D.ax_avg.get(), D.aty_avg.get(), D, D.omega)
+                                       : kInf;
+        const bool use_current = mu_cur < mu_avg;
+        const double cand_mu = use_current ? mu_cur : mu_avg;
+        const int reason = should_restart(cand_mu, D.mu_last, D.prev_candidate_mu,
+                                          D.k() - D.k_last_restart, D.k(), cfg.th);
+        if (reason != kNone) {
+          const double* cx = use_current ? D.x[c].get() : D.avg_x.get();
+          const double* cy = use_current ? D.y[c].get() : D.avg_y.get();
+          const double* cax = use_current ? D.ax_cur.get() : D.ax_avg.get();
+          const double* caty = use_current ? D.aty[c].get() : D.aty_avg.get();
+          if (cfg.allow_omega_updates) {
+            const pdlpk_red r = red();
+            PDLP_LAUNCH(pdlpk_diff_norm_sq(cx, D.ref_x.get(), P.n, &r, slot(0), s()));
+            PDLP_LAUNCH(pdlpk_diff_norm_sq(cy, D.ref_y.get(), P.m, &r, slot(1), s()));
+            const double* h = read_slots(2);
+            const double dx = std::sqrt(h[0]);
+            const double dy = std::sqrt(h[1]);
+            D.omega = update_primal_weight(dx, dy, D.omega);
+          }
+          D.mu_last = restart_metric(P, cx, cy, cax, caty, D, D.omega);
+          if (!use_current) {
+            dev_copy(D.x[c].get(), D.avg_x.get(), P.n, s());
+            dev_copy(D.y[c].get(), D.avg_y.get(), P.m, s());
+            dev_copy(D.aty[c].get(), D.aty_avg.get(), P.n, s());
+          }
+          dev_copy(D.ref_x.get(), D.x[c].get(), P.n, s());
+          dev_copy(D.ref_y.get(), D.y[c].get(), P.m, s());
+          dev_zero(D.sum_x.get(), P.n, s());
+          dev_zero(D.sum_y.get(), P.m, s());
+          read_state(D);
+          D.hs.avg_weight = 0.0;
+          D.hs.avg_count = 0;
+          D.hs.avg_pending = 0;
+          D.hs.omega = D.omega;
+          write_state(D);
+          D.prev_candidate_mu = kInf;
+          D.k_last_restart = D.k();
+          ++D.restarts;
+          if (cfg.logging) {
+            std::fprintf(stderr, "phase=%s event=restart iter=%lld reason=%s omega=%.6e mu=%.6e\n",
+                         cfg.tag, static_cast<long long>(D.k()), reason_name(reason), D.omega,
+                         D.mu_last);
+          }
+        } else {
+          D.prev_candidate_mu = cand_mu;
+        }
+      }
+      if (cfg.logging) {
+        std::fprintf(stderr,
+                     "phase=%s iter=%lld primal_res=%.6e dual_res=%.6e rel_gap=%.6e mu=%.6e "
+                     "omega=%.6e eta=%.6e restarts=%lld\n",
+                     cfg.tag, static_cast<long long>(D.k()), screen_cur.primal, screen_cur.dual,
+                     screen_cur.rel_gap, D.mu_last, D.omega, D.last_eta,
+                     static_cast<long long>(D.restarts));
+      }
+      if (timed_out) {
+        capture_current(P, cfg, D);
+        D.detail = "time limit reached";
+        return kTimeLimit;
+      }
+      if (budget_hit) {
+        capture_current(P, cfg, D);
+        D.detail = "iteration limit reached";
+        return kIterLimit;
+      }
+    }
+
+    maybe_start_timer(D);
+    // Accepted steps up to the next cadence point (or one, with an observer).
+    int64_t target = (D.k() / cfg.check_interval + 1) * cfg.check_interval;
+    target = std::min(target, cfg.budget);
+    if (cfg.observer != nullptr) target = D.k() + 1;
+    if (cfg.fixed_eta.has_value() && D.hs.eta != *cfg.fixed_eta) {
+      D.hs.eta = *cfg.fixed_eta;
+      write_state(D);
+    }
+    run_steps(P, D, target);
+    D.last_eta = D.hs.eta_used;
+    if (D.hs.status != 0) {
+      if (!cfg.fixed_eta.has_value()) {
+        // One recovery screen of the last good point and the window average
+        // (solver.hpp:494-516).
+        const int c = D.cur();
+        PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.x[c].get(), D.ax_cur.get(), parity_, s()));
+        Summary tmp;
+        if (screen_and_verify(P, cfg, D.x[c].get(), D.y[c].get(), D.ax_cur.get(), D.aty[c].get(),
+                              D.rc_a.get(), tmp, D, "current iterate after a numerical error")) {
+          return kOptimal;
+        }
+        if (D.hs.avg_count > 0) {
+          flush_average(P, D);
+          PDLP_LAUNCH(pdlpk_average_into(D.state.get(), D.sum_x.get(), D.sum_y.get(),
+                                         D.avg_x.get(), D.avg_y.get(), P.n, P.m, s()));
+          PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.avg_x.get(), D.ax_avg.get(), parity_, s()));
+          PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.avg_y.get(), D.aty_avg.get(), parity_, s()));
+          if (screen_and_verify(P, cfg, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
+                                D.aty_avg.get(), D.rc_b.get(), tmp, D,
+                                "window average after a numerical error")) {
+            return kOptimal;
+          }
+        }
+        capture_current(P, cfg, D);
+        D.detail = "adaptive step failed to find a usable step size";
+        return kNumErr;
+      }
+      capture_current(P, cfg, D);
+      D.detail = "fixed-size step produced non-finite values";
+      return kNumErr;
+    }
+    if (cfg.observer != nullptr) {
+      const int c = D.cur();
+      std::vector<double> hx(P.n), hy(P.m);
+      if (P.n > 0) PDLP_CK(cudaMemcpyAsync(hx.data(), D.x[c].get(), P.n * 8, cudaMemcpyDeviceToHost, s()));
+      if (P.m > 0) PDLP_CK(cudaMemcpyAsync(hy.data(), D.y[c].get(), P.m * 8, cudaMemcpyDeviceToHost, s()));
+      PDLP_CK(cudaStreamSynchronize(s()));
+      pdlp_iteration_record rec{};
+      rec.iteration = D.k();
+      rec.x = hx.data();
+      rec.x_len = P.n;
+      rec.y = hy.data();
+      rec.y_len = P.m;
+      rec.eta = D.hs.eta_used;
+      rec.omega = D.omega;
+      cfg.observer(cfg.observer_user, &rec);
+    }
+  }
+}
+
+void copy_to_host(double* dst, const double* src, int64_t n, cudaStream_t s) {
+  if (dst != nullptr && n > 0) PDLP_CK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToHost, s));
+}
+
+// solve (solver.hpp:535-608)
+void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result* res) {
+  const auto t0 = Clock::now();
+  validate(problem);
+  Engine E(problem, *o);
+  if (o->enable_scaling) E.precondition(o->ruiz_passes, o->pock_chambolle != 0);
+  const pdlpk_problem P = E.problem().view();
+
+  InnerCfg cfg;
+  cfg.tol.eps_primal = o->eps_primal;
+  cfg.tol.eps_dual = o->eps_dual;
+  cfg.tol.eps_rel_gap = o->eps_rel_gap;
+  cfg.feasibility_only = false;
+  cfg.rc_mode = o->enable_polish ? 0 : 1;
+  cfg.budget = o->iteration_limit;
+  if (std::isfinite(o->time_limit_seconds)) {
+    cfg.deadline = t0 + std::chrono::duration_cast<Clock::duration>(
+                            std::chrono::duration<double>(o->time_limit_seconds));
+  }
+  cfg.enable_restarts = o->enable_restarts != 0;
+  cfg.detect_infeasibility = o->detect_infeasibility != 0;
+  cfg.enable_polish = o->enable_polish != 0;
+  cfg.eps_ray = o->eps_ray;
+  cfg.check_interval = o->check_interval > 0 ? o->check_interval : 64;
+  cfg.th.sufficient = o->restart_sufficient;
+  cfg.th.necessary = o->restart_necessary;
+  cfg.th.artificial = o->restart_artificial;
+  if (o->has_fixed_step_size) cfg.fixed_eta = o->fixed_step_size;
+  cfg.allow_omega_updates = o->has_fixed_primal_weight == 0;
+  cfg.observer = o->observer;
+  cfg.observer_user = o->observer_user;
+  cfg.logging = o->logging != 0;
+  cfg.tag = "main";
+
+  const double eta0 = o->has_fixed_step_size ? o->fixed_step_size : E.initial_step_size();
+  const double omega0 =
+      o->has_fixed_primal_weight ? o->fixed_primal_weight : E.initialize_primal_weight();
+  Inner& D = E.main_;
+  {
+    DevBuf<double> x0(P.n);
+    PDLP_LAUNCH(pdlpk_initial_point(P.lv, P.uv, x0.get(), P.n, E.s()));
+    E.prepare(D, P, x0.get(), eta0, omega0, cfg.fixed_eta.has_value());
+  }
+  E.ensure_table(std::min<int64_t>(o->iteration_limit, 1 << 20) + 2);
+
+  E.profile_ = o->profile_kernels != 0;
+  E.timing_warmup_ = std::max<int64_t>(0, o->timing_warmup_iterations);
+  const auto loop_t0 = Clock::now();
+  const int status = E.run_inner(P, P, cfg, D);
+  E.timed_end_.record(E.s());
+  PDLP_CK(cudaStreamSynchronize(E.s()));
+  const double loop_seconds = std::chrono::duration<double>(Clock::now() - loop_t0).count();
+  if (E.timing_started_) {
+    res->timed_seconds = elapsed_seconds(E.timed_begin_, E.timed_end_);
+    res->timed_iterations = D.k() - E.timed_k0_;
+    res->timed_attempts = D.hs.attempts - E.timed_att0_;
+  }
+  for (int q = 0; q < 4; ++q) {
+    res->kernel_seconds[q] = E.kernel_seconds_[q];
+    res->kernel_launches[q] = E.kernel_launches_[q];
+  }
+
+  res->status = status;
+  copy_to_host(res->x, D.sol_x.get(), P.n, E.s());
+  copy_to_host(res->y, D.sol_y.get(), P.m, E.s());
+  copy_to_host(res->reduced_costs, D.sol_r.get(), P.n, E.s());
+  res->summary.primal_residual_inf = D.sol_summary.primal;
+  res->summary.dual_residual_inf = D.sol_summary.dual;
+  res->summary.primal_objective = D.sol_summary.pobj;
+  res->summary.dual_objective = D.sol_summary.dobj;
+  res->summary.abs_gap = D.sol_summary.abs_gap;
+  res->summary.rel_gap = D.sol_summary.rel_gap;
+  res->has_certificate = D.cert.have ? 1 : 0;
+  if (D.cert.have) {
+    res->cert_kind = D.cert.kind;
+    if (D.cert.kind == PDLP_CERT_PRIMAL_INFEASIBLE) {
+      copy_to_host(res->cert_ray_y, D.cert.ray_y.get(), P.m, E.s());
+      copy_to_host(res->cert_ray_r, D.cert.ray_r.get(), P.n, E.s());
+    } else {
+      copy_to_host(res->cert_ray_x, D.cert.ray_x.get(), P.n, E.s());
+    }
+    res->cert_residual_inf = D.cert.residual;
+    res->cert_objective = D.cert.objective;
+    std::snprintf(res->cert_source, sizeof(res->cert_source), "%s", D.cert.source.c_str());
+  }
+  PDLP_CK(cudaStreamSynchronize(E.s()));
+  res->iterations = D.k();
+  res->polish_iterations = D.polish_iterations;
+  res->restarts = D.restarts;
+  res->step_retries = D.hs.retries;
+  res->final_step_size = D.hs.eta;
+  res->final_primal_weight = D.omega;
+  res->min_step_size_limit = D.hs.min_eta_bar;
+  res->attempts = D.hs.attempts + E.attempts_total_;
+  res->upload_seconds = E.upload_seconds_;
+  res->precondition_seconds = E.precondition_seconds_;
+  res->loop_seconds = loop_seconds;
+  res->step_seconds = E.step_seconds_;
+  res->solve_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+  std::snprintf(res->termination_detail, sizeof(res->termination_detail), "%s", D.detail.c_str());
+  if (o->logging) {
+    std::fprintf(stderr,
+                 "phase=main event=done status=%s iters=%lld polish_iters=%lld detail=\"%s\"\n",
+                 status_name(status), static_cast<long long>(res->iterations),
+                 static_cast<long long>(res->polish_iterations), res->termination_detail);
+  }
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PDLP_OK;
+  } catch (const InvalidProblem& e) {
+    g_last_error = e.what();
+    return PDLP_ERR_INVALID_PROBLEM;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return PDLP_ERR_CUDA;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = e.what();
+    return PDLP_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PDLP_ERR_INTERNAL;
+  }
+}
+
+}  // namespace pdlp_host
+
+// =========================================================== public C-ABI ===
+using namespace pdlp_host;
+
+extern "C" {
+
+void pdlp_default_options(pdlp_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->eps_primal = 1e-8;
+  o->eps_dual = 1e-8;
+  o->eps_rel_gap = 1e-2;
+  o->iteration_limit = 200000;
+  o->time_limit_seconds = kInf;
+  o->threads = 1;
+  o->shards_per_thread = 4;
+  o->enable_scaling = 1;
+  o->ruiz_passes = 10;
+  o->pock_chambolle = 1;
+  o->enable_polish = 1;
+  o->enable_restarts = 1;
+  o->detect_infeasibility = 1;
+  o->eps_ray = 1e-12;
+  o->check_interval = 64;
+  o->restart_sufficient = 0.1;
+  o->restart_necessary = 0.9;
+  o->restart_artificial = 0.5;
+  o->mode = PDLP_MODE_PERF;
+  o->device = 0;
+  o->use_graphs = 0;
+}
+
+int pdlp_solve(const pdlp_problem_view* problem, const pdlp_options* options,
+               pdlp_result* result) {
+  if (problem == nullptr || options == nullptr || result == nullptr) {
+    g_last_error = "null argument";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&] { solve(problem, options, result); });
+}
+
+const char* pdlp_last_error(void) { return g_last_error.c_str(); }
+
+int pdlp_abi_version(void) { return PDLP_ABI_VERSION; }
+
+int pdlp_device_count(void) {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    g_last_error = cudaGetErrorString(e);
+    return PDLP_ERR_CUDA;
+  }
+  return n;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------- component entry points ---
+namespace pdlp_host {
+
+struct Component {
+  pdlp_options o;
+  std::unique_ptr<Engine> E;
+  Component(const pdlp_problem_view* p, int mode, int shards) {
+    pdlp_default_options(&o);
+    o.mode = mode;
+    o.threads = 1;
+    o.shards_per_thread = shards > 0 ? shards : 4;
+    E = std::make_unique<Engine>(p, o);
+  }
+};
+
+DevBuf<double> to_dev(const double* h, int64_t n, cudaStream_t s) { return upload_vec(h, n, s); }
+
+void from_dev(double* h, const DevBuf<double>& d, int64_t n, cudaStream_t s) {
+  if (h != nullptr && n > 0) {
+    PDLP_CK(cudaMemcpyAsync(h, d.get(), n * 8, cudaMemcpyDeviceToHost, s));
+    PDLP_CK(cudaStreamSynchronize(s));
+  }
+}
+
+}  // namespace pdlp_host
+
+extern "C" {
+
+int pdlp_pdhg_step(const pdlp_problem_view* problem, const double* x, const double* y,
+                   double omega, double eta, int32_t mode, int32_t shards, double* x_out,
+                   double* y_out, int32_t* finite) {
+  return guarded([&] {
+    Component C(problem, mode, shards);
+    Engine& E = *C.E;
+    const pdlpk_problem P = E.problem().view();
+    Inner& D = E.main_;
+    DevBuf<double> x0 = to_dev(x, P.n, E.s());
+    E.prepare(D, P, x0.get(), eta, omega, true);
+    if (P.m > 0) PDLP_CK(cudaMemcpyAsync(D.y[0].get(), y, P.m * 8, cudaMemcpyHostToDevice, E.s()));
+    PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.y[0].get(), D.aty[0].get(), E.parity(), E.s()));
+    E.run_steps(P, D, 1);
+    // On a non-finite trial the controller keeps the old iterate; the trial
+    // itself sits in the other buffer.
+    const int c = D.hs.status == 0 ? D.cur() : (D.cur() ^ 1);
+    std::vector<double> hx(P.n), hy(P.m);
+    from_dev(hx.data(), D.x[c], P.n, E.s());
+    from_dev(hy.data(), D.y[c], P.m, E.s());
+    // pdhg_step (step.hpp:100-115) reports nullopt on any non-finite entry.
+    bool all_finite = true;
+    for (double v : hx) all_finite = all_finite && std::isfinite(v);
+    for (double v : hy) all_finite = all_finite && std::isfinite(v);
+    *finite = all_finite ? 1 : 0;
+    if (x_out != nullptr && P.n > 0) std::memcpy(x_out, hx.data(), P.n * 8);
+    if (y_out != nullptr && P.m > 0) std::memcpy(y_out, hy.data(), P.m * 8);
+  });
+}
+
+int pdlp_adaptive_step(const pdlp_problem_view* problem, double* x, double* y, double* aty,
+                       double* io_state, int32_t mode, int32_t shards, double* prev_x,
+                       double* prev_y, double* stats, int32_t* outcome) {
+  return guarded([&] {
+    Component C(problem, mode, shards);
+    Engine& E = *C.E;
+    const pdlpk_problem P = E.problem().view();
+    Inner& D = E.main_;
+    DevBuf<double> x0 = to_dev(x, P.n, E.s());
+    E.prepare(D, P, x0.get(), io_state[0], io_state[3], false);
+    if (P.m > 0) PDLP_CK(cudaMemcpyAsync(D.y[0].get(), y, P.m * 8, cudaMemcpyHostToDevice, E.s()));
+    if (P.n > 0) PDLP_CK(cudaMemcpyAsync(D.aty[0].get(), aty, P.n * 8, cudaMemcpyHostToDevice, E.s()));
+    D.hs.k = static_cast<int64_t>(io_state[1]);
+    D.hs.max_retries = static_cast<int32_t>(io_state[2]);
+    E.write_state(D);
+    E.run_steps(P, D, D.hs.k + 1);
+    *outcome = D.hs.status == 0 ? 0 : 1;
+    const int c = D.cur();
+    from_dev(x, D.x[c], P.n, E.s());
+    from_dev(y, D.y[c], P.m, E.s());
+    from_dev(aty, D.aty[c], P.n, E.s());
+    from_dev(prev_x, D.x[c ^ 1], P.n, E.s());
+    from_dev(prev_y, D.y[c ^ 1], P.m, E.s());
+    io_state[0] = D.hs.eta;
+    io_state[1] = static_cast<double>(D.hs.k);
+    stats[0] = static_cast<double>(D.hs.accepted);
+    stats[1] = static_cast<double>(D.hs.retries);
+    stats[2] = D.hs.min_eta_bar;
+    stats[3] = D.hs.eta_used;
+  });
+}
+
+int pdlp_spmv(const pdlp_problem_view* problem, const double* x, double* out, int32_t mode) {
+  return guarded([&] {
+    Component C(problem, mode, 4);
+    Engine& E = *C.E;
+    const pdlpk_problem P = E.problem().view();
+    DevBuf<double> dx = to_dev(x, P.n, E.s()), dout(P.m);
+    PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, dx.get(), dout.get(), E.parity(), E.s()));
+    from_dev(out, dout, P.m, E.s());
+  });
+}
+
+int pdlp_spmv_transpose(const pdlp_problem_view* problem, const double* y, double* out,
+                        int32_t mode) {
+  return guarded([&] {
+    Component C(problem, mode, 4);
+    Engine& E = *C.E;
+    const pdlpk_problem P = E.problem().view();
+    DevBuf<double> dy = to_dev(y, P.m, E.s()), dout(P.n);
+    PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, dy.get(), dout.get(), E.parity(), E.s()));
+    from_dev(out, dout, P.n, E.s());
+  });
+}
+
+int pdlp_apply_rescaling(const pdlp_problem_view* problem, int32_t ruiz_passes,
+                         int32_t pock_chambolle, double* row_values, double* col_values,
+                         double* objective, double* con_lower, double* con_upper,
+                         double* var_lower, double* var_upper, double* row_scale,
+                         double* col_scale) {
+  return guarded([&] {
+    Component C(problem, PDLP_MODE_PARITY, 4);
+    Engine& E = *C.E;
+    E.precondition(ruiz_passes, pock_chambolle != 0);
+    const DevProblem& Q = E.problem();
+    from_dev(row_values, Q.row.value, Q.row.view.nnz, E.s());
+    from_dev(col_values, Q.col.value, Q.col.view.nnz, E.s());
+    from_dev(objective, Q.c, Q.n, E.s());
+    from_dev(con_lower, Q.lc, Q.m, E.s());
+    from_dev(con_upper, Q.uc, Q.m, E.s());
+    from_dev(var_lower, Q.lv, Q.n, E.s());
+    from_dev(var_upper, Q.uv, Q.n, E.s());
+    from_dev(row_scale, Q.row_scale, Q.m, E.s());
+    from_dev(col_scale, Q.col_scale, Q.n, E.s());
+  });
+}
+
+int pdlp_normalized_duality_gap(const pdlp_problem_view* problem, const double* x,
+                                const double* y, const double* ax, const double* aty,
+                                double omega, double r, int32_t mode, double* gap) {
+  return guarded([&] {
+    Component C(problem, mode, 4);
+    Engine& E = *C.E;
+    const pdlpk_problem P = E.problem().view();
+    DevBuf<double> dx = to_dev(x, P.n, E.s()), dy = to_dev(y, P.m, E.s());
+    DevBuf<double> dax = to_dev(ax, P.m, E.s()), daty = to_dev(aty, P.n, E.s());
+    const pdlpk_red red = E.red();
+    PDLP_LAUNCH(pdlpk_gap(&P, dx.get(), dy.get(), dax.get(), daty.get(), omega, nullptr, r, &red,
+                          E.gap_work_.get(), E.slot(0), E.s()));
+    *gap = E.read_slots(1)[0];
+  });
+}
+
+int pdlp_kkt_residuals(const pdlp_problem_view* problem, const double* x, const double* y,
+                       int32_t rc_mode, int32_t mode, double* r_out,
+                       pdlp_residual_summary* summary) {
+  return guarded([&] {
+    Component C(problem, mode, 4);
+    Engine& E = *C.E;
+    const pdlpk_problem P = E.problem().view();
+    Inner& D = E.main_;
+    D.allocate(P.n, P.m, pdlpk_step_partials(&P), 4);
+    DevBuf<double> dx = to_dev(x, P.n, E.s()), dy = to_dev(y, P.m, E.s()), dr(P.n);
+    const Summary s = E.original_kkt(P, dx.get(), dy.get(), rc_mode, dr.get(), D);
+    from_dev(r_out, dr, P.n, E.s());
+    summary->primal_residual_inf = s.primal;
+    summary->dual_residual_inf = s.dual;
+    summary->primal_objective = s.pobj;
+    summary->dual_objective = s.dobj;
+    summary->abs_gap = s.abs_gap;
+    summary->rel_gap = s.rel_gap;
+  });
+}
+
+int pdlp_step_size_rules(double movement, double curvature, double eta_bar, double eta,
+                         int64_t k, double* limit_out, double* next_out) {
+  // Scalar rules (step.hpp:126-141), evaluated with the host table values the
+  // device decision kernel reads.
+  const double denom = 2.0 * std::abs(curvature);
+  *limit_out = (denom > 0.0) ? movement / denom : kInf;
+  const double kk = static_cast<double>(k < 1 ? 1 : k) + 1.0;
+  const double down = (1.0 - std::pow(kk, -0.3)) * eta_bar;
+  const double up = (1.0 + std::pow(kk, -0.6)) * eta;
+  *next_out = (up < down) ? up : down;
+  return PDLP_OK;
+}
+
+}  // extern "C"
