@@ -1,25 +1,27 @@
 // Exact normalized duality gap on device (reference
-// proj/include/pdhglp/restarts.hpp:107-220):
+// proj/include/pdhglp/restarts.hpp:107-220), in two launches around one host
+// read of the event count:
 //
-//   1. breakpoint events: <= 1 per primal coordinate (slot i), <= 2 per dual
-//      coordinate (slots n+2j, n+2j+1), so slot order == the reference's
-//      push order; plus the lam->inf masses b_inf, c_inf (SEQ in parity)
-//   2. stable radix sort of the events by lambda, descending (order-preserving
-//      uint64 transform; invalid slots get key 0 and sort last)
-//   3. sweep to the first group with phi(lam) = C + B/lam^2 >= r^2:
-//      parity — the reference's sequential loop on one thread;
-//      perf   — exclusive scans of the event masses + a parallel first-hit
-//   4. closed-form lambda*, candidate assembly (assemble_candidate :73-101)
-//      and the gap value (gap_value_at :50-71), SEQ in parity.
+//   prepare  1. lam -> inf masses b_inf, c_inf (SEQ order in parity mode)
+//            2. breakpoint events: <= 1 per primal coordinate (slot i), <= 2
+//               per dual coordinate (slots n+2j, n+2j+1) — slot order is the
+//               reference's push order — flagged and compacted with an
+//               order-preserving select, so only real events go further
+//   finish   3. stable radix sort of the E events by lambda, descending, on an
+//               order-preserving uint64 key (decoded back to lambda exactly)
+//            4. sweep to the first group with phi(lam) = C + B/lam^2 >= r^2:
+//               parity — the reference's sequential loop on one thread;
+//               perf   — exclusive scans of the event masses + parallel first hit
+//            5. closed-form lambda*, candidate assembly (assemble_candidate
+//               :73-101) and the gap value (gap_value_at :50-71), SEQ in parity.
 //
 // Parity caveat: std::sort is not stable, so events with EQUAL lambda may be
 // visited in a different order than the reference's introsort puts them,
 // which can change the last bit of the running masses.  Exact ties need
 // bitwise-equal breakpoints; DESIGN.md records this.
 //
-// CUB (part of the CUDA toolkit) provides the radix sort and scans; this is
-// cadence work (2-3 evaluations per 64 steps), not the per-step hot loop.
-//
+// CUB (part of the CUDA toolkit) provides select/sort/scan; this is cadence
+// work (2-3 evaluations per 64 steps), not the per-step hot loop.
 // Translation unit compiled with -fmad=false (see common.cuh).
 
 #include <cub/cub.cuh>
@@ -45,16 +47,20 @@ inline int ew_blocks(int64_t n) {
 
 struct GapScalars {
   double sums[2];  // b_inf, c_inf
-  double count;    // number of valid events
   double lambda_star;
   double value;
   unsigned long long first;  // first crossing group index (perf)
+  int num_events;            // compacted event count (select output)
+  int pad;
 };
 
 struct Work {
+  uint8_t* flag;  // per slot
+  double *lam, *dc, *di;  // per slot
+  int32_t *sel;            // compacted slot ids (slot order)
   uint64_t *keys_in, *keys_out;
-  int32_t *vals_in, *vals_out;
-  double *lam, *dc, *di, *cs, *bs;
+  int32_t* vals_out;
+  double *cs, *bs;  // sorted masses (perf scans)
   GapScalars* sc;
   void* cub_tmp;
   size_t cub_bytes;
@@ -63,14 +69,17 @@ struct Work {
 __host__ __device__ inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 size_t cub_bytes_for(int64_t N) {
-  size_t a = 0, b = 0;
+  size_t a = 0, b = 0, c = 0;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, a, static_cast<uint64_t*>(nullptr),
                                             static_cast<uint64_t*>(nullptr),
                                             static_cast<int32_t*>(nullptr),
                                             static_cast<int32_t*>(nullptr), static_cast<int>(N));
   cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<double*>(nullptr),
                                 static_cast<double*>(nullptr), static_cast<int>(N));
-  return a > b ? a : b;
+  cub::DeviceSelect::Flagged(nullptr, c, cub::CountingInputIterator<int32_t>(0),
+                             static_cast<uint8_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                             static_cast<int*>(nullptr), static_cast<int>(N));
+  return std::max(a, std::max(b, c));
 }
 
 Work carve(void* base, int64_t n, int64_t m) {
@@ -82,13 +91,14 @@ Work carve(void* base, int64_t n, int64_t m) {
     p += align_up(bytes);
     return r;
   };
-  w.keys_in = reinterpret_cast<uint64_t*>(take(8 * N));
-  w.keys_out = reinterpret_cast<uint64_t*>(take(8 * N));
-  w.vals_in = reinterpret_cast<int32_t*>(take(4 * N));
-  w.vals_out = reinterpret_cast<int32_t*>(take(4 * N));
+  w.flag = reinterpret_cast<uint8_t*>(take(N));
   w.lam = reinterpret_cast<double*>(take(8 * N));
   w.dc = reinterpret_cast<double*>(take(8 * N));
   w.di = reinterpret_cast<double*>(take(8 * N));
+  w.sel = reinterpret_cast<int32_t*>(take(4 * N));
+  w.keys_in = reinterpret_cast<uint64_t*>(take(8 * N));
+  w.keys_out = reinterpret_cast<uint64_t*>(take(8 * N));
+  w.vals_out = reinterpret_cast<int32_t*>(take(4 * N));
   w.cs = reinterpret_cast<double*>(take(8 * N));
   w.bs = reinterpret_cast<double*>(take(8 * N));
   w.sc = reinterpret_cast<GapScalars*>(take(sizeof(GapScalars)));
@@ -97,11 +107,14 @@ Work carve(void* base, int64_t n, int64_t m) {
   return w;
 }
 
-// Order-preserving map double -> uint64 (larger double, larger key); key 0 is
-// reserved for "no event" (only reachable by an all-ones negative NaN).
+// Order-preserving map double -> uint64 and its exact inverse.
 __device__ __forceinline__ uint64_t order_key(double d) {
   const uint64_t b = static_cast<uint64_t>(__double_as_longlong(d));
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_value(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
 }
 
 struct GapIn {
@@ -111,7 +124,7 @@ struct GapIn {
   double omega;
 };
 
-// Per-coordinate logic of restarts.hpp:117-170.  Returns the b_inf / c_inf
+// Per-coordinate logic of restarts.hpp:117-170: the b_inf / c_inf
 // contributions (flags bit0 / bit1) and up to two events.
 struct Coord {
   unsigned mass_use = 0;
@@ -213,20 +226,19 @@ __global__ void events_kernel(GapIn g, Work w) {
     const int slots = t < g.n ? 1 : 2;
     for (int e = 0; e < slots; ++e) {
       const int64_t s = s0 + e;
-      if (e < o.ne) {
-        w.keys_in[s] = order_key(o.lam[e]);
+      const bool valid = e < o.ne;
+      w.flag[s] = valid ? 1 : 0;
+      if (valid) {
         w.lam[s] = o.lam[e];
         w.dc[s] = o.dc[e];
         w.di[s] = o.di[e];
-      } else {
-        w.keys_in[s] = 0;
-        w.lam[s] = 0.0;
-        w.dc[s] = 0.0;
-        w.di[s] = 0.0;
       }
-      w.vals_in[s] = static_cast<int32_t>(s);
     }
   }
+}
+
+__global__ void keys_kernel(Work w, int64_t E) {
+  GRID_STRIDE(e, E) w.keys_in[e] = order_key(w.lam[w.sel[e]]);
 }
 
 __device__ double finish_lambda(double lambda_star) {
@@ -236,17 +248,16 @@ __device__ double finish_lambda(double lambda_star) {
 }
 
 // Reference sweep (restarts.hpp:175-212), one thread, sorted order.
-__global__ void sweep_seq_kernel(Work w, const double* r_slot, double r_value) {
+__global__ void sweep_seq_kernel(Work w, int64_t E, const double* r_slot, double r_value) {
   const double r = r_slot ? *r_slot : r_value;
   const double r2 = r * r;
-  const int64_t E = static_cast<int64_t>(w.sc->count);
   double c_sum = w.sc->sums[1];
   double b_sum = w.sc->sums[0];
   double hi = CUDART_INF;
   double ls = -1.0;
   int64_t idx = 0;
   while (idx < E) {
-    const double lam = w.lam[w.vals_out[idx]];
+    const double lam = key_value(w.keys_out[idx]);
     const double phi_lo = c_sum + b_sum / (lam * lam);
     if (phi_lo >= r2) {
       if (b_sum > 0.0 && r2 > c_sum) {
@@ -257,7 +268,7 @@ __global__ void sweep_seq_kernel(Work w, const double* r_slot, double r_value) {
       ls = clampd(ls, lam, hi);
       break;
     }
-    while (idx < E && w.lam[w.vals_out[idx]] == lam) {
+    while (idx < E && key_value(w.keys_out[idx]) == lam) {
       const int32_t s = w.vals_out[idx];
       c_sum += w.dc[s];
       b_sum += w.di[s];
@@ -278,8 +289,8 @@ __global__ void sweep_seq_kernel(Work w, const double* r_slot, double r_value) {
   w.sc->lambda_star = finish_lambda(ls);
 }
 
-__global__ void gather_masses_kernel(Work w, int64_t N) {
-  GRID_STRIDE(idx, N) {
+__global__ void gather_masses_kernel(Work w, int64_t E) {
+  GRID_STRIDE(idx, E) {
     const int32_t s = w.vals_out[idx];
     w.cs[idx] = w.dc[s];
     w.bs[idx] = w.di[s];
@@ -288,33 +299,31 @@ __global__ void gather_masses_kernel(Work w, int64_t N) {
 
 __global__ void init_first_kernel(Work w) { w.sc->first = ~0ull; }
 
-// Parallel sweep: scans hold exclusive prefix masses in sorted order.
-__global__ void first_hit_kernel(Work w, const double* r_slot, double r_value, int64_t N) {
+// Parallel sweep: cs/bs hold exclusive prefix masses in sorted order.
+__global__ void first_hit_kernel(Work w, int64_t E, const double* r_slot, double r_value) {
   const double r = r_slot ? *r_slot : r_value;
   const double r2 = r * r;
-  const int64_t E = static_cast<int64_t>(w.sc->count);
   const double c0 = w.sc->sums[1], b0 = w.sc->sums[0];
   GRID_STRIDE(idx, E) {
-    const double lam = w.lam[w.vals_out[idx]];
-    if (idx > 0 && w.lam[w.vals_out[idx - 1]] == lam) continue;  // not a group head
+    const uint64_t key = w.keys_out[idx];
+    if (idx > 0 && w.keys_out[idx - 1] == key) continue;  // not a group head
+    const double lam = key_value(key);
     const double c_sum = c0 + w.cs[idx];
     const double b_sum = b0 + w.bs[idx];
     if (c_sum + b_sum / (lam * lam) >= r2) atomicMin(&w.sc->first, static_cast<unsigned long long>(idx));
   }
-  (void)N;
 }
 
-__global__ void finalize_perf_kernel(Work w, const double* r_slot, double r_value) {
+__global__ void finalize_perf_kernel(Work w, int64_t E, const double* r_slot, double r_value) {
   const double r = r_slot ? *r_slot : r_value;
   const double r2 = r * r;
-  const int64_t E = static_cast<int64_t>(w.sc->count);
   const double c0 = w.sc->sums[1], b0 = w.sc->sums[0];
   double ls;
   const unsigned long long f = w.sc->first;
   if (f != ~0ull) {
     const int64_t idx = static_cast<int64_t>(f);
-    const double lam = w.lam[w.vals_out[idx]];
-    const double hi = idx > 0 ? w.lam[w.vals_out[idx - 1]] : CUDART_INF;
+    const double lam = key_value(w.keys_out[idx]);
+    const double hi = idx > 0 ? key_value(w.keys_out[idx - 1]) : CUDART_INF;
     const double c_sum = c0 + w.cs[idx], b_sum = b0 + w.bs[idx];
     if (b_sum > 0.0 && r2 > c_sum) {
       ls = sqrt(b_sum / (r2 - c_sum));
@@ -327,7 +336,7 @@ __global__ void finalize_perf_kernel(Work w, const double* r_slot, double r_valu
     if (E > 0) {
       c_sum = c0 + (w.cs[E - 1] + w.dc[w.vals_out[E - 1]]);
       b_sum = b0 + (w.bs[E - 1] + w.di[w.vals_out[E - 1]]);
-      hi = w.lam[w.vals_out[E - 1]];
+      hi = key_value(w.keys_out[E - 1]);
     }
     if (b_sum > 0.0 && r2 > c_sum) {
       ls = sqrt(b_sum / (r2 - c_sum));
@@ -402,6 +411,11 @@ __global__ void value_finish_kernel(const double* sum, const double* r_slot, dou
   *out = (r > 0.0 && value > 0.0) ? value / r : 0.0;
 }
 
+GapIn make_in(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
+              const double* aty, double omega) {
+  return GapIn{P->c, P->lv, P->uv, P->lc, P->uc, x, y, ax, aty, P->n, P->m, omega};
+}
+
 }  // namespace
 }  // namespace pdlp
 
@@ -409,90 +423,102 @@ using namespace pdlp;
 
 extern "C" size_t pdlpk_gap_work_bytes(int64_t n, int64_t m) {
   const int64_t N = n + 2 * m;
-  return align_up(8 * N) * 2 + align_up(4 * N) * 2 + align_up(8 * N) * 5 +
-         align_up(sizeof(GapScalars)) + align_up(cub_bytes_for(N)) + 256;
+  return align_up(N) + align_up(8 * N) * 3 + align_up(4 * N) + align_up(8 * N) * 2 +
+         align_up(4 * N) + align_up(8 * N) * 2 + align_up(sizeof(GapScalars)) +
+         align_up(cub_bytes_for(N)) + 256;
 }
 
-extern "C" int pdlpk_gap(const pdlpk_problem* P, const double* x, const double* y,
-                         const double* ax, const double* aty, double omega, const double* r_slot,
-                         double r_value, const pdlpk_red* red, void* work, double* gap_slot,
-                         cudaStream_t s) {
+extern "C" int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const double* y,
+                                 const double* ax, const double* aty, double omega,
+                                 const pdlpk_red* red, void* work, int* count_out,
+                                 cudaStream_t s) {
   const int64_t n = P->n, m = P->m, N = n + 2 * m;
   Work w = carve(work, n, m);
-  GapIn g{P->c, P->lv, P->uv, P->lc, P->uc, x, y, ax, aty, n, m, omega};
-  const bool parity = red->parity != 0;
-  // lam -> inf masses in the reference's accumulation order
+  const GapIn g = make_in(P, x, y, ax, aty, omega);
   auto fm = [g] __device__(int64_t t, double* v) -> unsigned {
     const Coord o = gap_coord(g, t);
     v[0] = o.b;
     v[1] = o.c;
     return o.mass_use;
   };
-  if (multi_reduce<2>(fm, n + m, parity ? PDLPK_RED_SEQ : PDLPK_RED_TREE, red->shards, 0u,
-                      red->scratch, w.sc->sums, s) != 0) {
-    return -1;
-  }
+  int rc = multi_reduce<2>(fm, n + m, red->parity ? PDLPK_RED_SEQ : PDLPK_RED_TREE, red->shards, 0u,
+                           red->scratch, w.sc->sums, s);
+  if (rc != 0) return rc;
   if (N > 0) {
     events_kernel<<<ew_blocks(n + m), kT, 0, s>>>(g, w);
-    auto fc = [w] __device__(int64_t idx, double* v) -> unsigned {
-      v[0] = 1.0;
-      return w.keys_in[idx] != 0 ? 1u : 0u;
-    };
-    if (multi_reduce<1>(fc, N, PDLPK_RED_TREE, red->shards, 0u, red->scratch, &w.sc->count, s) != 0)
-      return -1;
     size_t bytes = w.cub_bytes;
-    if (cub::DeviceRadixSort::SortPairsDescending(w.cub_tmp, bytes, w.keys_in, w.keys_out,
-                                                  w.vals_in, w.vals_out, static_cast<int>(N), 0,
-                                                  64, s) != cudaSuccess) {
-      return -1;
-    }
+    const cudaError_t e = cub::DeviceSelect::Flagged(w.cub_tmp, bytes, cub::CountingInputIterator<int32_t>(0),
+                                                     w.flag, w.sel, &w.sc->num_events,
+                                                     static_cast<int>(N), s);
+    if (e != cudaSuccess) return static_cast<int>(e);
   } else {
-    cudaMemsetAsync(&w.sc->count, 0, sizeof(double), s);
+    cudaMemsetAsync(&w.sc->num_events, 0, sizeof(int), s);
+  }
+  if (count_out != nullptr) {
+    cudaMemcpyAsync(count_out, &w.sc->num_events, sizeof(int), cudaMemcpyDeviceToDevice, s);
+  }
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const double* y,
+                                const double* ax, const double* aty, double omega,
+                                const double* r_slot, double r_value, int64_t E,
+                                const pdlpk_red* red, void* work, double* gap_slot,
+                                cudaStream_t s) {
+  const int64_t n = P->n, m = P->m;
+  Work w = carve(work, n, m);
+  const GapIn g = make_in(P, x, y, ax, aty, omega);
+  const bool parity = red->parity != 0;
+  if (E > 0) {
+    keys_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+    size_t bytes = w.cub_bytes;
+    const cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(
+        w.cub_tmp, bytes, w.keys_in, w.keys_out, w.sel, w.vals_out, static_cast<int>(E), 0, 64, s);
+    if (e != cudaSuccess) return static_cast<int>(e);
   }
   if (parity) {
-    sweep_seq_kernel<<<1, 1, 0, s>>>(w, r_slot, r_value);
+    sweep_seq_kernel<<<1, 1, 0, s>>>(w, E, r_slot, r_value);
     value_seq_kernel<<<1, 1, 0, s>>>(g, w, r_slot, r_value, gap_slot);
-  } else {
-    if (N > 0) {
-      gather_masses_kernel<<<ew_blocks(N), kT, 0, s>>>(w, N);
-      size_t bytes = w.cub_bytes;
-      cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.cs, w.cs, static_cast<int>(N), s);
-      bytes = w.cub_bytes;
-      cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.bs, w.bs, static_cast<int>(N), s);
-    }
-    init_first_kernel<<<1, 1, 0, s>>>(w);
-    if (N > 0) first_hit_kernel<<<ew_blocks(N), kT, 0, s>>>(w, r_slot, r_value, N);
-    finalize_perf_kernel<<<1, 1, 0, s>>>(w, r_slot, r_value);
-    const double* lam_star = &w.sc->lambda_star;
-    auto fv = [g, lam_star] __device__(int64_t t, double* v) -> unsigned {
-      const double lambda = *lam_star;
-      if (t < g.n) {
-        const double xh = cand_x(g, t, lambda);
-        v[0] = g.c[t] * (g.x[t] - xh) + g.aty[t] * xh;
-        return 1u;
-      }
-      const int64_t j = t - g.n;
-      const double yh = cand_y(g, j, lambda);
-      const double yj = g.y[j];
-      double d = -(yh * g.ax[j]);
-      if (yh > 0.0) {
-        d -= mul_zero_inf(-g.lc[j], yh);
-      } else if (yh < 0.0) {
-        d -= mul_zero_inf(-g.uc[j], yh);
-      }
-      if (yj > 0.0) {
-        d += mul_zero_inf(-g.lc[j], yj);
-      } else if (yj < 0.0) {
-        d += mul_zero_inf(-g.uc[j], yj);
-      }
-      v[0] = d;
-      return 1u;
-    };
-    if (multi_reduce<1>(fv, n + m, PDLPK_RED_TREE, red->shards, 0u, red->scratch, &w.sc->value,
-                        s) != 0) {
-      return -1;
-    }
-    value_finish_kernel<<<1, 1, 0, s>>>(&w.sc->value, r_slot, r_value, gap_slot);
+    return static_cast<int>(cudaGetLastError());
   }
+  if (E > 0) {
+    gather_masses_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+    size_t bytes = w.cub_bytes;
+    cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.cs, w.cs, static_cast<int>(E), s);
+    bytes = w.cub_bytes;
+    cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.bs, w.bs, static_cast<int>(E), s);
+  }
+  init_first_kernel<<<1, 1, 0, s>>>(w);
+  if (E > 0) first_hit_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E, r_slot, r_value);
+  finalize_perf_kernel<<<1, 1, 0, s>>>(w, E, r_slot, r_value);
+  const double* lam_star = &w.sc->lambda_star;
+  auto fv = [g, lam_star] __device__(int64_t t, double* v) -> unsigned {
+    const double lambda = *lam_star;
+    if (t < g.n) {
+      const double xh = cand_x(g, t, lambda);
+      v[0] = g.c[t] * (g.x[t] - xh) + g.aty[t] * xh;
+      return 1u;
+    }
+    const int64_t j = t - g.n;
+    const double yh = cand_y(g, j, lambda);
+    const double yj = g.y[j];
+    double d = -(yh * g.ax[j]);
+    if (yh > 0.0) {
+      d -= mul_zero_inf(-g.lc[j], yh);
+    } else if (yh < 0.0) {
+      d -= mul_zero_inf(-g.uc[j], yh);
+    }
+    if (yj > 0.0) {
+      d += mul_zero_inf(-g.lc[j], yj);
+    } else if (yj < 0.0) {
+      d += mul_zero_inf(-g.uc[j], yj);
+    }
+    v[0] = d;
+    return 1u;
+  };
+  const int rc = multi_reduce<1>(fv, n + m, PDLPK_RED_TREE, red->shards, 0u, red->scratch,
+                                 &w.sc->value, s);
+  if (rc != 0) return rc;
+  value_finish_kernel<<<1, 1, 0, s>>>(&w.sc->value, r_slot, r_value, gap_slot);
   return static_cast<int>(cudaGetLastError());
 }

@@ -158,22 +158,28 @@ struct RowEpi {
   double sigma, w;
   bool pend;
   double dy2 = 0.0, infy = 0.0;
-  __device__ __forceinline__ void line(int64_t r, double acc) {
-    const double yr = y[r];
+  struct Pre {
+    double y, lc, uc, sy;
+  };
+  __device__ __forceinline__ Pre load(int64_t r) const {
+    return {y[r], lc[r], uc[r], pend ? sy[r] : 0.0};
+  }
+  __device__ __forceinline__ void line(int64_t r, double acc, const Pre& p) {
+    const double yr = p.y;
     const double yhat = yr - sigma * acc;
-    const double proj = clampd(yhat / sigma, -uc[r], -lc[r]);
+    const double proj = clampd(yhat / sigma, -p.uc, -p.lc);
     const double yp = yhat - sigma * proj;  // exact cancellation: no FMA (step.hpp:85)
     yn[r] = yp;
     const double d = yp - yr;
     dy[r] = d;
-    if (pend) sy[r] = sy[r] + w * yr;
+    if (pend) sy[r] = p.sy + w * yr;
     dy2 += d * d;
     infy = max_keep(infy, fabs(yp));
   }
 };
 
-template <class P, int V>
-__global__ void __launch_bounds__(kSpmvThreads) row_pass(pdlpk_step_args a) {
+template <class P, int Seg>
+__global__ void __launch_bounds__(kSpmvThreads, 4) row_pass(pdlpk_step_args a) {
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(kSpmvThreads) row_pass(pdlpk_step_args a) {
   e.sigma = st->eta * st->omega;
   e.pend = st->avg_pending != 0;
   e.w = st->avg_w;
-  sched_spmv<P, V>(a.P.K, a.P.K.value, a.xbar, e);
+  sched_spmv<P, Seg>(a.P.K, a.P.K.value, a.xbar, e);
   __shared__ double red[32];
   const double s1 = block_sum(e.dy2, red);
   __syncthreads();
@@ -205,18 +211,21 @@ struct ColEpi {
   const double* __restrict__ x;
   const double* __restrict__ xn;
   double dx2 = 0.0, curv = 0.0, infx = 0.0;
-  __device__ __forceinline__ void line(int64_t i, double d) {
-    atyn[i] = aty[i] + d;
-    const double xp = xn[i];
-    const double dxi = xp - x[i];
+  struct Pre {
+    double aty, x, xn;
+  };
+  __device__ __forceinline__ Pre load(int64_t i) const { return {aty[i], x[i], xn[i]}; }
+  __device__ __forceinline__ void line(int64_t i, double d, const Pre& p) {
+    atyn[i] = p.aty + d;
+    const double dxi = p.xn - p.x;
     dx2 += dxi * dxi;
     curv += d * dxi;
-    infx = max_keep(infx, fabs(xp));
+    infx = max_keep(infx, fabs(p.xn));
   }
 };
 
-template <class P, int V>
-__global__ void __launch_bounds__(kSpmvThreads) col_pass(pdlpk_step_args a) {
+template <class P, int Seg>
+__global__ void __launch_bounds__(kSpmvThreads, 4) col_pass(pdlpk_step_args a) {
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;
@@ -225,7 +234,7 @@ __global__ void __launch_bounds__(kSpmvThreads) col_pass(pdlpk_step_args a) {
   e.atyn = a.aty[cur ^ 1];
   e.x = a.x[cur];
   e.xn = a.x[cur ^ 1];
-  sched_spmv<P, V>(a.P.KT, a.P.KT.value, a.dy, e);
+  sched_spmv<P, Seg>(a.P.KT, a.P.KT.value, a.dy, e);
   __shared__ double red[32];
   __shared__ bool last;
   const double s1 = block_sum(e.dx2, red);
@@ -420,15 +429,16 @@ struct LaunchRowCol {
   const pdlpk_step_args* a;
   cudaStream_t s;
   bool row;
-  template <class P, int V>
+  template <class P, int Seg>
   int go() {
     const pdlpk_csr& A = row ? a->P.K : a->P.KT;
     const int64_t g = sched_blocks(A);
     if (g <= 0) return 0;
+    const size_t smem = (Seg & 4) ? kSpmvSmem : 0;
     if (row) {
-      row_pass<P, V><<<static_cast<unsigned>(g), kSpmvThreads, 0, s>>>(*a);
+      row_pass<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
     } else {
-      col_pass<P, V><<<static_cast<unsigned>(g), kSpmvThreads, 0, s>>>(*a);
+      col_pass<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
     }
     return 0;
   }
@@ -454,8 +464,8 @@ extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
   if (a->mode == 0) {
     // Degenerate shapes (an empty side) still need the decision, which the
     // column pass performs: it always has >= 1 CTA (short_blocks >= 1).
-    dispatch_pv(a->P.K, LaunchRowCol{a, s, true});
-    dispatch_pv(a->P.KT, LaunchRowCol{a, s, false});
+    dispatch_p(a->P.K, LaunchRowCol{a, s, true});
+    dispatch_p(a->P.KT, LaunchRowCol{a, s, false});
   } else {
     const int gm = ew_blocks(a->P.m), gn = ew_blocks(a->P.n);
     if (a->P.K.wide) {
@@ -477,9 +487,9 @@ extern "C" int pdlpk_attempt_timed(const pdlpk_step_args* a, cudaEvent_t* ev, cu
   primal_pass<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a);
   cudaEventRecord(ev[1], s);
   if (a->mode == 0) {
-    dispatch_pv(a->P.K, LaunchRowCol{a, s, true});
+    dispatch_p(a->P.K, LaunchRowCol{a, s, true});
     cudaEventRecord(ev[2], s);
-    dispatch_pv(a->P.KT, LaunchRowCol{a, s, false});
+    dispatch_p(a->P.KT, LaunchRowCol{a, s, false});
   } else {
     const int gm = ew_blocks(a->P.m), gn = ew_blocks(a->P.n);
     if (a->P.K.wide) {

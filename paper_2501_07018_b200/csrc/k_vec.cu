@@ -28,12 +28,15 @@ inline int ew_blocks(int64_t n) {
 inline int ok() { return static_cast<int>(cudaGetLastError()); }
 
 // -------------------------------------------------------------- products ---
+// cond: optional device flag; the product is skipped when *cond == 0.
 template <class P>
 __global__ void __launch_bounds__(kT) seq_spmv_kernel(const P* __restrict__ start,
                                                       const int32_t* __restrict__ idx,
                                                       const double* __restrict__ val,
                                                       const double* __restrict__ v,
-                                                      double* __restrict__ out, int64_t dim) {
+                                                      double* __restrict__ out, int64_t dim,
+                                                      const double* cond) {
+  if (cond != nullptr && *cond == 0.0) return;
   GRID_STRIDE(r, dim) {
     double acc = 0.0;
     for (int64_t k = start[r]; k < start[r + 1]; ++k) acc = acc + val[k] * v[idx[k]];
@@ -43,15 +46,19 @@ __global__ void __launch_bounds__(kT) seq_spmv_kernel(const P* __restrict__ star
 
 struct StoreEpi {
   double* out;
-  __device__ __forceinline__ void line(int64_t r, double acc) { out[r] = acc; }
+  struct Pre {};
+  __device__ __forceinline__ Pre load(int64_t) const { return {}; }
+  __device__ __forceinline__ void line(int64_t r, double acc, const Pre&) { out[r] = acc; }
 };
 
-template <class P, int V>
-__global__ void __launch_bounds__(kSpmvThreads) sched_spmv_kernel(pdlpk_csr A,
+template <class P, int Seg>
+__global__ void __launch_bounds__(kSpmvThreads, 4) sched_spmv_kernel(pdlpk_csr A,
                                                                   const double* vals,
-                                                                  const double* v, double* out) {
+                                                                  const double* v, double* out,
+                                                                  const double* cond) {
+  if (cond != nullptr && *cond == 0.0) return;
   StoreEpi e{out};
-  sched_spmv<P, V>(A, vals, v, e);
+  sched_spmv<P, Seg>(A, vals, v, e);
 }
 
 struct LaunchSpmv {
@@ -59,11 +66,15 @@ struct LaunchSpmv {
   const double* vals;
   const double* v;
   double* out;
+  const double* cond;
   cudaStream_t s;
-  template <class P, int V>
+  template <class P, int Seg>
   int go() {
     const int64_t g = sched_blocks(*A);
-    if (g > 0) sched_spmv_kernel<P, V><<<static_cast<unsigned>(g), kSpmvThreads, 0, s>>>(*A, vals, v, out);
+    if (g > 0) {
+      sched_spmv_kernel<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, (Seg & 4) ? kSpmvSmem : 0, s>>>(
+          *A, vals, v, out, cond);
+    }
     return ok();
   }
 };
@@ -129,30 +140,7 @@ __global__ void radius_kernel(const double* dx2, const double* dy2, double omega
 }
 
 // ------------------------------------------------------ preconditioning ---
-template <class P>
-__global__ void line_factor_kernel(const P* __restrict__ start, const double* __restrict__ val,
-                                   int64_t dim, int one_norm, double* __restrict__ f) {
-  GRID_STRIDE(r, dim) {
-    double a = 0.0;
-    if (one_norm) {
-      for (int64_t k = start[r]; k < start[r + 1]; ++k) a += fabs(val[k]);  // rescaling.hpp:111-116
-    } else {
-      for (int64_t k = start[r]; k < start[r + 1]; ++k) a = max_keep(a, fabs(val[k]));
-    }
-    f[r] = a > 0.0 ? sqrt(a) : 1.0;
-  }
-}
-
-template <class P>
-__global__ void apply_factor_kernel(const P* __restrict__ start, const int32_t* __restrict__ idx,
-                                    double* __restrict__ val, int64_t dim,
-                                    const double* __restrict__ fp, const double* __restrict__ fs) {
-  GRID_STRIDE(r, dim) {
-    const double a = fp[r];
-    for (int64_t k = start[r]; k < start[r + 1]; ++k) val[k] = val[k] / (a * fs[idx[k]]);
-  }
-}
-
+// (line norms and matrix scaling live in k_scale.cu)
 __global__ void apply_vec_factor_kernel(double* lc, double* uc, double* rs, const double* fr,
                                         int64_t m, double* c, double* lv, double* uv,
                                         double* cs, const double* fc, int64_t n) {
@@ -223,22 +211,27 @@ int pdlpk_start_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t
   return pdlpk_index_to_i32(src, dst, n, s);
 }
 
-int pdlpk_spmv(const pdlpk_csr* A, int32_t orig, const double* v, double* out, int32_t parity,
-               cudaStream_t s) {
+int pdlpk_spmv_cond(const pdlpk_csr* A, int32_t orig, const double* v, double* out,
+                    int32_t parity, const double* cond, cudaStream_t s) {
   if (A->dim == 0) return 0;
   const double* vals = orig ? A->value_orig : A->value;
   if (parity) {
     const int g = ew_blocks(A->dim);
     if (A->wide) {
       seq_spmv_kernel<int64_t><<<g, kT, 0, s>>>(static_cast<const int64_t*>(A->start), A->index,
-                                                vals, v, out, A->dim);
+                                                vals, v, out, A->dim, cond);
     } else {
       seq_spmv_kernel<int32_t><<<g, kT, 0, s>>>(static_cast<const int32_t*>(A->start), A->index,
-                                                vals, v, out, A->dim);
+                                                vals, v, out, A->dim, cond);
     }
     return ok();
   }
-  return dispatch_pv(*A, LaunchSpmv{A, vals, v, out, s});
+  return dispatch_p(*A, LaunchSpmv{A, vals, v, out, cond, s});
+}
+
+int pdlpk_spmv(const pdlpk_csr* A, int32_t orig, const double* v, double* out, int32_t parity,
+               cudaStream_t s) {
+  return pdlpk_spmv_cond(A, orig, v, out, parity, nullptr, s);
 }
 
 int pdlpk_diff_norm_sq(const double* a, const double* b, int64_t n, const pdlpk_red* red,
@@ -311,18 +304,21 @@ int pdlpk_ray_primal_prep(const pdlpk_problem* P, int32_t orig, const double* yc
                           const pdlpk_red* red, double* slots, cudaStream_t s) {
   const double* lc = orig ? P->lc_o : P->lc;
   const double* uc = orig ? P->uc_o : P->uc;
+  // values: 0 |ray|_inf (max), 1 coordinates changed by the projection (count)
   auto f = [=] __device__(int64_t j, double* v) -> unsigned {
-    const double r = cone_project(yc[j], cone_of_bounds(lc[j], uc[j]));
+    const double y = yc[j];
+    const double r = cone_project(y, cone_of_bounds(lc[j], uc[j]));
     ray[j] = r;
     v[0] = fabs(r);
-    return 1u;
+    v[1] = (r != y) ? 1.0 : 0.0;
+    return 3u;
   };
-  return multi_reduce<1>(f, P->m, PDLPK_RED_TREE, red->shards, 0x1u, red->scratch, slots, s);
+  return multi_reduce<2>(f, P->m, PDLPK_RED_TREE, red->shards, 0x1u, red->scratch, slots, s);
 }
 
 int pdlpk_ray_primal_finish(const pdlpk_problem* P, int32_t orig, const double* ray,
-                            const double* aty, double* rhat, const pdlpk_red* red,
-                            double* slots, cudaStream_t s) {
+                            const double* aty, const double* aty_alt, const double* changed,
+                            double* rhat, const pdlpk_red* red, double* slots, cudaStream_t s) {
   const int64_t m = P->m, n = P->n;
   const double* lc = orig ? P->lc_o : P->lc;
   const double* uc = orig ? P->uc_o : P->uc;
@@ -332,7 +328,7 @@ int pdlpk_ray_primal_finish(const pdlpk_problem* P, int32_t orig, const double* 
   auto f = [=] __device__(int64_t t, double* v) -> unsigned {
     if (t < m) return penalty_term(ray[t], lc[t], uc[t], v[1]) ? 2u : 0u;
     const int64_t i = t - m;
-    const double a = aty[i];
+    const double a = (aty_alt != nullptr && *changed == 0.0) ? aty_alt[i] : aty[i];
     const double rh = cone_project(-a, cone_of_bounds(lv[i], uv[i]));
     rhat[i] = rh;
     v[0] = fabs(a + rh);
@@ -376,33 +372,6 @@ int pdlpk_ray_dual_finish(const pdlpk_problem* P, int32_t orig, const double* ax
 int pdlpk_radius(const double* dx2, const double* dy2, double omega, double* out,
                  cudaStream_t s) {
   radius_kernel<<<1, 1, 0, s>>>(dx2, dy2, omega, out);
-  return ok();
-}
-
-int pdlpk_line_factors(const pdlpk_csr* A, int32_t one_norm, double* f, cudaStream_t s) {
-  if (A->dim == 0) return 0;
-  const int g = ew_blocks(A->dim);
-  if (A->wide) {
-    line_factor_kernel<int64_t><<<g, kT, 0, s>>>(static_cast<const int64_t*>(A->start), A->value,
-                                                 A->dim, one_norm, f);
-  } else {
-    line_factor_kernel<int32_t><<<g, kT, 0, s>>>(static_cast<const int32_t*>(A->start), A->value,
-                                                 A->dim, one_norm, f);
-  }
-  return ok();
-}
-
-int pdlpk_apply_factors(const pdlpk_csr* A, double* value, const double* f_primary,
-                        const double* f_secondary, cudaStream_t s) {
-  if (A->dim == 0) return 0;
-  const int g = ew_blocks(A->dim);
-  if (A->wide) {
-    apply_factor_kernel<int64_t><<<g, kT, 0, s>>>(static_cast<const int64_t*>(A->start), A->index,
-                                                  value, A->dim, f_primary, f_secondary);
-  } else {
-    apply_factor_kernel<int32_t><<<g, kT, 0, s>>>(static_cast<const int32_t*>(A->start), A->index,
-                                                  value, A->dim, f_primary, f_secondary);
-  }
   return ok();
 }
 

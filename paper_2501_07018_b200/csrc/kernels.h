@@ -31,19 +31,24 @@ typedef struct pdlpk_csr {
   int64_t nnz;
   const void* start; /* dim+1 entries, int32 or int64 */
   int32_t wide;      /* 1: start is int64 */
-  int32_t vec;       /* lanes per short row (power of two, 1..32) */
+  int32_t tile_blocks; /* CTAs for the tiled short-line segment */
   const int32_t* index;
   const double* value;      /* scaled values (the iteration matrix) */
   const double* value_orig; /* original values (verification products) */
-  const int32_t* long_rows; /* rows with len > t_med, one CTA each */
+  const int32_t* long_rows; /* lines with len > kMedMax, one CTA each */
   int64_t n_long;
-  const int32_t* med_rows; /* rows with t_short < len <= t_med, one warp each */
+  const int32_t* med_rows; /* lines with kShortMax < len <= kMedMax, one warp each */
   int64_t n_med;
-  int32_t t_short;
-  int32_t t_med;
-  int32_t short_blocks; /* CTAs for the short-row segment */
-  int32_t _pad;
+  const int32_t* tile_row0; /* first line of each warp tile of short lines */
+  const int32_t* tile_rows; /* lines in each tile (<= kTileRows) */
+  int64_t n_tiles;
 } pdlpk_csr;
+
+/* Schedule limits (spmv.cuh) the host planner must respect. */
+#define PDLPK_SHORT_MAX 32
+#define PDLPK_MED_MAX 8192
+#define PDLPK_TILE_NNZ 512
+#define PDLPK_TILE_ROWS 64
 
 /* Device-resident step controller: one per inner loop (main / polish). */
 typedef struct pdlpk_step_state {
@@ -131,9 +136,12 @@ int pdlpk_attempt_timed(const pdlpk_step_args* a, cudaEvent_t* ev, cudaStream_t 
 int pdlpk_flush_average(const pdlpk_step_args* a, cudaStream_t s);
 
 /* ------------------------------------------------------------- cadence --- */
-/* out = A v with the given layout; orig != 0 uses the original values. */
+/* out = A v with the given layout; orig != 0 uses the original values.
+ * cond (device scalar, may be NULL): the product is skipped when *cond == 0. */
 int pdlpk_spmv(const pdlpk_csr* A, int32_t orig, const double* v, double* out, int32_t parity,
                cudaStream_t s);
+int pdlpk_spmv_cond(const pdlpk_csr* A, int32_t orig, const double* v, double* out,
+                    int32_t parity, const double* cond, cudaStream_t s);
 
 /* slot = sum_i (a_i - b_i)^2 over dim n (sharded in parity). */
 int pdlpk_diff_norm_sq(const double* a, const double* b, int64_t n, const pdlpk_red* red,
@@ -156,39 +164,54 @@ int pdlpk_screen(const pdlpk_problem* P, int32_t orig, const double* x, const do
                  double* r_out, double* slots, cudaStream_t s);
 
 /* Ray tests (residuals.hpp:222-299), split around their matrix product:
- *  primal: prep writes ray = proj_cone(yc), slot0 = |ray|_inf;
- *          finish (after aty = A'ray) writes rhat, slot1 = residual,
- *          slot2 = penalty of (ray, rhat) (objective = -slot2).
- *  dual:   prep: slot0 = |xc|_inf, slot1 = box residual, slot2 = c'xc;
- *          finish (after ax = A xc): slot3 = row residual. */
+ *  primal: prep writes ray = proj_cone(yc), slots[0] = |ray|_inf,
+ *          slots[1] = number of coordinates the projection changed;
+ *          finish (after aty = A'ray) writes rhat, slots[0] = residual,
+ *          slots[1] = penalty of (ray, rhat) (objective = -penalty).  When
+ *          aty_alt and changed are given and *changed == 0 the ray equals yc
+ *          and aty_alt (= A'yc, same kernel) is used instead of aty.
+ *  dual:   prep: slots[0] = |xc|_inf, slots[1] = box residual, slots[2] = c'xc;
+ *          finish (after ax = A xc): slots[0] = row residual. */
 int pdlpk_ray_primal_prep(const pdlpk_problem* P, int32_t orig, const double* yc, double* ray,
                           const pdlpk_red* red, double* slots, cudaStream_t s);
 int pdlpk_ray_primal_finish(const pdlpk_problem* P, int32_t orig, const double* ray,
-                            const double* aty, double* rhat, const pdlpk_red* red,
-                            double* slots, cudaStream_t s);
+                            const double* aty, const double* aty_alt, const double* changed,
+                            double* rhat, const pdlpk_red* red, double* slots, cudaStream_t s);
 int pdlpk_ray_dual_prep(const pdlpk_problem* P, int32_t orig, const double* xc,
                         const pdlpk_red* red, double* slots, cudaStream_t s);
 int pdlpk_ray_dual_finish(const pdlpk_problem* P, int32_t orig, const double* ax,
                           const pdlpk_red* red, double* slots, cudaStream_t s);
 
-/* Normalized duality gap (restarts.hpp:107-220).  r read from slot r_slot
- * (radius) unless r_slot == NULL, in which case r_value is used.  Result in
- * *gap_slot.  work must hold pdlpk_gap_work_bytes(n, m) bytes. */
+/* Normalized duality gap (restarts.hpp:107-220), k_gap.cu.  prepare computes
+ * the lam->inf masses and compacts the breakpoint events (their count goes to
+ * *count_out, a device int); finish sorts the E events the host read back,
+ * sweeps, assembles the candidate and writes the gap to *gap_slot.  r read
+ * from r_slot (radius) unless r_slot == NULL (then r_value).  work must hold
+ * pdlpk_gap_work_bytes(n, m) bytes and stay untouched between the two calls. */
 size_t pdlpk_gap_work_bytes(int64_t n, int64_t m);
-int pdlpk_gap(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
-              const double* aty, double omega, const double* r_slot, double r_value,
-              const pdlpk_red* red, void* work, double* gap_slot, cudaStream_t s);
+int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
+                      const double* aty, double omega, const pdlpk_red* red, void* work,
+                      int* count_out, cudaStream_t s);
+int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
+                     const double* aty, double omega, const double* r_slot, double r_value,
+                     int64_t E, const pdlpk_red* red, void* work, double* gap_slot,
+                     cudaStream_t s);
 /* slot = sqrt(omega*dx2 + dy2/omega) from two slots (restart_progress_metric). */
 int pdlpk_radius(const double* dx2, const double* dy2, double omega, double* out,
                  cudaStream_t s);
 
 /* ------------------------------------------------------- preconditioning --- */
+/* line_of[k] = line owning entry k (max-scan over line heads; k_scale.cu). */
+size_t pdlpk_line_of_work_bytes(int64_t nnz);
+int pdlpk_line_of(const pdlpk_csr* A, int32_t* line_of, void* work, size_t work_bytes,
+                  cudaStream_t s);
 /* f[line] = sqrt(max|v|) or 1 (ruiz) / sqrt(sum|v|) or 1 (pock-chambolle),
- * per line of the layout (rescaling.hpp:80-127). */
-int pdlpk_line_factors(const pdlpk_csr* A, int32_t one_norm, double* f, cudaStream_t s);
+ * per line of the layout (rescaling.hpp:80-127).  bits: dim scratch words. */
+int pdlpk_line_factors(const pdlpk_csr* A, const int32_t* line_of, int32_t one_norm, double* f,
+                       unsigned long long* bits, cudaStream_t s);
 /* value /= f_primary[line] * f_secondary[index] for one layout. */
-int pdlpk_apply_factors(const pdlpk_csr* A, double* value, const double* f_primary,
-                        const double* f_secondary, cudaStream_t s);
+int pdlpk_apply_factors(const pdlpk_csr* A, const int32_t* line_of, double* value,
+                        const double* f_primary, const double* f_secondary, cudaStream_t s);
 /* Vector part of apply_factors (rescaling.hpp:61-73). */
 int pdlpk_apply_vec_factors(double* lc, double* uc, double* row_scale, const double* fr,
                             int64_t m, double* c, double* lv, double* uv, double* col_scale,

@@ -15,7 +15,7 @@
 namespace pdlp {
 
 constexpr int kRedThreads = 256;
-constexpr int kRedMaxBlocks = 148 * 4;
+constexpr int kRedMaxBlocks = 148 * 8;
 
 template <int K>
 __device__ __forceinline__ void red_accum(double* acc, const double* v, unsigned use,

@@ -118,48 +118,62 @@ struct DevLayout {
   DevBuf<int64_t> start64;
   DevBuf<int32_t> index;
   DevBuf<double> value, value_orig;
-  DevBuf<int32_t> long_rows, med_rows;
+  DevBuf<int32_t> long_rows, med_rows, tile_row0, tile_rows;
   pdlpk_csr view{};
 };
 
-// Perf-mode schedule (spmv.cuh): lanes per short line from the mean length,
-// medium lines one warp, long lines one CTA.
+template <class T>
+void upload_list(const std::vector<T>& h, DevBuf<T>& d) {
+  d.alloc(h.size());
+  if (!h.empty()) PDLP_CK(cudaMemcpy(d.get(), h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+// Perf-mode schedule (spmv.cuh), the analysis phase of the SpMV: lines of
+// <= PDLPK_SHORT_MAX entries are packed into warp tiles of consecutive lines
+// (<= PDLPK_TILE_ROWS lines, <= PDLPK_TILE_NNZ entries), medium lines get a
+// warp each, long lines a CTA each.  O(lines) host pass over the row pointer.
 void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
-  const int64_t nnz = dim > 0 ? start[dim] : 0;
-  const double mean = dim > 0 ? static_cast<double>(nnz) / static_cast<double>(dim) : 0.0;
-  int vec = 1;
-  while (vec < 32 && static_cast<double>(vec) * 8.0 < mean) vec *= 2;
-  const int64_t t_short = std::max<int64_t>(16 * vec, 32);
-  const int64_t t_med = 1024;
-  std::vector<int32_t> med, lng;
+  std::vector<int32_t> med, lng, t0, tc;
+  int64_t cur0 = -1, cur_rows = 0, cur_nnz = 0;
+  auto close = [&] {
+    if (cur_rows > 0) {
+      t0.push_back(static_cast<int32_t>(cur0));
+      tc.push_back(static_cast<int32_t>(cur_rows));
+    }
+    cur0 = -1;
+    cur_rows = 0;
+    cur_nnz = 0;
+  };
   for (int64_t r = 0; r < dim; ++r) {
     const int64_t len = start[r + 1] - start[r];
-    if (len > t_med) {
-      lng.push_back(static_cast<int32_t>(r));
-    } else if (len > t_short) {
-      med.push_back(static_cast<int32_t>(r));
+    if (len > PDLPK_SHORT_MAX) {
+      close();
+      (len > PDLPK_MED_MAX ? lng : med).push_back(static_cast<int32_t>(r));
+      continue;
     }
+    if (cur_rows == PDLPK_TILE_ROWS || cur_nnz + len > PDLPK_TILE_NNZ) close();
+    if (cur_rows == 0) cur0 = r;
+    ++cur_rows;
+    cur_nnz += len;
   }
-  L.long_rows.alloc(lng.size());
-  L.med_rows.alloc(med.size());
-  if (!lng.empty()) {
-    PDLP_CK(cudaMemcpy(L.long_rows.get(), lng.data(), lng.size() * 4, cudaMemcpyHostToDevice));
-  }
-  if (!med.empty()) {
-    PDLP_CK(cudaMemcpy(L.med_rows.get(), med.data(), med.size() * 4, cudaMemcpyHostToDevice));
-  }
-  const int64_t groups_per_block = 256 / vec;
-  int64_t sb = (dim + groups_per_block - 1) / groups_per_block;
-  sb = std::min<int64_t>(sb, 148 * 16);
-  sb = std::max<int64_t>(sb, 1);
-  L.view.vec = vec;
-  L.view.t_short = static_cast<int32_t>(t_short);
-  L.view.t_med = static_cast<int32_t>(t_med);
+  close();
+  upload_list(lng, L.long_rows);
+  upload_list(med, L.med_rows);
+  upload_list(t0, L.tile_row0);
+  upload_list(tc, L.tile_rows);
+  const int64_t n_tiles = static_cast<int64_t>(t0.size());
+  // 32 KB of tile smem per CTA -> 7 CTAs per SM; grid-stride over tiles.
+  int64_t tb = (n_tiles + 7) / 8;
+  tb = std::min<int64_t>(tb, 148 * 7);
+  tb = std::max<int64_t>(tb, 1);  // the column pass's last CTA decides, so never empty
   L.view.long_rows = L.long_rows.get();
   L.view.n_long = static_cast<int64_t>(lng.size());
   L.view.med_rows = L.med_rows.get();
   L.view.n_med = static_cast<int64_t>(med.size());
-  L.view.short_blocks = static_cast<int32_t>(sb);
+  L.view.tile_row0 = L.tile_row0.get();
+  L.view.tile_rows = L.tile_rows.get();
+  L.view.n_tiles = n_tiles;
+  L.view.tile_blocks = static_cast<int32_t>(tb);
 }
 
 void upload_layout(const pdlp_csr_view& v, DevLayout& L, cudaStream_t s) {
@@ -345,6 +359,7 @@ struct Inner {  // InnerState (solver.hpp:135-193), vectors on device
   DevBuf<double> xbar, dy, aty_diff, sum_x, sum_y;
   DevBuf<double> ref_x, ref_y, ax_cur, avg_x, avg_y, ax_avg, aty_avg, diff_x, diff_y, rc_a, rc_b;
   DevBuf<double> sol_x, sol_y, sol_r, tmp_x, tmp_y, tmp_r, ray_n, ray_m, prod_n, prod_m;
+  DevBuf<double> ray_y[3], rhat[3];  // per ray candidate (batched cadence)
   DevBuf<pdlpk_step_state> state;
   DevBuf<double> part2, part3, shard_part;
   pdlpk_step_state hs{};  // host mirror of the controller
@@ -375,6 +390,10 @@ struct Inner {  // InnerState (solver.hpp:135-193), vectors on device
     for (DevBuf<double>* v :
          {&dy, &sum_y, &ref_y, &ax_cur, &avg_y, &ax_avg, &diff_y, &sol_y, &tmp_y, &ray_m, &prod_m}) {
       v->alloc(m);
+    }
+    for (int q = 0; q < 3; ++q) {
+      ray_y[q].alloc(m);
+      rhat[q].alloc(n);
     }
     cert.ray_x.alloc(n);
     cert.ray_y.alloc(m);
@@ -453,7 +472,9 @@ class Engine {
     red_scratch_.alloc(std::max<int64_t>(pdlpk_red_scratch_doubles(), 8 * int64_t(shards_) + 64));
     const int64_t gap_n = std::max(n + 2 * m, m + 2 * n);
     (void)gap_n;
-    gap_work_.alloc(std::max(pdlpk_gap_work_bytes(n, m), pdlpk_gap_work_bytes(m, n)));
+    for (auto& w : gap_work_) w.alloc(std::max(pdlpk_gap_work_bytes(n, m), pdlpk_gap_work_bytes(m, n)));
+    islots_.alloc(8);
+    PDLP_CK(cudaMallocHost(&host_islots_, 8 * sizeof(int)));
     zeros_n_ = dev_fill(n, 0.0, s());
     zeros_m_ = dev_fill(m, 0.0, s());
     PDLP_CK(cudaStreamSynchronize(s()));
@@ -462,6 +483,7 @@ class Engine {
 
   ~Engine() {
     if (host_slots_ != nullptr) cudaFreeHost(host_slots_);
+    if (host_islots_ != nullptr) cudaFreeHost(host_islots_);
     for (cudaEvent_t e : prof_ev_) cudaEventDestroy(e);
   }
 
@@ -491,6 +513,15 @@ class Engine {
     return r;
   }
 
+  // Device slot layout (doubles) of one cadence batch.
+  static constexpr int kSlotScrCur = 0;  // 4: primal_inf, dual_inf, pobj, penalty
+  static constexpr int kSlotScrAvg = 4;  // 4
+  static constexpr int kSlotDist = 8;    // dx2/dy2 of current, then of average
+  static constexpr int kSlotRay = 16;    // 3 candidates x 8
+  static constexpr int kSlotGap = 40;    // 2
+  static constexpr int kSlotTmp = 48;    // scratch for follow-up checks
+  static constexpr int kSlots = 64;
+
   double* slot(int i) { return slots_.get() + i; }
   // Copies slots [0, count) to the host (one sync).
   const double* read_slots(int count) {
@@ -505,11 +536,18 @@ class Engine {
     const auto t0 = Clock::now();
     const int64_t m = prob_.m, n = prob_.n;
     DevBuf<double> fr(m), fc(n);
+    DevBuf<unsigned long long> bits(std::max<int64_t>(std::max(m, n), 1));
+    const int64_t nnz = prob_.row.view.nnz;
+    DevBuf<int32_t> row_of(nnz), col_of(nnz);
+    const size_t work_bytes = pdlpk_line_of_work_bytes(nnz);
+    DevBuf<char> work(work_bytes);
+    PDLP_LAUNCH(pdlpk_line_of(&prob_.row.view, row_of.get(), work.get(), work_bytes, s()));
+    PDLP_LAUNCH(pdlpk_line_of(&prob_.col.view, col_of.get(), work.get(), work_bytes, s()));
     auto pass = [&](int one_norm) {
-      PDLP_LAUNCH(pdlpk_line_factors(&prob_.row.view, one_norm, fr.get(), s()));
-      PDLP_LAUNCH(pdlpk_line_factors(&prob_.col.view, one_norm, fc.get(), s()));
-      PDLP_LAUNCH(pdlpk_apply_factors(&prob_.row.view, prob_.row.value.get(), fr.get(), fc.get(), s()));
-      PDLP_LAUNCH(pdlpk_apply_factors(&prob_.col.view, prob_.col.value.get(), fc.get(), fr.get(), s()));
+      PDLP_LAUNCH(pdlpk_line_factors(&prob_.row.view, row_of.get(), one_norm, fr.get(), bits.get(), s()));
+      PDLP_LAUNCH(pdlpk_line_factors(&prob_.col.view, col_of.get(), one_norm, fc.get(), bits.get(), s()));
+      PDLP_LAUNCH(pdlpk_apply_factors(&prob_.row.view, row_of.get(), prob_.row.value.get(), fr.get(), fc.get(), s()));
+      PDLP_LAUNCH(pdlpk_apply_factors(&prob_.col.view, col_of.get(), prob_.col.value.get(), fc.get(), fr.get(), s()));
       PDLP_LAUNCH(pdlpk_apply_vec_factors(prob_.lc.get(), prob_.uc.get(), prob_.row_scale.get(),
                                           fr.get(), m, prob_.c.get(), prob_.lv.get(),
                                           prob_.uv.get(), prob_.col_scale.get(), fc.get(), n, s()));
@@ -690,14 +728,23 @@ class Engine {
     return screen(P, 1, x, y, D.prod_m.get(), D.prod_n.get(), rc_mode, r_out);
   }
 
+  static bool screen_passes(const InnerCfg& cfg, const Summary& s) {
+    return cfg.feasibility_only ? s.primal <= cfg.tol.eps_primal : check_termination(s, cfg.tol);
+  }
+
   // screen_and_verify (solver.hpp:207-232)
   bool screen_and_verify(const pdlpk_problem& P, const InnerCfg& cfg, const double* xs,
                          const double* ys, const double* ax_s, const double* aty_s, double* rc,
                          Summary& screened, Inner& D, const char* which) {
     screened = screen(P, 0, xs, ys, ax_s, aty_s, cfg.rc_mode, rc);
-    const bool pass = cfg.feasibility_only ? screened.primal <= cfg.tol.eps_primal
-                                           : check_termination(screened, cfg.tol);
-    if (!pass) return false;
+    if (!screen_passes(cfg, screened)) return false;
+    return verify_point(P, cfg, xs, ys, D, which);
+  }
+
+  // The verification half of screen_and_verify (solver.hpp:218-231): a
+  // genuine original-space recomputation before committing to a status.
+  bool verify_point(const pdlpk_problem& P, const InnerCfg& cfg, const double* xs,
+                    const double* ys, Inner& D, const char* which) {
     PDLP_LAUNCH(pdlpk_scale_mul(P.col_scale, xs, D.tmp_x.get(), P.n, s()));
     PDLP_LAUNCH(pdlpk_scale_mul(P.row_scale, ys, D.tmp_y.get(), P.m, s()));
     const Summary truth = original_kkt(P, D.tmp_x.get(), D.tmp_y.get(), cfg.rc_mode, D.tmp_r.get(), D);
@@ -732,8 +779,8 @@ class Engine {
     const double norm = read_slots(1)[0];
     if (!(norm > 0.0)) return false;
     PDLP_LAUNCH(pdlpk_spmv(&P.KT, orig, D.ray_m.get(), D.prod_n.get(), parity_, s()));
-    PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, orig, D.ray_m.get(), D.prod_n.get(), D.ray_n.get(), &r,
-                                        slot(0), s()));
+    PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, orig, D.ray_m.get(), D.prod_n.get(), nullptr, nullptr,
+                                        D.ray_n.get(), &r, slot(0), s()));
     const double* h = read_slots(2);
     residual = h[0];
     if (residual > eps_ray * norm) return false;
@@ -761,43 +808,86 @@ class Engine {
     return true;
   }
 
-  // detect_rays (solver.hpp:246-280)
-  std::optional<int> detect_rays(const pdlpk_problem& P, const InnerCfg& cfg, Inner& D,
-                                 bool have_avg) {
-    struct Cand {
-      const double* x;
-      const double* y;
-      const char* source;
-    };
-    std::vector<Cand> cands;
+  // Ray candidates of detect_rays (solver.hpp:246-257), in the reference's order.
+  struct RayCand {
+    const double* x;
+    const double* y;
+    const double* known_aty;  // A'y already on device (same kernel), or NULL
+    const char* source;
+  };
+
+  std::vector<RayCand> ray_candidates(const pdlpk_problem& P, Inner& D, bool have_avg) {
+    std::vector<RayCand> cands;
     const int c = D.cur();
     if (D.k() > 0) {
       PDLP_LAUNCH(pdlpk_sub(D.x[c].get(), D.x[c ^ 1].get(), D.diff_x.get(), P.n, s()));
       PDLP_LAUNCH(pdlpk_sub(D.y[c].get(), D.y[c ^ 1].get(), D.diff_y.get(), P.m, s()));
-      cands.push_back({D.diff_x.get(), D.diff_y.get(), "difference"});
+      cands.push_back({D.diff_x.get(), D.diff_y.get(), nullptr, "difference"});
     }
-    cands.push_back({D.x[c].get(), D.y[c].get(), "current"});
-    if (have_avg) cands.push_back({D.avg_x.get(), D.avg_y.get(), "average"});
-    int kind = -1;
-    const char* source = "";
-    for (const Cand& cd : cands) {
-      double res = 0.0, obj = 0.0;
-      if (try_primal(P, 0, cd.y, cfg.eps_ray, D, res, obj)) {
-        kind = PDLP_CERT_PRIMAL_INFEASIBLE;
-        source = cd.source;
-        break;
+    cands.push_back({D.x[c].get(), D.y[c].get(), D.aty[c].get(), "current"});
+    if (have_avg) cands.push_back({D.avg_x.get(), D.avg_y.get(), D.aty_avg.get(), "average"});
+    return cands;
+  }
+
+  // Enqueue the scaled-space ray tests of every candidate (no sync): slots
+  // kSlotRay + 8q hold [|ray|, changed, residual, penalty, |xc|, box, c'xc].
+  // When the cone projection leaves y unchanged the cached A'y is reused
+  // (the product kernel is skipped on device), which is bit-identical.
+  void enqueue_rays(const pdlpk_problem& P, Inner& D, const std::vector<RayCand>& cands) {
+    const pdlpk_red r = red();
+    for (size_t q = 0; q < cands.size(); ++q) {
+      double* sl = slot(kSlotRay + 8 * static_cast<int>(q));
+      double* ray = D.ray_y[q].get();
+      PDLP_LAUNCH(pdlpk_ray_primal_prep(&P, 0, cands[q].y, ray, &r, sl, s()));
+      if (cands[q].known_aty != nullptr) {
+        PDLP_LAUNCH(pdlpk_spmv_cond(&P.KT, 0, ray, D.prod_n.get(), parity_, sl + 1, s()));
+      } else {
+        PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, ray, D.prod_n.get(), parity_, s()));
       }
-      if (try_dual(P, 0, cd.x, cfg.eps_ray, D, res, obj)) {
-        kind = PDLP_CERT_DUAL_INFEASIBLE;
-        source = cd.source;
-        // keep the scaled primal ray for the verification below
-        dev_copy(D.ray_n.get(), cd.x, P.n, s());
-        break;
+      PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, 0, ray, D.prod_n.get(), cands[q].known_aty, sl + 1,
+                                          D.rhat[q].get(), &r, sl + 2, s()));
+      PDLP_LAUNCH(pdlpk_ray_dual_prep(&P, 0, cands[q].x, &r, sl + 4, s()));
+    }
+  }
+
+  // detect_rays (solver.hpp:246-280) from the batched scaled-space verdicts;
+  // h = host copy of the slots.  The first certificate wins; a hit is then
+  // re-verified on the original data.
+  std::optional<int> detect_rays(const pdlpk_problem& P, const InnerCfg& cfg, Inner& D,
+                                 const std::vector<RayCand>& cands, const double* h) {
+    int kind = -1;
+    size_t hit = 0;
+    const double eps = cfg.eps_ray;
+    for (size_t q = 0; q < cands.size() && kind < 0; ++q) {
+      const double* sl = h + kSlotRay + 8 * q;
+      const double norm = sl[0];
+      if (norm > 0.0 && !(sl[2] > eps * norm)) {
+        const double objective = -sl[3];
+        if (objective > 0.0 && std::isfinite(objective)) {
+          kind = PDLP_CERT_PRIMAL_INFEASIBLE;
+          hit = q;
+          break;
+        }
+      }
+      const double xn = sl[4], box = sl[5], obj = sl[6];
+      if (xn > 0.0 && !(box > eps * xn) && obj < 0.0) {
+        const pdlpk_red r = red();
+        PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, cands[q].x, D.prod_m.get(), parity_, s()));
+        PDLP_LAUNCH(pdlpk_ray_dual_finish(&P, 0, D.prod_m.get(), &r, slot(kSlotTmp), s()));
+        const double row = read_slots(kSlotTmp + 1)[kSlotTmp];
+        const double residual = (box < row) ? row : box;
+        if (!(residual > eps * xn)) {
+          kind = PDLP_CERT_DUAL_INFEASIBLE;
+          hit = q;
+          dev_copy(D.ray_n.get(), cands[q].x, P.n, s());
+        }
       }
     }
     if (kind < 0) return std::nullopt;
+    const char* source = cands[hit].source;
     double res = 0.0, obj = 0.0;
     if (kind == PDLP_CERT_PRIMAL_INFEASIBLE) {
+      dev_copy(D.ray_m.get(), D.ray_y[hit].get(), P.m, s());
       PDLP_LAUNCH(pdlpk_scale_mul(P.row_scale, D.ray_m.get(), D.tmp_y.get(), P.m, s()));
       if (try_primal(P, 1, D.tmp_y.get(), cfg.eps_ray, D, res, obj)) {
         D.cert.have = true;
@@ -826,15 +916,29 @@ class Engine {
     return std::nullopt;
   }
 
-  // restart_progress_metric (restarts.hpp:223-231)
-  double restart_metric(const pdlpk_problem& P, const double* x, const double* y, const double* ax,
-                        const double* aty, Inner& D, double omega) {
+  // restart_progress_metric (restarts.hpp:223-231) for up to two points at
+  // once: the radius sqrt(omega dx2 + dy2/omega) is evaluated on the host
+  // from the device-reduced distances (same IEEE operations), then each gap
+  // runs prepare -> (one sync for both event counts) -> finish -> one sync.
+  struct GapQuery {
+    const double *x, *y, *ax, *aty;
+    double dx2, dy2;
+  };
+  void gaps(const pdlpk_problem& P, const GapQuery* q, int count, double omega, double* out) {
     const pdlpk_red r = red();
-    PDLP_LAUNCH(pdlpk_diff_norm_sq(x, D.ref_x.get(), P.n, &r, slot(0), s()));
-    PDLP_LAUNCH(pdlpk_diff_norm_sq(y, D.ref_y.get(), P.m, &r, slot(1), s()));
-    PDLP_LAUNCH(pdlpk_radius(slot(0), slot(1), omega, slot(2), s()));
-    PDLP_LAUNCH(pdlpk_gap(&P, x, y, ax, aty, omega, slot(2), 0.0, &r, gap_work_.get(), slot(3), s()));
-    return read_slots(4)[3];
+    for (int i = 0; i < count; ++i) {
+      PDLP_LAUNCH(pdlpk_gap_prepare(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, &r,
+                                    gap_work_[i].get(), islots_.get() + i, s()));
+    }
+    PDLP_CK(cudaMemcpyAsync(host_islots_, islots_.get(), 8 * sizeof(int), cudaMemcpyDeviceToHost, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));
+    for (int i = 0; i < count; ++i) {
+      const double radius = std::sqrt(omega * q[i].dx2 + q[i].dy2 / omega);
+      PDLP_LAUNCH(pdlpk_gap_finish(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, nullptr, radius,
+                                   host_islots_[i], &r, gap_work_[i].get(), slot(kSlotGap + i), s()));
+    }
+    const double* h = read_slots(kSlotGap + count);
+    for (int i = 0; i < count; ++i) out[i] = h[kSlotGap + i];
   }
 
   // ---- the loop ----------------------------------------------------------
@@ -897,7 +1001,9 @@ class Engine {
   DevBuf<double> slots_;
   double* host_slots_ = nullptr;
   DevBuf<double> red_scratch_;
-  DevBuf<char> gap_work_;
+  DevBuf<char> gap_work_[2];
+  DevBuf<int> islots_;
+  int* host_islots_ = nullptr;
   DevBuf<double> zeros_n_, zeros_m_;
   DevBuf<double> sub_lc_, sub_uc_, sub_lv_, sub_uv_, sub_lc_o_, sub_uc_o_, sub_lv_o_, sub_uv_o_;
   DevBuf<double> f_down_, f_up_;
@@ -983,18 +1089,50 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
         PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.avg_x.get(), D.ax_avg.get(), parity_, s()));
         PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.avg_y.get(), D.aty_avg.get(), parity_, s()));
       }
-      if (screen_and_verify(P, cfg, D.x[c].get(), D.y[c].get(), D.ax_cur.get(), D.aty[c].get(),
-                            D.rc_a.get(), screen_cur, D, "current iterate")) {
+      // One batch, one sync: both residual screens, every ray candidate's
+      // scaled-space test, and the restart distances to the reference point.
+      // Decisions below are then taken in the reference's order.
+      const pdlpk_red rr = red();
+      PDLP_LAUNCH(pdlpk_screen(&P, 0, D.x[c].get(), D.y[c].get(), D.ax_cur.get(), D.aty[c].get(),
+                               cfg.rc_mode, &rr, D.rc_a.get(), slot(kSlotScrCur), s()));
+      if (have_avg) {
+        PDLP_LAUNCH(pdlpk_screen(&P, 0, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
+                                 D.aty_avg.get(), cfg.rc_mode, &rr, D.rc_b.get(),
+                                 slot(kSlotScrAvg), s()));
+      }
+      std::vector<RayCand> cands;
+      if (cfg.detect_infeasibility) {
+        cands = ray_candidates(P, D, have_avg);
+        enqueue_rays(P, D, cands);
+      }
+      const bool want_restart = cfg.enable_restarts && D.k() > D.k_last_restart;
+      if (want_restart) {
+        PDLP_LAUNCH(pdlpk_diff_norm_sq(D.x[c].get(), D.ref_x.get(), P.n, &rr, slot(kSlotDist), s()));
+        PDLP_LAUNCH(pdlpk_diff_norm_sq(D.y[c].get(), D.ref_y.get(), P.m, &rr, slot(kSlotDist + 1), s()));
+        if (have_avg) {
+          PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_x.get(), D.ref_x.get(), P.n, &rr, slot(kSlotDist + 2), s()));
+          PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_y.get(), D.ref_y.get(), P.m, &rr, slot(kSlotDist + 3), s()));
+        }
+      }
+      double h[kSlots];
+      std::memcpy(h, read_slots(kSlots), sizeof(h));
+      screen_cur = finish_summary(h[kSlotScrCur], h[kSlotScrCur + 1], h[kSlotScrCur + 2],
+                                  -h[kSlotScrCur + 3]);
+      if (screen_passes(cfg, screen_cur) &&
+          verify_point(P, cfg, D.x[c].get(), D.y[c].get(), D, "current iterate")) {
         return kOptimal;
       }
       Summary screen_avg;
-      if (have_avg && screen_and_verify(P, cfg, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
-                                        D.aty_avg.get(), D.rc_b.get(), screen_avg, D,
-                                        "window average")) {
-        return kOptimal;
+      if (have_avg) {
+        screen_avg = finish_summary(h[kSlotScrAvg], h[kSlotScrAvg + 1], h[kSlotScrAvg + 2],
+                                    -h[kSlotScrAvg + 3]);
+        if (screen_passes(cfg, screen_avg) &&
+            verify_point(P, cfg, D.avg_x.get(), D.avg_y.get(), D, "window average")) {
+          return kOptimal;
+        }
       }
       if (cfg.detect_infeasibility) {
-        auto st = detect_rays(P, cfg, D, have_avg);
+        auto st = detect_rays(P, cfg, D, cands, h);
         if (st.has_value()) {
           const std::string keep = D.detail;
           capture_current(P, cfg, D);
@@ -1009,31 +1147,28 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
           while (D.next_polish_trigger <= D.k()) D.next_polish_trigger *= 2;
         }
       }
-      if (cfg.enable_restarts && D.k() > D.k_last_restart) {
-        const double mu_cur = restart_metric(P, D.x[c].get(), D.y[c].get(), D.ax_cur.get(),
-                                             D.aty[c].get(), D, D.omega);
-        const double mu_avg = have_avg ? restart_metric(P, D.avg_x.get(), D.avg_y.get(),
-                                                        D.ax_avg.get(), D.aty_avg.get(), D, D.omega)
-                                       : kInf;
+      if (want_restart) {
+        // restart_progress_metric of current and average (solver.hpp:405-412)
+        GapQuery q[2] = {
+            {D.x[c].get(), D.y[c].get(), D.ax_cur.get(), D.aty[c].get(), h[kSlotDist],
+             h[kSlotDist + 1]},
+            {D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(), D.aty_avg.get(), h[kSlotDist + 2],
+             h[kSlotDist + 3]}};
+        double mu[2] = {0.0, kInf};
+        gaps(P, q, have_avg ? 2 : 1, D.omega, mu);
+        const double mu_cur = mu[0];
+        const double mu_avg = have_avg ? mu[1] : kInf;
         const bool use_current = mu_cur < mu_avg;
         const double cand_mu = use_current ? mu_cur : mu_avg;
         const int reason = should_restart(cand_mu, D.mu_last, D.prev_candidate_mu,
                                           D.k() - D.k_last_restart, D.k(), cfg.th);
         if (reason != kNone) {
-          const double* cx = use_current ? D.x[c].get() : D.avg_x.get();
-          const double* cy = use_current ? D.y[c].get() : D.avg_y.get();
-          const double* cax = use_current ? D.ax_cur.get() : D.ax_avg.get();
-          const double* caty = use_current ? D.aty[c].get() : D.aty_avg.get();
+          const GapQuery& cq = q[use_current ? 0 : 1];
           if (cfg.allow_omega_updates) {
-            const pdlpk_red r = red();
-            PDLP_LAUNCH(pdlpk_diff_norm_sq(cx, D.ref_x.get(), P.n, &r, slot(0), s()));
-            PDLP_LAUNCH(pdlpk_diff_norm_sq(cy, D.ref_y.get(), P.m, &r, slot(1), s()));
-            const double* h = read_slots(2);
-            const double dx = std::sqrt(h[0]);
-            const double dy = std::sqrt(h[1]);
-            D.omega = update_primal_weight(dx, dy, D.omega);
+            // diff_norm_sq(candidate, ref) is exactly the metric's distance
+            D.omega = update_primal_weight(std::sqrt(cq.dx2), std::sqrt(cq.dy2), D.omega);
           }
-          D.mu_last = restart_metric(P, cx, cy, cax, caty, D, D.omega);
+          gaps(P, &cq, 1, D.omega, &D.mu_last);
           if (!use_current) {
             dev_copy(D.x[c].get(), D.avg_x.get(), P.n, s());
             dev_copy(D.y[c].get(), D.avg_y.get(), P.m, s());
@@ -1475,8 +1610,13 @@ int pdlp_normalized_duality_gap(const pdlp_problem_view* problem, const double* 
     DevBuf<double> dx = to_dev(x, P.n, E.s()), dy = to_dev(y, P.m, E.s());
     DevBuf<double> dax = to_dev(ax, P.m, E.s()), daty = to_dev(aty, P.n, E.s());
     const pdlpk_red red = E.red();
-    PDLP_LAUNCH(pdlpk_gap(&P, dx.get(), dy.get(), dax.get(), daty.get(), omega, nullptr, r, &red,
-                          E.gap_work_.get(), E.slot(0), E.s()));
+    PDLP_LAUNCH(pdlpk_gap_prepare(&P, dx.get(), dy.get(), dax.get(), daty.get(), omega, &red,
+                                  E.gap_work_[0].get(), E.islots_.get(), E.s()));
+    int events = 0;
+    PDLP_CK(cudaMemcpyAsync(&events, E.islots_.get(), sizeof(int), cudaMemcpyDeviceToHost, E.s()));
+    PDLP_CK(cudaStreamSynchronize(E.s()));
+    PDLP_LAUNCH(pdlpk_gap_finish(&P, dx.get(), dy.get(), dax.get(), daty.get(), omega, nullptr, r,
+                                 events, &red, E.gap_work_[0].get(), E.slot(0), E.s()));
     *gap = E.read_slots(1)[0];
   });
 }
