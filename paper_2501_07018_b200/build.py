@@ -32,7 +32,7 @@ CU_FLAGS = ARCH + [
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-ffp-contract=off",
              f"-I{INCLUDE}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
 
-CU_SOURCES = ["k_step.cu", "k_vec.cu", "k_gap.cu", "k_scale.cu"]
+CU_SOURCES = ["k_step.cu", "k_vec.cu", "k_gap.cu", "k_scale.cu", "k_valid.cu"]
 CPP_SOURCES = ["solver.cpp"]
 HEADERS = ["common.cuh", "spmv.cuh", "reduce.cuh", "kernels.h", "device.hpp"]
 

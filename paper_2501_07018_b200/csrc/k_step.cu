@@ -61,11 +61,37 @@ __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a) {
   double* __restrict__ sx = a.sum_x;
   const int64_t n = a.P.n;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += stride) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // 128-bit accesses (every vector is a separate cudaMalloc, so 16B aligned);
+  // c, l_v, u_v are read once per pass: streaming loads.
+  const int64_t n2 = n >> 1;
+  const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
+  const double2* __restrict__ a2 = reinterpret_cast<const double2*>(aty);
+  const double2* __restrict__ c2 = reinterpret_cast<const double2*>(c);
+  const double2* __restrict__ l2 = reinterpret_cast<const double2*>(lv);
+  const double2* __restrict__ u2 = reinterpret_cast<const double2*>(uv);
+  double2* __restrict__ xn2 = reinterpret_cast<double2*>(xn);
+  double2* __restrict__ xb2 = reinterpret_cast<double2*>(xbar);
+  double2* __restrict__ sx2 = reinterpret_cast<double2*>(sx);
+  for (int64_t p = tid; p < n2; p += stride) {
+    const double2 xi = x2[p], ai = a2[p];
+    const double2 ci = __ldcs(c2 + p), li = __ldcs(l2 + p), ui = __ldcs(u2 + p);
+    double2 xp, xb;
+    xp.x = clampd(xi.x - tau * (ci.x - ai.x), li.x, ui.x);
+    xp.y = clampd(xi.y - tau * (ci.y - ai.y), li.y, ui.y);
+    xb.x = 2.0 * xp.x - xi.x;
+    xb.y = 2.0 * xp.y - xi.y;
+    xn2[p] = xp;
+    xb2[p] = xb;
+    if (pend) {
+      const double2 s = sx2[p];
+      sx2[p] = make_double2(s.x + w * xi.x, s.y + w * xi.y);
+    }
+  }
+  if ((n & 1) && tid == 0) {
+    const int64_t i = n - 1;
     const double xi = x[i];
-    const double step = xi - tau * (c[i] - aty[i]);
-    const double xp = clampd(step, lv[i], uv[i]);
+    const double xp = clampd(xi - tau * (c[i] - aty[i]), lv[i], uv[i]);
     xn[i] = xp;
     xbar[i] = 2.0 * xp - xi;
     if (pend) sx[i] = sx[i] + w * xi;
@@ -159,11 +185,9 @@ struct RowEpi {
   bool pend;
   double dy2 = 0.0, infy = 0.0;
   struct Pre {
-    double y, lc, uc, sy;
+    double y, lc, uc;
   };
-  __device__ __forceinline__ Pre load(int64_t r) const {
-    return {y[r], lc[r], uc[r], pend ? sy[r] : 0.0};
-  }
+  __device__ __forceinline__ Pre load(int64_t r) const { return {y[r], lc[r], uc[r]}; }
   __device__ __forceinline__ void line(int64_t r, double acc, const Pre& p) {
     const double yr = p.y;
     const double yhat = yr - sigma * acc;
@@ -172,14 +196,14 @@ struct RowEpi {
     yn[r] = yp;
     const double d = yp - yr;
     dy[r] = d;
-    if (pend) sy[r] = p.sy + w * yr;
+    if (pend) sy[r] = sy[r] + w * yr;
     dy2 += d * d;
     infy = max_keep(infy, fabs(yp));
   }
 };
 
 template <class P, int Seg>
-__global__ void __launch_bounds__(kSpmvThreads, 4) row_pass(pdlpk_step_args a) {
+__global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) row_pass(pdlpk_step_args a) {
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;
@@ -225,7 +249,7 @@ struct ColEpi {
 };
 
 template <class P, int Seg>
-__global__ void __launch_bounds__(kSpmvThreads, 4) col_pass(pdlpk_step_args a) {
+__global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(pdlpk_step_args a) {
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;

@@ -52,7 +52,7 @@ struct StoreEpi {
 };
 
 template <class P, int Seg>
-__global__ void __launch_bounds__(kSpmvThreads, 4) sched_spmv_kernel(pdlpk_csr A,
+__global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) sched_spmv_kernel(pdlpk_csr A,
                                                                   const double* vals,
                                                                   const double* v, double* out,
                                                                   const double* cond) {

@@ -40,14 +40,15 @@ typedef struct pdlpk_csr {
   const int32_t* med_rows; /* lines with kShortMax < len <= kMedMax, one warp each */
   int64_t n_med;
   const int32_t* tile_row0; /* first line of each warp tile of short lines */
-  const int32_t* tile_rows; /* lines in each tile (<= kTileRows) */
+  const int32_t* tile_rows; /* lines | (entries << 8) of each tile */
+  const int64_t* tile_nnz0; /* first entry of each tile (= start[tile_row0]) */
   int64_t n_tiles;
 } pdlpk_csr;
 
 /* Schedule limits (spmv.cuh) the host planner must respect. */
 #define PDLPK_SHORT_MAX 32
 #define PDLPK_MED_MAX 8192
-#define PDLPK_TILE_NNZ 512
+#define PDLPK_TILE_NNZ 256
 #define PDLPK_TILE_ROWS 64
 
 /* Device-resident step controller: one per inner loop (main / polish). */
@@ -123,6 +124,22 @@ int64_t pdlpk_step_partials(const pdlpk_problem* P);
 /* ---------------------------------------------------------------- setup --- */
 int pdlpk_index_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s);
 int pdlpk_start_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s);
+
+/* Validation (k_valid.cu; reference problem.hpp:119-154, sparse.hpp:118-133).
+ * keys[0..3] receive (first failing index << 3 | condition) for objective,
+ * variable bounds, constraint bounds and matrix values (all ones = none).
+ * Layout checks OR bits into *bad: 1 row pointers, 2 index range, 4 row line
+ * order, 8 column entry without an equal row entry, 16 per-row counts. */
+int pdlpk_validate_vectors(const double* c, const double* lv, const double* uv, int64_t n,
+                           const double* lc, const double* uc, int64_t m,
+                           const double* row_values, int64_t nnz, unsigned long long* keys,
+                           cudaStream_t s);
+int pdlpk_validate_raw_layout(const int64_t* start, int64_t dim, const int64_t* idx,
+                              int64_t count, int64_t nnz, int64_t bound, unsigned* bad,
+                              cudaStream_t s);
+int pdlpk_validate_consistency(const pdlpk_csr* R, const int32_t* row_of, const pdlpk_csr* C,
+                               const int32_t* col_of, int* row_count, unsigned* bad,
+                               cudaStream_t s);
 
 /* ----------------------------------------------------------------- step --- */
 /* Arm the controller for a run: k_target, halt = 0. */

@@ -119,6 +119,7 @@ struct DevLayout {
   DevBuf<int32_t> index;
   DevBuf<double> value, value_orig;
   DevBuf<int32_t> long_rows, med_rows, tile_row0, tile_rows;
+  DevBuf<int64_t> tile_nnz0;
   pdlpk_csr view{};
 };
 
@@ -134,11 +135,13 @@ void upload_list(const std::vector<T>& h, DevBuf<T>& d) {
 // warp each, long lines a CTA each.  O(lines) host pass over the row pointer.
 void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   std::vector<int32_t> med, lng, t0, tc;
+  std::vector<int64_t> tn;
   int64_t cur0 = -1, cur_rows = 0, cur_nnz = 0;
   auto close = [&] {
     if (cur_rows > 0) {
       t0.push_back(static_cast<int32_t>(cur0));
-      tc.push_back(static_cast<int32_t>(cur_rows));
+      tc.push_back(static_cast<int32_t>(cur_rows | (cur_nnz << 8)));
+      tn.push_back(start[cur0]);
     }
     cur0 = -1;
     cur_rows = 0;
@@ -161,6 +164,7 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   upload_list(med, L.med_rows);
   upload_list(t0, L.tile_row0);
   upload_list(tc, L.tile_rows);
+  upload_list(tn, L.tile_nnz0);
   const int64_t n_tiles = static_cast<int64_t>(t0.size());
   // 32 KB of tile smem per CTA -> 7 CTAs per SM; grid-stride over tiles.
   int64_t tb = (n_tiles + 7) / 8;
@@ -172,11 +176,16 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   L.view.n_med = static_cast<int64_t>(med.size());
   L.view.tile_row0 = L.tile_row0.get();
   L.view.tile_rows = L.tile_rows.get();
+  L.view.tile_nnz0 = L.tile_nnz0.get();
   L.view.n_tiles = n_tiles;
   L.view.tile_blocks = static_cast<int32_t>(tb);
 }
 
-void upload_layout(const pdlp_csr_view& v, DevLayout& L, cudaStream_t s) {
+// Uploads one orientation; the raw int64 row pointers and indices are checked
+// on device before the int32 conversion (bad: device flag word, see
+// k_valid.cu).  bound = the secondary dimension.
+void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayout& L,
+                   cudaStream_t s) {
   const int64_t dim = v.primary_dim, nnz = v.nnz;
   const bool wide = nnz >= (int64_t(1) << 31) - 1;
   DevBuf<int64_t> tmp;
@@ -184,10 +193,12 @@ void upload_layout(const pdlp_csr_view& v, DevLayout& L, cudaStream_t s) {
   if (wide) {
     L.start64.alloc(dim + 1);
     PDLP_CK(cudaMemcpyAsync(L.start64.get(), v.start, (dim + 1) * 8, cudaMemcpyHostToDevice, s));
+    PDLP_LAUNCH(pdlpk_validate_raw_layout(L.start64.get(), dim, nullptr, 0, nnz, bound, bad, s));
   } else {
     tmp.alloc(dim + 1);
     L.start32.alloc(dim + 1);
     PDLP_CK(cudaMemcpyAsync(tmp.get(), v.start, (dim + 1) * 8, cudaMemcpyHostToDevice, s));
+    PDLP_LAUNCH(pdlpk_validate_raw_layout(tmp.get(), dim, nullptr, 0, nnz, bound, bad, s));
     PDLP_LAUNCH(pdlpk_start_to_i32(tmp.get(), L.start32.get(), dim + 1, s));
   }
   // index (int64 -> int32) in chunks to bound the staging buffer
@@ -199,6 +210,7 @@ void upload_layout(const pdlp_csr_view& v, DevLayout& L, cudaStream_t s) {
     for (int64_t off = 0; off < nnz; off += chunk) {
       const int64_t len = std::min(chunk, nnz - off);
       PDLP_CK(cudaMemcpyAsync(tmp.get(), v.index + off, len * 8, cudaMemcpyHostToDevice, s));
+      PDLP_LAUNCH(pdlpk_validate_raw_layout(nullptr, 0, tmp.get(), len, nnz, bound, bad, s));
       PDLP_LAUNCH(pdlpk_index_to_i32(tmp.get(), L.index.get() + off, len, s));
     }
   }
@@ -273,75 +285,10 @@ struct DevProblem {
   }
 };
 
-// validate (problem.hpp:119-154), including layouts_consistent
-// (sparse.hpp:118-133) as a per-entry lookup instead of a rebuild.
-void validate(const pdlp_problem_view* p) {
-  auto fail = [](const char* msg, int64_t idx) {
-    throw InvalidProblem(std::string("invalid problem: ") + msg + " (index " +
-                         std::to_string(idx) + ")");
-  };
-  const int64_t m = p->rows, n = p->cols;
-  if (m < 0 || n < 0) fail("negative dimension", -1);
-  if (p->by_row.primary_dim != m) fail("row layout dimension != rows", -1);
-  if (p->by_col.primary_dim != n) fail("column layout dimension != cols", -1);
-  for (int64_t i = 0; i < n; ++i) {
-    if (!std::isfinite(p->objective[i])) fail("objective entry not finite", i);
-  }
-  for (int64_t i = 0; i < n; ++i) {
-    const double lo = p->var_lower[i], hi = p->var_upper[i];
-    if (std::isnan(lo) || std::isnan(hi)) fail("variable bound is NaN", i);
-    if (lo == kInf) fail("variable lower bound is +inf", i);
-    if (hi == -kInf) fail("variable upper bound is -inf", i);
-    if (lo > hi) fail("variable bounds crossed", i);
-  }
-  for (int64_t j = 0; j < m; ++j) {
-    const double lo = p->con_lower[j], hi = p->con_upper[j];
-    if (std::isnan(lo) || std::isnan(hi)) fail("constraint bound is NaN", j);
-    if (lo == kInf) fail("constraint lower bound is +inf", j);
-    if (hi == -kInf) fail("constraint upper bound is -inf", j);
-    if (lo > hi) fail("constraint bounds crossed", j);
-  }
-  const int64_t nnz = p->by_row.nnz;
-  for (int64_t k = 0; k < nnz; ++k) {
-    if (!std::isfinite(p->by_row.value[k])) fail("matrix entry not finite", k);
-  }
-  // layouts_consistent: same nnz, row lines strictly sorted, and every column
-  // entry found with an equal value in its row (a bijection since counts match
-  // and row lines are duplicate free).
-  const pdlp_csr_view& R = p->by_row;
-  const pdlp_csr_view& C = p->by_col;
-  bool consistent = R.nnz == C.nnz && R.start[0] == 0 && C.start[0] == 0 &&
-                    R.start[m] == R.nnz && C.start[n] == C.nnz;
-  std::vector<int64_t> row_count(consistent ? m : 0, 0);
-  for (int64_t r = 0; consistent && r < m; ++r) {
-    if (R.start[r + 1] < R.start[r]) consistent = false;
-    for (int64_t k = R.start[r]; consistent && k < R.start[r + 1]; ++k) {
-      if (R.index[k] < 0 || R.index[k] >= n) consistent = false;
-      if (k > R.start[r] && R.index[k] <= R.index[k - 1]) consistent = false;
-    }
-  }
-  for (int64_t c = 0; consistent && c < n; ++c) {
-    if (C.start[c + 1] < C.start[c]) {
-      consistent = false;
-      break;
-    }
-    for (int64_t k = C.start[c]; consistent && k < C.start[c + 1]; ++k) {
-      const int64_t r = C.index[k];
-      if (r < 0 || r >= m) {
-        consistent = false;
-        break;
-      }
-      const int64_t* lo = R.index + R.start[r];
-      const int64_t* hi = R.index + R.start[r + 1];
-      const int64_t* it = std::lower_bound(lo, hi, c);
-      if (it == hi || *it != c || R.value[it - R.index] != C.value[k]) consistent = false;
-      ++row_count[r];
-    }
-  }
-  for (int64_t r = 0; consistent && r < m; ++r) {
-    if (row_count[r] != R.start[r + 1] - R.start[r]) consistent = false;
-  }
-  if (!consistent) fail("row/column layouts disagree", -1);
+// Problem validation (problem.hpp:119-154, sparse.hpp:118-133) runs on device
+// inside Engine::load (k_valid.cu); the host never walks the matrix.
+[[noreturn]] void invalid(const char* msg, int64_t idx) {
+  throw InvalidProblem(std::string("invalid problem: ") + msg + " (index " + std::to_string(idx) + ")");
 }
 
 // ------------------------------------------------------------ inner state ---
@@ -448,13 +395,59 @@ class Engine {
     prob_.m = p->rows;
     prob_.n = p->cols;
     const int64_t m = p->rows, n = p->cols;
-    upload_layout(p->by_row, prob_.row, s());
-    upload_layout(p->by_col, prob_.col, s());
+    if (m < 0 || n < 0 || p->by_row.primary_dim != m || p->by_col.primary_dim != n ||
+        p->by_row.nnz != p->by_col.nnz || p->by_row.nnz < 0) {
+      invalid("row/column layouts disagree", -1);
+    }
+    DevBuf<unsigned long long> keys(4);
+    DevBuf<unsigned> bad(1);
+    PDLP_CK(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned), s()));
+    upload_layout(p->by_row, n, bad.get(), prob_.row, s());
+    upload_layout(p->by_col, m, bad.get(), prob_.col, s());
     prob_.c_o = upload_vec(p->objective, n, s());
     prob_.lc_o = upload_vec(p->con_lower, m, s());
     prob_.uc_o = upload_vec(p->con_upper, m, s());
     prob_.lv_o = upload_vec(p->var_lower, n, s());
     prob_.uv_o = upload_vec(p->var_upper, n, s());
+    // validate (problem.hpp:119-154) on device, first failure in the
+    // reference's order; layouts_consistent last.
+    PDLP_LAUNCH(pdlpk_validate_vectors(prob_.c_o.get(), prob_.lv_o.get(), prob_.uv_o.get(), n,
+                                       prob_.lc_o.get(), prob_.uc_o.get(), m,
+                                       prob_.row.value_orig.get(), prob_.row.view.nnz, keys.get(), s()));
+    {
+      unsigned long long hk[4];
+      unsigned hb = 0;
+      PDLP_CK(cudaMemcpyAsync(hk, keys.get(), sizeof(hk), cudaMemcpyDeviceToHost, s()));
+      PDLP_CK(cudaMemcpyAsync(&hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, s()));
+      PDLP_CK(cudaStreamSynchronize(s()));
+      static const char* var_msg[] = {"", "variable bound is NaN", "variable lower bound is +inf",
+                                      "variable upper bound is -inf", "variable bounds crossed"};
+      static const char* con_msg[] = {"", "constraint bound is NaN",
+                                      "constraint lower bound is +inf",
+                                      "constraint upper bound is -inf", "constraint bounds crossed"};
+      const unsigned long long none = ~0ull;
+      if (hk[0] != none) invalid("objective entry not finite", static_cast<int64_t>(hk[0] >> 3));
+      if (hk[1] != none) invalid(var_msg[hk[1] & 7], static_cast<int64_t>(hk[1] >> 3));
+      if (hk[2] != none) invalid(con_msg[hk[2] & 7], static_cast<int64_t>(hk[2] >> 3));
+      if (hk[3] != none) invalid("matrix entry not finite", static_cast<int64_t>(hk[3] >> 3));
+      if (hb != 0) invalid("row/column layouts disagree", -1);
+    }
+    {
+      const int64_t nnz = prob_.row.view.nnz;
+      row_of_.alloc(nnz);
+      col_of_.alloc(nnz);
+      const size_t work_bytes = pdlpk_line_of_work_bytes(nnz);
+      DevBuf<char> work(work_bytes);
+      PDLP_LAUNCH(pdlpk_line_of(&prob_.row.view, row_of_.get(), work.get(), work_bytes, s()));
+      PDLP_LAUNCH(pdlpk_line_of(&prob_.col.view, col_of_.get(), work.get(), work_bytes, s()));
+      DevBuf<int> row_count(std::max<int64_t>(m, 1));
+      PDLP_LAUNCH(pdlpk_validate_consistency(&prob_.row.view, row_of_.get(), &prob_.col.view,
+                                             col_of_.get(), row_count.get(), bad.get(), s()));
+      unsigned hb = 0;
+      PDLP_CK(cudaMemcpyAsync(&hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, s()));
+      PDLP_CK(cudaStreamSynchronize(s()));
+      if (hb != 0) invalid("row/column layouts disagree", -1);
+    }
     prob_.c.alloc(n);
     prob_.lc.alloc(m);
     prob_.uc.alloc(m);
@@ -467,16 +460,16 @@ class Engine {
     dev_copy(prob_.uv.get(), prob_.uv_o.get(), n, s());
     prob_.row_scale = dev_fill(m, 1.0, s());
     prob_.col_scale = dev_fill(n, 1.0, s());
-    slots_.alloc(64);
+    slots_.alloc(kSlots);
     PDLP_CK(cudaMallocHost(&host_slots_, 64 * sizeof(double)));
     red_scratch_.alloc(std::max<int64_t>(pdlpk_red_scratch_doubles(), 8 * int64_t(shards_) + 64));
-    const int64_t gap_n = std::max(n + 2 * m, m + 2 * n);
-    (void)gap_n;
     for (auto& w : gap_work_) w.alloc(std::max(pdlpk_gap_work_bytes(n, m), pdlpk_gap_work_bytes(m, n)));
     islots_.alloc(8);
     PDLP_CK(cudaMallocHost(&host_islots_, 8 * sizeof(int)));
-    zeros_n_ = dev_fill(n, 0.0, s());
-    zeros_m_ = dev_fill(m, 0.0, s());
+    zeros_n_.alloc(n);
+    zeros_m_.alloc(m);
+    dev_zero(zeros_n_.get(), n, s());
+    dev_zero(zeros_m_.get(), m, s());
     PDLP_CK(cudaStreamSynchronize(s()));
     upload_seconds_ = std::chrono::duration<double>(Clock::now() - t0).count();
   }
@@ -538,11 +531,9 @@ class Engine {
     DevBuf<double> fr(m), fc(n);
     DevBuf<unsigned long long> bits(std::max<int64_t>(std::max(m, n), 1));
     const int64_t nnz = prob_.row.view.nnz;
-    DevBuf<int32_t> row_of(nnz), col_of(nnz);
-    const size_t work_bytes = pdlpk_line_of_work_bytes(nnz);
-    DevBuf<char> work(work_bytes);
-    PDLP_LAUNCH(pdlpk_line_of(&prob_.row.view, row_of.get(), work.get(), work_bytes, s()));
-    PDLP_LAUNCH(pdlpk_line_of(&prob_.col.view, col_of.get(), work.get(), work_bytes, s()));
+    (void)nnz;
+    const DevBuf<int32_t>& row_of = row_of_;  // line maps built during validation
+    const DevBuf<int32_t>& col_of = col_of_;
     auto pass = [&](int one_norm) {
       PDLP_LAUNCH(pdlpk_line_factors(&prob_.row.view, row_of.get(), one_norm, fr.get(), bits.get(), s()));
       PDLP_LAUNCH(pdlpk_line_factors(&prob_.col.view, col_of.get(), one_norm, fc.get(), bits.get(), s()));
@@ -1005,6 +996,7 @@ class Engine {
   DevBuf<int> islots_;
   int* host_islots_ = nullptr;
   DevBuf<double> zeros_n_, zeros_m_;
+  DevBuf<int32_t> row_of_, col_of_;  // line of each entry, both layouts
   DevBuf<double> sub_lc_, sub_uc_, sub_lv_, sub_uv_, sub_lc_o_, sub_uc_o_, sub_lv_o_, sub_uv_o_;
   DevBuf<double> f_down_, f_up_;
   int64_t table_len_ = 0;
@@ -1284,8 +1276,7 @@ void copy_to_host(double* dst, const double* src, int64_t n, cudaStream_t s) {
 // solve (solver.hpp:535-608)
 void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result* res) {
   const auto t0 = Clock::now();
-  validate(problem);
-  Engine E(problem, *o);
+  Engine E(problem, *o);  // uploads and validates on device
   if (o->enable_scaling) E.precondition(o->ruiz_passes, o->pock_chambolle != 0);
   const pdlpk_problem P = E.problem().view();
 

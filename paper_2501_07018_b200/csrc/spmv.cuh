@@ -51,6 +51,10 @@ __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
   return s;
 }
 
+// Occupancy target per variant: tile variants keep a tile's index/value
+// stream in registers (ILP), so they trade one CTA per SM for it.
+__host__ __device__ constexpr int spmv_min_blocks(int seg) { return (seg & 4) ? 3 : 4; }
+
 __host__ __device__ inline int64_t sched_blocks(const pdlpk_csr& A) {
   return A.n_long + (A.n_med + kSpmvWarps - 1) / kSpmvWarps +
          ((seg_mask(A) & 4) ? A.tile_blocks : 0);
@@ -124,9 +128,38 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
   extern __shared__ double tile_smem[];
   double* sm = tile_smem + warp * kTileNnz;
   const int64_t nwarps = static_cast<int64_t>(A.tile_blocks) * kSpmvWarps;
-  for (int64_t t = b * kSpmvWarps + warp; t < A.n_tiles; t += nwarps) {
-    const int64_t r0 = A.tile_row0[t];
-    const int cnt = A.tile_rows[t];
+  int64_t t = b * kSpmvWarps + warp;
+  // Tile metadata (first line, lines | entries << 8, first entry) comes from
+  // the host schedule, so the index/value stream of a tile does not wait for
+  // its row pointers; the next tile's metadata is prefetched.
+  int64_t n_r0 = 0, n_s0 = 0;
+  int n_pack = 0;
+  if (t < A.n_tiles) {
+    n_r0 = A.tile_row0[t];
+    n_pack = A.tile_rows[t];
+    n_s0 = A.tile_nnz0[t];
+  }
+  for (; t < A.n_tiles; t += nwarps) {
+    const int64_t r0 = n_r0, s0 = n_s0;
+    const int cnt = n_pack & 0xff;
+    const int len = n_pack >> 8;
+    const int64_t tn = t + nwarps;
+    if (tn < A.n_tiles) {
+      n_r0 = A.tile_row0[tn];
+      n_pack = A.tile_rows[tn];
+      n_s0 = A.tile_nnz0[tn];
+    }
+    // index/value stream of the tile: independent of everything but s0
+    int32_t ci[kTileNnz / 32];
+    double av[kTileNnz / 32];
+#pragma unroll
+    for (int u = 0; u < kTileNnz / 32; ++u) {
+      const int j = lane + 32 * u;
+      if (j < len) {
+        ci[u] = ld_stream(idx + s0 + j);
+        av[u] = ld_stream(vals + s0 + j);
+      }
+    }
     // Line i = lane + 32q of the tile starts at rb[q]; it ends where line i+1
     // starts (lane+1's rb[q], or lane 0's rb[q+1] for lane 31), or at s1.
     int64_t rb[kTileRowsPerLane];
@@ -135,17 +168,14 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
     for (int q = 0; q < kTileRowsPerLane; ++q) {
       const int i = lane + 32 * q;
       rb[q] = i < cnt ? static_cast<int64_t>(start[r0 + i]) : 0;
-      // epilogue operands do not depend on the products: issue them now so
-      // they overlap the index -> gather chain
+      // epilogue operands do not depend on the products either
       if (i < cnt) pre[q] = epi.load(r0 + i);
     }
-    const int64_t s0 = __shfl_sync(0xffffffffu, rb[0], 0);
-    const int64_t s1 = static_cast<int64_t>(start[r0 + cnt]);
-    const int len = static_cast<int>(s1 - s0);
-#pragma unroll 4
-    for (int j = lane; j < len; j += 32) {
-      const int64_t k = s0 + j;
-      sm[j] = ld_stream(vals + k) * __ldg(v + ld_stream(idx + k));
+    const int64_t s1 = s0 + len;
+#pragma unroll
+    for (int u = 0; u < kTileNnz / 32; ++u) {
+      const int j = lane + 32 * u;
+      if (j < len) sm[j] = av[u] * __ldg(v + ci[u]);
     }
     __syncwarp();
 #pragma unroll

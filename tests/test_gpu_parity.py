@@ -349,3 +349,51 @@ def test_invalid_problem_rejected(gpu):
     q.var_upper[0] = 1.0
     with pytest.raises(ValueError, match="variable bounds crossed"):
         P.solve(q)
+
+
+def _tamper(kind):
+    p = P.generate("c0", 0, rows=40, cols=60)
+    nan = float("nan")
+    if kind == "objective":
+        p.objective[7] = nan
+    elif kind == "var_nan":
+        p.var_upper[3] = nan
+    elif kind == "var_lo_inf":
+        p.var_lower[5] = INF
+    elif kind == "var_crossed":
+        p.var_lower[9], p.var_upper[9] = 3.0, 1.0
+    elif kind == "con_hi_neginf":
+        p.con_upper[4] = -INF
+    elif kind == "con_crossed":
+        p.con_lower[11], p.con_upper[11] = 5.0, 4.0
+    elif kind == "matrix_inf":
+        p.a.by_row.value[13] = INF
+    elif kind == "layout_value":
+        p.a.by_col.value[2] += 1.0
+    elif kind == "layout_index":
+        p.a.by_row.index[0] = p.cols() + 3
+    elif kind == "layout_order":
+        L = p.a.by_row
+        r = next(r for r in range(p.rows()) if L.start[r + 1] - L.start[r] >= 2)
+        k = L.start[r]
+        L.index[k], L.index[k + 1] = L.index[k + 1], L.index[k]
+        L.value[k], L.value[k + 1] = L.value[k + 1], L.value[k]
+    elif kind == "first_of_many":
+        p.var_lower[20], p.var_upper[20] = 3.0, 1.0
+        p.var_upper[8] = nan
+        p.con_lower[2] = INF
+    return p
+
+
+@pytest.mark.parametrize("kind", ["objective", "var_nan", "var_lo_inf", "var_crossed",
+                                  "con_hi_neginf", "con_crossed", "matrix_inf", "layout_value",
+                                  "layout_index", "layout_order", "first_of_many"])
+def test_validation_messages_match_reference(gpu, ref, kind):
+    """validate (problem.hpp:119-154) runs on device; same first failure and
+    message as the reference's std::invalid_argument."""
+    p = _tamper(kind)
+    with pytest.raises(ValueError) as ours:
+        P.solve(p)
+    with pytest.raises(ValueError) as theirs:
+        ref.solve(p)
+    assert str(ours.value) == str(theirs.value)
