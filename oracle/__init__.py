@@ -254,5 +254,8 @@ def build(with_reference: bool | None = None) -> None:
         with_reference = os.path.isdir("/root/reference/proj/include")
     if with_reference:
         targets.append("ref")
+        lib = os.path.join(os.path.dirname(HERE), "paper_2501_07018_b200", "libpdlp_b200.so")
+        if os.path.exists(lib):
+            targets.append("acceptance")
     if targets:
         subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)

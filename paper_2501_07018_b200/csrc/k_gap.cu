@@ -130,7 +130,17 @@ struct Coord {
   unsigned mass_use = 0;
   double b = 0.0, c = 0.0;
   int ne = 0;
-  double lam[2], dc[2], di[2];
+  double lam0 = 0.0, dc0 = 0.0, di0 = 0.0, lam1 = 0.0, dc1 = 0.0, di1 = 0.0;
+  // events are pushed in the reference's order; fixed slots keep them in
+  // registers (a dynamically indexed array would live in local memory)
+  __device__ __forceinline__ void push(double l, double c_, double d_) {
+    if (ne == 0) {
+      lam0 = l; dc0 = c_; di0 = d_;
+    } else {
+      lam1 = l; dc1 = c_; di1 = d_;
+    }
+    ++ne;
+  }
 };
 
 __device__ __forceinline__ Coord gap_coord(const GapIn& g, int64_t t) {
@@ -145,10 +155,7 @@ __device__ __forceinline__ Coord gap_coord(const GapIn& g, int64_t t) {
     o.b = gg * gg / omega;
     o.mass_use |= 1u;
     if (finite_d(off)) {
-      o.lam[0] = gg / (omega * off);
-      o.dc[0] = omega * off * off;
-      o.di[0] = -gg * gg / omega;
-      o.ne = 1;
+      o.push(gg / (omega * off), omega * off * off, -gg * gg / omega);
     }
     return o;
   }
@@ -168,19 +175,13 @@ __device__ __forceinline__ Coord gap_coord(const GapIn& g, int64_t t) {
     if (finite_d(bp)) {
       o.b = omega * bp * bp;
       o.mass_use |= 1u;
-      o.lam[o.ne] = omega * bp / yj;
-      o.dc[o.ne] = im;
-      o.di[o.ne] = -omega * bp * bp;
-      ++o.ne;
+      o.push(omega * bp / yj, im, -omega * bp * bp);
     } else {
       o.c = im;
       o.mass_use |= 2u;
     }
     if (bm > 0.0) {
-      o.lam[o.ne] = omega * bm / yj;
-      o.dc[o.ne] = -im;
-      o.di[o.ne] = omega * bm * bm;
-      ++o.ne;
+      o.push(omega * bm / yj, -im, omega * bm * bm);
     }
   } else if (yj < 0.0) {
     if (bm >= 0.0) {
@@ -193,19 +194,13 @@ __device__ __forceinline__ Coord gap_coord(const GapIn& g, int64_t t) {
     if (finite_d(bm)) {
       o.b = omega * bm * bm;
       o.mass_use |= 1u;
-      o.lam[o.ne] = omega * bm / yj;
-      o.dc[o.ne] = im;
-      o.di[o.ne] = -omega * bm * bm;
-      ++o.ne;
+      o.push(omega * bm / yj, im, -omega * bm * bm);
     } else {
       o.c = im;
       o.mass_use |= 2u;
     }
     if (bp < 0.0) {
-      o.lam[o.ne] = omega * bp / yj;
-      o.dc[o.ne] = -im;
-      o.di[o.ne] = omega * bp * bp;
-      ++o.ne;
+      o.push(omega * bp / yj, -im, omega * bp * bp);
     }
   } else {
     if (bm > 0.0) {
@@ -229,9 +224,9 @@ __global__ void events_kernel(GapIn g, Work w) {
       const bool valid = e < o.ne;
       w.flag[s] = valid ? 1 : 0;
       if (valid) {
-        w.lam[s] = o.lam[e];
-        w.dc[s] = o.dc[e];
-        w.di[s] = o.di[e];
+        w.lam[s] = e == 0 ? o.lam0 : o.lam1;
+        w.dc[s] = e == 0 ? o.dc0 : o.dc1;
+        w.di[s] = e == 0 ? o.di0 : o.di1;
       }
     }
   }
@@ -304,14 +299,26 @@ __global__ void first_hit_kernel(Work w, int64_t E, const double* r_slot, double
   const double r = r_slot ? *r_slot : r_value;
   const double r2 = r * r;
   const double c0 = w.sc->sums[1], b0 = w.sc->sums[0];
+  unsigned long long best = ~0ull;
   GRID_STRIDE(idx, E) {
     const uint64_t key = w.keys_out[idx];
     if (idx > 0 && w.keys_out[idx - 1] == key) continue;  // not a group head
     const double lam = key_value(key);
     const double c_sum = c0 + w.cs[idx];
     const double b_sum = b0 + w.bs[idx];
-    if (c_sum + b_sum / (lam * lam) >= r2) atomicMin(&w.sc->first, static_cast<unsigned long long>(idx));
+    if (c_sum + b_sum / (lam * lam) >= r2) {
+      best = static_cast<unsigned long long>(idx);
+      break;  // grid-stride order: this thread's later hits are larger
+    }
   }
+  // min over the CTA, then one atomic (the predicate holds for a suffix of
+  // group heads, so per-hit atomics would serialize on one word)
+  __shared__ unsigned long long sbest;
+  if (threadIdx.x == 0) sbest = ~0ull;
+  __syncthreads();
+  if (best != ~0ull) atomicMin(&sbest, best);
+  __syncthreads();
+  if (threadIdx.x == 0 && sbest != ~0ull) atomicMin(&w.sc->first, sbest);
 }
 
 __global__ void finalize_perf_kernel(Work w, int64_t E, const double* r_slot, double r_value) {

@@ -40,11 +40,30 @@ __global__ void mark_heads(const P* __restrict__ start, int64_t dim, int32_t* __
   }
 }
 
+// Each thread folds a contiguous chunk of kChunk entries with a running max
+// and flushes one atomic per line segment: a 2,000-entry line costs ~60
+// atomics instead of 2,000 on the same word.
+constexpr int kChunk = 32;
+
 __global__ void absmax_kernel(const double* __restrict__ val, const int32_t* __restrict__ line_of,
                               int64_t nnz, unsigned long long* __restrict__ bits) {
-  GRID_STRIDE(k, nnz) {
-    const double a = fabs(val[k]);
-    atomicMax(bits + line_of[k], static_cast<unsigned long long>(__double_as_longlong(a)));
+  const int64_t chunks = (nnz + kChunk - 1) / kChunk;
+  GRID_STRIDE(ch, chunks) {
+    const int64_t k0 = ch * kChunk;
+    const int64_t k1 = k0 + kChunk < nnz ? k0 + kChunk : nnz;
+    int32_t line = line_of[k0];
+    unsigned long long mx = 0;
+    for (int64_t k = k0; k < k1; ++k) {
+      const int32_t l = line_of[k];
+      const unsigned long long a = static_cast<unsigned long long>(__double_as_longlong(fabs(val[k])));
+      if (l != line) {
+        atomicMax(bits + line, mx);
+        line = l;
+        mx = 0;
+      }
+      mx = a > mx ? a : mx;
+    }
+    atomicMax(bits + line, mx);
   }
 }
 
@@ -116,7 +135,9 @@ extern "C" int pdlpk_line_factors(const pdlpk_csr* A, const int32_t* line_of, in
     return static_cast<int>(cudaGetLastError());
   }
   cudaMemsetAsync(bits, 0, A->dim * sizeof(unsigned long long), s);
-  if (A->nnz > 0) absmax_kernel<<<ew_blocks(A->nnz), kT, 0, s>>>(A->value, line_of, A->nnz, bits);
+  if (A->nnz > 0) {
+    absmax_kernel<<<ew_blocks((A->nnz + kChunk - 1) / kChunk), kT, 0, s>>>(A->value, line_of, A->nnz, bits);
+  }
   factor_from_bits<<<ew_blocks(A->dim), kT, 0, s>>>(bits, A->dim, f);
   return static_cast<int>(cudaGetLastError());
 }
