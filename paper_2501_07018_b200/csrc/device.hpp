@@ -57,7 +57,9 @@ class DevBuf {
     n_ = n;
     if (n == 0) return;
     void* p = nullptr;
-    PDLP_CK(cudaMalloc(&p, n * sizeof(T)));
+    // +16 bytes: the SpMV tile path bulk-copies 16-byte-aligned windows that
+    // may extend up to 15 bytes past the last element.
+    PDLP_CK(cudaMalloc(&p, n * sizeof(T) + 16));
     p_ = static_cast<T*>(p);
   }
   void release() {

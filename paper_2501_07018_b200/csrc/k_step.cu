@@ -188,6 +188,14 @@ struct RowEpi {
     double y, lc, uc;
   };
   __device__ __forceinline__ Pre load(int64_t r) const { return {y[r], lc[r], uc[r]}; }
+  // per-line operands the tile path stages with bulk copies
+  static constexpr int kStaged = 3;
+  __device__ __forceinline__ const double* staged_src(int q) const {
+    return q == 0 ? y : (q == 1 ? lc : uc);
+  }
+  __device__ __forceinline__ Pre from_stage(const double* const* s, int li) const {
+    return {s[0][li], s[1][li], s[2][li]};
+  }
   __device__ __forceinline__ void line(int64_t r, double acc, const Pre& p) {
     const double yr = p.y;
     const double yhat = yr - sigma * acc;
@@ -239,6 +247,13 @@ struct ColEpi {
     double aty, x, xn;
   };
   __device__ __forceinline__ Pre load(int64_t i) const { return {aty[i], x[i], xn[i]}; }
+  static constexpr int kStaged = 3;
+  __device__ __forceinline__ const double* staged_src(int q) const {
+    return q == 0 ? aty : (q == 1 ? x : xn);
+  }
+  __device__ __forceinline__ Pre from_stage(const double* const* s, int li) const {
+    return {s[0][li], s[1][li], s[2][li]};
+  }
   __device__ __forceinline__ void line(int64_t i, double d, const Pre& p) {
     atyn[i] = p.aty + d;
     const double dxi = p.xn - p.x;

@@ -48,6 +48,9 @@ struct StoreEpi {
   double* out;
   struct Pre {};
   __device__ __forceinline__ Pre load(int64_t) const { return {}; }
+  static constexpr int kStaged = 0;
+  __device__ __forceinline__ const double* staged_src(int) const { return nullptr; }
+  __device__ __forceinline__ Pre from_stage(const double* const*, int) const { return {}; }
   __device__ __forceinline__ void line(int64_t r, double acc, const Pre&) { out[r] = acc; }
 };
 

@@ -48,8 +48,9 @@ typedef struct pdlpk_csr {
 /* Schedule limits (spmv.cuh) the host planner must respect. */
 #define PDLPK_SHORT_MAX 32
 #define PDLPK_MED_MAX 8192
-#define PDLPK_TILE_NNZ 256
-#define PDLPK_TILE_ROWS 64
+#define PDLPK_TILE_NNZ 512
+#define PDLPK_TILE_ROWS 224
+#define PDLPK_TILE_STAGES 3
 
 /* Device-resident step controller: one per inner loop (main / polish). */
 typedef struct pdlpk_step_state {

@@ -140,7 +140,7 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   auto close = [&] {
     if (cur_rows > 0) {
       t0.push_back(static_cast<int32_t>(cur0));
-      tc.push_back(static_cast<int32_t>(cur_rows | (cur_nnz << 8)));
+      tc.push_back(static_cast<int32_t>(cur_rows | (cur_nnz << 12)));
       tn.push_back(start[cur0]);
     }
     cur0 = -1;
@@ -166,9 +166,10 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   upload_list(tc, L.tile_rows);
   upload_list(tn, L.tile_nnz0);
   const int64_t n_tiles = static_cast<int64_t>(t0.size());
-  // 32 KB of tile smem per CTA -> 7 CTAs per SM; grid-stride over tiles.
-  int64_t tb = (n_tiles + 7) / 8;
-  tb = std::min<int64_t>(tb, 148 * 7);
+  // ~42 KB of staging ring per CTA -> 5 CTAs per SM; each CTA walks its
+  // tiles grid-stride with a two-deep bulk-copy prefetch.
+  int64_t tb = n_tiles;
+  tb = std::min<int64_t>(tb, 148 * 5);
   tb = std::max<int64_t>(tb, 1);  // the column pass's last CTA decides, so never empty
   L.view.long_rows = L.long_rows.get();
   L.view.n_long = static_cast<int64_t>(lng.size());

@@ -1,29 +1,33 @@
 // Load-balanced CSR SpMV skeleton with a fused per-line epilogue.
 //
-// One launch covers three segments of CTAs (schedule built at upload time
-// from the line lengths, see solver.cpp build_schedule):
-//   [0, n_long)                one CTA per long line    (len > kMedMax)
-//   [.., + ceil(n_med/8))      one warp per medium line (kShortMax < len <= kMedMax),
-//                              8 independent accumulator chains per lane
-//   [.., + tile_blocks)        warp tiles of consecutive short lines
-//                              (len <= kShortMax, <= kTileRows lines and
-//                              <= kTileNnz entries per tile), grid-stride
-// Tiles: the warp loads the tile's entries cooperatively (coalesced
-// index/value streams, independent gathers), stores the rounded products
-// value*x in shared memory, then each lane sums its own lines sequentially in
-// storage order.  Because every product is rounded on its own and added in
-// storage order starting from 0.0, a tiled line's sum is bit-identical to
-// the reference's `acc += value * x[idx]` (kernels.hpp:30-59).
+// One launch covers up to three segments of CTAs (schedule built once per
+// solve from the line lengths, see solver.cpp build_schedule):
+//   [0, n_long)               one CTA per long line    (len > kMedMax)
+//   [.., + ceil(n_med/8))     one warp per medium line (kShortMax < len <= kMedMax),
+//                             8 independent accumulator chains per lane
+//   [.., + tile_blocks)       CTA tiles of consecutive short lines
+//                             (len <= kShortMax; <= kTileRows lines and
+//                             <= kTileNnz entries per tile), grid-stride
 //
-// Each line's sum is produced by exactly one group with a fixed order, so
-// results are deterministic run to run.  The epilogue functor sees
-// (line, sum) once per line and accumulates its own per-thread partials.
-// Matrix entries are streamed with evict-first loads; the dense operand goes
-// through the read-only path so it stays L2-resident across the pass.
+// Tiles are fed by the TMA engine: an elected thread bulk-copies the tile's
+// contiguous streams — column indices, values, row pointers and the
+// epilogue's per-line operands — into a multi-stage shared-memory ring
+// (cp.async.bulk, completion on an mbarrier), kStages tiles ahead of the
+// consumers.  The CTA then forms the rounded products value*x[index] (the
+// only dependent global access is the gather), and each thread sums one
+// line's products in storage order.  Because every product is rounded on its
+// own and added in storage order starting from 0.0, a tiled line's sum is
+// bit-identical to the reference's `acc += value * x[idx]`
+// (kernels.hpp:30-59).
+//
+// Each line's sum is produced by exactly one thread/warp/CTA with a fixed
+// order, so results are deterministic run to run.  The epilogue functor sees
+// (line, sum, operands) once per line and accumulates its own partials.
 #pragma once
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace pdlp {
 
@@ -31,10 +35,23 @@ constexpr int kSpmvThreads = 256;
 constexpr int kSpmvWarps = kSpmvThreads / 32;
 constexpr int kShortMax = PDLPK_SHORT_MAX;  // longest tiled line
 constexpr int kMedMax = PDLPK_MED_MAX;      // longest warp-per-line line
-constexpr int kTileNnz = PDLPK_TILE_NNZ;    // entries per warp tile (4 KB of products)
-constexpr int kTileRows = PDLPK_TILE_ROWS;
-constexpr int kTileRowsPerLane = kTileRows / 32;
-constexpr size_t kSpmvSmem = sizeof(double) * kSpmvWarps * kTileNnz;  // 32 KB / CTA
+constexpr int kTileNnz = PDLPK_TILE_NNZ;    // entries per CTA tile
+constexpr int kTileRows = PDLPK_TILE_ROWS;  // lines per CTA tile
+constexpr int kMaxStaged = 3;               // epilogue operand streams per line
+constexpr int kConsumerWarps = kSpmvWarps - 1;  // warp 0 produces
+static_assert(kTileRows <= 32 * kConsumerWarps, "a consumer warp owns 32 lines of a tile");
+
+__host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+// Stage buffer: [indices | values | row pointers | staged operands...].
+constexpr size_t kStIdx = 0;
+constexpr size_t kStVal = kStIdx + align16(sizeof(int32_t) * kTileNnz + 32);
+constexpr size_t kStPtr = kStVal + align16(sizeof(double) * kTileNnz + 32);
+constexpr size_t kStEpi = kStPtr + align16(sizeof(int64_t) * (kTileRows + 1) + 32);
+constexpr size_t kStEpiStride = align16(sizeof(double) * kTileRows + 32);
+constexpr size_t kStageBytes = kStEpi + kMaxStaged * kStEpiStride;
+constexpr int kStages = PDLPK_TILE_STAGES;  // ring depth: tiles in flight per CTA
+constexpr size_t kRingHeader = 128;         // one mbarrier per stage
+constexpr size_t kSpmvSmem = kRingHeader + kStages * kStageBytes;
 
 // acc + a*b with the product rounded separately (the TU is built with
 // -fmad=false): per-term rounding identical to the reference.  No cost: the
@@ -42,22 +59,49 @@ constexpr size_t kSpmvSmem = sizeof(double) * kSpmvWarps * kTileNnz;  // 32 KB /
 __device__ __forceinline__ double mac(double acc, double a, double b) { return acc + a * b; }
 
 // Segment mask of a layout: 1 long, 2 medium, 4 tiles.  Kernels are
-// instantiated per mask so each pass only pays the registers of the paths it
-// runs.  The tile segment is kept when nothing else exists so the grid is
-// never empty (the column pass's last CTA makes the step decision).
+// instantiated per mask so each pass only pays the registers and shared
+// memory of the paths it runs.  The tile segment is kept when nothing else
+// exists so the grid is never empty (the column pass's last CTA makes the
+// step decision).
 __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
   int s = (A.n_long > 0 ? 1 : 0) | (A.n_med > 0 ? 2 : 0);
   if (A.n_tiles > 0 || s == 0) s |= 4;
   return s;
 }
 
-// Occupancy target per variant: tile variants keep a tile's index/value
-// stream in registers (ILP), so they trade one CTA per SM for it.
-__host__ __device__ constexpr int spmv_min_blocks(int seg) { return (seg & 4) ? 3 : 4; }
+__host__ __device__ constexpr int spmv_min_blocks(int seg) { return (seg & 4) ? 4 : 4; }
 
 __host__ __device__ inline int64_t sched_blocks(const pdlpk_csr& A) {
   return A.n_long + (A.n_med + kSpmvWarps - 1) / kSpmvWarps +
          ((seg_mask(A) & 4) ? A.tile_blocks : 0);
+}
+
+__host__ __device__ inline size_t spmv_smem(int seg) { return (seg & 4) ? kSpmvSmem : 0; }
+
+// 16-byte-aligned window of elements [first, first + count) of a global array.
+struct Win {
+  const char* src;
+  uint32_t bytes;
+  uint32_t shift;  // byte offset of element `first` inside the window
+};
+
+__device__ __forceinline__ Win win(const void* base, int64_t first, int64_t count, int esz) {
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(base) + static_cast<uintptr_t>(first) * esz;
+  const uintptr_t hi = lo + static_cast<uintptr_t>(count) * esz;
+  const uintptr_t alo = lo & ~uintptr_t(15);
+  const uintptr_t ahi = (hi + 15) & ~uintptr_t(15);
+  return Win{reinterpret_cast<const char*>(alo), count > 0 ? static_cast<uint32_t>(ahi - alo) : 0u,
+             static_cast<uint32_t>(lo - alo)};
+}
+
+struct TileMeta {
+  int64_t r0, s0;
+  int cnt, len;
+};
+
+__device__ __forceinline__ TileMeta tile_meta(const pdlpk_csr& A, int64_t t) {
+  const int pack = A.tile_rows[t];
+  return TileMeta{A.tile_row0[t], A.tile_nnz0[t], pack & 0xfff, pack >> 12};
 }
 
 template <class P, int Seg, class Epi>
@@ -69,129 +113,152 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
   const int warp = threadIdx.x >> 5;
   int64_t b = blockIdx.x;
   if constexpr ((Seg & 1) != 0) {
-  if (b < A.n_long) {
-    __shared__ double red_long[32];
-    const int64_t r = A.long_rows[b];
-    const int64_t lo = start[r], hi = start[r + 1];
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int64_t k = lo + threadIdx.x;
-    for (; k + 3 * kSpmvThreads < hi; k += 4 * kSpmvThreads) {
-      int32_t c[4];
-      double a[4];
+    if (b < A.n_long) {
+      __shared__ double red_long[32];
+      const int64_t r = A.long_rows[b];
+      const int64_t lo = start[r], hi = start[r + 1];
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      int64_t k = lo + threadIdx.x;
+      for (; k + 3 * kSpmvThreads < hi; k += 4 * kSpmvThreads) {
+        int32_t c[4];
+        double a[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        c[u] = ld_stream(idx + k + u * kSpmvThreads);
-        a[u] = ld_stream(vals + k + u * kSpmvThreads);
+        for (int u = 0; u < 4; ++u) {
+          c[u] = ld_stream(idx + k + u * kSpmvThreads);
+          a[u] = ld_stream(vals + k + u * kSpmvThreads);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = mac(acc[u], a[u], __ldg(v + c[u]));
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = mac(acc[u], a[u], __ldg(v + c[u]));
+      for (; k < hi; k += kSpmvThreads) acc[0] = mac(acc[0], ld_stream(vals + k), __ldg(v + ld_stream(idx + k)));
+      const double s = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), red_long);
+      if (threadIdx.x == 0) epi.line(r, s, epi.load(r));
+      return;
     }
-    for (; k < hi; k += kSpmvThreads) acc[0] = mac(acc[0], ld_stream(vals + k), __ldg(v + ld_stream(idx + k)));
-    const double s = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), red_long);
-    if (threadIdx.x == 0) epi.line(r, s, epi.load(r));
-    return;
-  }
   }
   b -= A.n_long;
   const int64_t med_blocks = (A.n_med + kSpmvWarps - 1) / kSpmvWarps;
   if constexpr ((Seg & 2) != 0) {
-  if (b < med_blocks) {
-    const int64_t w = b * kSpmvWarps + warp;
-    if (w < A.n_med) {
-      const int64_t r = A.med_rows[w];
-      typename Epi::Pre pre{};
-      if (lane == 0) pre = epi.load(r);
-      const int64_t lo = start[r], hi = start[r + 1];
-      double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      int64_t k = lo + lane;
-      for (; k + 7 * 32 < hi; k += 8 * 32) {
-        int32_t c[8];
-        double a[8];
+    if (b < med_blocks) {
+      const int64_t w = b * kSpmvWarps + warp;
+      if (w < A.n_med) {
+        const int64_t r = A.med_rows[w];
+        typename Epi::Pre pre{};
+        if (lane == 0) pre = epi.load(r);
+        const int64_t lo = start[r], hi = start[r + 1];
+        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        int64_t k = lo + lane;
+        for (; k + 7 * 32 < hi; k += 8 * 32) {
+          int32_t c[8];
+          double a[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          c[u] = ld_stream(idx + k + u * 32);
-          a[u] = ld_stream(vals + k + u * 32);
+          for (int u = 0; u < 8; ++u) {
+            c[u] = ld_stream(idx + k + u * 32);
+            a[u] = ld_stream(vals + k + u * 32);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = mac(acc[u], a[u], __ldg(v + c[u]));
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] = mac(acc[u], a[u], __ldg(v + c[u]));
+        for (; k < hi; k += 32) acc[0] = mac(acc[0], ld_stream(vals + k), __ldg(v + ld_stream(idx + k)));
+        const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        const double t = warp_sum(s);
+        if (lane == 0) epi.line(r, t, pre);
       }
-      for (; k < hi; k += 32) acc[0] = mac(acc[0], ld_stream(vals + k), __ldg(v + ld_stream(idx + k)));
-      const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      const double t = warp_sum(s);
-      if (lane == 0) epi.line(r, t, pre);
+      return;
     }
-    return;
-  }
   }
   b -= med_blocks;
-  if constexpr ((Seg & 4) == 0) return;
-  extern __shared__ double tile_smem[];
-  double* sm = tile_smem + warp * kTileNnz;
-  const int64_t nwarps = static_cast<int64_t>(A.tile_blocks) * kSpmvWarps;
-  int64_t t = b * kSpmvWarps + warp;
-  // Tile metadata (first line, lines | entries << 8, first entry) comes from
-  // the host schedule, so the index/value stream of a tile does not wait for
-  // its row pointers; the next tile's metadata is prefetched.
-  int64_t n_r0 = 0, n_s0 = 0;
-  int n_pack = 0;
-  if (t < A.n_tiles) {
-    n_r0 = A.tile_row0[t];
-    n_pack = A.tile_rows[t];
-    n_s0 = A.tile_nnz0[t];
-  }
-  for (; t < A.n_tiles; t += nwarps) {
-    const int64_t r0 = n_r0, s0 = n_s0;
-    const int cnt = n_pack & 0xff;
-    const int len = n_pack >> 8;
-    const int64_t tn = t + nwarps;
-    if (tn < A.n_tiles) {
-      n_r0 = A.tile_row0[tn];
-      n_pack = A.tile_rows[tn];
-      n_s0 = A.tile_nnz0[tn];
-    }
-    // index/value stream of the tile: independent of everything but s0
-    int32_t ci[kTileNnz / 32];
-    double av[kTileNnz / 32];
+  if constexpr ((Seg & 4) != 0) {
+    // Warp-specialized ring: warp 0 produces (one lane issues the bulk
+    // copies of a whole tile), warps 1..kConsumerWarps consume, each owning
+    // 32 consecutive lines of the tile.  full[s] completes on the copies'
+    // transaction bytes, empty[s] on one arrive per consumer warp; no CTA
+    // barrier inside the loop.
+    extern __shared__ __align__(128) unsigned char ring[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring);
+    uint64_t* empty = full + kStages;
+    unsigned char* stage0 = ring + kRingHeader;
+    const int64_t tb = A.tile_blocks;
+    if (threadIdx.x == 0) {
 #pragma unroll
-    for (int u = 0; u < kTileNnz / 32; ++u) {
-      const int j = lane + 32 * u;
-      if (j < len) {
-        ci[u] = ld_stream(idx + s0 + j);
-        av[u] = ld_stream(vals + s0 + j);
+      for (int q = 0; q < kStages; ++q) {
+        mbar_init(&full[q], 1);
+        mbar_init(&empty[q], kConsumerWarps);
+      }
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+      if (lane == 0) {
+        int i = 0;
+        for (int64_t t = b; t < A.n_tiles; t += tb, ++i) {
+          const int stage = i % kStages;
+          if (i >= kStages) mbar_wait(&empty[stage], ((i / kStages) + 1) & 1);
+          const TileMeta tm = tile_meta(A, t);
+          unsigned char* buf = stage0 + stage * kStageBytes;
+          const Win wi = win(idx, tm.s0, tm.len, 4);
+          const Win wv = win(vals, tm.s0, tm.len, 8);
+          const Win wp = win(start, tm.r0, tm.cnt + 1, static_cast<int>(sizeof(P)));
+          uint32_t total = wi.bytes + wv.bytes + wp.bytes;
+          Win we[kMaxStaged];
+#pragma unroll
+          for (int q = 0; q < Epi::kStaged; ++q) {
+            we[q] = win(epi.staged_src(q), tm.r0, tm.cnt, 8);
+            total += we[q].bytes;
+          }
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&full[stage], total);
+          if (wi.bytes) bulk_g2s(buf + kStIdx, wi.src, wi.bytes, &full[stage]);
+          if (wv.bytes) bulk_g2s(buf + kStVal, wv.src, wv.bytes, &full[stage]);
+          if (wp.bytes) bulk_g2s(buf + kStPtr, wp.src, wp.bytes, &full[stage]);
+#pragma unroll
+          for (int q = 0; q < Epi::kStaged; ++q) {
+            if (we[q].bytes) {
+              bulk_g2s(buf + kStEpi + q * kStEpiStride, we[q].src, we[q].bytes, &full[stage]);
+            }
+          }
+        }
+      }
+    } else {
+      const int cw = warp - 1;  // consumer warp: lines [32 cw, 32 cw + 32) of each tile
+      int i = 0;
+      for (int64_t t = b; t < A.n_tiles; t += tb, ++i) {
+        const int stage = i % kStages;
+        const TileMeta tm = tile_meta(A, t);
+        unsigned char* buf = stage0 + stage * kStageBytes;
+        const int32_t* s_idx =
+            reinterpret_cast<const int32_t*>(buf + kStIdx + win(idx, tm.s0, tm.len, 4).shift);
+        double* s_val = reinterpret_cast<double*>(buf + kStVal + win(vals, tm.s0, tm.len, 8).shift);
+        const P* s_ptr = reinterpret_cast<const P*>(
+            buf + kStPtr + win(start, tm.r0, tm.cnt + 1, static_cast<int>(sizeof(P))).shift);
+        const double* s_epi[kMaxStaged];
+#pragma unroll
+        for (int q = 0; q < Epi::kStaged; ++q) {
+          s_epi[q] = reinterpret_cast<const double*>(buf + kStEpi + q * kStEpiStride +
+                                                     win(epi.staged_src(q), tm.r0, tm.cnt, 8).shift);
+        }
+        const int l0 = 32 * cw;
+        mbar_wait(&full[stage], (i / kStages) & 1);
+        if (l0 < tm.cnt) {
+          const int l1 = l0 + 32 < tm.cnt ? l0 + 32 : tm.cnt;
+          const int e0 = static_cast<int>(static_cast<int64_t>(s_ptr[l0]) - tm.s0);
+          const int e1 = static_cast<int>(static_cast<int64_t>(s_ptr[l1]) - tm.s0);
+          // this warp's products in place (the gather is the only global access)
+          for (int j = e0 + lane; j < e1; j += 32) s_val[j] = s_val[j] * __ldg(v + s_idx[j]);
+          __syncwarp();
+          const int li = l0 + lane;
+          if (li < l1) {
+            const int a = static_cast<int>(static_cast<int64_t>(s_ptr[li]) - tm.s0);
+            const int e = static_cast<int>(static_cast<int64_t>(s_ptr[li + 1]) - tm.s0);
+            double acc = 0.0;
+            for (int j = a; j < e; ++j) acc += s_val[j];
+            epi.line(tm.r0 + li, acc, epi.from_stage(s_epi, li));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
       }
     }
-    // Line i = lane + 32q of the tile starts at rb[q]; it ends where line i+1
-    // starts (lane+1's rb[q], or lane 0's rb[q+1] for lane 31), or at s1.
-    int64_t rb[kTileRowsPerLane];
-    typename Epi::Pre pre[kTileRowsPerLane];
-#pragma unroll
-    for (int q = 0; q < kTileRowsPerLane; ++q) {
-      const int i = lane + 32 * q;
-      rb[q] = i < cnt ? static_cast<int64_t>(start[r0 + i]) : 0;
-      // epilogue operands do not depend on the products either
-      if (i < cnt) pre[q] = epi.load(r0 + i);
-    }
-    const int64_t s1 = s0 + len;
-#pragma unroll
-    for (int u = 0; u < kTileNnz / 32; ++u) {
-      const int j = lane + 32 * u;
-      if (j < len) sm[j] = av[u] * __ldg(v + ci[u]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < kTileRowsPerLane; ++q) {
-      const int i = lane + 32 * q;
-      const int64_t next_same = __shfl_down_sync(0xffffffffu, rb[q], 1);
-      const int64_t next_wrap =
-          __shfl_sync(0xffffffffu, q + 1 < kTileRowsPerLane ? rb[q + 1 < kTileRowsPerLane ? q + 1 : q] : 0, 0);
-      if (i < cnt) {
-        const int64_t end = (i + 1 < cnt) ? (lane < 31 ? next_same : next_wrap) : s1;
-        double acc = 0.0;
-        for (int j = static_cast<int>(rb[q] - s0); j < static_cast<int>(end - s0); ++j) acc += sm[j];
-        epi.line(r0 + i, acc, pre[q]);
-      }
-    }
-    __syncwarp();
   }
 }
 
