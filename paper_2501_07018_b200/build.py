@@ -31,6 +31,10 @@ CU_FLAGS = ARCH + [
 ]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-ffp-contract=off",
              f"-I{INCLUDE}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
+# Tuning sweeps only (e.g. PDLP_DEFINES="-DPDLPK_CHUNK=1024"); pair with --force.
+_DEFINES = os.environ.get("PDLP_DEFINES", "").split()
+CU_FLAGS += _DEFINES
+CXX_FLAGS += _DEFINES
 
 CU_SOURCES = ["k_step.cu", "k_vec.cu", "k_gap.cu", "k_scale.cu", "k_valid.cu"]
 CPP_SOURCES = ["solver.cpp"]
@@ -52,8 +56,11 @@ def _run(cmd: list[str]) -> None:
         sys.stderr.write(r.stderr)
 
 
-def build(verbose: bool = False) -> list[str]:
+def build(verbose: bool = False, force: bool = False) -> list[str]:
     os.makedirs(OBJ, exist_ok=True)
+    if force:
+        for f in os.listdir(OBJ):
+            os.remove(os.path.join(OBJ, f))
     hdr_time = max(_mtime(os.path.join(CSRC, h)) for h in HEADERS)
     hdr_time = max(hdr_time, _mtime(os.path.join(INCLUDE, "pdlp_b200.h")))
     jobs, objs = [], []
@@ -84,5 +91,5 @@ def build(verbose: bool = False) -> list[str]:
 
 
 if __name__ == "__main__":
-    for p in build(verbose="-v" in sys.argv):
+    for p in build(verbose="-v" in sys.argv, force="--force" in sys.argv):
         print(p)

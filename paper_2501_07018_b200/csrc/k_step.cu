@@ -193,6 +193,12 @@ struct RowEpi {
   __device__ __forceinline__ const double* staged_src(int q) const {
     return q == 0 ? y : (q == 1 ? lc : uc);
   }
+  // accumulators of a multi-chunk line go to its fixed slot: [dy2, infy]
+  __device__ __forceinline__ void reset_acc() { dy2 = 0.0; infy = 0.0; }
+  __device__ __forceinline__ void export_acc(double* dst) const {
+    dst[0] = dy2;
+    dst[1] = infy;
+  }
   __device__ __forceinline__ Pre from_stage(const double* const* s, int li) const {
     return {s[0][li], s[1][li], s[2][li]};
   }
@@ -251,6 +257,13 @@ struct ColEpi {
   __device__ __forceinline__ const double* staged_src(int q) const {
     return q == 0 ? aty : (q == 1 ? x : xn);
   }
+  // [dx2, curv, infx] of a multi-chunk line
+  __device__ __forceinline__ void reset_acc() { dx2 = 0.0; curv = 0.0; infx = 0.0; }
+  __device__ __forceinline__ void export_acc(double* dst) const {
+    dst[0] = dx2;
+    dst[1] = curv;
+    dst[2] = infx;
+  }
   __device__ __forceinline__ Pre from_stage(const double* const* s, int li) const {
     return {s[0][li], s[1][li], s[2][li]};
   }
@@ -304,6 +317,18 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(p
     dx2 += __ldcg(a.part3 + b);
     curv += __ldcg(a.part3 + g3 + b);
     infx = max_keep(infx, __ldcg(a.part3 + 2 * g3 + b));
+  }
+  // then the fixed slots of multi-chunk lines (spmv.cuh), in slot order
+  for (int64_t q = threadIdx.x; q < a.P.K.n_multi; q += blockDim.x) {
+    const double* s = a.P.K.line_acc + q * PDLPK_LINE_ACC;
+    dy2 += __ldcg(s);
+    infy = max_keep(infy, __ldcg(s + 1));
+  }
+  for (int64_t q = threadIdx.x; q < a.P.KT.n_multi; q += blockDim.x) {
+    const double* s = a.P.KT.line_acc + q * PDLPK_LINE_ACC;
+    dx2 += __ldcg(s);
+    curv += __ldcg(s + 1);
+    infx = max_keep(infx, __ldcg(s + 2));
   }
   dy2 = block_sum(dy2, red);
   __syncthreads();

@@ -51,6 +51,8 @@ struct StoreEpi {
   static constexpr int kStaged = 0;
   __device__ __forceinline__ const double* staged_src(int) const { return nullptr; }
   __device__ __forceinline__ Pre from_stage(const double* const*, int) const { return {}; }
+  __device__ __forceinline__ void reset_acc() {}
+  __device__ __forceinline__ void export_acc(double*) const {}
   __device__ __forceinline__ void line(int64_t r, double acc, const Pre&) { out[r] = acc; }
 };
 

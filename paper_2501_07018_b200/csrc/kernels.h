@@ -35,10 +35,22 @@ typedef struct pdlpk_csr {
   const int32_t* index;
   const double* value;      /* scaled values (the iteration matrix) */
   const double* value_orig; /* original values (verification products) */
-  const int32_t* long_rows; /* lines with len > kMedMax, one CTA each */
-  int64_t n_long;
-  const int32_t* med_rows; /* lines with kShortMax < len <= kMedMax, one warp each */
-  int64_t n_med;
+  /* Lines longer than PDLPK_SHORT_MAX are cut into chunks of at most
+   * PDLPK_CHUNK entries, one warp each.  A line's chunks are consecutive;
+   * the last-arriving warp of a multi-chunk line sums the chunk partials in
+   * chunk order and writes the line's epilogue contributions to its slot in
+   * line_acc (kept out of the per-CTA partials so the totals stay
+   * deterministic). */
+  const int32_t* chunk_row;  /* line of each chunk */
+  const int64_t* chunk_beg;  /* first entry of each chunk */
+  const int32_t* chunk_len;  /* entries of each chunk */
+  const int32_t* chunk_pos;  /* index in line | (chunks in line << 16) */
+  const int32_t* chunk_slot; /* multi-chunk line slot, -1 for single-chunk lines */
+  int64_t n_chunks;
+  int64_t n_multi;     /* multi-chunk lines */
+  double* chunk_part;  /* n_chunks partial sums */
+  unsigned* chunk_cnt; /* arrival counters, at each line's first chunk */
+  double* line_acc;    /* n_multi * PDLPK_LINE_ACC epilogue contributions */
   const int32_t* tile_row0; /* first line of each warp tile of short lines */
   const int32_t* tile_rows; /* lines | (entries << 8) of each tile */
   const int64_t* tile_nnz0; /* first entry of each tile (= start[tile_row0]) */
@@ -47,7 +59,10 @@ typedef struct pdlpk_csr {
 
 /* Schedule limits (spmv.cuh) the host planner must respect. */
 #define PDLPK_SHORT_MAX 32
-#define PDLPK_MED_MAX 8192
+#ifndef PDLPK_CHUNK
+#define PDLPK_CHUNK 2048
+#endif
+#define PDLPK_LINE_ACC 4
 #define PDLPK_TILE_NNZ 512
 #define PDLPK_TILE_ROWS 224
 #define PDLPK_TILE_STAGES 3

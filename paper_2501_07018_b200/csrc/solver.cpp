@@ -118,8 +118,10 @@ struct DevLayout {
   DevBuf<int64_t> start64;
   DevBuf<int32_t> index;
   DevBuf<double> value, value_orig;
-  DevBuf<int32_t> long_rows, med_rows, tile_row0, tile_rows;
-  DevBuf<int64_t> tile_nnz0;
+  DevBuf<int32_t> tile_row0, tile_rows, chunk_row, chunk_len, chunk_pos, chunk_slot;
+  DevBuf<int64_t> tile_nnz0, chunk_beg;
+  DevBuf<double> chunk_part, line_acc;
+  DevBuf<unsigned> chunk_cnt;
   pdlpk_csr view{};
 };
 
@@ -134,8 +136,9 @@ void upload_list(const std::vector<T>& h, DevBuf<T>& d) {
 // (<= PDLPK_TILE_ROWS lines, <= PDLPK_TILE_NNZ entries), medium lines get a
 // warp each, long lines a CTA each.  O(lines) host pass over the row pointer.
 void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
-  std::vector<int32_t> med, lng, t0, tc;
-  std::vector<int64_t> tn;
+  std::vector<int32_t> t0, tc, ck_row, ck_len, ck_pos, ck_slot;
+  std::vector<int64_t> tn, ck_beg;
+  int64_t n_multi = 0;
   int64_t cur0 = -1, cur_rows = 0, cur_nnz = 0;
   auto close = [&] {
     if (cur_rows > 0) {
@@ -150,8 +153,21 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   for (int64_t r = 0; r < dim; ++r) {
     const int64_t len = start[r + 1] - start[r];
     if (len > PDLPK_SHORT_MAX) {
+      // a long line: consecutive warp chunks of <= PDLPK_CHUNK entries
       close();
-      (len > PDLPK_MED_MAX ? lng : med).push_back(static_cast<int32_t>(r));
+      int64_t nch = (len + PDLPK_CHUNK - 1) / PDLPK_CHUNK;
+      const int64_t per = (len + nch - 1) / nch;  // balanced chunk length
+      nch = (len + per - 1) / per;
+      if (nch > 0xffff) throw std::runtime_error("line too long for the chunk schedule");
+      const int32_t slot = nch > 1 ? static_cast<int32_t>(n_multi++) : -1;
+      for (int64_t q = 0; q < nch; ++q) {
+        const int64_t b = start[r] + q * per;
+        ck_row.push_back(static_cast<int32_t>(r));
+        ck_beg.push_back(b);
+        ck_len.push_back(static_cast<int32_t>(std::min(per, start[r + 1] - b)));
+        ck_pos.push_back(static_cast<int32_t>(q | (nch << 16)));
+        ck_slot.push_back(slot);
+      }
       continue;
     }
     if (cur_rows == PDLPK_TILE_ROWS || cur_nnz + len > PDLPK_TILE_NNZ) close();
@@ -160,21 +176,35 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
     cur_nnz += len;
   }
   close();
-  upload_list(lng, L.long_rows);
-  upload_list(med, L.med_rows);
   upload_list(t0, L.tile_row0);
   upload_list(tc, L.tile_rows);
   upload_list(tn, L.tile_nnz0);
+  upload_list(ck_row, L.chunk_row);
+  upload_list(ck_beg, L.chunk_beg);
+  upload_list(ck_len, L.chunk_len);
+  upload_list(ck_pos, L.chunk_pos);
+  upload_list(ck_slot, L.chunk_slot);
+  const int64_t n_chunks = static_cast<int64_t>(ck_row.size());
+  L.chunk_part.alloc(n_chunks);
+  L.chunk_cnt.alloc(n_chunks);
+  if (n_chunks > 0) PDLP_CK(cudaMemset(L.chunk_cnt.get(), 0, n_chunks * sizeof(unsigned)));
+  L.line_acc.alloc(n_multi * PDLPK_LINE_ACC);
   const int64_t n_tiles = static_cast<int64_t>(t0.size());
-  // ~42 KB of staging ring per CTA -> 5 CTAs per SM; each CTA walks its
-  // tiles grid-stride with a two-deep bulk-copy prefetch.
+  // ~41 KB staging ring per CTA -> 5 CTAs per SM; each CTA walks its tiles
+  // grid-stride with a kStages-deep bulk-copy prefetch.
   int64_t tb = n_tiles;
   tb = std::min<int64_t>(tb, 148 * 5);
   tb = std::max<int64_t>(tb, 1);  // the column pass's last CTA decides, so never empty
-  L.view.long_rows = L.long_rows.get();
-  L.view.n_long = static_cast<int64_t>(lng.size());
-  L.view.med_rows = L.med_rows.get();
-  L.view.n_med = static_cast<int64_t>(med.size());
+  L.view.chunk_row = L.chunk_row.get();
+  L.view.chunk_beg = L.chunk_beg.get();
+  L.view.chunk_len = L.chunk_len.get();
+  L.view.chunk_pos = L.chunk_pos.get();
+  L.view.chunk_slot = L.chunk_slot.get();
+  L.view.n_chunks = n_chunks;
+  L.view.n_multi = n_multi;
+  L.view.chunk_part = L.chunk_part.get();
+  L.view.chunk_cnt = L.chunk_cnt.get();
+  L.view.line_acc = L.line_acc.get();
   L.view.tile_row0 = L.tile_row0.get();
   L.view.tile_rows = L.tile_rows.get();
   L.view.tile_nnz0 = L.tile_nnz0.get();

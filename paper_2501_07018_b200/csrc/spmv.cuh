@@ -1,13 +1,18 @@
 // Load-balanced CSR SpMV skeleton with a fused per-line epilogue.
 //
-// One launch covers up to three segments of CTAs (schedule built once per
+// One launch covers up to two segments of CTAs (schedule built once per
 // solve from the line lengths, see solver.cpp build_schedule):
-//   [0, n_long)               one CTA per long line    (len > kMedMax)
-//   [.., + ceil(n_med/8))     one warp per medium line (kShortMax < len <= kMedMax),
-//                             8 independent accumulator chains per lane
+//   [0, ceil(n_chunks/8))     one warp per chunk of a line longer than
+//                             kShortMax (chunks of <= kChunk entries, 8
+//                             independent accumulator chains per lane); the
+//                             last-arriving warp of a multi-chunk line sums the
+//                             chunk partials in chunk order (deterministic)
+//                             and runs the epilogue, whose contributions go to
+//                             the line's fixed slot (line_acc)
 //   [.., + tile_blocks)       CTA tiles of consecutive short lines
 //                             (len <= kShortMax; <= kTileRows lines and
 //                             <= kTileNnz entries per tile), grid-stride
+// Skewed (power-law) line lengths thus cost the same as uniform ones.
 //
 // Tiles are fed by the TMA engine: an elected thread bulk-copies the tile's
 // contiguous streams — column indices, values, row pointers and the
@@ -34,7 +39,7 @@ namespace pdlp {
 constexpr int kSpmvThreads = 256;
 constexpr int kSpmvWarps = kSpmvThreads / 32;
 constexpr int kShortMax = PDLPK_SHORT_MAX;  // longest tiled line
-constexpr int kMedMax = PDLPK_MED_MAX;      // longest warp-per-line line
+constexpr int kChunk = PDLPK_CHUNK;         // entries per warp chunk of a long line
 constexpr int kTileNnz = PDLPK_TILE_NNZ;    // entries per CTA tile
 constexpr int kTileRows = PDLPK_TILE_ROWS;  // lines per CTA tile
 constexpr int kMaxStaged = 3;               // epilogue operand streams per line
@@ -58,13 +63,13 @@ constexpr size_t kSpmvSmem = kRingHeader + kStages * kStageBytes;
 // pass is HBM-bound.
 __device__ __forceinline__ double mac(double acc, double a, double b) { return acc + a * b; }
 
-// Segment mask of a layout: 1 long, 2 medium, 4 tiles.  Kernels are
+// Segment mask of a layout: 1 chunks, 4 tiles.  Kernels are
 // instantiated per mask so each pass only pays the registers and shared
 // memory of the paths it runs.  The tile segment is kept when nothing else
 // exists so the grid is never empty (the column pass's last CTA makes the
 // step decision).
 __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
-  int s = (A.n_long > 0 ? 1 : 0) | (A.n_med > 0 ? 2 : 0);
+  int s = A.n_chunks > 0 ? 1 : 0;
   if (A.n_tiles > 0 || s == 0) s |= 4;
   return s;
 }
@@ -72,8 +77,7 @@ __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
 __host__ __device__ constexpr int spmv_min_blocks(int seg) { return (seg & 4) ? 4 : 4; }
 
 __host__ __device__ inline int64_t sched_blocks(const pdlpk_csr& A) {
-  return A.n_long + (A.n_med + kSpmvWarps - 1) / kSpmvWarps +
-         ((seg_mask(A) & 4) ? A.tile_blocks : 0);
+  return (A.n_chunks + kSpmvWarps - 1) / kSpmvWarps + ((seg_mask(A) & 4) ? A.tile_blocks : 0);
 }
 
 __host__ __device__ inline size_t spmv_smem(int seg) { return (seg & 4) ? kSpmvSmem : 0; }
@@ -113,61 +117,62 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
   const int warp = threadIdx.x >> 5;
   int64_t b = blockIdx.x;
   if constexpr ((Seg & 1) != 0) {
-    if (b < A.n_long) {
-      __shared__ double red_long[32];
-      const int64_t r = A.long_rows[b];
-      const int64_t lo = start[r], hi = start[r + 1];
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      int64_t k = lo + threadIdx.x;
-      for (; k + 3 * kSpmvThreads < hi; k += 4 * kSpmvThreads) {
-        int32_t c[4];
-        double a[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          c[u] = ld_stream(idx + k + u * kSpmvThreads);
-          a[u] = ld_stream(vals + k + u * kSpmvThreads);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] = mac(acc[u], a[u], __ldg(v + c[u]));
-      }
-      for (; k < hi; k += kSpmvThreads) acc[0] = mac(acc[0], ld_stream(vals + k), __ldg(v + ld_stream(idx + k)));
-      const double s = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), red_long);
-      if (threadIdx.x == 0) epi.line(r, s, epi.load(r));
-      return;
-    }
-  }
-  b -= A.n_long;
-  const int64_t med_blocks = (A.n_med + kSpmvWarps - 1) / kSpmvWarps;
-  if constexpr ((Seg & 2) != 0) {
-    if (b < med_blocks) {
-      const int64_t w = b * kSpmvWarps + warp;
-      if (w < A.n_med) {
-        const int64_t r = A.med_rows[w];
+    const int64_t chunk_blocks = (A.n_chunks + kSpmvWarps - 1) / kSpmvWarps;
+    if (b < chunk_blocks) {
+      const int64_t c = b * kSpmvWarps + warp;
+      if (c < A.n_chunks) {
+        const int64_t r = A.chunk_row[c];
+        const int64_t lo = A.chunk_beg[c];
+        const int64_t hi = lo + A.chunk_len[c];
+        const int pos = A.chunk_pos[c];
+        const int nch = pos >> 16;
         typename Epi::Pre pre{};
-        if (lane == 0) pre = epi.load(r);
-        const int64_t lo = start[r], hi = start[r + 1];
+        if (nch == 1 && lane == 0) pre = epi.load(r);
+        // predicated batches of 8 entries per lane: a chunk (<= kChunk =
+        // 8 x 32 entries) is one batch of independent loads, then its gathers
         double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        int64_t k = lo + lane;
-        for (; k + 7 * 32 < hi; k += 8 * 32) {
-          int32_t c[8];
+        for (int64_t base = lo + lane; base < hi; base += 8 * 32) {
+          int32_t ci[8];
           double a[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            c[u] = ld_stream(idx + k + u * 32);
-            a[u] = ld_stream(vals + k + u * 32);
+            const int64_t k = base + u * 32;
+            if (k < hi) {
+              ci[u] = ld_stream(idx + k);
+              a[u] = ld_stream(vals + k);
+            }
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc[u] = mac(acc[u], a[u], __ldg(v + c[u]));
+          for (int u = 0; u < 8; ++u) {
+            if (base + u * 32 < hi) acc[u] = mac(acc[u], a[u], __ldg(v + ci[u]));
+          }
         }
-        for (; k < hi; k += 32) acc[0] = mac(acc[0], ld_stream(vals + k), __ldg(v + ld_stream(idx + k)));
         const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
         const double t = warp_sum(s);
-        if (lane == 0) epi.line(r, t, pre);
+        if (nch == 1) {
+          if (lane == 0) epi.line(r, t, pre);
+        } else if (lane == 0) {
+          const int64_t c0 = c - (pos & 0xffff);
+          A.chunk_part[c] = t;
+          __threadfence();
+          const unsigned arrived = atomicAdd(A.chunk_cnt + c0, 1u);
+          if (arrived == static_cast<unsigned>(nch - 1)) {
+            __threadfence();
+            double sum = 0.0;
+            for (int q = 0; q < nch; ++q) sum += __ldcg(A.chunk_part + c0 + q);
+            A.chunk_cnt[c0] = 0;
+            // the line's epilogue contributions go to its fixed slot
+            Epi solo = epi;
+            solo.reset_acc();
+            solo.line(r, sum, solo.load(r));
+            solo.export_acc(A.line_acc + static_cast<int64_t>(A.chunk_slot[c]) * PDLPK_LINE_ACC);
+          }
+        }
       }
       return;
     }
+    b -= chunk_blocks;
   }
-  b -= med_blocks;
   if constexpr ((Seg & 4) != 0) {
     // Warp-specialized ring: warp 0 produces (one lane issues the bulk
     // copies of a whole tile), warps 1..kConsumerWarps consume, each owning
@@ -268,12 +273,8 @@ template <class P, class F>
 inline int dispatch_seg(int seg, F&& f) {
   switch (seg) {
     case 1: return f.template go<P, 1>();
-    case 2: return f.template go<P, 2>();
-    case 3: return f.template go<P, 3>();
     case 4: return f.template go<P, 4>();
-    case 5: return f.template go<P, 5>();
-    case 6: return f.template go<P, 6>();
-    default: return f.template go<P, 7>();
+    default: return f.template go<P, 5>();
   }
 }
 

@@ -110,7 +110,8 @@ def test_spmv_matches_reference(gpu, ref, mode):
 
 def test_spmv_skewed_schedule(gpu, ref):
     # C2-style power-law columns exercise the warp and CTA segments.
-    p = P.generate("c2", 3, rows=3000, cols=6000, kmax=3000)
+    p = P.generate("c2", 3, rows=5000, cols=6000, kmax=5000)
+    assert np.diff(p.a.by_col.start).max() > 2048  # > PDLPK_CHUNK: multi-chunk lines
     rng = np.random.default_rng(1)
     x = rng.uniform(-1, 1, p.cols())
     y = rng.uniform(-1, 1, p.rows())
@@ -397,3 +398,19 @@ def test_validation_messages_match_reference(gpu, ref, kind):
     with pytest.raises(ValueError) as theirs:
         ref.solve(p)
     assert str(ours.value) == str(theirs.value)
+
+
+def test_perf_mode_deterministic_on_skewed_instance(gpu, ref):
+    """Power-law columns put long lines on the chunked warp path (multi-chunk
+    lines combine partials in chunk order and write their epilogue terms to
+    fixed slots): two perf runs must be bitwise identical, and the iterates
+    must track the reference."""
+    p = P.generate("c2", 5, rows=5000, cols=6000, kmax=5000)
+    assert np.diff(p.a.by_col.start).max() > 2048  # > PDLPK_CHUNK: multi-chunk lines
+    o = _opts(iteration_limit=200, tol=(0.0, 0.0, 0.0), mode="perf")
+    a, b = P.solve(p, o), P.solve(p, o)
+    assert same_bits(a.x, b.x) and same_bits(a.y, b.y)
+    assert a.iterations == b.iterations == 200 and a.restarts == b.restarts
+    gx, gy = _trace(P.solve, p, _opts(tol=(0.0, 0.0, 0.0), mode="perf"), n_iter=30)
+    rx, ry = _trace(ref.solve, p, _opts(tol=(0.0, 0.0, 0.0)), n_iter=30)
+    assert max_rel(gx, rx) <= 1e-9 and max_rel(gy, ry) <= 1e-9
