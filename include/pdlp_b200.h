@@ -214,6 +214,10 @@ const char* pdlp_last_error(void);
 int pdlp_abi_version(void);
 /* Number of CUDA devices visible, or a negative error code. */
 int pdlp_device_count(void);
+/* B200 extension.  Solves allocate from the device's stream-ordered memory
+ * pool and keep it between calls (no map/unmap per solve); this returns the
+ * pool's unused memory on `device` to the driver.  0 or a negative error. */
+int pdlp_trim_device_memory(int device);
 
 /* ------------------------------------------------------ component entry --- *
  * Single-component entry points used by the parity tests (each runs the same

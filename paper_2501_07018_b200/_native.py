@@ -180,6 +180,7 @@ SOLVER_SIGNATURES = {
     "pdlp_last_error": (C.c_char_p, []),
     "pdlp_abi_version": (C.c_int, []),
     "pdlp_device_count": (C.c_int, []),
+    "pdlp_trim_device_memory": (C.c_int, [C.c_int]),
     "pdlp_pdhg_step": (C.c_int, [C.POINTER(ProblemView), c_double_p, c_double_p, C.c_double,
                                  C.c_double, C.c_int32, C.c_int32, c_double_p, c_double_p,
                                  c_int32_p]),

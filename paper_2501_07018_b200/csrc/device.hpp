@@ -30,6 +30,35 @@ inline void check_launch(int rc, const char* what) {
 #define PDLP_CK(expr) ::pdlp_host::check_cuda((expr), #expr)
 #define PDLP_LAUNCH(expr) ::pdlp_host::check_launch((expr), #expr)
 
+// Stream-ordered allocation.  While an Engine is alive its stream is the
+// thread's allocation stream: buffers come from the device's default memory
+// pool (cudaMallocAsync) and go back to it in stream order, so a solve neither
+// maps nor unmaps device memory once the pool is warm (the pool keeps what it
+// holds, like a caching allocator; pdlp_trim_device_memory() returns it).
+// Without an allocation stream DevBuf falls back to cudaMalloc/cudaFree.
+inline thread_local cudaStream_t g_alloc_stream = nullptr;
+
+inline void retain_pool_memory(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  PDLP_CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = ~0ull;
+  PDLP_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done[device] = true;
+}
+
+class AllocStreamScope {
+ public:
+  explicit AllocStreamScope(cudaStream_t s) : prev_(g_alloc_stream) { g_alloc_stream = s; }
+  ~AllocStreamScope() { g_alloc_stream = prev_; }
+  AllocStreamScope(const AllocStreamScope&) = delete;
+  AllocStreamScope& operator=(const AllocStreamScope&) = delete;
+
+ private:
+  cudaStream_t prev_;
+};
+
 template <class T>
 class DevBuf {
  public:
@@ -38,7 +67,7 @@ class DevBuf {
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) {
     o.p_ = nullptr;
     o.n_ = 0;
   }
@@ -47,6 +76,7 @@ class DevBuf {
       release();
       p_ = o.p_;
       n_ = o.n_;
+      s_ = o.s_;
       o.p_ = nullptr;
       o.n_ = 0;
     }
@@ -59,11 +89,22 @@ class DevBuf {
     void* p = nullptr;
     // +16 bytes: the SpMV tile path bulk-copies 16-byte-aligned windows that
     // may extend up to 15 bytes past the last element.
-    PDLP_CK(cudaMalloc(&p, n * sizeof(T) + 16));
+    s_ = g_alloc_stream;
+    if (s_ != nullptr) {
+      PDLP_CK(cudaMallocAsync(&p, n * sizeof(T) + 16, s_));
+    } else {
+      PDLP_CK(cudaMalloc(&p, n * sizeof(T) + 16));
+    }
     p_ = static_cast<T*>(p);
   }
   void release() {
-    if (p_ != nullptr) cudaFree(p_);
+    if (p_ != nullptr) {
+      if (s_ != nullptr) {
+        cudaFreeAsync(p_, s_);
+      } else {
+        cudaFree(p_);
+      }
+    }
     p_ = nullptr;
     n_ = 0;
   }
@@ -72,11 +113,13 @@ class DevBuf {
   void swap(DevBuf& o) noexcept {
     std::swap(p_, o.p_);
     std::swap(n_, o.n_);
+    std::swap(s_, o.s_);
   }
 
  private:
   T* p_ = nullptr;
   size_t n_ = 0;
+  cudaStream_t s_ = nullptr;  // allocation stream (nullptr: cudaMalloc)
 };
 
 class Stream {

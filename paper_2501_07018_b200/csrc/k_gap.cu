@@ -25,6 +25,7 @@
 // Translation unit compiled with -fmad=false (see common.cuh).
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -76,7 +77,7 @@ size_t cub_bytes_for(int64_t N) {
                                             static_cast<int32_t*>(nullptr), static_cast<int>(N));
   cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<double*>(nullptr),
                                 static_cast<double*>(nullptr), static_cast<int>(N));
-  cub::DeviceSelect::Flagged(nullptr, c, cub::CountingInputIterator<int32_t>(0),
+  cub::DeviceSelect::Flagged(nullptr, c, thrust::counting_iterator<int32_t>(0),
                              static_cast<uint8_t*>(nullptr), static_cast<int32_t*>(nullptr),
                              static_cast<int*>(nullptr), static_cast<int>(N));
   return std::max(a, std::max(b, c));
@@ -454,7 +455,7 @@ extern "C" int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const 
   if (N > 0) {
     events_kernel<<<ew_blocks(n + m), kT, 0, s>>>(g, w);
     size_t bytes = w.cub_bytes;
-    const cudaError_t e = cub::DeviceSelect::Flagged(w.cub_tmp, bytes, cub::CountingInputIterator<int32_t>(0),
+    const cudaError_t e = cub::DeviceSelect::Flagged(w.cub_tmp, bytes, thrust::counting_iterator<int32_t>(0),
                                                      w.flag, w.sel, &w.sc->num_events,
                                                      static_cast<int>(N), s);
     if (e != cudaSuccess) return static_cast<int>(e);

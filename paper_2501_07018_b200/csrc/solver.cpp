@@ -413,6 +413,8 @@ class Engine {
     shards_ = std::max(1, o.threads) * std::max(1, o.shards_per_thread);
     PDLP_CK(cudaSetDevice(o.device));
     stream_ = std::make_unique<Stream>();
+    retain_pool_memory(o.device);
+    alloc_scope_ = std::make_unique<AllocStreamScope>(stream_->get());
     load(p);
   }
 
@@ -506,6 +508,7 @@ class Engine {
   }
 
   ~Engine() {
+    alloc_scope_.reset();  // members free on their own allocation stream
     if (host_slots_ != nullptr) cudaFreeHost(host_slots_);
     if (host_islots_ != nullptr) cudaFreeHost(host_islots_);
     for (cudaEvent_t e : prof_ev_) cudaEventDestroy(e);
@@ -1018,7 +1021,8 @@ class Engine {
   pdlp_options opt_;
   bool parity_ = false;
   int shards_ = 4;
-  std::unique_ptr<Stream> stream_;
+  std::unique_ptr<Stream> stream_;  // declared first: outlives every buffer
+  std::unique_ptr<AllocStreamScope> alloc_scope_;
   DevProblem prob_;
   DevBuf<double> slots_;
   double* host_slots_ = nullptr;
@@ -1473,6 +1477,16 @@ int pdlp_solve(const pdlp_problem_view* problem, const pdlp_options* options,
 }
 
 const char* pdlp_last_error(void) { return g_last_error.c_str(); }
+
+int pdlp_trim_device_memory(int device) {
+  return guarded([&] {
+    cudaMemPool_t pool;
+    PDLP_CK(cudaSetDevice(device));
+    PDLP_CK(cudaDeviceSynchronize());
+    PDLP_CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    PDLP_CK(cudaMemPoolTrimTo(pool, 0));
+  });
+}
 
 int pdlp_abi_version(void) { return PDLP_ABI_VERSION; }
 
