@@ -1,0 +1,24 @@
+// Host -> device upload through a pinned staging ring.
+//
+// A pageable cudaMemcpyAsync moves ~5-7 GB/s: the driver copies the source
+// into its own small pinned buffers with one thread, then DMAs.  The solve's
+// inputs are ~390 MB on the bench workload (two CSR layouts with 64-bit
+// indices plus the bound vectors), so the stager does the same job with a
+// process-wide ring of pinned chunks that a pool of host threads fills in
+// parallel while the copy engine drains the previous chunks on the caller's
+// stream.  Semantics match a pageable cudaMemcpyAsync: the source has been
+// read when the call returns; the device copy completes in stream order.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+namespace pdlp_host {
+
+// Copies `bytes` from pageable host memory to device memory in stream order.
+// Small copies go straight to cudaMemcpyAsync.  Thread-safe (one upload at a
+// time through the ring).
+void stage_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
+}  // namespace pdlp_host

@@ -85,6 +85,10 @@ struct LaunchSpmv {
 };
 
 // ------------------------------------------------------------ elementwise ---
+__global__ void fill_kernel(double* x, double v, int64_t n) {
+  GRID_STRIDE(i, n) x[i] = v;
+}
+
 __global__ void sub_kernel(const double* a, const double* b, double* out, int64_t n) {
   GRID_STRIDE(i, n) out[i] = a[i] - b[i];
 }
@@ -248,6 +252,11 @@ int pdlpk_diff_norm_sq(const double* a, const double* b, int64_t n, const pdlpk_
   };
   return multi_reduce<1>(f, n, red->parity ? PDLPK_RED_SHARD : PDLPK_RED_TREE, red->shards, 0u,
                          red->scratch, slot, s);
+}
+
+int pdlpk_fill(double* x, double v, int64_t n, cudaStream_t s) {
+  if (n > 0) fill_kernel<<<ew_blocks(n), kT, 0, s>>>(x, v, n);
+  return ok();
 }
 
 int pdlpk_sub(const double* a, const double* b, double* out, int64_t n, cudaStream_t s) {

@@ -180,6 +180,7 @@ int pdlpk_spmv_cond(const pdlpk_csr* A, int32_t orig, const double* v, double* o
 int pdlpk_diff_norm_sq(const double* a, const double* b, int64_t n, const pdlpk_red* red,
                        double* slot, cudaStream_t s);
 /* out = a - b */
+int pdlpk_fill(double* x, double v, int64_t n, cudaStream_t s);
 int pdlpk_sub(const double* a, const double* b, double* out, int64_t n, cudaStream_t s);
 /* out = sum * (1/weight), weight read from the state (average_into, step.hpp:219-227). */
 int pdlpk_average_into(const pdlpk_step_state* st, const double* sum_x, const double* sum_y,

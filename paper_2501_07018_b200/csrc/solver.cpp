@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "device.hpp"
+#include "host_stage.hpp"
 #include "kernels.h"
 #include "pdlp_b200.h"
 
@@ -223,12 +224,12 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
   // start
   if (wide) {
     L.start64.alloc(dim + 1);
-    PDLP_CK(cudaMemcpyAsync(L.start64.get(), v.start, (dim + 1) * 8, cudaMemcpyHostToDevice, s));
+    stage_h2d(L.start64.get(), v.start, (dim + 1) * 8, s);
     PDLP_LAUNCH(pdlpk_validate_raw_layout(L.start64.get(), dim, nullptr, 0, nnz, bound, bad, s));
   } else {
     tmp.alloc(dim + 1);
     L.start32.alloc(dim + 1);
-    PDLP_CK(cudaMemcpyAsync(tmp.get(), v.start, (dim + 1) * 8, cudaMemcpyHostToDevice, s));
+    stage_h2d(tmp.get(), v.start, (dim + 1) * 8, s);
     PDLP_LAUNCH(pdlpk_validate_raw_layout(tmp.get(), dim, nullptr, 0, nnz, bound, bad, s));
     PDLP_LAUNCH(pdlpk_start_to_i32(tmp.get(), L.start32.get(), dim + 1, s));
   }
@@ -240,7 +241,7 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
     tmp.alloc(chunk);
     for (int64_t off = 0; off < nnz; off += chunk) {
       const int64_t len = std::min(chunk, nnz - off);
-      PDLP_CK(cudaMemcpyAsync(tmp.get(), v.index + off, len * 8, cudaMemcpyHostToDevice, s));
+      stage_h2d(tmp.get(), v.index + off, len * 8, s);
       PDLP_LAUNCH(pdlpk_validate_raw_layout(nullptr, 0, tmp.get(), len, nnz, bound, bad, s));
       PDLP_LAUNCH(pdlpk_index_to_i32(tmp.get(), L.index.get() + off, len, s));
     }
@@ -248,7 +249,7 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
   L.value_orig.alloc(nnz);
   L.value.alloc(nnz);
   if (nnz > 0) {
-    PDLP_CK(cudaMemcpyAsync(L.value_orig.get(), v.value, nnz * 8, cudaMemcpyHostToDevice, s));
+    stage_h2d(L.value_orig.get(), v.value, nnz * 8, s);
     PDLP_CK(cudaMemcpyAsync(L.value.get(), L.value_orig.get(), nnz * 8, cudaMemcpyDeviceToDevice, s));
   }
   PDLP_CK(cudaStreamSynchronize(s));
@@ -265,17 +266,13 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
 
 DevBuf<double> upload_vec(const double* h, int64_t n, cudaStream_t s) {
   DevBuf<double> d(n);
-  if (n > 0) PDLP_CK(cudaMemcpyAsync(d.get(), h, n * 8, cudaMemcpyHostToDevice, s));
+  if (n > 0) stage_h2d(d.get(), h, n * 8, s);
   return d;
 }
 
 DevBuf<double> dev_fill(int64_t n, double v, cudaStream_t s) {
   DevBuf<double> d(n);
-  if (n > 0) {
-    std::vector<double> h(n, v);
-    PDLP_CK(cudaMemcpyAsync(d.get(), h.data(), n * 8, cudaMemcpyHostToDevice, s));
-    PDLP_CK(cudaStreamSynchronize(s));
-  }
+  PDLP_LAUNCH(pdlpk_fill(d.get(), v, n, s));
   return d;
 }
 
