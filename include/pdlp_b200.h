@@ -219,6 +219,62 @@ int pdlp_device_count(void);
  * pool's unused memory on `device` to the driver.  0 or a negative error. */
 int pdlp_trim_device_memory(int device);
 
+/* ------------------------------------------------- row-sharded solve --- *
+ * B200 extension (the reference solve is single-process).
+ * `world` ranks, one GPU each: rank g owns rows [row_begin,row_end) of A in
+ * both layouts (K_g and the matching entries of K^T) and the primal block
+ * [col_begin,col_end).  Per PDHG attempt: x-bar all-gather, local K_g x-bar +
+ * dual update, local partial K_g^T dy, reduce-scatter to the column owners,
+ * and one all-gather of 5 step scalars; every rank takes the same decisions.
+ * Blocks are equal-sized (NCCL all-gather / reduce-scatter); both are even. */
+typedef struct pdlp_shard_plan {
+  int32_t rank;
+  int32_t world;
+  int64_t rows, cols;           /* m, n of the whole problem */
+  int64_t row_block, col_block; /* mb, nb */
+  int64_t row_begin, row_end;
+  int64_t col_begin, col_end;
+} pdlp_shard_plan;
+
+/* One rank's shard, host side.  rows = K_g (lines local, global column
+ * indices, pointing into the caller's by_row arrays); cols = K_g^T (all n
+ * columns, local row indices, owned by the shard). */
+typedef struct pdlp_shard_view {
+  pdlp_shard_plan plan;
+  pdlp_csr_view rows;
+  pdlp_csr_view cols;
+  const double* objective; /* col_end - col_begin */
+  const double* var_lower;
+  const double* var_upper;
+  const double* con_lower; /* row_end - row_begin */
+  const double* con_upper;
+  int64_t entry_offset; /* by_row position of K_g's first entry */
+} pdlp_shard_view;
+
+int pdlp_shard_plan_for(int64_t rows, int64_t cols, int32_t rank, int32_t world,
+                        pdlp_shard_plan* out);
+/* CPU only.  *owner keeps the shard's arrays alive; release with
+ * pdlp_shard_free.  Structural layout errors -> PDLP_ERR_INVALID_PROBLEM. */
+int pdlp_shard_extract(const pdlp_problem_view* problem, int32_t rank, int32_t world,
+                       pdlp_shard_view* out, void** owner);
+void pdlp_shard_free(void* owner);
+
+/* 128-byte ncclUniqueId for pdlp_solve_sharded (rank 0 creates it, the
+ * launcher shares it); 0 or PDLP_ERR_CUDA when libnccl is unavailable. */
+int pdlp_nccl_unique_id(unsigned char out[128]);
+/* Collective over `world` processes, one GPU each (options->device).  Every
+ * rank passes the whole problem and receives the whole result (x, y and
+ * reduced costs gathered).  Perf mode only; no observer. */
+int pdlp_solve_sharded(const pdlp_problem_view* problem, const pdlp_options* options,
+                       int32_t rank, int32_t world, const unsigned char nccl_id[128],
+                       pdlp_result* result);
+/* The same sharded program with `world` ranks as threads of this process on
+ * one GPU (collectives = host barriers + device copies, no cross-kernel
+ * waits): validates the sharded path where fewer GPUs than ranks exist.
+ * Fills `result` from rank 0. */
+int pdlp_solve_sharded_emulated(const pdlp_problem_view* problem, const pdlp_options* options,
+                                int32_t world, pdlp_result* result);
+
 /* ------------------------------------------------------ component entry --- *
  * Single-component entry points used by the parity tests (each runs the same
  * device kernels the solver uses; host arrays in, host arrays out). */

@@ -173,6 +173,35 @@ class GenParams(C.Structure):
     ]
 
 
+class ShardPlan(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+        ("rows", C.c_int64),
+        ("cols", C.c_int64),
+        ("row_block", C.c_int64),
+        ("col_block", C.c_int64),
+        ("row_begin", C.c_int64),
+        ("row_end", C.c_int64),
+        ("col_begin", C.c_int64),
+        ("col_end", C.c_int64),
+    ]
+
+
+class ShardView(C.Structure):
+    _fields_ = [
+        ("plan", ShardPlan),
+        ("rows", CsrView),
+        ("cols", CsrView),
+        ("objective", c_double_p),
+        ("var_lower", c_double_p),
+        ("var_upper", c_double_p),
+        ("con_lower", c_double_p),
+        ("con_upper", c_double_p),
+        ("entry_offset", C.c_int64),
+    ]
+
+
 # Every symbol include/pdlp_b200.h declares, with its ctypes signature.
 SOLVER_SIGNATURES = {
     "pdlp_default_options": (None, [C.POINTER(Options)]),
@@ -181,6 +210,16 @@ SOLVER_SIGNATURES = {
     "pdlp_abi_version": (C.c_int, []),
     "pdlp_device_count": (C.c_int, []),
     "pdlp_trim_device_memory": (C.c_int, [C.c_int]),
+    "pdlp_shard_plan_for": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32,
+                                      C.POINTER(ShardPlan)]),
+    "pdlp_shard_extract": (C.c_int, [C.POINTER(ProblemView), C.c_int32, C.c_int32,
+                                     C.POINTER(ShardView), C.POINTER(C.c_void_p)]),
+    "pdlp_shard_free": (None, [C.c_void_p]),
+    "pdlp_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "pdlp_solve_sharded": (C.c_int, [C.POINTER(ProblemView), C.POINTER(Options), C.c_int32,
+                                     C.c_int32, C.c_char_p, C.POINTER(Result)]),
+    "pdlp_solve_sharded_emulated": (C.c_int, [C.POINTER(ProblemView), C.POINTER(Options),
+                                              C.c_int32, C.POINTER(Result)]),
     "pdlp_pdhg_step": (C.c_int, [C.POINTER(ProblemView), c_double_p, c_double_p, C.c_double,
                                  C.c_double, C.c_int32, C.c_int32, c_double_p, c_double_p,
                                  c_int32_p]),

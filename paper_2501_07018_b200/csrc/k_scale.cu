@@ -91,6 +91,40 @@ __global__ void apply_elem(double* __restrict__ val, const int32_t* __restrict__
   GRID_STRIDE(k, nnz) val[k] = val[k] / (fp[line_of[k]] * fs[idx[k]]);
 }
 
+__global__ void bits_to_norm(const unsigned long long* __restrict__ bits, int64_t dim,
+                             double* __restrict__ norm) {
+  GRID_STRIDE(r, dim) norm[r] = __longlong_as_double(static_cast<long long>(bits[r]));
+}
+
+template <class P>
+__global__ void onenorm_kernel(const P* __restrict__ start, const double* __restrict__ val,
+                               int64_t dim, double* __restrict__ norm) {
+  GRID_STRIDE(r, dim) {
+    double a = 0.0;
+    for (int64_t k = start[r]; k < start[r + 1]; ++k) a += fabs(val[k]);
+    norm[r] = a;
+  }
+}
+
+// acc[r] continues the sequential 1-norm of line r over this layout's
+// entries (row-sharded: each rank holds one consecutive run of every column).
+template <class P>
+__global__ void onenorm_continue_kernel(const P* __restrict__ start, const double* __restrict__ val,
+                                        int64_t dim, double* __restrict__ acc) {
+  GRID_STRIDE(r, dim) {
+    double a = acc[r];
+    for (int64_t k = start[r]; k < start[r + 1]; ++k) a += fabs(val[k]);
+    acc[r] = a;
+  }
+}
+
+__global__ void norm_factor(double* __restrict__ f, int64_t n) {
+  GRID_STRIDE(r, n) {
+    const double a = f[r];
+    f[r] = a > 0.0 ? sqrt(a) : 1.0;
+  }
+}
+
 struct MaxOp {
   __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
 };
@@ -147,5 +181,42 @@ extern "C" int pdlpk_apply_factors(const pdlpk_csr* A, const int32_t* line_of, d
                                    cudaStream_t s) {
   if (A->nnz == 0) return 0;
   apply_elem<<<ew_blocks(A->nnz), kT, 0, s>>>(value, A->index, line_of, A->nnz, f_primary, f_secondary);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Row-sharded preconditioning: a rank's K^T block holds partial column norms
+// (its rows only); the engine combines them across ranks (max / sum) before
+// norm_to_factor.
+extern "C" int pdlpk_line_norms(const pdlpk_csr* A, const int32_t* line_of, int32_t one_norm,
+                                double* norm, unsigned long long* bits, cudaStream_t s) {
+  if (A->dim == 0) return 0;
+  if (one_norm) {
+    if (A->wide) {
+      onenorm_kernel<int64_t><<<ew_blocks(A->dim), kT, 0, s>>>(static_cast<const int64_t*>(A->start), A->value, A->dim, norm);
+    } else {
+      onenorm_kernel<int32_t><<<ew_blocks(A->dim), kT, 0, s>>>(static_cast<const int32_t*>(A->start), A->value, A->dim, norm);
+    }
+    return static_cast<int>(cudaGetLastError());
+  }
+  cudaMemsetAsync(bits, 0, A->dim * sizeof(unsigned long long), s);
+  if (A->nnz > 0) {
+    absmax_kernel<<<ew_blocks((A->nnz + kChunk - 1) / kChunk), kT, 0, s>>>(A->value, line_of, A->nnz, bits);
+  }
+  bits_to_norm<<<ew_blocks(A->dim), kT, 0, s>>>(bits, A->dim, norm);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_norm_to_factor(double* f, int64_t n, cudaStream_t s) {
+  if (n > 0) norm_factor<<<ew_blocks(n), kT, 0, s>>>(f, n);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_line_onenorm_continue(const pdlpk_csr* A, double* acc, cudaStream_t s) {
+  if (A->dim == 0) return 0;
+  if (A->wide) {
+    onenorm_continue_kernel<int64_t><<<ew_blocks(A->dim), kT, 0, s>>>(static_cast<const int64_t*>(A->start), A->value, A->dim, acc);
+  } else {
+    onenorm_continue_kernel<int32_t><<<ew_blocks(A->dim), kT, 0, s>>>(static_cast<const int32_t*>(A->start), A->value, A->dim, acc);
+  }
   return static_cast<int>(cudaGetLastError());
 }

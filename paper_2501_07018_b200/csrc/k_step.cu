@@ -276,7 +276,7 @@ struct ColEpi {
   }
 };
 
-template <class P, int Seg>
+template <class P, int Seg, bool Decide>
 __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(pdlpk_step_args a) {
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
@@ -299,6 +299,9 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(p
     a.part3[blockIdx.x] = s1;
     a.part3[g3 + blockIdx.x] = s2;
     a.part3[2 * g3 + blockIdx.x] = s3;
+  }
+  if (!Decide) return;  // row-sharded: the host combines ranks first
+  if (threadIdx.x == 0) {
     __threadfence();
     const unsigned t = atomicAdd(&st->ticket, 1u);
     last = (t == gridDim.x - 1);
@@ -493,6 +496,7 @@ struct LaunchRowCol {
   const pdlpk_step_args* a;
   cudaStream_t s;
   bool row;
+  bool decide_here = true;
   template <class P, int Seg>
   int go() {
     const pdlpk_csr& A = row ? a->P.K : a->P.KT;
@@ -502,11 +506,142 @@ struct LaunchRowCol {
     if (row) {
       row_pass<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
     } else {
-      col_pass<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
+      if (decide_here) {
+        col_pass<P, Seg, true><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
+      } else {
+        col_pass<P, Seg, false><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
+      }
     }
     return 0;
   }
 };
+
+// ------------------------------------------------- row-sharded attempt ---
+// Epilogues over reduce-scattered line sums (the layout's lines live on
+// other ranks' partial products), and the cross-rank decision.
+__global__ void __launch_bounds__(kEwThreads) row_epi_kernel(pdlpk_step_args a, const double* acc) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int cur = st->cur;
+  RowEpi e;
+  e.y = a.y[cur];
+  e.yn = a.y[cur ^ 1];
+  e.dy = a.dy;
+  e.lc = a.P.lc;
+  e.uc = a.P.uc;
+  e.sy = a.sum_y;
+  e.sigma = st->eta * st->omega;
+  e.pend = st->avg_pending != 0;
+  e.w = st->avg_w;
+  const int64_t m = a.P.m;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < m;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    e.line(r, acc[r], e.load(r));
+  }
+  __shared__ double red[32];
+  const double s1 = block_sum(e.dy2, red);
+  __syncthreads();
+  const double s2 = block_max(e.infy, red);
+  if (threadIdx.x == 0) {
+    a.part2[blockIdx.x] = s1;
+    a.part2[gridDim.x + blockIdx.x] = s2;
+  }
+}
+
+__global__ void __launch_bounds__(kEwThreads) col_epi_kernel(pdlpk_step_args a, const double* d) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int cur = st->cur;
+  ColEpi e;
+  e.aty = a.aty[cur];
+  e.atyn = a.aty[cur ^ 1];
+  e.x = a.x[cur];
+  e.xn = a.x[cur ^ 1];
+  const int64_t n = a.P.n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    e.line(i, d[i], e.load(i));
+  }
+  __shared__ double red[32];
+  const double s1 = block_sum(e.dx2, red);
+  __syncthreads();
+  const double s2 = block_sum(e.curv, red);
+  __syncthreads();
+  const double s3 = block_max(e.infx, red);
+  const int64_t g3 = gridDim.x;
+  if (threadIdx.x == 0) {
+    a.part3[blockIdx.x] = s1;
+    a.part3[g3 + blockIdx.x] = s2;
+    a.part3[2 * g3 + blockIdx.x] = s3;
+  }
+}
+
+// This rank's totals, combined exactly like col_pass's last CTA.
+__global__ void __launch_bounds__(kEwThreads) dist_totals_kernel(pdlpk_step_args a, int64_t g2,
+                                                                 int64_t g3, int k_acc, int kt_acc,
+                                                                 double* out) {
+  if (a.state->halt) return;
+  __shared__ double red[32];
+  double dy2 = 0.0, infy = 0.0, dx2 = 0.0, curv = 0.0, infx = 0.0;
+  for (int64_t b = threadIdx.x; b < g2; b += blockDim.x) {
+    dy2 += a.part2[b];
+    infy = max_keep(infy, a.part2[g2 + b]);
+  }
+  for (int64_t b = threadIdx.x; b < g3; b += blockDim.x) {
+    dx2 += a.part3[b];
+    curv += a.part3[g3 + b];
+    infx = max_keep(infx, a.part3[2 * g3 + b]);
+  }
+  if (k_acc) {
+    for (int64_t q = threadIdx.x; q < a.P.K.n_multi; q += blockDim.x) {
+      const double* s = a.P.K.line_acc + q * PDLPK_LINE_ACC;
+      dy2 += s[0];
+      infy = max_keep(infy, s[1]);
+    }
+  }
+  if (kt_acc) {
+    for (int64_t q = threadIdx.x; q < a.P.KT.n_multi; q += blockDim.x) {
+      const double* s = a.P.KT.line_acc + q * PDLPK_LINE_ACC;
+      dx2 += s[0];
+      curv += s[1];
+      infx = max_keep(infx, s[2]);
+    }
+  }
+  dy2 = block_sum(dy2, red);
+  __syncthreads();
+  infy = block_max(infy, red);
+  __syncthreads();
+  dx2 = block_sum(dx2, red);
+  __syncthreads();
+  curv = block_sum(curv, red);
+  __syncthreads();
+  infx = block_max(infx, red);
+  if (threadIdx.x == 0) {
+    out[0] = dy2;
+    out[1] = infy;
+    out[2] = dx2;
+    out[3] = curv;
+    out[4] = infx;
+    out[5] = out[6] = out[7] = 0.0;
+  }
+}
+
+// All ranks run this on identical gathered totals, in rank order: the
+// controllers stay bitwise identical without another exchange.
+__global__ void dist_decide_kernel(pdlpk_step_args a, const double* all, int world) {
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  double dy2 = 0.0, infy = 0.0, dx2 = 0.0, curv = 0.0, infx = 0.0;
+  for (int r = 0; r < world; ++r) {
+    const double* t = all + 8 * r;
+    dy2 += t[0];
+    infy = max_keep(infy, t[1]);
+    dx2 += t[2];
+    curv += t[3];
+    infx = max_keep(infx, t[4]);
+  }
+  decide(st, dx2, dy2, curv, infx, infy, a.f_down, a.f_up, a.table_len);
+}
 
 }  // namespace
 }  // namespace pdlp
@@ -576,5 +711,47 @@ extern "C" int pdlpk_attempt_timed(const pdlpk_step_args* a, cudaEvent_t* ev, cu
 extern "C" int pdlpk_flush_average(const pdlpk_step_args* a, cudaStream_t s) {
   flush_average_kernel<<<ew_blocks(a->P.n + a->P.m), kEwThreads, 0, s>>>(*a);
   clear_pending_kernel<<<1, 1, 0, s>>>(a->state);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// ------------------------------------------------- row-sharded attempt ---
+extern "C" int64_t pdlpk_dist_ew_grid(int64_t n) { return ew_blocks(n); }
+
+extern "C" int64_t pdlpk_dist_sched_grid(const pdlpk_csr* A) { return sched_blocks(*A); }
+
+extern "C" int pdlpk_dist_primal(const pdlpk_step_args* a, cudaStream_t s) {
+  primal_pass<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_dist_row_fused(const pdlpk_step_args* a, cudaStream_t s) {
+  dispatch_p(a->P.K, LaunchRowCol{a, s, true});
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_dist_row_epi(const pdlpk_step_args* a, const double* acc, cudaStream_t s) {
+  row_epi_kernel<<<ew_blocks(a->P.m), kEwThreads, 0, s>>>(*a, acc);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_dist_col_fused(const pdlpk_step_args* a, cudaStream_t s) {
+  dispatch_p(a->P.KT, LaunchRowCol{a, s, false, false});
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_dist_col_epi(const pdlpk_step_args* a, const double* d, cudaStream_t s) {
+  col_epi_kernel<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, d);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_dist_totals(const pdlpk_step_args* a, int64_t g2, int64_t g3, int32_t k_acc,
+                                 int32_t kt_acc, double* out8, cudaStream_t s) {
+  dist_totals_kernel<<<1, kEwThreads, 0, s>>>(*a, g2, g3, k_acc, kt_acc, out8);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_dist_decide(const pdlpk_step_args* a, const double* all8, int32_t world,
+                                 cudaStream_t s) {
+  dist_decide_kernel<<<1, 1, 0, s>>>(*a, all8, world);
   return static_cast<int>(cudaGetLastError());
 }

@@ -89,6 +89,23 @@ __global__ void fill_kernel(double* x, double v, int64_t n) {
   GRID_STRIDE(i, n) x[i] = v;
 }
 
+__global__ void combine_slots_kernel(const double* all, int world, int stride, uint64_t marked,
+                                     uint64_t maxbits, double* slots) {
+  const int i = threadIdx.x;
+  if (i >= 64 || !((marked >> i) & 1ull)) return;
+  const bool mx = (maxbits >> i) & 1ull;
+  double t = all[i];
+  for (int r = 1; r < world; ++r) {
+    const double v = all[static_cast<int64_t>(r) * stride + i];
+    t = mx ? max_keep(t, v) : t + v;
+  }
+  slots[i] = t;
+}
+
+__global__ void accumulate_kernel(double* out, const double* in, int64_t n, int use_max) {
+  GRID_STRIDE(i, n) out[i] = use_max ? max_keep(out[i], in[i]) : out[i] + in[i];
+}
+
 __global__ void sub_kernel(const double* a, const double* b, double* out, int64_t n) {
   GRID_STRIDE(i, n) out[i] = a[i] - b[i];
 }
@@ -252,6 +269,19 @@ int pdlpk_diff_norm_sq(const double* a, const double* b, int64_t n, const pdlpk_
   };
   return multi_reduce<1>(f, n, red->parity ? PDLPK_RED_SHARD : PDLPK_RED_TREE, red->shards, 0u,
                          red->scratch, slot, s);
+}
+
+void pdlpk_set_red_log(pdlpk_red_log* log) { g_red_log = log; }
+
+int pdlpk_combine_slots(const double* all, int32_t world, int32_t stride, uint64_t marked,
+                        uint64_t maxbits, double* slots, cudaStream_t s) {
+  if (marked != 0) combine_slots_kernel<<<1, 64, 0, s>>>(all, world, stride, marked, maxbits, slots);
+  return ok();
+}
+
+int pdlpk_accumulate(double* out, const double* in, int64_t n, int32_t use_max, cudaStream_t s) {
+  if (n > 0) accumulate_kernel<<<ew_blocks(n), kT, 0, s>>>(out, in, n, use_max);
+  return ok();
 }
 
 int pdlpk_fill(double* x, double v, int64_t n, cudaStream_t s) {

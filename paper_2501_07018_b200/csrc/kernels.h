@@ -55,7 +55,18 @@ typedef struct pdlpk_csr {
   const int32_t* tile_rows; /* lines | (entries << 8) of each tile */
   const int64_t* tile_nnz0; /* first entry of each tile (= start[tile_row0]) */
   int64_t n_tiles;
+  /* Row-sharded solves (solver.cpp): how a product with this
+   * layout crosses ranks.  PDLPK_DIST_GATHER: lines are local, entries index
+   * the all-gathered column-side operand.  PDLPK_DIST_PARTIAL: lines are all
+   * n columns, entries index local rows; the output is reduce-scattered to
+   * the column owners.  PDLPK_DIST_NONE on one GPU. */
+  int32_t dist_kind;
+  int32_t _pad_dist;
 } pdlpk_csr;
+
+#define PDLPK_DIST_NONE 0
+#define PDLPK_DIST_GATHER 1
+#define PDLPK_DIST_PARTIAL 2
 
 /* Schedule limits (spmv.cuh) the host planner must respect. */
 #define PDLPK_SHORT_MAX 32
@@ -136,6 +147,53 @@ typedef struct pdlpk_red {
 
 int64_t pdlpk_red_scratch_doubles(void);
 int64_t pdlpk_step_partials(const pdlpk_problem* P);
+
+/* ---- row-sharded attempt pieces (the host interleaves the collectives) ----
+ * primal:     primal_pass; xbar is written at a->xbar
+ * row_fused:  K xbar + dual update, operand a->xbar, dy written at a->dy
+ * row_epi:    dual update from reduce-scattered sums acc[m]
+ * col_fused:  K^T dy + column epilogue (no decision), operand a->dy
+ * col_epi:    column epilogue from reduce-scattered sums d[n]
+ * totals:     this rank's [dy2, infy, dx2, curv, infx] from the partials
+ *             (g2 / g3 CTAs; *_acc: add the multi-chunk line slots)
+ * decide:     combine world x 8 gathered totals in rank order, then the
+ *             accept/reject rule.  Every piece is a no-op once halted. */
+int64_t pdlpk_dist_ew_grid(int64_t n);
+int64_t pdlpk_dist_sched_grid(const pdlpk_csr* A);
+int pdlpk_dist_primal(const pdlpk_step_args* a, cudaStream_t s);
+int pdlpk_dist_row_fused(const pdlpk_step_args* a, cudaStream_t s);
+int pdlpk_dist_row_epi(const pdlpk_step_args* a, const double* acc, cudaStream_t s);
+int pdlpk_dist_col_fused(const pdlpk_step_args* a, cudaStream_t s);
+int pdlpk_dist_col_epi(const pdlpk_step_args* a, const double* d, cudaStream_t s);
+int pdlpk_dist_totals(const pdlpk_step_args* a, int64_t g2, int64_t g3, int32_t k_acc,
+                      int32_t kt_acc, double* out8, cudaStream_t s);
+int pdlpk_dist_decide(const pdlpk_step_args* a, const double* all8, int32_t world,
+                      cudaStream_t s);
+
+/* ---- cross-rank combines ----
+ * Reductions launched while a log is set on this host thread record their
+ * output (count, sum/max mask) so the engine can combine them across ranks
+ * before the host reads them. */
+typedef struct pdlpk_red_log {
+  int32_t count;
+  int32_t k[48];
+  uint32_t maxmask[48];
+  double* out[48];
+} pdlpk_red_log;
+void pdlpk_set_red_log(pdlpk_red_log* log);
+/* slots[i] for bit i of `marked` = rank-ordered sum (or max, bit i of
+ * `maxbits`) of all[r * stride + i], r < world. */
+int pdlpk_combine_slots(const double* all, int32_t world, int32_t stride, uint64_t marked,
+                        uint64_t maxbits, double* slots, cudaStream_t s);
+/* out[i] = out[i] + in[i] (or max) */
+int pdlpk_accumulate(double* out, const double* in, int64_t n, int32_t use_max, cudaStream_t s);
+/* f = sqrt(norm) where norm > 0, else 1 (rescaling.hpp:90,98,115,123) */
+int pdlpk_norm_to_factor(double* f, int64_t n, cudaStream_t s);
+/* acc[line] += sequential sum of |a| over the layout's entries of each line */
+int pdlpk_line_onenorm_continue(const pdlpk_csr* A, double* acc, cudaStream_t s);
+/* raw line norms (inf or 1) of a layout into `norm` */
+int pdlpk_line_norms(const pdlpk_csr* A, const int32_t* line_of, int32_t one_norm, double* norm,
+                     unsigned long long* bits, cudaStream_t s);
 
 /* ---------------------------------------------------------------- setup --- */
 int pdlpk_index_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s);

@@ -15,6 +15,21 @@
 namespace pdlp {
 
 constexpr int kRedThreads = 256;
+
+// Row-sharded solves: reductions launched while a log is set on this host
+// thread record where their K values went (pdlpk_set_red_log, kernels.h).
+inline thread_local pdlpk_red_log* g_red_log = nullptr;
+
+inline void red_log_record(double* out, int k, unsigned maxmask) {
+  pdlpk_red_log* L = g_red_log;
+  if (L == nullptr) return;
+  if (L->count < 48) {
+    L->k[L->count] = k;
+    L->maxmask[L->count] = maxmask;
+    L->out[L->count] = out;
+  }
+  ++L->count;  // > 48: the engine reports an overflow
+}
 constexpr int kRedMaxBlocks = 148 * 8;
 
 template <int K>
@@ -130,6 +145,7 @@ inline int multi_reduce(F f, int64_t n, int order, int shards, unsigned maxmask,
     red_tree_kernel<K><<<g, kRedThreads, 0, s>>>(f, n, maxmask, scratch);
     red_tree_final<K><<<1, kRedThreads, 0, s>>>(scratch, g, maxmask, out);
   }
+  red_log_record(out, K, maxmask);
   return static_cast<int>(cudaGetLastError());
 }
 

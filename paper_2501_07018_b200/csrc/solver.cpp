@@ -17,16 +17,20 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "device.hpp"
+#include "comm.hpp"
 #include "host_stage.hpp"
+#include "shard.hpp"
 #include "kernels.h"
 #include "pdlp_b200.h"
 
@@ -337,6 +341,7 @@ struct Inner {  // InnerState (solver.hpp:135-193), vectors on device
   DevBuf<double> ray_y[3], rhat[3];  // per ray candidate (batched cadence)
   DevBuf<pdlpk_step_state> state;
   DevBuf<double> part2, part3, shard_part;
+  DevBuf<double> pbuf, dloc, tot_all;  // sharded attempts (partial product, RS output, totals)
   pdlpk_step_state hs{};  // host mirror of the controller
 
   // Host scalars of InnerState
@@ -350,7 +355,10 @@ struct Inner {  // InnerState (solver.hpp:135-193), vectors on device
   std::string detail;
   Cert cert;
 
-  void allocate(int64_t cols, int64_t rows, int64_t partials, int shards) {
+  // full > 0 (sharded): x-bar and dy double as the gathered column-side
+  // buffers of `full` entries; block = the column block, world = ranks.
+  void allocate(int64_t cols, int64_t rows, int64_t partials, int shards, int64_t full = 0,
+                int64_t block = 0, int world = 1) {
     n = cols;
     m = rows;
     for (int b = 0; b < 2; ++b) {
@@ -377,6 +385,14 @@ struct Inner {  // InnerState (solver.hpp:135-193), vectors on device
     part2.alloc(partials);
     part3.alloc(partials);
     shard_part.alloc(5 * std::max(shards, 1));
+    if (full > 0) {
+      xbar.alloc(std::max(n, full));
+      dy.alloc(std::max(m, full));
+      pbuf.alloc(full);
+      dloc.alloc(std::max<int64_t>(block, 1));
+      tot_all.alloc(8 * static_cast<int64_t>(world));
+      PDLP_CK(cudaMemset(pbuf.get(), 0, full * sizeof(double)));
+    }
   }
   int cur() const { return hs.cur; }
   int64_t k() const { return hs.k; }
@@ -400,18 +416,30 @@ struct InnerCfg {  // InnerConfig (solver.hpp:114-133)
   void* observer_user = nullptr;
   bool logging = false;
   const char* tag = "main";
+  // sharded solves: the whole-problem view the gap runs on, and whether the
+  // problem is the swapped (dual polishing) one
+  const pdlpk_problem* full = nullptr;
+  bool swapped = false;
 };
 
 // ------------------------------------------------------------------ engine ---
 class Engine {
  public:
-  Engine(const pdlp_problem_view* p, const pdlp_options& o) : opt_(o) {
+  // comm != nullptr: one rank of a row-sharded solve; this
+  // engine then holds rows [r0,r1) of A in both layouts and the column
+  // block [c0,c1), and every product / reduction crosses ranks.
+  Engine(const pdlp_problem_view* p, const pdlp_options& o, Comm* comm = nullptr)
+      : opt_(o), comm_(comm) {
     parity_ = o.mode == PDLP_MODE_PARITY;
     shards_ = std::max(1, o.threads) * std::max(1, o.shards_per_thread);
     PDLP_CK(cudaSetDevice(o.device));
     stream_ = std::make_unique<Stream>();
     retain_pool_memory(o.device);
     alloc_scope_ = std::make_unique<AllocStreamScope>(stream_->get());
+    if (comm_ != nullptr) {
+      red_log_.count = 0;
+      pdlpk_set_red_log(&red_log_);
+    }
     load(p);
   }
 
@@ -422,23 +450,60 @@ class Engine {
   // ---- setup -------------------------------------------------------------
   void load(const pdlp_problem_view* p) {
     const auto t0 = Clock::now();
-    prob_.m = p->rows;
-    prob_.n = p->cols;
-    const int64_t m = p->rows, n = p->cols;
-    if (m < 0 || n < 0 || p->by_row.primary_dim != m || p->by_col.primary_dim != n ||
-        p->by_row.nnz != p->by_col.nnz || p->by_row.nnz < 0) {
-      invalid("row/column layouts disagree", -1);
+    if (comm_ == nullptr) {
+      m_glob_ = p->rows;
+      n_glob_ = p->cols;
+      if (m_glob_ < 0 || n_glob_ < 0 || p->by_row.primary_dim != m_glob_ ||
+          p->by_col.primary_dim != n_glob_ || p->by_row.nnz != p->by_col.nnz || p->by_row.nnz < 0) {
+        invalid("row/column layouts disagree", -1);
+      }
+      load_parts(p->by_row, p->by_col, p->rows, p->cols, p->objective, p->con_lower,
+                 p->con_upper, p->var_lower, p->var_upper, 0, 0, 0);
+    } else {
+      // Every rank sees the whole problem, so structural errors throw on
+      // every rank alike before any collective.
+      ShardData sh;
+      extract_shard(*p, comm_->rank(), comm_->world(), sh);
+      flag_.alloc(8);
+      plan_ = sh.view.plan;
+      m_glob_ = p->rows;
+      n_glob_ = p->cols;
+      const pdlp_shard_view& v = sh.view;
+      load_parts(v.rows, v.cols, plan_.row_end - plan_.row_begin, plan_.col_end - plan_.col_begin,
+                 v.objective, v.con_lower, v.con_upper, v.var_lower, v.var_upper, plan_.row_begin,
+                 plan_.col_begin, v.entry_offset);
+      prob_.row.view.dist_kind = PDLPK_DIST_GATHER;
+      prob_.col.view.dist_kind = PDLPK_DIST_PARTIAL;
+      gbuf_.alloc(full_cols());
+      pbuf_.alloc(full_cols());
+      dev_zero(gbuf_.get(), full_cols(), s());
+      dev_zero(pbuf_.get(), full_cols(), s());
+      slots_all_.alloc(static_cast<size_t>(kSlots) * comm_->world());
+      PDLP_CK(cudaStreamSynchronize(s()));
     }
+    upload_seconds_ = std::chrono::duration<double>(Clock::now() - t0).count();
+  }
+
+  // Uploads and validates the engine's part: m rows, n columns of the primal
+  // block; the row layout's entries index n_glob_ columns and the column
+  // layout has n_glob_ lines.  r0 / c0 / e0 shift reported indices to the
+  // whole problem's numbering.
+  void load_parts(const pdlp_csr_view& by_row, const pdlp_csr_view& by_col, int64_t m, int64_t n,
+                  const double* objective, const double* con_lower, const double* con_upper,
+                  const double* var_lower, const double* var_upper, int64_t r0, int64_t c0,
+                  int64_t e0) {
+    prob_.m = m;
+    prob_.n = n;
     DevBuf<unsigned long long> keys(4);
     DevBuf<unsigned> bad(1);
     PDLP_CK(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned), s()));
-    upload_layout(p->by_row, n, bad.get(), prob_.row, s());
-    upload_layout(p->by_col, m, bad.get(), prob_.col, s());
-    prob_.c_o = upload_vec(p->objective, n, s());
-    prob_.lc_o = upload_vec(p->con_lower, m, s());
-    prob_.uc_o = upload_vec(p->con_upper, m, s());
-    prob_.lv_o = upload_vec(p->var_lower, n, s());
-    prob_.uv_o = upload_vec(p->var_upper, n, s());
+    upload_layout(by_row, n_glob_, bad.get(), prob_.row, s());
+    upload_layout(by_col, m, bad.get(), prob_.col, s());
+    prob_.c_o = upload_vec(objective, n, s());
+    prob_.lc_o = upload_vec(con_lower, m, s());
+    prob_.uc_o = upload_vec(con_upper, m, s());
+    prob_.lv_o = upload_vec(var_lower, n, s());
+    prob_.uv_o = upload_vec(var_upper, n, s());
     // validate (problem.hpp:119-154) on device, first failure in the
     // reference's order; layouts_consistent last.
     PDLP_LAUNCH(pdlpk_validate_vectors(prob_.c_o.get(), prob_.lv_o.get(), prob_.uv_o.get(), n,
@@ -450,6 +515,7 @@ class Engine {
       PDLP_CK(cudaMemcpyAsync(hk, keys.get(), sizeof(hk), cudaMemcpyDeviceToHost, s()));
       PDLP_CK(cudaMemcpyAsync(&hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, s()));
       PDLP_CK(cudaStreamSynchronize(s()));
+      if (comm_ != nullptr) combine_validation(hk, hb, r0, c0, e0);
       static const char* var_msg[] = {"", "variable bound is NaN", "variable lower bound is +inf",
                                       "variable upper bound is -inf", "variable bounds crossed"};
       static const char* con_msg[] = {"", "constraint bound is NaN",
@@ -476,6 +542,7 @@ class Engine {
       unsigned hb = 0;
       PDLP_CK(cudaMemcpyAsync(&hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, s()));
       PDLP_CK(cudaStreamSynchronize(s()));
+      if (comm_ != nullptr) hb = any_rank(hb != 0) ? 1u : 0u;
       if (hb != 0) invalid("row/column layouts disagree", -1);
     }
     prob_.c.alloc(n);
@@ -493,7 +560,10 @@ class Engine {
     slots_.alloc(kSlots);
     PDLP_CK(cudaMallocHost(&host_slots_, 64 * sizeof(double)));
     red_scratch_.alloc(std::max<int64_t>(pdlpk_red_scratch_doubles(), 8 * int64_t(shards_) + 64));
-    for (auto& w : gap_work_) w.alloc(std::max(pdlpk_gap_work_bytes(n, m), pdlpk_gap_work_bytes(m, n)));
+    // the gap runs on whole vectors (gathered when sharded)
+    for (auto& w : gap_work_) {
+      w.alloc(std::max(pdlpk_gap_work_bytes(n_glob_, m_glob_), pdlpk_gap_work_bytes(m_glob_, n_glob_)));
+    }
     islots_.alloc(8);
     PDLP_CK(cudaMallocHost(&host_islots_, 8 * sizeof(int)));
     zeros_n_.alloc(n);
@@ -501,10 +571,10 @@ class Engine {
     dev_zero(zeros_n_.get(), n, s());
     dev_zero(zeros_m_.get(), m, s());
     PDLP_CK(cudaStreamSynchronize(s()));
-    upload_seconds_ = std::chrono::duration<double>(Clock::now() - t0).count();
   }
 
   ~Engine() {
+    if (comm_ != nullptr) pdlpk_set_red_log(nullptr);
     alloc_scope_.reset();  // members free on their own allocation stream
     if (host_slots_ != nullptr) cudaFreeHost(host_slots_);
     if (host_islots_ != nullptr) cudaFreeHost(host_islots_);
@@ -537,6 +607,198 @@ class Engine {
     return r;
   }
 
+  // ---- row-sharded plumbing (comm_ != nullptr) ---------------------------
+  bool dist() const { return comm_ != nullptr; }
+  int64_t full_cols() const { return plan_.col_block * comm_->world(); }
+  int64_t full_rows() const { return plan_.row_block * comm_->world(); }
+  int64_t full_len() const { return std::max<int64_t>(std::max(full_cols(), full_rows()), 1); }
+
+  // The same verdict on every rank: true iff `flag` holds on any rank.
+  bool any_rank(bool flag) {
+    double v = flag ? 1.0 : 0.0;
+    PDLP_CK(cudaStreamSynchronize(s()));
+    PDLP_CK(cudaMemcpy(flag_.get(), &v, sizeof(double), cudaMemcpyHostToDevice));
+    comm_->allreduce(flag_.get(), 1, true, s());
+    PDLP_CK(cudaMemcpyAsync(&v, flag_.get(), sizeof(double), cudaMemcpyDeviceToHost, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));
+    return v > 0.5;
+  }
+
+  // First failure per validation category over all ranks, in whole-problem
+  // numbering (keys are index << 3 | code, see k_valid.cu).
+  void combine_validation(unsigned long long hk[4], unsigned& hb, int64_t r0, int64_t c0,
+                          int64_t e0) {
+    const unsigned long long none = ~0ull;
+    const int64_t off[4] = {c0, c0, r0, e0};
+    double v[5];
+    for (int q = 0; q < 4; ++q) {
+      if (hk[q] == none) {
+        v[q] = -kInf;
+      } else {
+        const unsigned long long idx = (hk[q] >> 3) + static_cast<unsigned long long>(off[q]);
+        v[q] = -static_cast<double>((idx << 3) | (hk[q] & 7ull));
+      }
+    }
+    v[4] = hb != 0 ? 1.0 : 0.0;
+    PDLP_CK(cudaStreamSynchronize(s()));
+    PDLP_CK(cudaMemcpy(flag_.get(), v, sizeof(v), cudaMemcpyHostToDevice));
+    comm_->allreduce(flag_.get(), 5, true, s());
+    PDLP_CK(cudaMemcpyAsync(v, flag_.get(), sizeof(v), cudaMemcpyDeviceToHost, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));
+    for (int q = 0; q < 4; ++q) {
+      hk[q] = std::isinf(v[q]) ? none : static_cast<unsigned long long>(-v[q]);
+    }
+    hb = v[4] > 0.5 ? 1u : 0u;
+  }
+
+  // local (n_local entries) -> this rank's block of `full`, then all-gather.
+  void gather(const double* local, int64_t n_local, int64_t block, double* full) {
+    if (local != full + block * comm_->rank()) {
+      dev_copy(full + block * comm_->rank(), local, n_local, s());
+    }
+    comm_->allgather(full, static_cast<size_t>(block), s());
+  }
+
+  // A x (or A' y): on one GPU the plain product; sharded, the layout's kind
+  // says whether the column-side operand is gathered first (K_g) or the
+  // column-side output is reduce-scattered after (K_g^T).
+  void product(const pdlpk_csr& L, int orig, const double* in, double* out) {
+    if (!dist() || L.dist_kind == PDLPK_DIST_NONE) {
+      PDLP_LAUNCH(pdlpk_spmv(&L, orig, in, out, parity_, s()));
+      return;
+    }
+    const int64_t nb = plan_.col_block;
+    const int64_t nloc = plan_.col_end - plan_.col_begin;
+    if (L.dist_kind == PDLPK_DIST_GATHER) {
+      gather(in, nloc, nb, gbuf_.get());
+      PDLP_LAUNCH(pdlpk_spmv(&L, orig, gbuf_.get(), out, 0, s()));
+    } else {
+      PDLP_LAUNCH(pdlpk_spmv(&L, orig, in, pbuf_.get(), 0, s()));
+      comm_->reduce_scatter(pbuf_.get(), gbuf_.get(), static_cast<size_t>(nb), s());
+      dev_copy(out, gbuf_.get(), nloc, s());
+    }
+  }
+
+  // Combines the reductions logged since the last read across ranks (one
+  // all-gather of the slot array, rank-ordered sums / maxima).
+  void combine_logged() {
+    const int count = red_log_.count;
+    if (count == 0) return;
+    red_log_.count = 0;
+    if (count > 48) throw CudaError("internal: reduction log overflow");
+    uint64_t marked = 0, maxbits = 0;
+    for (int i = 0; i < count; ++i) {
+      const int64_t off = red_log_.out[i] - slots_.get();
+      const int k = red_log_.k[i];
+      if (off < 0 || off + k > kSlots) throw CudaError("internal: reduction outside the slots");
+      for (int j = 0; j < k; ++j) {
+        const uint64_t bit = 1ull << (off + j);
+        marked |= bit;
+        if ((red_log_.maxmask[i] >> j) & 1u) {
+          maxbits |= bit;
+        } else {
+          maxbits &= ~bit;
+        }
+      }
+    }
+    double* all = slots_all_.get();
+    dev_copy(all + static_cast<int64_t>(kSlots) * comm_->rank(), slots_.get(), kSlots, s());
+    comm_->allgather(all, kSlots, s());
+    PDLP_LAUNCH(pdlpk_combine_slots(all, comm_->world(), kSlots, marked, maxbits, slots_.get(), s()));
+  }
+
+  // One sharded attempt, all stream-ordered:
+  // primal -> [AG x-bar] -> K x-bar + dual update -> K^T dy partial -> [RS]
+  // -> column epilogue -> [AG 8 scalars] -> rank-ordered decision.  For the
+  // dual polishing subproblem the layouts swap kinds and so do the
+  // collectives (K partial + RS, K^T gathered).
+  void attempt_dist(const pdlpk_problem& P, Inner& D, const pdlpk_step_args& a) {
+    const int rank = comm_->rank();
+    const int64_t nb = plan_.col_block;
+    const bool kg = P.K.dist_kind == PDLPK_DIST_GATHER;
+    const bool ktg = P.KT.dist_kind == PDLPK_DIST_GATHER;
+    double* xfull = D.xbar.get();
+    double* dyfull = D.dy.get();
+    pdlpk_step_args b = a;
+    b.xbar = kg ? xfull + nb * rank : xfull;
+    PDLP_LAUNCH(pdlpk_dist_primal(&b, s()));
+    b.xbar = xfull;
+    b.dy = ktg ? dyfull + nb * rank : dyfull;
+    int64_t g2 = 0, g3 = 0;
+    int k_acc = 0, kt_acc = 0;
+    if (kg) {
+      comm_->allgather(xfull, static_cast<size_t>(nb), s());
+      PDLP_LAUNCH(pdlpk_dist_row_fused(&b, s()));
+      g2 = pdlpk_dist_sched_grid(&P.K);
+      k_acc = 1;
+    } else {
+      PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, xfull, D.pbuf.get(), 0, s()));
+      comm_->reduce_scatter(D.pbuf.get(), D.dloc.get(), static_cast<size_t>(nb), s());
+      PDLP_LAUNCH(pdlpk_dist_row_epi(&b, D.dloc.get(), s()));
+      g2 = pdlpk_dist_ew_grid(P.m);
+    }
+    if (ktg) {
+      comm_->allgather(dyfull, static_cast<size_t>(nb), s());
+      b.dy = dyfull;
+      PDLP_LAUNCH(pdlpk_dist_col_fused(&b, s()));
+      g3 = pdlpk_dist_sched_grid(&P.KT);
+      kt_acc = 1;
+    } else {
+      PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, b.dy, D.pbuf.get(), 0, s()));
+      comm_->reduce_scatter(D.pbuf.get(), D.dloc.get(), static_cast<size_t>(nb), s());
+      PDLP_LAUNCH(pdlpk_dist_col_epi(&b, D.dloc.get(), s()));
+      g3 = pdlpk_dist_ew_grid(P.n);
+    }
+    double* tot = D.tot_all.get();
+    PDLP_LAUNCH(pdlpk_dist_totals(&b, g2, g3, k_acc, kt_acc, tot + 8 * rank, s()));
+    comm_->allgather(tot, 8, s());
+    PDLP_LAUNCH(pdlpk_dist_decide(&b, tot, comm_->world(), s()));
+  }
+
+  // Whole-problem views for the gap (computed redundantly on gathered
+  // vectors by every rank): the main problem, its primal polishing problem
+  // (c = 0) and the swapped dual polishing problem.
+  void build_full_views() {
+    const int64_t nb = plan_.col_block, mb = plan_.row_block;
+    const int64_t nloc = prob_.n, mloc = prob_.m;
+    for (DevBuf<double>* b : {&fc_c_, &fc_lv_, &fc_uv_, &fc_zero_}) b->alloc(full_cols());
+    for (DevBuf<double>* b : {&fr_lc_, &fr_uc_, &fr_zero_}) b->alloc(full_rows());
+    gather(prob_.c.get(), nloc, nb, fc_c_.get());
+    gather(prob_.lv.get(), nloc, nb, fc_lv_.get());
+    gather(prob_.uv.get(), nloc, nb, fc_uv_.get());
+    gather(prob_.lc.get(), mloc, mb, fr_lc_.get());
+    gather(prob_.uc.get(), mloc, mb, fr_uc_.get());
+    dev_zero(fc_zero_.get(), full_cols(), s());
+    dev_zero(fr_zero_.get(), full_rows(), s());
+    pdlpk_problem F{};
+    F.m = m_glob_;
+    F.n = n_glob_;
+    F.c = F.c_o = fc_c_.get();
+    F.lv = F.lv_o = fc_lv_.get();
+    F.uv = F.uv_o = fc_uv_.get();
+    F.lc = F.lc_o = fr_lc_.get();
+    F.uc = F.uc_o = fr_uc_.get();
+    full_main_ = F;
+    full_primal_ = F;
+    full_primal_.c = full_primal_.c_o = fc_zero_.get();
+    for (DevBuf<double>* b : {&fs_lc_, &fs_uc_}) b->alloc(std::max<int64_t>(n_glob_, 1));
+    for (DevBuf<double>* b : {&fs_lv_, &fs_uv_}) b->alloc(std::max<int64_t>(m_glob_, 1));
+    PDLP_LAUNCH(pdlpk_dual_feas_bounds(F.c, F.lv, F.uv, n_glob_, F.lc, F.uc, m_glob_, fs_lc_.get(),
+                                       fs_uc_.get(), fs_lv_.get(), fs_uv_.get(), s()));
+    pdlpk_problem Q{};
+    Q.m = n_glob_;
+    Q.n = m_glob_;
+    Q.c = Q.c_o = fr_zero_.get();
+    Q.lc = Q.lc_o = fs_lc_.get();
+    Q.uc = Q.uc_o = fs_uc_.get();
+    Q.lv = Q.lv_o = fs_lv_.get();
+    Q.uv = Q.uv_o = fs_uv_.get();
+    full_dual_ = Q;
+    for (auto& q : gq_) {
+      for (auto& b : q) b.alloc(full_len());
+    }
+  }
+
   // Device slot layout (doubles) of one cadence batch.
   static constexpr int kSlotScrCur = 0;  // 4: primal_inf, dual_inf, pobj, penalty
   static constexpr int kSlotScrAvg = 4;  // 4
@@ -549,6 +811,7 @@ class Engine {
   double* slot(int i) { return slots_.get() + i; }
   // Copies slots [0, count) to the host (one sync).
   const double* read_slots(int count) {
+    if (dist()) combine_logged();
     PDLP_CK(cudaMemcpyAsync(host_slots_, slots_.get(), count * sizeof(double),
                             cudaMemcpyDeviceToHost, s()));
     PDLP_CK(cudaStreamSynchronize(s()));
@@ -559,20 +822,41 @@ class Engine {
   void precondition(int ruiz_passes, bool pock_chambolle) {
     const auto t0 = Clock::now();
     const int64_t m = prob_.m, n = prob_.n;
-    DevBuf<double> fr(m), fc(n);
-    DevBuf<unsigned long long> bits(std::max<int64_t>(std::max(m, n), 1));
+    // fc spans every column of the layouts (all n when sharded)
+    DevBuf<double> fr(m), fc(n_glob_);
+    DevBuf<unsigned long long> bits(std::max<int64_t>(std::max(m, n_glob_), 1));
+    const int64_t c0 = dist() ? plan_.col_begin : 0;
     const int64_t nnz = prob_.row.view.nnz;
     (void)nnz;
     const DevBuf<int32_t>& row_of = row_of_;  // line maps built during validation
     const DevBuf<int32_t>& col_of = col_of_;
     auto pass = [&](int one_norm) {
       PDLP_LAUNCH(pdlpk_line_factors(&prob_.row.view, row_of.get(), one_norm, fr.get(), bits.get(), s()));
-      PDLP_LAUNCH(pdlpk_line_factors(&prob_.col.view, col_of.get(), one_norm, fc.get(), bits.get(), s()));
+      if (dist()) {
+        // A rank holds one consecutive run (its rows) of every column.
+        // inf-norms: max over ranks is exact.  1-norms: continue the
+        // reference's sequential sum rank by rank (rank r adds its run to the
+        // carried sums, an all-reduce max publishes them since the sums only
+        // grow), so the scaled problem is bit-identical to one GPU's.
+        if (one_norm == 0) {
+          PDLP_LAUNCH(pdlpk_line_norms(&prob_.col.view, col_of.get(), 0, fc.get(), bits.get(), s()));
+          comm_->allreduce(fc.get(), static_cast<size_t>(n_glob_), true, s());
+        } else {
+          dev_zero(fc.get(), n_glob_, s());
+          for (int r = 0; r < comm_->world(); ++r) {
+            if (r == comm_->rank()) PDLP_LAUNCH(pdlpk_line_onenorm_continue(&prob_.col.view, fc.get(), s()));
+            comm_->allreduce(fc.get(), static_cast<size_t>(n_glob_), true, s());
+          }
+        }
+        PDLP_LAUNCH(pdlpk_norm_to_factor(fc.get(), n_glob_, s()));
+      } else {
+        PDLP_LAUNCH(pdlpk_line_factors(&prob_.col.view, col_of.get(), one_norm, fc.get(), bits.get(), s()));
+      }
       PDLP_LAUNCH(pdlpk_apply_factors(&prob_.row.view, row_of.get(), prob_.row.value.get(), fr.get(), fc.get(), s()));
       PDLP_LAUNCH(pdlpk_apply_factors(&prob_.col.view, col_of.get(), prob_.col.value.get(), fc.get(), fr.get(), s()));
       PDLP_LAUNCH(pdlpk_apply_vec_factors(prob_.lc.get(), prob_.uc.get(), prob_.row_scale.get(),
                                           fr.get(), m, prob_.c.get(), prob_.lv.get(),
-                                          prob_.uv.get(), prob_.col_scale.get(), fc.get(), n, s()));
+                                          prob_.uv.get(), prob_.col_scale.get(), fc.get() + c0, n, s()));
     };
     for (int p = 0; p < ruiz_passes; ++p) pass(0);
     if (pock_chambolle) pass(1);
@@ -656,9 +940,16 @@ class Engine {
   // InnerState::prepare (solver.hpp:167-192); x0 is a device vector.
   void prepare(Inner& D, const pdlpk_problem& P, const double* x0, double eta0, double omega0,
                bool fixed) {
-    const int64_t partials = pdlpk_step_partials(&P);
+    int64_t partials = pdlpk_step_partials(&P);
+    if (dist()) {
+      partials = std::max<int64_t>(partials, 3 * pdlpk_dist_ew_grid(std::max(P.n, P.m)) + 64);
+    }
     if (D.n != P.n || D.m != P.m || static_cast<int64_t>(D.part2.size()) < partials) {
-      D.allocate(P.n, P.m, partials, shards_);
+      if (dist()) {
+        D.allocate(P.n, P.m, partials, shards_, full_cols(), plan_.col_block, comm_->world());
+      } else {
+        D.allocate(P.n, P.m, partials, shards_);
+      }
     }
     dev_copy(D.x[0].get(), x0, P.n, s());
     dev_zero(D.y[0].get(), P.m, s());
@@ -698,7 +989,10 @@ class Engine {
     while (true) {
       const int64_t need = target - known_k;
       if (need <= 0) break;
-      if (profile_) {
+      if (dist()) {
+        for (int64_t t = 0; t < need; ++t) attempt_dist(P, D, a);
+        read_state(D);
+      } else if (profile_) {
         const int64_t attempts0 = D.hs.attempts;
         ensure_prof_events(need);
         for (int64_t t = 0; t < need; ++t) {
@@ -745,8 +1039,8 @@ class Engine {
   // (residuals.hpp:49-64, 135-158): genuine original-space products.
   Summary original_kkt(const pdlpk_problem& P, const double* x, const double* y, int rc_mode,
                        double* r_out, Inner& D) {
-    PDLP_LAUNCH(pdlpk_spmv(&P.K, 1, x, D.prod_m.get(), parity_, s()));
-    PDLP_LAUNCH(pdlpk_spmv(&P.KT, 1, y, D.prod_n.get(), parity_, s()));
+    product(P.K, 1, x, D.prod_m.get());
+    product(P.KT, 1, y, D.prod_n.get());
     return screen(P, 1, x, y, D.prod_m.get(), D.prod_n.get(), rc_mode, r_out);
   }
 
@@ -800,7 +1094,7 @@ class Engine {
     PDLP_LAUNCH(pdlpk_ray_primal_prep(&P, orig, yc, D.ray_m.get(), &r, slot(0), s()));
     const double norm = read_slots(1)[0];
     if (!(norm > 0.0)) return false;
-    PDLP_LAUNCH(pdlpk_spmv(&P.KT, orig, D.ray_m.get(), D.prod_n.get(), parity_, s()));
+    product(P.KT, orig, D.ray_m.get(), D.prod_n.get());
     PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, orig, D.ray_m.get(), D.prod_n.get(), nullptr, nullptr,
                                         D.ray_n.get(), &r, slot(0), s()));
     const double* h = read_slots(2);
@@ -821,7 +1115,7 @@ class Engine {
     // Both conditions below must hold for a certificate; testing the cheap
     // ones first skips the product without changing the verdict.
     if (box > eps_ray * norm || !(obj < 0.0)) return false;
-    PDLP_LAUNCH(pdlpk_spmv(&P.K, orig, xc, D.prod_m.get(), parity_, s()));
+    product(P.K, orig, xc, D.prod_m.get());
     PDLP_LAUNCH(pdlpk_ray_dual_finish(&P, orig, D.prod_m.get(), &r, slot(0), s()));
     const double row = read_slots(1)[0];
     residual = (box < row) ? row : box;
@@ -861,12 +1155,15 @@ class Engine {
       double* sl = slot(kSlotRay + 8 * static_cast<int>(q));
       double* ray = D.ray_y[q].get();
       PDLP_LAUNCH(pdlpk_ray_primal_prep(&P, 0, cands[q].y, ray, &r, sl, s()));
-      if (cands[q].known_aty != nullptr) {
+      if (cands[q].known_aty != nullptr && !dist()) {
         PDLP_LAUNCH(pdlpk_spmv_cond(&P.KT, 0, ray, D.prod_n.get(), parity_, sl + 1, s()));
       } else {
-        PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, ray, D.prod_n.get(), parity_, s()));
+        product(P.KT, 0, ray, D.prod_n.get());
       }
-      PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, 0, ray, D.prod_n.get(), cands[q].known_aty, sl + 1,
+      // (sharded: the changed-count is still rank-local here, so the
+      // product is always recomputed and the cached A'y is not used)
+      PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, 0, ray, D.prod_n.get(),
+                                          dist() ? nullptr : cands[q].known_aty, sl + 1,
                                           D.rhat[q].get(), &r, sl + 2, s()));
       PDLP_LAUNCH(pdlpk_ray_dual_prep(&P, 0, cands[q].x, &r, sl + 4, s()));
     }
@@ -894,7 +1191,7 @@ class Engine {
       const double xn = sl[4], box = sl[5], obj = sl[6];
       if (xn > 0.0 && !(box > eps * xn) && obj < 0.0) {
         const pdlpk_red r = red();
-        PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, cands[q].x, D.prod_m.get(), parity_, s()));
+        product(P.K, 0, cands[q].x, D.prod_m.get());
         PDLP_LAUNCH(pdlpk_ray_dual_finish(&P, 0, D.prod_m.get(), &r, slot(kSlotTmp), s()));
         const double row = read_slots(kSlotTmp + 1)[kSlotTmp];
         const double residual = (box < row) ? row : box;
@@ -946,7 +1243,32 @@ class Engine {
     const double *x, *y, *ax, *aty;
     double dx2, dy2;
   };
-  void gaps(const pdlpk_problem& P, const GapQuery* q, int count, double omega, double* out) {
+  void gaps(const InnerCfg& cfg, const pdlpk_problem& P, const GapQuery* q, int count,
+            double omega, double* out) {
+    if (dist()) {
+      // Sharded: every rank evaluates the same whole-problem gap on gathered
+      // vectors (identical inputs -> identical mu everywhere); the cadence
+      // runs it 2-3 times per 64 steps.
+      const int64_t nb = plan_.col_block, mb = plan_.row_block;
+      const int64_t xb = cfg.swapped ? mb : nb, yb = cfg.swapped ? nb : mb;
+      GapQuery g[2];
+      for (int i = 0; i < count; ++i) {
+        gather(q[i].x, P.n, xb, gq_[i][0].get());
+        gather(q[i].aty, P.n, xb, gq_[i][1].get());
+        gather(q[i].y, P.m, yb, gq_[i][2].get());
+        gather(q[i].ax, P.m, yb, gq_[i][3].get());
+        g[i] = {gq_[i][0].get(), gq_[i][2].get(), gq_[i][3].get(), gq_[i][1].get(), q[i].dx2, q[i].dy2};
+      }
+      combine_logged();  // nothing may stay pending across the unlogged gap
+      pdlpk_set_red_log(nullptr);
+      gaps_local(*cfg.full, g, count, omega, out);
+      pdlpk_set_red_log(&red_log_);
+      return;
+    }
+    gaps_local(P, q, count, omega, out);
+  }
+
+  void gaps_local(const pdlpk_problem& P, const GapQuery* q, int count, double omega, double* out) {
     const pdlpk_red r = red();
     for (int i = 0; i < count; ++i) {
       PDLP_LAUNCH(pdlpk_gap_prepare(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, &r,
@@ -1020,6 +1342,16 @@ class Engine {
   int shards_ = 4;
   std::unique_ptr<Stream> stream_;  // declared first: outlives every buffer
   std::unique_ptr<AllocStreamScope> alloc_scope_;
+  // sharded solve
+  Comm* comm_ = nullptr;
+  pdlp_shard_plan plan_{};
+  int64_t m_glob_ = 0, n_glob_ = 0;
+  pdlpk_red_log red_log_{};
+  DevBuf<double> gbuf_, pbuf_, slots_all_, flag_;
+  DevBuf<double> fc_c_, fc_lv_, fc_uv_, fc_zero_, fr_lc_, fr_uc_, fr_zero_;
+  DevBuf<double> fs_lc_, fs_uc_, fs_lv_, fs_uv_;
+  DevBuf<double> gq_[2][4];
+  pdlpk_problem full_main_{}, full_primal_{}, full_dual_{};
   DevProblem prob_;
   DevBuf<double> slots_;
   double* host_slots_ = nullptr;
@@ -1063,6 +1395,10 @@ bool Engine::attempt_polish(const pdlpk_problem& P, const InnerCfg& cfg, Inner& 
 
   const pdlpk_problem P2 = primal_feas_view(P);
   Inner& D2 = polish_primal_;
+  if (dist()) {
+    sub.full = &full_primal_;
+    sub.swapped = false;
+  }
   prepare(D2, P2, D.avg_x.get(), D.hs.eta, D.omega, cfg.fixed_eta.has_value());
   sub.tag = "polish_primal";
   const int s2 = run_inner(P2, P2, sub, D2);
@@ -1077,6 +1413,10 @@ bool Engine::attempt_polish(const pdlpk_problem& P, const InnerCfg& cfg, Inner& 
   if (sub.budget <= 0) return false;
   sub.tol.eps_primal = cfg.tol.eps_dual;
   sub.tag = "polish_dual";
+  if (dist()) {
+    sub.full = &full_dual_;
+    sub.swapped = true;
+  }
   const int s3 = run_inner(P3, P3, sub, D3);
   D.polish_iterations += D3.k();
   attempts_total_ += D3.hs.attempts;
@@ -1101,17 +1441,18 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
     const bool budget_hit = D.k() >= cfg.budget;
     const bool at_cadence = budget_hit || (D.k() % cfg.check_interval == 0);
     if (at_cadence) {
-      const bool timed_out = Clock::now() >= cfg.deadline;
+      bool timed_out = Clock::now() >= cfg.deadline;
+      if (dist()) timed_out = any_rank(timed_out);  // ranks must agree
       const int c = D.cur();
       flush_average(P, D);
-      PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.x[c].get(), D.ax_cur.get(), parity_, s()));
-      PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.y[c].get(), D.aty[c].get(), parity_, s()));
+      product(P.K, 0, D.x[c].get(), D.ax_cur.get());
+      product(P.KT, 0, D.y[c].get(), D.aty[c].get());
       const bool have_avg = D.hs.avg_count > 0;
       if (have_avg) {
         PDLP_LAUNCH(pdlpk_average_into(D.state.get(), D.sum_x.get(), D.sum_y.get(), D.avg_x.get(),
                                        D.avg_y.get(), P.n, P.m, s()));
-        PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.avg_x.get(), D.ax_avg.get(), parity_, s()));
-        PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.avg_y.get(), D.aty_avg.get(), parity_, s()));
+        product(P.K, 0, D.avg_x.get(), D.ax_avg.get());
+        product(P.KT, 0, D.avg_y.get(), D.aty_avg.get());
       }
       // One batch, one sync: both residual screens, every ray candidate's
       // scaled-space test, and the restart distances to the reference point.
@@ -1179,7 +1520,7 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
             {D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(), D.aty_avg.get(), h[kSlotDist + 2],
              h[kSlotDist + 3]}};
         double mu[2] = {0.0, kInf};
-        gaps(P, q, have_avg ? 2 : 1, D.omega, mu);
+        gaps(cfg, P, q, have_avg ? 2 : 1, D.omega, mu);
         const double mu_cur = mu[0];
         const double mu_avg = have_avg ? mu[1] : kInf;
         const bool use_current = mu_cur < mu_avg;
@@ -1192,7 +1533,7 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
             // diff_norm_sq(candidate, ref) is exactly the metric's distance
             D.omega = update_primal_weight(std::sqrt(cq.dx2), std::sqrt(cq.dy2), D.omega);
           }
-          gaps(P, &cq, 1, D.omega, &D.mu_last);
+          gaps(cfg, P, &cq, 1, D.omega, &D.mu_last);
           if (!use_current) {
             dev_copy(D.x[c].get(), D.avg_x.get(), P.n, s());
             dev_copy(D.y[c].get(), D.avg_y.get(), P.m, s());
@@ -1256,7 +1597,7 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
         // One recovery screen of the last good point and the window average
         // (solver.hpp:494-516).
         const int c = D.cur();
-        PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.x[c].get(), D.ax_cur.get(), parity_, s()));
+        product(P.K, 0, D.x[c].get(), D.ax_cur.get());
         Summary tmp;
         if (screen_and_verify(P, cfg, D.x[c].get(), D.y[c].get(), D.ax_cur.get(), D.aty[c].get(),
                               D.rc_a.get(), tmp, D, "current iterate after a numerical error")) {
@@ -1266,8 +1607,8 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
           flush_average(P, D);
           PDLP_LAUNCH(pdlpk_average_into(D.state.get(), D.sum_x.get(), D.sum_y.get(),
                                          D.avg_x.get(), D.avg_y.get(), P.n, P.m, s()));
-          PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.avg_x.get(), D.ax_avg.get(), parity_, s()));
-          PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.avg_y.get(), D.aty_avg.get(), parity_, s()));
+          product(P.K, 0, D.avg_x.get(), D.ax_avg.get());
+          product(P.KT, 0, D.avg_y.get(), D.aty_avg.get());
           if (screen_and_verify(P, cfg, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
                                 D.aty_avg.get(), D.rc_b.get(), tmp, D,
                                 "window average after a numerical error")) {
@@ -1306,10 +1647,13 @@ void copy_to_host(double* dst, const double* src, int64_t n, cudaStream_t s) {
 }
 
 // solve (solver.hpp:535-608)
-void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result* res) {
+// comm != nullptr: this process/thread is one rank of a row-sharded solve.
+void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result* res,
+           Comm* comm = nullptr) {
   const auto t0 = Clock::now();
-  Engine E(problem, *o);  // uploads and validates on device
+  Engine E(problem, *o, comm);  // uploads and validates on device
   if (o->enable_scaling) E.precondition(o->ruiz_passes, o->pock_chambolle != 0);
+  if (E.dist()) E.build_full_views();
   const pdlpk_problem P = E.problem().view();
 
   InnerCfg cfg;
@@ -1337,6 +1681,7 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result*
   cfg.observer_user = o->observer_user;
   cfg.logging = o->logging != 0;
   cfg.tag = "main";
+  if (E.dist()) cfg.full = &E.full_main_;
 
   const double eta0 = o->has_fixed_step_size ? o->fixed_step_size : E.initial_step_size();
   const double omega0 =
@@ -1367,9 +1712,21 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result*
   }
 
   res->status = status;
-  copy_to_host(res->x, D.sol_x.get(), P.n, E.s());
-  copy_to_host(res->y, D.sol_y.get(), P.m, E.s());
-  copy_to_host(res->reduced_costs, D.sol_r.get(), P.n, E.s());
+  // Sharded: every rank gathers the whole vectors (collectively, so every
+  // rank makes the same calls) and returns the whole result.
+  auto out_vec = [&](double* host, const double* dev, bool col_side) {
+    if (!E.dist()) {
+      copy_to_host(host, dev, col_side ? P.n : P.m, E.s());
+      return;
+    }
+    double* full = col_side ? E.gbuf_.get() : E.gq_[0][0].get();
+    E.gather(dev, col_side ? P.n : P.m, col_side ? E.plan_.col_block : E.plan_.row_block, full);
+    copy_to_host(host, full, col_side ? E.n_glob_ : E.m_glob_, E.s());
+    PDLP_CK(cudaStreamSynchronize(E.s()));
+  };
+  out_vec(res->x, D.sol_x.get(), true);
+  out_vec(res->y, D.sol_y.get(), false);
+  out_vec(res->reduced_costs, D.sol_r.get(), true);
   res->summary.primal_residual_inf = D.sol_summary.primal;
   res->summary.dual_residual_inf = D.sol_summary.dual;
   res->summary.primal_objective = D.sol_summary.pobj;
@@ -1380,10 +1737,10 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result*
   if (D.cert.have) {
     res->cert_kind = D.cert.kind;
     if (D.cert.kind == PDLP_CERT_PRIMAL_INFEASIBLE) {
-      copy_to_host(res->cert_ray_y, D.cert.ray_y.get(), P.m, E.s());
-      copy_to_host(res->cert_ray_r, D.cert.ray_r.get(), P.n, E.s());
+      out_vec(res->cert_ray_y, D.cert.ray_y.get(), false);
+      out_vec(res->cert_ray_r, D.cert.ray_r.get(), true);
     } else {
-      copy_to_host(res->cert_ray_x, D.cert.ray_x.get(), P.n, E.s());
+      out_vec(res->cert_ray_x, D.cert.ray_x.get(), true);
     }
     res->cert_residual_inf = D.cert.residual;
     res->cert_objective = D.cert.objective;
@@ -1417,7 +1774,7 @@ int guarded(F&& f) {
   try {
     f();
     return PDLP_OK;
-  } catch (const InvalidProblem& e) {
+  } catch (const std::invalid_argument& e) {  // InvalidProblem, shard extraction
     g_last_error = e.what();
     return PDLP_ERR_INVALID_PROBLEM;
   } catch (const CudaError& e) {
@@ -1474,6 +1831,153 @@ int pdlp_solve(const pdlp_problem_view* problem, const pdlp_options* options,
 }
 
 const char* pdlp_last_error(void) { return g_last_error.c_str(); }
+
+int pdlp_shard_plan_for(int64_t rows, int64_t cols, int32_t rank, int32_t world,
+                        pdlp_shard_plan* out) {
+  if (out == nullptr || world < 1 || rank < 0 || rank >= world || rows < 0 || cols < 0) {
+    g_last_error = "invalid shard request";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  *out = shard_plan(rows, cols, rank, world);
+  return PDLP_OK;
+}
+
+int pdlp_shard_extract(const pdlp_problem_view* problem, int32_t rank, int32_t world,
+                       pdlp_shard_view* out, void** owner) {
+  if (problem == nullptr || out == nullptr || owner == nullptr || world < 1 || rank < 0 ||
+      rank >= world) {
+    g_last_error = "invalid shard request";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&] {
+    auto d = std::make_unique<ShardData>();
+    extract_shard(*problem, rank, world, *d);
+    *out = d->view;
+    *owner = d.release();
+  });
+}
+
+void pdlp_shard_free(void* owner) { delete static_cast<ShardData*>(owner); }
+
+int pdlp_nccl_unique_id(unsigned char out[128]) {
+  const char* why = "";
+  if (out == nullptr) {
+    g_last_error = "null argument";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  if (!nccl_unique_id(out, &why)) {
+    g_last_error = why;
+    return PDLP_ERR_CUDA;
+  }
+  return PDLP_OK;
+}
+
+static int check_sharded_args(const pdlp_problem_view* problem, const pdlp_options* o,
+                              int32_t rank, int32_t world, const pdlp_result* result) {
+  if (problem == nullptr || o == nullptr || result == nullptr || world < 1 || rank < 0 ||
+      rank >= world) {
+    g_last_error = "invalid sharded-solve arguments";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  if (o->mode != PDLP_MODE_PERF) {
+    g_last_error = "the sharded solve runs in perf mode only (parity needs one GPU)";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  if (o->observer != nullptr) {
+    g_last_error = "the sharded solve does not support an observer";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  return PDLP_OK;
+}
+
+int pdlp_solve_sharded(const pdlp_problem_view* problem, const pdlp_options* options,
+                       int32_t rank, int32_t world, const unsigned char nccl_id[128],
+                       pdlp_result* result) {
+  int rc = check_sharded_args(problem, options, rank, world, result);
+  if (rc != PDLP_OK) return rc;
+  if (nccl_id == nullptr) {
+    g_last_error = "null nccl id";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&] {
+    std::unique_ptr<Comm> comm = make_nccl_comm(nccl_id, rank, world, options->device);
+    solve(problem, options, result, comm.get());
+  });
+}
+
+int pdlp_solve_sharded_emulated(const pdlp_problem_view* problem, const pdlp_options* options,
+                                int32_t world, pdlp_result* result) {
+  int rc = check_sharded_args(problem, options, 0, world, result);
+  if (rc != PDLP_OK) return rc;
+  const size_t n = static_cast<size_t>(std::max<int64_t>(problem->cols, 0));
+  const size_t m = static_cast<size_t>(std::max<int64_t>(problem->rows, 0));
+  // ranks > 0 fill private copies of the (identical) result
+  std::vector<pdlp_result> res(static_cast<size_t>(world));
+  struct Bufs {
+    std::vector<double> x, y, r, rx, ry, rr;
+  };
+  std::vector<Bufs> store(static_cast<size_t>(world));
+  for (int r = 0; r < world; ++r) {
+    if (r == 0) {
+      res[0] = *result;
+      continue;
+    }
+    Bufs& b = store[r];
+    for (auto* v : {&b.x, &b.r, &b.rx, &b.rr}) v->assign(n + 1, 0.0);
+    for (auto* v : {&b.y, &b.ry}) v->assign(m + 1, 0.0);
+    res[r] = pdlp_result{};
+    res[r].x = b.x.data();
+    res[r].y = b.y.data();
+    res[r].reduced_costs = b.r.data();
+    res[r].cert_ray_x = b.rx.data();
+    res[r].cert_ray_y = b.ry.data();
+    res[r].cert_ray_r = b.rr.data();
+  }
+  std::shared_ptr<ThreadHub> hub = make_thread_hub(world);
+  std::vector<int> codes(static_cast<size_t>(world), PDLP_OK);
+  std::vector<std::string> errs(static_cast<size_t>(world));
+  std::vector<std::thread> th;
+  for (int r = 0; r < world; ++r) {
+    th.emplace_back([&, r] {
+      codes[r] = guarded([&] {
+        std::unique_ptr<Comm> comm = make_thread_comm(hub, r);
+        solve(problem, options, &res[r], comm.get());
+      });
+      if (codes[r] != PDLP_OK) {
+        errs[r] = g_last_error;
+        abort_thread_hub(*hub);
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  // report the first rank's own failure (not the "another rank failed" echo)
+  int pick = -1;
+  for (int r = 0; r < world; ++r) {
+    if (codes[r] != PDLP_OK && errs[r].find("another rank of the group failed") == std::string::npos) {
+      pick = r;
+      break;
+    }
+  }
+  if (pick < 0) {
+    for (int r = 0; r < world && pick < 0; ++r) {
+      if (codes[r] != PDLP_OK) pick = r;
+    }
+  }
+  if (pick >= 0) {
+    g_last_error = errs[pick];
+    return codes[pick];
+  }
+  const pdlp_result user = *result;
+  *result = res[0];
+  // keep the caller's buffer pointers (res[0] was filled through them)
+  result->x = user.x;
+  result->y = user.y;
+  result->reduced_costs = user.reduced_costs;
+  result->cert_ray_x = user.cert_ray_x;
+  result->cert_ray_y = user.cert_ray_y;
+  result->cert_ray_r = user.cert_ray_r;
+  return PDLP_OK;
+}
 
 int pdlp_trim_device_memory(int device) {
   return guarded([&] {

@@ -209,8 +209,10 @@ def _check(rc: int) -> None:
     raise RuntimeError(f"pdlp error {rc}: {msg}")
 
 
-def run_solve(lib, fn_name: str, p: LpProblem, options: SolverOptions, c_opts: N.Options) -> SolveResult:
-    """Shared marshalling for pdlp_solve and the oracle's ref_solve."""
+def run_solve(lib, fn_name: str, p: LpProblem, options: SolverOptions, c_opts: N.Options,
+              extra: tuple = ()) -> SolveResult:
+    """Shared marshalling for pdlp_solve, the sharded solves (extra = the
+    arguments between options and result) and the oracle's ref_solve."""
     view = p.view()
     m, n = p.rows(), p.cols()
     x = np.zeros(n)
@@ -226,7 +228,7 @@ def run_solve(lib, fn_name: str, p: LpProblem, options: SolverOptions, c_opts: N
     if options.observer is not None:
         thunk = _observer_thunk(options.observer)
         c_opts.observer = thunk
-    rc = getattr(lib, fn_name)(C.byref(view), C.byref(c_opts), C.byref(res))
+    rc = getattr(lib, fn_name)(C.byref(view), C.byref(c_opts), *extra, C.byref(res))
     if rc != 0:
         err = lib.pdlp_last_error() if hasattr(lib, "pdlp_last_error") else lib.ref_last_error()
         msg = err.decode()

@@ -1,0 +1,267 @@
+"""Row-sharded solve.
+
+CPU: the shard plan and the host-side shard extraction, and a world_size-2
+gloo run of the per-step exchange schedule (x-bar all-gather, partial K^T dy
+reduced to the column owners) on extracted shards.  GPU: the sharded solve
+with threads-emulated ranks on one GPU (collectives = host barriers + device
+copies, no cross-kernel waits) and the NCCL communicator at world 1, both
+against the single-GPU solve.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2501_07018_b200 as P
+from paper_2501_07018_b200 import sharded as S
+from tests.helpers import contradictory_rows, dense, random_box_lp, tiny_lp, unbounded_lp
+
+
+def _dense_shard(sh, n):
+    rows, cols = sh["rows"], sh["cols"]
+    ml = rows["dim"]
+    kg = np.zeros((ml, n))
+    for i in range(ml):
+        for k in range(rows["start"][i], rows["start"][i + 1]):
+            kg[i, rows["index"][k]] += rows["value"][k]
+    kgt = np.zeros((n, ml))
+    for j in range(cols["dim"]):
+        for k in range(cols["start"][j], cols["start"][j + 1]):
+            kgt[j, cols["index"][k]] += cols["value"][k]
+    return kg, kgt
+
+
+# ------------------------------------------------------------------ CPU ---
+@pytest.mark.parametrize("m,n,world", [(10, 7, 1), (10, 7, 2), (10, 7, 3), (5, 40, 4), (1, 1, 4),
+                                       (0, 3, 2), (4000, 4_000_000, 8)])
+def test_shard_plan_partitions(m, n, world):
+    plans = [S.shard_plan(m, n, r, world) for r in range(world)]
+    for pl in plans:
+        assert pl.row_block % 2 == 0 and pl.col_block % 2 == 0
+        assert pl.row_block * world >= m and pl.col_block * world >= n
+    rows = [(pl.row_begin, pl.row_end) for pl in plans]
+    cols = [(pl.col_begin, pl.col_end) for pl in plans]
+    for spans, total in ((rows, m), (cols, n)):
+        assert spans[0][0] == 0 and spans[-1][1] == total
+        for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+            assert a0 <= a1 == b0 <= b1
+    for r, pl in enumerate(plans):  # equal blocks: block r starts at r * block
+        assert pl.col_begin == min(n, r * pl.col_block)
+        assert pl.row_begin == min(m, r * pl.row_block)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_extract_shard_reassembles_matrix(world):
+    rng = np.random.default_rng(world)
+    p = random_box_lp(rng, 23, 17)
+    a = dense(p)
+    m, n = a.shape
+    x = rng.uniform(-1, 1, n)
+    y = rng.uniform(-1, 1, m)
+    ax = np.zeros(m)
+    aty = np.zeros(n)
+    seen = 0
+    for r in range(world):
+        sh = S.extract_shard(p, r, world)
+        pl = sh["plan"]
+        kg, kgt = _dense_shard(sh, n)
+        np.testing.assert_array_equal(kg, a[pl.row_begin:pl.row_end])
+        np.testing.assert_array_equal(kgt, a[pl.row_begin:pl.row_end].T)
+        assert sh["entry_offset"] == p.a.by_row.start[pl.row_begin]
+        np.testing.assert_array_equal(sh["objective"], p.objective[pl.col_begin:pl.col_end])
+        np.testing.assert_array_equal(sh["con_lower"], p.con_lower[pl.row_begin:pl.row_end])
+        ax[pl.row_begin:pl.row_end] = kg @ x                      # K x stays local
+        aty += kgt @ y[pl.row_begin:pl.row_end]                   # partial K^T y, summed
+        seen += sh["rows"]["nnz"]
+        assert sh["cols"]["nnz"] == sh["rows"]["nnz"]
+    assert seen == p.a.nonzeros()
+    np.testing.assert_allclose(ax, a @ x, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(aty, a.T @ y, rtol=1e-13, atol=1e-13)
+
+
+def test_extract_shard_rejects_broken_layout():
+    p = tiny_lp()
+    view_start = p.a.by_col.start.copy()
+    p.a.by_col.start[1] = p.a.by_col.start[2] + 1  # non-monotone pointers
+    try:
+        with pytest.raises(ValueError, match="layouts disagree"):
+            S.extract_shard(p, 0, 2)
+    finally:
+        p.a.by_col.start[:] = view_start
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _exchange_worker(rank, world, port, out):
+    """One rank of the sharded step's linear algebra on CPU: primal block ->
+    x-bar all-gather (equal padded blocks) -> local K_g x-bar -> local dual
+    block -> partial K_g^T dy over all n columns -> reduction to the column
+    owners (gloo has no reduce-scatter: all-reduce, keep the own block)."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = P.generate("c0", 3, rows=60, cols=90)
+        m, n = p.rows(), p.cols()
+        sh = S.extract_shard(p, rank, world)
+        pl = sh["plan"]
+        kg, kgt = _dense_shard(sh, n)
+        rng = np.random.default_rng(7)
+        x = rng.uniform(-1, 1, n)
+        xn = rng.uniform(-1, 1, n)
+        y = rng.uniform(-1, 1, m)
+        nb = pl.col_block
+        c0, c1, r0, r1 = pl.col_begin, pl.col_end, pl.row_begin, pl.row_end
+        blk = np.zeros(nb)
+        blk[: c1 - c0] = 2 * xn[c0:c1] - x[c0:c1]          # x-bar of my block
+        parts = [torch.zeros(nb, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(blk))
+        xbar = torch.cat(parts).numpy()[:n]
+        ax = kg @ xbar                                       # rows [r0, r1)
+        dy = -0.5 * ax + 0.25 * y[r0:r1]                     # a local dual update
+        part = np.zeros(nb * world)
+        part[:n] = kgt @ dy
+        t = torch.from_numpy(part)
+        dist.all_reduce(t)
+        mine = t.numpy()[rank * nb: rank * nb + (c1 - c0)]   # K^T dy on my columns
+        a = dense(p)
+        full_ax = a @ (2 * xn - x)
+        full_dy = -0.5 * full_ax + 0.25 * y
+        out[rank] = (float(np.max(np.abs(ax - full_ax[r0:r1]), initial=0.0)),
+                     float(np.max(np.abs(mine - (a.T @ full_dy)[c0:c1]), initial=0.0)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_schedule_gloo_world2():
+    import torch.multiprocessing as mp
+
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_exchange_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert sorted(out.keys()) == [0, 1]
+    for r in range(world):
+        assert out[r][0] < 1e-11 and out[r][1] < 1e-11, out[r]
+
+
+# ------------------------------------------------------------------ GPU ---
+def _opts(**kw):
+    o = P.SolverOptions(mode="perf")
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(1e-300, np.max(np.abs(b))))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_sharded_first_100_iterates_track_single_gpu(gpu, world):
+    """iterates within 1e-9 relative over the first 100 steps.
+
+    The sharded solve scales the problem bit-identically (max-norms are
+    exact, 1-norms are chained rank by rank) but sums the step and cadence
+    reductions per rank, so iterates differ from one GPU's in the last bits,
+    like the reference's own shard plans do.  The restart choice compares
+    two normalized duality gaps, and near ties it can amplify such
+    differences: on P.generate("c2", 2, rows=800, cols=1600, kmax=600) the
+    reference's gap takes 7324.19 vs 6524.97 on average-iterate inputs that
+    agree to 1e-12.  So the restart-free power-law case runs
+    with restarts off; the others exercise the whole cadence."""
+    cases = [(P.generate("c0", 0), {}), (P.generate("c1", 1, sources=50, sinks=70), {}),
+             (P.generate("c2", 2, rows=800, cols=1600, kmax=600), {"enable_restarts": False})]
+    for p, kw in cases:
+        o = _opts(iteration_limit=100, tolerances=P.TerminationTolerances(0.0, 0.0, 0.0), **kw)
+        a = P.solve(p, o)
+        b = S.solve_sharded_emulated(p, o, world)
+        assert b.iterations == a.iterations == 100
+        assert _rel(b.x, a.x) <= 1e-9 and _rel(b.y, a.y) <= 1e-9
+        assert b.restarts == a.restarts
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_solve_reaches_the_same_optimum(gpu, ref, world):
+    for p in (P.generate("c0", 0), P.generate("c1", 0, sources=60, sinks=60)):
+        tol = P.relative_tolerances(p, 1e-4)
+        o = _opts(tolerances=P.TerminationTolerances(*tol))
+        a = P.solve(p, o)
+        b = S.solve_sharded_emulated(p, o, world)
+        assert a.status == b.status == P.SolveStatus.OPTIMAL
+        # the whole result comes back verified in original space
+        assert b.summary.primal_residual_inf <= tol[0] and b.summary.dual_residual_inf <= tol[1]
+        assert b.summary.rel_gap <= tol[2]
+        assert abs(b.summary.primal_objective - a.summary.primal_objective) <= \
+            2e-4 * abs(a.summary.primal_objective)
+        # and the oracle agrees that the returned point meets the tolerances
+        _, kkt = ref.kkt_residuals(p, b.x, b.y)
+        assert kkt.primal_residual_inf <= tol[0] and kkt.dual_residual_inf <= tol[1]
+        assert kkt.rel_gap <= tol[2]
+
+
+@pytest.mark.gpu
+def test_sharded_polishing_and_fixed_step(gpu):
+    p = P.generate("c0", 1)
+    tol = P.relative_tolerances(p, 1e-4)
+    for kw in ({}, {"enable_polish": False}, {"fixed_step_size": 0.05, "iteration_limit": 300}):
+        o = _opts(tolerances=P.TerminationTolerances(*tol), **kw)
+        a = P.solve(p, o)
+        b = S.solve_sharded_emulated(p, o, 2)
+        assert a.status == b.status
+        if a.status == P.SolveStatus.OPTIMAL:
+            assert abs(b.summary.primal_objective - a.summary.primal_objective) <= \
+                2e-4 * abs(a.summary.primal_objective)
+
+
+@pytest.mark.gpu
+def test_sharded_certificates(gpu):
+    for p, kind in ((contradictory_rows(), P.CertificateKind.PRIMAL_INFEASIBLE),
+                    (unbounded_lp(), P.CertificateKind.DUAL_INFEASIBLE)):
+        a = P.solve(p, _opts())
+        b = S.solve_sharded_emulated(p, _opts(), 2)
+        assert a.status == b.status
+        assert b.certificate is not None and b.certificate.kind == kind
+
+
+@pytest.mark.gpu
+def test_sharded_validation_messages_match(gpu):
+    p = P.generate("c0", 0)
+    p.objective[1500] = np.nan   # lives on rank 1 of 2
+    with pytest.raises(ValueError) as e1:
+        P.solve(p, _opts())
+    with pytest.raises(ValueError) as e2:
+        S.solve_sharded_emulated(p, _opts(), 2)
+    assert str(e1.value) == str(e2.value)
+
+
+@pytest.mark.gpu
+def test_sharded_rejects_parity_and_observer(gpu):
+    p = tiny_lp()
+    with pytest.raises(RuntimeError, match="perf mode only"):
+        S.solve_sharded_emulated(p, P.SolverOptions(mode="parity"), 2)
+    with pytest.raises(RuntimeError, match="observer"):
+        S.solve_sharded_emulated(p, _opts(observer=lambda rec: None), 2)
+
+
+@pytest.mark.gpu
+def test_nccl_world1_matches_emulated(gpu):
+    p = P.generate("c1", 2, sources=40, sinks=50)
+    o = _opts(iteration_limit=300, tolerances=P.TerminationTolerances(0.0, 0.0, 0.0))
+    a = S.solve_sharded_emulated(p, o, 1)
+    b = S.solve_sharded(p, o, 0, 1, S.nccl_unique_id())
+    assert a.iterations == b.iterations == 300
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
