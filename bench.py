@@ -19,8 +19,12 @@ Line keys beyond the base contract:
                event launch time vs MEASURED_PEAKS.json hbm_gbs
   cpu_baseline the compiled reference (oracle/_ref) on this host's cores
   time_to_tol  C1 solved to BASELINE's 1e-4 relative KKT (SURVEY §8(d) mapping)
-Multi-GPU (torchrun): round 1 runs one independent C1 replica per GPU
-(config.parallelism = "replicas"); the row-sharded NCCL path is not built yet.
+Multi-GPU (torchrun, N > 1): ONE C1 solve row-sharded over the N GPUs
+(paper_2501_07018_b200.sharded): rank g owns rows
+[g*mb, (g+1)*mb) of A in both layouts and the column block [g*nb, (g+1)*nb);
+per attempt x-bar is all-gathered, K_g^T dy reduce-scattered and 5 step
+scalars all-gathered over NCCL.  Total work is fixed, so scaling = "strong"
+and value = iterations/s of that one solve, timed as the max over ranks.
 """
 from __future__ import annotations
 
@@ -34,6 +38,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# stdout carries exactly one JSON line: keep NCCL's version banner off it
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 METRIC = "PDHG iters/sec, time to 1e-4 rel. KKT, achieved HBM GB/s vs peak"
 UNIT = "iters/s"
@@ -174,50 +181,68 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl")
     device = local if world > 1 else 0
 
-    p = P.generate("c1", rank, sources=args.sources, sinks=args.sinks)
+    # every rank builds the same instance; the sharded solve keeps its shard
+    p = P.generate("c1", 0, sources=args.sources, sinks=args.sinks)
     m, n, nnz = p.rows(), p.cols(), p.a.nonzeros()
     K, W = args.steps, args.warmup
+    if world > 1 or args.sharded:
+        from paper_2501_07018_b200 import sharded as S
+        if dist is None:  # --sharded at N=1: the same path over a 1-rank NCCL communicator
+            solve = lambda o: S.solve_sharded(p, o, 0, 1, S.nccl_unique_id())  # noqa: E731
+        else:
+            solve = lambda o: S.solve_distributed(p, o)  # noqa: E731
+    else:
+        solve = lambda o: P.solve(p, o)  # noqa: E731
 
-    # untimed warm-up solve (context, module load, allocator)
-    P.solve(p, _options(P, 64, 0, device=device))
+    # untimed warm-up solve (context, module load, allocator, NCCL init)
+    solve(_options(P, 64, 0, device=device))
 
     if dist is not None:
         dist.barrier()
     with ClockSampler(device) as clocks:
-        res = P.solve(p, _options(P, K, W, device=device))
+        res = solve(_options(P, K, W, device=device))
     timed = res.timed_seconds
     if dist is not None:
         import torch
         t = torch.tensor([timed], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         timed = float(t.item())
-    value = world * res.timed_iterations / timed
+    value = res.timed_iterations / timed  # one solve (sharded when N > 1)
 
     # e2e: through the C-ABI from host buffers, K iterations, wall clock
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
-    e2e_res = P.solve(p, _options(P, K, 0, device=device))
+    e2e_res = solve(_options(P, K, 0, device=device))
     e2e_wall = time.perf_counter() - t0
     if dist is not None:
         import torch
         t = torch.tensor([e2e_wall], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_wall = float(t.item())
-    e2e_value = world * e2e_res.iterations / e2e_wall
+    e2e_value = e2e_res.iterations / e2e_wall
 
-    # kernel roofline from an instrumented run (CUDA events per launch)
-    prof = P.solve(p, _options(P, K, W, device=device, profile_kernels=True))
     kb = step_kernel_bytes(m, n, nnz)
     names = ["primal_pass", "row_pass", "col_pass"]
     per = {}
-    for q, nm in enumerate(names):
-        launches = max(prof.kernel_launches[q], 1)
-        mean_s = prof.kernel_seconds[q] / launches
-        per[nm] = {"mean_us": mean_s * 1e6, "bytes": kb[nm],
-                   "gbs": kb[nm] / mean_s / 1e9 if mean_s > 0 else 0.0}
-    total_kernel_s = sum(prof.kernel_seconds[:3])
-    dom = max(names, key=lambda nm: prof.kernel_seconds[names.index(nm)])
+    if world == 1 and not args.sharded:
+        # kernel roofline from an instrumented run (CUDA events per launch)
+        prof = P.solve(p, _options(P, K, W, device=device, profile_kernels=True))
+        for q, nm in enumerate(names):
+            launches = max(prof.kernel_launches[q], 1)
+            mean_s = prof.kernel_seconds[q] / launches
+            per[nm] = {"mean_us": mean_s * 1e6, "bytes": kb[nm],
+                       "gbs": kb[nm] / mean_s / 1e9 if mean_s > 0 else 0.0}
+        total_kernel_s = sum(prof.kernel_seconds[:3])
+        dom = max(names, key=lambda nm: prof.kernel_seconds[names.index(nm)])
+        attempts_prof = max(prof.kernel_launches[0], 1)
+    else:
+        # sharded: per-GPU share of the algorithmic step bytes over the
+        # measured time per attempt (collectives included in the time)
+        t_att = timed / max(res.timed_attempts, 1)
+        share = sum(kb.values()) / world
+        per["sharded_attempt"] = {"mean_us": t_att * 1e6, "bytes": share, "gbs": share / t_att / 1e9}
+        total_kernel_s, dom, attempts_prof = t_att, "sharded_attempt", 1
     peak, peak_src = _peaks()
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -226,13 +251,13 @@ def run_ours(args) -> None:
             traffic = json.load(open(prof_json)).get(dom)
         except Exception:
             traffic = None
-    step_bytes = sum(kb.values())
-    attempt_s = total_kernel_s / max(prof.kernel_launches[0], 1)
+    step_bytes = sum(kb.values()) / world
+    attempt_s = total_kernel_s / attempts_prof
 
     # time to BASELINE's 1e-4 relative KKT (SURVEY §8(d) mapping), polishing on
     tol = P.relative_tolerances(p)
-    ttt = P.solve(p, P.SolverOptions(tolerances=P.TerminationTolerances(*tol),
-                                     iteration_limit=100000, device=device))
+    ttt = solve(P.SolverOptions(tolerances=P.TerminationTolerances(*tol),
+                                iteration_limit=100000, device=device))
 
     if rank != 0:
         if dist is not None:
@@ -248,14 +273,16 @@ def run_ours(args) -> None:
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
-    launches = res.timed_attempts * 3 + getattr(res, "timed_cadence_kernels", 0)
+    # primal, row, column passes per attempt (one GPU); sharded attempts add
+    # the partial product, column epilogue, totals and decision kernels
+    launches = res.timed_attempts * (3 if (world == 1 and not args.sharded) else 6)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": 1e3 * timed / max(res.timed_iterations, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C1 transportation recipe of BASELINE.json configs[1])",
         "config": {"workload": WORKLOAD, "m": m, "n": n, "nnz": nnz, "mode": "perf",
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": f"rowshard{world}" if (world > 1 or args.sharded) else "single",
                    "l2": "inputs larger than L2 (656 MB streamed per iteration)",
                    "tolerances": "unreachable (fixed-work window)",
                    "timed_attempts": res.timed_attempts, "restarts": res.restarts},
@@ -300,7 +327,7 @@ def run_reference(args) -> None:
     line = {
         "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": UNIT,
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
-        "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded C1 transportation recipe of BASELINE.json configs[1])",
         "config": {"workload": WORKLOAD, "bounded_sample_iterations": iters},
         "cpu_baseline": cpu,
@@ -321,6 +348,8 @@ def main():
     ap.add_argument("--cpu-iterations", type=int, default=96)
     ap.add_argument("--ref-iterations", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded solve even at N=1 (1-rank NCCL communicator)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

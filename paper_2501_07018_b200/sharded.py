@@ -87,7 +87,14 @@ def extract_shard(problem: LpProblem, rank: int, world: int) -> dict:
         N.lib().pdlp_shard_free(owner)
 
 
+def _quiet_nccl() -> None:
+    # NCCL_DEBUG=VERSION (or unset on some images) prints a banner on stdout
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
+
+
 def nccl_unique_id() -> bytes:
+    _quiet_nccl()
     buf = C.create_string_buffer(128)
     _check(N.lib().pdlp_nccl_unique_id(buf))
     return buf.raw
@@ -98,6 +105,7 @@ def solve_sharded(problem: LpProblem, options: SolverOptions | None, rank: int, 
     """This process's rank of a `world`-GPU sharded solve (NCCL).  Every
     rank gets the whole result."""
     options = options or SolverOptions(mode="perf")
+    _quiet_nccl()
     if len(nccl_id) != 128:
         raise ValueError("nccl_id must be the 128-byte ncclUniqueId")
     return run_solve(N.lib(), "pdlp_solve_sharded", problem, options, to_c_options(options),
