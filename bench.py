@@ -288,9 +288,10 @@ def run_ours(args) -> None:
                    "timed_attempts": res.timed_attempts, "restarts": res.restarts},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": problem_bytes(p) / K,
                 "d2h_bytes_per_step": 8 * (2 * n + m) / K,
-                "note": f"pdlp_solve() wall time from host buffers for K={K} iterations incl. "
-                        f"upload {e2e_res.upload_seconds:.3f}s and preconditioning "
-                        f"{e2e_res.precondition_seconds:.3f}s"},
+                "note": f"pdlp_solve() wall time from host buffers for K={K} iterations: "
+                        f"wall {e2e_wall:.3f}s = upload+validation {e2e_res.upload_seconds:.3f}s + "
+                        f"preconditioning {e2e_res.precondition_seconds:.3f}s + loop "
+                        f"{e2e_res.loop_seconds:.3f}s + rest (init, result copy, teardown)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": per[dom]["gbs"], "peak": peak,
                      "unit": "GB/s", "frac": per[dom]["gbs"] / peak, "traffic": traffic,
                      "peak_source": peak_src, "per_kernel": per,
