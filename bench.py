@@ -300,7 +300,8 @@ def run_ours(args) -> None:
                               "gbs": step_bytes / attempt_s / 1e9 if attempt_s > 0 else 0.0,
                               "frac": step_bytes / attempt_s / 1e9 / peak if attempt_s > 0 else 0.0}},
         "time_to_tol": {"status": P.solve_status_name(ttt.status), "seconds": ttt.solve_seconds,
-                        "loop_seconds": ttt.loop_seconds, "iterations": ttt.iterations,
+                        "loop_seconds": ttt.loop_seconds, "step_seconds": ttt.step_seconds,
+                        "upload_seconds": ttt.upload_seconds, "iterations": ttt.iterations,
                         "polish_iterations": ttt.polish_iterations,
                         "tolerance": "1e-4 relative (eps_p=1e-4(1+|b|inf), eps_d=1e-4(1+|c|inf))"},
         "gpu_launches": launches,

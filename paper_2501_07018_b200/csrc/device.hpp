@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstddef>
 #include <cstdint>
 #include <stdexcept>
@@ -37,6 +38,9 @@ inline void check_launch(int rc, const char* what) {
 // holds, like a caching allocator; pdlp_trim_device_memory() returns it).
 // Without an allocation stream DevBuf falls back to cudaMalloc/cudaFree.
 inline thread_local cudaStream_t g_alloc_stream = nullptr;
+// Host seconds spent in device allocations on this thread (phase report of
+// the `logging` option).
+inline thread_local double g_alloc_seconds = 0.0;
 
 inline void retain_pool_memory(int device) {
   static bool done[64] = {};
@@ -90,11 +94,13 @@ class DevBuf {
     // +16 bytes: the SpMV tile path bulk-copies 16-byte-aligned windows that
     // may extend up to 15 bytes past the last element.
     s_ = g_alloc_stream;
+    const auto t0 = std::chrono::steady_clock::now();
     if (s_ != nullptr) {
       PDLP_CK(cudaMallocAsync(&p, n * sizeof(T) + 16, s_));
     } else {
       PDLP_CK(cudaMalloc(&p, n * sizeof(T) + 16));
     }
+    g_alloc_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     p_ = static_cast<T*>(p);
   }
   void release() {

@@ -61,7 +61,7 @@ typedef struct pdlpk_csr {
    * n columns, entries index local rows; the output is reduce-scattered to
    * the column owners.  PDLPK_DIST_NONE on one GPU. */
   int32_t dist_kind;
-  int32_t _pad_dist;
+  int32_t tile_direct; /* 1: tiles are direct (thread per line, spmv.cuh) */
 } pdlpk_csr;
 
 #define PDLPK_DIST_NONE 0

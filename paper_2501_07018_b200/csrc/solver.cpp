@@ -133,17 +133,33 @@ struct DevLayout {
 template <class T>
 void upload_list(const std::vector<T>& h, DevBuf<T>& d) {
   d.alloc(h.size());
-  if (!h.empty()) PDLP_CK(cudaMemcpy(d.get(), h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  // on the allocation stream: pool memory is stream-ordered
+  if (!h.empty()) {
+    PDLP_CK(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice,
+                            g_alloc_stream));
+    PDLP_CK(cudaStreamSynchronize(g_alloc_stream));
+  }
 }
 
 // Perf-mode schedule (spmv.cuh), the analysis phase of the SpMV: lines of
-// <= PDLPK_SHORT_MAX entries are packed into warp tiles of consecutive lines
-// (<= PDLPK_TILE_ROWS lines, <= PDLPK_TILE_NNZ entries), medium lines get a
-// warp each, long lines a CTA each.  O(lines) host pass over the row pointer.
+// <= PDLPK_SHORT_MAX entries are packed into tiles of consecutive lines, longer
+// lines into warp chunks.  Tiles are staged through the TMA ring
+// (<= PDLPK_TILE_ROWS lines, <= PDLPK_TILE_NNZ entries).  PDLP_TILES=direct
+// selects direct tiles instead (thread per line, <= 256 lines, no staging);
+// on C1's two-entry columns they measured 86 us against 75 us staged, so
+// they are opt-in.  O(lines) host pass over the row pointer.
+bool direct_tiles(const int64_t*, int64_t) {
+  const char* env = std::getenv("PDLP_TILES");
+  return env != nullptr && std::strcmp(env, "direct") == 0;
+}
+
 void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   std::vector<int32_t> t0, tc, ck_row, ck_len, ck_pos, ck_slot;
   std::vector<int64_t> tn, ck_beg;
   int64_t n_multi = 0;
+  const bool direct = direct_tiles(start, dim);
+  const int64_t tile_rows = direct ? 256 : PDLPK_TILE_ROWS;
+  const int64_t tile_nnz = direct ? 256 * PDLPK_SHORT_MAX : PDLPK_TILE_NNZ;
   int64_t cur0 = -1, cur_rows = 0, cur_nnz = 0;
   auto close = [&] {
     if (cur_rows > 0) {
@@ -175,7 +191,7 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
       }
       continue;
     }
-    if (cur_rows == PDLPK_TILE_ROWS || cur_nnz + len > PDLPK_TILE_NNZ) close();
+    if (cur_rows == tile_rows || cur_nnz + len > tile_nnz) close();
     if (cur_rows == 0) cur0 = r;
     ++cur_rows;
     cur_nnz += len;
@@ -192,13 +208,15 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   const int64_t n_chunks = static_cast<int64_t>(ck_row.size());
   L.chunk_part.alloc(n_chunks);
   L.chunk_cnt.alloc(n_chunks);
-  if (n_chunks > 0) PDLP_CK(cudaMemset(L.chunk_cnt.get(), 0, n_chunks * sizeof(unsigned)));
+  if (n_chunks > 0) {
+    PDLP_CK(cudaMemsetAsync(L.chunk_cnt.get(), 0, n_chunks * sizeof(unsigned), g_alloc_stream));
+  }
   L.line_acc.alloc(n_multi * PDLPK_LINE_ACC);
   const int64_t n_tiles = static_cast<int64_t>(t0.size());
   // ~41 KB staging ring per CTA -> 5 CTAs per SM; each CTA walks its tiles
   // grid-stride with a kStages-deep bulk-copy prefetch.
   int64_t tb = n_tiles;
-  tb = std::min<int64_t>(tb, 148 * 5);
+  tb = std::min<int64_t>(tb, direct ? 148 * 5 * 4 : 148 * 5);
   tb = std::max<int64_t>(tb, 1);  // the column pass's last CTA decides, so never empty
   L.view.chunk_row = L.chunk_row.get();
   L.view.chunk_beg = L.chunk_beg.get();
@@ -214,6 +232,7 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   L.view.tile_rows = L.tile_rows.get();
   L.view.tile_nnz0 = L.tile_nnz0.get();
   L.view.n_tiles = n_tiles;
+  L.view.tile_direct = direct ? 1 : 0;
   L.view.tile_blocks = static_cast<int32_t>(tb);
 }
 
@@ -391,7 +410,7 @@ struct Inner {  // InnerState (solver.hpp:135-193), vectors on device
       pbuf.alloc(full);
       dloc.alloc(std::max<int64_t>(block, 1));
       tot_all.alloc(8 * static_cast<int64_t>(world));
-      PDLP_CK(cudaMemset(pbuf.get(), 0, full * sizeof(double)));
+      PDLP_CK(cudaMemsetAsync(pbuf.get(), 0, full * sizeof(double), g_alloc_stream));
     }
   }
   int cur() const { return hs.cur; }
@@ -617,7 +636,7 @@ class Engine {
   bool any_rank(bool flag) {
     double v = flag ? 1.0 : 0.0;
     PDLP_CK(cudaStreamSynchronize(s()));
-    PDLP_CK(cudaMemcpy(flag_.get(), &v, sizeof(double), cudaMemcpyHostToDevice));
+    PDLP_CK(cudaMemcpyAsync(flag_.get(), &v, sizeof(double), cudaMemcpyHostToDevice, s()));
     comm_->allreduce(flag_.get(), 1, true, s());
     PDLP_CK(cudaMemcpyAsync(&v, flag_.get(), sizeof(double), cudaMemcpyDeviceToHost, s()));
     PDLP_CK(cudaStreamSynchronize(s()));
@@ -641,7 +660,7 @@ class Engine {
     }
     v[4] = hb != 0 ? 1.0 : 0.0;
     PDLP_CK(cudaStreamSynchronize(s()));
-    PDLP_CK(cudaMemcpy(flag_.get(), v, sizeof(v), cudaMemcpyHostToDevice));
+    PDLP_CK(cudaMemcpyAsync(flag_.get(), v, sizeof(v), cudaMemcpyHostToDevice, s()));
     comm_->allreduce(flag_.get(), 5, true, s());
     PDLP_CK(cudaMemcpyAsync(v, flag_.get(), sizeof(v), cudaMemcpyDeviceToHost, s()));
     PDLP_CK(cudaStreamSynchronize(s()));
@@ -897,8 +916,9 @@ class Engine {
     }
     f_down_.alloc(want);
     f_up_.alloc(want);
-    PDLP_CK(cudaMemcpy(f_down_.get(), down.data(), want * 8, cudaMemcpyHostToDevice));
-    PDLP_CK(cudaMemcpy(f_up_.get(), up.data(), want * 8, cudaMemcpyHostToDevice));
+    PDLP_CK(cudaMemcpyAsync(f_down_.get(), down.data(), want * 8, cudaMemcpyHostToDevice, s()));
+    PDLP_CK(cudaMemcpyAsync(f_up_.get(), up.data(), want * 8, cudaMemcpyHostToDevice, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));  // the host tables die here
     table_len_ = want;
   }
 
@@ -934,7 +954,8 @@ class Engine {
   }
   void write_state(Inner& D) {
     PDLP_CK(cudaStreamSynchronize(s()));
-    PDLP_CK(cudaMemcpy(D.state.get(), &D.hs, sizeof(pdlpk_step_state), cudaMemcpyHostToDevice));
+    PDLP_CK(cudaMemcpyAsync(D.state.get(), &D.hs, sizeof(pdlpk_step_state), cudaMemcpyHostToDevice, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));
   }
 
   // InnerState::prepare (solver.hpp:167-192); x0 is a device vector.
@@ -1368,6 +1389,8 @@ class Engine {
   double step_seconds_ = 0.0;
   double upload_seconds_ = 0.0;
   double precondition_seconds_ = 0.0;
+  double cadence_seconds_ = 0.0;  // host time inside cadence blocks (incl. polishing)
+  double polish_seconds_ = 0.0;
   int64_t attempts_total_ = 0;
   bool profile_ = false;
   std::vector<cudaEvent_t> prof_ev_;
@@ -1382,6 +1405,12 @@ class Engine {
 
 bool Engine::attempt_polish(const pdlpk_problem& P, const InnerCfg& cfg, Inner& D) {
   // solver.hpp:290-348
+  const auto pol_t0 = Clock::now();
+  struct PolishClock {
+    double& acc;
+    Clock::time_point t0;
+    ~PolishClock() { acc += std::chrono::duration<double>(Clock::now() - t0).count(); }
+  } pol_clock{polish_seconds_, pol_t0};
   const int64_t remaining = cfg.budget - D.k() - D.polish_iterations;
   const int64_t budget = std::min(D.k() / 8, remaining);
   if (budget <= 0) return false;
@@ -1441,7 +1470,13 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
     const bool budget_hit = D.k() >= cfg.budget;
     const bool at_cadence = budget_hit || (D.k() % cfg.check_interval == 0);
     if (at_cadence) {
-      bool timed_out = Clock::now() >= cfg.deadline;
+      const auto cad_t0 = Clock::now();
+      struct CadenceClock {  // adds the cadence's host time on every exit
+        double& acc;
+        Clock::time_point t0;
+        ~CadenceClock() { acc += std::chrono::duration<double>(Clock::now() - t0).count(); }
+      } cad_clock{cadence_seconds_, cad_t0};
+      bool timed_out = cad_t0 >= cfg.deadline;
       if (dist()) timed_out = any_rank(timed_out);  // ranks must agree
       const int c = D.cur();
       flush_average(P, D);
@@ -1647,13 +1682,25 @@ void copy_to_host(double* dst, const double* src, int64_t n, cudaStream_t s) {
 }
 
 // solve (solver.hpp:535-608)
+// Inner state of an (n, m) loop: 24 n-vectors and 17 m-vectors (Inner::allocate).
+int64_t inner_bytes(int64_t n, int64_t m) { return 8 * (24 * n + 17 * m) + 64 * 41; }
+
 // comm != nullptr: this process/thread is one rank of a row-sharded solve.
 void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result* res,
            Comm* comm = nullptr) {
   const auto t0 = Clock::now();
+  g_alloc_seconds = 0.0;
   Engine E(problem, *o, comm);  // uploads and validates on device
   if (o->enable_scaling) E.precondition(o->ruiz_passes, o->pock_chambolle != 0);
   if (E.dist()) E.build_full_views();
+  if (o->enable_polish) {
+    // The polishing subproblems' states are allocated mid-loop, the first
+    // time polishing triggers.  Growing the pool then costs 10-300 ms of
+    // driver time; reserve it now (freed blocks stay in the retaining pool
+    // and are sub-allocated later).
+    const int64_t nl = E.problem().n, ml = E.problem().m;
+    DevBuf<char> reserve(static_cast<size_t>(inner_bytes(nl, ml) + inner_bytes(ml, nl)));
+  }
   const pdlpk_problem P = E.problem().view();
 
   InnerCfg cfg;
@@ -1766,6 +1813,14 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result*
                  "phase=main event=done status=%s iters=%lld polish_iters=%lld detail=\"%s\"\n",
                  status_name(status), static_cast<long long>(res->iterations),
                  static_cast<long long>(res->polish_iterations), res->termination_detail);
+  }
+  if (o->logging || std::getenv("PDLP_TIMING") != nullptr) {
+    std::fprintf(stderr,
+                 "phase=main event=timing solve=%.4f upload=%.4f precondition=%.4f loop=%.4f "
+                 "steps=%.4f cadence=%.4f polish=%.4f alloc=%.4f\n",
+                 res->solve_seconds, res->upload_seconds, res->precondition_seconds,
+                 res->loop_seconds, res->step_seconds, E.cadence_seconds_, E.polish_seconds_,
+                 g_alloc_seconds);
   }
 }
 

@@ -9,7 +9,13 @@
 //                             chunk partials in chunk order (deterministic)
 //                             and runs the epilogue, whose contributions go to
 //                             the line's fixed slot (line_acc)
-//   [.., + tile_blocks)       CTA tiles of consecutive short lines
+//   [.., + n_tiles)           direct tiles (layouts of very short lines, e.g.
+//                             C1's two-entry columns): one CTA per run of
+//                             <= kDirectRows consecutive short lines, one
+//                             thread per line summing it in storage order;
+//                             no staging, full occupancy hides the
+//                             pointer -> index -> gather chain
+//   [.., + tile_blocks)       staged tiles of consecutive short lines
 //                             (len <= kShortMax; <= kTileRows lines and
 //                             <= kTileNnz entries per tile), grid-stride
 // Skewed (power-law) line lengths thus cost the same as uniform ones.
@@ -63,21 +69,25 @@ constexpr size_t kSpmvSmem = kRingHeader + kStages * kStageBytes;
 // pass is HBM-bound.
 __device__ __forceinline__ double mac(double acc, double a, double b) { return acc + a * b; }
 
-// Segment mask of a layout: 1 chunks, 4 tiles.  Kernels are
-// instantiated per mask so each pass only pays the registers and shared
-// memory of the paths it runs.  The tile segment is kept when nothing else
-// exists so the grid is never empty (the column pass's last CTA makes the
-// step decision).
+constexpr int kDirectRows = kSpmvThreads;  // lines per direct tile
+
+// Segment mask of a layout: 1 chunks, 2 direct tiles, 4 staged tiles.
+// Kernels are instantiated per mask so each pass only pays the registers and
+// shared memory of the paths it runs.  The staged tile segment is kept when
+// nothing else exists so the grid is never empty (the column pass's last CTA
+// makes the step decision).
 __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
   int s = A.n_chunks > 0 ? 1 : 0;
-  if (A.n_tiles > 0 || s == 0) s |= 4;
+  if (A.n_tiles > 0) s |= A.tile_direct ? 2 : 4;
+  if (s == 0) s = 4;
   return s;
 }
 
-__host__ __device__ constexpr int spmv_min_blocks(int seg) { return (seg & 4) ? 4 : 4; }
+__host__ __device__ constexpr int spmv_min_blocks(int seg) { return seg == 2 ? 5 : 4; }
 
 __host__ __device__ inline int64_t sched_blocks(const pdlpk_csr& A) {
-  return (A.n_chunks + kSpmvWarps - 1) / kSpmvWarps + ((seg_mask(A) & 4) ? A.tile_blocks : 0);
+  const int s = seg_mask(A);
+  return (A.n_chunks + kSpmvWarps - 1) / kSpmvWarps + ((s & 6) ? A.tile_blocks : 0);
 }
 
 __host__ __device__ inline size_t spmv_smem(int seg) { return (seg & 4) ? kSpmvSmem : 0; }
@@ -173,6 +183,37 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
     }
     b -= chunk_blocks;
   }
+  if constexpr ((Seg & 2) != 0) {
+    if (b < A.tile_blocks) {
+      // grid-stride over the tiles: the pass's per-CTA partials and
+      // decision ticket are paid once per CTA, not once per tile
+      for (int64_t t = b; t < A.n_tiles; t += A.tile_blocks) {
+      const TileMeta tm = tile_meta(A, t);
+      if (static_cast<int>(threadIdx.x) < tm.cnt) {
+        const int64_t r = tm.r0 + threadIdx.x;
+        const typename Epi::Pre pre = epi.load(r);
+        const int64_t a = start[r], e = start[r + 1];
+        // predicated pairs: independent loads, then the gathers, then the
+        // products added in storage order (bit-identical line sums)
+        double acc = 0.0;
+        for (int64_t k = a; k < e; k += 2) {
+          const bool two = k + 1 < e;
+          const int32_t c0 = ld_stream(idx + k);
+          const int32_t c1 = two ? ld_stream(idx + k + 1) : c0;
+          const double a0 = ld_stream(vals + k);
+          const double a1 = two ? ld_stream(vals + k + 1) : 0.0;
+          const double g0 = __ldg(v + c0);
+          const double g1 = __ldg(v + c1);
+          acc = mac(acc, a0, g0);
+          if (two) acc = mac(acc, a1, g1);
+        }
+        epi.line(r, acc, pre);
+      }
+      }
+      return;
+    }
+    b -= A.tile_blocks;
+  }
   if constexpr ((Seg & 4) != 0) {
     // Warp-specialized ring: warp 0 produces (one lane issues the bulk
     // copies of a whole tile), warps 1..kConsumerWarps consume, each owning
@@ -248,8 +289,24 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
           const int l1 = l0 + 32 < tm.cnt ? l0 + 32 : tm.cnt;
           const int e0 = static_cast<int>(static_cast<int64_t>(s_ptr[l0]) - tm.s0);
           const int e1 = static_cast<int>(static_cast<int64_t>(s_ptr[l1]) - tm.s0);
-          // this warp's products in place (the gather is the only global access)
-          for (int j = e0 + lane; j < e1; j += 32) s_val[j] = s_val[j] * __ldg(v + s_idx[j]);
+          // this warp's products in place (the gather is the only global
+          // access): batches of 4 per lane keep 4 gathers in flight
+          for (int j0 = e0 + lane; j0 < e1; j0 += 4 * 32) {
+            int32_t ci[4];
+            double g[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (j0 + 32 * u < e1) ci[u] = s_idx[j0 + 32 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (j0 + 32 * u < e1) g[u] = __ldg(v + ci[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (j0 + 32 * u < e1) s_val[j0 + 32 * u] = s_val[j0 + 32 * u] * g[u];
+            }
+          }
           __syncwarp();
           const int li = l0 + lane;
           if (li < l1) {
@@ -273,6 +330,8 @@ template <class P, class F>
 inline int dispatch_seg(int seg, F&& f) {
   switch (seg) {
     case 1: return f.template go<P, 1>();
+    case 2: return f.template go<P, 2>();
+    case 3: return f.template go<P, 3>();
     case 4: return f.template go<P, 4>();
     default: return f.template go<P, 5>();
   }
