@@ -46,8 +46,9 @@ typedef struct pdlpk_csr {
   const int32_t* chunk_len;  /* entries of each chunk */
   const int32_t* chunk_pos;  /* index in line | (chunks in line << 16) */
   const int32_t* chunk_slot; /* multi-chunk line slot, -1 for single-chunk lines */
-  int64_t n_chunks;
-  int64_t n_multi;     /* multi-chunk lines */
+  int64_t n_chunks;     /* warp chunks first, then n_cta_chunks CTA chunks */
+  int64_t n_cta_chunks; /* chunks of lines > PDLPK_WARP_LINE_MAX, one CTA each */
+  int64_t n_multi;      /* multi-chunk lines */
   double* chunk_part;  /* n_chunks partial sums */
   unsigned* chunk_cnt; /* arrival counters, at each line's first chunk */
   double* line_acc;    /* n_multi * PDLPK_LINE_ACC epilogue contributions */
@@ -71,7 +72,10 @@ typedef struct pdlpk_csr {
 /* Schedule limits (spmv.cuh) the host planner must respect. */
 #define PDLPK_SHORT_MAX 32
 #ifndef PDLPK_CHUNK
-#define PDLPK_CHUNK 2048
+#define PDLPK_CHUNK 2048 /* entries per CTA chunk: 8 warps x one 256-entry batch */
+#endif
+#ifndef PDLPK_WARP_LINE_MAX
+#define PDLPK_WARP_LINE_MAX 2048 /* longer lines are processed by CTA chunks */
 #endif
 #define PDLPK_LINE_ACC 4
 #define PDLPK_TILE_NNZ 512

@@ -148,9 +148,13 @@ void upload_list(const std::vector<T>& h, DevBuf<T>& d) {
 // selects direct tiles instead (thread per line, <= 256 lines, no staging);
 // on C1's two-entry columns they measured 86 us against 75 us staged, so
 // they are opt-in.  O(lines) host pass over the row pointer.
-bool direct_tiles(const int64_t*, int64_t) {
+bool direct_tiles(const int64_t* start, int64_t dim) {
   const char* env = std::getenv("PDLP_TILES");
-  return env != nullptr && std::strcmp(env, "direct") == 0;
+  if (env == nullptr || std::strcmp(env, "direct") != 0) return false;
+  for (int64_t r = 0; r < dim; ++r) {  // kernels never mix direct tiles and CTA chunks
+    if (start[r + 1] - start[r] > PDLPK_WARP_LINE_MAX) return false;
+  }
+  return true;
 }
 
 void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
@@ -171,10 +175,23 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
     cur_rows = 0;
     cur_nnz = 0;
   };
+  // CTA chunks are collected apart and appended after the warp chunks.
+  std::vector<int32_t> cc_row, cc_len, cc_pos, cc_slot;
+  std::vector<int64_t> cc_beg;
   for (int64_t r = 0; r < dim; ++r) {
     const int64_t len = start[r + 1] - start[r];
-    if (len > PDLPK_SHORT_MAX) {
-      // a long line: consecutive warp chunks of <= PDLPK_CHUNK entries
+    if (len > PDLPK_SHORT_MAX && len <= PDLPK_WARP_LINE_MAX) {
+      // a medium line: one warp
+      close();
+      ck_row.push_back(static_cast<int32_t>(r));
+      ck_beg.push_back(start[r]);
+      ck_len.push_back(static_cast<int32_t>(len));
+      ck_pos.push_back(static_cast<int32_t>(1 << 16));
+      ck_slot.push_back(-1);
+      continue;
+    }
+    if (len > PDLPK_WARP_LINE_MAX) {
+      // a long line: consecutive CTA chunks of <= PDLPK_CHUNK entries
       close();
       int64_t nch = (len + PDLPK_CHUNK - 1) / PDLPK_CHUNK;
       const int64_t per = (len + nch - 1) / nch;  // balanced chunk length
@@ -183,11 +200,11 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
       const int32_t slot = nch > 1 ? static_cast<int32_t>(n_multi++) : -1;
       for (int64_t q = 0; q < nch; ++q) {
         const int64_t b = start[r] + q * per;
-        ck_row.push_back(static_cast<int32_t>(r));
-        ck_beg.push_back(b);
-        ck_len.push_back(static_cast<int32_t>(std::min(per, start[r + 1] - b)));
-        ck_pos.push_back(static_cast<int32_t>(q | (nch << 16)));
-        ck_slot.push_back(slot);
+        cc_row.push_back(static_cast<int32_t>(r));
+        cc_beg.push_back(b);
+        cc_len.push_back(static_cast<int32_t>(std::min(per, start[r + 1] - b)));
+        cc_pos.push_back(static_cast<int32_t>(q | (nch << 16)));
+        cc_slot.push_back(slot);
       }
       continue;
     }
@@ -197,6 +214,12 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
     cur_nnz += len;
   }
   close();
+  const int64_t n_cta_chunks = static_cast<int64_t>(cc_row.size());
+  ck_row.insert(ck_row.end(), cc_row.begin(), cc_row.end());
+  ck_beg.insert(ck_beg.end(), cc_beg.begin(), cc_beg.end());
+  ck_len.insert(ck_len.end(), cc_len.begin(), cc_len.end());
+  ck_pos.insert(ck_pos.end(), cc_pos.begin(), cc_pos.end());
+  ck_slot.insert(ck_slot.end(), cc_slot.begin(), cc_slot.end());
   upload_list(t0, L.tile_row0);
   upload_list(tc, L.tile_rows);
   upload_list(tn, L.tile_nnz0);
@@ -224,6 +247,7 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   L.view.chunk_pos = L.chunk_pos.get();
   L.view.chunk_slot = L.chunk_slot.get();
   L.view.n_chunks = n_chunks;
+  L.view.n_cta_chunks = n_cta_chunks;
   L.view.n_multi = n_multi;
   L.view.chunk_part = L.chunk_part.get();
   L.view.chunk_cnt = L.chunk_cnt.get();
@@ -441,6 +465,27 @@ struct InnerCfg {  // InnerConfig (solver.hpp:114-133)
   bool swapped = false;
 };
 
+// Pinned host words the cadence reads back, one set per host thread and kept
+// for its lifetime: a cudaMallocHost / cudaFreeHost pair per solve costs up
+// to tens of milliseconds of driver time (cudaFreeHost synchronizes).
+struct PinnedScratch {
+  double* slots = nullptr;  // 64
+  int* islots = nullptr;    // 8
+  PinnedScratch() {
+    PDLP_CK(cudaMallocHost(&slots, 64 * sizeof(double)));
+    PDLP_CK(cudaMallocHost(&islots, 8 * sizeof(int)));
+  }
+  ~PinnedScratch() {
+    cudaFreeHost(slots);
+    cudaFreeHost(islots);
+  }
+};
+
+PinnedScratch& pinned_scratch() {
+  thread_local PinnedScratch p;
+  return p;
+}
+
 // ------------------------------------------------------------------ engine ---
 class Engine {
  public:
@@ -577,14 +622,14 @@ class Engine {
     prob_.row_scale = dev_fill(m, 1.0, s());
     prob_.col_scale = dev_fill(n, 1.0, s());
     slots_.alloc(kSlots);
-    PDLP_CK(cudaMallocHost(&host_slots_, 64 * sizeof(double)));
+    host_slots_ = pinned_scratch().slots;
     red_scratch_.alloc(std::max<int64_t>(pdlpk_red_scratch_doubles(), 8 * int64_t(shards_) + 64));
     // the gap runs on whole vectors (gathered when sharded)
     for (auto& w : gap_work_) {
       w.alloc(std::max(pdlpk_gap_work_bytes(n_glob_, m_glob_), pdlpk_gap_work_bytes(m_glob_, n_glob_)));
     }
     islots_.alloc(8);
-    PDLP_CK(cudaMallocHost(&host_islots_, 8 * sizeof(int)));
+    host_islots_ = pinned_scratch().islots;
     zeros_n_.alloc(n);
     zeros_m_.alloc(m);
     dev_zero(zeros_n_.get(), n, s());
@@ -595,8 +640,6 @@ class Engine {
   ~Engine() {
     if (comm_ != nullptr) pdlpk_set_red_log(nullptr);
     alloc_scope_.reset();  // members free on their own allocation stream
-    if (host_slots_ != nullptr) cudaFreeHost(host_slots_);
-    if (host_islots_ != nullptr) cudaFreeHost(host_islots_);
     for (cudaEvent_t e : prof_ev_) cudaEventDestroy(e);
   }
 

@@ -2,13 +2,16 @@
 //
 // One launch covers up to two segments of CTAs (schedule built once per
 // solve from the line lengths, see solver.cpp build_schedule):
-//   [0, ceil(n_chunks/8))     one warp per chunk of a line longer than
-//                             kShortMax (chunks of <= kChunk entries, 8
-//                             independent accumulator chains per lane); the
-//                             last-arriving warp of a multi-chunk line sums the
-//                             chunk partials in chunk order (deterministic)
-//                             and runs the epilogue, whose contributions go to
-//                             the line's fixed slot (line_acc)
+//   [0, ceil(n_wchunks/8))    one warp per line of kShortMax < len <=
+//                             PDLPK_WARP_LINE_MAX entries (8 independent
+//                             accumulator chains per lane)
+//   [.., + n_cta_chunks)      one CTA per chunk (<= kChunk entries) of a
+//                             longer line, a 256-entry slice per warp, warp
+//                             sums added in warp order; the last-arriving CTA
+//                             of a multi-chunk line sums the chunk partials in
+//                             chunk order (deterministic) and runs the
+//                             epilogue, whose contributions go to the line's
+//                             fixed slot (line_acc)
 //   [.., + n_tiles)           direct tiles (layouts of very short lines, e.g.
 //                             C1's two-entry columns): one CTA per run of
 //                             <= kDirectRows consecutive short lines, one
@@ -77,7 +80,8 @@ constexpr int kDirectRows = kSpmvThreads;  // lines per direct tile
 // nothing else exists so the grid is never empty (the column pass's last CTA
 // makes the step decision).
 __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
-  int s = A.n_chunks > 0 ? 1 : 0;
+  int s = A.n_chunks > A.n_cta_chunks ? 1 : 0;
+  if (A.n_cta_chunks > 0) s |= 8;
   if (A.n_tiles > 0) s |= A.tile_direct ? 2 : 4;
   if (s == 0) s = 4;
   return s;
@@ -85,9 +89,13 @@ __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
 
 __host__ __device__ constexpr int spmv_min_blocks(int seg) { return seg == 2 ? 5 : 4; }
 
+__host__ __device__ inline int64_t warp_chunk_blocks(const pdlpk_csr& A) {
+  return (A.n_chunks - A.n_cta_chunks + kSpmvWarps - 1) / kSpmvWarps;
+}
+
 __host__ __device__ inline int64_t sched_blocks(const pdlpk_csr& A) {
   const int s = seg_mask(A);
-  return (A.n_chunks + kSpmvWarps - 1) / kSpmvWarps + ((s & 6) ? A.tile_blocks : 0);
+  return warp_chunk_blocks(A) + A.n_cta_chunks + ((s & 6) ? A.tile_blocks : 0);
 }
 
 __host__ __device__ inline size_t spmv_smem(int seg) { return (seg & 4) ? kSpmvSmem : 0; }
@@ -106,6 +114,31 @@ __device__ __forceinline__ Win win(const void* base, int64_t first, int64_t coun
   const uintptr_t ahi = (hi + 15) & ~uintptr_t(15);
   return Win{reinterpret_cast<const char*>(alo), count > 0 ? static_cast<uint32_t>(ahi - alo) : 0u,
              static_cast<uint32_t>(lo - alo)};
+}
+
+// Entries [k0, hi) stepping 32 (one lane's share of a warp's range), in
+// predicated batches of 8 independent loads then 8 gathers; acc[u] takes
+// every 8th of the lane's entries.
+__device__ __forceinline__ void warp_batches(const int32_t* __restrict__ idx,
+                                             const double* __restrict__ vals,
+                                             const double* __restrict__ v, int64_t k0, int64_t hi,
+                                             double (&acc)[8]) {
+  for (int64_t base = k0; base < hi; base += 8 * 32) {
+    int32_t ci[8];
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t k = base + u * 32;
+      if (k < hi) {
+        ci[u] = ld_stream(idx + k);
+        a[u] = ld_stream(vals + k);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (base + u * 32 < hi) acc[u] = mac(acc[u], a[u], __ldg(v + ci[u]));
+    }
+  }
 }
 
 struct TileMeta {
@@ -127,10 +160,10 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
   const int warp = threadIdx.x >> 5;
   int64_t b = blockIdx.x;
   if constexpr ((Seg & 1) != 0) {
-    const int64_t chunk_blocks = (A.n_chunks + kSpmvWarps - 1) / kSpmvWarps;
+    const int64_t chunk_blocks = warp_chunk_blocks(A);
     if (b < chunk_blocks) {
       const int64_t c = b * kSpmvWarps + warp;
-      if (c < A.n_chunks) {
+      if (c < A.n_chunks - A.n_cta_chunks) {
         const int64_t r = A.chunk_row[c];
         const int64_t lo = A.chunk_beg[c];
         const int64_t hi = lo + A.chunk_len[c];
@@ -138,25 +171,10 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
         const int nch = pos >> 16;
         typename Epi::Pre pre{};
         if (nch == 1 && lane == 0) pre = epi.load(r);
-        // predicated batches of 8 entries per lane: a chunk (<= kChunk =
-        // 8 x 32 entries) is one batch of independent loads, then its gathers
+        // predicated batches of 8 entries per lane: a chunk of <= 256
+        // entries is one batch of independent loads, then its gathers
         double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        for (int64_t base = lo + lane; base < hi; base += 8 * 32) {
-          int32_t ci[8];
-          double a[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int64_t k = base + u * 32;
-            if (k < hi) {
-              ci[u] = ld_stream(idx + k);
-              a[u] = ld_stream(vals + k);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (base + u * 32 < hi) acc[u] = mac(acc[u], a[u], __ldg(v + ci[u]));
-          }
-        }
+        warp_batches(idx, vals, v, lo + lane, hi, acc);
         const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
         const double t = warp_sum(s);
         if (nch == 1) {
@@ -182,6 +200,56 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
       return;
     }
     b -= chunk_blocks;
+  }
+  if constexpr ((Seg & 8) != 0) {
+    if (b < A.n_cta_chunks) {
+      // One CTA per chunk of <= kChunk entries: warp w takes one slice of
+      // <= 256 entries (a single batch of independent loads), the 8 warp
+      // sums are added in warp order, thread 0 runs the epilogue or the
+      // ordered multi-chunk combine.  C1's 2,000-entry rows: one round trip
+      // per row instead of eight per warp.
+      const int64_t c = (A.n_chunks - A.n_cta_chunks) + b;
+      const int64_t r = A.chunk_row[c];
+      const int64_t lo = A.chunk_beg[c];
+      const int64_t hi = lo + A.chunk_len[c];
+      const int pos = A.chunk_pos[c];
+      const int nch = pos >> 16;
+      const int64_t per = (((hi - lo) + kSpmvWarps - 1) / kSpmvWarps + 31) & ~int64_t(31);
+      const int64_t wlo = lo + warp * per;
+      const int64_t whi = wlo + per < hi ? wlo + per : hi;
+      double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      warp_batches(idx, vals, v, wlo + lane, whi, acc);
+      const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      const double t = warp_sum(s);
+      __shared__ double wsum[kSpmvWarps];
+      if (lane == 0) wsum[warp] = t;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kSpmvWarps; ++w) sum += wsum[w];
+        if (nch == 1) {
+          epi.line(r, sum, epi.load(r));
+        } else {
+          const int64_t c0 = c - (pos & 0xffff);
+          A.chunk_part[c] = sum;
+          __threadfence();
+          const unsigned arrived = atomicAdd(A.chunk_cnt + c0, 1u);
+          if (arrived == static_cast<unsigned>(nch - 1)) {
+            __threadfence();
+            double tot = 0.0;
+            for (int q = 0; q < nch; ++q) tot += __ldcg(A.chunk_part + c0 + q);
+            A.chunk_cnt[c0] = 0;
+            Epi solo = epi;
+            solo.reset_acc();
+            solo.line(r, tot, solo.load(r));
+            solo.export_acc(A.line_acc + static_cast<int64_t>(A.chunk_slot[c]) * PDLPK_LINE_ACC);
+          }
+        }
+      }
+      return;
+    }
+    b -= A.n_cta_chunks;
   }
   if constexpr ((Seg & 2) != 0) {
     if (b < A.tile_blocks) {
@@ -333,7 +401,11 @@ inline int dispatch_seg(int seg, F&& f) {
     case 2: return f.template go<P, 2>();
     case 3: return f.template go<P, 3>();
     case 4: return f.template go<P, 4>();
-    default: return f.template go<P, 5>();
+    case 5: return f.template go<P, 5>();
+    case 8: return f.template go<P, 8>();
+    case 9: return f.template go<P, 9>();
+    case 12: return f.template go<P, 12>();
+    default: return f.template go<P, 13>();  // (direct tiles never mix with CTA chunks)
   }
 }
 

@@ -15,6 +15,9 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
+import sys
+import time
 import math
 from dataclasses import dataclass, field
 from typing import Callable, Optional
@@ -213,6 +216,7 @@ def run_solve(lib, fn_name: str, p: LpProblem, options: SolverOptions, c_opts: N
               extra: tuple = ()) -> SolveResult:
     """Shared marshalling for pdlp_solve, the sharded solves (extra = the
     arguments between options and result) and the oracle's ref_solve."""
+    t_prep = time.perf_counter()
     view = p.view()
     m, n = p.rows(), p.cols()
     x = np.zeros(n)
@@ -228,7 +232,11 @@ def run_solve(lib, fn_name: str, p: LpProblem, options: SolverOptions, c_opts: N
     if options.observer is not None:
         thunk = _observer_thunk(options.observer)
         c_opts.observer = thunk
+    t_call = time.perf_counter()
     rc = getattr(lib, fn_name)(C.byref(view), C.byref(c_opts), *extra, C.byref(res))
+    if os.environ.get("PDLP_TIMING"):
+        print(f"phase=python event=timing call={time.perf_counter() - t_call:.4f} "
+              f"native_solve={res.solve_seconds:.4f} prep={t_call - t_prep:.4f}", file=sys.stderr)
     if rc != 0:
         err = lib.pdlp_last_error() if hasattr(lib, "pdlp_last_error") else lib.ref_last_error()
         msg = err.decode()
