@@ -89,13 +89,25 @@ __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
 
 __host__ __device__ constexpr int spmv_min_blocks(int seg) { return seg == 2 ? 5 : 4; }
 
+// Chunk segments are grid-stride with a bounded number of CTAs: a pass pays
+// its per-CTA partials (block reductions, the decision's combine) once per
+// CTA, so millions of short-lived CTAs (C2's 33..2048-entry rows) would cost
+// more than the products.
+constexpr int64_t kMaxWarpChunkBlocks = 148 * 8;
+constexpr int64_t kMaxCtaChunkBlocks = 148 * 4;
+
 __host__ __device__ inline int64_t warp_chunk_blocks(const pdlpk_csr& A) {
-  return (A.n_chunks - A.n_cta_chunks + kSpmvWarps - 1) / kSpmvWarps;
+  const int64_t b = (A.n_chunks - A.n_cta_chunks + kSpmvWarps - 1) / kSpmvWarps;
+  return b < kMaxWarpChunkBlocks ? b : kMaxWarpChunkBlocks;
+}
+
+__host__ __device__ inline int64_t cta_chunk_blocks(const pdlpk_csr& A) {
+  return A.n_cta_chunks < kMaxCtaChunkBlocks ? A.n_cta_chunks : kMaxCtaChunkBlocks;
 }
 
 __host__ __device__ inline int64_t sched_blocks(const pdlpk_csr& A) {
   const int s = seg_mask(A);
-  return warp_chunk_blocks(A) + A.n_cta_chunks + ((s & 6) ? A.tile_blocks : 0);
+  return warp_chunk_blocks(A) + cta_chunk_blocks(A) + ((s & 6) ? A.tile_blocks : 0);
 }
 
 __host__ __device__ inline size_t spmv_smem(int seg) { return (seg & 4) ? kSpmvSmem : 0; }
@@ -162,53 +174,37 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
   if constexpr ((Seg & 1) != 0) {
     const int64_t chunk_blocks = warp_chunk_blocks(A);
     if (b < chunk_blocks) {
-      const int64_t c = b * kSpmvWarps + warp;
-      if (c < A.n_chunks - A.n_cta_chunks) {
+      // one warp per medium line (a warp chunk is always a whole line)
+      const int64_t nw = A.n_chunks - A.n_cta_chunks;
+      for (int64_t c = b * kSpmvWarps + warp; c < nw; c += chunk_blocks * kSpmvWarps) {
         const int64_t r = A.chunk_row[c];
         const int64_t lo = A.chunk_beg[c];
         const int64_t hi = lo + A.chunk_len[c];
-        const int pos = A.chunk_pos[c];
-        const int nch = pos >> 16;
         typename Epi::Pre pre{};
-        if (nch == 1 && lane == 0) pre = epi.load(r);
-        // predicated batches of 8 entries per lane: a chunk of <= 256
-        // entries is one batch of independent loads, then its gathers
+        if (lane == 0) pre = epi.load(r);
+        // predicated batches of 8 entries per lane: independent loads, then
+        // their gathers
         double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         warp_batches(idx, vals, v, lo + lane, hi, acc);
         const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
         const double t = warp_sum(s);
-        if (nch == 1) {
-          if (lane == 0) epi.line(r, t, pre);
-        } else if (lane == 0) {
-          const int64_t c0 = c - (pos & 0xffff);
-          A.chunk_part[c] = t;
-          __threadfence();
-          const unsigned arrived = atomicAdd(A.chunk_cnt + c0, 1u);
-          if (arrived == static_cast<unsigned>(nch - 1)) {
-            __threadfence();
-            double sum = 0.0;
-            for (int q = 0; q < nch; ++q) sum += __ldcg(A.chunk_part + c0 + q);
-            A.chunk_cnt[c0] = 0;
-            // the line's epilogue contributions go to its fixed slot
-            Epi solo = epi;
-            solo.reset_acc();
-            solo.line(r, sum, solo.load(r));
-            solo.export_acc(A.line_acc + static_cast<int64_t>(A.chunk_slot[c]) * PDLPK_LINE_ACC);
-          }
-        }
+        if (lane == 0) epi.line(r, t, pre);
       }
       return;
     }
     b -= chunk_blocks;
   }
   if constexpr ((Seg & 8) != 0) {
-    if (b < A.n_cta_chunks) {
+    const int64_t cblocks = cta_chunk_blocks(A);
+    if (b < cblocks) {
+      __shared__ double wsum[kSpmvWarps];
+      for (int64_t cc = b; cc < A.n_cta_chunks; cc += cblocks) {
       // One CTA per chunk of <= kChunk entries: warp w takes one slice of
       // <= 256 entries (a single batch of independent loads), the 8 warp
       // sums are added in warp order, thread 0 runs the epilogue or the
       // ordered multi-chunk combine.  C1's 2,000-entry rows: one round trip
       // per row instead of eight per warp.
-      const int64_t c = (A.n_chunks - A.n_cta_chunks) + b;
+      const int64_t c = (A.n_chunks - A.n_cta_chunks) + cc;
       const int64_t r = A.chunk_row[c];
       const int64_t lo = A.chunk_beg[c];
       const int64_t hi = lo + A.chunk_len[c];
@@ -221,7 +217,6 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
       warp_batches(idx, vals, v, wlo + lane, whi, acc);
       const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       const double t = warp_sum(s);
-      __shared__ double wsum[kSpmvWarps];
       if (lane == 0) wsum[warp] = t;
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -247,9 +242,11 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
           }
         }
       }
+      __syncthreads();  // wsum is rewritten by the next chunk
+      }
       return;
     }
-    b -= A.n_cta_chunks;
+    b -= cblocks;
   }
   if constexpr ((Seg & 2) != 0) {
     if (b < A.tile_blocks) {

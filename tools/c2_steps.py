@@ -1,0 +1,6 @@
+"""A few C2 iterations (ncu target for the full-size power-law config)."""
+import paper_2501_07018_b200 as P
+
+p = P.generate("c2", 0)
+o = P.SolverOptions(tolerances=P.TerminationTolerances(0.0, 0.0, 0.0), iteration_limit=12)
+P.solve(p, o)
