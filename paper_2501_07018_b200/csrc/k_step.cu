@@ -504,11 +504,14 @@ struct LaunchRowCol {
     if (g <= 0) return 0;
     const size_t smem = (Seg & 4) ? kSpmvSmem : 0;
     if (row) {
+      allow_smem(row_pass<P, Seg>, smem);
       row_pass<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
     } else {
       if (decide_here) {
+        allow_smem(col_pass<P, Seg, true>, smem);
         col_pass<P, Seg, true><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
       } else {
+        allow_smem(col_pass<P, Seg, false>, smem);
         col_pass<P, Seg, false><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
       }
     }

@@ -77,7 +77,9 @@ struct LaunchSpmv {
   int go() {
     const int64_t g = sched_blocks(*A);
     if (g > 0) {
-      sched_spmv_kernel<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, (Seg & 4) ? kSpmvSmem : 0, s>>>(
+      const size_t smem = (Seg & 4) ? kSpmvSmem : 0;
+      allow_smem(sched_spmv_kernel<P, Seg>, smem);
+      sched_spmv_kernel<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(
           *A, vals, v, out, cond);
     }
     return ok();

@@ -78,9 +78,15 @@ typedef struct pdlpk_csr {
 #define PDLPK_WARP_LINE_MAX 2048 /* longer lines are processed by CTA chunks */
 #endif
 #define PDLPK_LINE_ACC 4
-#define PDLPK_TILE_NNZ 512
-#define PDLPK_TILE_ROWS 224
-#define PDLPK_TILE_STAGES 3
+#ifndef PDLPK_TILE_NNZ
+#define PDLPK_TILE_NNZ 1344 /* entries per staged tile */
+#endif
+#ifndef PDLPK_TILE_ROWS
+#define PDLPK_TILE_ROWS 672 /* lines per staged tile (7 consumer warps x 32 x 3 lines/lane) */
+#endif
+#ifndef PDLPK_TILE_STAGES
+#define PDLPK_TILE_STAGES 2 /* staged tiles in flight per CTA */
+#endif
 
 /* Device-resident step controller: one per inner loop (main / polish). */
 typedef struct pdlpk_step_state {

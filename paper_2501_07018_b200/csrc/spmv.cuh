@@ -53,7 +53,10 @@ constexpr int kTileNnz = PDLPK_TILE_NNZ;    // entries per CTA tile
 constexpr int kTileRows = PDLPK_TILE_ROWS;  // lines per CTA tile
 constexpr int kMaxStaged = 3;               // epilogue operand streams per line
 constexpr int kConsumerWarps = kSpmvWarps - 1;  // warp 0 produces
-static_assert(kTileRows <= 32 * kConsumerWarps, "a consumer warp owns 32 lines of a tile");
+// lines per consumer lane: a consumer warp owns 32 * kLinesPerLane lines of a
+// tile, lane l taking lines l, l + 32, ... (stores stay coalesced)
+constexpr int kLinesPerLane = (kTileRows + 32 * kConsumerWarps - 1) / (32 * kConsumerWarps);
+static_assert(kTileRows <= 32 * kConsumerWarps * kLinesPerLane, "tile lines per consumer warp");
 
 __host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 // Stage buffer: [indices | values | row pointers | staged operands...].
@@ -111,6 +114,15 @@ __host__ __device__ inline int64_t sched_blocks(const pdlpk_csr& A) {
 }
 
 __host__ __device__ inline size_t spmv_smem(int seg) { return (seg & 4) ? kSpmvSmem : 0; }
+
+// Opt a kernel into more than 48 KB of dynamic shared memory (the staged ring
+// of larger tile shapes); a no-op below.
+template <class Kernel>
+inline void allow_smem(Kernel k, size_t smem) {
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  }
+}
 
 // 16-byte-aligned window of elements [first, first + count) of a global array.
 struct Win {
@@ -331,7 +343,7 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
         }
       }
     } else {
-      const int cw = warp - 1;  // consumer warp: lines [32 cw, 32 cw + 32) of each tile
+      const int cw = warp - 1;  // consumer warp: lines [W cw, W cw + W), W = 32 kLinesPerLane
       int i = 0;
       for (int64_t t = b; t < A.n_tiles; t += tb, ++i) {
         const int stage = i % kStages;
@@ -348,10 +360,10 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
           s_epi[q] = reinterpret_cast<const double*>(buf + kStEpi + q * kStEpiStride +
                                                      win(epi.staged_src(q), tm.r0, tm.cnt, 8).shift);
         }
-        const int l0 = 32 * cw;
+        const int l0 = 32 * kLinesPerLane * cw;
         mbar_wait(&full[stage], (i / kStages) & 1);
         if (l0 < tm.cnt) {
-          const int l1 = l0 + 32 < tm.cnt ? l0 + 32 : tm.cnt;
+          const int l1 = l0 + 32 * kLinesPerLane < tm.cnt ? l0 + 32 * kLinesPerLane : tm.cnt;
           const int e0 = static_cast<int>(static_cast<int64_t>(s_ptr[l0]) - tm.s0);
           const int e1 = static_cast<int>(static_cast<int64_t>(s_ptr[l1]) - tm.s0);
           // this warp's products in place (the gather is the only global
@@ -373,13 +385,16 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
             }
           }
           __syncwarp();
-          const int li = l0 + lane;
-          if (li < l1) {
-            const int a = static_cast<int>(static_cast<int64_t>(s_ptr[li]) - tm.s0);
-            const int e = static_cast<int>(static_cast<int64_t>(s_ptr[li + 1]) - tm.s0);
-            double acc = 0.0;
-            for (int j = a; j < e; ++j) acc += s_val[j];
-            epi.line(tm.r0 + li, acc, epi.from_stage(s_epi, li));
+#pragma unroll
+          for (int q = 0; q < kLinesPerLane; ++q) {
+            const int li = l0 + lane + 32 * q;
+            if (li < l1) {
+              const int a = static_cast<int>(static_cast<int64_t>(s_ptr[li]) - tm.s0);
+              const int e = static_cast<int>(static_cast<int64_t>(s_ptr[li + 1]) - tm.s0);
+              double acc = 0.0;
+              for (int j = a; j < e; ++j) acc += s_val[j];
+              epi.line(tm.r0 + li, acc, epi.from_stage(s_epi, li));
+            }
           }
         }
         __syncwarp();
