@@ -90,7 +90,12 @@ __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
   return s;
 }
 
-__host__ __device__ constexpr int spmv_min_blocks(int seg) { return seg == 2 ? 5 : 4; }
+#ifndef PDLPK_CHUNK_MIN_BLOCKS
+#define PDLPK_CHUNK_MIN_BLOCKS 4 /* CTAs/SM the chunk-only kernels are compiled for */
+#endif
+__host__ __device__ constexpr int spmv_min_blocks(int seg) {
+  return seg == 2 ? 5 : (seg == 1 ? PDLPK_CHUNK_MIN_BLOCKS : 4);
+}
 
 // Chunk segments are grid-stride with a bounded number of CTAs: a pass pays
 // its per-CTA partials (block reductions, the decision's combine) once per
@@ -143,15 +148,52 @@ __device__ __forceinline__ Win win(const void* base, int64_t first, int64_t coun
 // Entries [k0, hi) stepping 32 (one lane's share of a warp's range), in
 // predicated batches of 8 independent loads then 8 gathers; acc[u] takes
 // every 8th of the lane's entries.
+#ifndef PDLPK_BATCH
+#define PDLPK_BATCH 8 /* independent loads per lane per batch (multiple of 8) */
+#endif
+constexpr int kBatch = PDLPK_BATCH;
+
+#ifndef PDLPK_IDX_PREFETCH
+#define PDLPK_IDX_PREFETCH 1
+#endif
+
 __device__ __forceinline__ void warp_batches(const int32_t* __restrict__ idx,
                                              const double* __restrict__ vals,
                                              const double* __restrict__ v, int64_t k0, int64_t hi,
                                              double (&acc)[8]) {
-  for (int64_t base = k0; base < hi; base += 8 * 32) {
-    int32_t ci[8];
-    double a[8];
+#if PDLPK_IDX_PREFETCH
+  // The dependent chain is index -> gather; the values are only needed by
+  // the multiply.  So each batch loads its values and the NEXT batch's
+  // indices while its gathers (indices loaded one batch earlier) resolve:
+  // one memory round trip per batch instead of two.
+  int32_t ci[kBatch];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+  for (int u = 0; u < kBatch; ++u) {
+    const int64_t k = k0 + u * 32;
+    if (k < hi) ci[u] = ld_stream(idx + k);
+  }
+  for (int64_t base = k0; base < hi; base += kBatch * 32) {
+    const int64_t nb = base + kBatch * 32;
+    double a[kBatch];
+    int32_t cn[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      if (base + u * 32 < hi) a[u] = ld_stream(vals + base + u * 32);
+      if (nb + u * 32 < hi) cn[u] = ld_stream(idx + nb + u * 32);
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      if (base + u * 32 < hi) acc[u & 3] = mac(acc[u & 3], a[u], __ldg(v + ci[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) ci[u] = cn[u];
+  }
+#else
+  for (int64_t base = k0; base < hi; base += kBatch * 32) {
+    int32_t ci[kBatch];
+    double a[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
       const int64_t k = base + u * 32;
       if (k < hi) {
         ci[u] = ld_stream(idx + k);
@@ -159,10 +201,11 @@ __device__ __forceinline__ void warp_batches(const int32_t* __restrict__ idx,
       }
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (base + u * 32 < hi) acc[u] = mac(acc[u], a[u], __ldg(v + ci[u]));
+    for (int u = 0; u < kBatch; ++u) {
+      if (base + u * 32 < hi) acc[u & 7] = mac(acc[u & 7], a[u], __ldg(v + ci[u]));
     }
   }
+#endif
 }
 
 struct TileMeta {
