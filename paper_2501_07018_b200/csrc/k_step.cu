@@ -502,7 +502,7 @@ struct LaunchRowCol {
     const pdlpk_csr& A = row ? a->P.K : a->P.KT;
     const int64_t g = sched_blocks(A);
     if (g <= 0) return 0;
-    const size_t smem = (Seg & 4) ? kSpmvSmem : 0;
+    const size_t smem = spmv_smem(A, Seg);
     if (row) {
       allow_smem(row_pass<P, Seg>, smem);
       row_pass<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
@@ -757,4 +757,21 @@ extern "C" int pdlpk_dist_decide(const pdlpk_step_args* a, const double* all8, i
                                  cudaStream_t s) {
   dist_decide_kernel<<<1, 1, 0, s>>>(*a, all8, world);
   return static_cast<int>(cudaGetLastError());
+}
+
+// CTAs of the staged-tile kernels that are resident at once (the tile
+// segment is grid-stride: a second wave of CTAs would start its tiles late).
+extern "C" int64_t pdlpk_tile_resident_ctas(int32_t stage_bytes) {
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = kRingHeader + kStages * static_cast<size_t>(stage_bytes);
+  allow_smem(col_pass<int32_t, 4, true>, smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, col_pass<int32_t, 4, true>,
+                                                    kSpmvThreads, smem) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return static_cast<int64_t>(sms) * per_sm;
 }

@@ -5,6 +5,9 @@
 //
 // Translation unit compiled with -fmad=false (see common.cuh).
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "reduce.cuh"
@@ -77,7 +80,7 @@ struct LaunchSpmv {
   int go() {
     const int64_t g = sched_blocks(*A);
     if (g > 0) {
-      const size_t smem = (Seg & 4) ? kSpmvSmem : 0;
+      const size_t smem = spmv_smem(*A, Seg);
       allow_smem(sched_spmv_kernel<P, Seg>, smem);
       sched_spmv_kernel<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(
           *A, vals, v, out, cond);
@@ -274,6 +277,21 @@ int pdlpk_diff_norm_sq(const double* a, const double* b, int64_t n, const pdlpk_
 }
 
 void pdlpk_set_red_log(pdlpk_red_log* log) { g_red_log = log; }
+
+void pdlpk_tile_shape(double avg_len, int32_t budget, int32_t* lines, int32_t* nnz,
+                      int32_t* stage_bytes) {
+  const double a = avg_len < 1.0 ? 1.0 : avg_len;
+  int L = kTileRows;
+  while (L > 32 && static_cast<double>(stage_nnz_for(L, budget)) < a * L) L -= 8;
+  const int E = stage_nnz_for(L, budget);
+  *lines = L;
+  *nnz = E;
+  *stage_bytes = static_cast<int32_t>(stage_layout(L, E).bytes);
+}
+
+int32_t pdlpk_stage_budget(int32_t nnz) {
+  return static_cast<int32_t>(stage_layout(kTileRows, nnz).bytes);
+}
 
 int pdlpk_combine_slots(const double* all, int32_t world, int32_t stride, uint64_t marked,
                         uint64_t maxbits, double* slots, cudaStream_t s) {

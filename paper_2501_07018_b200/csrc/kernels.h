@@ -63,6 +63,10 @@ typedef struct pdlpk_csr {
    * the column owners.  PDLPK_DIST_NONE on one GPU. */
   int32_t dist_kind;
   int32_t tile_direct; /* 1: tiles are direct (thread per line, spmv.cuh) */
+  int32_t tile_lines_cap;   /* staged tile shape of this layout: lines and */
+  int32_t tile_nnz_cap;     /* entries per tile ... */
+  int32_t tile_stage_bytes; /* ... and the bytes of one ring stage */
+  int32_t _pad_tile;
 } pdlpk_csr;
 
 #define PDLPK_DIST_NONE 0
@@ -70,7 +74,9 @@ typedef struct pdlpk_csr {
 #define PDLPK_DIST_PARTIAL 2
 
 /* Schedule limits (spmv.cuh) the host planner must respect. */
-#define PDLPK_SHORT_MAX 32
+#ifndef PDLPK_SHORT_MAX
+#define PDLPK_SHORT_MAX 32 /* longest line of a staged tile */
+#endif
 #ifndef PDLPK_CHUNK
 #define PDLPK_CHUNK 2048 /* entries per CTA chunk: 8 warps x one 256-entry batch */
 #endif
@@ -79,10 +85,10 @@ typedef struct pdlpk_csr {
 #endif
 #define PDLPK_LINE_ACC 4
 #ifndef PDLPK_TILE_NNZ
-#define PDLPK_TILE_NNZ 1344 /* entries per staged tile */
+#define PDLPK_TILE_NNZ 896 /* entries of the default stage budget (with PDLPK_TILE_ROWS lines) */
 #endif
 #ifndef PDLPK_TILE_ROWS
-#define PDLPK_TILE_ROWS 672 /* lines per staged tile (7 consumer warps x 32 x 3 lines/lane) */
+#define PDLPK_TILE_ROWS 448 /* most lines per staged tile (7 consumer warps x 32 x 2 lines/lane) */
 #endif
 #ifndef PDLPK_TILE_STAGES
 #define PDLPK_TILE_STAGES 2 /* staged tiles in flight per CTA */
@@ -157,6 +163,15 @@ typedef struct pdlpk_red {
 
 int64_t pdlpk_red_scratch_doubles(void);
 int64_t pdlpk_step_partials(const pdlpk_problem* P);
+/* Staged-tile shape for a layout whose short lines average `avg_len`
+ * entries: the most lines (<= PDLPK_TILE_ROWS) whose entries still fit one
+ * ring stage, and the entry cap for that line count. */
+void pdlpk_tile_shape(double avg_len, int32_t budget, int32_t* lines, int32_t* nnz,
+                      int32_t* stage_bytes);
+/* Ring-stage bytes of a PDLPK_TILE_ROWS x nnz tile (budgets for tile_shape). */
+int32_t pdlpk_stage_budget(int32_t nnz);
+/* SMs x resident CTAs of the staged-tile kernels with this ring. */
+int64_t pdlpk_tile_resident_ctas(int32_t stage_bytes);
 
 /* ---- row-sharded attempt pieces (the host interleaves the collectives) ----
  * primal:     primal_pass; xbar is written at a->xbar

@@ -157,13 +157,29 @@ bool direct_tiles(const int64_t* start, int64_t dim) {
   return true;
 }
 
-void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
+void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
+                    int64_t short_max = PDLPK_SHORT_MAX, int32_t budget = 0) {
+  if (budget <= 0) budget = pdlpk_stage_budget(PDLPK_TILE_NNZ);
   std::vector<int32_t> t0, tc, ck_row, ck_len, ck_pos, ck_slot;
   std::vector<int64_t> tn, ck_beg;
   int64_t n_multi = 0;
   const bool direct = direct_tiles(start, dim);
-  const int64_t tile_rows = direct ? 256 : PDLPK_TILE_ROWS;
-  const int64_t tile_nnz = direct ? 256 * PDLPK_SHORT_MAX : PDLPK_TILE_NNZ;
+  int32_t shape_lines = PDLPK_TILE_ROWS, shape_nnz = PDLPK_TILE_NNZ, stage_bytes = budget;
+  if (!direct) {
+    int64_t short_lines = 0, short_nnz = 0;
+    for (int64_t r = 0; r < dim; ++r) {
+      const int64_t len = start[r + 1] - start[r];
+      if (len <= short_max) {
+        ++short_lines;
+        short_nnz += len;
+      }
+    }
+    const double avg = short_lines > 0 ? static_cast<double>(short_nnz) / short_lines : 1.0;
+    pdlpk_tile_shape(avg, budget, &shape_lines, &shape_nnz, &stage_bytes);
+  }
+  const int64_t tile_rows = direct ? 256 : shape_lines;
+  const int64_t tile_nnz = direct ? 256 * PDLPK_SHORT_MAX : shape_nnz;
+  if (direct) short_max = PDLPK_SHORT_MAX;
   int64_t cur0 = -1, cur_rows = 0, cur_nnz = 0;
   auto close = [&] {
     if (cur_rows > 0) {
@@ -180,7 +196,7 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   std::vector<int64_t> cc_beg;
   for (int64_t r = 0; r < dim; ++r) {
     const int64_t len = start[r + 1] - start[r];
-    if (len > PDLPK_SHORT_MAX && len <= PDLPK_WARP_LINE_MAX) {
+    if (len > short_max && len <= PDLPK_WARP_LINE_MAX) {
       // a medium line: one warp
       close();
       ck_row.push_back(static_cast<int32_t>(r));
@@ -238,8 +254,10 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   const int64_t n_tiles = static_cast<int64_t>(t0.size());
   // ~41 KB staging ring per CTA -> 5 CTAs per SM; each CTA walks its tiles
   // grid-stride with a kStages-deep bulk-copy prefetch.
+  // staged tiles: exactly the resident CTAs (one wave, each walks its tiles
+  // grid-stride); direct tiles have no ring and run 4 waves of 5 per SM
   int64_t tb = n_tiles;
-  tb = std::min<int64_t>(tb, direct ? 148 * 5 * 4 : 148 * 5);
+  tb = std::min<int64_t>(tb, direct ? 148 * 5 * 4 : pdlpk_tile_resident_ctas(stage_bytes));
   tb = std::max<int64_t>(tb, 1);  // the column pass's last CTA decides, so never empty
   L.view.chunk_row = L.chunk_row.get();
   L.view.chunk_beg = L.chunk_beg.get();
@@ -257,7 +275,58 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L) {
   L.view.tile_nnz0 = L.tile_nnz0.get();
   L.view.n_tiles = n_tiles;
   L.view.tile_direct = direct ? 1 : 0;
+  L.view.tile_lines_cap = static_cast<int32_t>(tile_rows);
+  L.view.tile_nnz_cap = static_cast<int32_t>(tile_nnz);
+  L.view.tile_stage_bytes = stage_bytes;
   L.view.tile_blocks = static_cast<int32_t>(tb);
+}
+
+// Tile line threshold per layout.  Which lines are cheaper in staged tiles
+// than one warp each depends on the whole length distribution (C2's ~33-entry
+// rows: 64 is best, 3.5 vs 4.0 ms at 256; its power-law columns: 256 is best,
+// 2.8 vs 3.5 ms at 64), so a large layout times one product per candidate at
+// setup and keeps the fastest; small layouts use 64.
+// PDLP_SHORT_MAX=<n> forces a threshold.
+int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t operand_len, DevLayout& L,
+                          cudaStream_t s) {
+  const char* env = std::getenv("PDLP_SHORT_MAX");
+  if (env != nullptr && std::atoi(env) > 0) {
+    const int64_t t = std::atoi(env);
+    build_schedule(start, dim, L, t);
+    return t;
+  }
+  const int64_t kDefault = 64;
+  if (L.view.nnz < (int64_t(16) << 20) || L.view.tile_direct) {
+    build_schedule(start, dim, L, kDefault);
+    return kDefault;
+  }
+  // candidates: tile line threshold x ring-stage budget (entries of a
+  // PDLPK_TILE_ROWS-line stage); the budget sets both the tile shape and how
+  // many CTAs are resident
+  DevBuf<double> x(std::max<int64_t>(operand_len, 1)), out(std::max<int64_t>(dim, 1));
+  PDLP_LAUNCH(pdlpk_fill(x.get(), 1.0, operand_len, s));
+  Event e0, e1;
+  int64_t best = kDefault;
+  int32_t best_budget = pdlpk_stage_budget(PDLPK_TILE_NNZ);
+  double best_t = kInf;
+  for (const int64_t t : {32, 64, 256}) {
+    for (const int32_t nnz : {896, 1344, 2016}) {
+      const int32_t budget = pdlpk_stage_budget(nnz);
+      build_schedule(start, dim, L, t, budget);
+      PDLP_LAUNCH(pdlpk_spmv(&L.view, 0, x.get(), out.get(), 0, s));  // warm
+      e0.record(s);
+      for (int rep = 0; rep < 2; ++rep) PDLP_LAUNCH(pdlpk_spmv(&L.view, 0, x.get(), out.get(), 0, s));
+      e1.record(s);
+      const double el = elapsed_seconds(e0, e1);
+      if (el < best_t) {
+        best_t = el;
+        best = t;
+        best_budget = budget;
+      }
+    }
+  }
+  build_schedule(start, dim, L, best, best_budget);
+  return best;
 }
 
 // Uploads one orientation; the raw int64 row pointers and indices are checked
@@ -308,7 +377,7 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
   L.view.index = L.index.get();
   L.view.value = L.value.get();
   L.view.value_orig = L.value_orig.get();
-  build_schedule(v.start, dim, L);
+  autotune_schedule(v.start, dim, bound, L, s);
 }
 
 DevBuf<double> upload_vec(const double* h, int64_t n, cudaStream_t s) {
@@ -1309,6 +1378,12 @@ class Engine {
   };
   void gaps(const InnerCfg& cfg, const pdlpk_problem& P, const GapQuery* q, int count,
             double omega, double* out) {
+    const auto gap_t0 = Clock::now();
+    struct GapClock {
+      double& acc;
+      Clock::time_point t0;
+      ~GapClock() { acc += std::chrono::duration<double>(Clock::now() - t0).count(); }
+    } gap_clock{gap_seconds_, gap_t0};
     if (dist()) {
       // Sharded: every rank evaluates the same whole-problem gap on gathered
       // vectors (identical inputs -> identical mu everywhere); the cadence
@@ -1434,6 +1509,7 @@ class Engine {
   double precondition_seconds_ = 0.0;
   double cadence_seconds_ = 0.0;  // host time inside cadence blocks (incl. polishing)
   double polish_seconds_ = 0.0;
+  double gap_seconds_ = 0.0;  // host time in normalized-gap evaluations (syncs included)
   int64_t attempts_total_ = 0;
   bool profile_ = false;
   std::vector<cudaEvent_t> prof_ev_;
@@ -1860,10 +1936,10 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result*
   if (o->logging || std::getenv("PDLP_TIMING") != nullptr) {
     std::fprintf(stderr,
                  "phase=main event=timing solve=%.4f upload=%.4f precondition=%.4f loop=%.4f "
-                 "steps=%.4f cadence=%.4f polish=%.4f alloc=%.4f\n",
+                 "steps=%.4f cadence=%.4f gap=%.4f polish=%.4f alloc=%.4f\n",
                  res->solve_seconds, res->upload_seconds, res->precondition_seconds,
-                 res->loop_seconds, res->step_seconds, E.cadence_seconds_, E.polish_seconds_,
-                 g_alloc_seconds);
+                 res->loop_seconds, res->step_seconds, E.cadence_seconds_, E.gap_seconds_,
+                 E.polish_seconds_, g_alloc_seconds);
   }
 }
 

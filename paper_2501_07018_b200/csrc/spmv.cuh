@@ -59,16 +59,42 @@ constexpr int kLinesPerLane = (kTileRows + 32 * kConsumerWarps - 1) / (32 * kCon
 static_assert(kTileRows <= 32 * kConsumerWarps * kLinesPerLane, "tile lines per consumer warp");
 
 __host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
-// Stage buffer: [indices | values | row pointers | staged operands...].
-constexpr size_t kStIdx = 0;
-constexpr size_t kStVal = kStIdx + align16(sizeof(int32_t) * kTileNnz + 32);
-constexpr size_t kStPtr = kStVal + align16(sizeof(double) * kTileNnz + 32);
-constexpr size_t kStEpi = kStPtr + align16(sizeof(int64_t) * (kTileRows + 1) + 32);
-constexpr size_t kStEpiStride = align16(sizeof(double) * kTileRows + 32);
-constexpr size_t kStageBytes = kStEpi + kMaxStaged * kStEpiStride;
+// Stage buffer: [indices | values | row pointers | staged operands...] for a
+// tile of <= L lines and <= E entries.  Every ring stage has the bytes of the
+// default shape (kTileRows, kTileNnz); a layout picks its own (L, E) inside
+// that budget from its line lengths (solver.cpp build_schedule): C1's
+// two-entry columns use 672 x 1344, C2's ~27-entry rows ~100 x 2900, so both
+// fill their stages.
+struct StageLayout {
+  uint32_t val, ptr, epi, epi_stride, bytes;
+};
+__host__ __device__ constexpr StageLayout stage_layout(int L, int E) {
+  return StageLayout{
+      static_cast<uint32_t>(align16(sizeof(int32_t) * E + 32)),
+      static_cast<uint32_t>(align16(sizeof(int32_t) * E + 32) + align16(sizeof(double) * E + 32)),
+      static_cast<uint32_t>(align16(sizeof(int32_t) * E + 32) + align16(sizeof(double) * E + 32) +
+                            align16(sizeof(int64_t) * (L + 1) + 32)),
+      static_cast<uint32_t>(align16(sizeof(double) * L + 32)),
+      static_cast<uint32_t>(align16(sizeof(int32_t) * E + 32) + align16(sizeof(double) * E + 32) +
+                            align16(sizeof(int64_t) * (L + 1) + 32) +
+                            kMaxStaged * align16(sizeof(double) * L + 32))};
+}
+// Largest entry count that fits a stage of `budget` bytes next to L lines.
+__host__ __device__ inline int stage_nnz_for(int L, size_t budget) {
+  int lo = 32, hi = 1 << 18;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (stage_layout(L, mid).bytes <= budget) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
 constexpr int kStages = PDLPK_TILE_STAGES;  // ring depth: tiles in flight per CTA
 constexpr size_t kRingHeader = 128;         // one mbarrier per stage
-constexpr size_t kSpmvSmem = kRingHeader + kStages * kStageBytes;
+// Dynamic shared memory of a layout's staged ring (its stage size is chosen
+// per layout, see solver.cpp build_schedule).
+__host__ __device__ inline size_t ring_smem(const pdlpk_csr& A) {
+  return kRingHeader + kStages * static_cast<size_t>(A.tile_stage_bytes);
+}
 
 // acc + a*b with the product rounded separately (the TU is built with
 // -fmad=false): per-term rounding identical to the reference.  No cost: the
@@ -76,6 +102,10 @@ constexpr size_t kSpmvSmem = kRingHeader + kStages * kStageBytes;
 __device__ __forceinline__ double mac(double acc, double a, double b) { return acc + a * b; }
 
 constexpr int kDirectRows = kSpmvThreads;  // lines per direct tile
+#ifndef PDLPK_TILE_GATHER
+#define PDLPK_TILE_GATHER 4 /* gathers in flight per consumer lane */
+#endif
+constexpr int kTileGather = PDLPK_TILE_GATHER;
 
 // Segment mask of a layout: 1 chunks, 2 direct tiles, 4 staged tiles.
 // Kernels are instantiated per mask so each pass only pays the registers and
@@ -118,14 +148,20 @@ __host__ __device__ inline int64_t sched_blocks(const pdlpk_csr& A) {
   return warp_chunk_blocks(A) + cta_chunk_blocks(A) + ((s & 6) ? A.tile_blocks : 0);
 }
 
-__host__ __device__ inline size_t spmv_smem(int seg) { return (seg & 4) ? kSpmvSmem : 0; }
+__host__ __device__ inline size_t spmv_smem(const pdlpk_csr& A, int seg) {
+  return (seg & 4) ? ring_smem(A) : 0;
+}
 
-// Opt a kernel into more than 48 KB of dynamic shared memory (the staged ring
-// of larger tile shapes); a no-op below.
+// Opt a kernel into more than 48 KB of dynamic shared memory (staged rings
+// above that).  Always the device maximum, never the launch's own size:
+// layouts have different rings, and with ranks as threads (ThreadComm) a
+// smaller value set by one rank would invalidate another rank's launch.  The
+// cap does not change occupancy (the launch's actual size does).
+constexpr int kMaxDynSmem = 160 * 1024;  // rings stay far below; leaves room for static smem
 template <class Kernel>
 inline void allow_smem(Kernel k, size_t smem) {
   if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
   }
 }
 
@@ -361,7 +397,8 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
           const int stage = i % kStages;
           if (i >= kStages) mbar_wait(&empty[stage], ((i / kStages) + 1) & 1);
           const TileMeta tm = tile_meta(A, t);
-          unsigned char* buf = stage0 + stage * kStageBytes;
+          unsigned char* buf = stage0 + stage * static_cast<size_t>(A.tile_stage_bytes);
+          const StageLayout sl = stage_layout(A.tile_lines_cap, A.tile_nnz_cap);
           const Win wi = win(idx, tm.s0, tm.len, 4);
           const Win wv = win(vals, tm.s0, tm.len, 8);
           const Win wp = win(start, tm.r0, tm.cnt + 1, static_cast<int>(sizeof(P)));
@@ -374,56 +411,62 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
           }
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&full[stage], total);
-          if (wi.bytes) bulk_g2s(buf + kStIdx, wi.src, wi.bytes, &full[stage]);
-          if (wv.bytes) bulk_g2s(buf + kStVal, wv.src, wv.bytes, &full[stage]);
-          if (wp.bytes) bulk_g2s(buf + kStPtr, wp.src, wp.bytes, &full[stage]);
+          if (wi.bytes) bulk_g2s(buf, wi.src, wi.bytes, &full[stage]);
+          if (wv.bytes) bulk_g2s(buf + sl.val, wv.src, wv.bytes, &full[stage]);
+          if (wp.bytes) bulk_g2s(buf + sl.ptr, wp.src, wp.bytes, &full[stage]);
 #pragma unroll
           for (int q = 0; q < Epi::kStaged; ++q) {
             if (we[q].bytes) {
-              bulk_g2s(buf + kStEpi + q * kStEpiStride, we[q].src, we[q].bytes, &full[stage]);
+              bulk_g2s(buf + sl.epi + q * sl.epi_stride, we[q].src, we[q].bytes, &full[stage]);
             }
           }
         }
       }
     } else {
-      const int cw = warp - 1;  // consumer warp: lines [W cw, W cw + W), W = 32 kLinesPerLane
+      const int cw = warp - 1;  // consumer warp: lines [per cw, per cw + per) of each tile
       int i = 0;
       for (int64_t t = b; t < A.n_tiles; t += tb, ++i) {
         const int stage = i % kStages;
         const TileMeta tm = tile_meta(A, t);
-        unsigned char* buf = stage0 + stage * kStageBytes;
+        unsigned char* buf = stage0 + stage * static_cast<size_t>(A.tile_stage_bytes);
+        const StageLayout sl = stage_layout(A.tile_lines_cap, A.tile_nnz_cap);
         const int32_t* s_idx =
-            reinterpret_cast<const int32_t*>(buf + kStIdx + win(idx, tm.s0, tm.len, 4).shift);
-        double* s_val = reinterpret_cast<double*>(buf + kStVal + win(vals, tm.s0, tm.len, 8).shift);
+            reinterpret_cast<const int32_t*>(buf + win(idx, tm.s0, tm.len, 4).shift);
+        double* s_val = reinterpret_cast<double*>(buf + sl.val + win(vals, tm.s0, tm.len, 8).shift);
         const P* s_ptr = reinterpret_cast<const P*>(
-            buf + kStPtr + win(start, tm.r0, tm.cnt + 1, static_cast<int>(sizeof(P))).shift);
+            buf + sl.ptr + win(start, tm.r0, tm.cnt + 1, static_cast<int>(sizeof(P))).shift);
         const double* s_epi[kMaxStaged];
 #pragma unroll
         for (int q = 0; q < Epi::kStaged; ++q) {
-          s_epi[q] = reinterpret_cast<const double*>(buf + kStEpi + q * kStEpiStride +
+          s_epi[q] = reinterpret_cast<const double*>(buf + sl.epi + q * sl.epi_stride +
                                                      win(epi.staged_src(q), tm.r0, tm.cnt, 8).shift);
         }
-        const int l0 = 32 * kLinesPerLane * cw;
+        // the tile's lines split evenly over the consumer warps (a tile of
+        // 20-32-entry lines holds only ~45 lines: fixed 96-line ranges would
+        // leave six warps idle)
+        const int per = (tm.cnt + kConsumerWarps - 1) / kConsumerWarps;
+        const int l0 = per * cw;
         mbar_wait(&full[stage], (i / kStages) & 1);
         if (l0 < tm.cnt) {
-          const int l1 = l0 + 32 * kLinesPerLane < tm.cnt ? l0 + 32 * kLinesPerLane : tm.cnt;
+          const int l1 = l0 + per < tm.cnt ? l0 + per : tm.cnt;
           const int e0 = static_cast<int>(static_cast<int64_t>(s_ptr[l0]) - tm.s0);
           const int e1 = static_cast<int>(static_cast<int64_t>(s_ptr[l1]) - tm.s0);
           // this warp's products in place (the gather is the only global
-          // access): batches of 4 per lane keep 4 gathers in flight
-          for (int j0 = e0 + lane; j0 < e1; j0 += 4 * 32) {
-            int32_t ci[4];
-            double g[4];
+          // access): batches of kTileGather per lane keep that many gathers
+          // in flight
+          for (int j0 = e0 + lane; j0 < e1; j0 += kTileGather * 32) {
+            int32_t ci[kTileGather];
+            double g[kTileGather];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kTileGather; ++u) {
               if (j0 + 32 * u < e1) ci[u] = s_idx[j0 + 32 * u];
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kTileGather; ++u) {
               if (j0 + 32 * u < e1) g[u] = __ldg(v + ci[u]);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kTileGather; ++u) {
               if (j0 + 32 * u < e1) s_val[j0 + 32 * u] = s_val[j0 + 32 * u] * g[u];
             }
           }
