@@ -60,6 +60,10 @@ void pdlp_gen_c4_params(pdlp_gen_params* p, uint64_t seed);
 
 /* Random sparse LP constructed feasible and bounded (C0/C2/C4 recipes). */
 pdlp_instance* pdlp_gen_random_lp(const pdlp_gen_params* params);
+/* Rows [r0, r1) of the random-LP family as a standalone LP (a row shard of a
+ * large instance without building the whole; per-column / per-row
+ * counter-based streams, multi-threaded).  NULL on bad arguments. */
+pdlp_instance* pdlp_gen_random_lp_window(const pdlp_gen_params* params, int64_t r0, int64_t r1);
 
 /* Transportation LP (C1): `sources` supply rows sum_d x_sd <= s_s (s integer
  * U[50,150]), `sinks` demand rows sum_s x_sd >= d_d (d scaled to 95 % of total

@@ -243,6 +243,7 @@ GEN_SIGNATURES = {
     "pdlp_gen_c2_params": (None, [C.POINTER(GenParams), C.c_uint64]),
     "pdlp_gen_c4_params": (None, [C.POINTER(GenParams), C.c_uint64]),
     "pdlp_gen_random_lp": (C.c_void_p, [C.POINTER(GenParams)]),
+    "pdlp_gen_random_lp_window": (C.c_void_p, [C.POINTER(GenParams), C.c_int64, C.c_int64]),
     "pdlp_gen_transport": (C.c_void_p, [C.c_int64, C.c_int64, C.c_uint64]),
     "pdlp_gen_unit_commitment": (C.c_void_p, [C.c_int64, C.c_int64, C.c_uint64]),
     "pdlp_instance_from_triplets": (C.c_void_p, [C.c_int64, C.c_int64, C.c_int64, c_int64_p,

@@ -17,6 +17,8 @@
 #include <numeric>
 #include <vector>
 
+#include <thread>
+
 #include "pdlp_gen.h"
 
 namespace {
@@ -286,6 +288,125 @@ pdlp_instance* pdlp_gen_random_lp(const pdlp_gen_params* params) {
     }
   }
   // c = A'y* + r*: (y*, r*) is dual feasible, so the LP is bounded.
+  const std::vector<double> aty = col_product(inst, ys);
+  inst->objective.resize(n);
+  for (int64_t i = 0; i < n; ++i) inst->objective[i] = aty[i] + rs[i];
+  inst->feasible_point = std::move(xs);
+  return inst;
+}
+
+// Rows [r0, r1) of the random-LP family as a standalone LP (SURVEY 8(f) 1:
+// a C4 row shard is 18.75M x 300M with 375M entries; the whole instance, 3B
+// entries, is never built).  Every column and every row has its own
+// counter-based stream, so the draws parallelize over host threads and a
+// window's entries do not depend on the window: the matrix of window [r0, r1)
+// is exactly the rows r0..r1-1 of window [0, m).  Bounds, x*, y*, r* follow
+// the sequential recipe per index; b = A_w x* and c = A_w' y*_w + r* are
+// formed over the window, so the window LP is feasible and bounded on its
+// own.  (Draws differ from pdlp_gen_random_lp's single sequential stream.)
+pdlp_instance* pdlp_gen_random_lp_window(const pdlp_gen_params* params, int64_t r0, int64_t r1) {
+  const pdlp_gen_params& p = *params;
+  if (p.rows < 1 || p.cols < 1 || r0 < 0 || r1 > p.rows || r0 >= r1) return nullptr;
+  const int64_t m = p.rows, n = p.cols, mw = r1 - r0;
+  auto stream = [&](uint64_t kind, int64_t i) {
+    SplitMix h(p.seed ^ (kind * 0xd1b54a32d192ed03ull));
+    h.s += static_cast<uint64_t>(i) * 0x9e3779b97f4a7c15ull;
+    return SplitMix(h.next());
+  };
+  const int T = static_cast<int>(std::max<unsigned>(1u, std::min(32u, std::thread::hardware_concurrency())));
+  auto parallel = [&](int64_t count, auto&& body) {
+    std::vector<std::thread> th;
+    const int64_t per = (count + T - 1) / T;
+    for (int t = 0; t < T; ++t) {
+      const int64_t lo = std::min(count, per * t), hi = std::min(count, lo + per);
+      th.emplace_back([&, t, lo, hi] { body(t, lo, hi); });
+    }
+    for (auto& x : th) x.join();
+  };
+  // Matrix: column streams, entries of the window kept (column-major order).
+  std::vector<Triplets> part(static_cast<size_t>(T));
+  parallel(n, [&](int t, int64_t lo, int64_t hi) {
+    Triplets& tr = part[static_cast<size_t>(t)];
+    for (int64_t c = lo; c < hi; ++c) {
+      SplitMix rng = stream(1, c);
+      const int64_t k = sample_count(rng, p);
+      for (int64_t e = 0; e < k; ++e) {
+        const int64_t row = rng.below(m);
+        const double v = sample_value(rng, p);
+        if (row >= r0 && row < r1) tr.push(row - r0, c, v);
+      }
+    }
+  });
+  Triplets all;
+  size_t total = 0;
+  for (const auto& tr : part) total += tr.v.size();
+  all.r.reserve(total);
+  all.c.reserve(total);
+  all.v.reserve(total);
+  for (auto& tr : part) {
+    all.r.insert(all.r.end(), tr.r.begin(), tr.r.end());
+    all.c.insert(all.c.end(), tr.c.begin(), tr.c.end());
+    all.v.insert(all.v.end(), tr.v.begin(), tr.v.end());
+    tr = Triplets{};
+  }
+  auto* inst = new pdlp_instance;
+  inst->rows = mw;
+  inst->cols = n;
+  build_both(inst, all);
+  all = Triplets{};
+
+  inst->var_lower.resize(n);
+  inst->var_upper.resize(n);
+  std::vector<double> xs(n), rs(n);
+  parallel(n, [&](int, int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      SplitMix rng = stream(2, i);
+      int kind = 0;
+      if (p.bound_kind == 1) {
+        const double u = rng.u01();
+        kind = u < 0.6 ? 0 : (u < 0.9 ? 1 : 2);
+      }
+      if (kind == 0) {
+        inst->var_lower[i] = 0.0;
+        inst->var_upper[i] = p.bound_kind == 0 ? p.box_hi : kInf;
+        xs[i] = rng.uniform(0.0, p.box_hi);
+        rs[i] = std::fabs(rng.normal());
+      } else if (kind == 1) {
+        const double l = rng.uniform(-p.box_hi, 0.0);
+        const double u = l + rng.uniform(1.0, 2.0 * p.box_hi);
+        inst->var_lower[i] = l;
+        inst->var_upper[i] = u;
+        xs[i] = rng.uniform(l, u);
+        rs[i] = rng.normal();
+      } else {
+        inst->var_lower[i] = -kInf;
+        inst->var_upper[i] = kInf;
+        xs[i] = p.box_hi * 0.5 * rng.normal();
+        rs[i] = 0.0;
+      }
+    }
+  });
+  const std::vector<double> ax = row_product(inst, xs);
+  inst->con_lower.resize(mw);
+  inst->con_upper.resize(mw);
+  std::vector<double> ys(mw);
+  const int64_t n_eq_first = static_cast<int64_t>(std::llround(p.eq_frac * static_cast<double>(m)));
+  parallel(mw, [&](int, int64_t lo, int64_t hi) {
+    for (int64_t j = lo; j < hi; ++j) {
+      const int64_t g = r0 + j;
+      SplitMix rng = stream(3, g);
+      const bool eq = p.eq_rows_first ? (g < n_eq_first) : (rng.u01() < p.eq_frac);
+      if (eq) {
+        inst->con_lower[j] = ax[j];
+        inst->con_upper[j] = ax[j];
+        ys[j] = rng.normal();
+      } else {
+        inst->con_lower[j] = -kInf;
+        inst->con_upper[j] = ax[j] + rng.uniform(0.0, p.slack_hi);
+        ys[j] = -std::fabs(rng.normal());
+      }
+    }
+  });
   const std::vector<double> aty = col_product(inst, ys);
   inst->objective.resize(n);
   for (int64_t i = 0; i < n; ++i) inst->objective[i] = aty[i] + rs[i];

@@ -694,8 +694,13 @@ class Engine {
     host_slots_ = pinned_scratch().slots;
     red_scratch_.alloc(std::max<int64_t>(pdlpk_red_scratch_doubles(), 8 * int64_t(shards_) + 64));
     // the gap runs on whole vectors (gathered when sharded)
-    for (auto& w : gap_work_) {
-      w.alloc(std::max(pdlpk_gap_work_bytes(n_glob_, m_glob_), pdlpk_gap_work_bytes(m_glob_, n_glob_)));
+    // Two buffers let both gap queries of a cadence share one sync; above
+    // 1 GB each (C4-shard sizes: 24 GB) one buffer is reused query by query.
+    {
+      const size_t gw = std::max(pdlpk_gap_work_bytes(n_glob_, m_glob_), pdlpk_gap_work_bytes(m_glob_, n_glob_));
+      gap_shared_ = gw > (size_t(1) << 30);
+      gap_work_[0].alloc(gw);
+      if (!gap_shared_) gap_work_[1].alloc(gw);
     }
     islots_.alloc(8);
     host_islots_ = pinned_scratch().islots;
@@ -1408,6 +1413,10 @@ class Engine {
   }
 
   void gaps_local(const pdlpk_problem& P, const GapQuery* q, int count, double omega, double* out) {
+    if (gap_shared_ && count > 1) {
+      for (int i = 0; i < count; ++i) gaps_local(P, q + i, 1, omega, out + i);
+      return;
+    }
     const pdlpk_red r = red();
     for (int i = 0; i < count; ++i) {
       PDLP_LAUNCH(pdlpk_gap_prepare(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, &r,
@@ -1496,6 +1505,7 @@ class Engine {
   double* host_slots_ = nullptr;
   DevBuf<double> red_scratch_;
   DevBuf<char> gap_work_[2];
+  bool gap_shared_ = false;  // one gap buffer, queries evaluated one at a time
   DevBuf<int> islots_;
   int* host_islots_ = nullptr;
   DevBuf<double> zeros_n_, zeros_m_;

@@ -213,8 +213,13 @@ def generate_with_point(config: str, seed: int = 0, **overrides):
     if cfg in ("c0", "c2", "c4"):
         prm = N.GenParams()
         getattr(g, f"pdlp_gen_{cfg}_params")(C.byref(prm), seed)
+        window = overrides.pop("row_window", None)
         for k, val in overrides.items():
             setattr(prm, k, val)
+        if window is not None:
+            # rows [r0, r1) as a standalone LP (counter-based streams, threaded)
+            r0, r1 = window
+            return _wrap(g.pdlp_gen_random_lp_window(C.byref(prm), int(r0), int(r1)))
         return _wrap(g.pdlp_gen_random_lp(C.byref(prm)))
     if cfg in ("c1", "transport"):
         return _wrap(g.pdlp_gen_transport(overrides.get("sources", 2000),

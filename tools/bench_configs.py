@@ -29,13 +29,21 @@ import paper_2501_07018_b200 as P  # noqa: E402
 
 def measure(cfg: str, steps: int, warmup: int, ttt_limit: float) -> dict:
     t0 = time.perf_counter()
-    p = P.generate(cfg, 0)
+    extra = {}
+    if cfg == "c4w":
+        # C4 recipe, 1/8 row shard as a standalone LP (SURVEY 8(d) C4 row:
+        # 18.75M x 300M, ~375M entries on one GPU); polishing off so the
+        # polishing states of 300M columns are not reserved
+        p = P.generate("c4", 0, row_window=(0, 150_000_000 // 8))
+        extra = {"enable_polish": False}
+    else:
+        p = P.generate(cfg, 0)
     gen_s = time.perf_counter() - t0
     m, n, nnz = p.rows(), p.cols(), p.a.nonzeros()
-    P.solve(p, bench._options(P, 8, 0))  # warm-up (module, pool, staging)
-    res = P.solve(p, bench._options(P, steps, warmup))
+    P.solve(p, bench._options(P, 8, 0, **extra))  # warm-up (module, pool, staging)
+    res = P.solve(p, bench._options(P, steps, warmup, **extra))
     value = res.timed_iterations / res.timed_seconds
-    prof = P.solve(p, bench._options(P, steps, warmup, profile_kernels=True))
+    prof = P.solve(p, bench._options(P, steps, warmup, profile_kernels=True, **extra))
     kb = bench.step_kernel_bytes(m, n, nnz)
     peak, peak_src = bench._peaks()
     per = {}
@@ -47,7 +55,8 @@ def measure(cfg: str, steps: int, warmup: int, ttt_limit: float) -> dict:
     step_bytes = sum(kb.values())
     tol = P.relative_tolerances(p)
     ttt = P.solve(p, P.SolverOptions(tolerances=P.TerminationTolerances(*tol),
-                                     iteration_limit=1_000_000, time_limit_seconds=ttt_limit))
+                                     iteration_limit=1_000_000, time_limit_seconds=ttt_limit,
+                                     **extra))
     return {
         "config": cfg, "m": m, "n": n, "nnz": nnz, "generate_seconds": gen_s,
         "value": value, "unit": "iters/s", "steps": steps, "warmup": warmup,
