@@ -52,7 +52,8 @@ struct GapScalars {
   double value;
   unsigned long long first;  // first crossing group index (perf)
   int num_events;            // compacted event count (select output)
-  int pad;
+  int num_high;              // partial sort: events at or above the threshold
+  unsigned long long thresh; // partial sort: threshold key
 };
 
 struct Work {
@@ -62,12 +63,16 @@ struct Work {
   uint64_t *keys_in, *keys_out;
   int32_t* vals_out;
   double *cs, *bs;  // sorted masses (perf scans)
+  int32_t* hsel;    // partial sort: slots of the selected (top) events
+  uint64_t *samp_in, *samp_out;  // partial sort: key sample and its sort
   GapScalars* sc;
   void* cub_tmp;
   size_t cub_bytes;
 };
 
 __host__ __device__ inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+constexpr int kGapSample = 65536;  // keys sampled to place the partial-sort threshold
 
 size_t cub_bytes_for(int64_t N) {
   size_t a = 0, b = 0, c = 0;
@@ -80,7 +85,13 @@ size_t cub_bytes_for(int64_t N) {
   cub::DeviceSelect::Flagged(nullptr, c, thrust::counting_iterator<int32_t>(0),
                              static_cast<uint8_t*>(nullptr), static_cast<int32_t*>(nullptr),
                              static_cast<int*>(nullptr), static_cast<int>(N));
-  return std::max(a, std::max(b, c));
+  size_t d = 0, e = 0;
+  cub::DeviceSelect::Flagged(nullptr, d, static_cast<uint64_t*>(nullptr),
+                             static_cast<uint8_t*>(nullptr), static_cast<uint64_t*>(nullptr),
+                             static_cast<int*>(nullptr), static_cast<int>(N));
+  cub::DeviceRadixSort::SortKeysDescending(nullptr, e, static_cast<uint64_t*>(nullptr),
+                                           static_cast<uint64_t*>(nullptr), kGapSample);
+  return std::max(std::max(a, std::max(b, c)), std::max(d, e));
 }
 
 Work carve(void* base, int64_t n, int64_t m) {
@@ -102,6 +113,9 @@ Work carve(void* base, int64_t n, int64_t m) {
   w.vals_out = reinterpret_cast<int32_t*>(take(4 * N));
   w.cs = reinterpret_cast<double*>(take(8 * N));
   w.bs = reinterpret_cast<double*>(take(8 * N));
+  w.hsel = reinterpret_cast<int32_t*>(take(4 * N));
+  w.samp_in = reinterpret_cast<uint64_t*>(take(8 * kGapSample));
+  w.samp_out = reinterpret_cast<uint64_t*>(take(8 * kGapSample));
   w.sc = reinterpret_cast<GapScalars*>(take(sizeof(GapScalars)));
   w.cub_bytes = cub_bytes_for(N);
   w.cub_tmp = take(w.cub_bytes);
@@ -295,6 +309,23 @@ __global__ void gather_masses_kernel(Work w, int64_t E) {
 
 __global__ void init_first_kernel(Work w) { w.sc->first = ~0ull; }
 
+// Partial sort: a strided sample of the keys places a threshold so that
+// about a fraction q of the events lie at or above it.
+__global__ void sample_keys_kernel(Work w, int64_t E) {
+  GRID_STRIDE(i, kGapSample) w.samp_in[i] = w.keys_in[(i * E) / kGapSample];
+}
+__global__ void threshold_kernel(Work w, int rank) { w.sc->thresh = w.samp_out[rank]; }
+__global__ void high_flags_kernel(Work w, int64_t E) {
+  const uint64_t t = w.sc->thresh;
+  GRID_STRIDE(i, E) w.flag[i] = w.keys_in[i] >= t ? 1 : 0;
+}
+// Position of the first crossing as a fraction of all events (1 when none):
+// the engine sizes the next partial sort from it.
+__global__ void hit_fraction_kernel(Work w, int64_t E, double* out) {
+  const unsigned long long f = w.sc->first;
+  *out = (f == ~0ull || E <= 0) ? 1.0 : static_cast<double>(f) / static_cast<double>(E);
+}
+
 // Parallel sweep: cs/bs hold exclusive prefix masses in sorted order.
 __global__ void first_hit_kernel(Work w, int64_t E, const double* r_slot, double r_value) {
   const double r = r_slot ? *r_slot : r_value;
@@ -432,8 +463,8 @@ using namespace pdlp;
 extern "C" size_t pdlpk_gap_work_bytes(int64_t n, int64_t m) {
   const int64_t N = n + 2 * m;
   return align_up(N) + align_up(8 * N) * 3 + align_up(4 * N) + align_up(8 * N) * 2 +
-         align_up(4 * N) + align_up(8 * N) * 2 + align_up(sizeof(GapScalars)) +
-         align_up(cub_bytes_for(N)) + 256;
+         align_up(4 * N) + align_up(8 * N) * 2 + align_up(4 * N) + 2 * align_up(8 * kGapSample) +
+         align_up(sizeof(GapScalars)) + align_up(cub_bytes_for(N)) + 256;
 }
 
 extern "C" int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const double* y,
@@ -468,16 +499,73 @@ extern "C" int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const 
   return static_cast<int>(cudaGetLastError());
 }
 
+// Perf mode, large E, 0 < q < 0.5: sort only the top ~q of the events.  The
+// sweep runs in descending lambda and stops at its first crossing, so if the
+// crossing lies among the selected events (all events with a key at or above
+// the threshold: whole tie groups) the result equals the full sweep's; else
+// the full sort runs.  Returns 1 when the partial path decided, 0 to fall
+// back.  Two host syncs (the selected count, the hit).
+static int gap_partial(const Work& w, int64_t E, double q, const double* r_slot, double r_value,
+                       cudaStream_t s) {
+  keys_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+  sample_keys_kernel<<<ew_blocks(kGapSample), kT, 0, s>>>(w, E);
+  size_t bytes = w.cub_bytes;
+  if (cub::DeviceRadixSort::SortKeysDescending(w.cub_tmp, bytes, w.samp_in, w.samp_out, kGapSample,
+                                               0, 64, s) != cudaSuccess) {
+    return -1;
+  }
+  const int rank = std::min(kGapSample - 1, static_cast<int>(q * kGapSample));
+  threshold_kernel<<<1, 1, 0, s>>>(w, rank);
+  high_flags_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+  uint64_t* keys_h = reinterpret_cast<uint64_t*>(w.cs);
+  bytes = w.cub_bytes;
+  if (cub::DeviceSelect::Flagged(w.cub_tmp, bytes, w.keys_in, w.flag, keys_h, &w.sc->num_high,
+                                 static_cast<int>(E), s) != cudaSuccess) {
+    return -1;
+  }
+  bytes = w.cub_bytes;
+  if (cub::DeviceSelect::Flagged(w.cub_tmp, bytes, w.sel, w.flag, w.hsel, &w.sc->num_high,
+                                 static_cast<int>(E), s) != cudaSuccess) {
+    return -1;
+  }
+  int eh = 0;
+  cudaMemcpyAsync(&eh, &w.sc->num_high, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+  if (eh <= 0 || eh >= E) return 0;
+  bytes = w.cub_bytes;
+  if (cub::DeviceRadixSort::SortPairsDescending(w.cub_tmp, bytes, keys_h, w.keys_out, w.hsel,
+                                                w.vals_out, eh, 0, 64, s) != cudaSuccess) {
+    return -1;
+  }
+  gather_masses_kernel<<<ew_blocks(eh), kT, 0, s>>>(w, eh);
+  bytes = w.cub_bytes;
+  cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.cs, w.cs, eh, s);
+  bytes = w.cub_bytes;
+  cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.bs, w.bs, eh, s);
+  init_first_kernel<<<1, 1, 0, s>>>(w);
+  first_hit_kernel<<<ew_blocks(eh), kT, 0, s>>>(w, eh, r_slot, r_value);
+  unsigned long long first = 0;
+  cudaMemcpyAsync(&first, &w.sc->first, sizeof(first), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+  return first == ~0ull ? 0 : 1;
+}
+
 extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const double* y,
                                 const double* ax, const double* aty, double omega,
                                 const double* r_slot, double r_value, int64_t E,
-                                const pdlpk_red* red, void* work, double* gap_slot,
+                                const pdlpk_red* red, void* work, double* gap_slot, double q,
                                 cudaStream_t s) {
   const int64_t n = P->n, m = P->m;
   Work w = carve(work, n, m);
   const GapIn g = make_in(P, x, y, ax, aty, omega);
   const bool parity = red->parity != 0;
-  if (E > 0) {
+  bool decided = false;
+  if (!parity && q > 0.0 && q < 0.5 && E > (int64_t(1) << 20)) {
+    const int pr = gap_partial(w, E, q, r_slot, r_value, s);
+    if (pr < 0) return static_cast<int>(cudaGetLastError());
+    decided = pr == 1;
+  }
+  if (E > 0 && !decided) {
     keys_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
     size_t bytes = w.cub_bytes;
     const cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(
@@ -489,16 +577,21 @@ extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const d
     value_seq_kernel<<<1, 1, 0, s>>>(g, w, r_slot, r_value, gap_slot);
     return static_cast<int>(cudaGetLastError());
   }
-  if (E > 0) {
-    gather_masses_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
-    size_t bytes = w.cub_bytes;
-    cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.cs, w.cs, static_cast<int>(E), s);
-    bytes = w.cub_bytes;
-    cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.bs, w.bs, static_cast<int>(E), s);
+  if (!decided) {
+    if (E > 0) {
+      gather_masses_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+      size_t bytes = w.cub_bytes;
+      cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.cs, w.cs, static_cast<int>(E), s);
+      bytes = w.cub_bytes;
+      cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.bs, w.bs, static_cast<int>(E), s);
+    }
+    init_first_kernel<<<1, 1, 0, s>>>(w);
+    if (E > 0) first_hit_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E, r_slot, r_value);
   }
-  init_first_kernel<<<1, 1, 0, s>>>(w);
-  if (E > 0) first_hit_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E, r_slot, r_value);
+  // (a decided partial path has its crossing index < E_high: the no-crossing
+  // branch of finalize, which reads the last of all E events, is not taken)
   finalize_perf_kernel<<<1, 1, 0, s>>>(w, E, r_slot, r_value);
+  hit_fraction_kernel<<<1, 1, 0, s>>>(w, E, gap_slot + 2);
   const double* lam_star = &w.sc->lambda_star;
   auto fv = [g, lam_star] __device__(int64_t t, double* v) -> unsigned {
     const double lambda = *lam_star;

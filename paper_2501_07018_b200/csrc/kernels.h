@@ -309,9 +309,12 @@ size_t pdlpk_gap_work_bytes(int64_t n, int64_t m);
 int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
                       const double* aty, double omega, const pdlpk_red* red, void* work,
                       int* count_out, cudaStream_t s);
+/* gap_slot[0] = the gap, gap_slot[2] = the first crossing's position as a
+ * fraction of E (1 if none).  q in (0, 0.5): perf mode may sort only the
+ * top ~q of the events first (exact; falls back to the full sort). */
 int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
                      const double* aty, double omega, const double* r_slot, double r_value,
-                     int64_t E, const pdlpk_red* red, void* work, double* gap_slot,
+                     int64_t E, const pdlpk_red* red, void* work, double* gap_slot, double q,
                      cudaStream_t s);
 /* slot = sqrt(omega*dx2 + dy2/omega) from two slots (restart_progress_metric). */
 int pdlpk_radius(const double* dx2, const double* dy2, double omega, double* out,

@@ -1413,6 +1413,7 @@ class Engine {
   }
 
   void gaps_local(const pdlpk_problem& P, const GapQuery* q, int count, double omega, double* out) {
+    if (gap_partial_off_) gap_q_ = 1.0;
     if (gap_shared_ && count > 1) {
       for (int i = 0; i < count; ++i) gaps_local(P, q + i, 1, omega, out + i);
       return;
@@ -1427,10 +1428,19 @@ class Engine {
     for (int i = 0; i < count; ++i) {
       const double radius = std::sqrt(omega * q[i].dx2 + q[i].dy2 / omega);
       PDLP_LAUNCH(pdlpk_gap_finish(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, nullptr, radius,
-                                   host_islots_[i], &r, gap_work_[i].get(), slot(kSlotGap + i), s()));
+                                   host_islots_[i], &r, gap_work_[i].get(), slot(kSlotGap + i),
+                                   gap_q_, s()));
     }
-    const double* h = read_slots(kSlotGap + count);
-    for (int i = 0; i < count; ++i) out[i] = h[kSlotGap + i];
+    const double* h = read_slots(kSlotGap + count + 2);
+    double hit = 0.0;
+    for (int i = 0; i < count; ++i) {
+      out[i] = h[kSlotGap + i];
+      hit = std::max(hit, h[kSlotGap + 2 + i]);
+    }
+    // Size the next partial sort from where this crossing fell (twice its
+    // depth plus a margin); deep crossings (C1: ~50 %) use the full sort.
+    gap_q_ = std::min(1.0, 2.0 * hit + 0.02);
+    if (gap_partial_off_) gap_q_ = 1.0;
   }
 
   // ---- the loop ----------------------------------------------------------
@@ -1506,6 +1516,12 @@ class Engine {
   DevBuf<double> red_scratch_;
   DevBuf<char> gap_work_[2];
   bool gap_shared_ = false;  // one gap buffer, queries evaluated one at a time
+  double gap_q_ = 0.25;      // partial-sort fraction for the next gap evaluation
+  // PDLP_GAP_PARTIAL=0: always the full sort (measurements)
+  bool gap_partial_off_ = [] {
+    const char* e = std::getenv("PDLP_GAP_PARTIAL");
+    return e != nullptr && e[0] == '0';
+  }();
   DevBuf<int> islots_;
   int* host_islots_ = nullptr;
   DevBuf<double> zeros_n_, zeros_m_;
@@ -2337,7 +2353,7 @@ int pdlp_normalized_duality_gap(const pdlp_problem_view* problem, const double* 
     PDLP_CK(cudaMemcpyAsync(&events, E.islots_.get(), sizeof(int), cudaMemcpyDeviceToHost, E.s()));
     PDLP_CK(cudaStreamSynchronize(E.s()));
     PDLP_LAUNCH(pdlpk_gap_finish(&P, dx.get(), dy.get(), dax.get(), daty.get(), omega, nullptr, r,
-                                 events, &red, E.gap_work_[0].get(), E.slot(0), E.s()));
+                                 events, &red, E.gap_work_[0].get(), E.slot(0), 0.0, E.s()));
     *gap = E.read_slots(1)[0];
   });
 }
