@@ -35,6 +35,7 @@
 #ifndef PDLP_B200_H_
 #define PDLP_B200_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -218,6 +219,29 @@ int pdlp_device_count(void);
  * pool and keep it between calls (no map/unmap per solve); this returns the
  * pool's unused memory on `device` to the driver.  0 or a negative error. */
 int pdlp_trim_device_memory(int device);
+
+/* ------------------------------------------------------------- MPS --- *
+ * Free-format MPS reader / writer with the reference's behaviour
+ * (proj/include/pdhglp/mps.hpp:87-535: parse_mps, read_mps_file, write_mps).
+ * The parsed model is in minimization form (OBJSENSE MAX negates the
+ * objective; pdlp_mps_maximize reports it).  Parse errors return
+ * PDLP_ERR_INVALID_PROBLEM with the reference's message ("line N: ...", or
+ * "invalid model: ..." for a model that fails validation). */
+typedef struct pdlp_mps pdlp_mps;
+int pdlp_mps_parse(const char* text, size_t len, pdlp_mps** out);
+int pdlp_mps_read_file(const char* path, pdlp_mps** out);
+/* Borrowed view, valid until pdlp_mps_free. */
+void pdlp_mps_view(const pdlp_mps* model, pdlp_problem_view* view);
+int32_t pdlp_mps_maximize(const pdlp_mps* model);
+const char* pdlp_mps_name(const pdlp_mps* model);
+const char* pdlp_mps_objective_name(const pdlp_mps* model);
+const char* pdlp_mps_row_name(const pdlp_mps* model, int64_t row);
+const char* pdlp_mps_col_name(const pdlp_mps* model, int64_t col);
+void pdlp_mps_free(pdlp_mps* model);
+/* write_mps text (generated names OBJ / R# / C#); free with pdlp_mps_free_text. */
+int pdlp_mps_write(const pdlp_problem_view* problem, const char* name, int32_t maximize,
+                   char** text, size_t* len);
+void pdlp_mps_free_text(char* text);
 
 /* ------------------------------------------------- row-sharded solve --- *
  * B200 extension (the reference solve is single-process).

@@ -55,6 +55,17 @@ _REF_ONLY = {
     "ref_instance_view": (None, [C.c_void_p, P]),
     "ref_instance_optimal_objective": (C.c_double, [C.c_void_p]),
     "ref_instance_free": (None, [C.c_void_p]),
+    "ref_mps_parse": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "ref_mps_view": (None, [C.c_void_p, P]),
+    "ref_mps_maximize": (C.c_int32, [C.c_void_p]),
+    "ref_mps_name": (C.c_char_p, [C.c_void_p]),
+    "ref_mps_objective_name": (C.c_char_p, [C.c_void_p]),
+    "ref_mps_row_name": (C.c_char_p, [C.c_void_p, C.c_int64]),
+    "ref_mps_col_name": (C.c_char_p, [C.c_void_p, C.c_int64]),
+    "ref_mps_free": (None, [C.c_void_p]),
+    "ref_mps_write": (C.c_int, [P, C.c_char_p, C.c_int32, C.POINTER(C.c_void_p),
+                                C.POINTER(C.c_size_t)]),
+    "ref_mps_free_text": (None, [C.c_void_p]),
 }
 
 KIND = {"random-feasible": 0, "random-infeasible": 1, "transport": 2, "feasibility-system": 3}
@@ -100,6 +111,21 @@ class Oracle:
             ref_last_error = lib.ref_last_error
 
         return S.run_solve(_Shim, "ref_solve", p, o, self.options(o))
+
+    # reference MPS reader / writer (mps.hpp), compiled reference only
+    def parse_mps(self, text):
+        from paper_2501_07018_b200.mps import model_from_handle
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        h = C.c_void_p()
+        self._check(self.lib.ref_mps_parse(data, len(data), C.byref(h)))
+        try:
+            return model_from_handle(self.lib, "ref_mps_", h)
+        finally:
+            self.lib.ref_mps_free(h)
+
+    def write_mps(self, p, name="", maximize=False):
+        from paper_2501_07018_b200.mps import write_text
+        return write_text(self.lib, "ref_mps_write", "ref_mps_free_text", p, name, maximize)
 
     def pdhg_step(self, p, x, y, omega, eta):
         x = np.ascontiguousarray(x, np.float64)

@@ -10,12 +10,14 @@
 // Only marshalling lives here; every number comes from the reference code.
 
 #include <pdhglp/generator.hpp>
+#include <pdhglp/mps.hpp>
 #include <pdhglp/rescaling.hpp>
 #include <pdhglp/residuals.hpp>
 #include <pdhglp/restarts.hpp>
 #include <pdhglp/solver.hpp>
 #include <pdhglp/step.hpp>
 
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -314,6 +316,66 @@ int ref_step_size_rules(double movement, double curvature, double eta_bar, doubl
   *next_out = next_step_size(eta_bar, eta, k);
   return PDLP_OK;
 }
+
+// ---- MPS: the reference's parse_mps / write_mps (mps.hpp:87-535) -------
+struct RefMps {
+  MpsModel model;
+};
+
+int ref_mps_parse(const char* text, size_t len, void** out) {
+  try {
+    *out = new RefMps{parse_mps(std::string_view(text ? text : "", len))};
+    return PDLP_OK;
+  } catch (const MpsParseError& e) {
+    g_err = e.what();
+    return PDLP_ERR_INVALID_PROBLEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PDLP_ERR_INTERNAL;
+  }
+}
+
+void ref_mps_view(const void* h, pdlp_problem_view* v) {
+  const LpProblem& p = static_cast<const RefMps*>(h)->model.problem;
+  v->rows = p.a.rows;
+  v->cols = p.a.cols;
+  v->by_row = {p.a.rows, static_cast<int64_t>(p.a.by_row.value.size()), p.a.by_row.start.data(),
+               p.a.by_row.index.data(), p.a.by_row.value.data()};
+  v->by_col = {p.a.cols, static_cast<int64_t>(p.a.by_col.value.size()), p.a.by_col.start.data(),
+               p.a.by_col.index.data(), p.a.by_col.value.data()};
+  v->objective = p.objective.data();
+  v->con_lower = p.con_lower.data();
+  v->con_upper = p.con_upper.data();
+  v->var_lower = p.var_lower.data();
+  v->var_upper = p.var_upper.data();
+}
+
+int32_t ref_mps_maximize(const void* h) { return static_cast<const RefMps*>(h)->model.maximize ? 1 : 0; }
+const char* ref_mps_name(const void* h) { return static_cast<const RefMps*>(h)->model.name.c_str(); }
+const char* ref_mps_objective_name(const void* h) {
+  return static_cast<const RefMps*>(h)->model.objective_name.c_str();
+}
+const char* ref_mps_row_name(const void* h, int64_t j) {
+  return static_cast<const RefMps*>(h)->model.row_names[static_cast<size_t>(j)].c_str();
+}
+const char* ref_mps_col_name(const void* h, int64_t i) {
+  return static_cast<const RefMps*>(h)->model.col_names[static_cast<size_t>(i)].c_str();
+}
+void ref_mps_free(void* h) { delete static_cast<RefMps*>(h); }
+
+int ref_mps_write(const pdlp_problem_view* pv, const char* name, int32_t maximize, char** text,
+                  size_t* len) {
+  return guarded([&] {
+    const std::string s = write_mps(to_problem(pv), name ? name : "", maximize != 0);
+    char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    *text = buf;
+    *len = s.size();
+    return PDLP_OK;
+  });
+}
+
+void ref_mps_free_text(char* t) { std::free(t); }
 
 double ref_initialize_primal_weight(const pdlp_problem_view* pv) {
   return initialize_primal_weight(to_problem(pv));

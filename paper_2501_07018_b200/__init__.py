@@ -12,7 +12,10 @@ from .solver import (CertificateKind, InfeasibilityCertificate, IterationRecord,
                      kkt_residuals, normalized_duality_gap, pdhg_step, solve, solve_status_name,
                      spmv, spmv_transpose, step_size_rules)
 
+from .mps import MpsModel, parse_mps, read_mps, write_mps, write_mps_file
+
 __all__ = [
+    "MpsModel", "parse_mps", "read_mps", "write_mps", "write_mps_file",
     "CompressedLayout", "LpProblem", "SparseMatrix", "generate", "generate_with_point", "problem",
     "relative_tolerances", "CertificateKind", "InfeasibilityCertificate", "IterationRecord",
     "ResidualSummary", "RestartThresholds", "SolveResult", "SolverOptions", "SolveStatus",

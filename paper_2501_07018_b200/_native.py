@@ -216,6 +216,18 @@ SOLVER_SIGNATURES = {
                                      C.POINTER(ShardView), C.POINTER(C.c_void_p)]),
     "pdlp_shard_free": (None, [C.c_void_p]),
     "pdlp_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "pdlp_mps_parse": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "pdlp_mps_read_file": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "pdlp_mps_view": (None, [C.c_void_p, C.POINTER(ProblemView)]),
+    "pdlp_mps_maximize": (C.c_int32, [C.c_void_p]),
+    "pdlp_mps_name": (C.c_char_p, [C.c_void_p]),
+    "pdlp_mps_objective_name": (C.c_char_p, [C.c_void_p]),
+    "pdlp_mps_row_name": (C.c_char_p, [C.c_void_p, C.c_int64]),
+    "pdlp_mps_col_name": (C.c_char_p, [C.c_void_p, C.c_int64]),
+    "pdlp_mps_free": (None, [C.c_void_p]),
+    "pdlp_mps_write": (C.c_int, [C.POINTER(ProblemView), C.c_char_p, C.c_int32,
+                                 C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "pdlp_mps_free_text": (None, [C.c_void_p]),
     "pdlp_solve_sharded": (C.c_int, [C.POINTER(ProblemView), C.POINTER(Options), C.c_int32,
                                      C.c_int32, C.c_char_p, C.POINTER(Result)]),
     "pdlp_solve_sharded_emulated": (C.c_int, [C.POINTER(ProblemView), C.POINTER(Options),

@@ -37,7 +37,7 @@ CU_FLAGS += _DEFINES
 CXX_FLAGS += _DEFINES
 
 CU_SOURCES = ["k_step.cu", "k_vec.cu", "k_gap.cu", "k_scale.cu", "k_valid.cu"]
-CPP_SOURCES = ["solver.cpp", "host_stage.cpp", "comm.cpp", "shard.cpp"]
+CPP_SOURCES = ["solver.cpp", "host_stage.cpp", "comm.cpp", "shard.cpp", "mps.cpp"]
 HEADERS = ["common.cuh", "spmv.cuh", "reduce.cuh", "kernels.h", "device.hpp", "host_stage.hpp", "comm.hpp", "shard.hpp"]
 
 LIB = os.path.join(HERE, "libpdlp_b200.so")
