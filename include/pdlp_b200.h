@@ -220,6 +220,15 @@ int pdlp_device_count(void);
  * pool's unused memory on `device` to the driver.  0 or a negative error. */
 int pdlp_trim_device_memory(int device);
 
+/* Original-space re-verification of an infeasibility certificate (the `check`
+ * command, tools/main.cpp:199-311 -> residuals.hpp:222-299): kind 0 tests a
+ * primal-infeasibility ray y (rows), kind 1 a dual-infeasibility ray x
+ * (columns), at relative tolerance eps_ray.  *verified = 1 when it holds;
+ * residual / objective as the reference's try_*_infeasibility reports them. */
+int pdlp_check_certificate(const pdlp_problem_view* problem, int32_t kind, const double* ray,
+                           double eps_ray, int32_t* verified, double* residual,
+                           double* objective);
+
 /* ------------------------------------------------------------- MPS --- *
  * Free-format MPS reader / writer with the reference's behaviour
  * (proj/include/pdhglp/mps.hpp:87-535: parse_mps, read_mps_file, write_mps).
@@ -340,7 +349,8 @@ int pdlp_normalized_duality_gap(const pdlp_problem_view* problem, const double* 
 
 /* recover_reduced_costs (residuals.hpp:49-64) + kkt_residuals
  * (residuals.hpp:135-158) on the given problem.  rc_mode 0 = Natural,
- * 1 = BoundRobust.  r_out may be NULL. */
+ * 1 = BoundRobust (r_out, may be NULL, receives them); 2 = use the reduced
+ * costs passed in r_out (kkt_residuals(p, x, y, r), the `check` command). */
 int pdlp_kkt_residuals(const pdlp_problem_view* problem, const double* x, const double* y,
                        int32_t rc_mode, int32_t mode, double* r_out,
                        pdlp_residual_summary* summary);

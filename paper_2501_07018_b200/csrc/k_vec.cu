@@ -351,8 +351,9 @@ int pdlpk_screen(const pdlpk_problem* P, int32_t orig, const double* x, const do
     const double xi = x[i];
     const double d = interval_distance(xi, lv[i], uv[i]);
     v[0] = cs ? d * cs[i] : d;
-    const double ri = reduced_cost(c[i], aty[i], xi, lv[i], uv[i], rc_mode);
-    if (r_out) r_out[i] = ri;
+    // rc_mode 2: r is given (read from r_out), as in kkt_residuals(p, x, y, r)
+    const double ri = rc_mode == 2 ? r_out[i] : reduced_cost(c[i], aty[i], xi, lv[i], uv[i], rc_mode);
+    if (r_out && rc_mode != 2) r_out[i] = ri;
     const double dd = fabs(c[i] - aty[i] - ri);
     v[1] = cs ? dd / cs[i] : dd;
     v[2] = c[i] * xi;

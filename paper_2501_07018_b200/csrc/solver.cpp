@@ -2367,15 +2367,46 @@ int pdlp_kkt_residuals(const pdlp_problem_view* problem, const double* x, const 
     const pdlpk_problem P = E.problem().view();
     Inner& D = E.main_;
     D.allocate(P.n, P.m, pdlpk_step_partials(&P), 4);
-    DevBuf<double> dx = to_dev(x, P.n, E.s()), dy = to_dev(y, P.m, E.s()), dr(P.n);
+    DevBuf<double> dx = to_dev(x, P.n, E.s()), dy = to_dev(y, P.m, E.s());
+    // rc_mode 2: r_out carries the reduced costs to use (kkt_residuals with r,
+    // residuals.hpp:135-158), else it receives the recovered ones
+    DevBuf<double> dr = rc_mode == 2 ? to_dev(r_out, P.n, E.s()) : DevBuf<double>(P.n);
     const Summary s = E.original_kkt(P, dx.get(), dy.get(), rc_mode, dr.get(), D);
-    from_dev(r_out, dr, P.n, E.s());
+    if (rc_mode != 2) from_dev(r_out, dr, P.n, E.s());
     summary->primal_residual_inf = s.primal;
     summary->dual_residual_inf = s.dual;
     summary->primal_objective = s.pobj;
     summary->dual_objective = s.dobj;
     summary->abs_gap = s.abs_gap;
     summary->rel_gap = s.rel_gap;
+  });
+}
+
+int pdlp_check_certificate(const pdlp_problem_view* problem, int32_t kind, const double* ray,
+                           double eps_ray, int32_t* verified, double* residual,
+                           double* objective) {
+  if (problem == nullptr || ray == nullptr || verified == nullptr || (kind != 0 && kind != 1)) {
+    g_last_error = "invalid certificate check";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&] {
+    Component C(problem, PDLP_MODE_PERF, 4);
+    Engine& E = *C.E;
+    const pdlpk_problem P = E.problem().view();
+    Inner& D = E.main_;
+    D.allocate(P.n, P.m, pdlpk_step_partials(&P), 4);
+    double res = kInf, obj = 0.0;
+    bool ok;
+    if (kind == PDLP_CERT_PRIMAL_INFEASIBLE) {
+      DevBuf<double> dy = to_dev(ray, P.m, E.s());
+      ok = E.try_primal(P, 1, dy.get(), eps_ray, D, res, obj);
+    } else {
+      DevBuf<double> dx = to_dev(ray, P.n, E.s());
+      ok = E.try_dual(P, 1, dx.get(), eps_ray, D, res, obj);
+    }
+    *verified = ok ? 1 : 0;
+    if (residual != nullptr) *residual = res;
+    if (objective != nullptr) *objective = obj;
   });
 }
 

@@ -354,6 +354,29 @@ def kkt_residuals(p: LpProblem, x, y, rc_mode: int = 0, mode="parity"):
                               s.dual_objective, s.abs_gap, s.rel_gap)
 
 
+def kkt_residuals_given(p: LpProblem, x, y, r, mode="perf") -> ResidualSummary:
+    """kkt_residuals(p, x, y, r) with the given reduced costs (residuals.hpp:
+    135-158), original space, on the device (the `check` command)."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    r = np.array(r, np.float64)
+    s = N.ResidualSummary()
+    _check(N.lib().pdlp_kkt_residuals(C.byref(p.view()), _pd(x), _pd(y), 2, _mode(mode), _pd(r),
+                                      C.byref(s)))
+    return ResidualSummary(s.primal_residual_inf, s.dual_residual_inf, s.primal_objective,
+                           s.dual_objective, s.abs_gap, s.rel_gap)
+
+
+def check_certificate(p: LpProblem, kind, ray, eps_ray: float = 1e-12):
+    """try_primal_infeasibility / try_dual_infeasibility (residuals.hpp:222-299)
+    on the original data, on the device.  Returns (verified, residual, objective)."""
+    ray = np.ascontiguousarray(ray, np.float64)
+    ok, res, obj = C.c_int32(0), C.c_double(0.0), C.c_double(0.0)
+    _check(N.lib().pdlp_check_certificate(C.byref(p.view()), int(kind), _pd(ray), eps_ray,
+                                          C.byref(ok), C.byref(res), C.byref(obj)))
+    return bool(ok.value), res.value, obj.value
+
+
 def step_size_rules(movement: float, curvature: float, eta_bar: float, eta: float, k: int):
     lim, nxt = C.c_double(0.0), C.c_double(0.0)
     _check(N.lib().pdlp_step_size_rules(movement, curvature, eta_bar, eta, k, C.byref(lim),
