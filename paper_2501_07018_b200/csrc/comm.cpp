@@ -4,7 +4,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <condition_variable>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -80,9 +82,7 @@ class NcclComm final : public Comm {
     std::memcpy(uid.internal, id, 128);
     check_nccl(api.comm_init_rank(&comm_, world, uid, rank), "ncclCommInitRank");
   }
-  ~NcclComm() override {
-    if (comm_ != nullptr) nccl().comm_destroy(comm_);
-  }
+
   int rank() const override { return rank_; }
   int world() const override { return world_; }
   void allgather(double* buf, size_t count, cudaStream_t s) override {
@@ -100,10 +100,67 @@ class NcclComm final : public Comm {
     check_nccl(nccl().all_reduce(buf, buf, count, ncclDouble, use_max ? ncclMax : ncclSum, comm_, s),
                "ncclAllReduce");
   }
+  void barrier(cudaStream_t s) override {
+    if (token_ == nullptr) PDLP_CK(cudaMalloc(&token_, sizeof(double)));
+    check_nccl(nccl().all_reduce(token_, token_, 1, ncclDouble, ncclSum, comm_, s), "ncclAllReduce");
+  }
+  std::vector<double*> peer_pointers(double* mine, cudaStream_t s) override {
+    // Exchange CUDA IPC handles (64 bytes per rank) with one all-gather.  A
+    // local failure still takes part in the exchange (all-zero handle) and
+    // returns an empty vector, so no peer is left waiting in a collective.
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    std::vector<char> all(hb * world_, 0);
+    bool ok = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(all.data() + hb * rank_),
+                                  mine) == cudaSuccess;
+    cudaGetLastError();
+    char* dev = nullptr;
+    PDLP_CK(cudaMalloc(&dev, hb * world_));
+    PDLP_CK(cudaMemcpyAsync(dev, all.data(), hb * world_, cudaMemcpyHostToDevice, s));
+    check_nccl(nccl().all_gather(dev + hb * rank_, dev, hb, ncclChar, comm_, s), "ncclAllGather");
+    PDLP_CK(cudaMemcpyAsync(all.data(), dev, hb * world_, cudaMemcpyDeviceToHost, s));
+    PDLP_CK(cudaStreamSynchronize(s));
+    cudaFree(dev);
+    std::vector<double*> out(static_cast<size_t>(world_), nullptr);
+    for (int r = 0; r < world_ && ok; ++r) {
+      if (r == rank_) {
+        out[r] = mine;
+        continue;
+      }
+      cudaIpcMemHandle_t peer;
+      std::memcpy(&peer, all.data() + hb * r, hb);
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, peer, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+        break;
+      }
+      opened_.push_back(p);
+      out[r] = static_cast<double*>(p);
+    }
+    if (!ok) {
+      for (void* p : opened_) cudaIpcCloseMemHandle(p);
+      opened_.clear();
+      out.clear();
+    }
+    return out;
+  }
+  double* alloc_peer_buffer(size_t count) override {
+    double* p = nullptr;
+    PDLP_CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
+    return p;
+  }
+  void free_peer_buffer(double* p) override { cudaFree(p); }
+  ~NcclComm() override {
+    for (void* p : opened_) cudaIpcCloseMemHandle(p);
+    if (token_ != nullptr) cudaFree(token_);
+    if (comm_ != nullptr) nccl().comm_destroy(comm_);
+  }
 
  private:
   int rank_, world_;
   ncclComm_t comm_ = nullptr;
+  double* token_ = nullptr;
+  std::vector<void*> opened_;
 };
 
 }  // namespace
@@ -207,6 +264,23 @@ class ThreadComm final : public Comm {
     }
     release(s);
   }
+  void barrier(cudaStream_t s) override {
+    publish(nullptr, s);
+    release(s);
+  }
+  std::vector<double*> peer_pointers(double* mine, cudaStream_t s) override {
+    publish(mine, s);
+    std::vector<double*> out(static_cast<size_t>(world()));
+    for (int r = 0; r < world(); ++r) out[r] = const_cast<double*>(hub_->ptr[r]);
+    release(s);
+    return out;
+  }
+  double* alloc_peer_buffer(size_t count) override {
+    double* p = nullptr;
+    PDLP_CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
+    return p;
+  }
+  void free_peer_buffer(double* p) override { cudaFree(p); }
   void allreduce(double* buf, size_t count, bool use_max, cudaStream_t s) override {
     DevBuf<double> tmp(count);
     publish(buf, s);

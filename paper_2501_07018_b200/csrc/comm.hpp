@@ -19,6 +19,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <memory>
+#include <vector>
 
 namespace pdlp_host {
 
@@ -34,6 +35,18 @@ class Comm {
   virtual void reduce_scatter(const double* send, double* recv, size_t count, cudaStream_t s) = 0;
   // In place elementwise sum (or max) over ranks.
   virtual void allreduce(double* buf, size_t count, bool use_max, cudaStream_t s) = 0;
+  // Stream-level barrier: work enqueued on every rank's stream before the
+  // call is complete before work enqueued after it runs (no kernel spins).
+  virtual void barrier(cudaStream_t s) = 0;
+  // Every rank's address of a buffer each rank allocated with
+  // alloc_peer_buffer (collective; index = rank).  NVLink P2P across
+  // processes (CUDA IPC), plain pointers for ranks sharing a process.
+  // Empty if this rank could not map its peers (the caller agrees on a
+  // fallback with the other ranks).
+  virtual std::vector<double*> peer_pointers(double* mine, cudaStream_t s) = 0;
+  // Device memory that peers can map (not from the stream-ordered pool).
+  virtual double* alloc_peer_buffer(size_t count) = 0;
+  virtual void free_peer_buffer(double* p) = 0;
 };
 
 // NCCL communicator from a 128-byte ncclUniqueId created by rank 0 and

@@ -36,7 +36,12 @@ inline int ew_blocks(int64_t n) {
 }
 
 // ------------------------------------------------------------ primal pass ---
-__global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a) {
+// Push = the all-gather of x-bar folded in (row-sharded solve): each x-bar
+// pair is also stored into every peer's gathered vector over NVLink, so the
+// transfer overlaps this HBM-bound pass; dst.p[rank] is null (local block
+// is a.xbar itself).
+template <bool Push>
+__global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a, pdlpk_peer_sum dst) {
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const double eta = st->eta;
@@ -83,6 +88,14 @@ __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a) {
     xb.y = 2.0 * xp.y - xi.y;
     xn2[p] = xp;
     xb2[p] = xb;
+    if constexpr (Push) {
+#pragma unroll
+      for (int r = 0; r < PDLPK_MAX_PEERS; ++r) {
+        if (r < dst.world && dst.p[r] != nullptr) {
+          reinterpret_cast<double2*>(const_cast<double*>(dst.p[r]) + dst.offset)[p] = xb;
+        }
+      }
+    }
     if (pend) {
       const double2 s = sx2[p];
       sx2[p] = make_double2(s.x + w * xi.x, s.y + w * xi.y);
@@ -94,6 +107,11 @@ __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a) {
     const double xp = clampd(xi - tau * (c[i] - aty[i]), lv[i], uv[i]);
     xn[i] = xp;
     xbar[i] = 2.0 * xp - xi;
+    if constexpr (Push) {
+      for (int r = 0; r < dst.world; ++r) {
+        if (dst.p[r] != nullptr) const_cast<double*>(dst.p[r])[dst.offset + i] = 2.0 * xp - xi;
+      }
+    }
     if (pend) sx[i] = sx[i] + w * xi;
   }
 }
@@ -522,7 +540,26 @@ struct LaunchRowCol {
 // ------------------------------------------------- row-sharded attempt ---
 // Epilogues over reduce-scattered line sums (the layout's lines live on
 // other ranks' partial products), and the cross-rank decision.
-__global__ void __launch_bounds__(kEwThreads) row_epi_kernel(pdlpk_step_args a, const double* acc) {
+// Line sum i: acc[i], or the rank-ordered sum of the peers' partials.  The
+// loads are independent (one per rank, issued together) so the NVLink
+// latency of the remote reads overlaps.
+__device__ __forceinline__ double peer_value(const pdlpk_peer_sum& ps, const double* acc, int64_t i) {
+  if (ps.world == 0) return acc[i];
+  double v[PDLPK_MAX_PEERS];
+#pragma unroll
+  for (int r = 0; r < PDLPK_MAX_PEERS; ++r) {
+    if (r < ps.world) v[r] = __ldcg(ps.p[r] + ps.offset + i);
+  }
+  double t = v[0];
+#pragma unroll
+  for (int r = 1; r < PDLPK_MAX_PEERS; ++r) {
+    if (r < ps.world) t += v[r];
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(kEwThreads) row_epi_kernel(pdlpk_step_args a, const double* acc,
+                                                            pdlpk_peer_sum ps) {
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;
@@ -539,7 +576,7 @@ __global__ void __launch_bounds__(kEwThreads) row_epi_kernel(pdlpk_step_args a, 
   const int64_t m = a.P.m;
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < m;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    e.line(r, acc[r], e.load(r));
+    e.line(r, peer_value(ps, acc, r), e.load(r));
   }
   __shared__ double red[32];
   const double s1 = block_sum(e.dy2, red);
@@ -551,7 +588,8 @@ __global__ void __launch_bounds__(kEwThreads) row_epi_kernel(pdlpk_step_args a, 
   }
 }
 
-__global__ void __launch_bounds__(kEwThreads) col_epi_kernel(pdlpk_step_args a, const double* d) {
+__global__ void __launch_bounds__(kEwThreads) col_epi_kernel(pdlpk_step_args a, const double* d,
+                                                            pdlpk_peer_sum ps) {
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;
@@ -563,7 +601,7 @@ __global__ void __launch_bounds__(kEwThreads) col_epi_kernel(pdlpk_step_args a, 
   const int64_t n = a.P.n;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    e.line(i, d[i], e.load(i));
+    e.line(i, peer_value(ps, d, i), e.load(i));
   }
   __shared__ double red[32];
   const double s1 = block_sum(e.dx2, red);
@@ -662,7 +700,7 @@ extern "C" int pdlpk_arm(pdlpk_step_state* st, int64_t k_target, cudaStream_t s)
 }
 
 extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
-  primal_pass<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a);
+  primal_pass<false><<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, pdlpk_peer_sum{});
   if (a->mode == 0) {
     // Degenerate shapes (an empty side) still need the decision, which the
     // column pass performs: it always has >= 1 CTA (short_blocks >= 1).
@@ -686,7 +724,7 @@ extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
 
 extern "C" int pdlpk_attempt_timed(const pdlpk_step_args* a, cudaEvent_t* ev, cudaStream_t s) {
   cudaEventRecord(ev[0], s);
-  primal_pass<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a);
+  primal_pass<false><<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, pdlpk_peer_sum{});
   cudaEventRecord(ev[1], s);
   if (a->mode == 0) {
     dispatch_p(a->P.K, LaunchRowCol{a, s, true});
@@ -723,7 +761,13 @@ extern "C" int64_t pdlpk_dist_ew_grid(int64_t n) { return ew_blocks(n); }
 extern "C" int64_t pdlpk_dist_sched_grid(const pdlpk_csr* A) { return sched_blocks(*A); }
 
 extern "C" int pdlpk_dist_primal(const pdlpk_step_args* a, cudaStream_t s) {
-  primal_pass<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a);
+  primal_pass<false><<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, pdlpk_peer_sum{});
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_dist_primal_push(const pdlpk_step_args* a, const pdlpk_peer_sum* dst,
+                                      cudaStream_t s) {
+  primal_pass<true><<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, *dst);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -733,7 +777,29 @@ extern "C" int pdlpk_dist_row_fused(const pdlpk_step_args* a, cudaStream_t s) {
 }
 
 extern "C" int pdlpk_dist_row_epi(const pdlpk_step_args* a, const double* acc, cudaStream_t s) {
-  row_epi_kernel<<<ew_blocks(a->P.m), kEwThreads, 0, s>>>(*a, acc);
+  pdlpk_peer_sum none{};
+  row_epi_kernel<<<ew_blocks(a->P.m), kEwThreads, 0, s>>>(*a, acc, none);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_dist_row_epi_peers(const pdlpk_step_args* a, const pdlpk_peer_sum* ps,
+                                        cudaStream_t s) {
+  row_epi_kernel<<<ew_blocks(a->P.m), kEwThreads, 0, s>>>(*a, nullptr, *ps);
+  return static_cast<int>(cudaGetLastError());
+}
+
+__global__ void __launch_bounds__(kEwThreads) peer_reduce_kernel(double* out, pdlpk_peer_sum ps,
+                                                                int64_t count) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    out[i] = peer_value(ps, nullptr, i);
+  }
+}
+
+extern "C" int pdlpk_peer_reduce(double* out, const pdlpk_peer_sum* ps, int64_t count,
+                                 cudaStream_t s) {
+  if (count <= 0) return 0;
+  peer_reduce_kernel<<<ew_blocks(count), kEwThreads, 0, s>>>(out, *ps, count);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -743,7 +809,14 @@ extern "C" int pdlpk_dist_col_fused(const pdlpk_step_args* a, cudaStream_t s) {
 }
 
 extern "C" int pdlpk_dist_col_epi(const pdlpk_step_args* a, const double* d, cudaStream_t s) {
-  col_epi_kernel<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, d);
+  pdlpk_peer_sum none{};
+  col_epi_kernel<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, d, none);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_dist_col_epi_peers(const pdlpk_step_args* a, const pdlpk_peer_sum* ps,
+                                        cudaStream_t s) {
+  col_epi_kernel<<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, nullptr, *ps);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -187,6 +187,22 @@ int64_t pdlpk_dist_ew_grid(int64_t n);
 int64_t pdlpk_dist_sched_grid(const pdlpk_csr* A);
 int pdlpk_dist_primal(const pdlpk_step_args* a, cudaStream_t s);
 int pdlpk_dist_row_fused(const pdlpk_step_args* a, cudaStream_t s);
+// Reduce-scatter folded into the epilogue: the line sums are read straight
+// from every rank's partial product over NVLink P2P (rank order, so the sum
+// is deterministic); world == 0 means `acc` already holds them.
+#define PDLPK_MAX_PEERS 8
+typedef struct {
+  const double* p[PDLPK_MAX_PEERS];
+  int32_t world;
+  int64_t offset;  // this rank's block within each partial product
+} pdlpk_peer_sum;
+int pdlpk_dist_row_epi_peers(const pdlpk_step_args* a, const pdlpk_peer_sum* ps, cudaStream_t s);
+int pdlpk_dist_col_epi_peers(const pdlpk_step_args* a, const pdlpk_peer_sum* ps, cudaStream_t s);
+// primal pass that also stores x-bar into every peer's gathered vector
+// (dst.p[r] + dst.offset; null entries are skipped): all-gather folded in.
+int pdlpk_dist_primal_push(const pdlpk_step_args* a, const pdlpk_peer_sum* dst, cudaStream_t s);
+// out[i] = sum over ranks (rank order) of p[r][offset + i], i < count.
+int pdlpk_peer_reduce(double* out, const pdlpk_peer_sum* ps, int64_t count, cudaStream_t s);
 int pdlpk_dist_row_epi(const pdlpk_step_args* a, const double* acc, cudaStream_t s);
 int pdlpk_dist_col_fused(const pdlpk_step_args* a, cudaStream_t s);
 int pdlpk_dist_col_epi(const pdlpk_step_args* a, const double* d, cudaStream_t s);

@@ -611,6 +611,38 @@ class Engine {
       pbuf_.alloc(full_cols());
       dev_zero(gbuf_.get(), full_cols(), s());
       dev_zero(pbuf_.get(), full_cols(), s());
+      const char* pe = std::getenv("PDLP_PEER_RS");
+      const int w = comm_->world();
+      if (w > 1 && w <= PDLPK_MAX_PEERS && !(pe != nullptr && pe[0] == '0')) {
+        peer_pbuf_ = comm_->alloc_peer_buffer(static_cast<size_t>(full_cols()));
+        peer_gather_ = comm_->alloc_peer_buffer(static_cast<size_t>(full_cols()));
+        dev_zero(peer_pbuf_, full_cols(), s());
+        dev_zero(peer_gather_, full_cols(), s());
+        const std::vector<double*> ptrs = comm_->peer_pointers(peer_pbuf_, s());
+        const std::vector<double*> gptrs = comm_->peer_pointers(peer_gather_, s());
+        // every rank must take the same path: fall back together if any
+        // rank could not map its peers
+        if (any_rank(ptrs.empty() || gptrs.empty())) {
+          PDLP_CK(cudaStreamSynchronize(s()));
+          comm_->free_peer_buffer(peer_pbuf_);
+          comm_->free_peer_buffer(peer_gather_);
+          peer_pbuf_ = peer_gather_ = nullptr;
+          if (opt_.logging && comm_->rank() == 0) {
+            std::fprintf(stderr, "phase=setup event=peer_exchange_unavailable fallback=nccl\n");
+          }
+        } else {
+          const int rank = comm_->rank();
+          peers_.world = push_.world = w;
+          peers_.offset = push_.offset = plan_.col_block * rank;
+          for (int r = 0; r < w; ++r) {
+            peers_.p[r] = ptrs[r];
+            push_.p[r] = r == rank ? nullptr : gptrs[r];
+          }
+          if (opt_.logging && rank == 0) {
+            std::fprintf(stderr, "phase=setup event=peer_exchange world=%d\n", w);
+          }
+        }
+      }
       slots_all_.alloc(static_cast<size_t>(kSlots) * comm_->world());
       PDLP_CK(cudaStreamSynchronize(s()));
     }
@@ -713,6 +745,11 @@ class Engine {
 
   ~Engine() {
     if (comm_ != nullptr) pdlpk_set_red_log(nullptr);
+    if (peer_pbuf_ != nullptr) {
+      cudaStreamSynchronize(s());
+      comm_->free_peer_buffer(peer_pbuf_);
+      comm_->free_peer_buffer(peer_gather_);
+    }
     alloc_scope_.reset();  // members free on their own allocation stream
     for (cudaEvent_t e : prof_ev_) cudaEventDestroy(e);
   }
@@ -808,11 +845,31 @@ class Engine {
     if (L.dist_kind == PDLPK_DIST_GATHER) {
       gather(in, nloc, nb, gbuf_.get());
       PDLP_LAUNCH(pdlpk_spmv(&L, orig, gbuf_.get(), out, 0, s()));
+    } else if (peer_pbuf_ != nullptr) {
+      peer_fence();
+      PDLP_LAUNCH(pdlpk_spmv(&L, orig, in, peer_pbuf_, 0, s()));
+      comm_->barrier(s());
+      PDLP_LAUNCH(pdlpk_peer_reduce(out, &peers_, nloc, s()));
+      peer_pending_ = true;
     } else {
       PDLP_LAUNCH(pdlpk_spmv(&L, orig, in, pbuf_.get(), 0, s()));
       comm_->reduce_scatter(pbuf_.get(), gbuf_.get(), static_cast<size_t>(nb), s());
       dev_copy(out, gbuf_.get(), nloc, s());
     }
+  }
+
+  // Before this rank overwrites its peer buffer: every peer has finished
+  // reading it (a barrier unless a collective has intervened since).
+  void peer_fence() {
+    if (peer_pending_) {
+      comm_->barrier(s());
+      peer_pending_ = false;
+    }
+  }
+
+  // Peers' last reads of this rank's buffer are done before it is freed.
+  void peer_finish() {
+    if (peer_pbuf_ != nullptr) peer_fence();
   }
 
   // Combines the reductions logged since the last read across ranks (one
@@ -853,20 +910,40 @@ class Engine {
     const int64_t nb = plan_.col_block;
     const bool kg = P.K.dist_kind == PDLPK_DIST_GATHER;
     const bool ktg = P.KT.dist_kind == PDLPK_DIST_GATHER;
-    double* xfull = D.xbar.get();
+    // x-bar is only read inside an attempt, so one peer-mappable gathered
+    // vector serves every subproblem.  Reuse needs no fence: each attempt
+    // ends with the totals all-gather, which completes only after every
+    // rank's row pass (the last reader) of that attempt.
+    const bool push = kg && peer_gather_ != nullptr;
+    double* xfull = push ? peer_gather_ : D.xbar.get();
     double* dyfull = D.dy.get();
     pdlpk_step_args b = a;
     b.xbar = kg ? xfull + nb * rank : xfull;
-    PDLP_LAUNCH(pdlpk_dist_primal(&b, s()));
+    if (push) {
+      PDLP_LAUNCH(pdlpk_dist_primal_push(&b, &push_, s()));
+    } else {
+      PDLP_LAUNCH(pdlpk_dist_primal(&b, s()));
+    }
     b.xbar = xfull;
     b.dy = ktg ? dyfull + nb * rank : dyfull;
     int64_t g2 = 0, g3 = 0;
     int k_acc = 0, kt_acc = 0;
     if (kg) {
-      comm_->allgather(xfull, static_cast<size_t>(nb), s());
+      if (push) {
+        comm_->barrier(s());  // every peer's x-bar block has landed
+      } else {
+        comm_->allgather(xfull, static_cast<size_t>(nb), s());
+      }
       PDLP_LAUNCH(pdlpk_dist_row_fused(&b, s()));
       g2 = pdlpk_dist_sched_grid(&P.K);
       k_acc = 1;
+    } else if (peer_pbuf_ != nullptr) {
+      peer_fence();
+      PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, xfull, peer_pbuf_, 0, s()));
+      comm_->barrier(s());
+      PDLP_LAUNCH(pdlpk_dist_row_epi_peers(&b, &peers_, s()));
+      peer_pending_ = true;
+      g2 = pdlpk_dist_ew_grid(P.m);
     } else {
       PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, xfull, D.pbuf.get(), 0, s()));
       comm_->reduce_scatter(D.pbuf.get(), D.dloc.get(), static_cast<size_t>(nb), s());
@@ -879,6 +956,13 @@ class Engine {
       PDLP_LAUNCH(pdlpk_dist_col_fused(&b, s()));
       g3 = pdlpk_dist_sched_grid(&P.KT);
       kt_acc = 1;
+    } else if (peer_pbuf_ != nullptr) {
+      peer_fence();
+      PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, b.dy, peer_pbuf_, 0, s()));
+      comm_->barrier(s());
+      PDLP_LAUNCH(pdlpk_dist_col_epi_peers(&b, &peers_, s()));
+      peer_pending_ = true;
+      g3 = pdlpk_dist_ew_grid(P.n);
     } else {
       PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, b.dy, D.pbuf.get(), 0, s()));
       comm_->reduce_scatter(D.pbuf.get(), D.dloc.get(), static_cast<size_t>(nb), s());
@@ -888,6 +972,7 @@ class Engine {
     double* tot = D.tot_all.get();
     PDLP_LAUNCH(pdlpk_dist_totals(&b, g2, g3, k_acc, kt_acc, tot + 8 * rank, s()));
     comm_->allgather(tot, 8, s());
+    peer_pending_ = false;  // the all-gather ordered every peer's reads
     PDLP_LAUNCH(pdlpk_dist_decide(&b, tot, comm_->world(), s()));
   }
 
@@ -1506,6 +1591,18 @@ class Engine {
   int64_t m_glob_ = 0, n_glob_ = 0;
   pdlpk_red_log red_log_{};
   DevBuf<double> gbuf_, pbuf_, slots_all_, flag_;
+  // Reduce-scatter folded into the consumer (PDLP_PEER_RS=0 restores the
+  // NCCL reduce-scatter): every rank writes its partial product into a
+  // peer-mappable buffer; after a stream-level barrier each owner reads its
+  // block from all ranks over NVLink inside the epilogue kernel.
+  double* peer_pbuf_ = nullptr;
+  pdlpk_peer_sum peers_{};
+  // all-gather folded into the primal pass: peers store their x-bar blocks
+  // straight into this rank's gathered vector
+  double* peer_gather_ = nullptr;
+  pdlpk_peer_sum push_{};
+  bool peer_pending_ = false;  // a peer-read kernel may still be reading
+
   DevBuf<double> fc_c_, fc_lv_, fc_uv_, fc_zero_, fr_lc_, fr_uc_, fr_zero_;
   DevBuf<double> fs_lc_, fs_uc_, fs_lv_, fs_uv_;
   DevBuf<double> gq_[2][4];
@@ -1951,6 +2048,7 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result*
   res->precondition_seconds = E.precondition_seconds_;
   res->loop_seconds = loop_seconds;
   res->step_seconds = E.step_seconds_;
+  E.peer_finish();
   res->solve_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
   std::snprintf(res->termination_detail, sizeof(res->termination_detail), "%s", D.detail.c_str());
   if (o->logging) {

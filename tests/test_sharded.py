@@ -265,3 +265,26 @@ def test_nccl_world1_matches_emulated(gpu):
     assert a.iterations == b.iterations == 300
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_peer_read_epilogue_matches_reduce_scatter(gpu, monkeypatch, world):
+    """The reduce-scatter folded into the epilogue (owners read every rank's
+    partial product over P2P and sum in rank order) gives the same bits as
+    the collective path it replaces, over whole solves: attempts, cadence
+    products, both polishing subproblems and the final verification."""
+    cases = [(P.generate("c0", 3), {}), (P.generate("c1", 3, sources=45, sinks=55), {}),
+             (P.generate("c0", 4), {"enable_polish": False, "iteration_limit": 700})]
+    for p, kw in cases:
+        tol = P.relative_tolerances(p, 1e-4)
+        o = _opts(tolerances=P.TerminationTolerances(*tol), **kw)
+        monkeypatch.setenv("PDLP_PEER_RS", "0")
+        a = S.solve_sharded_emulated(p, o, world)
+        monkeypatch.delenv("PDLP_PEER_RS")
+        b = S.solve_sharded_emulated(p, o, world)
+        assert a.status == b.status
+        assert (a.iterations, a.polish_iterations, a.restarts) == \
+            (b.iterations, b.polish_iterations, b.restarts)
+        np.testing.assert_array_equal(a.x, b.x)
+        np.testing.assert_array_equal(a.y, b.y)
