@@ -1928,9 +1928,13 @@ void copy_to_host(double* dst, const double* src, int64_t n, cudaStream_t s) {
 int64_t inner_bytes(int64_t n, int64_t m) { return 8 * (24 * n + 17 * m) + 64 * 41; }
 
 // comm != nullptr: this process/thread is one rank of a row-sharded solve.
-void solve(const pdlp_problem_view* problem, const pdlp_options* o, pdlp_result* res,
+void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_result* res,
            Comm* comm = nullptr) {
   const auto t0 = Clock::now();
+  // sharded: one log (rank 0); every rank computes the same trajectory
+  pdlp_options local = *opts;
+  if (comm != nullptr && comm->rank() != 0) local.logging = 0;
+  const pdlp_options* o = &local;
   g_alloc_seconds = 0.0;
   Engine E(problem, *o, comm);  // uploads and validates on device
   if (o->enable_scaling) E.precondition(o->ruiz_passes, o->pock_chambolle != 0);
