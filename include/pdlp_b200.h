@@ -229,6 +229,23 @@ int pdlp_check_certificate(const pdlp_problem_view* problem, int32_t kind, const
                            double eps_ray, int32_t* verified, double* residual,
                            double* objective);
 
+/* ---------------------------------------------- feasibility harness --- *
+ * The reference's Appendix-B fixed-restart feasibility iteration
+ * (proj/tests/feasibility_method.hpp:40-85, testharness::
+ * fixed_restart_feasibility; acceptance criterion 10) on the device: find
+ * x >= 0 with A x = b by primal-dual steps of fixed size eta; each round runs
+ * restart_length steps from the last restart point with y = 0, averages the
+ * primal iterates and adopts the average.  Only A (both layouts) of `a` is
+ * read.  restart_points ((rounds+1) * cols, may be NULL) and residuals
+ * (rounds+1, ||A x - b||_2) receive x0 and every finite restart point;
+ * *recorded = how many; *finite = 0 if a round produced a non-finite point
+ * (the run stops there, like FeasibilityRun::finite).  PARITY mode
+ * reproduces the reference bit for bit. */
+int pdlp_feasibility_run(const pdlp_problem_view* a, const double* b, const double* x0,
+                         double eta, int64_t restart_length, int32_t rounds, int32_t mode,
+                         int32_t device, double* restart_points, double* residuals,
+                         int32_t* recorded, int32_t* finite);
+
 /* ------------------------------------------------------------- MPS --- *
  * Free-format MPS reader / writer with the reference's behaviour
  * (proj/include/pdhglp/mps.hpp:87-535: parse_mps, read_mps_file, write_mps).

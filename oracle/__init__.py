@@ -47,6 +47,8 @@ _SIGS = {
     "ref_initialize_primal_weight": (C.c_double, [P]),
     "ref_initial_step_size": (C.c_double, [P]),
     "ref_validate": (C.c_int, [P, C.c_char_p, C.c_int32]),
+    "ref_feasibility_run": (C.c_int, [P, D, D, C.c_double, C.c_int64, C.c_int32, D, D,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
 }
 _REF_ONLY = {
     "ref_generate": (C.c_void_p, [C.c_int32, C.c_int64, C.c_int64, C.c_double, C.c_uint64]),
@@ -55,6 +57,7 @@ _REF_ONLY = {
     "ref_instance_view": (None, [C.c_void_p, P]),
     "ref_instance_optimal_objective": (C.c_double, [C.c_void_p]),
     "ref_instance_free": (None, [C.c_void_p]),
+    "ref_instance_feasible_point": (None, [C.c_void_p, D]),
     "ref_mps_parse": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "ref_mps_view": (None, [C.c_void_p, P]),
     "ref_mps_maximize": (C.c_int32, [C.c_void_p]),
@@ -207,6 +210,31 @@ class Oracle:
         buf = C.create_string_buffer(256)
         bad = self.lib.ref_validate(C.byref(p.view()), buf, 256)
         return buf.value.decode() if bad else None
+
+    # Appendix-B harness (tests/feasibility_method.hpp:60-85)
+    def feasibility_run(self, p, b, x0, eta: float, restart_length: int, rounds: int):
+        """(restart points [k, n], residuals [k], finite) like FeasibilityRun."""
+        n = p.cols()
+        pts = np.zeros((rounds + 1, n))
+        res = np.zeros(rounds + 1)
+        rec, fin = C.c_int32(0), C.c_int32(0)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        self._check(self.lib.ref_feasibility_run(C.byref(p.view()), _pd(b), _pd(x0), eta,
+                                                 restart_length, rounds, _pd(pts), _pd(res),
+                                                 C.byref(rec), C.byref(fin)))
+        return pts[:rec.value].copy(), res[:rec.value].copy(), bool(fin.value)
+
+    def generate_feasibility_system(self, rows: int, cols: int, density: float, seed: int):
+        """The reference's FeasibilitySystem instance and its positive point."""
+        h = self.lib.ref_generate(KIND["feasibility-system"], rows, cols, density, seed)
+        if not h:
+            raise ValueError(self.lib.ref_last_error().decode())
+        inst = _RefInstance(self, h)
+        p = inst.problem()
+        pt = np.zeros(p.cols())
+        self.lib.ref_instance_feasible_point(h, _pd(pt))
+        return p, pt
 
     # reference generator (generator.hpp:347-374), reference oracle only
     def generate(self, kind: str, rows: int, cols: int, density: float, seed: int):

@@ -1146,6 +1146,57 @@ double ref_initialize_primal_weight(const pdlp_problem_view* pv) { return weight
 
 double ref_initial_step_size(const pdlp_problem_view* pv) { return eta0(from_view(pv)); }
 
+// Appendix-B fixed-restart feasibility harness, restated from the
+// reference's test harness (proj/tests/feasibility_method.hpp:40-85):
+// residual ||A x - b||_2 in row order (:26-34); one step = A^T y by columns,
+// x' = max(0, x - eta A^T y), mid = 2x' - x, y -= eta (b - A mid) (:42-57);
+// a round averages its restart_length primal iterates (:62-81).
+int ref_feasibility_run(const pdlp_problem_view* pv, const double* b, const double* x0,
+                        double eta, int64_t restart_length, int32_t rounds, double* points,
+                        double* residuals, int32_t* recorded, int32_t* finite) {
+  return guarded([&] {
+    const Lp p = from_view(pv);
+    const size_t m = static_cast<size_t>(p.m), n = static_cast<size_t>(p.n);
+    const Vec rhs(b, b + m);
+    Vec start(x0, x0 + n), x, y, sum, aty, mid, ax;
+    auto residual = [&](const Vec& pt) {
+      line_products(p.rows, pt, ax);
+      double acc = 0.0;
+      for (size_t j = 0; j < m; ++j) acc += (ax[j] - rhs[j]) * (ax[j] - rhs[j]);
+      return std::sqrt(acc);
+    };
+    auto keep = [&](int32_t k) {
+      if (points != nullptr) std::copy(start.begin(), start.end(), points + k * static_cast<int64_t>(n));
+      residuals[k] = residual(start);
+    };
+    keep(0);
+    int32_t count = 1, ok = 1;
+    for (int32_t r = 0; r < rounds && ok; ++r) {
+      x = start;
+      y.assign(m, 0.0);
+      sum.assign(n, 0.0);
+      mid.assign(n, 0.0);
+      for (int64_t t = 0; t < restart_length; ++t) {
+        line_products(p.cols, y, aty);
+        for (size_t i = 0; i < n; ++i) {
+          const double cand = x[i] - eta * aty[i];
+          const double nx = 0.0 < cand ? cand : 0.0;
+          mid[i] = 2.0 * nx - x[i];
+          x[i] = nx;
+        }
+        line_products(p.rows, mid, ax);
+        for (size_t j = 0; j < m; ++j) y[j] = y[j] - eta * (rhs[j] - ax[j]);
+        for (size_t i = 0; i < n; ++i) sum[i] += x[i];
+      }
+      for (size_t i = 0; i < n; ++i) start[i] = sum[i] / static_cast<double>(restart_length);
+      for (double v : start) ok &= std::isfinite(v) ? 1 : 0;
+      if (ok) keep(count++);
+    }
+    *recorded = count;
+    *finite = ok;
+  });
+}
+
 int ref_validate(const pdlp_problem_view* pv, char* msg, int32_t len) {
   try {
     validate(from_view(pv));

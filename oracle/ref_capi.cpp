@@ -22,6 +22,7 @@
 #include <exception>
 #include <string>
 
+#include "feasibility_method.hpp"  // proj/tests: the Appendix-B harness
 #include "pdlp_b200.h"
 
 using namespace pdhglp;
@@ -383,6 +384,36 @@ double ref_initialize_primal_weight(const pdlp_problem_view* pv) {
 
 double ref_initial_step_size(const pdlp_problem_view* pv) {
   return initial_step_size(to_problem(pv));
+}
+
+// ---- Appendix-B harness (tests/feasibility_method.hpp:60-85), as is -------
+
+int ref_feasibility_run(const pdlp_problem_view* pv, const double* b, const double* x0,
+                        double eta, int64_t restart_length, int32_t rounds, double* points,
+                        double* residuals, int32_t* recorded, int32_t* finite) {
+  return guarded([&]() -> int {
+    const LpProblem p = to_problem(pv);
+    const Vector rhs(b, b + pv->rows), start(x0, x0 + pv->cols);
+    const testharness::FeasibilityRun run =
+        testharness::fixed_restart_feasibility(p.a, rhs, start, eta, restart_length, rounds);
+    for (size_t k = 0; k < run.restart_points.size(); ++k) {
+      if (points != nullptr) copy_out(run.restart_points[k], points + k * pv->cols);
+      residuals[k] = run.residuals[k];
+    }
+    *recorded = static_cast<int32_t>(run.restart_points.size());
+    *finite = run.finite ? 1 : 0;
+    return PDLP_OK;
+  });
+}
+
+// Strictly positive point of a feasibility-system instance (A x = b), for
+// the criterion-10 starts; NaN-filled when the instance kind has none.
+void ref_instance_feasible_point(void* h, double* out) {
+  const auto& inst = static_cast<RefInstance*>(h)->inst;
+  const size_t n = static_cast<size_t>(inst.problem.cols());
+  for (size_t i = 0; i < n; ++i) {
+    out[i] = i < inst.feasible_point.size() ? inst.feasible_point[i] : std::nan("");
+  }
 }
 
 // ---- instances from the reference generator (generator.hpp:347-374) ------

@@ -13,8 +13,10 @@ from .solver import (CertificateKind, InfeasibilityCertificate, IterationRecord,
                      spmv, spmv_transpose, step_size_rules)
 
 from .mps import MpsModel, parse_mps, read_mps, write_mps, write_mps_file
+from .feasibility import FeasibilityRun, feasibility_residual, fixed_restart_feasibility
 
 __all__ = [
+    "FeasibilityRun", "feasibility_residual", "fixed_restart_feasibility",
     "MpsModel", "parse_mps", "read_mps", "write_mps", "write_mps_file",
     "CompressedLayout", "LpProblem", "SparseMatrix", "generate", "generate_with_point", "problem",
     "relative_tolerances", "CertificateKind", "InfeasibilityCertificate", "IterationRecord",

@@ -218,6 +218,9 @@ SOLVER_SIGNATURES = {
     "pdlp_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "pdlp_check_certificate": (C.c_int, [C.POINTER(ProblemView), C.c_int32, c_double_p, C.c_double,
                                          C.POINTER(C.c_int32), c_double_p, c_double_p]),
+    "pdlp_feasibility_run": (C.c_int, [C.POINTER(ProblemView), c_double_p, c_double_p, C.c_double,
+                                       C.c_int64, C.c_int32, C.c_int32, C.c_int32, c_double_p,
+                                       c_double_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "pdlp_mps_parse": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "pdlp_mps_read_file": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
     "pdlp_mps_view": (None, [C.c_void_p, C.POINTER(ProblemView)]),

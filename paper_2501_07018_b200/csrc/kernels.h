@@ -267,6 +267,16 @@ int pdlpk_attempt_timed(const pdlpk_step_args* a, cudaEvent_t* ev, cudaStream_t 
 /* Apply a pending deferred average add (AverageState::add, step.hpp:209-216). */
 int pdlpk_flush_average(const pdlpk_step_args* a, cudaStream_t s);
 
+/* ------------------------------------- feasibility harness (k_feas.cu) --- */
+/* Appendix-B fixed-restart feasibility iteration
+ * (tests/feasibility_method.hpp:40-85), per-entry parts. */
+int pdlpk_feas_primal(double* x, const double* aty, double* scratch, double* x_sum, double eta,
+                      int64_t n, cudaStream_t s);
+int pdlpk_feas_dual(double* y, const double* b, const double* ax_mid, double eta, int64_t m,
+                    cudaStream_t s);
+int pdlpk_feas_average(double* x_start, double* x, double* x_sum, double len, int64_t n,
+                       int32_t* finite, cudaStream_t s);
+
 /* ------------------------------------------------------------- cadence --- */
 /* out = A v with the given layout; orig != 0 uses the original values.
  * cond (device scalar, may be NULL): the product is skipped when *cond == 0. */

@@ -2512,6 +2512,110 @@ int pdlp_check_certificate(const pdlp_problem_view* problem, int32_t kind, const
   });
 }
 
+int pdlp_feasibility_run(const pdlp_problem_view* a, const double* b, const double* x0,
+                         double eta, int64_t restart_length, int32_t rounds, int32_t mode,
+                         int32_t device, double* restart_points, double* residuals,
+                         int32_t* recorded, int32_t* finite) {
+  if (a == nullptr || b == nullptr || x0 == nullptr || residuals == nullptr ||
+      recorded == nullptr || finite == nullptr || restart_length < 1 || rounds < 0 ||
+      (mode != PDLP_MODE_PERF && mode != PDLP_MODE_PARITY)) {
+    g_last_error = "invalid feasibility run";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&] {
+    const int64_t m = a->rows, n = a->cols;
+    // The harness reads only A and b: an LP view around them (c = 0,
+    // A x = b, x >= 0) lets the engine upload, validate and schedule A.
+    std::vector<double> zero(static_cast<size_t>(std::max<int64_t>(n, 1)), 0.0);
+    std::vector<double> inf(static_cast<size_t>(std::max<int64_t>(n, 1)), kInf);
+    pdlp_problem_view v = *a;
+    v.objective = zero.data();
+    v.var_lower = zero.data();
+    v.var_upper = inf.data();
+    v.con_lower = b;
+    v.con_upper = b;
+    pdlp_options o;
+    pdlp_default_options(&o);
+    o.mode = mode;
+    o.device = device;
+    o.threads = 1;
+    o.shards_per_thread = 1;  // one shard: the residual sums run in row order
+    Engine E(&v, o);
+    const DevProblem& Q = E.problem();
+    const cudaStream_t s = E.s();
+    const int parity = mode == PDLP_MODE_PARITY ? 1 : 0;
+    DevBuf<double> x = to_dev(x0, n, s), xs = to_dev(x0, n, s), db = to_dev(b, m, s);
+    DevBuf<double> xsum(n), y(m), aty(n), scr(n), axm(m), ax(m);
+    DevBuf<int32_t> flag(1);
+    dev_zero(xsum.get(), n, s);
+    const int32_t one = 1;
+    PDLP_CK(cudaMemcpyAsync(flag.get(), &one, sizeof(one), cudaMemcpyHostToDevice, s));
+    const pdlpk_red red = E.red();
+    // feasibility_residual (feasibility_method.hpp:26-34): ||A x - b||_2
+    auto residual = [&](const double* pt) {
+      PDLP_LAUNCH(pdlpk_spmv(&Q.row.view, 0, pt, ax.get(), parity, s));
+      PDLP_LAUNCH(pdlpk_diff_norm_sq(ax.get(), db.get(), m, &red, E.slot(0), s));
+      return std::sqrt(E.read_slots(1)[0]);
+    };
+    // One feasibility_step (:42-57): aty = A^T y; primal half; A scratch;
+    // dual half.  Rounds replay captured graphs of up to 64 steps.
+    auto enqueue_steps = [&](int64_t steps) {
+      for (int64_t t = 0; t < steps; ++t) {
+        PDLP_LAUNCH(pdlpk_spmv(&Q.col.view, 0, y.get(), aty.get(), parity, s));
+        PDLP_LAUNCH(pdlpk_feas_primal(x.get(), aty.get(), scr.get(), xsum.get(), eta, n, s));
+        PDLP_LAUNCH(pdlpk_spmv(&Q.row.view, 0, scr.get(), axm.get(), parity, s));
+        PDLP_LAUNCH(pdlpk_feas_dual(y.get(), db.get(), axm.get(), eta, m, s));
+      }
+    };
+    struct Graph {
+      cudaGraphExec_t exec = nullptr;
+      ~Graph() {
+        if (exec != nullptr) cudaGraphExecDestroy(exec);
+      }
+    };
+    auto capture = [&](int64_t steps, Graph& g) {
+      if (steps == 0) return;
+      cudaGraph_t graph = nullptr;
+      PDLP_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      enqueue_steps(steps);
+      PDLP_CK(cudaStreamEndCapture(s, &graph));
+      const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      PDLP_CK(e);
+    };
+    const int64_t chunk = std::min<int64_t>(restart_length, 64);
+    const int64_t reps = restart_length / chunk, rest = restart_length % chunk;
+    Graph body, tail;
+    capture(chunk, body);
+    capture(rest, tail);
+
+    auto record = [&](int32_t k) {
+      if (restart_points != nullptr && n > 0) {
+        PDLP_CK(cudaMemcpyAsync(restart_points + static_cast<int64_t>(k) * n, xs.get(), n * 8,
+                                cudaMemcpyDeviceToHost, s));
+      }
+      residuals[k] = residual(xs.get());
+    };
+    record(0);
+    int32_t rec = 1, ok = 1;
+    for (int32_t r = 0; r < rounds; ++r) {
+      dev_zero(y.get(), m, s);  // y reset (:67)
+      for (int64_t q = 0; q < reps; ++q) PDLP_CK(cudaGraphLaunch(body.exec, s));
+      if (rest > 0) PDLP_CK(cudaGraphLaunch(tail.exec, s));
+      PDLP_LAUNCH(pdlpk_feas_average(xs.get(), x.get(), xsum.get(),
+                                     static_cast<double>(restart_length), n, flag.get(), s));
+      PDLP_CK(cudaMemcpyAsync(&ok, flag.get(), sizeof(ok), cudaMemcpyDeviceToHost, s));
+      PDLP_CK(cudaStreamSynchronize(s));
+      if (!ok) break;
+      record(rec);
+      ++rec;
+    }
+    PDLP_CK(cudaStreamSynchronize(s));
+    *recorded = rec;
+    *finite = ok;
+  });
+}
+
 int pdlp_step_size_rules(double movement, double curvature, double eta_bar, double eta,
                          int64_t k, double* limit_out, double* next_out) {
   // Scalar rules (step.hpp:126-141), evaluated with the host table values the
