@@ -126,6 +126,23 @@ __device__ __forceinline__ double block_max(double v, double* smem) {
 
 // Streaming loads for data touched once per pass (matrix entries): evict
 // first so the gathered dense operand keeps its L2 residency.
+// L2 eviction priority for a vector that a later kernel gathers from (x-bar
+// for the row pass): stores carry an evict_last policy on `frac` of the
+// lines, so the streams around them (evict_first / .cs) go first.
+__device__ __forceinline__ uint64_t l2_keep_policy(float frac) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+  return pol;
+}
+__device__ __forceinline__ void st_keep(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
 __device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs(p); }

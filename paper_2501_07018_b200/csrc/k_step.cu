@@ -70,6 +70,13 @@ __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a, pdl
   // 128-bit accesses (every vector is a separate cudaMalloc, so 16B aligned);
   // c, l_v, u_v are read once per pass: streaming loads.
   const int64_t n2 = n >> 1;
+#if PDLPK_XBAR_KEEP
+  // keep x-bar (<= kXbarKeepBytes of it) in L2 for the row pass's gathers;
+  // x' and the running sum are streamed out
+  const float keep = fminf(1.0f, static_cast<float>(PDLPK_XBAR_KEEP_MB * 1048576.0 /
+                                                    (8.0 * static_cast<double>(n > 0 ? n : 1))));
+  const uint64_t pol = l2_keep_policy(keep);
+#endif
   const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x);
   const double2* __restrict__ a2 = reinterpret_cast<const double2*>(aty);
   const double2* __restrict__ c2 = reinterpret_cast<const double2*>(c);
@@ -86,8 +93,13 @@ __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a, pdl
     xp.y = clampd(xi.y - tau * (ci.y - ai.y), li.y, ui.y);
     xb.x = 2.0 * xp.x - xi.x;
     xb.y = 2.0 * xp.y - xi.y;
+#if PDLPK_XBAR_KEEP
+    __stcs(xn2 + p, xp);
+    st_keep(xb2 + p, xb, pol);
+#else
     xn2[p] = xp;
     xb2[p] = xb;
+#endif
     if constexpr (Push) {
 #pragma unroll
       for (int r = 0; r < PDLPK_MAX_PEERS; ++r) {

@@ -90,6 +90,12 @@ typedef struct pdlpk_csr {
 #ifndef PDLPK_TILE_ROWS
 #define PDLPK_TILE_ROWS 448 /* most lines per staged tile (7 consumer warps x 32 x 2 lines/lane) */
 #endif
+#ifndef PDLPK_XBAR_KEEP
+#define PDLPK_XBAR_KEEP 1
+#endif
+#ifndef PDLPK_XBAR_KEEP_MB
+#define PDLPK_XBAR_KEEP_MB 48
+#endif
 #ifndef PDLPK_TILE_STAGES
 #define PDLPK_TILE_STAGES 2 /* staged tiles in flight per CTA */
 #endif
