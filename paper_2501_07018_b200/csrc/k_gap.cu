@@ -52,8 +52,16 @@ struct GapScalars {
   double value;
   unsigned long long first;  // first crossing group index (perf)
   int num_events;            // compacted event count (select output)
-  int num_high;              // partial sort: events at or above the threshold
-  unsigned long long thresh; // partial sort: threshold key
+  int num_high;              // window sort: events inside the window
+  unsigned long long thresh; // (unused)
+  // Sweep start: masses before the first sorted event (c, b) and the lambda
+  // of the group before it (hi0).  Full sort: the lambda -> inf masses and
+  // inf; window sort: plus every event above the window.
+  double base[3];
+  unsigned long long lo_key, hi_key;  // window [lo_key, hi_key]
+  unsigned long long above_min;       // smallest key above the window
+  unsigned long long above_count;     // events above the window
+  double above[2];                    // their masses (c, b), tree order
 };
 
 struct Work {
@@ -323,14 +331,63 @@ __global__ void high_flags_kernel(Work w, int64_t E) {
 // the engine sizes the next partial sort from it.
 __global__ void hit_fraction_kernel(Work w, int64_t E, double* out) {
   const unsigned long long f = w.sc->first;
-  *out = (f == ~0ull || E <= 0) ? 1.0 : static_cast<double>(f) / static_cast<double>(E);
+  *out = (f == ~0ull || E <= 0)
+             ? 1.0
+             : static_cast<double>(f + w.sc->above_count) / static_cast<double>(E);
+}
+
+__global__ void base_full_kernel(Work w) {
+  w.sc->base[0] = w.sc->sums[1];
+  w.sc->base[1] = w.sc->sums[0];
+  w.sc->base[2] = CUDART_INF;
+  w.sc->above_count = 0;
+}
+
+// Window [lo_key, hi_key] between sample ranks ra (0: no events above) and rb.
+__global__ void window_keys_kernel(Work w, int ra, int rb) {
+  w.sc->hi_key = ra > 0 ? w.samp_out[ra] : ~0ull;
+  w.sc->lo_key = rb >= 0 ? w.samp_out[rb] : 0ull;  // rb < 0: down to the last event
+  w.sc->above_min = ~0ull;
+  w.sc->above_count = 0;
+}
+
+// Flags the window's events (whole tie groups: the window is a key range)
+// and finds the smallest key and the count above it (exact integer work).
+__global__ void __launch_bounds__(kT) window_flags_kernel(Work w, int64_t E) {
+  const uint64_t lo = w.sc->lo_key, hi = w.sc->hi_key;
+  unsigned long long mn = ~0ull, cnt = 0;
+  GRID_STRIDE(i, E) {
+    const uint64_t k = w.keys_in[i];
+    w.flag[i] = (k >= lo && k <= hi) ? 1 : 0;
+    if (k > hi) {
+      mn = k < mn ? k : mn;
+      ++cnt;
+    }
+  }
+  using BR = cub::BlockReduce<unsigned long long, kT>;
+  __shared__ typename BR::TempStorage tmp;
+  const unsigned long long bmn = BR(tmp).Reduce(mn, [](unsigned long long a, unsigned long long b) {
+    return a < b ? a : b;
+  });
+  __syncthreads();
+  const unsigned long long bcnt = BR(tmp).Sum(cnt);
+  if (threadIdx.x == 0 && bcnt > 0) {
+    atomicMin(&w.sc->above_min, bmn);
+    atomicAdd(&w.sc->above_count, bcnt);
+  }
+}
+
+__global__ void base_window_kernel(Work w) {
+  w.sc->base[0] = w.sc->sums[1] + w.sc->above[0];
+  w.sc->base[1] = w.sc->sums[0] + w.sc->above[1];
+  w.sc->base[2] = w.sc->above_count > 0 ? key_value(w.sc->above_min) : CUDART_INF;
 }
 
 // Parallel sweep: cs/bs hold exclusive prefix masses in sorted order.
 __global__ void first_hit_kernel(Work w, int64_t E, const double* r_slot, double r_value) {
   const double r = r_slot ? *r_slot : r_value;
   const double r2 = r * r;
-  const double c0 = w.sc->sums[1], b0 = w.sc->sums[0];
+  const double c0 = w.sc->base[0], b0 = w.sc->base[1];
   unsigned long long best = ~0ull;
   GRID_STRIDE(idx, E) {
     const uint64_t key = w.keys_out[idx];
@@ -356,13 +413,13 @@ __global__ void first_hit_kernel(Work w, int64_t E, const double* r_slot, double
 __global__ void finalize_perf_kernel(Work w, int64_t E, const double* r_slot, double r_value) {
   const double r = r_slot ? *r_slot : r_value;
   const double r2 = r * r;
-  const double c0 = w.sc->sums[1], b0 = w.sc->sums[0];
+  const double c0 = w.sc->base[0], b0 = w.sc->base[1];
   double ls;
   const unsigned long long f = w.sc->first;
   if (f != ~0ull) {
     const int64_t idx = static_cast<int64_t>(f);
     const double lam = key_value(w.keys_out[idx]);
-    const double hi = idx > 0 ? key_value(w.keys_out[idx - 1]) : CUDART_INF;
+    const double hi = idx > 0 ? key_value(w.keys_out[idx - 1]) : w.sc->base[2];
     const double c_sum = c0 + w.cs[idx], b_sum = b0 + w.bs[idx];
     if (b_sum > 0.0 && r2 > c_sum) {
       ls = sqrt(b_sum / (r2 - c_sum));
@@ -499,14 +556,22 @@ extern "C" int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const 
   return static_cast<int>(cudaGetLastError());
 }
 
-// Perf mode, large E, 0 < q < 0.5: sort only the top ~q of the events.  The
-// sweep runs in descending lambda and stops at its first crossing, so if the
-// crossing lies among the selected events (all events with a key at or above
-// the threshold: whole tie groups) the result equals the full sweep's; else
-// the full sort runs.  Returns 1 when the partial path decided, 0 to fall
-// back.  Two host syncs (the selected count, the hit).
-static int gap_partial(const Work& w, int64_t E, double q, const double* r_slot, double r_value,
-                       cudaStream_t s) {
+thread_local int64_t g_window_stats[2] = {0, 0};  // windows tried, decided
+
+// Perf mode, large E: sort only the events whose keys lie in a window
+// [lo_key, hi_key] placed (from a strided key sample) at depth fractions
+// [qa, qb] of the descending order.  Events above the window enter the sweep
+// as summed masses (a deterministic tree reduction) and the lambda of their
+// last group; the window is a key range, so tie groups are never split.  The
+// sweep's predicate holds on a suffix of group heads, so a hit at a window
+// head other than the first (or at the first one when nothing lies above)
+// is the full sweep's first crossing; no hit in a window that reaches the
+// last event (qb >= 1) means no crossing at all.  A hit at the first head
+// with events above, or no hit above the bottom, returns 0 and the full sort
+// runs.  Returns the window's event count when it decided.  Two host syncs
+// (the window count, the hit).
+static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const pdlpk_red* red,
+                          const double* r_slot, double r_value, cudaStream_t s) {
   keys_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
   sample_keys_kernel<<<ew_blocks(kGapSample), kT, 0, s>>>(w, E);
   size_t bytes = w.cub_bytes;
@@ -514,9 +579,27 @@ static int gap_partial(const Work& w, int64_t E, double q, const double* r_slot,
                                                0, 64, s) != cudaSuccess) {
     return -1;
   }
-  const int rank = std::min(kGapSample - 1, static_cast<int>(q * kGapSample));
-  threshold_kernel<<<1, 1, 0, s>>>(w, rank);
-  high_flags_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+  const int ra = qa <= 0.0 ? 0 : std::min(kGapSample - 1, static_cast<int>(qa * kGapSample));
+  const bool to_bottom = qb >= 1.0;
+  const int rb = to_bottom ? -1 : std::min(kGapSample - 1, static_cast<int>(qb * kGapSample));
+  window_keys_kernel<<<1, 1, 0, s>>>(w, ra, rb);
+  window_flags_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+  if (ra > 0) {
+    const Work wc = w;
+    auto fa = [wc] __device__(int64_t e, double* v) -> unsigned {
+      if (wc.keys_in[e] <= wc.sc->hi_key) return 0u;
+      const int32_t t = wc.sel[e];
+      v[0] = wc.dc[t];
+      v[1] = wc.di[t];
+      return 3u;
+    };
+    if (multi_reduce<2>(fa, E, PDLPK_RED_TREE, red->shards, 0u, red->scratch, w.sc->above, s) != 0) {
+      return -1;
+    }
+  } else {
+    cudaMemsetAsync(w.sc->above, 0, sizeof(w.sc->above), s);
+  }
+  base_window_kernel<<<1, 1, 0, s>>>(w);
   uint64_t* keys_h = reinterpret_cast<uint64_t*>(w.cs);
   bytes = w.cub_bytes;
   if (cub::DeviceSelect::Flagged(w.cub_tmp, bytes, w.keys_in, w.flag, keys_h, &w.sc->num_high,
@@ -544,27 +627,42 @@ static int gap_partial(const Work& w, int64_t E, double q, const double* r_slot,
   cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.bs, w.bs, eh, s);
   init_first_kernel<<<1, 1, 0, s>>>(w);
   first_hit_kernel<<<ew_blocks(eh), kT, 0, s>>>(w, eh, r_slot, r_value);
-  unsigned long long first = 0;
-  cudaMemcpyAsync(&first, &w.sc->first, sizeof(first), cudaMemcpyDeviceToHost, s);
+  struct {
+    unsigned long long first, above;
+  } h{};
+  cudaMemcpyAsync(&h.first, &w.sc->first, sizeof(h.first), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&h.above, &w.sc->above_count, sizeof(h.above), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
-  return first == ~0ull ? 0 : 1;
+  if (h.first == ~0ull) return to_bottom ? eh : 0;
+  if (h.first == 0 && h.above > 0) return 0;
+  return eh;
+}
+
+extern "C" void pdlpk_gap_window_stats(int64_t* tried, int64_t* decided) {
+  *tried = g_window_stats[0];
+  *decided = g_window_stats[1];
 }
 
 extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const double* y,
                                 const double* ax, const double* aty, double omega,
                                 const double* r_slot, double r_value, int64_t E,
-                                const pdlpk_red* red, void* work, double* gap_slot, double q,
-                                cudaStream_t s) {
+                                const pdlpk_red* red, void* work, double* gap_slot, double qa,
+                                double qb, cudaStream_t s) {
   const int64_t n = P->n, m = P->m;
   Work w = carve(work, n, m);
   const GapIn g = make_in(P, x, y, ax, aty, omega);
   const bool parity = red->parity != 0;
   bool decided = false;
-  if (!parity && q > 0.0 && q < 0.5 && E > (int64_t(1) << 20)) {
-    const int pr = gap_partial(w, E, q, r_slot, r_value, s);
+  int64_t E_fin = E;  // events the finalize reads (the window's when it decided)
+  if (!parity && qa >= 0.0 && qb > qa && qb - qa < 0.5 && E > (int64_t(1) << 20)) {
+    const int64_t pr = gap_window(w, E, qa, qb, red, r_slot, r_value, s);
     if (pr < 0) return static_cast<int>(cudaGetLastError());
-    decided = pr == 1;
+    decided = pr > 0;
+    if (decided) E_fin = pr;
+    ++g_window_stats[0];
+    if (decided) ++g_window_stats[1];
   }
+  if (!decided) base_full_kernel<<<1, 1, 0, s>>>(w);
   if (E > 0 && !decided) {
     keys_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
     size_t bytes = w.cub_bytes;
@@ -588,9 +686,9 @@ extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const d
     init_first_kernel<<<1, 1, 0, s>>>(w);
     if (E > 0) first_hit_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E, r_slot, r_value);
   }
-  // (a decided partial path has its crossing index < E_high: the no-crossing
-  // branch of finalize, which reads the last of all E events, is not taken)
-  finalize_perf_kernel<<<1, 1, 0, s>>>(w, E, r_slot, r_value);
+  // (a decided window: its crossing index, or the no-crossing branch over
+  // the window's events with the masses above in base)
+  finalize_perf_kernel<<<1, 1, 0, s>>>(w, E_fin, r_slot, r_value);
   hit_fraction_kernel<<<1, 1, 0, s>>>(w, E, gap_slot + 2);
   const double* lam_star = &w.sc->lambda_star;
   auto fv = [g, lam_star] __device__(int64_t t, double* v) -> unsigned {

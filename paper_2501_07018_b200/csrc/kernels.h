@@ -342,12 +342,15 @@ int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const double* y, 
                       const double* aty, double omega, const pdlpk_red* red, void* work,
                       int* count_out, cudaStream_t s);
 /* gap_slot[0] = the gap, gap_slot[2] = the first crossing's position as a
- * fraction of E (1 if none).  q in (0, 0.5): perf mode may sort only the
- * top ~q of the events first (exact; falls back to the full sort). */
+ * fraction of E (1 if none).  0 <= qa < qb, qb - qa < 0.5: perf mode first
+ * sorts only the events at depth fractions [qa, qb] of the descending order
+ * (exact when the crossing lies inside; else the full sort runs). */
 int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
                      const double* aty, double omega, const double* r_slot, double r_value,
-                     int64_t E, const pdlpk_red* red, void* work, double* gap_slot, double q,
-                     cudaStream_t s);
+                     int64_t E, const pdlpk_red* red, void* work, double* gap_slot, double qa,
+                     double qb, cudaStream_t s);
+/* Window sorts tried / decided on this host thread (cumulative). */
+void pdlpk_gap_window_stats(int64_t* tried, int64_t* decided);
 /* slot = sqrt(omega*dx2 + dy2/omega) from two slots (restart_progress_metric). */
 int pdlpk_radius(const double* dx2, const double* dy2, double omega, double* out,
                  cudaStream_t s);

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -1497,8 +1498,17 @@ class Engine {
     gaps_local(P, q, count, omega, out);
   }
 
+  // Window of the next window sort for (subproblem, query): the last
+  // crossing depth +- half, widened after a miss, narrowed after a hit.
+  struct GapWindow {
+    double depth = -1.0;  // unknown: full sort
+    double half = 0.04;
+  };
+  GapWindow& gap_window_for(const pdlpk_problem& P, int i) {
+    return gap_windows_[std::make_pair(static_cast<const void*>(P.c), i)];
+  }
+
   void gaps_local(const pdlpk_problem& P, const GapQuery* q, int count, double omega, double* out) {
-    if (gap_partial_off_) gap_q_ = 1.0;
     if (gap_shared_ && count > 1) {
       for (int i = 0; i < count; ++i) gaps_local(P, q + i, 1, omega, out + i);
       return;
@@ -1510,22 +1520,37 @@ class Engine {
     }
     PDLP_CK(cudaMemcpyAsync(host_islots_, islots_.get(), 8 * sizeof(int), cudaMemcpyDeviceToHost, s()));
     PDLP_CK(cudaStreamSynchronize(s()));
+    double qa[2] = {-1.0, -1.0}, qb[2] = {-1.0, -1.0};
     for (int i = 0; i < count; ++i) {
+      const GapWindow& gw = gap_window_for(P, i);
+      if (!gap_partial_off_ && gw.depth >= 1.0) {
+        qa[i] = 0.9995;  // no crossing last time: only the last ~0.05 % sorted
+        qb[i] = 1.0;
+      } else if (!gap_partial_off_ && gw.depth >= 0.0) {
+        qa[i] = std::max(0.0, gw.depth - gw.half);
+        qb[i] = std::min(1.0, gw.depth + gw.half);
+      }
       const double radius = std::sqrt(omega * q[i].dx2 + q[i].dy2 / omega);
       PDLP_LAUNCH(pdlpk_gap_finish(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, nullptr, radius,
                                    host_islots_[i], &r, gap_work_[i].get(), slot(kSlotGap + i),
-                                   gap_q_, s()));
+                                   qa[i], qb[i], s()));
     }
     const double* h = read_slots(kSlotGap + count + 2);
-    double hit = 0.0;
+    static const bool gap_debug = std::getenv("PDLP_GAP_DEBUG") != nullptr;
     for (int i = 0; i < count; ++i) {
       out[i] = h[kSlotGap + i];
-      hit = std::max(hit, h[kSlotGap + 2 + i]);
+      const double hit = h[kSlotGap + 2 + i];
+      if (gap_debug) {
+        std::fprintf(stderr, "gap q=%d/%d c=%p E=%d window=[%.4f,%.4f] hit=%.5f\n", i, count,
+                     static_cast<const void*>(P.c), host_islots_[i], qa[i], qb[i], hit);
+      }
+      GapWindow& gw = gap_window_for(P, i);
+      if (qb[i] > qa[i] && hit < 1.0 && qa[i] < 0.999) {  // did the crossing fall inside?
+        const bool inside = hit >= qa[i] && hit <= qb[i];
+        gw.half = inside ? std::max(0.02, 0.75 * gw.half) : std::min(0.24, 2.0 * gw.half);
+      }
+      gw.depth = hit;  // 1: no crossing
     }
-    // Size the next partial sort from where this crossing fell (twice its
-    // depth plus a margin); deep crossings (C1: ~50 %) use the full sort.
-    gap_q_ = std::min(1.0, 2.0 * hit + 0.02);
-    if (gap_partial_off_) gap_q_ = 1.0;
   }
 
   // ---- the loop ----------------------------------------------------------
@@ -1613,7 +1638,7 @@ class Engine {
   DevBuf<double> red_scratch_;
   DevBuf<char> gap_work_[2];
   bool gap_shared_ = false;  // one gap buffer, queries evaluated one at a time
-  double gap_q_ = 0.25;      // partial-sort fraction for the next gap evaluation
+  std::map<std::pair<const void*, int>, GapWindow> gap_windows_;
   // PDLP_GAP_PARTIAL=0: always the full sort (measurements)
   bool gap_partial_off_ = [] {
     const char* e = std::getenv("PDLP_GAP_PARTIAL");
@@ -2062,12 +2087,16 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
                  static_cast<long long>(res->polish_iterations), res->termination_detail);
   }
   if (o->logging || std::getenv("PDLP_TIMING") != nullptr) {
+    int64_t wt = 0, wd = 0;
+    pdlpk_gap_window_stats(&wt, &wd);
     std::fprintf(stderr,
                  "phase=main event=timing solve=%.4f upload=%.4f precondition=%.4f loop=%.4f "
-                 "steps=%.4f cadence=%.4f gap=%.4f polish=%.4f alloc=%.4f\n",
+                 "steps=%.4f cadence=%.4f gap=%.4f gap_windows=%lld/%lld polish=%.4f "
+                 "alloc=%.4f\n",
                  res->solve_seconds, res->upload_seconds, res->precondition_seconds,
                  res->loop_seconds, res->step_seconds, E.cadence_seconds_, E.gap_seconds_,
-                 E.polish_seconds_, g_alloc_seconds);
+                 static_cast<long long>(wd), static_cast<long long>(wt), E.polish_seconds_,
+                 g_alloc_seconds);
   }
 }
 
@@ -2454,8 +2483,11 @@ int pdlp_normalized_duality_gap(const pdlp_problem_view* problem, const double* 
     int events = 0;
     PDLP_CK(cudaMemcpyAsync(&events, E.islots_.get(), sizeof(int), cudaMemcpyDeviceToHost, E.s()));
     PDLP_CK(cudaStreamSynchronize(E.s()));
+    // PDLP_GAP_WINDOW="qa:qb" forces a window sort (tests of the perf path)
+    double qa = -1.0, qb = -1.0;
+    if (const char* wv = std::getenv("PDLP_GAP_WINDOW")) std::sscanf(wv, "%lf:%lf", &qa, &qb);
     PDLP_LAUNCH(pdlpk_gap_finish(&P, dx.get(), dy.get(), dax.get(), daty.get(), omega, nullptr, r,
-                                 events, &red, E.gap_work_[0].get(), E.slot(0), 0.0, E.s()));
+                                 events, &red, E.gap_work_[0].get(), E.slot(0), qa, qb, E.s()));
     *gap = E.read_slots(1)[0];
   });
 }

@@ -89,7 +89,20 @@ __host__ __device__ inline int stage_nnz_for(int L, size_t budget) {
   return lo;
 }
 constexpr int kStages = PDLPK_TILE_STAGES;  // ring depth: tiles in flight per CTA
-constexpr size_t kRingHeader = 128;         // one mbarrier per stage
+// Ring header: full/empty mbarriers, then one TileHdr per stage.
+constexpr size_t kRingHeader = 128;
+// What the consumers of a stage need about its tile, written by the producer
+// lane (which computes it anyway for the bulk copies) before its arrive on
+// full[stage]: the consumers read 32 bytes instead of re-deriving the tile's
+// metadata and six window shifts per warp.
+struct TileHdr {
+  int64_t r0, s0;    // first line, first entry
+  int32_t cnt;       // lines
+  uint32_t shifts;   // 4-bit byte shifts: idx, val, ptr, staged operands 0..2
+  int32_t per;       // lines per consumer warp
+  int32_t pad;
+};
+static_assert(2 * 8 * kStages + sizeof(TileHdr) * kStages <= kRingHeader, "ring header");
 // Dynamic shared memory of a layout's staged ring (its stage size is chosen
 // per layout, see solver.cpp build_schedule).
 __host__ __device__ inline size_t ring_smem(const pdlpk_csr& A) {
@@ -379,8 +392,11 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
     extern __shared__ __align__(128) unsigned char ring[];
     uint64_t* full = reinterpret_cast<uint64_t*>(ring);
     uint64_t* empty = full + kStages;
+    TileHdr* hdr = reinterpret_cast<TileHdr*>(ring + 2 * 8 * kStages);
     unsigned char* stage0 = ring + kRingHeader;
     const int64_t tb = A.tile_blocks;
+    const StageLayout sl = stage_layout(A.tile_lines_cap, A.tile_nnz_cap);
+    const size_t stage_bytes = static_cast<size_t>(A.tile_stage_bytes);
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int q = 0; q < kStages; ++q) {
@@ -397,18 +413,27 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
           const int stage = i % kStages;
           if (i >= kStages) mbar_wait(&empty[stage], ((i / kStages) + 1) & 1);
           const TileMeta tm = tile_meta(A, t);
-          unsigned char* buf = stage0 + stage * static_cast<size_t>(A.tile_stage_bytes);
-          const StageLayout sl = stage_layout(A.tile_lines_cap, A.tile_nnz_cap);
+          unsigned char* buf = stage0 + stage * stage_bytes;
           const Win wi = win(idx, tm.s0, tm.len, 4);
           const Win wv = win(vals, tm.s0, tm.len, 8);
           const Win wp = win(start, tm.r0, tm.cnt + 1, static_cast<int>(sizeof(P)));
           uint32_t total = wi.bytes + wv.bytes + wp.bytes;
+          uint32_t shifts = wi.shift | (wv.shift << 4) | (wp.shift << 8);
           Win we[kMaxStaged];
 #pragma unroll
           for (int q = 0; q < Epi::kStaged; ++q) {
             we[q] = win(epi.staged_src(q), tm.r0, tm.cnt, 8);
             total += we[q].bytes;
+            shifts |= we[q].shift << (12 + 4 * q);
           }
+          TileHdr h;
+          h.r0 = tm.r0;
+          h.s0 = tm.s0;
+          h.cnt = tm.cnt;
+          h.shifts = shifts;
+          h.per = (tm.cnt + kConsumerWarps - 1) / kConsumerWarps;
+          h.pad = 0;
+          hdr[stage] = h;  // released by the arrive below
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&full[stage], total);
           if (wi.bytes) bulk_g2s(buf, wi.src, wi.bytes, &full[stage]);
@@ -427,26 +452,25 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
       int i = 0;
       for (int64_t t = b; t < A.n_tiles; t += tb, ++i) {
         const int stage = i % kStages;
-        const TileMeta tm = tile_meta(A, t);
-        unsigned char* buf = stage0 + stage * static_cast<size_t>(A.tile_stage_bytes);
-        const StageLayout sl = stage_layout(A.tile_lines_cap, A.tile_nnz_cap);
-        const int32_t* s_idx =
-            reinterpret_cast<const int32_t*>(buf + win(idx, tm.s0, tm.len, 4).shift);
-        double* s_val = reinterpret_cast<double*>(buf + sl.val + win(vals, tm.s0, tm.len, 8).shift);
-        const P* s_ptr = reinterpret_cast<const P*>(
-            buf + sl.ptr + win(start, tm.r0, tm.cnt + 1, static_cast<int>(sizeof(P))).shift);
+        unsigned char* buf = stage0 + stage * stage_bytes;
+        mbar_wait(&full[stage], (i / kStages) & 1);
+        const TileHdr h = hdr[stage];
+        const TileMeta tm{h.r0, h.s0, h.cnt, 0};
+        const uint32_t sh = h.shifts;
+        const int32_t* s_idx = reinterpret_cast<const int32_t*>(buf + (sh & 15u));
+        double* s_val = reinterpret_cast<double*>(buf + sl.val + ((sh >> 4) & 15u));
+        const P* s_ptr = reinterpret_cast<const P*>(buf + sl.ptr + ((sh >> 8) & 15u));
         const double* s_epi[kMaxStaged];
 #pragma unroll
         for (int q = 0; q < Epi::kStaged; ++q) {
           s_epi[q] = reinterpret_cast<const double*>(buf + sl.epi + q * sl.epi_stride +
-                                                     win(epi.staged_src(q), tm.r0, tm.cnt, 8).shift);
+                                                     ((sh >> (12 + 4 * q)) & 15u));
         }
         // the tile's lines split evenly over the consumer warps (a tile of
         // 20-32-entry lines holds only ~45 lines: fixed 96-line ranges would
         // leave six warps idle)
-        const int per = (tm.cnt + kConsumerWarps - 1) / kConsumerWarps;
+        const int per = h.per;
         const int l0 = per * cw;
-        mbar_wait(&full[stage], (i / kStages) & 1);
         if (l0 < tm.cnt) {
           const int l1 = l0 + per < tm.cnt ? l0 + per : tm.cnt;
           const int e0 = static_cast<int>(static_cast<int64_t>(s_ptr[l0]) - tm.s0);
