@@ -37,11 +37,18 @@ class CopyPool {
   }
   int width() const { return static_cast<int>(threads_.size()) + 1; }
 
-  void run(char* dst, const char* src, size_t len) {
+  // narrow: src holds len / 4 int64 values, dst receives them as saturated
+  // int32 (len = destination bytes)
+  void run(char* dst, const char* src, size_t len, bool narrow = false) {
     const int parts = static_cast<int>(
         std::max<size_t>(1, std::min<size_t>(width(), (len + kMinPart - 1) / kMinPart)));
     if (parts == 1) {
-      std::memcpy(dst, src, len);
+      narrow_ = narrow;
+      dst_ = dst;
+      src_ = src;
+      len_ = len;
+      parts_ = 1;
+      copy_part(0);
       return;
     }
     {
@@ -49,6 +56,7 @@ class CopyPool {
       dst_ = dst;
       src_ = src;
       len_ = len;
+      narrow_ = narrow;
       parts_ = parts;
       pending_ = parts - 1;
       ++gen_;
@@ -61,9 +69,21 @@ class CopyPool {
 
  private:
   void copy_part(int i) const {
-    const size_t per = (len_ + parts_ - 1) / parts_;
+    size_t per = (len_ + parts_ - 1) / parts_;
+    per = (per + 7) & ~size_t(7);  // whole 4- and 8-byte elements per part
     const size_t lo = std::min(len_, per * i), hi = std::min(len_, lo + per);
-    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+    if (hi <= lo) return;
+    if (!narrow_) {
+      std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+      return;
+    }
+    int32_t* d = reinterpret_cast<int32_t*>(dst_ + lo);
+    const int64_t* v = reinterpret_cast<const int64_t*>(src_) + lo / 4;
+    const size_t n = (hi - lo) / 4;
+    for (size_t k = 0; k < n; ++k) {
+      const int64_t x = v[k];
+      d[k] = x < 0 ? -1 : (x > INT32_MAX ? INT32_MAX : static_cast<int32_t>(x));
+    }
   }
   void loop(int id) {
     uint64_t seen = 0;
@@ -86,6 +106,7 @@ class CopyPool {
   char* dst_ = nullptr;
   const char* src_ = nullptr;
   size_t len_ = 0;
+  bool narrow_ = false;
   int parts_ = 0;
   int pending_ = 0;
   uint64_t gen_ = 0;
@@ -94,8 +115,16 @@ class CopyPool {
 
 struct Ring {
   char* slot[kSlots] = {};
+  // The last DMA that touched each slot (recorded on that call's stream):
+  // a slot is reused only after it completes, so calls need not drain the
+  // ring and successive uploads overlap.  Events belong to one device; a call
+  // on another device waits for them and recreates them there.
+  cudaEvent_t ev[kSlots] = {};
+  bool pending[kSlots] = {};
+  int device = -1;
+  int next = 0;  // round-robin slot cursor
   CopyPool pool;
-  std::mutex mu;  // one upload at a time
+  std::mutex mu;  // one transfer at a time
   bool ok = false;
   Ring() {
     // Portable pinned memory: usable from every device's streams.  Kept for
@@ -109,6 +138,34 @@ struct Ring {
     for (int i = 0; i < kSlots; ++i) slot[i] = p + kChunk * i;
     ok = true;
   }
+  // Caller holds mu.
+  void bind_device() {
+    int d = 0;
+    PDLP_CK(cudaGetDevice(&d));
+    if (d == device) return;
+    for (int k = 0; k < kSlots; ++k) {
+      if (ev[k] != nullptr) {
+        if (pending[k]) cudaEventSynchronize(ev[k]);
+        cudaEventDestroy(ev[k]);
+        ev[k] = nullptr;
+      }
+      pending[k] = false;
+    }
+    for (int k = 0; k < kSlots; ++k) {
+      PDLP_CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    }
+    device = d;
+  }
+  // Slot k is free for the host (its last DMA has completed).
+  cudaError_t acquire(int k) {
+    if (!pending[k]) return cudaSuccess;
+    pending[k] = false;
+    return cudaEventSynchronize(ev[k]);
+  }
+  cudaError_t release(int k, cudaStream_t s) {
+    pending[k] = true;
+    return cudaEventRecord(ev[k], s);
+  }
 };
 
 Ring& ring() {
@@ -116,47 +173,86 @@ Ring& ring() {
   return *r;
 }
 
+// src bytes per destination byte: 2 when narrowing int64 -> int32
+void stage_h2d_impl(void* dst, const void* src, size_t bytes, cudaStream_t s, bool narrow) {
+  Ring& R = ring();
+  std::lock_guard<std::mutex> g(R.mu);
+  R.bind_device();
+  const char* in = static_cast<const char*>(src);
+  char* out = static_cast<char*>(dst);
+  const size_t ratio = narrow ? 2 : 1;
+  cudaError_t err = cudaSuccess;
+  for (size_t off = 0; off < bytes && err == cudaSuccess; off += kChunk) {
+    const int k = R.next;
+    R.next = (R.next + 1) % kSlots;
+    const size_t len = std::min(kChunk, bytes - off);
+    if ((err = R.acquire(k)) != cudaSuccess) break;
+    R.pool.run(R.slot[k], in + off * ratio, len, narrow);
+    if ((err = cudaMemcpyAsync(out + off, R.slot[k], len, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      break;
+    err = R.release(k, s);
+  }
+  PDLP_CK(err);
+}
+
 }  // namespace
 
 void stage_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return;
-  if (bytes <= kDirectMax) {
+  if (bytes <= kDirectMax || !ring().ok) {
     PDLP_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return;
   }
+  stage_h2d_impl(dst, src, bytes, s, false);
+}
+
+void stage_h2d_narrow(int32_t* dst, const int64_t* src, size_t count, cudaStream_t s) {
+  if (count == 0) return;
+  if (!ring().ok || count * 8 <= kDirectMax) {
+    // small: narrow on the host into a temporary, one pageable copy
+    std::vector<int32_t> tmp(count);
+    for (size_t k = 0; k < count; ++k) {
+      const int64_t x = src[k];
+      tmp[k] = x < 0 ? -1 : (x > INT32_MAX ? INT32_MAX : static_cast<int32_t>(x));
+    }
+    PDLP_CK(cudaMemcpyAsync(dst, tmp.data(), count * 4, cudaMemcpyHostToDevice, s));
+    PDLP_CK(cudaStreamSynchronize(s));  // tmp dies here
+    return;
+  }
+  stage_h2d_impl(dst, src, count * 4, s, true);
+}
+
+void stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
   Ring& R = ring();
-  if (!R.ok) {
-    PDLP_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  if (bytes <= kDirectMax || !R.ok) {
+    PDLP_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    PDLP_CK(cudaStreamSynchronize(s));
     return;
   }
   std::lock_guard<std::mutex> g(R.mu);
-  // Events belong to the current device, so they live for one upload; the
-  // ring is drained before returning, which also frees the slots for the
-  // next upload.
-  cudaEvent_t ev[kSlots];
-  for (int i = 0; i < kSlots; ++i) PDLP_CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-  bool used[kSlots] = {};
+  R.bind_device();
   const char* in = static_cast<const char*>(src);
   char* out = static_cast<char*>(dst);
+  const size_t chunks = (bytes + kChunk - 1) / kChunk;
   cudaError_t err = cudaSuccess;
-  int i = 0;
-  for (size_t off = 0; off < bytes && err == cudaSuccess; off += kChunk, ++i) {
-    const int k = i % kSlots;
-    const size_t len = std::min(kChunk, bytes - off);
-    if (used[k] && (err = cudaEventSynchronize(ev[k])) != cudaSuccess) break;
-    R.pool.run(R.slot[k], in + off, len);
-    if ((err = cudaMemcpyAsync(out + off, R.slot[k], len, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-      break;
-    err = cudaEventRecord(ev[k], s);
-    used[k] = true;
+  auto issue = [&](size_t c) {
+    const int k = static_cast<int>(c % kSlots);
+    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+    if (err == cudaSuccess) err = R.acquire(k);  // an upload may still read it
+    if (err == cudaSuccess) err = cudaMemcpyAsync(R.slot[k], in + off, len, cudaMemcpyDeviceToHost, s);
+    if (err == cudaSuccess) err = R.release(k, s);
+  };
+  size_t issued = 0;
+  for (; issued < chunks && issued < static_cast<size_t>(kSlots); ++issued) issue(issued);
+  for (size_t c = 0; c < chunks && err == cudaSuccess; ++c) {
+    const int k = static_cast<int>(c % kSlots);
+    if ((err = R.acquire(k)) != cudaSuccess) break;
+    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+    R.pool.run(out + off, R.slot[k], len);
+    if (issued < chunks) issue(issued++);  // the slot is free again
   }
-  for (int k = 0; k < kSlots; ++k) {
-    if (used[k]) {
-      const cudaError_t e = cudaEventSynchronize(ev[k]);
-      if (err == cudaSuccess) err = e;
-    }
-    cudaEventDestroy(ev[k]);
-  }
+  if (err != cudaSuccess) cudaStreamSynchronize(s);  // no DMA may outlive the ring lock
   PDLP_CK(err);
 }
 

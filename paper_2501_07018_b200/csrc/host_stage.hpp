@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <cstdint>
 
 namespace pdlp_host {
 
@@ -20,5 +21,16 @@ namespace pdlp_host {
 // Small copies go straight to cudaMemcpyAsync.  Thread-safe (one upload at a
 // time through the ring).
 void stage_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
+// Uploads `count` int64 values narrowed to int32 (saturating: a value outside
+// int32 becomes -1 or INT32_MAX, so range checks still reject it): half the
+// bytes over PCIe for indices and line starts.
+void stage_h2d_narrow(int32_t* dst, const int64_t* src, size_t count, cudaStream_t s);
+
+// Device -> pageable host download through the same ring: the copy engine
+// fills pinned chunks while the pool copies finished chunks out.  Runs after
+// the work already in `s`; returns with `dst` filled (synchronous, like a
+// pageable cudaMemcpy).
+void stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
 }  // namespace pdlp_host

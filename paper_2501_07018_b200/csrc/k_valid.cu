@@ -73,7 +73,8 @@ __global__ void value_check_kernel(const double* v, int64_t nnz, unsigned long l
 }
 
 // Raw int64 row pointers and indices (before the int32 conversion).
-__global__ void ptr_check_kernel(const int64_t* start, int64_t dim, int64_t nnz, unsigned* bad) {
+template <class T>
+__global__ void ptr_check_kernel(const T* start, int64_t dim, int64_t nnz, unsigned* bad) {
   GRID_STRIDE(r, dim + 1) {
     const int64_t a = start[r];
     if (r == 0 && a != 0) atomicOr(bad, 1u);
@@ -82,7 +83,8 @@ __global__ void ptr_check_kernel(const int64_t* start, int64_t dim, int64_t nnz,
   }
 }
 
-__global__ void index_range_kernel(const int64_t* idx, int64_t count, int64_t bound, unsigned* bad) {
+template <class T>
+__global__ void index_range_kernel(const T* idx, int64_t count, int64_t bound, unsigned* bad) {
   GRID_STRIDE(k, count) {
     const int64_t v = idx[k];
     if (v < 0 || v >= bound) atomicOr(bad, 2u);
@@ -141,6 +143,14 @@ extern "C" int pdlpk_validate_vectors(const double* c, const double* lv, const d
 extern "C" int pdlpk_validate_raw_layout(const int64_t* start, int64_t dim, const int64_t* idx,
                                          int64_t count, int64_t nnz, int64_t bound, unsigned* bad,
                                          cudaStream_t s) {
+  if (start != nullptr) ptr_check_kernel<<<ew_blocks(dim + 1), kT, 0, s>>>(start, dim, nnz, bad);
+  if (idx != nullptr && count > 0) index_range_kernel<<<ew_blocks(count), kT, 0, s>>>(idx, count, bound, bad);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_validate_raw_layout32(const int32_t* start, int64_t dim, const int32_t* idx,
+                                           int64_t count, int64_t nnz, int64_t bound,
+                                           unsigned* bad, cudaStream_t s) {
   if (start != nullptr) ptr_check_kernel<<<ew_blocks(dim + 1), kT, 0, s>>>(start, dim, nnz, bad);
   if (idx != nullptr && count > 0) index_range_kernel<<<ew_blocks(count), kT, 0, s>>>(idx, count, bound, bad);
   return static_cast<int>(cudaGetLastError());

@@ -258,6 +258,11 @@ int pdlpk_validate_vectors(const double* c, const double* lv, const double* uv, 
 int pdlpk_validate_raw_layout(const int64_t* start, int64_t dim, const int64_t* idx,
                               int64_t count, int64_t nnz, int64_t bound, unsigned* bad,
                               cudaStream_t s);
+/* Same on 32-bit arrays (narrowed on the host with saturation, so an
+ * out-of-range 64-bit value stays out of range). */
+int pdlpk_validate_raw_layout32(const int32_t* start, int64_t dim, const int32_t* idx,
+                                int64_t count, int64_t nnz, int64_t bound, unsigned* bad,
+                                cudaStream_t s);
 int pdlpk_validate_consistency(const pdlpk_csr* R, const int32_t* row_of, const pdlpk_csr* C,
                                const int32_t* col_of, int* row_count, unsigned* bad,
                                cudaStream_t s);

@@ -25,6 +25,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <exception>
 #include <thread>
 #include <vector>
 
@@ -158,22 +159,66 @@ bool direct_tiles(const int64_t* start, int64_t dim) {
   return true;
 }
 
+// Line segments of a schedule build: [lo, hi) line ranges built by host
+// threads (fixed boundaries, so the schedule is deterministic) and joined in
+// line order.  A tile never spans a segment boundary.
+struct SchedPart {
+  std::vector<int32_t> t0, tc, ck_row, ck_len, ck_pos, ck_slot;
+  std::vector<int64_t> tn, ck_beg;
+  std::vector<int32_t> cc_row, cc_len, cc_pos, cc_slot;
+  std::vector<int64_t> cc_beg;
+  int64_t n_multi = 0;
+  int64_t short_lines = 0, short_nnz = 0;
+};
+
+template <class F>
+void for_segments(int64_t dim, int parts, F&& f) {
+  if (parts <= 1) {
+    f(0, 0, dim);
+    return;
+  }
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(static_cast<size_t>(parts));
+  for (int q = 0; q < parts; ++q) {
+    th.emplace_back([&, q] {
+      try {
+        f(q, dim * q / parts, dim * (q + 1) / parts);
+      } catch (...) {
+        err[q] = std::current_exception();
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  for (auto& e : err) {
+    if (e) std::rethrow_exception(e);
+  }
+}
+
 void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
                     int64_t short_max = PDLPK_SHORT_MAX, int32_t budget = 0) {
   if (budget <= 0) budget = pdlpk_stage_budget(PDLPK_TILE_NNZ);
-  std::vector<int32_t> t0, tc, ck_row, ck_len, ck_pos, ck_slot;
-  std::vector<int64_t> tn, ck_beg;
-  int64_t n_multi = 0;
+  const int parts = static_cast<int>(std::clamp<int64_t>(
+      dim / (int64_t(1) << 18), 1, std::max(1u, std::min(16u, std::thread::hardware_concurrency()))));
+  std::vector<SchedPart> seg(static_cast<size_t>(parts));
   const bool direct = direct_tiles(start, dim);
   int32_t shape_lines = PDLPK_TILE_ROWS, shape_nnz = PDLPK_TILE_NNZ, stage_bytes = budget;
   if (!direct) {
-    int64_t short_lines = 0, short_nnz = 0;
-    for (int64_t r = 0; r < dim; ++r) {
-      const int64_t len = start[r + 1] - start[r];
-      if (len <= short_max) {
-        ++short_lines;
-        short_nnz += len;
+    for_segments(dim, parts, [&](int q, int64_t lo, int64_t hi) {
+      int64_t sl = 0, sn = 0;
+      for (int64_t r = lo; r < hi; ++r) {
+        const int64_t len = start[r + 1] - start[r];
+        if (len <= short_max) {
+          ++sl;
+          sn += len;
+        }
       }
+      seg[q].short_lines = sl;
+      seg[q].short_nnz = sn;
+    });
+    int64_t short_lines = 0, short_nnz = 0;
+    for (const SchedPart& g : seg) {
+      short_lines += g.short_lines;
+      short_nnz += g.short_nnz;
     }
     const double avg = short_lines > 0 ? static_cast<double>(short_nnz) / short_lines : 1.0;
     pdlpk_tile_shape(avg, budget, &shape_lines, &shape_nnz, &stage_bytes);
@@ -181,56 +226,80 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
   const int64_t tile_rows = direct ? 256 : shape_lines;
   const int64_t tile_nnz = direct ? 256 * PDLPK_SHORT_MAX : shape_nnz;
   if (direct) short_max = PDLPK_SHORT_MAX;
-  int64_t cur0 = -1, cur_rows = 0, cur_nnz = 0;
-  auto close = [&] {
-    if (cur_rows > 0) {
-      t0.push_back(static_cast<int32_t>(cur0));
-      tc.push_back(static_cast<int32_t>(cur_rows | (cur_nnz << 12)));
-      tn.push_back(start[cur0]);
+  for_segments(dim, parts, [&](int q, int64_t lo, int64_t hi) {
+    SchedPart& g = seg[q];
+    int64_t cur0 = -1, cur_rows = 0, cur_nnz = 0;
+    auto close = [&] {
+      if (cur_rows > 0) {
+        g.t0.push_back(static_cast<int32_t>(cur0));
+        g.tc.push_back(static_cast<int32_t>(cur_rows | (cur_nnz << 12)));
+        g.tn.push_back(start[cur0]);
+      }
+      cur0 = -1;
+      cur_rows = 0;
+      cur_nnz = 0;
+    };
+    for (int64_t r = lo; r < hi; ++r) {
+      const int64_t len = start[r + 1] - start[r];
+      if (len > short_max && len <= PDLPK_WARP_LINE_MAX) {
+        // a medium line: one warp
+        close();
+        g.ck_row.push_back(static_cast<int32_t>(r));
+        g.ck_beg.push_back(start[r]);
+        g.ck_len.push_back(static_cast<int32_t>(len));
+        g.ck_pos.push_back(static_cast<int32_t>(1 << 16));
+        g.ck_slot.push_back(-1);
+        continue;
+      }
+      if (len > PDLPK_WARP_LINE_MAX) {
+        // a long line: consecutive CTA chunks of <= PDLPK_CHUNK entries
+        // (multi-chunk slots numbered per segment, offset when joined)
+        close();
+        int64_t nch = (len + PDLPK_CHUNK - 1) / PDLPK_CHUNK;
+        const int64_t per = (len + nch - 1) / nch;  // balanced chunk length
+        nch = (len + per - 1) / per;
+        if (nch > 0xffff) throw std::runtime_error("line too long for the chunk schedule");
+        const int32_t slot = nch > 1 ? static_cast<int32_t>(g.n_multi++) : -1;
+        for (int64_t c = 0; c < nch; ++c) {
+          const int64_t b = start[r] + c * per;
+          g.cc_row.push_back(static_cast<int32_t>(r));
+          g.cc_beg.push_back(b);
+          g.cc_len.push_back(static_cast<int32_t>(std::min(per, start[r + 1] - b)));
+          g.cc_pos.push_back(static_cast<int32_t>(c | (nch << 16)));
+          g.cc_slot.push_back(slot);
+        }
+        continue;
+      }
+      if (cur_rows == tile_rows || cur_nnz + len > tile_nnz) close();
+      if (cur_rows == 0) cur0 = r;
+      ++cur_rows;
+      cur_nnz += len;
     }
-    cur0 = -1;
-    cur_rows = 0;
-    cur_nnz = 0;
-  };
-  // CTA chunks are collected apart and appended after the warp chunks.
+    close();
+  });
+  // join in line order: tiles, warp chunks, then every CTA chunk
+  std::vector<int32_t> t0, tc, ck_row, ck_len, ck_pos, ck_slot;
+  std::vector<int64_t> tn, ck_beg;
   std::vector<int32_t> cc_row, cc_len, cc_pos, cc_slot;
   std::vector<int64_t> cc_beg;
-  for (int64_t r = 0; r < dim; ++r) {
-    const int64_t len = start[r + 1] - start[r];
-    if (len > short_max && len <= PDLPK_WARP_LINE_MAX) {
-      // a medium line: one warp
-      close();
-      ck_row.push_back(static_cast<int32_t>(r));
-      ck_beg.push_back(start[r]);
-      ck_len.push_back(static_cast<int32_t>(len));
-      ck_pos.push_back(static_cast<int32_t>(1 << 16));
-      ck_slot.push_back(-1);
-      continue;
-    }
-    if (len > PDLPK_WARP_LINE_MAX) {
-      // a long line: consecutive CTA chunks of <= PDLPK_CHUNK entries
-      close();
-      int64_t nch = (len + PDLPK_CHUNK - 1) / PDLPK_CHUNK;
-      const int64_t per = (len + nch - 1) / nch;  // balanced chunk length
-      nch = (len + per - 1) / per;
-      if (nch > 0xffff) throw std::runtime_error("line too long for the chunk schedule");
-      const int32_t slot = nch > 1 ? static_cast<int32_t>(n_multi++) : -1;
-      for (int64_t q = 0; q < nch; ++q) {
-        const int64_t b = start[r] + q * per;
-        cc_row.push_back(static_cast<int32_t>(r));
-        cc_beg.push_back(b);
-        cc_len.push_back(static_cast<int32_t>(std::min(per, start[r + 1] - b)));
-        cc_pos.push_back(static_cast<int32_t>(q | (nch << 16)));
-        cc_slot.push_back(slot);
-      }
-      continue;
-    }
-    if (cur_rows == tile_rows || cur_nnz + len > tile_nnz) close();
-    if (cur_rows == 0) cur0 = r;
-    ++cur_rows;
-    cur_nnz += len;
+  int64_t n_multi = 0;
+  auto append = [](auto& dst, const auto& src) { dst.insert(dst.end(), src.begin(), src.end()); };
+  for (SchedPart& g : seg) {
+    append(t0, g.t0);
+    append(tc, g.tc);
+    append(tn, g.tn);
+    append(ck_row, g.ck_row);
+    append(ck_beg, g.ck_beg);
+    append(ck_len, g.ck_len);
+    append(ck_pos, g.ck_pos);
+    append(ck_slot, g.ck_slot);
+    append(cc_row, g.cc_row);
+    append(cc_beg, g.cc_beg);
+    append(cc_len, g.cc_len);
+    append(cc_pos, g.cc_pos);
+    for (int32_t sl : g.cc_slot) cc_slot.push_back(sl < 0 ? sl : static_cast<int32_t>(sl + n_multi));
+    n_multi += g.n_multi;
   }
-  close();
   const int64_t n_cta_chunks = static_cast<int64_t>(cc_row.size());
   ck_row.insert(ck_row.end(), cc_row.begin(), cc_row.end());
   ck_beg.insert(ck_beg.end(), cc_beg.begin(), cc_beg.end());
@@ -337,31 +406,22 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
                    cudaStream_t s) {
   const int64_t dim = v.primary_dim, nnz = v.nnz;
   const bool wide = nnz >= (int64_t(1) << 31) - 1;
-  DevBuf<int64_t> tmp;
-  // start
+  // start: 64-bit for wide layouts, else narrowed to 32 bits on the host
+  // (saturating, so the range checks below still see a bad value)
   if (wide) {
     L.start64.alloc(dim + 1);
     stage_h2d(L.start64.get(), v.start, (dim + 1) * 8, s);
     PDLP_LAUNCH(pdlpk_validate_raw_layout(L.start64.get(), dim, nullptr, 0, nnz, bound, bad, s));
   } else {
-    tmp.alloc(dim + 1);
     L.start32.alloc(dim + 1);
-    stage_h2d(tmp.get(), v.start, (dim + 1) * 8, s);
-    PDLP_LAUNCH(pdlpk_validate_raw_layout(tmp.get(), dim, nullptr, 0, nnz, bound, bad, s));
-    PDLP_LAUNCH(pdlpk_start_to_i32(tmp.get(), L.start32.get(), dim + 1, s));
+    stage_h2d_narrow(L.start32.get(), v.start, static_cast<size_t>(dim + 1), s);
+    PDLP_LAUNCH(pdlpk_validate_raw_layout32(L.start32.get(), dim, nullptr, 0, nnz, bound, bad, s));
   }
-  // index (int64 -> int32) in chunks to bound the staging buffer
+  // index: always 32 bits on device (bound < 2^31)
   L.index.alloc(nnz);
-  const int64_t chunk = std::min<int64_t>(nnz, int64_t(1) << 26);
-  if (chunk > 0) {
-    PDLP_CK(cudaStreamSynchronize(s));
-    tmp.alloc(chunk);
-    for (int64_t off = 0; off < nnz; off += chunk) {
-      const int64_t len = std::min(chunk, nnz - off);
-      stage_h2d(tmp.get(), v.index + off, len * 8, s);
-      PDLP_LAUNCH(pdlpk_validate_raw_layout(nullptr, 0, tmp.get(), len, nnz, bound, bad, s));
-      PDLP_LAUNCH(pdlpk_index_to_i32(tmp.get(), L.index.get() + off, len, s));
-    }
+  if (nnz > 0) {
+    stage_h2d_narrow(L.index.get(), v.index, static_cast<size_t>(nnz), s);
+    PDLP_LAUNCH(pdlpk_validate_raw_layout32(nullptr, 0, L.index.get(), nnz, nnz, bound, bad, s));
   }
   L.value_orig.alloc(nnz);
   L.value.alloc(nnz);
@@ -369,7 +429,7 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
     stage_h2d(L.value_orig.get(), v.value, nnz * 8, s);
     PDLP_CK(cudaMemcpyAsync(L.value.get(), L.value_orig.get(), nnz * 8, cudaMemcpyDeviceToDevice, s));
   }
-  PDLP_CK(cudaStreamSynchronize(s));
+  // (no sync: the host schedule build below overlaps the copies in flight)
   L.view.dim = dim;
   L.view.nnz = nnz;
   L.view.wide = wide ? 1 : 0;
@@ -378,7 +438,14 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
   L.view.index = L.index.get();
   L.view.value = L.value.get();
   L.view.value_orig = L.value_orig.get();
+  const auto ts = std::chrono::steady_clock::now();
   autotune_schedule(v.start, dim, bound, L, s);
+  if (std::getenv("PDLP_TIMING") != nullptr) {
+    PDLP_CK(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "phase=setup event=schedule lines=%lld nnz=%lld seconds=%.4f\n",
+                 static_cast<long long>(dim), static_cast<long long>(nnz),
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count());
+  }
 }
 
 DevBuf<double> upload_vec(const double* h, int64_t n, cudaStream_t s) {
@@ -660,16 +727,27 @@ class Engine {
                   int64_t e0) {
     prob_.m = m;
     prob_.n = n;
+    static const bool timing = std::getenv("PDLP_TIMING") != nullptr;
+    auto lap = [&, t = Clock::now()]() mutable {
+      if (timing) PDLP_CK(cudaStreamSynchronize(s()));
+      const auto now = Clock::now();
+      const double d = std::chrono::duration<double>(now - t).count();
+      t = now;
+      return d;
+    };
     DevBuf<unsigned long long> keys(4);
     DevBuf<unsigned> bad(1);
     PDLP_CK(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned), s()));
     upload_layout(by_row, n_glob_, bad.get(), prob_.row, s());
+    const double t_row = lap();
     upload_layout(by_col, m, bad.get(), prob_.col, s());
+    const double t_col = lap();
     prob_.c_o = upload_vec(objective, n, s());
     prob_.lc_o = upload_vec(con_lower, m, s());
     prob_.uc_o = upload_vec(con_upper, m, s());
     prob_.lv_o = upload_vec(var_lower, n, s());
     prob_.uv_o = upload_vec(var_upper, n, s());
+    const double t_vec = lap();
     // validate (problem.hpp:119-154) on device, first failure in the
     // reference's order; layouts_consistent last.
     PDLP_LAUNCH(pdlpk_validate_vectors(prob_.c_o.get(), prob_.lv_o.get(), prob_.uv_o.get(), n,
@@ -694,6 +772,7 @@ class Engine {
       if (hk[3] != none) invalid("matrix entry not finite", static_cast<int64_t>(hk[3] >> 3));
       if (hb != 0) invalid("row/column layouts disagree", -1);
     }
+    const double t_valid = lap();
     {
       const int64_t nnz = prob_.row.view.nnz;
       row_of_.alloc(nnz);
@@ -711,6 +790,7 @@ class Engine {
       if (comm_ != nullptr) hb = any_rank(hb != 0) ? 1u : 0u;
       if (hb != 0) invalid("row/column layouts disagree", -1);
     }
+    const double t_cons = lap();
     prob_.c.alloc(n);
     prob_.lc.alloc(m);
     prob_.uc.alloc(m);
@@ -742,6 +822,12 @@ class Engine {
     dev_zero(zeros_n_.get(), n, s());
     dev_zero(zeros_m_.get(), m, s());
     PDLP_CK(cudaStreamSynchronize(s()));
+    if (timing) {
+      std::fprintf(stderr,
+                   "phase=setup event=load row_layout=%.4f col_layout=%.4f vectors=%.4f "
+                   "validate=%.4f consistency=%.4f rest=%.4f\n",
+                   t_row, t_col, t_vec, t_valid, t_cons, lap());
+    }
   }
 
   ~Engine() {
@@ -1514,12 +1600,21 @@ class Engine {
       return;
     }
     const pdlpk_red r = red();
+    static const bool gap_debug = std::getenv("PDLP_GAP_DEBUG") != nullptr;
+    cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
+    if (gap_debug) {
+      for (auto& e : gev) cudaEventCreate(&e);
+      cudaEventRecord(gev[0], s());
+    }
+    const auto t_prep = Clock::now();
     for (int i = 0; i < count; ++i) {
       PDLP_LAUNCH(pdlpk_gap_prepare(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, &r,
                                     gap_work_[i].get(), islots_.get() + i, s()));
     }
+    if (gap_debug) cudaEventRecord(gev[1], s());
     PDLP_CK(cudaMemcpyAsync(host_islots_, islots_.get(), 8 * sizeof(int), cudaMemcpyDeviceToHost, s()));
     PDLP_CK(cudaStreamSynchronize(s()));
+    const auto t_fin = Clock::now();
     double qa[2] = {-1.0, -1.0}, qb[2] = {-1.0, -1.0};
     for (int i = 0; i < count; ++i) {
       const GapWindow& gw = gap_window_for(P, i);
@@ -1535,14 +1630,26 @@ class Engine {
                                    host_islots_[i], &r, gap_work_[i].get(), slot(kSlotGap + i),
                                    qa[i], qb[i], s()));
     }
+    if (gap_debug) cudaEventRecord(gev[2], s());
     const double* h = read_slots(kSlotGap + count + 2);
-    static const bool gap_debug = std::getenv("PDLP_GAP_DEBUG") != nullptr;
+    float gpu_prep = 0.f, gpu_fin = 0.f;
+    if (gap_debug) {
+      cudaEventElapsedTime(&gpu_prep, gev[0], gev[1]);
+      cudaEventElapsedTime(&gpu_fin, gev[1], gev[2]);
+      for (auto& e : gev) cudaEventDestroy(e);
+    }
     for (int i = 0; i < count; ++i) {
       out[i] = h[kSlotGap + i];
       const double hit = h[kSlotGap + 2 + i];
       if (gap_debug) {
-        std::fprintf(stderr, "gap q=%d/%d c=%p E=%d window=[%.4f,%.4f] hit=%.5f\n", i, count,
-                     static_cast<const void*>(P.c), host_islots_[i], qa[i], qb[i], hit);
+        const auto t_end = Clock::now();
+        std::fprintf(stderr,
+                     "gap q=%d/%d c=%p E=%d window=[%.4f,%.4f] hit=%.5f prep=%.1fus "
+                     "finish=%.1fus (gpu span prep %.1fus, finish %.1fus)\n",
+                     i, count, static_cast<const void*>(P.c), host_islots_[i], qa[i], qb[i], hit,
+                     1e6 * std::chrono::duration<double>(t_fin - t_prep).count(),
+                     1e6 * std::chrono::duration<double>(t_end - t_fin).count(), 1e3 * gpu_prep,
+                     1e3 * gpu_fin);
       }
       GapWindow& gw = gap_window_for(P, i);
       if (qb[i] > qa[i] && hit < 1.0 && qa[i] < 0.999) {  // did the crossing fall inside?
@@ -1945,7 +2052,7 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
 }
 
 void copy_to_host(double* dst, const double* src, int64_t n, cudaStream_t s) {
-  if (dst != nullptr && n > 0) PDLP_CK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToHost, s));
+  if (dst != nullptr && n > 0) stage_d2h(dst, src, static_cast<size_t>(n) * 8, s);
 }
 
 // solve (solver.hpp:535-608)
@@ -2015,6 +2122,8 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
   E.profile_ = o->profile_kernels != 0;
   E.timing_warmup_ = std::max<int64_t>(0, o->timing_warmup_iterations);
   const auto loop_t0 = Clock::now();
+  const double prep_seconds = std::chrono::duration<double>(loop_t0 - t0).count() -
+                              E.upload_seconds_ - E.precondition_seconds_;
   const int status = E.run_inner(P, P, cfg, D);
   E.timed_end_.record(E.s());
   PDLP_CK(cudaStreamSynchronize(E.s()));
@@ -2042,6 +2151,7 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
     copy_to_host(host, full, col_side ? E.n_glob_ : E.m_glob_, E.s());
     PDLP_CK(cudaStreamSynchronize(E.s()));
   };
+  const auto results_t0 = Clock::now();
   out_vec(res->x, D.sol_x.get(), true);
   out_vec(res->y, D.sol_y.get(), false);
   out_vec(res->reduced_costs, D.sol_r.get(), true);
@@ -2092,11 +2202,12 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
     std::fprintf(stderr,
                  "phase=main event=timing solve=%.4f upload=%.4f precondition=%.4f loop=%.4f "
                  "steps=%.4f cadence=%.4f gap=%.4f gap_windows=%lld/%lld polish=%.4f "
-                 "alloc=%.4f\n",
+                 "alloc=%.4f prep=%.4f results=%.4f\n",
                  res->solve_seconds, res->upload_seconds, res->precondition_seconds,
                  res->loop_seconds, res->step_seconds, E.cadence_seconds_, E.gap_seconds_,
                  static_cast<long long>(wd), static_cast<long long>(wt), E.polish_seconds_,
-                 g_alloc_seconds);
+                 g_alloc_seconds, prep_seconds,
+                 std::chrono::duration<double>(Clock::now() - results_t0).count());
   }
 }
 
