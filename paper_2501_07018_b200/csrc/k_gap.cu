@@ -237,22 +237,25 @@ __device__ __forceinline__ Coord gap_coord(const GapIn& g, int64_t t) {
   return o;
 }
 
-__global__ void events_kernel(GapIn g, Work w) {
-  GRID_STRIDE(t, g.n + g.m) {
-    const Coord o = gap_coord(g, t);
-    const int64_t s0 = t < g.n ? t : g.n + 2 * (t - g.n);
-    const int slots = t < g.n ? 1 : 2;
-    for (int e = 0; e < slots; ++e) {
-      const int64_t s = s0 + e;
-      const bool valid = e < o.ne;
-      w.flag[s] = valid ? 1 : 0;
-      if (valid) {
-        w.lam[s] = e == 0 ? o.lam0 : o.lam1;
-        w.dc[s] = e == 0 ? o.dc0 : o.dc1;
-        w.di[s] = e == 0 ? o.di0 : o.di1;
-      }
+// Breakpoint events of coordinate t into its slot(s).
+__device__ __forceinline__ void write_events(const GapIn& g, const Work& w, int64_t t,
+                                             const Coord& o) {
+  const int64_t s0 = t < g.n ? t : g.n + 2 * (t - g.n);
+  const int slots = t < g.n ? 1 : 2;
+  for (int e = 0; e < slots; ++e) {
+    const int64_t s = s0 + e;
+    const bool valid = e < o.ne;
+    w.flag[s] = valid ? 1 : 0;
+    if (valid) {
+      w.lam[s] = e == 0 ? o.lam0 : o.lam1;
+      w.dc[s] = e == 0 ? o.dc0 : o.dc1;
+      w.di[s] = e == 0 ? o.di0 : o.di1;
     }
   }
+}
+
+__global__ void events_kernel(GapIn g, Work w) {
+  GRID_STRIDE(t, g.n + g.m) write_events(g, w, t, gap_coord(g, t));
 }
 
 __global__ void keys_kernel(Work w, int64_t E) {
@@ -531,17 +534,32 @@ extern "C" int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const 
   const int64_t n = P->n, m = P->m, N = n + 2 * m;
   Work w = carve(work, n, m);
   const GapIn g = make_in(P, x, y, ax, aty, omega);
-  auto fm = [g] __device__(int64_t t, double* v) -> unsigned {
-    const Coord o = gap_coord(g, t);
-    v[0] = o.b;
-    v[1] = o.c;
-    return o.mass_use;
-  };
-  int rc = multi_reduce<2>(fm, n + m, red->parity ? PDLPK_RED_SEQ : PDLPK_RED_TREE, red->shards, 0u,
-                           red->scratch, w.sc->sums, s);
+  int rc;
+  if (red->parity) {
+    // the lambda -> inf masses in the reference's order (one thread), then
+    // the events in parallel
+    auto fm = [g] __device__(int64_t t, double* v) -> unsigned {
+      const Coord o = gap_coord(g, t);
+      v[0] = o.b;
+      v[1] = o.c;
+      return o.mass_use;
+    };
+    rc = multi_reduce<2>(fm, n + m, PDLPK_RED_SEQ, red->shards, 0u, red->scratch, w.sc->sums, s);
+    if (rc == 0 && N > 0) events_kernel<<<ew_blocks(n + m), kT, 0, s>>>(g, w);
+  } else {
+    // one pass: the tree reduction visits every coordinate once and writes
+    // its events on the way
+    auto fe = [g, w] __device__(int64_t t, double* v) -> unsigned {
+      const Coord o = gap_coord(g, t);
+      write_events(g, w, t, o);
+      v[0] = o.b;
+      v[1] = o.c;
+      return o.mass_use;
+    };
+    rc = multi_reduce<2>(fe, n + m, PDLPK_RED_TREE, red->shards, 0u, red->scratch, w.sc->sums, s);
+  }
   if (rc != 0) return rc;
   if (N > 0) {
-    events_kernel<<<ew_blocks(n + m), kT, 0, s>>>(g, w);
     size_t bytes = w.cub_bytes;
     const cudaError_t e = cub::DeviceSelect::Flagged(w.cub_tmp, bytes, thrust::counting_iterator<int32_t>(0),
                                                      w.flag, w.sel, &w.sc->num_events,
