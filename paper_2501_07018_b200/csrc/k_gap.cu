@@ -381,8 +381,10 @@ __global__ void __launch_bounds__(kT) window_flags_kernel(Work w, int64_t E) {
 }
 
 __global__ void base_window_kernel(Work w) {
-  w.sc->base[0] = w.sc->sums[1] + w.sc->above[0];
-  w.sc->base[1] = w.sc->sums[0] + w.sc->above[1];
+  // nothing above (a top window): exactly the full sort's start
+  const bool none = w.sc->above_count == 0;
+  w.sc->base[0] = none ? w.sc->sums[1] : w.sc->sums[1] + w.sc->above[0];
+  w.sc->base[1] = none ? w.sc->sums[0] : w.sc->sums[0] + w.sc->above[1];
   w.sc->base[2] = w.sc->above_count > 0 ? key_value(w.sc->above_min) : CUDART_INF;
 }
 

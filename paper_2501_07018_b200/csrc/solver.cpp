@@ -197,8 +197,9 @@ void for_segments(int64_t dim, int parts, F&& f) {
 void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
                     int64_t short_max = PDLPK_SHORT_MAX, int32_t budget = 0) {
   if (budget <= 0) budget = pdlpk_stage_budget(PDLPK_TILE_NNZ);
-  const int parts = static_cast<int>(std::clamp<int64_t>(
+  int parts = static_cast<int>(std::clamp<int64_t>(
       dim / (int64_t(1) << 18), 1, std::max(1u, std::min(16u, std::thread::hardware_concurrency()))));
+  if (const char* e = std::getenv("PDLP_SCHED_THREADS")) parts = std::max(1, std::atoi(e));
   std::vector<SchedPart> seg(static_cast<size_t>(parts));
   const bool direct = direct_tiles(start, dim);
   int32_t shape_lines = PDLPK_TILE_ROWS, shape_nnz = PDLPK_TILE_NNZ, stage_bytes = budget;
@@ -226,18 +227,29 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
   const int64_t tile_rows = direct ? 256 : shape_lines;
   const int64_t tile_nnz = direct ? 256 * PDLPK_SHORT_MAX : shape_nnz;
   if (direct) short_max = PDLPK_SHORT_MAX;
-  for_segments(dim, parts, [&](int q, int64_t lo, int64_t hi) {
+  // Segment boundaries on multiples of the tile's line count (uniform
+  // layouts then re-synchronize at once, see the splice below).
+  std::vector<int64_t> bnd(static_cast<size_t>(parts) + 1);
+  for (int q = 0; q <= parts; ++q) {
+    const int64_t raw = dim * q / parts;
+    bnd[q] = q == parts ? dim : std::min<int64_t>(dim, raw / tile_rows * tile_rows);
+  }
+  // open tile of the greedy tiling: lines [r0, r0 + rows) with nnz entries
+  struct Open {
+    int64_t r0 = -1, rows = 0, nnz = 0;
+  };
+  std::vector<Open> tail(static_cast<size_t>(parts));
+  for_segments(dim, parts, [&](int q, int64_t, int64_t) {
+    const int64_t lo = bnd[q], hi = bnd[q + 1];
     SchedPart& g = seg[q];
-    int64_t cur0 = -1, cur_rows = 0, cur_nnz = 0;
+    Open o;
     auto close = [&] {
-      if (cur_rows > 0) {
-        g.t0.push_back(static_cast<int32_t>(cur0));
-        g.tc.push_back(static_cast<int32_t>(cur_rows | (cur_nnz << 12)));
-        g.tn.push_back(start[cur0]);
+      if (o.rows > 0) {
+        g.t0.push_back(static_cast<int32_t>(o.r0));
+        g.tc.push_back(static_cast<int32_t>(o.rows | (o.nnz << 12)));
+        g.tn.push_back(start[o.r0]);
       }
-      cur0 = -1;
-      cur_rows = 0;
-      cur_nnz = 0;
+      o = Open{};
     };
     for (int64_t r = lo; r < hi; ++r) {
       const int64_t len = start[r + 1] - start[r];
@@ -270,24 +282,73 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
         }
         continue;
       }
-      if (cur_rows == tile_rows || cur_nnz + len > tile_nnz) close();
-      if (cur_rows == 0) cur0 = r;
-      ++cur_rows;
-      cur_nnz += len;
+      if (o.rows == tile_rows || o.nnz + len > tile_nnz) close();
+      if (o.rows == 0) o.r0 = r;
+      ++o.rows;
+      o.nnz += len;
     }
-    close();
+    tail[q] = o;  // left open: the next segment may extend it
   });
-  // join in line order: tiles, warp chunks, then every CTA chunk
-  std::vector<int32_t> t0, tc, ck_row, ck_len, ck_pos, ck_slot;
-  std::vector<int64_t> tn, ck_beg;
+  // Splice the speculative tilings into exactly the sequential greedy one:
+  // the open tile carried out of segment q-1 is extended through segment q
+  // until the greedy starts a tile where segment q's own run started one (or
+  // a non-tiled line closes both); from there segment q's tiles are exact.
+  std::vector<int32_t> t0, tc;
+  std::vector<int64_t> tn;
+  {
+    Open carry;
+    auto emit = [&](const Open& o) {
+      if (o.rows > 0) {
+        t0.push_back(static_cast<int32_t>(o.r0));
+        tc.push_back(static_cast<int32_t>(o.rows | (o.nnz << 12)));
+        tn.push_back(start[o.r0]);
+      }
+    };
+    for (int q = 0; q < parts; ++q) {
+      const SchedPart& g = seg[q];
+      const int64_t lo = bnd[q], hi = bnd[q + 1];
+      size_t k = 0;  // first speculative tile of segment q not yet replaced
+      bool synced = carry.rows == 0;
+      for (int64_t r = lo; r < hi && !synced; ++r) {
+        const int64_t len = start[r + 1] - start[r];
+        if (len > short_max) {  // a chunked line closes the tile in both runs
+          emit(carry);
+          carry = Open{};
+          while (k < g.t0.size() && g.t0[k] <= r) ++k;
+          synced = true;
+          break;
+        }
+        if (carry.rows == tile_rows || carry.nnz + len > tile_nnz) {
+          emit(carry);
+          carry = Open{};
+          while (k < g.t0.size() && g.t0[k] < r) ++k;
+          if (k < g.t0.size() && g.t0[k] == r) {  // both runs start a tile at r
+            synced = true;
+            break;
+          }
+        }
+        if (carry.rows == 0) carry.r0 = r;
+        ++carry.rows;
+        carry.nnz += len;
+      }
+      if (!synced) continue;  // the carry spans the whole segment
+      for (; k < g.t0.size(); ++k) {
+        t0.push_back(g.t0[k]);
+        tc.push_back(g.tc[k]);
+        tn.push_back(g.tn[k]);
+      }
+      carry = tail[q];
+    }
+    emit(carry);
+  }
+  // join in line order: warp chunks, then every CTA chunk
+  std::vector<int32_t> ck_row, ck_len, ck_pos, ck_slot;
+  std::vector<int64_t> ck_beg;
   std::vector<int32_t> cc_row, cc_len, cc_pos, cc_slot;
   std::vector<int64_t> cc_beg;
   int64_t n_multi = 0;
   auto append = [](auto& dst, const auto& src) { dst.insert(dst.end(), src.begin(), src.end()); };
   for (SchedPart& g : seg) {
-    append(t0, g.t0);
-    append(tc, g.tc);
-    append(tn, g.tn);
     append(ck_row, g.ck_row);
     append(ck_beg, g.ck_beg);
     append(ck_len, g.ck_len);
@@ -1618,11 +1679,17 @@ class Engine {
     double qa[2] = {-1.0, -1.0}, qb[2] = {-1.0, -1.0};
     for (int i = 0; i < count; ++i) {
       const GapWindow& gw = gap_window_for(P, i);
-      if (!gap_partial_off_ && gw.depth >= 1.0) {
+      // Default: windows from the top only, whose gap is bit-identical to
+      // the full sort's (nothing is summed outside the sorted order), so the
+      // gap stays a function of its inputs.  PDLP_GAP_WINDOWS=any also
+      // places windows mid-depth and at the bottom (faster for deep or
+      // absent crossings; the masses above such a window are tree-summed,
+      // which changes the gap's last bits).
+      if (!gap_partial_off_ && gw.depth >= 1.0 && gap_any_window_) {
         qa[i] = 0.9995;  // no crossing last time: only the last ~0.05 % sorted
         qb[i] = 1.0;
-      } else if (!gap_partial_off_ && gw.depth >= 0.0) {
-        qa[i] = std::max(0.0, gw.depth - gw.half);
+      } else if (!gap_partial_off_ && gw.depth >= 0.0 && gw.depth < 1.0) {
+        qa[i] = gap_any_window_ ? std::max(0.0, gw.depth - gw.half) : 0.0;
         qb[i] = std::min(1.0, gw.depth + gw.half);
       }
       const double radius = std::sqrt(omega * q[i].dx2 + q[i].dy2 / omega);
@@ -1747,6 +1814,10 @@ class Engine {
   bool gap_shared_ = false;  // one gap buffer, queries evaluated one at a time
   std::map<std::pair<const void*, int>, GapWindow> gap_windows_;
   // PDLP_GAP_PARTIAL=0: always the full sort (measurements)
+  bool gap_any_window_ = [] {
+    const char* e = std::getenv("PDLP_GAP_WINDOWS");
+    return e != nullptr && std::strcmp(e, "any") == 0;
+  }();
   bool gap_partial_off_ = [] {
     const char* e = std::getenv("PDLP_GAP_PARTIAL");
     return e != nullptr && e[0] == '0';

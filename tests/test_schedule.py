@@ -1,0 +1,47 @@
+"""The SpMV schedule (tiles, warp lines, CTA chunks) built by host threads
+equals the sequential greedy build: perf-mode iterates depend on the tiling
+through the per-CTA partial sums of the step reductions, so solves with one
+and with many schedule threads must agree bit for bit."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2501_07018_b200 as P
+
+
+def _mixed_lp(seed: int, rows: int, cols: int):
+    """Columns of mixed lengths: mostly 1-3 entries (tiled), some ~100
+    (warp lines) and a few ~3000 (CTA chunks) -- every segment kind, with
+    enough lines (>= 2^19) for the threaded build to split them."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, 4, cols)
+    lens[rng.choice(cols, 300, replace=False)] = 100
+    lens[rng.choice(cols, 5, replace=False)] = 3000
+    c = np.repeat(np.arange(cols), lens)
+    r = rng.integers(0, rows, c.size)
+    v = rng.uniform(-1, 1, c.size)
+    key = r.astype(np.int64) * cols + c
+    _, first = np.unique(key, return_index=True)
+    r, c, v = r[first], c[first], v[first]
+    trip = list(zip(r.tolist(), c.tolist(), v.tolist()))
+    xs = rng.uniform(0, 1, cols)
+    A = np.zeros(rows)
+    np.add.at(A, r, v * xs[c])
+    return P.problem(rows, cols, trip, rng.normal(size=cols), A - 1.0, A + 1.0,
+                     np.zeros(cols), np.full(cols, 5.0))
+
+
+@pytest.mark.gpu
+def test_threaded_schedule_equals_sequential(gpu, monkeypatch):
+    cases = [P.generate("c1", 0, sources=1100, sinks=1000), _mixed_lp(3, 20000, 700000)]
+    for p in cases:
+        o = P.SolverOptions(mode="perf", iteration_limit=300,
+                            tolerances=P.TerminationTolerances(0.0, 0.0, 0.0))
+        monkeypatch.setenv("PDLP_SCHED_THREADS", "1")
+        a = P.solve(p, o)
+        monkeypatch.setenv("PDLP_SCHED_THREADS", "7")
+        b = P.solve(p, o)
+        assert a.iterations == b.iterations == 300
+        np.testing.assert_array_equal(a.x.view(np.int64), b.x.view(np.int64))
+        np.testing.assert_array_equal(a.y.view(np.int64), b.y.view(np.int64))
