@@ -255,9 +255,14 @@ def run_ours(args) -> None:
     attempt_s = total_kernel_s / attempts_prof
 
     # time to BASELINE's 1e-4 relative KKT (SURVEY §8(d) mapping), polishing on
+    # Run twice: the first solve in a process that polishes maps the polishing
+    # states' memory (0.01-0.3 s on a freshly acquired box); the second is
+    # the warm number reported, the first is kept as cold_seconds.
     tol = P.relative_tolerances(p)
-    ttt = solve(P.SolverOptions(tolerances=P.TerminationTolerances(*tol),
-                                iteration_limit=100000, device=device))
+    ttt_opts = P.SolverOptions(tolerances=P.TerminationTolerances(*tol), iteration_limit=100000,
+                               device=device)
+    ttt_cold = solve(ttt_opts)
+    ttt = solve(ttt_opts)
 
     if rank != 0:
         if dist is not None:
@@ -303,6 +308,7 @@ def run_ours(args) -> None:
                         "loop_seconds": ttt.loop_seconds, "step_seconds": ttt.step_seconds,
                         "upload_seconds": ttt.upload_seconds, "iterations": ttt.iterations,
                         "polish_iterations": ttt.polish_iterations,
+                        "cold_seconds": ttt_cold.solve_seconds,
                         "tolerance": "1e-4 relative (eps_p=1e-4(1+|b|inf), eps_d=1e-4(1+|c|inf))"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),

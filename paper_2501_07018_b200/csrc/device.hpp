@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstddef>
 #include <cstdint>
 #include <stdexcept>
@@ -100,7 +102,12 @@ class DevBuf {
     } else {
       PDLP_CK(cudaMalloc(&p, n * sizeof(T) + 16));
     }
-    g_alloc_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    g_alloc_seconds += dt;
+    static const bool debug = std::getenv("PDLP_ALLOC_DEBUG") != nullptr;
+    if (debug && dt > 2e-3) {
+      std::fprintf(stderr, "alloc %.1f MB took %.1f ms\n", n * sizeof(T) / 1048576.0, 1e3 * dt);
+    }
     p_ = static_cast<T*>(p);
   }
   void release() {

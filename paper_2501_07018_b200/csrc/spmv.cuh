@@ -89,8 +89,6 @@ __host__ __device__ inline int stage_nnz_for(int L, size_t budget) {
   return lo;
 }
 constexpr int kStages = PDLPK_TILE_STAGES;  // ring depth: tiles in flight per CTA
-// Ring header: full/empty mbarriers, then one TileHdr per stage.
-constexpr size_t kRingHeader = 128;
 // What the consumers of a stage need about its tile, written by the producer
 // lane (which computes it anyway for the bulk copies) before its arrive on
 // full[stage]: the consumers read 32 bytes instead of re-deriving the tile's
@@ -102,7 +100,9 @@ struct TileHdr {
   int32_t per;       // lines per consumer warp
   int32_t pad;
 };
-static_assert(2 * 8 * kStages + sizeof(TileHdr) * kStages <= kRingHeader, "ring header");
+// Ring header: full/empty mbarriers, then one TileHdr per stage (128-byte
+// aligned so every stage buffer stays aligned for the bulk copies).
+constexpr size_t kRingHeader = (2 * 8 * kStages + sizeof(TileHdr) * kStages + 127) / 128 * 128;
 // Dynamic shared memory of a layout's staged ring (its stage size is chosen
 // per layout, see solver.cpp build_schedule).
 __host__ __device__ inline size_t ring_smem(const pdlpk_csr& A) {
