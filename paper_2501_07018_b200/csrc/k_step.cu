@@ -220,6 +220,8 @@ struct RowEpi {
   __device__ __forceinline__ Pre load(int64_t r) const { return {y[r], lc[r], uc[r]}; }
   // per-line operands the tile path stages with bulk copies
   static constexpr int kStaged = 3;
+  // y, l_c, u_c: not read again before they would leave L2 anyway
+  __device__ __forceinline__ bool staged_reused(int) const { return false; }
   __device__ __forceinline__ const double* staged_src(int q) const {
     return q == 0 ? y : (q == 1 ? lc : uc);
   }
@@ -284,6 +286,8 @@ struct ColEpi {
   };
   __device__ __forceinline__ Pre load(int64_t i) const { return {aty[i], x[i], xn[i]}; }
   static constexpr int kStaged = 3;
+  // aty and x are dead after this pass; x' is the next primal pass's x
+  __device__ __forceinline__ bool staged_reused(int q) const { return q == 2; }
   __device__ __forceinline__ const double* staged_src(int q) const {
     return q == 0 ? aty : (q == 1 ? x : xn);
   }

@@ -53,6 +53,7 @@ struct StoreEpi {
   __device__ __forceinline__ Pre load(int64_t) const { return {}; }
   static constexpr int kStaged = 0;
   __device__ __forceinline__ const double* staged_src(int) const { return nullptr; }
+  __device__ __forceinline__ bool staged_reused(int) const { return false; }
   __device__ __forceinline__ Pre from_stage(const double* const*, int) const { return {}; }
   __device__ __forceinline__ void reset_acc() {}
   __device__ __forceinline__ void export_acc(double*) const {}

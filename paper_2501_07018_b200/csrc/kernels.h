@@ -93,6 +93,9 @@ typedef struct pdlpk_csr {
 #ifndef PDLPK_XBAR_KEEP
 #define PDLPK_XBAR_KEEP 1
 #endif
+#ifndef PDLPK_MATRIX_EVICT_FIRST
+#define PDLPK_MATRIX_EVICT_FIRST 1
+#endif
 #ifndef PDLPK_XBAR_KEEP_MB
 #define PDLPK_XBAR_KEEP_MB 48
 #endif

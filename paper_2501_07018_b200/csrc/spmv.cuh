@@ -436,12 +436,26 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
           hdr[stage] = h;  // released by the arrive below
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&full[stage], total);
+#if PDLPK_MATRIX_EVICT_FIRST
+          const uint64_t pol = l2_evict_first_policy();
+          if (wi.bytes) bulk_g2s_hint(buf, wi.src, wi.bytes, &full[stage], pol);
+          if (wv.bytes) bulk_g2s_hint(buf + sl.val, wv.src, wv.bytes, &full[stage], pol);
+          if (wp.bytes) bulk_g2s_hint(buf + sl.ptr, wp.src, wp.bytes, &full[stage], pol);
+#else
           if (wi.bytes) bulk_g2s(buf, wi.src, wi.bytes, &full[stage]);
           if (wv.bytes) bulk_g2s(buf + sl.val, wv.src, wv.bytes, &full[stage]);
           if (wp.bytes) bulk_g2s(buf + sl.ptr, wp.src, wp.bytes, &full[stage]);
+#endif
 #pragma unroll
           for (int q = 0; q < Epi::kStaged; ++q) {
             if (we[q].bytes) {
+#if PDLPK_MATRIX_EVICT_FIRST
+              if (!epi.staged_reused(q)) {
+                bulk_g2s_hint(buf + sl.epi + q * sl.epi_stride, we[q].src, we[q].bytes,
+                              &full[stage], pol);
+                continue;
+              }
+#endif
               bulk_g2s(buf + sl.epi + q * sl.epi_stride, we[q].src, we[q].bytes, &full[stage]);
             }
           }

@@ -54,6 +54,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// L2 evict-first policy for data read once per pass.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// Same, with an L2 cache-policy hint (a matrix stream, read once per pass:
+// evict_first keeps it from pushing out the vector the consumers gather from
+// and the operands the next pass reads).
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // Stage elements [first, first + count) of a global array into shared memory
 // with one bulk copy: the byte range is widened to 16-byte boundaries (every
 // device array is allocated with >= 16 bytes of tail padding), and the
