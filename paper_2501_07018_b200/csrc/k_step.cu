@@ -94,7 +94,11 @@ __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a, pdl
     xb.x = 2.0 * xp.x - xi.x;
     xb.y = 2.0 * xp.y - xi.y;
 #if PDLPK_XBAR_KEEP
+#if PDLPK_XN_STREAM
     __stcs(xn2 + p, xp);
+#else
+    xn2[p] = xp;
+#endif
     st_keep(xb2 + p, xb, pol);
 #else
     xn2[p] = xp;

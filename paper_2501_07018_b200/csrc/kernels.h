@@ -93,6 +93,9 @@ typedef struct pdlpk_csr {
 #ifndef PDLPK_XBAR_KEEP
 #define PDLPK_XBAR_KEEP 1
 #endif
+#ifndef PDLPK_XN_STREAM
+#define PDLPK_XN_STREAM 1
+#endif
 #ifndef PDLPK_MATRIX_EVICT_FIRST
 #define PDLPK_MATRIX_EVICT_FIRST 1
 #endif
