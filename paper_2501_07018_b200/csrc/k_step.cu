@@ -217,6 +217,7 @@ struct RowEpi {
   double* __restrict__ sy;
   double sigma, w;
   bool pend;
+  uint64_t keep = 0;  // L2 evict_last policy for dy (gathered by the column pass)
   double dy2 = 0.0, infy = 0.0;
   struct Pre {
     double y, lc, uc;
@@ -245,7 +246,11 @@ struct RowEpi {
     const double yp = yhat - sigma * proj;  // exact cancellation: no FMA (step.hpp:85)
     yn[r] = yp;
     const double d = yp - yr;
+#if PDLPK_DY_KEEP
+    st_keep(dy + r, d, keep);
+#else
     dy[r] = d;
+#endif
     if (pend) sy[r] = sy[r] + w * yr;
     dy2 += d * d;
     infy = max_keep(infy, fabs(yp));
@@ -265,6 +270,10 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) row_pass(p
   e.uc = a.P.uc;
   e.sy = a.sum_y;
   e.sigma = st->eta * st->omega;
+#if PDLPK_DY_KEEP
+  e.keep = l2_keep_policy(fminf(1.0f, static_cast<float>(PDLPK_XBAR_KEEP_MB * 1048576.0 /
+                                                         (8.0 * static_cast<double>(a.P.m > 0 ? a.P.m : 1)))));
+#endif
   e.pend = st->avg_pending != 0;
   e.w = st->avg_w;
   sched_spmv<P, Seg>(a.P.K, a.P.K.value, a.xbar, e);
@@ -591,6 +600,10 @@ __global__ void __launch_bounds__(kEwThreads) row_epi_kernel(pdlpk_step_args a, 
   e.uc = a.P.uc;
   e.sy = a.sum_y;
   e.sigma = st->eta * st->omega;
+#if PDLPK_DY_KEEP
+  e.keep = l2_keep_policy(fminf(1.0f, static_cast<float>(PDLPK_XBAR_KEEP_MB * 1048576.0 /
+                                                         (8.0 * static_cast<double>(a.P.m > 0 ? a.P.m : 1)))));
+#endif
   e.pend = st->avg_pending != 0;
   e.w = st->avg_w;
   const int64_t m = a.P.m;

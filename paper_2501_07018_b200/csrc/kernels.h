@@ -93,6 +93,9 @@ typedef struct pdlpk_csr {
 #ifndef PDLPK_XBAR_KEEP
 #define PDLPK_XBAR_KEEP 1
 #endif
+#ifndef PDLPK_DY_KEEP
+#define PDLPK_DY_KEEP 0
+#endif
 #ifndef PDLPK_XN_STREAM
 #define PDLPK_XN_STREAM 1
 #endif
