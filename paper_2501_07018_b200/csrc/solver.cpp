@@ -418,8 +418,31 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
 // 2.8 vs 3.5 ms at 64), so a large layout times one product per candidate at
 // setup and keeps the fastest; small layouts use 64.
 // PDLP_SHORT_MAX=<n> forces a threshold.
+// start[0] == 0, non-decreasing, start[dim] == nnz (what the schedule build
+// relies on; the device validation reports the reference's message).
+bool starts_valid(const int64_t* start, int64_t dim, int64_t nnz) {
+  if (start[0] != 0 || start[dim] != nnz) return false;
+  const int parts = static_cast<int>(std::clamp<int64_t>(dim / (int64_t(1) << 18), 1, 16));
+  std::vector<uint8_t> ok(static_cast<size_t>(parts), 1);
+  for_segments(dim, parts, [&](int q, int64_t lo, int64_t hi) {
+    for (int64_t r = lo; r < hi; ++r) {
+      if (start[r + 1] < start[r]) {
+        ok[q] = 0;
+        return;
+      }
+    }
+  });
+  return std::all_of(ok.begin(), ok.end(), [](uint8_t v) { return v != 0; });
+}
+
+// bad: the device validation flags of this upload; autotuning runs products
+// on the layout, so only after they are known clean.
 int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t operand_len, DevLayout& L,
-                          cudaStream_t s) {
+                          cudaStream_t s, const unsigned* bad) {
+  if (!starts_valid(start, dim, L.view.nnz)) {
+    build_schedule(start, 0, L, PDLPK_SHORT_MAX);  // empty: validation throws before use
+    return PDLPK_SHORT_MAX;
+  }
   const char* env = std::getenv("PDLP_SHORT_MAX");
   if (env != nullptr && std::atoi(env) > 0) {
     const int64_t t = std::atoi(env);
@@ -430,6 +453,15 @@ int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t operand_len
   if (L.view.nnz < (int64_t(16) << 20) || L.view.tile_direct) {
     build_schedule(start, dim, L, kDefault);
     return kDefault;
+  }
+  {
+    unsigned hb = 0;
+    PDLP_CK(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s));
+    PDLP_CK(cudaStreamSynchronize(s));
+    if (hb != 0) {  // an index out of range: no products on this layout
+      build_schedule(start, dim, L, kDefault);
+      return kDefault;
+    }
   }
   // candidates: tile line threshold x ring-stage budget (entries of a
   // PDLPK_TILE_ROWS-line stage); the budget sets both the tile shape and how
@@ -500,7 +532,7 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
   L.view.value = L.value.get();
   L.view.value_orig = L.value_orig.get();
   const auto ts = std::chrono::steady_clock::now();
-  autotune_schedule(v.start, dim, bound, L, s);
+  autotune_schedule(v.start, dim, bound, L, s, bad);
   if (std::getenv("PDLP_TIMING") != nullptr) {
     PDLP_CK(cudaStreamSynchronize(s));
     std::fprintf(stderr, "phase=setup event=schedule lines=%lld nnz=%lld seconds=%.4f\n",

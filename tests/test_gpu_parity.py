@@ -379,6 +379,18 @@ def _tamper(kind):
         k = L.start[r]
         L.index[k], L.index[k + 1] = L.index[k + 1], L.index[k]
         L.value[k], L.value[k + 1] = L.value[k + 1], L.value[k]
+    elif kind == "index_wraps":  # 2^32 + 5 would truncate to a valid 5
+        p.a.by_row.index[3] = (1 << 32) + 5
+    elif kind == "index_huge":
+        p.a.by_col.index[1] = (1 << 40)
+    elif kind == "index_negative":
+        p.a.by_row.index[2] = -7
+    elif kind == "start_wraps":
+        p.a.by_col.start[5] = (1 << 32) + int(p.a.by_col.start[5])
+    elif kind == "index_wraps_staged":  # > 1 MB of indices: the pinned-ring path
+        p = P.generate("c0", 1, rows=7000, cols=14000)
+        assert p.a.nonzeros() * 8 > (1 << 20)
+        p.a.by_row.index[p.a.nonzeros() - 2] = (1 << 32) + 1
     elif kind == "first_of_many":
         p.var_lower[20], p.var_upper[20] = 3.0, 1.0
         p.var_upper[8] = nan
@@ -398,6 +410,22 @@ def test_validation_messages_match_reference(gpu, ref, kind):
     with pytest.raises(ValueError) as theirs:
         ref.solve(p)
     assert str(ours.value) == str(theirs.value)
+
+
+@pytest.mark.parametrize("kind", ["index_wraps", "index_huge", "index_negative", "start_wraps",
+                                  "index_wraps_staged"])
+def test_out_of_range_layout_values_are_rejected(gpu, ref, kind):
+    """Indices and line starts far outside the problem (beyond int32, where a
+    plain narrowing would wrap them into range; negative) are rejected with
+    the reference's layout error.  The compiled reference itself indexes with
+    such values before validating and crashes, so the expected message is
+    the one it gives for an index just past the last column."""
+    with pytest.raises(ValueError) as theirs:
+        ref.solve(_tamper("layout_index"))
+    want = str(theirs.value)
+    with pytest.raises(ValueError) as ours:
+        P.solve(_tamper(kind))
+    assert str(ours.value) == want
 
 
 def test_perf_mode_deterministic_on_skewed_instance(gpu, ref):
