@@ -14,8 +14,17 @@ namespace pdlp_host {
 namespace {
 
 constexpr size_t kDirectMax = size_t(1) << 20;  // below this: plain cudaMemcpyAsync
-constexpr size_t kChunk = size_t(8) << 20;      // bytes per ring slot
-constexpr int kSlots = 6;                       // ring depth
+#ifndef PDLPH_STAGE_CHUNK_MB
+#define PDLPH_STAGE_CHUNK_MB 8
+#endif
+#ifndef PDLPH_STAGE_SLOTS
+#define PDLPH_STAGE_SLOTS 6
+#endif
+#ifndef PDLPH_STAGE_THREADS
+#define PDLPH_STAGE_THREADS 12
+#endif
+constexpr size_t kChunk = size_t(PDLPH_STAGE_CHUNK_MB) << 20;  // bytes per ring slot
+constexpr int kSlots = PDLPH_STAGE_SLOTS;                      // ring depth
 constexpr size_t kMinPart = size_t(256) << 10;  // smallest per-thread memcpy
 
 // Fixed pool of memcpy workers; run() splits one chunk copy across them and
@@ -24,7 +33,7 @@ class CopyPool {
  public:
   CopyPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const int workers = static_cast<int>(std::min(12u, hw)) - 1;
+    const int workers = static_cast<int>(std::min<unsigned>(PDLPH_STAGE_THREADS, hw)) - 1;
     for (int i = 0; i < workers; ++i) threads_.emplace_back([this, i] { loop(i + 1); });
   }
   ~CopyPool() {

@@ -320,15 +320,10 @@ __global__ void gather_masses_kernel(Work w, int64_t E) {
 
 __global__ void init_first_kernel(Work w) { w.sc->first = ~0ull; }
 
-// Partial sort: a strided sample of the keys places a threshold so that
-// about a fraction q of the events lie at or above it.
+// Window sort: a strided sample of the keys places the window's bounds at
+// depth fractions of the descending order.
 __global__ void sample_keys_kernel(Work w, int64_t E) {
   GRID_STRIDE(i, kGapSample) w.samp_in[i] = w.keys_in[(i * E) / kGapSample];
-}
-__global__ void threshold_kernel(Work w, int rank) { w.sc->thresh = w.samp_out[rank]; }
-__global__ void high_flags_kernel(Work w, int64_t E) {
-  const uint64_t t = w.sc->thresh;
-  GRID_STRIDE(i, E) w.flag[i] = w.keys_in[i] >= t ? 1 : 0;
 }
 // Position of the first crossing as a fraction of all events (1 when none):
 // the engine sizes the next partial sort from it.
