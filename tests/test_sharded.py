@@ -276,6 +276,7 @@ def test_peer_read_epilogue_matches_reduce_scatter(gpu, monkeypatch, world):
     products, both polishing subproblems and the final verification."""
     cases = [(P.generate("c0", 3), {}), (P.generate("c1", 3, sources=45, sinks=55), {}),
              (P.generate("c0", 4), {"enable_polish": False, "iteration_limit": 700})]
+    polished = []
     for p, kw in cases:
         tol = P.relative_tolerances(p, 1e-4)
         o = _opts(tolerances=P.TerminationTolerances(*tol), **kw)
@@ -288,3 +289,7 @@ def test_peer_read_epilogue_matches_reduce_scatter(gpu, monkeypatch, world):
             (b.iterations, b.polish_iterations, b.restarts)
         np.testing.assert_array_equal(a.x, b.x)
         np.testing.assert_array_equal(a.y, b.y)
+        polished.append(b.polish_iterations)
+    # the transport case polishes: both subproblems (the dual one reads the
+    # partial products in its row epilogue) ran over the peer exchange
+    assert polished[1] > 0
