@@ -1693,6 +1693,29 @@ class Engine {
       return;
     }
     const pdlpk_red r = red();
+    // Two queries (current and average): the second runs on a side stream
+    // with its own reduction scratch, so their chains of small, latency-bound
+    // kernels overlap.  Same kernels and order per query: same values.
+    const bool two = count == 2 && !gap_serial_;
+    pdlpk_red r2 = r;
+    if (two) {
+      if (!gap_side_) {  // created here: the engine's device is current
+        gap_side_ = std::make_unique<Stream>();
+        gap_fork_ = std::make_unique<Event>();
+        gap_join_ = std::make_unique<Event>();
+        gap_scratch2_.alloc(red_scratch_.size());
+      }
+      r2.scratch = gap_scratch2_.get();
+      gap_fork_->record(s());
+      PDLP_CK(cudaStreamWaitEvent(gap_side_->get(), gap_fork_->get(), 0));
+    }
+    auto qs = [&](int i) { return two && i == 1 ? gap_side_->get() : s(); };
+    auto qr = [&](int i) { return two && i == 1 ? &r2 : &r; };
+    auto join = [&] {
+      if (!two) return;
+      gap_join_->record(gap_side_->get());
+      PDLP_CK(cudaStreamWaitEvent(s(), gap_join_->get(), 0));
+    };
     static const bool gap_debug = std::getenv("PDLP_GAP_DEBUG") != nullptr;
     cudaEvent_t gev[3] = {nullptr, nullptr, nullptr};
     if (gap_debug) {
@@ -1701,9 +1724,10 @@ class Engine {
     }
     const auto t_prep = Clock::now();
     for (int i = 0; i < count; ++i) {
-      PDLP_LAUNCH(pdlpk_gap_prepare(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, &r,
-                                    gap_work_[i].get(), islots_.get() + i, s()));
+      PDLP_LAUNCH(pdlpk_gap_prepare(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, qr(i),
+                                    gap_work_[i].get(), islots_.get() + i, qs(i)));
     }
+    join();
     if (gap_debug) cudaEventRecord(gev[1], s());
     PDLP_CK(cudaMemcpyAsync(host_islots_, islots_.get(), 8 * sizeof(int), cudaMemcpyDeviceToHost, s()));
     PDLP_CK(cudaStreamSynchronize(s()));
@@ -1726,9 +1750,10 @@ class Engine {
       }
       const double radius = std::sqrt(omega * q[i].dx2 + q[i].dy2 / omega);
       PDLP_LAUNCH(pdlpk_gap_finish(&P, q[i].x, q[i].y, q[i].ax, q[i].aty, omega, nullptr, radius,
-                                   host_islots_[i], &r, gap_work_[i].get(), slot(kSlotGap + i),
-                                   qa[i], qb[i], s()));
+                                   host_islots_[i], qr(i), gap_work_[i].get(),
+                                   slot(kSlotGap + i), qa[i], qb[i], qs(i)));
     }
+    join();
     if (gap_debug) cudaEventRecord(gev[2], s());
     const double* h = read_slots(kSlotGap + count + 2);
     float gpu_prep = 0.f, gpu_fin = 0.f;
@@ -1845,6 +1870,14 @@ class Engine {
   DevBuf<char> gap_work_[2];
   bool gap_shared_ = false;  // one gap buffer, queries evaluated one at a time
   std::map<std::pair<const void*, int>, GapWindow> gap_windows_;
+  std::unique_ptr<Stream> gap_side_;  // second gap query's stream
+  DevBuf<double> gap_scratch2_;
+  std::unique_ptr<Event> gap_fork_, gap_join_;
+  // PDLP_GAP_SERIAL=1: both gap queries on the main stream (measurements)
+  bool gap_serial_ = [] {
+    const char* e = std::getenv("PDLP_GAP_SERIAL");
+    return e != nullptr && e[0] == '1';
+  }();
   // PDLP_GAP_PARTIAL=0: always the full sort (measurements)
   bool gap_any_window_ = [] {
     const char* e = std::getenv("PDLP_GAP_WINDOWS");
