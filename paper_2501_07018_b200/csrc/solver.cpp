@@ -1552,23 +1552,29 @@ class Engine {
   // kSlotRay + 8q hold [|ray|, changed, residual, penalty, |xc|, box, c'xc].
   // When the cone projection leaves y unchanged the cached A'y is reused
   // (the product kernel is skipped on device), which is bit-identical.
-  void enqueue_rays(const pdlpk_problem& P, Inner& D, const std::vector<RayCand>& cands) {
-    const pdlpk_red r = red();
-    for (size_t q = 0; q < cands.size(); ++q) {
+  // Candidates [q0, q1) on stream st with reduction scratch r and product
+  // temporary prod (the cadence runs the average's candidate on its side
+  // stream).
+  void enqueue_rays(const pdlpk_problem& P, Inner& D, const std::vector<RayCand>& cands,
+                    size_t q0 = 0, size_t q1 = ~size_t(0), cudaStream_t st = nullptr,
+                    const pdlpk_red* rs = nullptr, double* prod = nullptr) {
+    const pdlpk_red r = rs != nullptr ? *rs : red();
+    if (st == nullptr) st = s();
+    if (prod == nullptr) prod = D.prod_n.get();
+    for (size_t q = q0; q < std::min(q1, cands.size()); ++q) {
       double* sl = slot(kSlotRay + 8 * static_cast<int>(q));
       double* ray = D.ray_y[q].get();
-      PDLP_LAUNCH(pdlpk_ray_primal_prep(&P, 0, cands[q].y, ray, &r, sl, s()));
+      PDLP_LAUNCH(pdlpk_ray_primal_prep(&P, 0, cands[q].y, ray, &r, sl, st));
       if (cands[q].known_aty != nullptr && !dist()) {
-        PDLP_LAUNCH(pdlpk_spmv_cond(&P.KT, 0, ray, D.prod_n.get(), parity_, sl + 1, s()));
+        PDLP_LAUNCH(pdlpk_spmv_cond(&P.KT, 0, ray, prod, parity_, sl + 1, st));
       } else {
-        product(P.KT, 0, ray, D.prod_n.get());
+        product(P.KT, 0, ray, prod);  // (sharded only: always on the main stream)
       }
       // (sharded: the changed-count is still rank-local here, so the
       // product is always recomputed and the cached A'y is not used)
-      PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, 0, ray, D.prod_n.get(),
-                                          dist() ? nullptr : cands[q].known_aty, sl + 1,
-                                          D.rhat[q].get(), &r, sl + 2, s()));
-      PDLP_LAUNCH(pdlpk_ray_dual_prep(&P, 0, cands[q].x, &r, sl + 4, s()));
+      PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, 0, ray, prod, dist() ? nullptr : cands[q].known_aty,
+                                          sl + 1, D.rhat[q].get(), &r, sl + 2, st));
+      PDLP_LAUNCH(pdlpk_ray_dual_prep(&P, 0, cands[q].x, &r, sl + 4, st));
     }
   }
 
@@ -1699,12 +1705,7 @@ class Engine {
     const bool two = count == 2 && !gap_serial_;
     pdlpk_red r2 = r;
     if (two) {
-      if (!gap_side_) {  // created here: the engine's device is current
-        gap_side_ = std::make_unique<Stream>();
-        gap_fork_ = std::make_unique<Event>();
-        gap_join_ = std::make_unique<Event>();
-        gap_scratch2_.alloc(red_scratch_.size());
-      }
+      ensure_side();
       r2.scratch = gap_scratch2_.get();
       gap_fork_->record(s());
       PDLP_CK(cudaStreamWaitEvent(gap_side_->get(), gap_fork_->get(), 0));
@@ -1870,6 +1871,16 @@ class Engine {
   DevBuf<char> gap_work_[2];
   bool gap_shared_ = false;  // one gap buffer, queries evaluated one at a time
   std::map<std::pair<const void*, int>, GapWindow> gap_windows_;
+  // The cadence's side stream (the window average's share, the second gap
+  // query), created on first use: the engine's device is current then.
+  void ensure_side() {
+    if (gap_side_) return;
+    gap_side_ = std::make_unique<Stream>();
+    gap_fork_ = std::make_unique<Event>();
+    gap_join_ = std::make_unique<Event>();
+    gap_scratch2_.alloc(red_scratch_.size());
+  }
+  DevBuf<double> side_prod_;  // the average ray's A^T product
   std::unique_ptr<Stream> gap_side_;  // second gap query's stream
   DevBuf<double> gap_scratch2_;
   std::unique_ptr<Event> gap_fork_, gap_join_;
@@ -1990,39 +2001,77 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
       if (dist()) timed_out = any_rank(timed_out);  // ranks must agree
       const int c = D.cur();
       flush_average(P, D);
-      product(P.K, 0, D.x[c].get(), D.ax_cur.get());
-      product(P.KT, 0, D.y[c].get(), D.aty[c].get());
       const bool have_avg = D.hs.avg_count > 0;
+      const bool want_restart = cfg.enable_restarts && D.k() > D.k_last_restart;
+      // One batch, one sync: both residual screens, every ray candidate's
+      // scaled-space test, and the restart distances to the reference point.
+      // Decisions below are then taken in the reference's order.  On one GPU
+      // the window average's share (its products, screen, ray candidate and
+      // distances) runs on the side stream with its own reduction scratch:
+      // the same kernels on the same inputs, overlapped.
+      const pdlpk_red rr = red();
+      const bool side = have_avg && !dist() && !gap_serial_;
+      cudaStream_t sa = s();
+      pdlpk_red ra = rr;
+      double* prod_a = D.prod_n.get();
+      if (side) {
+        ensure_side();
+        sa = gap_side_->get();
+        ra.scratch = gap_scratch2_.get();
+        if (side_prod_.size() < static_cast<size_t>(P.n)) side_prod_.alloc(P.n);
+        prod_a = side_prod_.get();
+        gap_fork_->record(s());
+        PDLP_CK(cudaStreamWaitEvent(sa, gap_fork_->get(), 0));
+      }
+      std::vector<RayCand> cands;
+      if (cfg.detect_infeasibility) cands = ray_candidates(P, D, have_avg);
       if (have_avg) {
         PDLP_LAUNCH(pdlpk_average_into(D.state.get(), D.sum_x.get(), D.sum_y.get(), D.avg_x.get(),
-                                       D.avg_y.get(), P.n, P.m, s()));
+                                       D.avg_y.get(), P.n, P.m, sa));
+        if (side) {
+          PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.avg_x.get(), D.ax_avg.get(), parity_, sa));
+          PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.avg_y.get(), D.aty_avg.get(), parity_, sa));
+          PDLP_LAUNCH(pdlpk_screen(&P, 0, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
+                                   D.aty_avg.get(), cfg.rc_mode, &ra, D.rc_b.get(),
+                                   slot(kSlotScrAvg), sa));
+          if (cfg.detect_infeasibility) {
+            enqueue_rays(P, D, cands, cands.size() - 1, cands.size(), sa, &ra, prod_a);
+          }
+          if (want_restart) {
+            PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_x.get(), D.ref_x.get(), P.n, &ra,
+                                           slot(kSlotDist + 2), sa));
+            PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_y.get(), D.ref_y.get(), P.m, &ra,
+                                           slot(kSlotDist + 3), sa));
+          }
+        }
+      }
+      product(P.K, 0, D.x[c].get(), D.ax_cur.get());
+      product(P.KT, 0, D.y[c].get(), D.aty[c].get());
+      if (have_avg && !side) {
         product(P.K, 0, D.avg_x.get(), D.ax_avg.get());
         product(P.KT, 0, D.avg_y.get(), D.aty_avg.get());
       }
-      // One batch, one sync: both residual screens, every ray candidate's
-      // scaled-space test, and the restart distances to the reference point.
-      // Decisions below are then taken in the reference's order.
-      const pdlpk_red rr = red();
       PDLP_LAUNCH(pdlpk_screen(&P, 0, D.x[c].get(), D.y[c].get(), D.ax_cur.get(), D.aty[c].get(),
                                cfg.rc_mode, &rr, D.rc_a.get(), slot(kSlotScrCur), s()));
-      if (have_avg) {
+      if (have_avg && !side) {
         PDLP_LAUNCH(pdlpk_screen(&P, 0, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
                                  D.aty_avg.get(), cfg.rc_mode, &rr, D.rc_b.get(),
                                  slot(kSlotScrAvg), s()));
       }
-      std::vector<RayCand> cands;
       if (cfg.detect_infeasibility) {
-        cands = ray_candidates(P, D, have_avg);
-        enqueue_rays(P, D, cands);
+        enqueue_rays(P, D, cands, 0, side ? cands.size() - 1 : cands.size());
       }
-      const bool want_restart = cfg.enable_restarts && D.k() > D.k_last_restart;
       if (want_restart) {
         PDLP_LAUNCH(pdlpk_diff_norm_sq(D.x[c].get(), D.ref_x.get(), P.n, &rr, slot(kSlotDist), s()));
         PDLP_LAUNCH(pdlpk_diff_norm_sq(D.y[c].get(), D.ref_y.get(), P.m, &rr, slot(kSlotDist + 1), s()));
-        if (have_avg) {
+        if (have_avg && !side) {
           PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_x.get(), D.ref_x.get(), P.n, &rr, slot(kSlotDist + 2), s()));
           PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_y.get(), D.ref_y.get(), P.m, &rr, slot(kSlotDist + 3), s()));
         }
+      }
+      if (side) {
+        gap_join_->record(sa);
+        PDLP_CK(cudaStreamWaitEvent(s(), gap_join_->get(), 0));
       }
       double h[kSlots];
       std::memcpy(h, read_slots(kSlots), sizeof(h));
