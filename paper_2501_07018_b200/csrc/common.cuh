@@ -143,6 +143,17 @@ __device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
+// Programmatic dependent launch (the attempt's three kernels): let the next
+// kernel in the stream launch once every CTA of this one has started, then
+// wait until the previous kernel has completed and its writes are visible.
+// Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+#if PDLPK_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
 __device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs(p); }

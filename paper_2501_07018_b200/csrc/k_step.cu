@@ -42,6 +42,7 @@ inline int ew_blocks(int64_t n) {
 // is a.xbar itself).
 template <bool Push>
 __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a, pdlpk_peer_sum dst) {
+  pdl_enter();
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const double eta = st->eta;
@@ -259,6 +260,7 @@ struct RowEpi {
 
 template <class P, int Seg>
 __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) row_pass(pdlpk_step_args a) {
+  pdl_enter();
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;
@@ -325,6 +327,7 @@ struct ColEpi {
 
 template <class P, int Seg, bool Decide>
 __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(pdlpk_step_args a) {
+  pdl_enter();
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;
@@ -539,27 +542,51 @@ __global__ void __launch_bounds__(kEwThreads) flush_average_kernel(pdlpk_step_ar
 
 __global__ void clear_pending_kernel(pdlpk_step_state* st) { st->avg_pending = 0; }
 
+// <<<>>> or, with pdl, cudaLaunchKernelEx with programmatic stream
+// serialization (the kernels' pdl_enter() keeps the data dependence).
+template <class... KArgs, class... Args>
+inline void launch_step(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block,
+                        size_t smem, cudaStream_t s, Args... args) {
+  if (!(PDLPK_PDL && pdl)) {
+    kern<<<grid, block, smem, s>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 struct LaunchRowCol {
   const pdlpk_step_args* a;
   cudaStream_t s;
   bool row;
   bool decide_here = true;
+  bool pdl = false;
   template <class P, int Seg>
   int go() {
     const pdlpk_csr& A = row ? a->P.K : a->P.KT;
     const int64_t g = sched_blocks(A);
     if (g <= 0) return 0;
     const size_t smem = spmv_smem(A, Seg);
+    const unsigned gu = static_cast<unsigned>(g);
     if (row) {
       allow_smem(row_pass<P, Seg>, smem);
-      row_pass<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
+      launch_step(pdl, row_pass<P, Seg>, gu, kSpmvThreads, smem, s, *a);
     } else {
       if (decide_here) {
         allow_smem(col_pass<P, Seg, true>, smem);
-        col_pass<P, Seg, true><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
+        launch_step(pdl, col_pass<P, Seg, true>, gu, kSpmvThreads, smem, s, *a);
       } else {
         allow_smem(col_pass<P, Seg, false>, smem);
-        col_pass<P, Seg, false><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(*a);
+        launch_step(pdl, col_pass<P, Seg, false>, gu, kSpmvThreads, smem, s, *a);
       }
     }
     return 0;
@@ -733,12 +760,14 @@ extern "C" int pdlpk_arm(pdlpk_step_state* st, int64_t k_target, cudaStream_t s)
 }
 
 extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
-  primal_pass<false><<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, pdlpk_peer_sum{});
+  const bool pdl = a->mode == 0;  // perf mode: the three kernels chain with PDL
+  launch_step(pdl, primal_pass<false>, static_cast<unsigned>(ew_blocks(a->P.n)), kEwThreads, 0, s,
+              *a, pdlpk_peer_sum{});
   if (a->mode == 0) {
     // Degenerate shapes (an empty side) still need the decision, which the
     // column pass performs: it always has >= 1 CTA (short_blocks >= 1).
-    dispatch_p(a->P.K, LaunchRowCol{a, s, true});
-    dispatch_p(a->P.KT, LaunchRowCol{a, s, false});
+    dispatch_p(a->P.K, LaunchRowCol{a, s, true, true, true});
+    dispatch_p(a->P.KT, LaunchRowCol{a, s, false, true, true});
   } else {
     const int gm = ew_blocks(a->P.m), gn = ew_blocks(a->P.n);
     if (a->P.K.wide) {

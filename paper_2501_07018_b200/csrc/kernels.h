@@ -93,6 +93,9 @@ typedef struct pdlpk_csr {
 #ifndef PDLPK_XBAR_KEEP
 #define PDLPK_XBAR_KEEP 1
 #endif
+#ifndef PDLPK_PDL
+#define PDLPK_PDL 1
+#endif
 #ifndef PDLPK_DY_KEEP
 #define PDLPK_DY_KEEP 0
 #endif
