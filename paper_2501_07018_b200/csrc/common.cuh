@@ -10,6 +10,8 @@
 #include <cstdint>
 #include <math_constants.h>
 
+#include "kernels.h"  // tuning defaults (PDLPK_PDL, ...)
+
 namespace pdlp {
 
 constexpr int kWarp = 32;
@@ -143,15 +145,56 @@ __device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
-// Programmatic dependent launch (the attempt's three kernels): let the next
-// kernel in the stream launch once every CTA of this one has started, then
-// wait until the previous kernel has completed and its writes are visible.
-// Without the launch attribute both instructions are no-ops.
-__device__ __forceinline__ void pdl_enter() {
+// Programmatic dependent launch (the attempt's three kernels).  pdl_wait()
+// at the top of a kernel: block until the previous kernel of the stream has
+// completed and its writes are visible (before any dependent read).
+// pdl_trigger() once a CTA's main work is issued: the next kernel's CTAs may
+// then launch onto SMs this CTA's tail leaves free.  Triggering at kernel
+// start instead fills the SMs with waiting CTAs (measured: C1 6,440 ->
+// 3,950 it/s).  Outside a PDL launch both are no-ops.
+__device__ __forceinline__ void pdl_wait() {
 #if PDLPK_PDL
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if PDLPK_PDL && PDLPK_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+// The cadence's kernels (reductions, products): the same, when enabled.
+__device__ __forceinline__ void pdl_wait_cadence() {
+#if PDLPK_PDL && PDLPK_PDL_CADENCE
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger_cadence() {
+#if PDLPK_PDL && PDLPK_PDL_CADENCE
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+// <<<>>> or, with pdl, cudaLaunchKernelEx with programmatic stream
+// serialization.  Only for kernels that begin with pdl_enter(): their wait
+// keeps the dependence on the previous kernel of the stream.
+template <class... KArgs, class... Args>
+inline void launch_pdl(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block,
+                       size_t smem, cudaStream_t s, Args... args) {
+  if (!(PDLPK_PDL && pdl)) {
+    kern<<<grid, block, smem, s>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }

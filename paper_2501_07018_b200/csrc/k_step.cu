@@ -42,7 +42,7 @@ inline int ew_blocks(int64_t n) {
 // is a.xbar itself).
 template <bool Push>
 __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a, pdlpk_peer_sum dst) {
-  pdl_enter();
+  pdl_wait();
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const double eta = st->eta;
@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a, pdl
     }
     if (pend) sx[i] = sx[i] + w * xi;
   }
+  pdl_trigger();
 }
 
 // ---------------------------------------------------------- decision rule ---
@@ -260,7 +261,7 @@ struct RowEpi {
 
 template <class P, int Seg>
 __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) row_pass(pdlpk_step_args a) {
-  pdl_enter();
+  pdl_wait();
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) row_pass(p
   e.pend = st->avg_pending != 0;
   e.w = st->avg_w;
   sched_spmv<P, Seg>(a.P.K, a.P.K.value, a.xbar, e);
+  pdl_trigger();
   __shared__ double red[32];
   const double s1 = block_sum(e.dy2, red);
   __syncthreads();
@@ -327,7 +329,7 @@ struct ColEpi {
 
 template <class P, int Seg, bool Decide>
 __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(pdlpk_step_args a) {
-  pdl_enter();
+  pdl_wait();
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
   const int cur = st->cur;
@@ -337,6 +339,7 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(p
   e.x = a.x[cur];
   e.xn = a.x[cur ^ 1];
   sched_spmv<P, Seg>(a.P.KT, a.P.KT.value, a.dy, e);
+  pdl_trigger();
   __shared__ double red[32];
   __shared__ bool last;
   const double s1 = block_sum(e.dx2, red);
@@ -542,28 +545,6 @@ __global__ void __launch_bounds__(kEwThreads) flush_average_kernel(pdlpk_step_ar
 
 __global__ void clear_pending_kernel(pdlpk_step_state* st) { st->avg_pending = 0; }
 
-// <<<>>> or, with pdl, cudaLaunchKernelEx with programmatic stream
-// serialization (the kernels' pdl_enter() keeps the data dependence).
-template <class... KArgs, class... Args>
-inline void launch_step(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block,
-                        size_t smem, cudaStream_t s, Args... args) {
-  if (!(PDLPK_PDL && pdl)) {
-    kern<<<grid, block, smem, s>>>(args...);
-    return;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, args...);
-}
-
 struct LaunchRowCol {
   const pdlpk_step_args* a;
   cudaStream_t s;
@@ -579,14 +560,14 @@ struct LaunchRowCol {
     const unsigned gu = static_cast<unsigned>(g);
     if (row) {
       allow_smem(row_pass<P, Seg>, smem);
-      launch_step(pdl, row_pass<P, Seg>, gu, kSpmvThreads, smem, s, *a);
+      launch_pdl(pdl, row_pass<P, Seg>, gu, kSpmvThreads, smem, s, *a);
     } else {
       if (decide_here) {
         allow_smem(col_pass<P, Seg, true>, smem);
-        launch_step(pdl, col_pass<P, Seg, true>, gu, kSpmvThreads, smem, s, *a);
+        launch_pdl(pdl, col_pass<P, Seg, true>, gu, kSpmvThreads, smem, s, *a);
       } else {
         allow_smem(col_pass<P, Seg, false>, smem);
-        launch_step(pdl, col_pass<P, Seg, false>, gu, kSpmvThreads, smem, s, *a);
+        launch_pdl(pdl, col_pass<P, Seg, false>, gu, kSpmvThreads, smem, s, *a);
       }
     }
     return 0;
@@ -761,7 +742,7 @@ extern "C" int pdlpk_arm(pdlpk_step_state* st, int64_t k_target, cudaStream_t s)
 
 extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
   const bool pdl = a->mode == 0;  // perf mode: the three kernels chain with PDL
-  launch_step(pdl, primal_pass<false>, static_cast<unsigned>(ew_blocks(a->P.n)), kEwThreads, 0, s,
+  launch_pdl(pdl, primal_pass<false>, static_cast<unsigned>(ew_blocks(a->P.n)), kEwThreads, 0, s,
               *a, pdlpk_peer_sum{});
   if (a->mode == 0) {
     // Degenerate shapes (an empty side) still need the decision, which the

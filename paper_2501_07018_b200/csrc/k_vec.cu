@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(kT) seq_spmv_kernel(const P* __restrict__ star
                                                       const double* __restrict__ v,
                                                       double* __restrict__ out, int64_t dim,
                                                       const double* cond) {
+  pdl_wait_cadence();
   if (cond != nullptr && *cond == 0.0) return;
   GRID_STRIDE(r, dim) {
     double acc = 0.0;
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) sched_spmv
                                                                   const double* vals,
                                                                   const double* v, double* out,
                                                                   const double* cond) {
+  pdl_wait_cadence();
   if (cond != nullptr && *cond == 0.0) return;
   StoreEpi e{out};
   sched_spmv<P, Seg>(A, vals, v, e);
@@ -83,8 +85,8 @@ struct LaunchSpmv {
     if (g > 0) {
       const size_t smem = spmv_smem(*A, Seg);
       allow_smem(sched_spmv_kernel<P, Seg>, smem);
-      sched_spmv_kernel<P, Seg><<<static_cast<unsigned>(g), kSpmvThreads, smem, s>>>(
-          *A, vals, v, out, cond);
+      launch_pdl(PDLPK_PDL_CADENCE, sched_spmv_kernel<P, Seg>, static_cast<unsigned>(g), kSpmvThreads, smem, s,
+                 *A, vals, v, out, cond);
     }
     return ok();
   }
@@ -250,11 +252,13 @@ int pdlpk_spmv_cond(const pdlpk_csr* A, int32_t orig, const double* v, double* o
   if (parity) {
     const int g = ew_blocks(A->dim);
     if (A->wide) {
-      seq_spmv_kernel<int64_t><<<g, kT, 0, s>>>(static_cast<const int64_t*>(A->start), A->index,
-                                                vals, v, out, A->dim, cond);
+      launch_pdl(PDLPK_PDL_CADENCE, seq_spmv_kernel<int64_t>, static_cast<unsigned>(g), kT, 0, s,
+                 static_cast<const int64_t*>(A->start), static_cast<const int32_t*>(A->index), vals,
+                 v, out, A->dim, cond);
     } else {
-      seq_spmv_kernel<int32_t><<<g, kT, 0, s>>>(static_cast<const int32_t*>(A->start), A->index,
-                                                vals, v, out, A->dim, cond);
+      launch_pdl(PDLPK_PDL_CADENCE, seq_spmv_kernel<int32_t>, static_cast<unsigned>(g), kT, 0, s,
+                 static_cast<const int32_t*>(A->start), static_cast<const int32_t*>(A->index), vals,
+                 v, out, A->dim, cond);
     }
     return ok();
   }

@@ -96,6 +96,12 @@ typedef struct pdlpk_csr {
 #ifndef PDLPK_PDL
 #define PDLPK_PDL 1
 #endif
+#ifndef PDLPK_PDL_TRIGGER
+#define PDLPK_PDL_TRIGGER 0
+#endif
+#ifndef PDLPK_PDL_CADENCE
+#define PDLPK_PDL_CADENCE 1
+#endif
 #ifndef PDLPK_DY_KEEP
 #define PDLPK_DY_KEEP 0
 #endif

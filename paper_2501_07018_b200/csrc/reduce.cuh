@@ -43,6 +43,7 @@ __device__ __forceinline__ void red_accum(double* acc, const double* v, unsigned
 
 template <int K, class F>
 __global__ void red_seq_kernel(F f, int64_t n, unsigned maxmask, double* out) {
+  pdl_wait_cadence();
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
@@ -57,6 +58,7 @@ __global__ void red_seq_kernel(F f, int64_t n, unsigned maxmask, double* out) {
 
 template <int K, class F>
 __global__ void red_shard_kernel(F f, int64_t n, int S, unsigned maxmask, double* part) {
+  pdl_wait_cadence();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   const int64_t base = n / S, rem = n % S;
@@ -76,6 +78,7 @@ __global__ void red_shard_kernel(F f, int64_t n, int S, unsigned maxmask, double
 
 template <int K>
 __global__ void red_shard_final(const double* part, int S, unsigned maxmask, double* out) {
+  pdl_wait_cadence();
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     double t = 0.0;
@@ -89,6 +92,7 @@ __global__ void red_shard_final(const double* part, int S, unsigned maxmask, dou
 template <int K, class F>
 __global__ void __launch_bounds__(kRedThreads) red_tree_kernel(F f, int64_t n, unsigned maxmask,
                                                                double* part) {
+  pdl_wait_cadence();
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
@@ -111,6 +115,7 @@ __global__ void __launch_bounds__(kRedThreads) red_tree_kernel(F f, int64_t n, u
 template <int K>
 __global__ void __launch_bounds__(kRedThreads) red_tree_final(const double* part, int G,
                                                               unsigned maxmask, double* out) {
+  pdl_wait_cadence();
   __shared__ double sm[32];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -136,14 +141,18 @@ template <int K, class F>
 inline int multi_reduce(F f, int64_t n, int order, int shards, unsigned maxmask,
                         double* scratch, double* out, cudaStream_t s) {
   if (order == PDLPK_RED_SEQ) {
-    red_seq_kernel<K><<<1, 1, 0, s>>>(f, n, maxmask, out);
+    launch_pdl(PDLPK_PDL_CADENCE, red_seq_kernel<K, F>, 1, 1, 0, s, f, n, maxmask, out);
   } else if (order == PDLPK_RED_SHARD) {
-    red_shard_kernel<K><<<(shards + 127) / 128, 128, 0, s>>>(f, n, shards, maxmask, scratch);
-    red_shard_final<K><<<1, 1, 0, s>>>(scratch, shards, maxmask, out);
+    launch_pdl(PDLPK_PDL_CADENCE, red_shard_kernel<K, F>, static_cast<unsigned>((shards + 127) / 128), 128, 0, s,
+               f, n, shards, maxmask, scratch);
+    launch_pdl(PDLPK_PDL_CADENCE, red_shard_final<K>, 1, 1, 0, s, static_cast<const double*>(scratch), shards,
+               maxmask, out);
   } else {
     const int g = red_tree_blocks(n);
-    red_tree_kernel<K><<<g, kRedThreads, 0, s>>>(f, n, maxmask, scratch);
-    red_tree_final<K><<<1, kRedThreads, 0, s>>>(scratch, g, maxmask, out);
+    launch_pdl(PDLPK_PDL_CADENCE, red_tree_kernel<K, F>, static_cast<unsigned>(g), kRedThreads, 0, s, f, n,
+               maxmask, scratch);
+    launch_pdl(PDLPK_PDL_CADENCE, red_tree_final<K>, 1, kRedThreads, 0, s, static_cast<const double*>(scratch), g,
+               maxmask, out);
   }
   red_log_record(out, K, maxmask);
   return static_cast<int>(cudaGetLastError());
