@@ -255,10 +255,12 @@ __device__ __forceinline__ void write_events(const GapIn& g, const Work& w, int6
 }
 
 __global__ void events_kernel(GapIn g, Work w) {
+  pdl_wait_cadence();
   GRID_STRIDE(t, g.n + g.m) write_events(g, w, t, gap_coord(g, t));
 }
 
 __global__ void keys_kernel(Work w, int64_t E) {
+  pdl_wait_cadence();
   GRID_STRIDE(e, E) w.keys_in[e] = order_key(w.lam[w.sel[e]]);
 }
 
@@ -270,6 +272,7 @@ __device__ double finish_lambda(double lambda_star) {
 
 // Reference sweep (restarts.hpp:175-212), one thread, sorted order.
 __global__ void sweep_seq_kernel(Work w, int64_t E, const double* r_slot, double r_value) {
+  pdl_wait_cadence();
   const double r = r_slot ? *r_slot : r_value;
   const double r2 = r * r;
   double c_sum = w.sc->sums[1];
@@ -311,6 +314,7 @@ __global__ void sweep_seq_kernel(Work w, int64_t E, const double* r_slot, double
 }
 
 __global__ void gather_masses_kernel(Work w, int64_t E) {
+  pdl_wait_cadence();
   GRID_STRIDE(idx, E) {
     const int32_t s = w.vals_out[idx];
     w.cs[idx] = w.dc[s];
@@ -318,16 +322,21 @@ __global__ void gather_masses_kernel(Work w, int64_t E) {
   }
 }
 
-__global__ void init_first_kernel(Work w) { w.sc->first = ~0ull; }
+__global__ void init_first_kernel(Work w) {
+  pdl_wait_cadence();
+  w.sc->first = ~0ull;
+}
 
 // Window sort: a strided sample of the keys places the window's bounds at
 // depth fractions of the descending order.
 __global__ void sample_keys_kernel(Work w, int64_t E) {
+  pdl_wait_cadence();
   GRID_STRIDE(i, kGapSample) w.samp_in[i] = w.keys_in[(i * E) / kGapSample];
 }
 // Position of the first crossing as a fraction of all events (1 when none):
 // the engine sizes the next partial sort from it.
 __global__ void hit_fraction_kernel(Work w, int64_t E, double* out) {
+  pdl_wait_cadence();
   const unsigned long long f = w.sc->first;
   *out = (f == ~0ull || E <= 0)
              ? 1.0
@@ -335,6 +344,7 @@ __global__ void hit_fraction_kernel(Work w, int64_t E, double* out) {
 }
 
 __global__ void base_full_kernel(Work w) {
+  pdl_wait_cadence();
   w.sc->base[0] = w.sc->sums[1];
   w.sc->base[1] = w.sc->sums[0];
   w.sc->base[2] = CUDART_INF;
@@ -343,6 +353,7 @@ __global__ void base_full_kernel(Work w) {
 
 // Window [lo_key, hi_key] between sample ranks ra (0: no events above) and rb.
 __global__ void window_keys_kernel(Work w, int ra, int rb) {
+  pdl_wait_cadence();
   w.sc->hi_key = ra > 0 ? w.samp_out[ra] : ~0ull;
   w.sc->lo_key = rb >= 0 ? w.samp_out[rb] : 0ull;  // rb < 0: down to the last event
   w.sc->above_min = ~0ull;
@@ -352,6 +363,7 @@ __global__ void window_keys_kernel(Work w, int ra, int rb) {
 // Flags the window's events (whole tie groups: the window is a key range)
 // and finds the smallest key and the count above it (exact integer work).
 __global__ void __launch_bounds__(kT) window_flags_kernel(Work w, int64_t E) {
+  pdl_wait_cadence();
   const uint64_t lo = w.sc->lo_key, hi = w.sc->hi_key;
   unsigned long long mn = ~0ull, cnt = 0;
   GRID_STRIDE(i, E) {
@@ -376,6 +388,7 @@ __global__ void __launch_bounds__(kT) window_flags_kernel(Work w, int64_t E) {
 }
 
 __global__ void base_window_kernel(Work w) {
+  pdl_wait_cadence();
   // nothing above (a top window): exactly the full sort's start
   const bool none = w.sc->above_count == 0;
   w.sc->base[0] = none ? w.sc->sums[1] : w.sc->sums[1] + w.sc->above[0];
@@ -385,6 +398,7 @@ __global__ void base_window_kernel(Work w) {
 
 // Parallel sweep: cs/bs hold exclusive prefix masses in sorted order.
 __global__ void first_hit_kernel(Work w, int64_t E, const double* r_slot, double r_value) {
+  pdl_wait_cadence();
   const double r = r_slot ? *r_slot : r_value;
   const double r2 = r * r;
   const double c0 = w.sc->base[0], b0 = w.sc->base[1];
@@ -411,6 +425,7 @@ __global__ void first_hit_kernel(Work w, int64_t E, const double* r_slot, double
 }
 
 __global__ void finalize_perf_kernel(Work w, int64_t E, const double* r_slot, double r_value) {
+  pdl_wait_cadence();
   const double r = r_slot ? *r_slot : r_value;
   const double r2 = r * r;
   const double c0 = w.sc->base[0], b0 = w.sc->base[1];
@@ -471,6 +486,7 @@ __device__ __forceinline__ double cand_y(const GapIn& g, int64_t j, double lambd
 // gap_value_at (restarts.hpp:50-71) in the reference's exact order.
 __global__ void value_seq_kernel(GapIn g, Work w, const double* r_slot, double r_value,
                                  double* out) {
+  pdl_wait_cadence();
   const double r = r_slot ? *r_slot : r_value;
   if (!(r > 0.0)) {
     *out = 0.0;
@@ -502,6 +518,7 @@ __global__ void value_seq_kernel(GapIn g, Work w, const double* r_slot, double r
 
 __global__ void value_finish_kernel(const double* sum, const double* r_slot, double r_value,
                                     double* out) {
+  pdl_wait_cadence();
   const double r = r_slot ? *r_slot : r_value;
   const double value = *sum;
   *out = (r > 0.0 && value > 0.0) ? value / r : 0.0;
@@ -542,7 +559,7 @@ extern "C" int pdlpk_gap_prepare(const pdlpk_problem* P, const double* x, const 
       return o.mass_use;
     };
     rc = multi_reduce<2>(fm, n + m, PDLPK_RED_SEQ, red->shards, 0u, red->scratch, w.sc->sums, s);
-    if (rc == 0 && N > 0) events_kernel<<<ew_blocks(n + m), kT, 0, s>>>(g, w);
+    if (rc == 0 && N > 0) launch_pdl(PDLPK_PDL_CADENCE, events_kernel, static_cast<unsigned>(ew_blocks(n + m)), kT, 0, s, g, w);
   } else {
     // one pass: the tree reduction visits every coordinate once and writes
     // its events on the way
@@ -587,8 +604,8 @@ thread_local int64_t g_window_stats[2] = {0, 0};  // windows tried, decided
 // (the window count, the hit).
 static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const pdlpk_red* red,
                           const double* r_slot, double r_value, cudaStream_t s) {
-  keys_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
-  sample_keys_kernel<<<ew_blocks(kGapSample), kT, 0, s>>>(w, E);
+  launch_pdl(PDLPK_PDL_CADENCE, keys_kernel, static_cast<unsigned>(ew_blocks(E)), kT, 0, s, w, E);
+  launch_pdl(PDLPK_PDL_CADENCE, sample_keys_kernel, static_cast<unsigned>(ew_blocks(kGapSample)), kT, 0, s, w, E);
   size_t bytes = w.cub_bytes;
   if (cub::DeviceRadixSort::SortKeysDescending(w.cub_tmp, bytes, w.samp_in, w.samp_out, kGapSample,
                                                0, 64, s) != cudaSuccess) {
@@ -597,8 +614,8 @@ static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const 
   const int ra = qa <= 0.0 ? 0 : std::min(kGapSample - 1, static_cast<int>(qa * kGapSample));
   const bool to_bottom = qb >= 1.0;
   const int rb = to_bottom ? -1 : std::min(kGapSample - 1, static_cast<int>(qb * kGapSample));
-  window_keys_kernel<<<1, 1, 0, s>>>(w, ra, rb);
-  window_flags_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+  launch_pdl(PDLPK_PDL_CADENCE, window_keys_kernel, static_cast<unsigned>(1), 1, 0, s, w, ra, rb);
+  launch_pdl(PDLPK_PDL_CADENCE, window_flags_kernel, static_cast<unsigned>(ew_blocks(E)), kT, 0, s, w, E);
   if (ra > 0) {
     const Work wc = w;
     auto fa = [wc] __device__(int64_t e, double* v) -> unsigned {
@@ -614,7 +631,7 @@ static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const 
   } else {
     cudaMemsetAsync(w.sc->above, 0, sizeof(w.sc->above), s);
   }
-  base_window_kernel<<<1, 1, 0, s>>>(w);
+  launch_pdl(PDLPK_PDL_CADENCE, base_window_kernel, static_cast<unsigned>(1), 1, 0, s, w);
   uint64_t* keys_h = reinterpret_cast<uint64_t*>(w.cs);
   bytes = w.cub_bytes;
   if (cub::DeviceSelect::Flagged(w.cub_tmp, bytes, w.keys_in, w.flag, keys_h, &w.sc->num_high,
@@ -635,13 +652,13 @@ static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const 
                                                 w.vals_out, eh, 0, 64, s) != cudaSuccess) {
     return -1;
   }
-  gather_masses_kernel<<<ew_blocks(eh), kT, 0, s>>>(w, eh);
+  launch_pdl(PDLPK_PDL_CADENCE, gather_masses_kernel, static_cast<unsigned>(ew_blocks(eh)), kT, 0, s, w, eh);
   bytes = w.cub_bytes;
   cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.cs, w.cs, eh, s);
   bytes = w.cub_bytes;
   cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.bs, w.bs, eh, s);
-  init_first_kernel<<<1, 1, 0, s>>>(w);
-  first_hit_kernel<<<ew_blocks(eh), kT, 0, s>>>(w, eh, r_slot, r_value);
+  launch_pdl(PDLPK_PDL_CADENCE, init_first_kernel, static_cast<unsigned>(1), 1, 0, s, w);
+  launch_pdl(PDLPK_PDL_CADENCE, first_hit_kernel, static_cast<unsigned>(ew_blocks(eh)), kT, 0, s, w, eh, r_slot, r_value);
   struct {
     unsigned long long first, above;
   } h{};
@@ -677,34 +694,34 @@ extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const d
     ++g_window_stats[0];
     if (decided) ++g_window_stats[1];
   }
-  if (!decided) base_full_kernel<<<1, 1, 0, s>>>(w);
+  if (!decided) launch_pdl(PDLPK_PDL_CADENCE, base_full_kernel, static_cast<unsigned>(1), 1, 0, s, w);
   if (E > 0 && !decided) {
-    keys_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+    launch_pdl(PDLPK_PDL_CADENCE, keys_kernel, static_cast<unsigned>(ew_blocks(E)), kT, 0, s, w, E);
     size_t bytes = w.cub_bytes;
     const cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(
         w.cub_tmp, bytes, w.keys_in, w.keys_out, w.sel, w.vals_out, static_cast<int>(E), 0, 64, s);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   if (parity) {
-    sweep_seq_kernel<<<1, 1, 0, s>>>(w, E, r_slot, r_value);
-    value_seq_kernel<<<1, 1, 0, s>>>(g, w, r_slot, r_value, gap_slot);
+    launch_pdl(PDLPK_PDL_CADENCE, sweep_seq_kernel, static_cast<unsigned>(1), 1, 0, s, w, E, r_slot, r_value);
+    launch_pdl(PDLPK_PDL_CADENCE, value_seq_kernel, static_cast<unsigned>(1), 1, 0, s, g, w, r_slot, r_value, gap_slot);
     return static_cast<int>(cudaGetLastError());
   }
   if (!decided) {
     if (E > 0) {
-      gather_masses_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+      launch_pdl(PDLPK_PDL_CADENCE, gather_masses_kernel, static_cast<unsigned>(ew_blocks(E)), kT, 0, s, w, E);
       size_t bytes = w.cub_bytes;
       cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.cs, w.cs, static_cast<int>(E), s);
       bytes = w.cub_bytes;
       cub::DeviceScan::ExclusiveSum(w.cub_tmp, bytes, w.bs, w.bs, static_cast<int>(E), s);
     }
-    init_first_kernel<<<1, 1, 0, s>>>(w);
-    if (E > 0) first_hit_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E, r_slot, r_value);
+    launch_pdl(PDLPK_PDL_CADENCE, init_first_kernel, static_cast<unsigned>(1), 1, 0, s, w);
+    if (E > 0) launch_pdl(PDLPK_PDL_CADENCE, first_hit_kernel, static_cast<unsigned>(ew_blocks(E)), kT, 0, s, w, E, r_slot, r_value);
   }
   // (a decided window: its crossing index, or the no-crossing branch over
   // the window's events with the masses above in base)
-  finalize_perf_kernel<<<1, 1, 0, s>>>(w, E_fin, r_slot, r_value);
-  hit_fraction_kernel<<<1, 1, 0, s>>>(w, E, gap_slot + 2);
+  launch_pdl(PDLPK_PDL_CADENCE, finalize_perf_kernel, static_cast<unsigned>(1), 1, 0, s, w, E_fin, r_slot, r_value);
+  launch_pdl(PDLPK_PDL_CADENCE, hit_fraction_kernel, static_cast<unsigned>(1), 1, 0, s, w, E, gap_slot + 2);
   const double* lam_star = &w.sc->lambda_star;
   auto fv = [g, lam_star] __device__(int64_t t, double* v) -> unsigned {
     const double lambda = *lam_star;
@@ -733,6 +750,6 @@ extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const d
   const int rc = multi_reduce<1>(fv, n + m, PDLPK_RED_TREE, red->shards, 0u, red->scratch,
                                  &w.sc->value, s);
   if (rc != 0) return rc;
-  value_finish_kernel<<<1, 1, 0, s>>>(&w.sc->value, r_slot, r_value, gap_slot);
+  launch_pdl(PDLPK_PDL_CADENCE, value_finish_kernel, static_cast<unsigned>(1), 1, 0, s, &w.sc->value, r_slot, r_value, gap_slot);
   return static_cast<int>(cudaGetLastError());
 }
