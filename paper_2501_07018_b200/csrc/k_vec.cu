@@ -94,11 +94,13 @@ struct LaunchSpmv {
 
 // ------------------------------------------------------------ elementwise ---
 __global__ void fill_kernel(double* x, double v, int64_t n) {
+  pdl_wait_cadence();
   GRID_STRIDE(i, n) x[i] = v;
 }
 
 __global__ void combine_slots_kernel(const double* all, int world, int stride, uint64_t marked,
                                      uint64_t maxbits, double* slots) {
+  pdl_wait_cadence();
   const int i = threadIdx.x;
   if (i >= 64 || !((marked >> i) & 1ull)) return;
   const bool mx = (maxbits >> i) & 1ull;
@@ -111,20 +113,24 @@ __global__ void combine_slots_kernel(const double* all, int world, int stride, u
 }
 
 __global__ void accumulate_kernel(double* out, const double* in, int64_t n, int use_max) {
+  pdl_wait_cadence();
   GRID_STRIDE(i, n) out[i] = use_max ? max_keep(out[i], in[i]) : out[i] + in[i];
 }
 
 __global__ void sub_kernel(const double* a, const double* b, double* out, int64_t n) {
+  pdl_wait_cadence();
   GRID_STRIDE(i, n) out[i] = a[i] - b[i];
 }
 
 __global__ void scale_mul_kernel(const double* scale, const double* v, double* out, int64_t n) {
+  pdl_wait_cadence();
   GRID_STRIDE(i, n) out[i] = scale[i] * v[i];
 }
 
 __global__ void average_into_kernel(const pdlpk_step_state* st, const double* sx,
                                     const double* sy, double* x, double* y, int64_t n,
                                     int64_t m) {
+  pdl_wait_cadence();
   const double inv = 1.0 / st->avg_weight;
   GRID_STRIDE(i, n + m) {
     if (i < n) {
@@ -136,6 +142,7 @@ __global__ void average_into_kernel(const pdlpk_step_state* st, const double* sx
 }
 
 __global__ void initial_point_kernel(const double* lv, const double* uv, double* x, int64_t n) {
+  pdl_wait_cadence();
   GRID_STRIDE(i, n) x[i] = clampd(0.0, lv[i], uv[i]);
 }
 
@@ -143,6 +150,7 @@ __global__ void dual_feas_bounds_kernel(const double* c, const double* lv, const
                                         int64_t n, const double* lc, const double* uc,
                                         int64_t m, double* slc, double* suc, double* slv,
                                         double* suv) {
+  pdl_wait_cadence();
   GRID_STRIDE(t, n + m) {
     if (t < n) {
       const int64_t i = t;
@@ -166,10 +174,12 @@ __global__ void dual_feas_bounds_kernel(const double* c, const double* lv, const
 }
 
 __global__ void i64_to_i32_kernel(const int64_t* src, int32_t* dst, int64_t n) {
+  pdl_wait_cadence();
   GRID_STRIDE(i, n) dst[i] = static_cast<int32_t>(src[i]);
 }
 
 __global__ void radius_kernel(const double* dx2, const double* dy2, double omega, double* out) {
+  pdl_wait_cadence();
   *out = sqrt(omega * (*dx2) + (*dy2) / omega);
 }
 
@@ -178,6 +188,7 @@ __global__ void radius_kernel(const double* dx2, const double* dy2, double omega
 __global__ void apply_vec_factor_kernel(double* lc, double* uc, double* rs, const double* fr,
                                         int64_t m, double* c, double* lv, double* uv,
                                         double* cs, const double* fc, int64_t n) {
+  pdl_wait_cadence();
   GRID_STRIDE(t, m + n) {
     if (t < m) {
       const double f = fr[t];
@@ -196,6 +207,7 @@ __global__ void apply_vec_factor_kernel(double* lc, double* uc, double* rs, cons
 }
 
 __global__ void find_nonfinite_kernel(const double* v, int64_t n, int32_t code, int32_t* first) {
+  pdl_wait_cadence();
   GRID_STRIDE(i, n) {
     if (!finite_d(v[i])) atomicMin(reinterpret_cast<int*>(first + 1), static_cast<int>(i));
   }
@@ -237,7 +249,7 @@ extern "C" {
 int64_t pdlpk_red_scratch_doubles(void) { return 8 * kRedMaxBlocks; }
 
 int pdlpk_index_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s) {
-  if (n > 0) i64_to_i32_kernel<<<ew_blocks(n), kT, 0, s>>>(src, dst, n);
+  if (n > 0) launch_pdl(PDLPK_PDL_CADENCE, i64_to_i32_kernel, static_cast<unsigned>(ew_blocks(n)), kT, 0, s, src, dst, n);
   return ok();
 }
 
@@ -300,34 +312,34 @@ int32_t pdlpk_stage_budget(int32_t nnz) {
 
 int pdlpk_combine_slots(const double* all, int32_t world, int32_t stride, uint64_t marked,
                         uint64_t maxbits, double* slots, cudaStream_t s) {
-  if (marked != 0) combine_slots_kernel<<<1, 64, 0, s>>>(all, world, stride, marked, maxbits, slots);
+  if (marked != 0) launch_pdl(PDLPK_PDL_CADENCE, combine_slots_kernel, static_cast<unsigned>(1), 64, 0, s, all, world, stride, marked, maxbits, slots);
   return ok();
 }
 
 int pdlpk_accumulate(double* out, const double* in, int64_t n, int32_t use_max, cudaStream_t s) {
-  if (n > 0) accumulate_kernel<<<ew_blocks(n), kT, 0, s>>>(out, in, n, use_max);
+  if (n > 0) launch_pdl(PDLPK_PDL_CADENCE, accumulate_kernel, static_cast<unsigned>(ew_blocks(n)), kT, 0, s, out, in, n, use_max);
   return ok();
 }
 
 int pdlpk_fill(double* x, double v, int64_t n, cudaStream_t s) {
-  if (n > 0) fill_kernel<<<ew_blocks(n), kT, 0, s>>>(x, v, n);
+  if (n > 0) launch_pdl(PDLPK_PDL_CADENCE, fill_kernel, static_cast<unsigned>(ew_blocks(n)), kT, 0, s, x, v, n);
   return ok();
 }
 
 int pdlpk_sub(const double* a, const double* b, double* out, int64_t n, cudaStream_t s) {
-  if (n > 0) sub_kernel<<<ew_blocks(n), kT, 0, s>>>(a, b, out, n);
+  if (n > 0) launch_pdl(PDLPK_PDL_CADENCE, sub_kernel, static_cast<unsigned>(ew_blocks(n)), kT, 0, s, a, b, out, n);
   return ok();
 }
 
 int pdlpk_average_into(const pdlpk_step_state* st, const double* sum_x, const double* sum_y,
                        double* x, double* y, int64_t n, int64_t m, cudaStream_t s) {
-  if (n + m > 0) average_into_kernel<<<ew_blocks(n + m), kT, 0, s>>>(st, sum_x, sum_y, x, y, n, m);
+  if (n + m > 0) launch_pdl(PDLPK_PDL_CADENCE, average_into_kernel, static_cast<unsigned>(ew_blocks(n + m)), kT, 0, s, st, sum_x, sum_y, x, y, n, m);
   return ok();
 }
 
 int pdlpk_scale_mul(const double* scale, const double* v, double* out, int64_t n,
                     cudaStream_t s) {
-  if (n > 0) scale_mul_kernel<<<ew_blocks(n), kT, 0, s>>>(scale, v, out, n);
+  if (n > 0) launch_pdl(PDLPK_PDL_CADENCE, scale_mul_kernel, static_cast<unsigned>(ew_blocks(n)), kT, 0, s, scale, v, out, n);
   return ok();
 }
 
@@ -441,7 +453,7 @@ int pdlpk_ray_dual_finish(const pdlpk_problem* P, int32_t orig, const double* ax
 
 int pdlpk_radius(const double* dx2, const double* dy2, double omega, double* out,
                  cudaStream_t s) {
-  radius_kernel<<<1, 1, 0, s>>>(dx2, dy2, omega, out);
+  launch_pdl(PDLPK_PDL_CADENCE, radius_kernel, static_cast<unsigned>(1), 1, 0, s, dx2, dy2, omega, out);
   return ok();
 }
 
@@ -449,7 +461,7 @@ int pdlpk_apply_vec_factors(double* lc, double* uc, double* row_scale, const dou
                             int64_t m, double* c, double* lv, double* uv, double* col_scale,
                             const double* fc, int64_t n, cudaStream_t s) {
   if (m + n > 0) {
-    apply_vec_factor_kernel<<<ew_blocks(m + n), kT, 0, s>>>(lc, uc, row_scale, fr, m, c, lv, uv,
+    launch_pdl(PDLPK_PDL_CADENCE, apply_vec_factor_kernel, static_cast<unsigned>(ew_blocks(m + n)), kT, 0, s, lc, uc, row_scale, fr, m, c, lv, uv,
                                                            col_scale, fc, n);
   }
   return ok();
@@ -485,7 +497,7 @@ int pdlpk_primal_weight_sums(const double* c, int64_t n, const double* lc, const
 
 int pdlpk_initial_point(const double* lv, const double* uv, double* x, int64_t n,
                         cudaStream_t s) {
-  if (n > 0) initial_point_kernel<<<ew_blocks(n), kT, 0, s>>>(lv, uv, x, n);
+  if (n > 0) launch_pdl(PDLPK_PDL_CADENCE, initial_point_kernel, static_cast<unsigned>(ew_blocks(n)), kT, 0, s, lv, uv, x, n);
   return ok();
 }
 
@@ -493,7 +505,7 @@ int pdlpk_dual_feas_bounds(const double* c, const double* lv, const double* uv, 
                            const double* lc, const double* uc, int64_t m, double* sub_lc,
                            double* sub_uc, double* sub_lv, double* sub_uv, cudaStream_t s) {
   if (n + m > 0) {
-    dual_feas_bounds_kernel<<<ew_blocks(n + m), kT, 0, s>>>(c, lv, uv, n, lc, uc, m, sub_lc,
+    launch_pdl(PDLPK_PDL_CADENCE, dual_feas_bounds_kernel, static_cast<unsigned>(ew_blocks(n + m)), kT, 0, s, c, lv, uv, n, lc, uc, m, sub_lc,
                                                            sub_uc, sub_lv, sub_uv);
   }
   return ok();
@@ -501,7 +513,7 @@ int pdlpk_dual_feas_bounds(const double* c, const double* lv, const double* uv, 
 
 int pdlpk_check_finite(const double* v, int64_t n, int32_t code, int32_t* first,
                        cudaStream_t s) {
-  if (n > 0) find_nonfinite_kernel<<<ew_blocks(n), kT, 0, s>>>(v, n, code, first);
+  if (n > 0) launch_pdl(PDLPK_PDL_CADENCE, find_nonfinite_kernel, static_cast<unsigned>(ew_blocks(n)), kT, 0, s, v, n, code, first);
   return ok();
 }
 
