@@ -56,12 +56,25 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def step_kernel_bytes(m: int, n: int, nnz: int) -> dict:
+def uniform_vectors(p) -> int:
+    """How many of c, l_v, u_v the solver reads as a scalar: bitwise uniform
+    and 0 or +-inf (the only uniform values column scaling keeps uniform)."""
+    import numpy as np
+    k = 0
+    for v in (p.objective, p.var_lower, p.var_upper):
+        b = v.view(np.int64)
+        if b.size and np.all(b == b[0]) and (v[0] == 0.0 or np.isinf(v[0])):
+            k += 1
+    return k
+
+
+def step_kernel_bytes(m: int, n: int, nnz: int, uniform: int = 0) -> dict:
     """Algorithmic bytes per launch of each perf-mode step kernel (SURVEY.md
-    §8(d) dataflow: every array touched once; int32 indices/row pointers)."""
+    §8(d) dataflow: every array touched once; int32 indices/row pointers).
+    uniform: vectors among c, l_v, u_v the primal pass takes as a scalar."""
     return {
         # R x, c, aty, l_v, u_v; W x', xbar; R+W sum_x (deferred average)
-        "primal_pass": 8 * 9 * n,
+        "primal_pass": 8 * (9 - uniform) * n,
         # CSR(K) 12 nnz + 4(m+1); gather xbar once (8n); R y, l_c, u_c; W y', dy; R+W sum_y
         "row_pass": 12 * nnz + 4 * (m + 1) + 8 * n + 8 * 7 * m,
         # CSR(K^T) 12 nnz + 4(n+1); gather dy once (8m); R aty, x, x'; W aty'
@@ -222,7 +235,7 @@ def run_ours(args) -> None:
         e2e_wall = float(t.item())
     e2e_value = e2e_res.iterations / e2e_wall
 
-    kb = step_kernel_bytes(m, n, nnz)
+    kb = step_kernel_bytes(m, n, nnz, uniform_vectors(p))
     names = ["primal_pass", "row_pass", "col_pass"]
     per = {}
     if world == 1 and not args.sharded:

@@ -86,9 +86,15 @@ __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a, pdl
   double2* __restrict__ xn2 = reinterpret_cast<double2*>(xn);
   double2* __restrict__ xb2 = reinterpret_cast<double2*>(xbar);
   double2* __restrict__ sx2 = reinterpret_cast<double2*>(sx);
+  // bitwise-uniform vectors come from their scalar (no stream)
+  const uint32_t uni = a.P.uniform;
+  const double2 cu = make_double2(a.P.c_u, a.P.c_u), lu = make_double2(a.P.lv_u, a.P.lv_u),
+                uu = make_double2(a.P.uv_u, a.P.uv_u);
   for (int64_t p = tid; p < n2; p += stride) {
     const double2 xi = x2[p], ai = a2[p];
-    const double2 ci = __ldcs(c2 + p), li = __ldcs(l2 + p), ui = __ldcs(u2 + p);
+    const double2 ci = (uni & 1u) ? cu : __ldcs(c2 + p);
+    const double2 li = (uni & 2u) ? lu : __ldcs(l2 + p);
+    const double2 ui = (uni & 4u) ? uu : __ldcs(u2 + p);
     double2 xp, xb;
     xp.x = clampd(xi.x - tau * (ci.x - ai.x), li.x, ui.x);
     xp.y = clampd(xi.y - tau * (ci.y - ai.y), li.y, ui.y);
@@ -121,7 +127,9 @@ __global__ void __launch_bounds__(kEwThreads) primal_pass(pdlpk_step_args a, pdl
   if ((n & 1) && tid == 0) {
     const int64_t i = n - 1;
     const double xi = x[i];
-    const double xp = clampd(xi - tau * (c[i] - aty[i]), lv[i], uv[i]);
+    const double ci = (uni & 1u) ? cu.x : c[i], li = (uni & 2u) ? lu.x : lv[i],
+                 ui = (uni & 4u) ? uu.x : uv[i];
+    const double xp = clampd(xi - tau * (ci - aty[i]), li, ui);
     xn[i] = xp;
     xbar[i] = 2.0 * xp - xi;
     if constexpr (Push) {

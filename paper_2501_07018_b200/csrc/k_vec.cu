@@ -24,6 +24,28 @@ inline int ew_blocks(int64_t n) {
   return b < 1 ? 1 : static_cast<int>(b);
 }
 
+// Bitwise OR / AND of the patterns of v (exact, order-free).
+__global__ void __launch_bounds__(kT) uniform_bits_kernel(const double* __restrict__ v, int64_t n,
+                                                          unsigned long long* or_and) {
+  pdl_wait_cadence();
+  unsigned long long o = 0ull, a = ~0ull;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v[i]));
+    o |= b;
+    a &= b;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    o |= __shfl_xor_sync(0xffffffffu, o, d);
+    a &= __shfl_xor_sync(0xffffffffu, a, d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(or_and, o);
+    atomicAnd(or_and + 1, a);
+  }
+}
+
 #define GRID_STRIDE(i, n)                                                                   \
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); \
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -247,6 +269,11 @@ using namespace pdlp;
 extern "C" {
 
 int64_t pdlpk_red_scratch_doubles(void) { return 8 * kRedMaxBlocks; }
+
+int pdlpk_uniform_bits(const double* v, int64_t n, unsigned long long* or_and, cudaStream_t s) {
+  if (n > 0) launch_pdl(PDLPK_PDL_CADENCE, uniform_bits_kernel, static_cast<unsigned>(ew_blocks(n)), kT, 0, s, v, n, or_and);
+  return ok();
+}
 
 int pdlpk_index_to_i32(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s) {
   if (n > 0) launch_pdl(PDLPK_PDL_CADENCE, i64_to_i32_kernel, static_cast<unsigned>(ew_blocks(n)), kT, 0, s, src, dst, n);

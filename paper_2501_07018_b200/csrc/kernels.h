@@ -153,7 +153,18 @@ typedef struct pdlpk_problem {
   const double *c, *lc, *uc, *lv, *uv;           /* scaled */
   const double *c_o, *lc_o, *uc_o, *lv_o, *uv_o; /* original */
   const double *row_scale, *col_scale;           /* m, n */
+  /* Bitwise-uniform scaled vectors (bit 0 c, 1 l_v, 2 u_v) and their value:
+   * the primal pass then uses the scalar instead of streaming the vector
+   * (x >= 0 problems, the zero objective of the polishing subproblems).
+   * 0 = no assumption. */
+  uint32_t uniform;
+  uint32_t _pad_uniform;
+  double c_u, lv_u, uv_u;
 } pdlpk_problem;
+
+/* or_and[0] |= OR of v's 64-bit patterns, or_and[1] &= AND (caller seeds 0 /
+ * all-ones): v is bitwise uniform iff they are equal. */
+int pdlpk_uniform_bits(const double* v, int64_t n, unsigned long long* or_and, cudaStream_t s);
 
 typedef struct pdlpk_step_args {
   pdlpk_problem P;

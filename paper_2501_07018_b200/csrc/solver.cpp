@@ -568,10 +568,16 @@ struct DevProblem {
   DevBuf<double> c_o, lc_o, uc_o, lv_o, uv_o;  // original
   DevBuf<double> row_scale, col_scale;
 
+  uint32_t uniform = 0;  // pdlpk_problem::uniform of the scaled c, l_v, u_v
+  double c_u = 0.0, lv_u = 0.0, uv_u = 0.0;
   pdlpk_problem view() const {
     pdlpk_problem P{};
     P.m = m;
     P.n = n;
+    P.uniform = uniform;
+    P.c_u = c_u;
+    P.lv_u = lv_u;
+    P.uv_u = uv_u;
     P.K = row.view;
     P.KT = col.view;
     P.c = c.get();
@@ -1792,10 +1798,34 @@ class Engine {
   bool attempt_polish(const pdlpk_problem& P, const InnerCfg& cfg, Inner& D);
 
   pdlpk_problem primal_feas_view(const pdlpk_problem& P) {
-    pdlpk_problem Q = P;
+    pdlpk_problem Q = P;  // l_v, u_v (and their uniform flags) are P's
     Q.c = zeros_n_.get();
     Q.c_o = zeros_n_.get();
+    Q.uniform = (P.uniform & ~1u) | (dist() ? 0u : 1u);  // c = +0.0 everywhere
+    Q.c_u = 0.0;
     return Q;
+  }
+
+  // Which of the scaled c, l_v, u_v are bitwise uniform (one sync; after
+  // preconditioning, which scales them in place).  Not on sharded solves.
+  void detect_uniform() {
+    prob_.uniform = 0;
+    if (dist() || prob_.n == 0) return;
+    DevBuf<unsigned long long> bits(6);
+    const unsigned long long seed[6] = {0ull, ~0ull, 0ull, ~0ull, 0ull, ~0ull};
+    PDLP_CK(cudaMemcpyAsync(bits.get(), seed, sizeof(seed), cudaMemcpyHostToDevice, s()));
+    const double* v[3] = {prob_.c.get(), prob_.lv.get(), prob_.uv.get()};
+    for (int q = 0; q < 3; ++q) PDLP_LAUNCH(pdlpk_uniform_bits(v[q], prob_.n, bits.get() + 2 * q, s()));
+    unsigned long long h[6];
+    PDLP_CK(cudaMemcpyAsync(h, bits.get(), sizeof(h), cudaMemcpyDeviceToHost, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));
+    double* out[3] = {&prob_.c_u, &prob_.lv_u, &prob_.uv_u};
+    for (int q = 0; q < 3; ++q) {
+      if (h[2 * q] == h[2 * q + 1]) {
+        prob_.uniform |= 1u << q;
+        std::memcpy(out[q], &h[2 * q], sizeof(double));
+      }
+    }
   }
 
   pdlpk_problem dual_feas_view(const pdlpk_problem& P) {
@@ -1823,6 +1853,8 @@ class Engine {
     Q.KT = P.K;
     Q.c = zeros_m_.get();
     Q.c_o = zeros_m_.get();
+    Q.uniform = dist() ? 0u : 1u;  // c = +0.0; the derived bounds are not checked
+    Q.c_u = 0.0;
     Q.lc = sub_lc_.get();
     Q.uc = sub_uc_.get();
     Q.lv = sub_lv_.get();
@@ -2255,6 +2287,7 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
   g_alloc_seconds = 0.0;
   Engine E(problem, *o, comm);  // uploads and validates on device
   if (o->enable_scaling) E.precondition(o->ruiz_passes, o->pock_chambolle != 0);
+  if (std::getenv("PDLP_NO_UNIFORM") == nullptr) E.detect_uniform();
   if (E.dist()) E.build_full_views();
   if (o->enable_polish) {
     // The polishing subproblems' states are allocated mid-loop, the first

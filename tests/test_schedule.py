@@ -45,3 +45,22 @@ def test_threaded_schedule_equals_sequential(gpu, monkeypatch):
         assert a.iterations == b.iterations == 300
         np.testing.assert_array_equal(a.x.view(np.int64), b.x.view(np.int64))
         np.testing.assert_array_equal(a.y.view(np.int64), b.y.view(np.int64))
+
+
+@pytest.mark.gpu
+def test_uniform_vectors_are_bit_identical(gpu, monkeypatch):
+    """Bitwise-uniform scaled c / l_v / u_v (x >= 0 problems; the polishing
+    subproblems' zero objective) are read as scalars by the primal pass: the
+    same values, so the same bits as streaming them."""
+    cases = [P.generate("c1", 6, sources=300, sinks=400),      # l_v = 0, u_v = inf everywhere
+             P.generate("c0", 7, rows=300, cols=600)]           # mixed bounds: no flags but c' = 0 in polish
+    for p in cases:
+        tol = P.relative_tolerances(p, 1e-4)
+        o = P.SolverOptions(mode="perf", tolerances=P.TerminationTolerances(*tol))
+        monkeypatch.setenv("PDLP_NO_UNIFORM", "1")
+        a = P.solve(p, o)
+        monkeypatch.delenv("PDLP_NO_UNIFORM")
+        b = P.solve(p, o)
+        assert (a.status, a.iterations, a.polish_iterations) == (b.status, b.iterations, b.polish_iterations)
+        np.testing.assert_array_equal(a.x.view(np.int64), b.x.view(np.int64))
+        np.testing.assert_array_equal(a.y.view(np.int64), b.y.view(np.int64))

@@ -44,7 +44,7 @@ def measure(cfg: str, steps: int, warmup: int, ttt_limit: float) -> dict:
     res = P.solve(p, bench._options(P, steps, warmup, **extra))
     value = res.timed_iterations / res.timed_seconds
     prof = P.solve(p, bench._options(P, steps, warmup, profile_kernels=True, **extra))
-    kb = bench.step_kernel_bytes(m, n, nnz)
+    kb = bench.step_kernel_bytes(m, n, nnz, bench.uniform_vectors(p))
     peak, peak_src = bench._peaks()
     per = {}
     for q, nm in enumerate(["primal_pass", "row_pass", "col_pass"]):
