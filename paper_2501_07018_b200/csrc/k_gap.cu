@@ -145,6 +145,11 @@ struct GapIn {
   const double *x, *y, *ax, *aty;
   int64_t n, m;
   double omega;
+  uint32_t uni;          // pdlpk_problem::uniform: scalar c / l_v / u_v
+  double cu, lvu, uvu;
+  __device__ __forceinline__ double cc(int64_t i) const { return (uni & 1u) ? cu : c[i]; }
+  __device__ __forceinline__ double lo(int64_t i) const { return (uni & 2u) ? lvu : lv[i]; }
+  __device__ __forceinline__ double hi(int64_t i) const { return (uni & 4u) ? uvu : uv[i]; }
 };
 
 // Per-coordinate logic of restarts.hpp:117-170: the b_inf / c_inf
@@ -171,9 +176,9 @@ __device__ __forceinline__ Coord gap_coord(const GapIn& g, int64_t t) {
   const double omega = g.omega;
   if (t < g.n) {
     const int64_t i = t;
-    const double gg = g.aty[i] - g.c[i];
+    const double gg = g.aty[i] - g.cc(i);
     if (gg == 0.0) return o;
-    const double off = (gg > 0.0 ? g.uv[i] : g.lv[i]) - g.x[i];
+    const double off = (gg > 0.0 ? g.hi(i) : g.lo(i)) - g.x[i];
     if (off == 0.0) return o;
     o.b = gg * gg / omega;
     o.mass_use |= 1u;
@@ -463,8 +468,8 @@ __global__ void finalize_perf_kernel(Work w, int64_t E, const double* r_slot, do
 
 // Candidate coordinate (assemble_candidate, restarts.hpp:73-101).
 __device__ __forceinline__ double cand_x(const GapIn& g, int64_t i, double lambda) {
-  const double gg = g.aty[i] - g.c[i];
-  return clampd(g.x[i] + gg / (lambda * g.omega), g.lv[i], g.uv[i]);
+  const double gg = g.aty[i] - g.cc(i);
+  return clampd(g.x[i] + gg / (lambda * g.omega), g.lo(i), g.hi(i));
 }
 
 __device__ __forceinline__ double cand_y(const GapIn& g, int64_t j, double lambda) {
@@ -496,7 +501,7 @@ __global__ void value_seq_kernel(GapIn g, Work w, const double* r_slot, double r
   double value = 0.0;
   for (int64_t i = 0; i < g.n; ++i) {
     const double xh = cand_x(g, i, lambda);
-    value += g.c[i] * (g.x[i] - xh) + g.aty[i] * xh;
+    value += g.cc(i) * (g.x[i] - xh) + g.aty[i] * xh;
   }
   for (int64_t j = 0; j < g.m; ++j) {
     const double yh = cand_y(g, j, lambda);
@@ -526,7 +531,8 @@ __global__ void value_finish_kernel(const double* sum, const double* r_slot, dou
 
 GapIn make_in(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
               const double* aty, double omega) {
-  return GapIn{P->c, P->lv, P->uv, P->lc, P->uc, x, y, ax, aty, P->n, P->m, omega};
+  return GapIn{P->c, P->lv, P->uv, P->lc, P->uc, x, y, ax, aty, P->n, P->m, omega,
+               P->uniform, P->c_u, P->lv_u, P->uv_u};
 }
 
 }  // namespace
@@ -727,7 +733,7 @@ extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const d
     const double lambda = *lam_star;
     if (t < g.n) {
       const double xh = cand_x(g, t, lambda);
-      v[0] = g.c[t] * (g.x[t] - xh) + g.aty[t] * xh;
+      v[0] = g.cc(t) * (g.x[t] - xh) + g.aty[t] * xh;
       return 1u;
     }
     const int64_t j = t - g.n;
