@@ -381,6 +381,9 @@ int pdlpk_screen(const pdlpk_problem* P, int32_t orig, const double* x, const do
   const double* uv = orig ? P->uv_o : P->uv;
   const double* rs = orig ? nullptr : P->row_scale;
   const double* cs = orig ? nullptr : P->col_scale;
+  // scaled space: bitwise-uniform c / l_v / u_v come from their scalar
+  const uint32_t uni = orig ? 0u : P->uniform;
+  const double cu = P->c_u, lu = P->lv_u, uu = P->uv_u;
   // values: 0 primal_inf (max), 1 dual_inf (max), 2 pobj (sum), 3 penalty (sum)
   auto f = [=] __device__(int64_t t, double* v) -> unsigned {
     if (t < m) {
@@ -393,16 +396,18 @@ int pdlpk_screen(const pdlpk_problem* P, int32_t orig, const double* x, const do
     }
     const int64_t i = t - m;
     const double xi = x[i];
-    const double d = interval_distance(xi, lv[i], uv[i]);
+    const double ci = (uni & 1u) ? cu : c[i], li = (uni & 2u) ? lu : lv[i],
+                 ui = (uni & 4u) ? uu : uv[i];
+    const double d = interval_distance(xi, li, ui);
     v[0] = cs ? d * cs[i] : d;
     // rc_mode 2: r is given (read from r_out), as in kkt_residuals(p, x, y, r)
-    const double ri = rc_mode == 2 ? r_out[i] : reduced_cost(c[i], aty[i], xi, lv[i], uv[i], rc_mode);
+    const double ri = rc_mode == 2 ? r_out[i] : reduced_cost(ci, aty[i], xi, li, ui, rc_mode);
     if (r_out && rc_mode != 2) r_out[i] = ri;
-    const double dd = fabs(c[i] - aty[i] - ri);
+    const double dd = fabs(ci - aty[i] - ri);
     v[1] = cs ? dd / cs[i] : dd;
-    v[2] = c[i] * xi;
+    v[2] = ci * xi;
     unsigned use = 7u;
-    if (penalty_term(ri, lv[i], uv[i], v[3])) use |= 8u;
+    if (penalty_term(ri, li, ui, v[3])) use |= 8u;
     return use;
   };
   return multi_reduce<4>(f, m + n, red->parity ? PDLPK_RED_SEQ : PDLPK_RED_TREE, red->shards,
