@@ -12,7 +12,7 @@ import re
 import subprocess
 import sys
 
-ALG_MB = {"primal_pass": 288.0, "row_pass": 128.24, "col_pass": 240.03}  # C1, SURVEY 8(d)
+ALG_MB = {"primal_pass": 224.0, "row_pass": 128.24, "col_pass": 240.03}  # C1; primal: l_v, u_v uniform
 
 
 def short(n: str) -> str:
