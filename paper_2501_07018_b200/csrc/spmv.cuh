@@ -45,7 +45,10 @@
 
 namespace pdlp {
 
-constexpr int kSpmvThreads = 256;
+#ifndef PDLPK_SPMV_THREADS
+#define PDLPK_SPMV_THREADS 256
+#endif
+constexpr int kSpmvThreads = PDLPK_SPMV_THREADS;
 constexpr int kSpmvWarps = kSpmvThreads / 32;
 constexpr int kShortMax = PDLPK_SHORT_MAX;  // longest tiled line
 constexpr int kChunk = PDLPK_CHUNK;         // entries per warp chunk of a long line
