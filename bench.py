@@ -324,7 +324,8 @@ def run_ours(args) -> None:
                         "cold_seconds": ttt_cold.solve_seconds,
                         "tolerance": "1e-4 relative (eps_p=1e-4(1+|b|inf), eps_d=1e-4(1+|c|inf))"},
         "gpu_launches": launches,
-        "gpu_launches_note": ("the step kernels only (3 per attempt, counted exactly); the cadence's "
+        "gpu_launches_note": (f"the step kernels only ({launches // max(res.timed_attempts, 1)} per "
+                              "attempt, counted exactly); the cadence's "
                               "reductions, products, gap and CUB sort/scan kernels add about 0.6 "
                               "launches per step kernel (profiles/r1_launches_v6.md)"),
         "clocks": clocks.summary(),
