@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <math_constants.h>
 
 #include "kernels.h"  // tuning defaults (PDLPK_PDL, ...)
@@ -177,10 +178,20 @@ __device__ __forceinline__ void pdl_trigger_cadence() {
 // <<<>>> or, with pdl, cudaLaunchKernelEx with programmatic stream
 // serialization.  Only for kernels that begin with pdl_enter(): their wait
 // keeps the dependence on the previous kernel of the stream.
+// PDLP_NO_PDL=1 in the environment launches everything plainly (tests
+// compare the two).
+inline bool pdl_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("PDLP_NO_PDL");
+    return e != nullptr && e[0] == '1';
+  }();
+  return off;
+}
+
 template <class... KArgs, class... Args>
 inline void launch_pdl(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block,
                        size_t smem, cudaStream_t s, Args... args) {
-  if (!(PDLPK_PDL && pdl)) {
+  if (!(PDLPK_PDL && pdl) || pdl_disabled()) {
     kern<<<grid, block, smem, s>>>(args...);
     return;
   }

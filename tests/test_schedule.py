@@ -64,3 +64,35 @@ def test_uniform_vectors_are_bit_identical(gpu, monkeypatch):
         assert (a.status, a.iterations, a.polish_iterations) == (b.status, b.iterations, b.polish_iterations)
         np.testing.assert_array_equal(a.x.view(np.int64), b.x.view(np.int64))
         np.testing.assert_array_equal(a.y.view(np.int64), b.y.view(np.int64))
+
+
+def _solve_in_subprocess(env_extra, cfg, kw):
+    """A solve in a fresh process (PDLP_NO_PDL is read once per process)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json, numpy as np, paper_2501_07018_b200 as P\n"
+        f"p = P.generate({cfg!r}, 8, **{kw!r})\n"
+        "tol = P.relative_tolerances(p, 1e-4)\n"
+        "r = P.solve(p, P.SolverOptions(mode='perf', tolerances=P.TerminationTolerances(*tol)))\n"
+        "print(json.dumps({'it': r.iterations, 'pol': r.polish_iterations,"
+        " 'x': r.x.view(np.int64).tolist()[:2000], 'hx': int(np.bitwise_xor.reduce(r.x.view(np.int64))),"
+        " 'hy': int(np.bitwise_xor.reduce(r.y.view(np.int64)))}))\n")
+    env = dict(os.environ, **env_extra)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+@pytest.mark.gpu
+def test_programmatic_dependent_launch_is_bit_identical(gpu):
+    """The step chain and the cadence's kernels launched with programmatic
+    dependent launch (each waits on griddepcontrol.wait) give the same bits as
+    plain launches: whole solves to 1e-4, polishing included."""
+    for cfg, kw in (("c1", {"sources": 300, "sinks": 400}), ("c0", {"rows": 400, "cols": 800})):
+        a = _solve_in_subprocess({"PDLP_NO_PDL": "1"}, cfg, kw)
+        b = _solve_in_subprocess({}, cfg, kw)
+        assert a == b
