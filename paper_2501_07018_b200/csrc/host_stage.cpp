@@ -2,6 +2,7 @@
 #include "host_stage.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -183,10 +184,14 @@ Ring& ring() {
 }
 
 // src bytes per destination byte: 2 when narrowing int64 -> int32
+// PDLP_TIMING: time in slot waits vs host copies (stage_report()).
+double g_wait_s = 0.0, g_copy_s = 0.0, g_bytes = 0.0;
+
 void stage_h2d_impl(void* dst, const void* src, size_t bytes, cudaStream_t s, bool narrow) {
   Ring& R = ring();
   std::lock_guard<std::mutex> g(R.mu);
   R.bind_device();
+  using C = std::chrono::steady_clock;
   const char* in = static_cast<const char*>(src);
   char* out = static_cast<char*>(dst);
   const size_t ratio = narrow ? 2 : 1;
@@ -195,8 +200,14 @@ void stage_h2d_impl(void* dst, const void* src, size_t bytes, cudaStream_t s, bo
     const int k = R.next;
     R.next = (R.next + 1) % kSlots;
     const size_t len = std::min(kChunk, bytes - off);
+    const auto t0 = C::now();
     if ((err = R.acquire(k)) != cudaSuccess) break;
+    const auto t1 = C::now();
     R.pool.run(R.slot[k], in + off * ratio, len, narrow);
+    const auto t2 = C::now();
+    g_wait_s += std::chrono::duration<double>(t1 - t0).count();
+    g_copy_s += std::chrono::duration<double>(t2 - t1).count();
+    g_bytes += static_cast<double>(len);
     if ((err = cudaMemcpyAsync(out + off, R.slot[k], len, cudaMemcpyHostToDevice, s)) != cudaSuccess)
       break;
     err = R.release(k, s);
@@ -205,6 +216,13 @@ void stage_h2d_impl(void* dst, const void* src, size_t bytes, cudaStream_t s, bo
 }
 
 }  // namespace
+
+void stage_report(double* wait_s, double* copy_s, double* mbytes) {
+  *wait_s = g_wait_s;
+  *copy_s = g_copy_s;
+  *mbytes = g_bytes / 1048576.0;
+  g_wait_s = g_copy_s = g_bytes = 0.0;
+}
 
 void stage_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return;

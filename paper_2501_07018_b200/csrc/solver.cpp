@@ -922,10 +922,13 @@ class Engine {
     dev_zero(zeros_m_.get(), m, s());
     PDLP_CK(cudaStreamSynchronize(s()));
     if (timing) {
+      double sw = 0.0, sc = 0.0, smb = 0.0;
+      stage_report(&sw, &sc, &smb);
       std::fprintf(stderr,
                    "phase=setup event=load row_layout=%.4f col_layout=%.4f vectors=%.4f "
-                   "validate=%.4f consistency=%.4f rest=%.4f\n",
-                   t_row, t_col, t_vec, t_valid, t_cons, lap());
+                   "validate=%.4f consistency=%.4f rest=%.4f staged_mb=%.1f slot_wait=%.4f "
+                   "host_copy=%.4f\n",
+                   t_row, t_col, t_vec, t_valid, t_cons, lap(), smb, sw, sc);
     }
   }
 
