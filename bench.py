@@ -38,9 +38,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: keep NCCL's version banner off it
-if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-    os.environ["NCCL_DEBUG"] = "WARN"
+# stdout carries exactly one JSON line: NCCL prints its version banner (and
+# any log) at every NCCL_DEBUG level from VERSION up, so its output goes to
+# stderr instead; the level itself is left as the environment sets it.
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "PDHG iters/sec, time to 1e-4 rel. KKT, achieved HBM GB/s vs peak"
 UNIT = "iters/s"
@@ -332,7 +333,7 @@ def run_ours(args) -> None:
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -359,10 +360,32 @@ def run_reference(args) -> None:
         "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    emit(line)
+
+
+# stdout carries exactly one JSON line.  Libraries print on the C-level
+# stdout too (NCCL's version banner at NCCL_DEBUG=VERSION/WARN goes there
+# whatever NCCL_DEBUG_FILE says), so fd 1 points at stderr for the whole run
+# and is restored only to print the line.
+_REAL_STDOUT = None
+
+
+def _stdout_to_stderr() -> None:
+    global _REAL_STDOUT
+    sys.stdout.flush()
+    _REAL_STDOUT = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    sys.stdout.flush()
+    if _REAL_STDOUT is not None:
+        os.dup2(_REAL_STDOUT, 1)
     print(json.dumps(line), flush=True)
 
 
 def main():
+    _stdout_to_stderr()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2048)

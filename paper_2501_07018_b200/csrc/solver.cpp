@@ -2215,6 +2215,12 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
     int64_t target = (D.k() / cfg.check_interval + 1) * cfg.check_interval;
     target = std::min(target, cfg.budget);
     if (cfg.observer != nullptr) target = D.k() + 1;
+    // A timed run whose warm-up ends inside this block stops there first, so
+    // the timed region opens exactly after the warm-up (block boundaries
+    // only decide when the host reads the controller: same values).
+    if (!timing_started_ && &D == &main_ && timing_warmup_ > D.k() && timing_warmup_ < target) {
+      target = timing_warmup_;
+    }
     if (cfg.fixed_eta.has_value() && D.hs.eta != *cfg.fixed_eta) {
       D.hs.eta = *cfg.fixed_eta;
       write_state(D);

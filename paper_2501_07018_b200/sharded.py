@@ -88,9 +88,9 @@ def extract_shard(problem: LpProblem, rank: int, world: int) -> dict:
 
 
 def _quiet_nccl() -> None:
-    # NCCL_DEBUG=VERSION (or unset on some images) prints a banner on stdout
-    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-        os.environ["NCCL_DEBUG"] = "WARN"
+    # NCCL prints its version banner (and logs) on stdout at every NCCL_DEBUG
+    # level from VERSION up: send them to stderr, keep the level
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 
 def nccl_unique_id() -> bytes:
