@@ -361,6 +361,21 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
     for (int32_t sl : g.cc_slot) cc_slot.push_back(sl < 0 ? sl : static_cast<int32_t>(sl + n_multi));
     n_multi += g.n_multi;
   }
+  if (std::getenv("PDLP_WARP_INTERLEAVE") != nullptr && ck_row.size() > 1) {
+    // measurement only: warp lines in the order 0, h, 1, h+1, ... (h = half)
+    const size_t nw = ck_row.size(), h = (nw + 1) / 2;
+    auto perm = [&](auto& v) {
+      auto w = v;
+      for (size_t c = 0; c < nw; ++c) v[c] = w[(c & 1) ? h + c / 2 : c / 2];
+    };
+    if (nw % 2 == 0) {
+      perm(ck_row);
+      perm(ck_beg);
+      perm(ck_len);
+      perm(ck_pos);
+      perm(ck_slot);
+    }
+  }
   const int64_t n_cta_chunks = static_cast<int64_t>(cc_row.size());
   ck_row.insert(ck_row.end(), cc_row.begin(), cc_row.end());
   ck_beg.insert(ck_beg.end(), cc_beg.begin(), cc_beg.end());
