@@ -228,6 +228,8 @@ struct RowEpi {
   double sigma, w;
   bool pend;
   uint64_t keep = 0;  // L2 evict_last policy for dy (gathered by the column pass)
+  double* lp = nullptr;  // line_partials: per-line terms (part2[r], part2[m + r])
+  int64_t lm = 0;
   double dy2 = 0.0, infy = 0.0;
   struct Pre {
     double y, lc, uc;
@@ -262,6 +264,11 @@ struct RowEpi {
     dy[r] = d;
 #endif
     if (pend) sy[r] = sy[r] + w * yr;
+    if (lp != nullptr) {
+      lp[r] = d * d;
+      lp[lm + r] = fabs(yp);
+      return;
+    }
     dy2 += d * d;
     infy = max_keep(infy, fabs(yp));
   }
@@ -287,8 +294,13 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) row_pass(p
 #endif
   e.pend = st->avg_pending != 0;
   e.w = st->avg_w;
+  if (a.line_partials) {
+    e.lp = a.part2;
+    e.lm = a.P.m;
+  }
   sched_spmv<P, Seg>(a.P.K, a.P.K.value, a.xbar, e);
   pdl_trigger();
+  if (a.line_partials) return;  // per-line terms already written
   __shared__ double red[32];
   const double s1 = block_sum(e.dy2, red);
   __syncthreads();
@@ -371,11 +383,30 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(p
   if (!last) return;
   __threadfence();
   // Last CTA: combine every partial in a fixed order, then decide.
-  const int64_t g2 = sched_blocks(a.P.K);
   double dy2 = 0.0, infy = 0.0, dx2 = 0.0, curv = 0.0, infx = 0.0;
-  for (int64_t b = threadIdx.x; b < g2; b += blockDim.x) {
-    dy2 += __ldcg(a.part2 + b);
-    infy = max_keep(infy, __ldcg(a.part2 + g2 + b));
+  if (a.line_partials) {
+    // per-line terms, grouped by line index into blocks of 8 summed as an
+    // 8-warp CTA's block_sum adds one line per warp -- the grouping the
+    // per-CTA partials had when every warp took one line in order -- then
+    // strided over the blocks like the CTA partials: independent of the
+    // SpMV schedule
+    const int64_t m = a.P.m, nb8 = (m + 7) / 8;
+    for (int64_t b = threadIdx.x; b < nb8; b += blockDim.x) {
+      double v[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const int64_t r = 8 * b + w;
+        v[w] = r < m ? __ldcg(a.part2 + r) : 0.0;
+        if (r < m) infy = max_keep(infy, __ldcg(a.part2 + m + r));
+      }
+      dy2 += ((v[0] + v[4]) + (v[2] + v[6])) + ((v[1] + v[5]) + (v[3] + v[7]));
+    }
+  } else {
+    const int64_t g2 = sched_blocks(a.P.K);
+    for (int64_t b = threadIdx.x; b < g2; b += blockDim.x) {
+      dy2 += __ldcg(a.part2 + b);
+      infy = max_keep(infy, __ldcg(a.part2 + g2 + b));
+    }
   }
   for (int64_t b = threadIdx.x; b < g3; b += blockDim.x) {
     dx2 += __ldcg(a.part3 + b);
@@ -740,7 +771,9 @@ using namespace pdlp;
 
 extern "C" int64_t pdlpk_step_partials(const pdlpk_problem* P) {
   const int64_t g2 = sched_blocks(P->K), g3 = sched_blocks(P->KT);
-  return (2 * g2 > 3 * g3 ? 2 * g2 : 3 * g3) + 64;
+  int64_t need = 2 * g2 > 3 * g3 ? 2 * g2 : 3 * g3;
+  if (P->m <= PDLPK_LINE_PARTIALS_MAX && 2 * P->m > need) need = 2 * P->m;  // line_partials
+  return need + 64;
 }
 
 extern "C" int pdlpk_arm(pdlpk_step_state* st, int64_t k_target, cudaStream_t s) {

@@ -185,7 +185,14 @@ typedef struct pdlpk_step_args {
   int32_t mode;  /* PDLP_MODE_PERF / PDLP_MODE_PARITY */
   int32_t shards;
   double* shard_part; /* parity: 4*shards partials */
+  /* 1: the row pass writes each line's |dy|^2 and |y'| terms to part2[r],
+   * part2[m + r] and the decision sums them in line order, so the step's
+   * reductions do not depend on the SpMV schedule (perf mode, one GPU,
+   * m <= PDLPK_LINE_PARTIALS_MAX). */
+  int32_t line_partials;
+  int32_t _pad_lp;
 } pdlpk_step_args;
+#define PDLPK_LINE_PARTIALS_MAX 262144
 
 /* Reduction context for cadence operations. */
 typedef struct pdlpk_red {

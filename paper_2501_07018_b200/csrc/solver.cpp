@@ -159,6 +159,9 @@ bool direct_tiles(const int64_t* start, int64_t dim) {
   return true;
 }
 
+// Set around the row layout's upload (Engine::load_parts).
+thread_local bool g_interleave_warp_lines = false;
+
 // Line segments of a schedule build: [lo, hi) line ranges built by host
 // threads (fixed boundaries, so the schedule is deterministic) and joined in
 // line order.  A tile never spans a segment boundary.
@@ -361,8 +364,12 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
     for (int32_t sl : g.cc_slot) cc_slot.push_back(sl < 0 ? sl : static_cast<int32_t>(sl + n_multi));
     n_multi += g.n_multi;
   }
-  if (std::getenv("PDLP_WARP_INTERLEAVE") != nullptr && ck_row.size() > 1) {
-    // measurement only: warp lines in the order 0, h, 1, h+1, ... (h = half)
+  if (g_interleave_warp_lines && ck_row.size() > 1) {
+    // warp lines in the order 0, h, 1, h+1, ... (h = half): a layout whose
+    // slow lines cluster (C1's strided demand rows) spreads them over the
+    // CTAs and SMs.  Only for the row layout when the row pass writes
+    // per-line partials (step_args().line_partials): the step's reductions
+    // then do not depend on the order, so neither do the iterates.
     const size_t nw = ck_row.size(), h = (nw + 1) / 2;
     auto perm = [&](auto& v) {
       auto w = v;
@@ -852,7 +859,13 @@ class Engine {
     DevBuf<unsigned long long> keys(4);
     DevBuf<unsigned> bad(1);
     PDLP_CK(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned), s()));
+    {
+      const char* e = std::getenv("PDLP_NO_INTERLEAVE");
+      g_interleave_warp_lines = comm_ == nullptr && m <= PDLPK_LINE_PARTIALS_MAX &&
+                                line_partials_on_ && !(e != nullptr && e[0] == '1');
+    }
     upload_layout(by_row, n_glob_, bad.get(), prob_.row, s());
+    g_interleave_warp_lines = false;
     const double t_row = lap();
     upload_layout(by_col, m, bad.get(), prob_.col, s());
     const double t_col = lap();
@@ -1350,6 +1363,8 @@ class Engine {
     a.mode = parity_ ? PDLP_MODE_PARITY : PDLP_MODE_PERF;
     a.shards = shards_;
     a.shard_part = D.shard_part.get();
+    a.line_partials = (!parity_ && !dist() && P.m <= PDLPK_LINE_PARTIALS_MAX && line_partials_on_)
+                          ? 1 : 0;
     return a;
   }
 
@@ -1940,6 +1955,11 @@ class Engine {
     return e != nullptr && e[0] == '1';
   }();
   // PDLP_GAP_PARTIAL=0: always the full sort (measurements)
+  // PDLP_LINE_PARTIALS=0: per-CTA row-pass partials (schedule-dependent)
+  bool line_partials_on_ = [] {
+    const char* e = std::getenv("PDLP_LINE_PARTIALS");
+    return !(e != nullptr && e[0] == '0');
+  }();
   bool gap_any_window_ = [] {
     const char* e = std::getenv("PDLP_GAP_WINDOWS");
     return e != nullptr && std::strcmp(e, "any") == 0;

@@ -96,3 +96,20 @@ def test_programmatic_dependent_launch_is_bit_identical(gpu):
         a = _solve_in_subprocess({"PDLP_NO_PDL": "1"}, cfg, kw)
         b = _solve_in_subprocess({}, cfg, kw)
         assert a == b
+
+
+@pytest.mark.gpu
+def test_interleaved_warp_lines_are_bit_identical(gpu, monkeypatch):
+    """With per-line row-pass partials the step's reductions do not depend on
+    the SpMV schedule: interleaving the row layout's warp lines changes no
+    bit of the iterates."""
+    for p in (P.generate("c1", 9, sources=300, sinks=400), P.generate("c0", 9, rows=500, cols=900)):
+        tol = P.relative_tolerances(p, 1e-4)
+        o = P.SolverOptions(mode="perf", tolerances=P.TerminationTolerances(*tol))
+        monkeypatch.setenv("PDLP_NO_INTERLEAVE", "1")
+        a = P.solve(p, o)
+        monkeypatch.delenv("PDLP_NO_INTERLEAVE")
+        b = P.solve(p, o)
+        assert (a.iterations, a.polish_iterations) == (b.iterations, b.polish_iterations)
+        np.testing.assert_array_equal(a.x.view(np.int64), b.x.view(np.int64))
+        np.testing.assert_array_equal(a.y.view(np.int64), b.y.view(np.int64))
