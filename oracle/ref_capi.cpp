@@ -17,6 +17,7 @@
 #include <pdhglp/solver.hpp>
 #include <pdhglp/step.hpp>
 
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -488,6 +489,62 @@ int ref_validate(const pdlp_problem_view* pv, char* msg, int32_t msg_len) {
   std::snprintf(msg, static_cast<size_t>(msg_len), "%s (index %lld)", issue->message.c_str(),
                 static_cast<long long>(issue->index));
   return 1;
+}
+
+// Timing harness of the bench's reference arm (bench.py --impl reference):
+// the unmodified solve() with tolerances unreachable, an iteration limit of
+// warmup + steps, and an observer that only takes a steady_clock stamp
+// (solver.hpp:521-529 calls it after every accepted main-loop step; no copy
+// of x or y).  The window runs from the stamp of iteration `warmup` to the
+// return of solve(): `steps` iterations plus the budget-hit cadence at the
+// end (solver.hpp:358-360), the same span the GPU arm's timed region covers.
+// out[0] = window seconds, out[1] = iterations in the window, out[2] =
+// seconds from the call to the window start (problem build, validation,
+// rescaling, warm-up iterations), out[3] = total seconds, out[4] = restarts,
+// out[5] = step retries.  stamps (optional, n_stamps doubles): seconds since
+// the call of each accepted iteration k at stamps[k].
+int ref_time_window(const pdlp_problem_view* pv, int32_t threads, int32_t shards_per_thread,
+                    int64_t warmup, int64_t steps, double* out, double* stamps,
+                    int64_t n_stamps) {
+  return guarded([&] {
+    using Clock = std::chrono::steady_clock;
+    const auto t0 = Clock::now();
+    const int64_t w = warmup < 1 ? 1 : warmup;
+    const LpProblem p = to_problem(pv);
+    SolverOptions s{};
+    s.tolerances.eps_primal = 0.0;
+    s.tolerances.eps_dual = 0.0;
+    s.tolerances.eps_rel_gap = 0.0;
+    s.iteration_limit = w + steps;
+    s.threads = threads;
+    s.shards_per_thread = shards_per_thread;
+    Clock::time_point tw = t0;
+    Index kw = -1;
+    s.observer = [&](const IterationRecord& rec) {
+      const auto now = Clock::now();
+      if (stamps != nullptr && rec.iteration >= 0 && rec.iteration < n_stamps) {
+        stamps[rec.iteration] = std::chrono::duration<double>(now - t0).count();
+      }
+      if (kw < 0 && rec.iteration >= w) {
+        kw = rec.iteration;
+        tw = now;
+      }
+    };
+    const SolveResult r = solve(p, s);
+    const auto t1 = Clock::now();
+    if (kw < 0) {
+      g_err = "ref_time_window: the solve stopped before the window opened (" +
+              std::string(solve_status_name(r.status)) + ")";
+      return PDLP_ERR_INTERNAL;
+    }
+    out[0] = std::chrono::duration<double>(t1 - tw).count();
+    out[1] = static_cast<double>(r.iterations - kw);
+    out[2] = std::chrono::duration<double>(tw - t0).count();
+    out[3] = std::chrono::duration<double>(t1 - t0).count();
+    out[4] = static_cast<double>(r.restarts);
+    out[5] = static_cast<double>(r.step_retries);
+    return PDLP_OK;
+  });
 }
 
 }  // extern "C"

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpdlp_b200.so")
+# PDLP_LIB: an alternative build of the same library (tuning sweeps only)
+LIB_PATH = os.environ.get("PDLP_LIB") or os.path.join(HERE, "libpdlp_b200.so")
 GEN_LIB_PATH = os.path.join(HERE, "libpdlp_gen.so")
 
 c_double_p = C.POINTER(C.c_double)

@@ -19,7 +19,8 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
+# PDLP_BUILD_DIR / PDLP_LIB: build a variant elsewhere (tuning sweeps with PDLP_DEFINES)
+OBJ = os.environ.get("PDLP_BUILD_DIR") or os.path.join(HERE, "_build")
 INCLUDE = os.path.join(ROOT, "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -40,7 +41,7 @@ CU_SOURCES = ["k_step.cu", "k_vec.cu", "k_gap.cu", "k_scale.cu", "k_valid.cu", "
 CPP_SOURCES = ["solver.cpp", "host_stage.cpp", "comm.cpp", "shard.cpp", "mps.cpp"]
 HEADERS = ["common.cuh", "spmv.cuh", "reduce.cuh", "kernels.h", "device.hpp", "host_stage.hpp", "comm.hpp", "shard.hpp"]
 
-LIB = os.path.join(HERE, "libpdlp_b200.so")
+LIB = os.environ.get("PDLP_LIB") or os.path.join(HERE, "libpdlp_b200.so")
 GEN_LIB = os.path.join(HERE, "libpdlp_gen.so")
 
 

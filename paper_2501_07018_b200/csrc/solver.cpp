@@ -1945,6 +1945,41 @@ class Engine {
     gap_join_ = std::make_unique<Event>();
     gap_scratch2_.alloc(red_scratch_.size());
   }
+  // Products on the side stream run concurrently with products of the same
+  // layouts on the main stream.  A layout's multi-chunk lines combine through
+  // per-layout scratch (chunk_part, chunk_cnt arrival counters, line_acc), so
+  // the side stream works on a copy of the layout's view whose scratch is its
+  // own (keyed by the main scratch; counters start at zero and the last CTA
+  // of each line resets them).
+  struct SideScratch {
+    DevBuf<double> part, acc;
+    DevBuf<unsigned> cnt;
+  };
+  std::map<const void*, SideScratch> side_scratch_;
+  pdlpk_csr side_csr(const pdlpk_csr& A) {
+    pdlpk_csr B = A;
+    if (A.n_chunks == 0) return B;
+    SideScratch& sc = side_scratch_[static_cast<const void*>(A.chunk_cnt)];
+    if (sc.cnt.size() < static_cast<size_t>(A.n_chunks)) {
+      sc.part.alloc(A.n_chunks);
+      sc.cnt.alloc(A.n_chunks);
+      PDLP_CK(cudaMemsetAsync(sc.cnt.get(), 0, A.n_chunks * sizeof(unsigned), g_alloc_stream));
+      PDLP_CK(cudaStreamSynchronize(g_alloc_stream));
+    }
+    if (sc.acc.size() < static_cast<size_t>(A.n_multi * PDLPK_LINE_ACC)) {
+      sc.acc.alloc(A.n_multi * PDLPK_LINE_ACC);
+    }
+    B.chunk_part = sc.part.get();
+    B.chunk_cnt = sc.cnt.get();
+    B.line_acc = sc.acc.get();
+    return B;
+  }
+  pdlpk_problem side_problem(const pdlpk_problem& P) {
+    pdlpk_problem Q = P;
+    Q.K = side_csr(P.K);
+    Q.KT = side_csr(P.KT);
+    return Q;
+  }
   DevBuf<double> side_prod_;  // the average ray's A^T product
   std::unique_ptr<Stream> gap_side_;  // second gap query's stream
   DevBuf<double> gap_scratch2_;
@@ -2084,8 +2119,10 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
       cudaStream_t sa = s();
       pdlpk_red ra = rr;
       double* prod_a = D.prod_n.get();
+      pdlpk_problem Ps = P;  // the side stream's view: own chunk scratch
       if (side) {
         ensure_side();
+        Ps = side_problem(P);
         sa = gap_side_->get();
         ra.scratch = gap_scratch2_.get();
         if (side_prod_.size() < static_cast<size_t>(P.n)) side_prod_.alloc(P.n);
@@ -2099,13 +2136,13 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
         PDLP_LAUNCH(pdlpk_average_into(D.state.get(), D.sum_x.get(), D.sum_y.get(), D.avg_x.get(),
                                        D.avg_y.get(), P.n, P.m, sa));
         if (side) {
-          PDLP_LAUNCH(pdlpk_spmv(&P.K, 0, D.avg_x.get(), D.ax_avg.get(), parity_, sa));
-          PDLP_LAUNCH(pdlpk_spmv(&P.KT, 0, D.avg_y.get(), D.aty_avg.get(), parity_, sa));
-          PDLP_LAUNCH(pdlpk_screen(&P, 0, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
+          PDLP_LAUNCH(pdlpk_spmv(&Ps.K, 0, D.avg_x.get(), D.ax_avg.get(), parity_, sa));
+          PDLP_LAUNCH(pdlpk_spmv(&Ps.KT, 0, D.avg_y.get(), D.aty_avg.get(), parity_, sa));
+          PDLP_LAUNCH(pdlpk_screen(&Ps, 0, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
                                    D.aty_avg.get(), cfg.rc_mode, &ra, D.rc_b.get(),
                                    slot(kSlotScrAvg), sa));
           if (cfg.detect_infeasibility) {
-            enqueue_rays(P, D, cands, cands.size() - 1, cands.size(), sa, &ra, prod_a);
+            enqueue_rays(Ps, D, cands, cands.size() - 1, cands.size(), sa, &ra, prod_a);
           }
           if (want_restart) {
             PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_x.get(), D.ref_x.get(), P.n, &ra,

@@ -139,8 +139,11 @@ __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
 #ifndef PDLPK_CHUNK_MIN_BLOCKS
 #define PDLPK_CHUNK_MIN_BLOCKS 4 /* CTAs/SM the chunk-only kernels are compiled for */
 #endif
+#ifndef PDLPK_TILE_MIN_BLOCKS
+#define PDLPK_TILE_MIN_BLOCKS 4 /* CTAs/SM the staged-tile kernels are compiled for */
+#endif
 __host__ __device__ constexpr int spmv_min_blocks(int seg) {
-  return seg == 2 ? 5 : (seg == 1 ? PDLPK_CHUNK_MIN_BLOCKS : 4);
+  return seg == 2 ? 5 : (seg == 1 ? PDLPK_CHUNK_MIN_BLOCKS : ((seg & 4) ? PDLPK_TILE_MIN_BLOCKS : 4));
 }
 
 // Chunk segments are grid-stride with a bounded number of CTAs: a pass pays

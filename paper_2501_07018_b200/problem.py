@@ -239,3 +239,37 @@ def relative_tolerances(p: LpProblem, eps: float = 1e-4) -> tuple[float, float, 
     bmax = float(np.max(np.abs(b))) if b.size else 0.0
     cmax = float(np.max(np.abs(p.objective))) if p.objective.size else 0.0
     return eps * (1.0 + bmax), eps * (1.0 + cmax), eps
+
+
+# On-disk form of an LpProblem: one .npy per array plus the shape, so a large
+# seeded instance is generated once and memory-mapped by later processes (the
+# bench's reference arm reads it without importing this package).
+_ARRAYS = ("row_start", "row_index", "row_value", "col_start", "col_index", "col_value",
+           "objective", "con_lower", "con_upper", "var_lower", "var_upper")
+
+
+def save_problem(p: LpProblem, path: str) -> None:
+    import json
+    import os
+    os.makedirs(path, exist_ok=True)
+    arrs = (p.a.by_row.start, p.a.by_row.index, p.a.by_row.value, p.a.by_col.start,
+            p.a.by_col.index, p.a.by_col.value, p.objective, p.con_lower, p.con_upper,
+            p.var_lower, p.var_upper)
+    for name, a in zip(_ARRAYS, arrs):
+        np.save(os.path.join(path, name + ".npy"), np.ascontiguousarray(a))
+    with open(os.path.join(path, "shape.json"), "w") as f:
+        json.dump({"rows": p.rows(), "cols": p.cols(), "nnz": p.a.nonzeros()}, f)
+
+
+def load_problem(path: str) -> LpProblem:
+    """Memory-mapped, read-only arrays (the solver only reads its inputs)."""
+    import json
+    import os
+    with open(os.path.join(path, "shape.json")) as f:
+        shape = json.load(f)
+    a = {name: np.load(os.path.join(path, name + ".npy"), mmap_mode="r") for name in _ARRAYS}
+    return LpProblem(
+        SparseMatrix(shape["rows"], shape["cols"],
+                     CompressedLayout(a["row_start"], a["row_index"], a["row_value"]),
+                     CompressedLayout(a["col_start"], a["col_index"], a["col_value"])),
+        a["objective"], a["con_lower"], a["con_upper"], a["var_lower"], a["var_upper"])

@@ -1,0 +1,900 @@
+// SpMV design lab (measurement probe, not product code): C2-shaped matrices
+// generated on the device, candidate row-pass / column-pass kernels timed
+// with CUDA events against their algorithmic bytes.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false \
+//        -o tools/spmv_lab/lab tools/spmv_lab/lab.cu
+//   tools/spmv_lab/lab [m] [n] [sorted]
+//
+// C2 recipe: column counts ~ discrete power law alpha=2 on [2, 1e4], entries
+// of a column at uniform random rows; |a| log-uniform [1e-3, 1e3].
+// sorted=1 numbers the columns by decreasing count (degree ordering).
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) {                                                          \
+      std::fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+      std::exit(1);                                                                   \
+    }                                                                                 \
+  } while (0)
+
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ inline double u01(uint64_t h) { return ((h >> 11) + 1) * (1.0 / 9007199254740992.0); }
+
+__global__ void counts_kernel(int32_t* cnt, int64_t n, uint64_t seed) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    int k = 0;
+    for (uint64_t t = 0;; ++t) {
+      const double u = u01(mix64(seed ^ (uint64_t(j) * 0x100000001b3ull + t)));
+      const double kk = floor(2.0 / u);
+      if (kk <= 10000.0) { k = (int)kk; break; }
+    }
+    cnt[j] = k;
+  }
+}
+
+// entries of column j: rows at random; key = (row << 24) | col for the row layout
+__global__ void entries_kernel(const int64_t* cstart, int64_t n, int64_t m, uint64_t seed,
+                               uint64_t* key_row, uint64_t* key_col) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; j < n;
+       j += (int64_t)gridDim.x * blockDim.x / 32) {
+    for (int64_t e = cstart[j] + lane; e < cstart[j + 1]; e += 32) {
+      const uint64_t r = mix64(seed * 31 + e) % uint64_t(m);
+      key_row[e] = (r << 24) | uint64_t(j);
+      key_col[e] = (uint64_t(j) << 23) | r;
+    }
+  }
+}
+
+__device__ inline double entry_value(uint64_t r, uint64_t c) {
+  const uint64_t h = mix64(r * 0x9e3779b97f4a7c15ull ^ c);
+  const double mag = exp(log(1e-3) + u01(h) * (log(1e3) - log(1e-3)));
+  return (h & 1) ? -mag : mag;
+}
+
+__global__ void split_row(const uint64_t* key, int64_t nnz, int32_t* idx, double* val, int32_t* rowcnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = key[e] >> 24, c = key[e] & 0xffffff;
+    idx[e] = (int32_t)c;
+    val[e] = entry_value(r, c);
+    atomicAdd(rowcnt + r, 1);
+  }
+}
+__global__ void split_col(const uint64_t* key, int64_t nnz, int32_t* idx, double* val) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = key[e] >> 23, r = key[e] & 0x7fffff;
+    idx[e] = (int32_t)r;
+    val[e] = entry_value(r, c);
+  }
+}
+__global__ void fill_kernel(double* v, int64_t n, uint64_t seed, double lo, double hi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = lo + (hi - lo) * u01(mix64(seed ^ i));
+}
+__global__ void i64_to_i32(const int64_t* a, int32_t* b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (int32_t)a[i];
+}
+
+struct Csr {
+  int64_t dim = 0, nnz = 0, other = 0;
+  int32_t* start = nullptr;  // dim+1
+  int32_t* idx = nullptr;
+  double* val = nullptr;
+  std::vector<int32_t> hstart;
+};
+
+// --------------------------------------------------------------- kernels ---
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double clampd(double v, double lo, double hi) { return fmin(fmax(v, lo), hi); }
+
+template <class T>
+__device__ __forceinline__ T ldcs(const T* p) { return __ldcs(p); }
+
+// Row-pass epilogue (dual update): R y, l_c, u_c; W y', dy; |dy|^2 partial.
+struct RowEpi {
+  const double *y, *lc, *uc;
+  double *yn, *dy;
+  double sigma;
+  double acc2 = 0.0;
+  struct Pre { double y, lc, uc; };
+  __device__ __forceinline__ Pre load(int64_t r) const { return {ldcs(y + r), ldcs(lc + r), ldcs(uc + r)}; }
+  __device__ __forceinline__ void line(int64_t r, double s, const Pre& p) {
+    const double yhat = p.y - sigma * s;
+    const double proj = clampd(yhat / sigma, -p.uc, -p.lc);
+    const double yp = yhat - sigma * proj;
+    yn[r] = yp;
+    const double d = yp - p.y;
+    dy[r] = d;
+    acc2 += d * d;
+  }
+  static constexpr int kRW = 5;  // 8-byte words per line
+};
+// Column-pass epilogue: R aty, x, x'; W aty'; |dx|^2, curvature partials.
+struct ColEpi {
+  const double *aty, *x, *xn;
+  double* atyn;
+  double acc2 = 0.0, curv = 0.0;
+  struct Pre { double a, x, xn; };
+  __device__ __forceinline__ Pre load(int64_t i) const { return {ldcs(aty + i), ldcs(x + i), xn[i]}; }
+  __device__ __forceinline__ void line(int64_t i, double d, const Pre& p) {
+    atyn[i] = p.a + d;
+    const double dx = p.xn - p.x;
+    acc2 += dx * dx;
+    curv += d * dx;
+  }
+  static constexpr int kRW = 4;
+};
+
+// Uniform warp items.  Block item {r0, cnt > 0}: lines r0..r0+cnt-1 (<= 63
+// lines, <= ITEM entries, each line <= SEQMAX), products in a per-warp shared
+// buffer, each lane sums its line in storage order.  Chunk item {r, -1-c,
+// slot, nch}: entries [start[r] + c*ITEM, ...) of a long line, lane chains
+// + warp tree; multi-chunk lines combine in chunk order in the last arriver.
+template <int ITEM, class Epi, int MINB>
+__global__ void __launch_bounds__(256, MINB) wb_kernel(const int4* __restrict__ items, int64_t n_items,
+                                                       const int32_t* __restrict__ start,
+                                                       const int32_t* __restrict__ idx,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ v, Epi epi,
+                                                       double* part, unsigned* cnt, double* out_part) {
+  constexpr int J = ITEM / 32;
+  __shared__ double sp_all[8][ITEM];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* sp = sp_all[wid];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = gw; it < n_items; it += nw) {
+    const int4 d = items[it];
+    if (d.y > 0) {
+      const int r0 = d.x, cnt_l = d.y;
+      const int p0 = lane <= cnt_l ? start[r0 + lane] : 0;
+      const int p1 = lane + 32 <= cnt_l ? start[r0 + 32 + lane] : 0;
+      const int s0 = __shfl_sync(0xffffffffu, p0, 0);
+      const int s1 = cnt_l <= 31 ? __shfl_sync(0xffffffffu, p0, cnt_l & 31)
+                                 : __shfl_sync(0xffffffffu, p1, (cnt_l - 32) & 31);
+      typename Epi::Pre pre0{}, pre1{};
+      if (lane < cnt_l) pre0 = epi.load(r0 + lane);
+      if (lane + 32 < cnt_l) pre1 = epi.load(r0 + 32 + lane);
+      int ci[J];
+      double a[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int k = s0 + j * 32 + lane;
+        if (k < s1) {
+          ci[j] = ldcs(idx + k);
+          a[j] = ldcs(val + k);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int k = s0 + j * 32 + lane;
+        if (k < s1) sp[j * 32 + lane] = a[j] * __ldg(v + ci[j]);
+      }
+      __syncwarp();
+      // line ends: lane l's line is [p(l), p(l+1))
+      const int q0 = __shfl_down_sync(0xffffffffu, p0, 1);
+      const int p1first = __shfl_sync(0xffffffffu, p1, 0);
+      const int e0 = lane == 31 ? p1first : q0;
+      if (lane < cnt_l) {
+        double acc = 0.0;
+        for (int k = p0 - s0; k < e0 - s0; ++k) acc += sp[k];
+        epi.line(r0 + lane, acc, pre0);
+      }
+      const int q1 = __shfl_down_sync(0xffffffffu, p1, 1);
+      if (lane + 32 < cnt_l) {
+        double acc = 0.0;
+        for (int k = p1 - s0; k < q1 - s0; ++k) acc += sp[k];
+        epi.line(r0 + 32 + lane, acc, pre1);
+      }
+      __syncwarp();
+    } else {
+      const int r = d.x, c = -1 - d.y, nch = d.w;
+      const int lo = start[r] + c * ITEM;
+      const int e = start[r + 1];
+      const int hi = lo + ITEM < e ? lo + ITEM : e;
+      typename Epi::Pre pre{};
+      if (nch == 1 && lane == 0) pre = epi.load(r);
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      int ci[J];
+      double a[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int k = lo + j * 32 + lane;
+        if (k < hi) {
+          ci[j] = ldcs(idx + k);
+          a[j] = ldcs(val + k);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int k = lo + j * 32 + lane;
+        if (k < hi) acc[j & 3] += a[j] * __ldg(v + ci[j]);
+      }
+      const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+      if (lane == 0) {
+        if (nch == 1) {
+          epi.line(r, t, pre);
+        } else {
+          part[d.z + c] = t;
+          __threadfence();
+          const unsigned old = atomicAdd(cnt + d.z, 1u);
+          if (old == (unsigned)(nch - 1)) {
+            __threadfence();
+            double tot = 0.0;
+            for (int q = 0; q < nch; ++q) tot += __ldcg(part + d.z + q);
+            cnt[d.z] = 0;
+            epi.line(r, tot, epi.load(r));
+          }
+        }
+      }
+    }
+  }
+  // per-CTA partial (lab: only to keep the epilogue's reduction work)
+  double s = warp_sum(epi.acc2);
+  if (lane == 0) out_part[blockIdx.x * 8 + wid] = s;
+}
+
+// CSR-vector reference: G lanes per line, tree sum (lines <= any length).
+template <int G, class Epi, int MINB>
+__global__ void __launch_bounds__(256, MINB) vec_kernel(int64_t dim, const int32_t* __restrict__ start,
+                                                        const int32_t* __restrict__ idx,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ v, Epi epi,
+                                                        double* out_part) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % G;
+  const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t base = g0 - (g0 % (32 / G)); base < dim; base += ng) {
+    const int64_t r = base + (lane / G);
+    double acc = 0.0;
+    typename Epi::Pre pre{};
+    if (r < dim) {
+      if (sub == 0) pre = epi.load(r);
+      const int s = start[r], e = start[r + 1];
+      for (int k = s + sub; k < e; k += G) acc += ldcs(val + k) * __ldg(v + ldcs(idx + k));
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (r < dim && sub == 0) epi.line(r, acc, pre);
+  }
+  double s = warp_sum(epi.acc2);
+  if (lane == 0) out_part[blockIdx.x * 8 + (threadIdx.x >> 5)] = s;
+}
+
+// Column panels: the row layout re-laid out panel-major (entries of column
+// panel p of every row, then panel p+1), one pass per panel carrying each
+// row's partial sum; only the last pass runs the epilogue.
+template <int G, class Epi, int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) panel_kernel(int64_t dim, const int32_t* __restrict__ start,
+                                                          const int32_t* __restrict__ idx,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ v, Epi epi,
+                                                          double* __restrict__ carry, double* out_part) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % G;
+  const int64_t g0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t base = g0 - (g0 % (32 / G)); base < dim; base += ng) {
+    const int64_t r = base + (lane / G);
+    double acc = 0.0;
+    typename Epi::Pre pre{};
+    double cin = 0.0;
+    if (r < dim) {
+      if (MODE == 2 && sub == 0) pre = epi.load(r);
+      if (MODE != 0 && sub == 0) cin = __ldcs(carry + r);
+      const int s = start[r], e = start[r + 1];
+      for (int k = s + sub; k < e; k += G) acc += ldcs(val + k) * __ldg(v + ldcs(idx + k));
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (r < dim && sub == 0) {
+      acc += cin;
+      if (MODE == 2) epi.line(r, acc, pre);
+      else __stcs(carry + r, acc);
+    }
+  }
+  if (MODE == 2) {
+    double s = warp_sum(epi.acc2);
+    if (lane == 0) out_part[blockIdx.x * 8 + (threadIdx.x >> 5)] = s;
+  }
+}
+
+__global__ void panel_count(const int32_t* st, const int32_t* idx, int64_t m, int P, int64_t W, int32_t* cnt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
+    for (int k = st[r]; k < st[r + 1]; ++k) cnt[(int64_t)(idx[k] / W) * m + r] += 1;
+}
+__global__ void panel_scatter(const int32_t* st, const int32_t* idx, const double* val, int64_t m, int P,
+                              int64_t W, const int64_t* pst, int32_t* nidx, double* nval) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t pos[8];
+    for (int p = 0; p < P; ++p) pos[p] = pst[p * m + r];
+    for (int k = st[r]; k < st[r + 1]; ++k) {
+      const int p = (int)(idx[k] / W);
+      nidx[pos[p]] = idx[k];
+      nval[pos[p]] = val[k];
+      ++pos[p];
+    }
+  }
+}
+
+// Random-gather throughput probe: `count` gathers of v[hash % len], UNROLL
+// independent per thread per round (no index stream).
+template <int UNROLL>
+__global__ void __launch_bounds__(256) gather_probe(const double* __restrict__ v, int64_t len, int64_t count,
+                                                    double* out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int64_t b = tid * UNROLL; b < count; b += nt * UNROLL) {
+    double g[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      uint32_t h = static_cast<uint32_t>(b + u) * 0x9E3779B1u;
+      h ^= h >> 15;
+      h *= 0x85EBCA77u;
+      h ^= h >> 13;
+      g[u] = __ldg(v + __umulhi(h, static_cast<uint32_t>(len)));
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) acc += g[u];
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
+// ---------------------------------------------- warp-private TMA rings ---
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}"
+               ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+struct WinL { const char* src; uint32_t bytes, shift; };
+__device__ __forceinline__ WinL winl(const void* base, int64_t first, int64_t count, int esz) {
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(base) + first * esz;
+  const uintptr_t hi = lo + count * esz;
+  const uintptr_t alo = lo & ~uintptr_t(15), ahi = (hi + 15) & ~uintptr_t(15);
+  return WinL{reinterpret_cast<const char*>(alo), count > 0 ? (uint32_t)(ahi - alo) : 0u, (uint32_t)(lo - alo)};
+}
+struct RingHdr { int r0, cnt, s0, len; uint32_t sh; int pad[3]; };
+struct RowStage {  // staged operands of the row epilogue
+  static constexpr int kStaged = 3;
+};
+
+// Tiles {r0, cnt, s0, len} of consecutive short lines.  Warp 0 lane 0 is the
+// producer; consumer warp w owns stages [w][0..S).  Each tile goes to one
+// consumer warp whole: gather phase (G gathers in flight per lane, products
+// in place), then one lane per line sums in storage order and runs the
+// epilogue from the staged operands.
+template <int CW, int S, int G, class Epi>
+__global__ void __launch_bounds__(32 * (CW + 1), 1) wr_kernel(const int4* __restrict__ tiles, int64_t n_tiles,
+                                                              const int32_t* __restrict__ start,
+                                                              const int32_t* __restrict__ idx,
+                                                              const double* __restrict__ val,
+                                                              const double* __restrict__ v, Epi epi,
+                                                              const double* st0, const double* st1,
+                                                              const double* st2, int E, int L,
+                                                              double* out_part) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + CW * S;
+  RingHdr* hdr = reinterpret_cast<RingHdr*>(sm + 16 * CW * S);
+  const uint32_t o_val = (uint32_t)((4 * E + 32 + 15) & ~15);
+  const uint32_t o_ptr = o_val + (uint32_t)((8 * E + 32 + 15) & ~15);
+  const uint32_t o_epi = o_ptr + (uint32_t)((4 * (L + 1) + 32 + 15) & ~15);
+  const uint32_t epi_stride = (uint32_t)((8 * L + 32 + 15) & ~15);
+  const uint32_t stage_bytes = o_epi + 3 * epi_stride;
+  unsigned char* stage0 = sm + ((16 * CW * S + sizeof(RingHdr) * CW * S + 127) & ~127);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < CW * S; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t G0 = gridDim.x;
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first();
+      int64_t i = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += G0, ++i) {
+        const int w = (int)(i % CW);
+        const int64_t j = i / CW;
+        const int s = (int)(j % S);
+        const int q = w * S + s;
+        if (j >= S) mbar_wait(&empty[q], (uint32_t)(((j / S) - 1) & 1));
+        const int4 d = tiles[t];
+        unsigned char* buf = stage0 + (size_t)q * stage_bytes;
+        const WinL wi = winl(idx, d.z, d.w, 4), wv = winl(val, d.z, d.w, 8), wp = winl(start, d.x, d.y + 1, 4);
+        const WinL w0 = winl(st0, d.x, d.y, 8), w1 = winl(st1, d.x, d.y, 8), w2 = winl(st2, d.x, d.y, 8);
+        RingHdr h;
+        h.r0 = d.x; h.cnt = d.y; h.s0 = d.z; h.len = d.w;
+        h.sh = wi.shift | (wv.shift << 4) | (wp.shift << 8) | (w0.shift << 12) | (w1.shift << 16) | (w2.shift << 20);
+        hdr[q] = h;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&full[q], wi.bytes + wv.bytes + wp.bytes + w0.bytes + w1.bytes + w2.bytes);
+        if (wi.bytes) bulk(buf, wi.src, wi.bytes, &full[q], pol);
+        if (wv.bytes) bulk(buf + o_val, wv.src, wv.bytes, &full[q], pol);
+        if (wp.bytes) bulk(buf + o_ptr, wp.src, wp.bytes, &full[q], pol);
+        if (w0.bytes) bulk(buf + o_epi, w0.src, w0.bytes, &full[q], pol);
+        if (w1.bytes) bulk(buf + o_epi + epi_stride, w1.src, w1.bytes, &full[q], pol);
+        if (w2.bytes) bulk(buf + o_epi + 2 * epi_stride, w2.src, w2.bytes, &full[q], pol);
+      }
+    }
+  } else {
+    const int w = warp - 1;
+    int64_t j = 0;
+    for (int64_t t = blockIdx.x + (int64_t)w * G0; t < n_tiles; t += (int64_t)CW * G0, ++j) {
+      const int s = (int)(j % S);
+      const int q = w * S + s;
+      mbar_wait(&full[q], (uint32_t)((j / S) & 1));
+      const RingHdr h = hdr[q];
+      unsigned char* buf = stage0 + (size_t)q * stage_bytes;
+      const int32_t* s_idx = reinterpret_cast<const int32_t*>(buf + (h.sh & 15u));
+      double* s_val = reinterpret_cast<double*>(buf + o_val + ((h.sh >> 4) & 15u));
+      const int32_t* s_ptr = reinterpret_cast<const int32_t*>(buf + o_ptr + ((h.sh >> 8) & 15u));
+      const double* e0 = reinterpret_cast<const double*>(buf + o_epi + ((h.sh >> 12) & 15u));
+      const double* e1 = reinterpret_cast<const double*>(buf + o_epi + epi_stride + ((h.sh >> 16) & 15u));
+      const double* e2 = reinterpret_cast<const double*>(buf + o_epi + 2 * epi_stride + ((h.sh >> 20) & 15u));
+      for (int e = lane; e < h.len; e += 32 * G) {
+        int ci[G];
+        double g[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+          if (e + 32 * u < h.len) ci[u] = s_idx[e + 32 * u];
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+          if (e + 32 * u < h.len) g[u] = __ldg(v + ci[u]);
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+          if (e + 32 * u < h.len) s_val[e + 32 * u] *= g[u];
+      }
+      __syncwarp();
+      for (int l = lane; l < h.cnt; l += 32) {
+        const int a = s_ptr[l] - h.s0, b = s_ptr[l + 1] - h.s0;
+        double acc = 0.0;
+        for (int k = a; k < b; ++k) acc += s_val[k];
+        epi.line(h.r0 + l, acc, typename Epi::Pre{e0[l], e1[l], e2[l]});
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[q]);
+    }
+  }
+  double s2 = warp_sum(epi.acc2);
+  if (lane == 0) out_part[blockIdx.x * 32 + warp] = s2;
+}
+
+std::vector<int4> build_tiles(const std::vector<int32_t>& st, int E, int L, int seqmax) {
+  std::vector<int4> t;
+  const int64_t dim = (int64_t)st.size() - 1;
+  int r0 = -1, cnt = 0, nz = 0;
+  auto close = [&] {
+    if (cnt > 0) t.push_back(make_int4(r0, cnt, st[r0], nz));
+    cnt = 0;
+    nz = 0;
+  };
+  for (int64_t r = 0; r < dim; ++r) {
+    const int len = st[r + 1] - st[r];
+    if (len > seqmax) { close(); continue; }
+    if (cnt == L || nz + len > E) close();
+    if (cnt == 0) r0 = (int)r;
+    ++cnt;
+    nz += len;
+  }
+  close();
+  return t;
+}
+
+// ------------------------------------------------------------- schedule ---
+std::vector<int4> build_items(const std::vector<int32_t>& st, int item, int seqmax, int64_t& n_slots,
+                              bool long_only = false) {
+  std::vector<int4> chunks, blocks;
+  const int64_t dim = (int64_t)st.size() - 1;
+  int64_t slots = 0;
+  int r0 = -1, cnt = 0, nz = 0;
+  auto close = [&] {
+    if (cnt > 0) blocks.push_back(make_int4(r0, cnt, 0, 0));
+    cnt = 0;
+    nz = 0;
+  };
+  for (int64_t r = 0; r < dim; ++r) {
+    const int len = st[r + 1] - st[r];
+    if (len > seqmax) {
+      const int nch = (len + item - 1) / item;
+      for (int c = 0; c < nch; ++c) chunks.push_back(make_int4((int)r, -1 - c, (int)slots, nch));
+      slots += nch;
+      continue;  // (a long line does not close the open block: blocks are line runs)
+    }
+    if (cnt == 63 || nz + len > item || (cnt > 0 && r != r0 + cnt)) close();
+    if (cnt == 0) r0 = (int)r;
+    ++cnt;
+    nz += len;
+  }
+  close();
+  if (long_only) blocks.clear();
+  n_slots = slots;
+  // long chunks first (they are the same cost per item as blocks)
+  std::vector<int4> all = chunks;
+  all.insert(all.end(), blocks.begin(), blocks.end());
+  return all;
+}
+
+// ---------------------------------------------------------------- driver ---
+struct Vecs {
+  double *xb, *y, *lc, *uc, *yn, *dy;      // row pass: gather xb (n)
+  double *aty, *x, *xn, *atyn, *dyg;       // column pass: gather dy (m)
+};
+
+template <class F>
+float time_it(F&& f, int reps) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  f();
+  CK(cudaDeviceSynchronize());
+  cudaEventRecord(a);
+  for (int i = 0; i < reps; ++i) f();
+  cudaEventRecord(b);
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  CK(cudaGetLastError());
+  return ms * 1000.0f / reps;
+}
+
+int main(int argc, char** argv) {
+  const int64_t m = argc > 1 ? atoll(argv[1]) : 5000000;
+  const int64_t n = argc > 2 ? atoll(argv[2]) : 10000000;
+  const int sorted = argc > 3 ? atoi(argv[3]) : 0;
+  const char* only = argc > 4 ? argv[4] : nullptr;  // run the variants whose label contains this
+  double peak = 6549.1;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+
+  int32_t* cnt;
+  CK(cudaMalloc(&cnt, n * 4));
+  counts_kernel<<<4096, 256>>>(cnt, n, 12345);
+  if (sorted) {  // degree ordering: column 0 has the largest count
+    int32_t* tmp;
+    CK(cudaMalloc(&tmp, n * 4));
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeysDescending(nullptr, tb, cnt, tmp, (int)n);
+    void* t;
+    CK(cudaMalloc(&t, tb));
+    cub::DeviceRadixSort::SortKeysDescending(t, tb, cnt, tmp, (int)n);
+    CK(cudaMemcpy(cnt, tmp, n * 4, cudaMemcpyDeviceToDevice));
+    cudaFree(t);
+    cudaFree(tmp);
+  }
+  int64_t* cst;
+  CK(cudaMalloc(&cst, (n + 1) * 8));
+  CK(cudaMemset(cst, 0, 8));
+  {
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, cnt, cst + 1, (int)n);
+    void* t;
+    CK(cudaMalloc(&t, tb));
+    cub::DeviceScan::InclusiveSum(t, tb, cnt, cst + 1, (int)n);
+    CK(cudaDeviceSynchronize());
+    cudaFree(t);
+  }
+  int64_t nnz = 0;
+  CK(cudaMemcpy(&nnz, cst + n, 8, cudaMemcpyDeviceToHost));
+  std::printf("m=%lld n=%lld nnz=%lld sorted=%d\n", (long long)m, (long long)n, (long long)nnz, sorted);
+  uint64_t *kr, *kc, *k2;
+  CK(cudaMalloc(&kr, nnz * 8));
+  CK(cudaMalloc(&kc, nnz * 8));
+  CK(cudaMalloc(&k2, nnz * 8));
+  entries_kernel<<<4096, 256>>>(cst, n, m, 777, kr, kc);
+  Csr K, KT;
+  K.dim = m; K.nnz = nnz; K.other = n;
+  KT.dim = n; KT.nnz = nnz; KT.other = m;
+  CK(cudaMalloc(&K.idx, nnz * 4));
+  CK(cudaMalloc(&K.val, nnz * 8));
+  CK(cudaMalloc(&KT.idx, nnz * 4));
+  CK(cudaMalloc(&KT.val, nnz * 8));
+  {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, kr, k2, nnz, 0, 47);
+    void* t;
+    CK(cudaMalloc(&t, tb));
+    cub::DeviceRadixSort::SortKeys(t, tb, kr, k2, nnz, 0, 47);
+    int32_t* rc;
+    CK(cudaMalloc(&rc, m * 4));
+    CK(cudaMemset(rc, 0, m * 4));
+    split_row<<<4096, 256>>>(k2, nnz, K.idx, K.val, rc);
+    int64_t* rs64;
+    CK(cudaMalloc(&rs64, (m + 1) * 8));
+    CK(cudaMemset(rs64, 0, 8));
+    size_t tb2 = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb2, rc, rs64 + 1, (int)m);
+    void* t2;
+    CK(cudaMalloc(&t2, tb2));
+    cub::DeviceScan::InclusiveSum(t2, tb2, rc, rs64 + 1, (int)m);
+    CK(cudaMalloc(&K.start, (m + 1) * 4));
+    i64_to_i32<<<1024, 256>>>(rs64, K.start, m + 1);
+    cub::DeviceRadixSort::SortKeys(t, tb, kc, k2, nnz, 0, 47);
+    split_col<<<4096, 256>>>(k2, nnz, KT.idx, KT.val);
+    CK(cudaMalloc(&KT.start, (n + 1) * 4));
+    i64_to_i32<<<1024, 256>>>(cst, KT.start, n + 1);
+    CK(cudaDeviceSynchronize());
+    cudaFree(t); cudaFree(t2); cudaFree(rc); cudaFree(rs64);
+  }
+  cudaFree(kr); cudaFree(kc); cudaFree(k2); cudaFree(cnt); cudaFree(cst);
+  K.hstart.resize(m + 1);
+  KT.hstart.resize(n + 1);
+  CK(cudaMemcpy(K.hstart.data(), K.start, (m + 1) * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(KT.hstart.data(), KT.start, (n + 1) * 4, cudaMemcpyDeviceToHost));
+
+  Vecs V;
+  auto vec = [&](int64_t len, double lo, double hi, uint64_t seed) {
+    double* p;
+    CK(cudaMalloc(&p, len * 8 + 16));
+    fill_kernel<<<2048, 256>>>(p, len, seed, lo, hi);
+    return p;
+  };
+  V.xb = vec(n, -1, 1, 1); V.y = vec(m, -1, 1, 2); V.lc = vec(m, -2, -1, 3); V.uc = vec(m, 1, 2, 4);
+  V.yn = vec(m, 0, 0, 5); V.dy = vec(m, 0, 0, 6);
+  V.aty = vec(n, -1, 1, 7); V.x = vec(n, 0, 1, 8); V.xn = vec(n, 0, 1, 9); V.atyn = vec(n, 0, 0, 10);
+  V.dyg = vec(m, -1, 1, 11);
+  double* outp;
+  CK(cudaMalloc(&outp, 148 * 64 * 8 * 8));
+  CK(cudaDeviceSynchronize());
+
+  const double row_bytes = 12.0 * nnz + 4.0 * (m + 1) + 8.0 * n + 8.0 * RowEpi::kRW * m;
+  const double col_bytes = 12.0 * nnz + 4.0 * (n + 1) + 8.0 * m + 8.0 * ColEpi::kRW * n;
+  RowEpi re{V.y, V.lc, V.uc, V.yn, V.dy, 0.37};
+  ColEpi ce{V.aty, V.x, V.xn, V.atyn};
+  auto want = [&](const char* label) { return only == nullptr || std::strstr(label, only) != nullptr; };
+  auto report = [&](const char* name, float us, double bytes) {
+    std::printf("%-44s %9.1f us  %7.0f GB/s  %.3f of peak\n", name, us, bytes / us / 1e3, bytes / us / 1e3 / peak);
+  };
+  const int reps = 10;
+
+  auto run_wb = [&](auto tag_item, auto tag_minb, const Csr& A, int seqmax, auto epi, const double* v,
+                    double bytes, const char* nm, bool long_only = false) {
+    constexpr int ITEM = decltype(tag_item)::value;
+    constexpr int MINB = decltype(tag_minb)::value;
+    {
+      char lb[160];
+      std::snprintf(lb, sizeof lb, "%s item=%d seq=%d minb=%d", nm, ITEM, seqmax, MINB);
+      if (!want(lb)) return;
+    }
+    int64_t slots = 0;
+    std::vector<int4> items = build_items(A.hstart, ITEM, seqmax, slots, long_only);
+    int4* d_items;
+    CK(cudaMalloc(&d_items, items.size() * sizeof(int4) + 16));
+    CK(cudaMemcpy(d_items, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    double* part;
+    unsigned* cntp;
+    CK(cudaMalloc(&part, (slots + 1) * 8));
+    CK(cudaMalloc(&cntp, (slots + 1) * 4));
+    CK(cudaMemset(cntp, 0, (slots + 1) * 4));
+    auto k = wb_kernel<ITEM, decltype(epi), MINB>;
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 256, 0));
+    const int grid = sms * per;
+    float us = time_it([&] { k<<<grid, 256>>>(d_items, (int64_t)items.size(), A.start, A.idx, A.val, v, epi, part, cntp, outp); }, reps);
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "%s item=%d seq=%d minb=%d (%d/SM, %zu items)", nm, ITEM, seqmax, MINB, per, items.size());
+    report(buf, us, bytes);
+    cudaFree(d_items); cudaFree(part); cudaFree(cntp);
+  };
+  auto run_vec = [&](auto tag_g, const Csr& A, auto epi, const double* v, double bytes, const char* nm) {
+    constexpr int G = decltype(tag_g)::value;
+    {
+      char lb[160];
+      std::snprintf(lb, sizeof lb, "%s vec G=%d", nm, G);
+      if (!want(lb)) return;
+    }
+    auto k = vec_kernel<G, decltype(epi), 4>;
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 256, 0));
+    const int grid = sms * per;
+    float us = time_it([&] { k<<<grid, 256>>>(A.dim, A.start, A.idx, A.val, v, epi, outp); }, reps);
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "%s vec G=%d (%d/SM)", nm, G, per);
+    report(buf, us, bytes);
+  };
+  using I128 = std::integral_constant<int, 128>;
+  using I256 = std::integral_constant<int, 256>;
+  using I512 = std::integral_constant<int, 512>;
+  using B1 = std::integral_constant<int, 1>;
+  using B2 = std::integral_constant<int, 2>;
+  using B3 = std::integral_constant<int, 3>;
+  using B4 = std::integral_constant<int, 4>;
+  using G4 = std::integral_constant<int, 4>;
+  using G8 = std::integral_constant<int, 8>;
+  using G16 = std::integral_constant<int, 16>;
+  using G32 = std::integral_constant<int, 32>;
+  // row pass (K x-bar + dual epilogue)
+  run_vec(G8{}, K, re, V.xb, row_bytes, "row");
+  run_vec(G16{}, K, re, V.xb, row_bytes, "row");
+  run_vec(G32{}, K, re, V.xb, row_bytes, "row");
+  run_wb(I256{}, B2{}, K, 64, re, V.xb, row_bytes, "row");
+  run_wb(I256{}, B3{}, K, 64, re, V.xb, row_bytes, "row");
+  run_wb(I256{}, B4{}, K, 64, re, V.xb, row_bytes, "row");
+  run_wb(I128{}, B4{}, K, 64, re, V.xb, row_bytes, "row");
+  run_wb(I512{}, B2{}, K, 64, re, V.xb, row_bytes, "row");
+  // column pass (K^T dy + aty epilogue)
+  run_vec(G4{}, KT, ce, V.dyg, col_bytes, "col");
+  run_vec(G32{}, KT, ce, V.dyg, col_bytes, "col");
+  run_wb(I256{}, B2{}, KT, 64, ce, V.dyg, col_bytes, "col");
+  run_wb(I256{}, B3{}, KT, 64, ce, V.dyg, col_bytes, "col");
+  run_wb(I256{}, B4{}, KT, 64, ce, V.dyg, col_bytes, "col");
+  run_wb(I256{}, B4{}, KT, 32, ce, V.dyg, col_bytes, "col");
+  run_wb(I256{}, B4{}, KT, 128, ce, V.dyg, col_bytes, "col");
+  run_wb(I128{}, B4{}, KT, 64, ce, V.dyg, col_bytes, "col");
+  run_wb(I512{}, B2{}, KT, 64, ce, V.dyg, col_bytes, "col");
+  if (want("gather")) {
+    double* big;
+    const int64_t maxlen = 20000000;
+    CK(cudaMalloc(&big, maxlen * 8));
+    fill_kernel<<<2048, 256>>>(big, maxlen, 99, -1, 1);
+    for (int64_t len : {(int64_t)500000, (int64_t)2500000, (int64_t)5000000, (int64_t)10000000, (int64_t)20000000}) {
+      for (int per : {4, 8}) {
+        const int grid = sms * per;
+        float us = time_it([&] { gather_probe<8><<<grid, 256>>>(big, len, nnz, outp); }, reps);
+        std::printf("  (unroll 8) ");
+        std::printf("gather probe len=%lld (%.0f MB) grid=%d/SM: %.1f us = %.1f Ggather/s\n", (long long)len,
+                    len * 8 / 1e6, per, us, nnz / us / 1e3);
+      }
+    }
+    cudaFree(big);
+  }
+  // warp-private rings
+  auto run_wr = [&](auto tag_cw, auto tag_s, auto tag_g, const Csr& A, int E, int L, int seqmax, auto epi,
+                    const double* v, const double* a0, const double* a1, const double* a2, double bytes,
+                    const char* nm) {
+    constexpr int CW = decltype(tag_cw)::value, S = decltype(tag_s)::value, G = decltype(tag_g)::value;
+    char lb[160];
+    std::snprintf(lb, sizeof lb, "%s ring cw=%d s=%d g=%d E=%d L=%d", nm, CW, S, G, E, L);
+    if (!want(lb)) return;
+    std::vector<int4> tiles = build_tiles(A.hstart, E, L, seqmax);
+    int4* d_t;
+    CK(cudaMalloc(&d_t, tiles.size() * sizeof(int4) + 16));
+    CK(cudaMemcpy(d_t, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    const size_t stage = ((4 * E + 32 + 15) & ~15) + ((8 * E + 32 + 15) & ~15) + ((4 * (L + 1) + 32 + 15) & ~15) +
+                         3 * ((8 * L + 32 + 15) & ~15);
+    const size_t smem = ((16 * CW * S + sizeof(RingHdr) * CW * S + 127) & ~127) + (size_t)CW * S * stage;
+    auto k = wr_kernel<CW, S, G, decltype(epi)>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 32 * (CW + 1), smem));
+    if (per < 1) { std::printf("%s: does not fit (%zu B)\n", lb, smem); cudaFree(d_t); return; }
+    const int grid = sms * per;
+    float us = time_it([&] { k<<<grid, 32 * (CW + 1), smem>>>(d_t, (int64_t)tiles.size(), A.start, A.idx, A.val, v, epi, a0, a1, a2, E, L, outp); }, reps);
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "%s (%d/SM, %zu KB, %zu tiles)", lb, per, smem / 1024, tiles.size());
+    report(buf, us, bytes);
+    cudaFree(d_t);
+  };
+  using C3 = std::integral_constant<int, 3>;
+  using C7 = std::integral_constant<int, 7>;
+  using C15 = std::integral_constant<int, 15>;
+  using S2 = std::integral_constant<int, 2>;
+  using S3 = std::integral_constant<int, 3>;
+  using Q4 = std::integral_constant<int, 4>;
+  using Q8 = std::integral_constant<int, 8>;
+  using Q16 = std::integral_constant<int, 16>;
+  run_wr(C7{}, S2{}, Q8{}, K, 1024, 64, 64, re, V.xb, V.y, V.lc, V.uc, row_bytes, "row");
+  run_wr(C7{}, S2{}, Q16{}, K, 1024, 64, 64, re, V.xb, V.y, V.lc, V.uc, row_bytes, "row");
+  run_wr(C7{}, S2{}, Q8{}, K, 2048, 96, 64, re, V.xb, V.y, V.lc, V.uc, row_bytes, "row");
+  run_wr(C15{}, S2{}, Q8{}, K, 512, 32, 64, re, V.xb, V.y, V.lc, V.uc, row_bytes, "row");
+  run_wr(C15{}, S2{}, Q8{}, K, 768, 32, 64, re, V.xb, V.y, V.lc, V.uc, row_bytes, "row");
+  run_wr(C15{}, S3{}, Q8{}, K, 512, 32, 64, re, V.xb, V.y, V.lc, V.uc, row_bytes, "row");
+  run_wr(C3{}, S2{}, Q8{}, K, 1024, 64, 64, re, V.xb, V.y, V.lc, V.uc, row_bytes, "row");
+  run_wr(C7{}, S3{}, Q4{}, K, 1024, 64, 64, re, V.xb, V.y, V.lc, V.uc, row_bytes, "row");
+  // column pass, short lines only (long lines: chunk items, reported separately)
+  run_wr(C7{}, S2{}, Q8{}, KT, 1024, 256, 64, ce, V.dyg, V.aty, V.x, V.xn, col_bytes, "colshort");
+  run_wr(C15{}, S2{}, Q8{}, KT, 512, 128, 64, ce, V.dyg, V.aty, V.x, V.xn, col_bytes, "colshort");
+  run_wb(I256{}, B4{}, KT, 64, ce, V.dyg, col_bytes, "collong", true);
+  run_wb(I256{}, B3{}, KT, 64, ce, V.dyg, col_bytes, "collong", true);
+  run_wb(I512{}, B2{}, KT, 64, ce, V.dyg, col_bytes, "collong", true);
+  // row pass over P column panels
+  for (int P : {2, 3, 4, 6}) {
+    {
+      char lb[64];
+      std::snprintf(lb, sizeof lb, "row panels P=%d", P);
+      if (!want(lb)) continue;
+    }
+    const int64_t W = (n + P - 1) / P;
+    int32_t* pc;
+    int64_t* pst;
+    CK(cudaMalloc(&pc, (int64_t)P * m * 4));
+    CK(cudaMalloc(&pst, ((int64_t)P * m + 1) * 8));
+    CK(cudaMemset(pc, 0, (int64_t)P * m * 4));
+    panel_count<<<2048, 256>>>(K.start, K.idx, m, P, W, pc);
+    CK(cudaMemset(pst, 0, 8));
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, pc, pst + 1, (int)(P * m));
+    void* t;
+    CK(cudaMalloc(&t, tb));
+    cub::DeviceScan::InclusiveSum(t, tb, pc, pst + 1, (int)(P * m));
+    int32_t* nidx;
+    double* nval;
+    CK(cudaMalloc(&nidx, nnz * 4 + 16));
+    CK(cudaMalloc(&nval, nnz * 8 + 16));
+    panel_scatter<<<2048, 256>>>(K.start, K.idx, K.val, m, P, W, pst, nidx, nval);
+    int32_t* pst32;
+    CK(cudaMalloc(&pst32, ((int64_t)P * m + 1) * 4));
+    i64_to_i32<<<1024, 256>>>(pst, pst32, (int64_t)P * m + 1);
+    double* carry;
+    CK(cudaMalloc(&carry, m * 8));
+    CK(cudaDeviceSynchronize());
+    auto run_panels = [&](auto tag_g) {
+      constexpr int G = decltype(tag_g)::value;
+      int per = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, panel_kernel<G, RowEpi, 1, 4>, 256, 0));
+      const int grid = sms * per;
+      float us = time_it([&] {
+        for (int p = 0; p < P; ++p) {
+          // panel p's row pointers are pst32[p*m .. p*m+m] (global positions)
+          const int32_t* st = pst32 + (int64_t)p * m;
+          if (p == 0) panel_kernel<G, RowEpi, 0, 4><<<grid, 256>>>(m, st, nidx, nval, V.xb, re, carry, outp);
+          else if (p == P - 1) panel_kernel<G, RowEpi, 2, 4><<<grid, 256>>>(m, st, nidx, nval, V.xb, re, carry, outp);
+          else panel_kernel<G, RowEpi, 1, 4><<<grid, 256>>>(m, st, nidx, nval, V.xb, re, carry, outp);
+        }
+      }, reps);
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "row panels P=%d G=%d (%d/SM)", P, G, per);
+      report(buf, us, row_bytes);
+    };
+    run_panels(G4{});
+    run_panels(G8{});
+    cudaFree(t); cudaFree(pc); cudaFree(pst); cudaFree(nidx); cudaFree(nval); cudaFree(pst32); cudaFree(carry);
+  }
+  // a copy of the same bytes, for calibration
+  {
+    double *a, *b;
+    const int64_t words = (int64_t)(row_bytes / 16);
+    CK(cudaMalloc(&a, words * 8));
+    CK(cudaMalloc(&b, words * 8));
+    float us = time_it([&] { cudaMemcpyAsync(b, a, words * 8, cudaMemcpyDeviceToDevice); }, reps);
+    report("memcpy (same bytes as row pass)", us, 16.0 * words);
+    cudaFree(a); cudaFree(b);
+  }
+  return 0;
+}
