@@ -211,5 +211,11 @@ inline void launch_pdl(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
 __device__ __forceinline__ int64_t ld_stream(const int64_t* p) { return __ldcs(p); }
+__device__ __forceinline__ int4 ld_stream(const int4* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+// Warm a line of global memory in L2 (the segmented spans' epilogue operands).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 }  // namespace pdlp

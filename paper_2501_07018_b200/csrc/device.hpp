@@ -93,14 +93,15 @@ class DevBuf {
     n_ = n;
     if (n == 0) return;
     void* p = nullptr;
-    // +16 bytes: the SpMV tile path bulk-copies 16-byte-aligned windows that
-    // may extend up to 15 bytes past the last element.
+    // +64 bytes: the SpMV tile path bulk-copies 16-byte-aligned windows that
+    // may extend up to 15 bytes past the last element, and the segmented
+    // spans load 8-entry blocks that may extend 7 entries past it.
     s_ = g_alloc_stream;
     const auto t0 = std::chrono::steady_clock::now();
     if (s_ != nullptr) {
-      PDLP_CK(cudaMallocAsync(&p, n * sizeof(T) + 16, s_));
+      PDLP_CK(cudaMallocAsync(&p, n * sizeof(T) + 64, s_));
     } else {
-      PDLP_CK(cudaMalloc(&p, n * sizeof(T) + 16));
+      PDLP_CK(cudaMalloc(&p, n * sizeof(T) + 64));
     }
     const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     g_alloc_seconds += dt;

@@ -218,7 +218,11 @@ __device__ void decide(pdlpk_step_state* s, double dx2, double dy2, double curv,
 }
 
 // --------------------------------------------------------- perf row pass ---
-struct RowEpi {
+// Carry = true: the last launch of a column-panel row pass -- the line sum
+// starts from the partial sum the earlier panels carried (staged as a 4th
+// operand).
+template <bool Carry>
+struct RowEpiT {
   const double* __restrict__ y;
   double* __restrict__ yn;
   double* __restrict__ dy;
@@ -231,16 +235,26 @@ struct RowEpi {
   double* lp = nullptr;  // line_partials: per-line terms (part2[r], part2[m + r])
   int64_t lm = 0;
   double dy2 = 0.0, infy = 0.0;
+  const double* __restrict__ carry = nullptr;
   struct Pre {
-    double y, lc, uc;
+    double y, lc, uc, c;
   };
-  __device__ __forceinline__ Pre load(int64_t r) const { return {y[r], lc[r], uc[r]}; }
+  __device__ __forceinline__ Pre load(int64_t r) const {
+    return {y[r], lc[r], uc[r], Carry ? carry[r] : 0.0};
+  }
+  __device__ __forceinline__ double init(const Pre& p) const { return Carry ? p.c : 0.0; }
+  __device__ __forceinline__ void prefetch(int64_t r) const {
+    prefetch_l2(y + r);
+    prefetch_l2(lc + r);
+    prefetch_l2(uc + r);
+  }
   // per-line operands the tile path stages with bulk copies
-  static constexpr int kStaged = 3;
-  // y, l_c, u_c: not read again before they would leave L2 anyway
+  static constexpr int kStaged = Carry ? 4 : 3;
+  // y, l_c, u_c (and the carried sums): not read again before they would
+  // leave L2 anyway
   __device__ __forceinline__ bool staged_reused(int) const { return false; }
   __device__ __forceinline__ const double* staged_src(int q) const {
-    return q == 0 ? y : (q == 1 ? lc : uc);
+    return q == 0 ? y : (q == 1 ? lc : (q == 2 ? uc : carry));
   }
   // accumulators of a multi-chunk line go to its fixed slot: [dy2, infy]
   __device__ __forceinline__ void reset_acc() { dy2 = 0.0; infy = 0.0; }
@@ -249,7 +263,7 @@ struct RowEpi {
     dst[1] = infy;
   }
   __device__ __forceinline__ Pre from_stage(const double* const* s, int li) const {
-    return {s[0][li], s[1][li], s[2][li]};
+    return {s[0][li], s[1][li], s[2][li], Carry ? s[3][li] : 0.0};
   }
   __device__ __forceinline__ void line(int64_t r, double acc, const Pre& p) {
     const double yr = p.y;
@@ -273,14 +287,48 @@ struct RowEpi {
     infy = max_keep(infy, fabs(yp));
   }
 };
+using RowEpi = RowEpiT<false>;
 
-template <class P, int Seg>
+// Earlier launches of a column-panel row pass: the line's running sum goes
+// to carry[r] (In: it starts from the previous panels' sum, staged).
+template <bool In>
+struct CarryEpi {
+  double* __restrict__ carry;
+  struct Pre {
+    double c;
+  };
+  __device__ __forceinline__ Pre load(int64_t r) const { return {In ? carry[r] : 0.0}; }
+  __device__ __forceinline__ double init(const Pre& p) const { return In ? p.c : 0.0; }
+  __device__ __forceinline__ void prefetch(int64_t r) const {
+    if (In) prefetch_l2(carry + r);
+  }
+  static constexpr int kStaged = In ? 1 : 0;
+  __device__ __forceinline__ bool staged_reused(int) const { return false; }
+  __device__ __forceinline__ const double* staged_src(int) const { return carry; }
+  __device__ __forceinline__ void reset_acc() {}
+  __device__ __forceinline__ void export_acc(double*) const {}
+  __device__ __forceinline__ Pre from_stage(const double* const* s, int li) const {
+    return {In ? s[0][li] : 0.0};
+  }
+  __device__ __forceinline__ void line(int64_t r, double acc, const Pre&) { carry[r] = acc; }
+};
+
+// Ph: 0 whole row pass; 1 / 2 first / middle column panel (carry out);
+// 3 last column panel (carry in, dual update)
+template <class P, int Seg, int Ph>
 __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) row_pass(pdlpk_step_args a) {
   pdl_wait();
   pdlpk_step_state* st = a.state;
   if (st->halt) return;
+  if constexpr (Ph == 1 || Ph == 2) {
+    CarryEpi<Ph == 2> ce{a.carry};
+    sched_spmv<P, Seg>(a.P.K, a.P.K.value, a.xbar, ce);
+    pdl_trigger();
+    return;
+  }
   const int cur = st->cur;
-  RowEpi e;
+  RowEpiT<Ph == 3> e;
+  e.carry = a.carry;
   e.y = a.y[cur];
   e.yn = a.y[cur ^ 1];
   e.dy = a.dy;
@@ -322,6 +370,12 @@ struct ColEpi {
     double aty, x, xn;
   };
   __device__ __forceinline__ Pre load(int64_t i) const { return {aty[i], x[i], xn[i]}; }
+  __device__ __forceinline__ double init(const Pre&) const { return 0.0; }
+  __device__ __forceinline__ void prefetch(int64_t i) const {
+    prefetch_l2(aty + i);
+    prefetch_l2(x + i);
+    prefetch_l2(xn + i);
+  }
   static constexpr int kStaged = 3;
   // aty and x are dead after this pass; x' is the next primal pass's x
   __device__ __forceinline__ bool staged_reused(int q) const { return q == 2; }
@@ -598,8 +652,23 @@ struct LaunchRowCol {
     const size_t smem = spmv_smem(A, Seg);
     const unsigned gu = static_cast<unsigned>(g);
     if (row) {
-      allow_smem(row_pass<P, Seg>, smem);
-      launch_pdl(pdl, row_pass<P, Seg>, gu, kSpmvThreads, smem, s, *a);
+      switch (a->panel_phase) {
+        case 1:
+          allow_smem(row_pass<P, Seg, 1>, smem);
+          launch_pdl(pdl, row_pass<P, Seg, 1>, gu, kSpmvThreads, smem, s, *a);
+          break;
+        case 2:
+          allow_smem(row_pass<P, Seg, 2>, smem);
+          launch_pdl(pdl, row_pass<P, Seg, 2>, gu, kSpmvThreads, smem, s, *a);
+          break;
+        case 3:
+          allow_smem(row_pass<P, Seg, 3>, smem);
+          launch_pdl(pdl, row_pass<P, Seg, 3>, gu, kSpmvThreads, smem, s, *a);
+          break;
+        default:
+          allow_smem(row_pass<P, Seg, 0>, smem);
+          launch_pdl(pdl, row_pass<P, Seg, 0>, gu, kSpmvThreads, smem, s, *a);
+      }
     } else {
       if (decide_here) {
         allow_smem(col_pass<P, Seg, true>, smem);
@@ -781,6 +850,25 @@ extern "C" int pdlpk_arm(pdlpk_step_state* st, int64_t k_target, cudaStream_t s)
   return static_cast<int>(cudaGetLastError());
 }
 
+// The row pass: one launch, or one per column panel (carry chained).  The
+// returned args are the column pass's: with panels its decision reads the
+// last panel launch's partials, so P.K is that layout.
+static pdlpk_step_args launch_row(const pdlpk_step_args* a, cudaStream_t s, bool pdl) {
+  if (a->n_row_panels < 2 || a->row_panels == nullptr) {
+    dispatch_p(a->P.K, LaunchRowCol{a, s, true, true, pdl});
+    return *a;
+  }
+  pdlpk_step_args b = *a;
+  const int np = a->n_row_panels;
+  for (int q = 0; q < np; ++q) {
+    b.P.K = a->row_panels[q];
+    b.panel_phase = q == 0 ? 1 : (q == np - 1 ? 3 : 2);
+    dispatch_p(b.P.K, LaunchRowCol{&b, s, true, true, pdl});
+  }
+  b.panel_phase = 0;
+  return b;
+}
+
 extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
   const bool pdl = a->mode == 0;  // perf mode: the three kernels chain with PDL
   launch_pdl(pdl, primal_pass<false>, static_cast<unsigned>(ew_blocks(a->P.n)), kEwThreads, 0, s,
@@ -788,8 +876,8 @@ extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
   if (a->mode == 0) {
     // Degenerate shapes (an empty side) still need the decision, which the
     // column pass performs: it always has >= 1 CTA (short_blocks >= 1).
-    dispatch_p(a->P.K, LaunchRowCol{a, s, true, true, true});
-    dispatch_p(a->P.KT, LaunchRowCol{a, s, false, true, true});
+    const pdlpk_step_args c = launch_row(a, s, true);
+    dispatch_p(c.P.KT, LaunchRowCol{&c, s, false, true, true});
   } else {
     const int gm = ew_blocks(a->P.m), gn = ew_blocks(a->P.n);
     if (a->P.K.wide) {
@@ -811,9 +899,9 @@ extern "C" int pdlpk_attempt_timed(const pdlpk_step_args* a, cudaEvent_t* ev, cu
   primal_pass<false><<<ew_blocks(a->P.n), kEwThreads, 0, s>>>(*a, pdlpk_peer_sum{});
   cudaEventRecord(ev[1], s);
   if (a->mode == 0) {
-    dispatch_p(a->P.K, LaunchRowCol{a, s, true});
+    const pdlpk_step_args c = launch_row(a, s, false);
     cudaEventRecord(ev[2], s);
-    dispatch_p(a->P.KT, LaunchRowCol{a, s, false});
+    dispatch_p(c.P.KT, LaunchRowCol{&c, s, false});
   } else {
     const int gm = ew_blocks(a->P.m), gn = ew_blocks(a->P.n);
     if (a->P.K.wide) {
@@ -926,6 +1014,21 @@ extern "C" int64_t pdlpk_tile_resident_ctas(int32_t stage_bytes) {
   allow_smem(col_pass<int32_t, 4, true>, smem);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, col_pass<int32_t, 4, true>,
                                                     kSpmvThreads, smem) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return static_cast<int64_t>(sms) * per_sm;
+}
+
+// CTAs of the segmented-span kernels resident at once (their grid: each warp
+// walks spans grid-stride).
+extern "C" int64_t pdlpk_seg_resident_ctas(void) {
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, col_pass<int32_t, 16, true>,
+                                                    kSpmvThreads, 0) != cudaSuccess ||
       per_sm < 1) {
     cudaGetLastError();
     per_sm = 1;

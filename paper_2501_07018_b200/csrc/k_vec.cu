@@ -5,6 +5,7 @@
 //
 // Translation unit compiled with -fmad=false (see common.cuh).
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -80,6 +81,8 @@ struct StoreEpi {
   __device__ __forceinline__ Pre from_stage(const double* const*, int) const { return {}; }
   __device__ __forceinline__ void reset_acc() {}
   __device__ __forceinline__ void export_acc(double*) const {}
+  __device__ __forceinline__ double init(const Pre&) const { return 0.0; }
+  __device__ __forceinline__ void prefetch(int64_t) const {}
   __device__ __forceinline__ void line(int64_t r, double acc, const Pre&) { out[r] = acc; }
 };
 
@@ -266,6 +269,38 @@ __device__ __forceinline__ bool penalty_term(double w, double lo, double hi, dou
 
 using namespace pdlp;
 
+// Column panels of the row layout (kernels.h pdlpk_step_args::n_row_panels):
+// entry k of row r (rows sorted by column) goes to panel q = its column's
+// range, at pp.start[q][r] + its rank among row r's panel-q entries.  Warp per
+// row, lanes over the row's entries.
+template <class P>
+__global__ void __launch_bounds__(kT) panel_scatter_kernel(const P* __restrict__ start,
+                                                          const int32_t* __restrict__ idx,
+                                                          const double* __restrict__ val, int64_t m,
+                                                          pdlpk_panel_ptrs pp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = w0; r < m; r += nw) {
+    const int64_t s = start[r], e = start[r + 1];
+    int64_t cum[PDLPK_MAX_ROW_PANELS + 1];
+    int64_t pos[PDLPK_MAX_ROW_PANELS];
+    cum[0] = 0;
+    for (int q = 0; q < pp.np; ++q) {
+      pos[q] = pp.start[q][r];
+      cum[q + 1] = cum[q] + (pp.start[q][r + 1] - pos[q]);
+    }
+    for (int64_t k = s + lane; k < e; k += 32) {
+      const int64_t o = k - s;
+      int q = 0;
+      while (q + 1 < pp.np && o >= cum[q + 1]) ++q;
+      const int64_t d = pos[q] + (o - cum[q]);
+      pp.idx[q][d] = idx[k];
+      pp.val[q][d] = val[k];
+    }
+  }
+}
+
 extern "C" {
 
 int64_t pdlpk_red_scratch_doubles(void) { return 8 * kRedMaxBlocks; }
@@ -322,15 +357,29 @@ int pdlpk_diff_norm_sq(const double* a, const double* b, int64_t n, const pdlpk_
 
 void pdlpk_set_red_log(pdlpk_red_log* log) { g_red_log = log; }
 
+int pdlpk_panel_scatter(const pdlpk_csr* K, const pdlpk_panel_ptrs* pp, cudaStream_t s) {
+  if (K->dim <= 0) return 0;
+  const unsigned g = static_cast<unsigned>(std::min<int64_t>((K->dim + 7) / 8, 148 * 16));
+  if (K->wide) {
+    panel_scatter_kernel<<<g, kT, 0, s>>>(static_cast<const int64_t*>(K->start), K->index, K->value,
+                                          K->dim, *pp);
+  } else {
+    panel_scatter_kernel<<<g, kT, 0, s>>>(static_cast<const int32_t*>(K->start), K->index, K->value,
+                                          K->dim, *pp);
+  }
+  return ok();
+}
+
 void pdlpk_tile_shape(double avg_len, int32_t budget, int32_t* lines, int32_t* nnz,
-                      int32_t* stage_bytes) {
+                      int32_t* stage_bytes, int32_t staged) {
+  const int ns = staged < 0 ? kDefaultStaged : staged;
   const double a = avg_len < 1.0 ? 1.0 : avg_len;
   int L = kTileRows;
-  while (L > 32 && static_cast<double>(stage_nnz_for(L, budget)) < a * L) L -= 8;
-  const int E = stage_nnz_for(L, budget);
+  while (L > 32 && static_cast<double>(stage_nnz_for(L, budget, ns)) < a * L) L -= 8;
+  const int E = stage_nnz_for(L, budget, ns);
   *lines = L;
   *nnz = E;
-  *stage_bytes = static_cast<int32_t>(stage_layout(L, E).bytes);
+  *stage_bytes = static_cast<int32_t>(stage_layout(L, E, ns).bytes);
 }
 
 int32_t pdlpk_stage_budget(int32_t nnz) {

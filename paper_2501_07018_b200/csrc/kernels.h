@@ -66,7 +66,19 @@ typedef struct pdlpk_csr {
   int32_t tile_lines_cap;   /* staged tile shape of this layout: lines and */
   int32_t tile_nnz_cap;     /* entries per tile ... */
   int32_t tile_stage_bytes; /* ... and the bytes of one ring stage */
-  int32_t _pad_tile;
+  /* Segmented spans (spmv.cuh seg_spans), an alternative schedule for
+   * skewed layouts: seg_mode = 1 replaces every other segment.  Span
+   * {r0, nl > 0, e0, len}: whole non-empty lines r0 .. r0+nl-1; span
+   * {r, -1-c, e0, len}: chunk c of a line longer than a span (or an empty
+   * line), seg_aux = {first partial slot, chunks, line_acc slot or -1, 0}.
+   * Per 256-entry step of a line run, 8 words of line-start bits and 8 of
+   * line-end bits (seg_masks, from seg_step0[span]). */
+  int32_t seg_mode;
+  const int4* seg_spans;
+  const int4* seg_aux;
+  const int32_t* seg_step0;
+  const uint32_t* seg_masks;
+  int64_t n_seg_spans;
 } pdlpk_csr;
 
 #define PDLPK_DIST_NONE 0
@@ -190,8 +202,32 @@ typedef struct pdlpk_step_args {
    * reductions do not depend on the SpMV schedule (perf mode, one GPU,
    * m <= PDLPK_LINE_PARTIALS_MAX). */
   int32_t line_partials;
-  int32_t _pad_lp;
+  /* Column panels of the row pass (perf mode, one GPU, large n): the row
+   * layout re-laid out as n_row_panels CSR matrices over consecutive column
+   * ranges (host array row_panels, each a full m-line layout).  The row pass
+   * then runs one launch per panel, carrying each line's running sum in
+   * carry[] from panel to panel (rows are sorted by column, so the chained
+   * sum adds the line's products in storage order); only the last launch
+   * runs the dual-update epilogue.  The x-bar range a launch gathers from
+   * then stays in L2.  panel_phase (set per launch): 0 no panels, 1 first,
+   * 2 middle, 3 last. */
+  int32_t n_row_panels;
+  int32_t panel_phase;
+  int32_t _pad_panel;
+  const pdlpk_csr* row_panels; /* host pointer: read by the launch code only */
+  double* carry;               /* m */
 } pdlpk_step_args;
+#define PDLPK_MAX_ROW_PANELS 8
+
+/* Device pointers of the column panels (k_vec.cu pdlpk_panel_scatter). */
+typedef struct pdlpk_panel_ptrs {
+  int32_t np;
+  int32_t _pad;
+  const int32_t* start[PDLPK_MAX_ROW_PANELS]; /* m+1 each, panel-local positions */
+  int32_t* idx[PDLPK_MAX_ROW_PANELS];
+  double* val[PDLPK_MAX_ROW_PANELS];
+} pdlpk_panel_ptrs;
+int pdlpk_panel_scatter(const pdlpk_csr* K, const pdlpk_panel_ptrs* pp, cudaStream_t s);
 #define PDLPK_LINE_PARTIALS_MAX 262144
 
 /* Reduction context for cadence operations. */
@@ -209,11 +245,12 @@ int64_t pdlpk_step_partials(const pdlpk_problem* P);
  * entries: the most lines (<= PDLPK_TILE_ROWS) whose entries still fit one
  * ring stage, and the entry cap for that line count. */
 void pdlpk_tile_shape(double avg_len, int32_t budget, int32_t* lines, int32_t* nnz,
-                      int32_t* stage_bytes);
+                      int32_t* stage_bytes, int32_t staged);
 /* Ring-stage bytes of a PDLPK_TILE_ROWS x nnz tile (budgets for tile_shape). */
 int32_t pdlpk_stage_budget(int32_t nnz);
 /* SMs x resident CTAs of the staged-tile kernels with this ring. */
 int64_t pdlpk_tile_resident_ctas(int32_t stage_bytes);
+int64_t pdlpk_seg_resident_ctas(void);
 
 /* ---- row-sharded attempt pieces (the host interleaves the collectives) ----
  * primal:     primal_pass; xbar is written at a->xbar

@@ -129,6 +129,9 @@ struct DevLayout {
   DevBuf<int64_t> tile_nnz0, chunk_beg;
   DevBuf<double> chunk_part, line_acc;
   DevBuf<unsigned> chunk_cnt;
+  DevBuf<int4> seg_spans, seg_aux;
+  DevBuf<int32_t> seg_step0;
+  DevBuf<uint32_t> seg_masks;
   pdlpk_csr view{};
 };
 
@@ -198,7 +201,7 @@ void for_segments(int64_t dim, int parts, F&& f) {
 }
 
 void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
-                    int64_t short_max = PDLPK_SHORT_MAX, int32_t budget = 0) {
+                    int64_t short_max = PDLPK_SHORT_MAX, int32_t budget = 0, int32_t staged = -1) {
   if (budget <= 0) budget = pdlpk_stage_budget(PDLPK_TILE_NNZ);
   int parts = static_cast<int>(std::clamp<int64_t>(
       dim / (int64_t(1) << 18), 1, std::max(1u, std::min(16u, std::thread::hardware_concurrency()))));
@@ -225,11 +228,13 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
       short_nnz += g.short_nnz;
     }
     const double avg = short_lines > 0 ? static_cast<double>(short_nnz) / short_lines : 1.0;
-    pdlpk_tile_shape(avg, budget, &shape_lines, &shape_nnz, &stage_bytes);
+    pdlpk_tile_shape(avg, budget, &shape_lines, &shape_nnz, &stage_bytes, staged);
   }
   const int64_t tile_rows = direct ? 256 : shape_lines;
   const int64_t tile_nnz = direct ? 256 * PDLPK_SHORT_MAX : shape_nnz;
   if (direct) short_max = PDLPK_SHORT_MAX;
+  // a tiled line must fit one stage on its own (longer ones go to warp lines)
+  short_max = std::min<int64_t>(short_max, tile_nnz);
   // Segment boundaries on multiples of the tile's line count (uniform
   // layouts then re-synchronize at once, see the splice below).
   std::vector<int64_t> bnd(static_cast<size_t>(parts) + 1);
@@ -428,6 +433,7 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
   L.view.tile_nnz0 = L.tile_nnz0.get();
   L.view.n_tiles = n_tiles;
   L.view.tile_direct = direct ? 1 : 0;
+  L.view.seg_mode = 0;
   L.view.tile_lines_cap = static_cast<int32_t>(tile_rows);
   L.view.tile_nnz_cap = static_cast<int32_t>(tile_nnz);
   L.view.tile_stage_bytes = stage_bytes;
@@ -457,13 +463,125 @@ bool starts_valid(const int64_t* start, int64_t dim, int64_t nnz) {
   return std::all_of(ok.begin(), ok.end(), [](uint8_t v) { return v != 0; });
 }
 
-// bad: the device validation flags of this upload; autotuning runs products
-// on the layout, so only after they are known clean.
-int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t operand_len, DevLayout& L,
-                          cudaStream_t s, const unsigned* bad) {
+// Segmented-span schedule (spmv.cuh seg_spans): runs of whole lines of at
+// most `span` entries, longer lines cut into chunks, empty lines as empty
+// chunks; per 256-entry step of a run, 8 line-start and 8 line-end words.
+void build_seg_schedule(const int64_t* start, int64_t dim, DevLayout& L, int64_t span) {
+  std::vector<int4> spans, aux;
+  std::vector<int32_t> step0;
+  int64_t parts = 0, n_multi = 0, steps = 0;
+  int64_t r0 = -1, nl = 0, nz = 0;
+  auto push = [&](int64_t r, int64_t y, int64_t e0, int64_t len, int32_t ax, int32_t ay, int32_t az) {
+    spans.push_back(make_int4(static_cast<int32_t>(r), static_cast<int32_t>(y),
+                              static_cast<int32_t>(static_cast<uint32_t>(e0 & 0xffffffff)),
+                              static_cast<int32_t>(len)));
+    aux.push_back(make_int4(ax, ay, az, static_cast<int32_t>(e0 >> 32)));
+    if (y > 0) {
+      step0.push_back(static_cast<int32_t>(steps));
+      steps += (e0 + len - (e0 & ~int64_t(7)) + 255) / 256;
+    } else {
+      step0.push_back(0);
+    }
+  };
+  auto close = [&] {
+    if (nl > 0) push(r0, nl, start[r0], nz, 0, 0, -1);
+    nl = 0;
+    nz = 0;
+  };
+  for (int64_t r = 0; r < dim; ++r) {
+    const int64_t len = start[r + 1] - start[r];
+    if (len == 0) {  // the epilogue still runs (sum 0)
+      close();
+      push(r, -1, start[r], 0, 0, 1, -1);
+      continue;
+    }
+    if (len > span) {
+      close();
+      const int64_t nch = (len + span - 1) / span;
+      const int32_t ms = static_cast<int32_t>(n_multi++);
+      for (int64_t c = 0; c < nch; ++c) {
+        const int64_t b = start[r] + c * span;
+        push(r, -1 - c, b, std::min(span, start[r + 1] - b), static_cast<int32_t>(parts),
+             static_cast<int32_t>(nch), ms);
+      }
+      parts += nch;
+      continue;
+    }
+    if (nz + len > span || nl >= (int64_t(1) << 30)) close();
+    if (nl == 0) r0 = r;
+    ++nl;
+    nz += len;
+  }
+  close();
+  std::vector<uint32_t> masks(static_cast<size_t>(steps) * 16 + 16, 0u);
+  for (size_t i = 0; i < spans.size(); ++i) {
+    const int4 d = spans[i];
+    if (d.y <= 0) continue;
+    const int64_t e0 = static_cast<int64_t>(static_cast<uint32_t>(d.z)) | (static_cast<int64_t>(aux[i].w) << 32);
+    const int64_t b0 = e0 & ~int64_t(7);
+    for (int64_t r = d.x; r < static_cast<int64_t>(d.x) + d.y; ++r) {
+      const int64_t oh = start[r] - b0, oe = start[r + 1] - 1 - b0;
+      masks[static_cast<size_t>((step0[i] + oh / 256) * 16 + (oh % 256) / 32)] |= 1u << (oh % 32);
+      masks[static_cast<size_t>((step0[i] + oe / 256) * 16 + 8 + (oe % 256) / 32)] |= 1u << (oe % 32);
+    }
+  }
+  upload_list(spans, L.seg_spans);
+  upload_list(aux, L.seg_aux);
+  upload_list(step0, L.seg_step0);
+  upload_list(masks, L.seg_masks);
+  L.chunk_part.alloc(parts);
+  L.chunk_cnt.alloc(parts);
+  if (parts > 0) {
+    PDLP_CK(cudaMemsetAsync(L.chunk_cnt.get(), 0, parts * sizeof(unsigned), g_alloc_stream));
+    PDLP_CK(cudaStreamSynchronize(g_alloc_stream));
+  }
+  L.line_acc.alloc(n_multi * PDLPK_LINE_ACC);
+  L.view.seg_mode = 1;
+  L.view.seg_spans = L.seg_spans.get();
+  L.view.seg_aux = L.seg_aux.get();
+  L.view.seg_step0 = L.seg_step0.get();
+  L.view.seg_masks = L.seg_masks.get();
+  L.view.n_seg_spans = static_cast<int64_t>(spans.size());
+  L.view.n_chunks = parts;  // partial slots (sizes the side stream's scratch)
+  L.view.n_cta_chunks = 0;
+  L.view.n_multi = n_multi;
+  L.view.chunk_part = L.chunk_part.get();
+  L.view.chunk_cnt = L.chunk_cnt.get();
+  L.view.line_acc = L.line_acc.get();
+  L.view.n_tiles = 0;
+  L.view.tile_direct = 0;
+  L.view.tile_blocks = static_cast<int32_t>(std::max<int64_t>(1, pdlpk_seg_resident_ctas()));
+}
+
+// Schedule choice per layout, a function of the line lengths only (so the
+// perf-mode iterates do not depend on timing noise):
+//  * skewed layouts of >= 16M entries (a tenth of the entries in lines over
+//    256, or a line 16x the mean): segmented spans of 2,048 entries;
+//  * otherwise staged tiles of lines <= 64 entries (<= 256 when a third of
+//    the entries sit in longer lines), a 2,016-entry stage budget for
+//    layouts of >= 16M entries.
+// PDLP_SEG=0/1 and PDLP_SHORT_MAX=<n> override (measurements).
+int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t /*operand_len*/, DevLayout& L,
+                          cudaStream_t /*s*/, const unsigned* /*bad*/) {
   if (!starts_valid(start, dim, L.view.nnz)) {
     build_schedule(start, 0, L, PDLPK_SHORT_MAX);  // empty: validation throws before use
     return PDLPK_SHORT_MAX;
+  }
+  const int64_t nnz = L.view.nnz;
+  int64_t over64 = 0, over256 = 0, maxlen = 0;
+  for (int64_t r = 0; r < dim; ++r) {
+    const int64_t len = start[r + 1] - start[r];
+    if (len > 64) over64 += len;
+    if (len > 256) over256 += len;
+    maxlen = std::max(maxlen, len);
+  }
+  const double mean = dim > 0 ? static_cast<double>(nnz) / static_cast<double>(dim) : 0.0;
+  bool seg = nnz >= (int64_t(16) << 20) && !L.view.tile_direct &&
+             (10 * over256 >= nnz || static_cast<double>(maxlen) > 16.0 * mean);
+  if (const char* e = std::getenv("PDLP_SEG")) seg = e[0] == '1';
+  if (seg) {
+    build_seg_schedule(start, dim, L, 2048);
+    return -1;
   }
   const char* env = std::getenv("PDLP_SHORT_MAX");
   if (env != nullptr && std::atoi(env) > 0) {
@@ -471,47 +589,10 @@ int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t operand_len
     build_schedule(start, dim, L, t);
     return t;
   }
-  const int64_t kDefault = 64;
-  if (L.view.nnz < (int64_t(16) << 20) || L.view.tile_direct) {
-    build_schedule(start, dim, L, kDefault);
-    return kDefault;
-  }
-  {
-    unsigned hb = 0;
-    PDLP_CK(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s));
-    PDLP_CK(cudaStreamSynchronize(s));
-    if (hb != 0) {  // an index out of range: no products on this layout
-      build_schedule(start, dim, L, kDefault);
-      return kDefault;
-    }
-  }
-  // candidates: tile line threshold x ring-stage budget (entries of a
-  // PDLPK_TILE_ROWS-line stage); the budget sets both the tile shape and how
-  // many CTAs are resident
-  DevBuf<double> x(std::max<int64_t>(operand_len, 1)), out(std::max<int64_t>(dim, 1));
-  PDLP_LAUNCH(pdlpk_fill(x.get(), 1.0, operand_len, s));
-  Event e0, e1;
-  int64_t best = kDefault;
-  int32_t best_budget = pdlpk_stage_budget(PDLPK_TILE_NNZ);
-  double best_t = kInf;
-  for (const int64_t t : {32, 64, 256}) {
-    for (const int32_t nnz : {896, 1344, 2016}) {
-      const int32_t budget = pdlpk_stage_budget(nnz);
-      build_schedule(start, dim, L, t, budget);
-      PDLP_LAUNCH(pdlpk_spmv(&L.view, 0, x.get(), out.get(), 0, s));  // warm
-      e0.record(s);
-      for (int rep = 0; rep < 2; ++rep) PDLP_LAUNCH(pdlpk_spmv(&L.view, 0, x.get(), out.get(), 0, s));
-      e1.record(s);
-      const double el = elapsed_seconds(e0, e1);
-      if (el < best_t) {
-        best_t = el;
-        best = t;
-        best_budget = budget;
-      }
-    }
-  }
-  build_schedule(start, dim, L, best, best_budget);
-  return best;
+  const int64_t t = 3 * over64 >= nnz ? 256 : 64;
+  const int32_t budget = nnz >= (int64_t(16) << 20) ? pdlpk_stage_budget(2016) : 0;
+  build_schedule(start, dim, L, t, budget);
+  return t;
 }
 
 // Uploads one orientation; the raw int64 row pointers and indices are checked
@@ -1365,6 +1446,11 @@ class Engine {
     a.shard_part = D.shard_part.get();
     a.line_partials = (!parity_ && !dist() && P.m <= PDLPK_LINE_PARTIALS_MAX && line_partials_on_)
                           ? 1 : 0;
+    if (!parity_ && uses_panels(P)) {
+      a.n_row_panels = panels_.np;
+      a.row_panels = panels_.views.data();
+      a.carry = panels_.carry.get();
+    }
     return a;
   }
 
@@ -1383,6 +1469,11 @@ class Engine {
   void prepare(Inner& D, const pdlpk_problem& P, const double* x0, double eta0, double omega0,
                bool fixed) {
     int64_t partials = pdlpk_step_partials(&P);
+    if (uses_panels(P)) {  // the decision reads the last panel launch's partials
+      pdlpk_problem Q = P;
+      Q.K = panels_.views.back();
+      partials = std::max(partials, pdlpk_step_partials(&Q));
+    }
     if (dist()) {
       partials = std::max<int64_t>(partials, 3 * pdlpk_dist_ew_grid(std::max(P.n, P.m)) + 64);
     }
@@ -1980,6 +2071,107 @@ class Engine {
     Q.KT = side_csr(P.KT);
     return Q;
   }
+  // ---- column panels of the row pass (kernels.h n_row_panels) ----------
+  // Perf mode on one GPU when the gathered x-bar is larger than L2 can keep
+  // next to the pass's streams: the row layout is re-laid out as np CSR
+  // matrices over consecutive column ranges of `width` columns, so each
+  // launch of the row pass gathers from an x-bar range that stays in L2.
+  struct Panels {
+    int np = 0;
+    int64_t width = 0;
+    std::vector<DevLayout> L;
+    std::vector<pdlpk_csr> views;
+    DevBuf<double> carry;
+  } panels_;
+
+  static int panel_count(int64_t n, int64_t nnz) {
+    if (const char* e = std::getenv("PDLP_ROW_PANELS")) {
+      const int v = std::atoi(e);
+      return v >= 2 ? std::min(v, PDLPK_MAX_ROW_PANELS) : 0;
+    }
+    // x-bar above 48 MB and a matrix large enough for the gathers to
+    // dominate; at most 4 panels (each launch re-reads the m-length row
+    // pointers and carries)
+    const double mb = 8.0 * static_cast<double>(n) / 1048576.0;
+    if (mb <= 48.0 || nnz < (int64_t(16) << 20)) return 0;
+    const int np = static_cast<int>(std::ceil(mb / 40.0));
+    return np <= 4 ? np : 0;
+  }
+
+  // Host part (structure and schedules) from the caller's row layout; the
+  // device arrays are filled from the scaled values by fill_panels().
+  void plan_panels(const pdlp_csr_view& v, int64_t n) {
+    panels_ = Panels{};
+    if (parity_ || comm_ != nullptr || v.primary_dim <= 0) return;
+    const int np = panel_count(n, v.nnz);
+    if (np < 2) return;
+    const int64_t m = v.primary_dim;
+    const int64_t width = (n + np - 1) / np;
+    std::vector<std::vector<int64_t>> st(static_cast<size_t>(np), std::vector<int64_t>(m + 1, 0));
+    for_segments(m, 16, [&](int, int64_t lo, int64_t hi) {
+      for (int64_t r = lo; r < hi; ++r) {
+        const int64_t* b = v.index + v.start[r];
+        const int64_t* e = v.index + v.start[r + 1];
+        const int64_t* prev = b;
+        for (int q = 0; q < np; ++q) {
+          const int64_t* cut = q + 1 < np ? std::lower_bound(prev, e, (q + 1) * width) : e;
+          st[q][r + 1] = cut - prev;  // count, prefix-summed below
+          prev = cut;
+        }
+      }
+    });
+    for (int q = 0; q < np; ++q) {
+      for (int64_t r = 0; r < m; ++r) st[q][r + 1] += st[q][r];
+      if (st[q][m] >= (int64_t(1) << 31) - 1) return;  // 32-bit panel starts only
+    }
+    panels_.np = np;
+    panels_.width = width;
+    panels_.L.resize(static_cast<size_t>(np));
+    panels_.views.resize(static_cast<size_t>(np));
+    for (int q = 0; q < np; ++q) {
+      DevLayout& L = panels_.L[static_cast<size_t>(q)];
+      const int64_t nz = st[q][m];
+      L.start32.alloc(m + 1);
+      std::vector<int32_t> s32(st[q].begin(), st[q].end());
+      PDLP_CK(cudaMemcpyAsync(L.start32.get(), s32.data(), (m + 1) * 4, cudaMemcpyHostToDevice, s()));
+      PDLP_CK(cudaStreamSynchronize(s()));
+      L.index.alloc(nz);
+      L.value.alloc(nz);
+      L.view.dim = m;
+      L.view.nnz = nz;
+      L.view.wide = 0;
+      L.view.start = L.start32.get();
+      L.view.index = L.index.get();
+      L.view.value = L.value.get();
+      L.view.value_orig = nullptr;
+      // staged operands: none (first), the carry (middle), y, l_c, u_c and
+      // the carry (last)
+      const int32_t staged = q == 0 ? 0 : (q == np - 1 ? 4 : 1);
+      const char* eb = std::getenv("PDLP_PANEL_BUDGET");
+      const int32_t budget = pdlpk_stage_budget(eb != nullptr ? std::atoi(eb) : 2016);
+      build_schedule(st[q].data(), m, L, 64, budget, staged);
+      panels_.views[static_cast<size_t>(q)] = L.view;
+    }
+    panels_.carry.alloc(m);
+  }
+
+  void fill_panels() {
+    if (panels_.np < 2) return;
+    pdlpk_panel_ptrs pp{};
+    pp.np = panels_.np;
+    for (int q = 0; q < panels_.np; ++q) {
+      DevLayout& L = panels_.L[static_cast<size_t>(q)];
+      pp.start[q] = L.start32.get();
+      pp.idx[q] = L.index.get();
+      pp.val[q] = L.value.get();
+    }
+    PDLP_LAUNCH(pdlpk_panel_scatter(&prob_.row.view, &pp, s()));
+  }
+
+  bool uses_panels(const pdlpk_problem& P) const {
+    return panels_.np >= 2 && P.K.index == prob_.row.view.index;
+  }
+
   DevBuf<double> side_prod_;  // the average ray's A^T product
   std::unique_ptr<Stream> gap_side_;  // second gap query's stream
   DevBuf<double> gap_scratch2_;
@@ -2369,6 +2561,10 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
   Engine E(problem, *o, comm);  // uploads and validates on device
   if (o->enable_scaling) E.precondition(o->ruiz_passes, o->pock_chambolle != 0);
   if (std::getenv("PDLP_NO_UNIFORM") == nullptr) E.detect_uniform();
+  if (!E.dist()) {
+    E.plan_panels(problem->by_row, problem->cols);
+    E.fill_panels();
+  }
   if (E.dist()) E.build_full_views();
   if (o->enable_polish) {
     // The polishing subproblems' states are allocated mid-loop, the first

@@ -54,7 +54,8 @@ constexpr int kShortMax = PDLPK_SHORT_MAX;  // longest tiled line
 constexpr int kChunk = PDLPK_CHUNK;         // entries per warp chunk of a long line
 constexpr int kTileNnz = PDLPK_TILE_NNZ;    // entries per CTA tile
 constexpr int kTileRows = PDLPK_TILE_ROWS;  // lines per CTA tile
-constexpr int kMaxStaged = 3;               // epilogue operand streams per line
+constexpr int kMaxStaged = 4;               // epilogue operand streams per line (at most)
+constexpr int kDefaultStaged = 3;           // what a layout's stage reserves unless told otherwise
 constexpr int kConsumerWarps = kSpmvWarps - 1;  // warp 0 produces
 // lines per consumer lane: a consumer warp owns 32 * kLinesPerLane lines of a
 // tile, lane l taking lines l, l + 32, ... (stores stay coalesced)
@@ -71,7 +72,7 @@ __host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~size
 struct StageLayout {
   uint32_t val, ptr, epi, epi_stride, bytes;
 };
-__host__ __device__ constexpr StageLayout stage_layout(int L, int E) {
+__host__ __device__ constexpr StageLayout stage_layout(int L, int E, int ns = kDefaultStaged) {
   return StageLayout{
       static_cast<uint32_t>(align16(sizeof(int32_t) * E + 32)),
       static_cast<uint32_t>(align16(sizeof(int32_t) * E + 32) + align16(sizeof(double) * E + 32)),
@@ -80,14 +81,14 @@ __host__ __device__ constexpr StageLayout stage_layout(int L, int E) {
       static_cast<uint32_t>(align16(sizeof(double) * L + 32)),
       static_cast<uint32_t>(align16(sizeof(int32_t) * E + 32) + align16(sizeof(double) * E + 32) +
                             align16(sizeof(int64_t) * (L + 1) + 32) +
-                            kMaxStaged * align16(sizeof(double) * L + 32))};
+                            ns * align16(sizeof(double) * L + 32))};
 }
 // Largest entry count that fits a stage of `budget` bytes next to L lines.
-__host__ __device__ inline int stage_nnz_for(int L, size_t budget) {
+__host__ __device__ inline int stage_nnz_for(int L, size_t budget, int ns = kDefaultStaged) {
   int lo = 32, hi = 1 << 18;
   while (lo < hi) {
     const int mid = (lo + hi + 1) / 2;
-    if (stage_layout(L, mid).bytes <= budget) lo = mid; else hi = mid - 1;
+    if (stage_layout(L, mid, ns).bytes <= budget) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
@@ -123,12 +124,164 @@ constexpr int kDirectRows = kSpmvThreads;  // lines per direct tile
 #endif
 constexpr int kTileGather = PDLPK_TILE_GATHER;
 
+// ------------------------------------------------------ segmented spans ---
+// A warp walks one span at a time (grid-stride over spans).  Line runs: steps
+// of 256 entries starting on 8-entry boundaries; lane l holds entries
+// [base + 8l, base + 8l + 8) (vector loads of indices and values, 8 gathers
+// in flight), sums the line segments inside its 8 entries in storage order,
+// and a segmented scan across the lanes joins segments that cross lanes; a
+// carry joins steps.  The lane holding a line's last entry runs the
+// epilogue (the operands of the step's lines are warmed in L2 first).  Lines
+// longer than a span are cut into chunks summed by lane chains + a warp tree
+// and combined in chunk order by the last-arriving chunk (deterministic).
+// Every line sum has one fixed association, so results are deterministic run
+// to run; only lines that cross lanes are not summed in storage order.
+__device__ __forceinline__ int warp_excl_scan_i(int v, int lane) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  return x - v;
+}
+
+template <class Epi>
+__device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __restrict__ vals,
+                                          const double* __restrict__ v, Epi& epi) {
+  const int32_t* __restrict__ idx = A.index;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t it = gw; it < A.n_seg_spans; it += nw) {
+    const int4 d = A.seg_spans[it];
+    const int64_t e0 = static_cast<int64_t>(static_cast<uint32_t>(d.z)) |
+                       (static_cast<int64_t>(A.seg_aux[it].w) << 32);
+    const int64_t e1 = e0 + d.w;
+    if (d.y < 0) {
+      // chunk c of a long line (or an empty line)
+      double acc = 0.0;
+      for (int64_t base = e0 & ~int64_t(7); base < e1; base += 256) {
+        const int64_t k0 = base + 8 * lane;
+        if (k0 + 8 > e0 && k0 < e1) {
+          const int4 i0 = ld_stream(reinterpret_cast<const int4*>(idx + k0));
+          const int4 i1 = ld_stream(reinterpret_cast<const int4*>(idx + k0 + 4));
+          const int ci[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+          double a[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double2 t = ld_stream(reinterpret_cast<const double2*>(vals + k0) + q);
+            a[2 * q] = t.x;
+            a[2 * q + 1] = t.y;
+          }
+          double g[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) g[u] = (k0 + u >= e0 && k0 + u < e1) ? __ldg(v + ci[u]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (k0 + u >= e0 && k0 + u < e1) acc = mac(acc, a[u], g[u]);
+          }
+        }
+      }
+      const double t = warp_sum(acc);
+      if (lane == 0) {
+        const int4 x = A.seg_aux[it];
+        const int c = -1 - d.y, nch = x.y;
+        if (nch == 1) {
+          const typename Epi::Pre pre = epi.load(d.x);
+          epi.line(d.x, epi.init(pre) + t, pre);
+        } else {
+          A.chunk_part[x.x + c] = t;
+          __threadfence();
+          const unsigned arrived = atomicAdd(A.chunk_cnt + x.x, 1u);
+          if (arrived == static_cast<unsigned>(nch - 1)) {
+            __threadfence();
+            double tot = 0.0;
+            for (int q = 0; q < nch; ++q) tot += __ldcg(A.chunk_part + x.x + q);
+            A.chunk_cnt[x.x] = 0;
+            Epi solo = epi;
+            solo.reset_acc();
+            const typename Epi::Pre pre = solo.load(d.x);
+            solo.line(d.x, solo.init(pre) + tot, pre);
+            solo.export_acc(A.line_acc + static_cast<int64_t>(x.z) * PDLPK_LINE_ACC);
+          }
+        }
+      }
+      continue;
+    }
+    int64_t rc = d.x;
+    double carry = 0.0;
+    int64_t sid = A.seg_step0[it];
+    for (int64_t base = e0 & ~int64_t(7); base < e1; base += 256, ++sid) {
+      const uint32_t mw = lane < 16 ? __ldg(A.seg_masks + sid * 16 + lane) : 0u;
+      const int64_t k0 = base + 8 * lane;
+      double p[8];
+      if (k0 + 8 > e0 && k0 < e1) {
+        const int4 i0 = ld_stream(reinterpret_cast<const int4*>(idx + k0));
+        const int4 i1 = ld_stream(reinterpret_cast<const int4*>(idx + k0 + 4));
+        const int ci[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 t = ld_stream(reinterpret_cast<const double2*>(vals + k0) + q);
+          p[2 * q] = t.x;
+          p[2 * q + 1] = t.y;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          p[u] = (k0 + u >= e0 && k0 + u < e1) ? p[u] * __ldg(v + ci[u]) : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = 0.0;
+      }
+      const uint32_t hw = __shfl_sync(0xffffffffu, mw, lane >> 2);
+      const uint32_t ew = __shfl_sync(0xffffffffu, mw, 8 + (lane >> 2));
+      const uint32_t hb = (hw >> (8 * (lane & 3))) & 0xffu, eb = (ew >> (8 * (lane & 3))) & 0xffu;
+      const int nend_lane = __popc(eb);
+      const int ends_before = warp_excl_scan_i(nend_lane, lane);
+      const int nend = __shfl_sync(0xffffffffu, ends_before + nend_lane, 31);
+      for (int j = lane; j < nend; j += 32) epi.prefetch(rc + j);
+      // the segment open at the lane's end, then the segmented scan of those
+      // across lanes: what flows into each lane
+      double tail = 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tail = ((hb >> u) & 1u) ? p[u] : tail + p[u];
+      const unsigned hmask = __ballot_sync(0xffffffffu, hb != 0u);
+      double inc = tail;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, inc, o);
+        const unsigned win = lane >= o ? (((2u << lane) - 1u) & ~((1u << (lane - o + 1)) - 1u)) : 0u;
+        if (lane >= o && (hmask & win) == 0u) inc += t;
+      }
+      double into = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) into = 0.0;
+      if ((hmask & ((1u << lane) - 1u)) == 0u) into += carry;
+      double run = into;
+      int64_t line = rc + ends_before;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        run = ((hb >> u) & 1u) ? p[u] : run + p[u];
+        if ((eb >> u) & 1u) {
+          const typename Epi::Pre pre = epi.load(line);
+          epi.line(line, epi.init(pre) + run, pre);
+          ++line;
+        }
+      }
+      carry = __shfl_sync(0xffffffffu, run, 31);
+      if ((__shfl_sync(0xffffffffu, eb, 31) >> 7) & 1u) carry = 0.0;
+      rc += nend;
+    }
+  }
+}
+
 // Segment mask of a layout: 1 chunks, 2 direct tiles, 4 staged tiles.
 // Kernels are instantiated per mask so each pass only pays the registers and
 // shared memory of the paths it runs.  The staged tile segment is kept when
 // nothing else exists so the grid is never empty (the column pass's last CTA
 // makes the step decision).
 __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
+  if (A.seg_mode) return 16;
   int s = A.n_chunks > A.n_cta_chunks ? 1 : 0;
   if (A.n_cta_chunks > 0) s |= 8;
   if (A.n_tiles > 0) s |= A.tile_direct ? 2 : 4;
@@ -142,8 +295,12 @@ __host__ __device__ inline int seg_mask(const pdlpk_csr& A) {
 #ifndef PDLPK_TILE_MIN_BLOCKS
 #define PDLPK_TILE_MIN_BLOCKS 4 /* CTAs/SM the staged-tile kernels are compiled for */
 #endif
+#ifndef PDLPK_SEG_MIN_BLOCKS
+#define PDLPK_SEG_MIN_BLOCKS 4 /* CTAs/SM the segmented-span kernels are compiled for */
+#endif
 __host__ __device__ constexpr int spmv_min_blocks(int seg) {
-  return seg == 2 ? 5 : (seg == 1 ? PDLPK_CHUNK_MIN_BLOCKS : ((seg & 4) ? PDLPK_TILE_MIN_BLOCKS : 4));
+  return seg == 16 ? PDLPK_SEG_MIN_BLOCKS
+                   : (seg == 2 ? 5 : (seg == 1 ? PDLPK_CHUNK_MIN_BLOCKS : ((seg & 4) ? PDLPK_TILE_MIN_BLOCKS : 4)));
 }
 
 // Chunk segments are grid-stride with a bounded number of CTAs: a pass pays
@@ -163,6 +320,7 @@ __host__ __device__ inline int64_t cta_chunk_blocks(const pdlpk_csr& A) {
 }
 
 __host__ __device__ inline int64_t sched_blocks(const pdlpk_csr& A) {
+  if (A.seg_mode) return A.tile_blocks;  // persistent warps over the spans
   const int s = seg_mask(A);
   return warp_chunk_blocks(A) + cta_chunk_blocks(A) + ((s & 6) ? A.tile_blocks : 0);
 }
@@ -281,6 +439,10 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   int64_t b = blockIdx.x;
+  if constexpr ((Seg & 16) != 0) {
+    seg_spans(A, vals, v, epi);
+    return;
+  }
   if constexpr ((Seg & 1) != 0) {
     const int64_t chunk_blocks = warp_chunk_blocks(A);
     if (b < chunk_blocks) {
@@ -298,7 +460,7 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
         warp_batches(idx, vals, v, lo + lane, hi, acc);
         const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
         const double t = warp_sum(s);
-        if (lane == 0) epi.line(r, t, pre);
+        if (lane == 0) epi.line(r, epi.init(pre) + t, pre);
       }
       return;
     }
@@ -334,7 +496,8 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
 #pragma unroll
         for (int w = 0; w < kSpmvWarps; ++w) sum += wsum[w];
         if (nch == 1) {
-          epi.line(r, sum, epi.load(r));
+          const typename Epi::Pre pre = epi.load(r);
+          epi.line(r, epi.init(pre) + sum, pre);
         } else {
           const int64_t c0 = c - (pos & 0xffff);
           A.chunk_part[c] = sum;
@@ -347,7 +510,8 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
             A.chunk_cnt[c0] = 0;
             Epi solo = epi;
             solo.reset_acc();
-            solo.line(r, tot, solo.load(r));
+            const typename Epi::Pre pre = solo.load(r);
+            solo.line(r, solo.init(pre) + tot, pre);
             solo.export_acc(A.line_acc + static_cast<int64_t>(A.chunk_slot[c]) * PDLPK_LINE_ACC);
           }
         }
@@ -370,7 +534,7 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
         const int64_t a = start[r], e = start[r + 1];
         // predicated pairs: independent loads, then the gathers, then the
         // products added in storage order (bit-identical line sums)
-        double acc = 0.0;
+        double acc = epi.init(pre);
         for (int64_t k = a; k < e; k += 2) {
           const bool two = k + 1 < e;
           const int32_t c0 = ld_stream(idx + k);
@@ -521,9 +685,10 @@ __device__ __forceinline__ void sched_spmv(const pdlpk_csr& A, const double* __r
             if (li < l1) {
               const int a = static_cast<int>(static_cast<int64_t>(s_ptr[li]) - tm.s0);
               const int e = static_cast<int>(static_cast<int64_t>(s_ptr[li + 1]) - tm.s0);
-              double acc = 0.0;
+              const typename Epi::Pre pre = epi.from_stage(s_epi, li);
+              double acc = epi.init(pre);  // 0, or the line's carried partial sum
               for (int j = a; j < e; ++j) acc += s_val[j];
-              epi.line(tm.r0 + li, acc, epi.from_stage(s_epi, li));
+              epi.line(tm.r0 + li, acc, pre);
             }
           }
         }
@@ -547,6 +712,7 @@ inline int dispatch_seg(int seg, F&& f) {
     case 8: return f.template go<P, 8>();
     case 9: return f.template go<P, 9>();
     case 12: return f.template go<P, 12>();
+    case 16: return f.template go<P, 16>();
     default: return f.template go<P, 13>();  // (direct tiles never mix with CTA chunks)
   }
 }

@@ -442,3 +442,62 @@ def test_perf_mode_deterministic_on_skewed_instance(gpu, ref):
     gx, gy = _trace(P.solve, p, _opts(tol=(0.0, 0.0, 0.0), mode="perf"), n_iter=30)
     rx, ry = _trace(ref.solve, p, _opts(tol=(0.0, 0.0, 0.0)), n_iter=30)
     assert max_rel(gx, rx) <= 1e-9 and max_rel(gy, ry) <= 1e-9
+
+
+# ------------------------------------------- segmented spans / row panels ---
+def _skewed_cases():
+    rng = np.random.default_rng(77)
+    cases = [P.generate("c2", 3, rows=5000, cols=6000, kmax=5000),
+             P.generate("c1", 0, sources=40, sinks=50)]
+    for _ in range(6):  # small random LPs: empty rows/columns, ragged lines
+        cases.append(random_box_lp(rng, 1 + rng.integers(60), 1 + rng.integers(60)))
+    return cases
+
+
+def test_spmv_segmented_spans(gpu, ref, monkeypatch):
+    # The segmented-span schedule (spmv.cuh seg_spans: lane-contiguous
+    # entries, segmented scan across lanes, chunked long lines, empty lines)
+    # forced on every layout; the products must match the reference's.
+    monkeypatch.setenv("PDLP_SEG", "1")
+    rng = np.random.default_rng(5)
+    for p in _skewed_cases():
+        x = rng.uniform(-1, 1, p.cols())
+        y = rng.uniform(-1, 1, p.rows())
+        np.testing.assert_allclose(P.spmv(p, x, mode="perf"), ref.spmv(p, x), rtol=1e-11, atol=1e-9)
+        np.testing.assert_allclose(P.spmv_transpose(p, y, mode="perf"), ref.spmv_transpose(p, y),
+                                   rtol=1e-11, atol=1e-9)
+
+
+def test_solve_segmented_spans_tracks_tiles(gpu, ref, monkeypatch):
+    # A perf-mode solve with the segmented spans on both layouts reaches the
+    # same outcome as with the tile schedule and as the reference.
+    p = P.generate("c2", 1, rows=500, cols=1000)
+    tol = P.relative_tolerances(p)
+    o = P.SolverOptions(tolerances=P.TerminationTolerances(*tol), iteration_limit=100000)
+    monkeypatch.setenv("PDLP_SEG", "0")
+    a = P.solve(p, o)
+    monkeypatch.setenv("PDLP_SEG", "1")
+    b = P.solve(p, o)
+    r = ref.solve(p, o)
+    assert a.status == b.status == r.status
+    for res in (a, b):
+        s = res.summary
+        assert s.primal_residual_inf <= tol[0] and s.dual_residual_inf <= tol[1]
+        assert abs(s.primal_objective - r.summary.primal_objective) <= 1e-3 * (1 + abs(r.summary.primal_objective))
+
+
+def test_row_panels_bit_identical(gpu, monkeypatch):
+    # Column panels chain each row's running sum from panel to panel in
+    # storage order, and the step's row-pass reductions are per line
+    # (m <= PDLPK_LINE_PARTIALS_MAX): iterates with and without panels are
+    # bit-identical.
+    p = P.generate("c2", 2, rows=20000, cols=40000, kmax=400)
+    assert np.diff(p.a.by_row.start).max() <= 64  # every row in the storage-order tile path
+    o = P.SolverOptions(tolerances=P.TerminationTolerances(0.0, 0.0, 0.0), iteration_limit=300)
+    monkeypatch.setenv("PDLP_ROW_PANELS", "0")
+    a = P.solve(p, o)
+    for np_ in ("2", "3"):
+        monkeypatch.setenv("PDLP_ROW_PANELS", np_)
+        b = P.solve(p, o)
+        assert a.iterations == b.iterations and a.restarts == b.restarts
+        assert same_bits(a.x, b.x) and same_bits(a.y, b.y), np_

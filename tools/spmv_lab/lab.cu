@@ -128,6 +128,11 @@ struct RowEpi {
     dy[r] = d;
     acc2 += d * d;
   }
+  __device__ __forceinline__ void prefetch(int64_t r) const {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(y + r));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(lc + r));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(uc + r));
+  }
   static constexpr int kRW = 5;  // 8-byte words per line
 };
 // Column-pass epilogue: R aty, x, x'; W aty'; |dx|^2, curvature partials.
@@ -143,7 +148,23 @@ struct ColEpi {
     acc2 += dx * dx;
     curv += d * dx;
   }
+  __device__ __forceinline__ void prefetch(int64_t i) const {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(aty + i));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(x + i));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(xn + i));
+  }
   static constexpr int kRW = 4;
+};
+
+// Column epilogue without operand loads (measurement: the products and the
+// one store only).
+struct ColEpiNull {
+  double* atyn;
+  double acc2 = 0.0;
+  struct Pre { double a; };
+  __device__ __forceinline__ Pre load(int64_t) const { return {0.0}; }
+  __device__ __forceinline__ void prefetch(int64_t) const {}
+  __device__ __forceinline__ void line(int64_t i, double d, const Pre&) { atyn[i] = d; acc2 += d; }
 };
 
 // Uniform warp items.  Block item {r0, cnt > 0}: lines r0..r0+cnt-1 (<= 63
@@ -527,6 +548,509 @@ std::vector<int4> build_tiles(const std::vector<int32_t>& st, int E, int L, int 
   return t;
 }
 
+// Stream + gather probe: acc += val[k] * v[idx[k]] over all entries with
+// coalesced LDG streams (no line structure): the ceiling of an LDG-fed SpMV.
+template <int U>
+__global__ void __launch_bounds__(256) stream_gather_probe(const int32_t* __restrict__ idx,
+                                                           const double* __restrict__ val,
+                                                           const double* __restrict__ v, int64_t nnz,
+                                                           double* out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = tid >> 5, nw = nt >> 5;
+  double acc = 0.0;
+  for (int64_t b = w * 32 * U; b < nnz; b += nw * 32 * U) {
+    int ci[U];
+    double a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = b + u * 32 + lane;
+      ci[u] = k < nnz ? __ldcs(idx + k) : 0;
+      a[u] = k < nnz ? __ldcs(val + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += a[u] * __ldg(v + ci[u]);
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
+// Segmented-scan warp spans.  Span {r0, nl > 0, e0, len}: whole lines
+// r0..r0+nl-1 (entries [e0, e0+len), no empty line).  Span {r, -1-c, e0, len}
+// with (slot, nch) in spanB: chunk c of a long line.  A warp walks its span in
+// steps of 256 entries: coalesced index/value loads, 8 gathers per lane,
+// then a segmented inclusive scan across lanes (head flags from the line
+// starts) with a carry between rows and steps; the lane holding a line's
+// last entry runs the epilogue.
+__device__ __forceinline__ double seg_scan(double v, bool head, int lane) {
+  // inclusive segmented scan over the warp; a head starts a new segment
+  unsigned hb = __ballot_sync(0xffffffffu, head);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, v, o);
+    // lanes (lane-o, lane] contain no head after lane-o ... include t iff no
+    // head in (lane-o, lane]
+    const unsigned span = lane >= o ? ((lane == 31 ? 0xffffffffu : ((1u << (lane + 1)) - 1u)) &
+                                       ~((1u << (lane - o + 1)) - 1u)) : 0u;
+    if (lane >= o && (hb & span) == 0u) v += t;
+  }
+  return v;
+}
+
+template <class Epi, int MINB>
+__global__ void __launch_bounds__(256, MINB) seg_kernel(const int4* __restrict__ spans, const int2* __restrict__ spanB,
+                                                        int64_t n_spans, const int32_t* __restrict__ start,
+                                                        const int32_t* __restrict__ idx,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ v, Epi epi,
+                                                        double* part, unsigned* cnt, double* out_part) {
+  __shared__ unsigned masks[8][16];  // per warp: 8 head words, 8 end words
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned* hm = masks[wid];
+  unsigned* em = masks[wid] + 8;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = gw; it < n_spans; it += nw) {
+    const int4 d = spans[it];
+    const int e0 = d.z, e1 = d.z + d.w;
+    if (d.y < 0) {
+      // chunk of a long line: tree sum, ordered combine of the chunks
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int base = e0; base < e1; base += 256) {
+        int ci[8];
+        double a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = base + 32 * u + lane;
+          ci[u] = k < e1 ? ldcs(idx + k) : 0;
+          a[u] = k < e1 ? ldcs(val + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u & 3] += a[u] * __ldg(v + ci[u]);
+      }
+      const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+      if (lane == 0) {
+        const int2 b = spanB[it];
+        const int c = -1 - d.y, nch = b.y;
+        if (nch == 1) {
+          epi.line(d.x, t, epi.load(d.x));
+        } else {
+          part[b.x + c] = t;
+          __threadfence();
+          const unsigned old = atomicAdd(cnt + b.x, 1u);
+          if (old == (unsigned)(nch - 1)) {
+            __threadfence();
+            double tot = 0.0;
+            for (int q = 0; q < nch; ++q) tot += __ldcg(part + b.x + q);
+            cnt[b.x] = 0;
+            epi.line(d.x, tot, epi.load(d.x));
+          }
+        }
+      }
+      continue;
+    }
+    const int rend = d.x + d.y;  // one past the last line
+    int rc = d.x;                // line containing the step's first entry
+    double carry = 0.0;          // running sum of the segment open at the step start
+    for (int base = e0; base < e1; base += 256) {
+      // products
+      double p[8];
+      {
+        int ci[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = base + 32 * u + lane;
+          ci[u] = k < e1 ? ldcs(idx + k) : 0;
+          p[u] = k < e1 ? ldcs(val + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = p[u] * __ldg(v + ci[u]);
+      }
+      // head / end masks of this step from the line starts
+      if (lane < 16) hm[lane] = 0u;
+      __syncwarp();
+      for (int j0 = rc; ; j0 += 32) {
+        const int r = j0 + lane;
+        const int sr = r <= rend ? start[r] : 0x7fffffff;
+        if (r <= rend) {
+          const int o = sr - base;
+          if (o >= 0 && o < 256 && r < rend) atomicOr(&hm[o >> 5], 1u << (o & 31));
+          if (o > 0 && o <= 256) atomicOr(&em[(o - 1) >> 5], 1u << ((o - 1) & 31));
+        }
+        const int last = __shfl_sync(0xffffffffu, sr, 31);
+        if (last > base + 256 || j0 + 32 > rend) break;
+      }
+      __syncwarp();
+      // segmented scan row by row, carrying the open segment
+      int lines_done = 0;  // lines completed before this row (in this step)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const unsigned h = hm[u], e = em[u];
+        const bool head = (h >> lane) & 1u;
+        double s = seg_scan(p[u], head, lane);
+        const unsigned upto = lane == 31 ? 0xffffffffu : ((1u << (lane + 1)) - 1u);
+        if ((h & upto) == 0u) s += carry;  // still in the segment open at the row start
+        // lines completed up to this lane: ends in earlier rows + ends in (.., lane)
+        const int rank = lines_done + __popc(e & (upto >> 1));
+        if ((e >> lane) & 1u) {
+          const int line = rc + rank;
+          epi.line(line, s, epi.load(line));
+        }
+        carry = __shfl_sync(0xffffffffu, s, 31);
+        if ((e >> 31) & 1u) carry = 0.0;
+        lines_done += __popc(e);
+      }
+      rc += lines_done;
+      __syncwarp();
+    }
+  }
+  double s = warp_sum(epi.acc2);
+  if (lane == 0) out_part[blockIdx.x * 8 + wid] = s;
+}
+
+// v2: head/end masks precomputed per step (2U words per step: U head words,
+// U end words), U rows of 32 entries per step, L2 prefetch of the step's
+// epilogue operands.
+template <int U, class Epi, int MINB>
+__global__ void __launch_bounds__(256, MINB) seg2_kernel(const int4* __restrict__ spans, const int2* __restrict__ spanB,
+                                                         const int32_t* __restrict__ step0, const uint32_t* __restrict__ masks,
+                                                         int64_t n_spans,
+                                                         const int32_t* __restrict__ idx,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ v, Epi epi,
+                                                         double* part, unsigned* cnt, double* out_part) {
+  constexpr int STEP = 32 * U;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = gw; it < n_spans; it += nw) {
+    const int4 d = spans[it];
+    const int e0 = d.z, e1 = d.z + d.w;
+    if (d.y < 0) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int base = e0; base < e1; base += 256) {
+        int ci[8];
+        double a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = base + 32 * u + lane;
+          ci[u] = k < e1 ? ldcs(idx + k) : 0;
+          a[u] = k < e1 ? ldcs(val + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u & 3] += a[u] * __ldg(v + ci[u]);
+      }
+      const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+      if (lane == 0) {
+        const int2 b = spanB[it];
+        const int c = -1 - d.y, nch = b.y;
+        if (nch == 1) {
+          epi.line(d.x, t, epi.load(d.x));
+        } else {
+          part[b.x + c] = t;
+          __threadfence();
+          const unsigned old = atomicAdd(cnt + b.x, 1u);
+          if (old == (unsigned)(nch - 1)) {
+            __threadfence();
+            double tot = 0.0;
+            for (int q = 0; q < nch; ++q) tot += __ldcg(part + b.x + q);
+            cnt[b.x] = 0;
+            epi.line(d.x, tot, epi.load(d.x));
+          }
+        }
+      }
+      continue;
+    }
+    int rc = d.x;
+    double carry = 0.0;
+    int sid = step0[it];
+    for (int base = e0; base < e1; base += STEP, ++sid) {
+      const uint32_t mw = lane < 2 * U ? __ldg(masks + (int64_t)sid * 2 * U + lane) : 0u;
+      double p[U];
+      {
+        int ci[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = base + 32 * u + lane;
+          ci[u] = k < e1 ? ldcs(idx + k) : 0;
+          p[u] = k < e1 ? ldcs(val + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) p[u] = p[u] * __ldg(v + ci[u]);
+      }
+      // the lines ending in this step: rc .. rc + nend - 1; warm their operands in L2
+      int nend = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) nend += __popc(__shfl_sync(0xffffffffu, mw, U + u));
+      for (int j = lane; j < nend; j += 32) epi.prefetch(rc + j);
+      int lines_done = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned h = __shfl_sync(0xffffffffu, mw, u), e = __shfl_sync(0xffffffffu, mw, U + u);
+        const bool head = (h >> lane) & 1u;
+        double s = seg_scan(p[u], head, lane);
+        const unsigned upto = lane == 31 ? 0xffffffffu : ((1u << (lane + 1)) - 1u);
+        if ((h & upto) == 0u) s += carry;
+        if ((e >> lane) & 1u) {
+          const int line = rc + lines_done + __popc(e & (upto >> 1));
+          epi.line(line, s, epi.load(line));
+        }
+        carry = __shfl_sync(0xffffffffu, s, 31);
+        if ((e >> 31) & 1u) carry = 0.0;
+        lines_done += __popc(e);
+      }
+      rc += lines_done;
+    }
+  }
+  double s = warp_sum(epi.acc2);
+  if (lane == 0) out_part[blockIdx.x * 8 + wid] = s;
+}
+
+// v3: lane-contiguous entries.  Steps of 256 entries start on 8-entry
+// boundaries; lane l holds entries [base + 8l, base + 8l + 8) (vector loads),
+// sums its line segments sequentially (storage order inside a lane), and one
+// segmented scan across lanes joins segments that span lanes; a carry joins
+// steps.  Head/end bits: per-step 256-bit masks (8 + 8 words).
+__device__ __forceinline__ int warp_excl_scan_int(int v, int lane) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  return x - v;
+}
+
+template <class Epi, int MINB>
+__global__ void __launch_bounds__(256, MINB) seg3_kernel(const int4* __restrict__ spans, const int2* __restrict__ spanB,
+                                                         const int32_t* __restrict__ step0, const uint32_t* __restrict__ masks,
+                                                         int64_t n_spans,
+                                                         const int32_t* __restrict__ idx,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ v, Epi epi,
+                                                         double* part, unsigned* cnt, double* out_part) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = gw; it < n_spans; it += nw) {
+    const int4 d = spans[it];
+    const int e0 = d.z, e1 = d.z + d.w;
+    if (d.y < 0) {
+      // chunk of a long line: lane-contiguous products, tree, ordered combine
+      double acc = 0.0;
+      for (int base = e0 & ~7; base < e1; base += 256) {
+        const int k0 = base + 8 * lane;
+        if (k0 + 8 > e0 && k0 < e1) {
+          const int4 i0 = __ldcs(reinterpret_cast<const int4*>(idx + k0));
+          const int4 i1 = __ldcs(reinterpret_cast<const int4*>(idx + k0 + 4));
+          const int ci[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+          double a[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double2 t = __ldcs(reinterpret_cast<const double2*>(val + k0) + q);
+            a[2 * q] = t.x;
+            a[2 * q + 1] = t.y;
+          }
+          double g[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) g[u] = (k0 + u >= e0 && k0 + u < e1) ? __ldg(v + ci[u]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc += (k0 + u >= e0 && k0 + u < e1) ? a[u] * g[u] : 0.0;
+        }
+      }
+      const double t = warp_sum(acc);
+      if (lane == 0) {
+        const int2 b = spanB[it];
+        const int c = -1 - d.y, nch = b.y;
+        if (nch == 1) {
+          epi.line(d.x, t, epi.load(d.x));
+        } else {
+          part[b.x + c] = t;
+          __threadfence();
+          const unsigned old = atomicAdd(cnt + b.x, 1u);
+          if (old == (unsigned)(nch - 1)) {
+            __threadfence();
+            double tot = 0.0;
+            for (int q = 0; q < nch; ++q) tot += __ldcg(part + b.x + q);
+            cnt[b.x] = 0;
+            epi.line(d.x, tot, epi.load(d.x));
+          }
+        }
+      }
+      continue;
+    }
+    int rc = d.x;
+    double carry = 0.0;
+    int sid = step0[it];
+    for (int base = e0 & ~7; base < e1; base += 256, ++sid) {
+      const uint32_t mw = lane < 16 ? __ldg(masks + (int64_t)sid * 16 + lane) : 0u;
+      const int k0 = base + 8 * lane;
+      const bool any = k0 + 8 > e0 && k0 < e1;
+      double p[8];
+      if (any) {
+        const int4 i0 = __ldcs(reinterpret_cast<const int4*>(idx + k0));
+        const int4 i1 = __ldcs(reinterpret_cast<const int4*>(idx + k0 + 4));
+        const int ci[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 t = __ldcs(reinterpret_cast<const double2*>(val + k0) + q);
+          p[2 * q] = t.x;
+          p[2 * q + 1] = t.y;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = (k0 + u >= e0 && k0 + u < e1) ? p[u] * __ldg(v + ci[u]) : 0.0;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = 0.0;
+      }
+      const uint32_t hw = __shfl_sync(0xffffffffu, mw, lane >> 2), ew = __shfl_sync(0xffffffffu, mw, 8 + (lane >> 2));
+      const uint32_t hb = (hw >> (8 * (lane & 3))) & 0xffu, eb = (ew >> (8 * (lane & 3))) & 0xffu;
+      // lines ending in this step: warm their operands in L2
+      const int nend_lane = __popc(eb);
+      const int ends_before = warp_excl_scan_int(nend_lane, lane);
+      const int nend = __shfl_sync(0xffffffffu, ends_before + nend_lane, 31);
+      for (int j = lane; j < nend; j += 32) epi.prefetch(rc + j);
+      // pass 1: the open segment at the lane's end
+      double tail = 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tail = ((hb >> u) & 1u) ? p[u] : tail + p[u];
+      // segmented exclusive scan of the tails: the sum carried into the lane
+      const bool hh = hb != 0u;
+      double inc = tail;
+      {
+        const unsigned hmask = __ballot_sync(0xffffffffu, hh);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double t = __shfl_up_sync(0xffffffffu, inc, o);
+          // add lanes (lane-o, lane-1]'s tails only if no head in lanes (lane-o, lane-1] ... i.e. window
+          const unsigned win = lane >= o ? (((1u << lane) - 1u) & ~((1u << (lane - o + 1)) - 1u)) : 0u;
+          if (lane >= o && (hmask & (win | (1u << lane))) == 0u) inc += t;
+        }
+        // inc = inclusive sum of tails back to (and including) the nearest
+        // lane with a head, excluding that lane's pre-head part (its tail
+        // starts at its head).  The carry enters lanes with no head before.
+        const unsigned before = hmask & ((1u << lane) - 1u);
+        double into = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) into = 0.0;
+        if (before == 0u) into += carry;
+        // pass 2: emit the lines ending in this lane
+        double run = into;
+        int rank = ends_before;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          run = ((hb >> u) & 1u) ? p[u] : run + p[u];
+          if ((eb >> u) & 1u) {
+            const int line = rc + rank;
+            epi.line(line, run, epi.load(line));
+            ++rank;
+          }
+        }
+        // carry out of the step: lane 31's open segment
+        double c31 = __shfl_sync(0xffffffffu, run, 31);
+        carry = c31;
+        const uint32_t eb31 = __shfl_sync(0xffffffffu, eb, 31);
+        if ((eb31 >> 7) & 1u) carry = 0.0;
+      }
+      rc += nend;
+    }
+  }
+  double s = warp_sum(epi.acc2);
+  if (lane == 0) out_part[blockIdx.x * 8 + wid] = s;
+}
+
+// masks for v3: steps from e0 & ~7 in 256-entry strides, 8 head + 8 end words
+std::vector<uint32_t> build_masks3(const std::vector<int32_t>& st, const std::vector<int4>& spans,
+                                   std::vector<int32_t>& step0) {
+  step0.assign(spans.size(), 0);
+  int64_t nsteps = 0;
+  for (size_t i = 0; i < spans.size(); ++i) {
+    step0[i] = (int32_t)nsteps;
+    if (spans[i].y > 0) {
+      const int b0 = spans[i].z & ~7;
+      nsteps += (spans[i].z + spans[i].w - b0 + 255) / 256;
+    }
+  }
+  std::vector<uint32_t> M((size_t)nsteps * 16 + 16, 0u);
+  for (size_t i = 0; i < spans.size(); ++i) {
+    const int4 d = spans[i];
+    if (d.y <= 0) continue;
+    const int b0 = d.z & ~7;
+    for (int r = d.x; r < d.x + d.y; ++r) {
+      const int oh = st[r] - b0, oe = st[r + 1] - 1 - b0;
+      M[(size_t)(step0[i] + oh / 256) * 16 + (oh % 256) / 32] |= 1u << (oh % 32);
+      M[(size_t)(step0[i] + oe / 256) * 16 + 8 + (oe % 256) / 32] |= 1u << (oe % 32);
+    }
+  }
+  return M;
+}
+
+// per-step masks of a span schedule (host)
+std::vector<uint32_t> build_masks(const std::vector<int32_t>& st, const std::vector<int4>& spans, int U,
+                                  std::vector<int32_t>& step0) {
+  const int STEP = 32 * U;
+  step0.assign(spans.size(), 0);
+  int64_t nsteps = 0;
+  for (size_t i = 0; i < spans.size(); ++i) {
+    step0[i] = (int32_t)nsteps;
+    if (spans[i].y > 0) nsteps += (spans[i].w + STEP - 1) / STEP;
+  }
+  std::vector<uint32_t> M((size_t)nsteps * 2 * U + 16, 0u);
+  for (size_t i = 0; i < spans.size(); ++i) {
+    const int4 d = spans[i];
+    if (d.y <= 0) continue;
+    for (int r = d.x; r < d.x + d.y; ++r) {
+      const int oh = st[r] - d.z, oe = st[r + 1] - 1 - d.z;
+      const int64_t sh = step0[i] + oh / STEP, se = step0[i] + oe / STEP;
+      M[(size_t)sh * 2 * U + (oh % STEP) / 32] |= 1u << (oh % 32);
+      M[(size_t)se * 2 * U + U + (oe % STEP) / 32] |= 1u << (oe % 32);
+    }
+  }
+  return M;
+}
+
+std::vector<int4> build_spans(const std::vector<int32_t>& st, int span, std::vector<int2>& B, int64_t& slots) {
+  std::vector<int4> out;
+  B.clear();
+  slots = 0;
+  const int64_t dim = (int64_t)st.size() - 1;
+  int r0 = -1, nl = 0, nz = 0;
+  auto close = [&] {
+    if (nl > 0) { out.push_back(make_int4(r0, nl, st[r0], nz)); B.push_back(make_int2(0, 0)); }
+    nl = 0; nz = 0;
+  };
+  for (int64_t r = 0; r < dim; ++r) {
+    const int len = st[r + 1] - st[r];
+    if (len == 0) { close(); continue; }  // (lab: empty lines skipped)
+    if (len > span) {
+      close();
+      const int nch = (len + span - 1) / span;
+      for (int c = 0; c < nch; ++c) {
+        const int b = st[r] + c * span;
+        out.push_back(make_int4((int)r, -1 - c, b, std::min(span, st[r + 1] - b)));
+        B.push_back(make_int2((int)slots, nch));
+      }
+      slots += nch;
+      continue;
+    }
+    if (nz + len > span) close();
+    if (nl == 0) r0 = (int)r;
+    ++nl;
+    nz += len;
+  }
+  close();
+  return out;
+}
+
+__global__ void compare_kernel(const double* a, const double* b, int64_t n, double* out) {
+  double mx = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = fabs(a[i] - b[i]) / fmax(1e-300, fmax(fabs(a[i]), fabs(b[i])));
+    mx = fmax(mx, (fabs(a[i] - b[i]) < 1e-300) ? 0.0 : d);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned long long*>(out), __double_as_longlong(mx));
+}
+
 // ------------------------------------------------------------- schedule ---
 std::vector<int4> build_items(const std::vector<int32_t>& st, int item, int seqmax, int64_t& n_slots,
                               bool long_only = false) {
@@ -631,10 +1155,10 @@ int main(int argc, char** argv) {
   Csr K, KT;
   K.dim = m; K.nnz = nnz; K.other = n;
   KT.dim = n; KT.nnz = nnz; KT.other = m;
-  CK(cudaMalloc(&K.idx, nnz * 4));
-  CK(cudaMalloc(&K.val, nnz * 8));
-  CK(cudaMalloc(&KT.idx, nnz * 4));
-  CK(cudaMalloc(&KT.val, nnz * 8));
+  CK(cudaMalloc(&K.idx, nnz * 4 + 256));
+  CK(cudaMalloc(&K.val, nnz * 8 + 256));
+  CK(cudaMalloc(&KT.idx, nnz * 4 + 256));
+  CK(cudaMalloc(&KT.val, nnz * 8 + 256));
   {
     size_t tb = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tb, kr, k2, nnz, 0, 47);
@@ -688,6 +1212,7 @@ int main(int argc, char** argv) {
   RowEpi re{V.y, V.lc, V.uc, V.yn, V.dy, 0.37};
   ColEpi ce{V.aty, V.x, V.xn, V.atyn};
   auto want = [&](const char* label) { return only == nullptr || std::strstr(label, only) != nullptr; };
+  auto group = [&](const char* g) { return only == nullptr || std::strstr(only, g) != nullptr; };
   auto report = [&](const char* name, float us, double bytes) {
     std::printf("%-44s %9.1f us  %7.0f GB/s  %.3f of peak\n", name, us, bytes / us / 1e3, bytes / us / 1e3 / peak);
   };
@@ -768,7 +1293,7 @@ int main(int argc, char** argv) {
   run_wb(I256{}, B4{}, KT, 128, ce, V.dyg, col_bytes, "col");
   run_wb(I128{}, B4{}, KT, 64, ce, V.dyg, col_bytes, "col");
   run_wb(I512{}, B2{}, KT, 64, ce, V.dyg, col_bytes, "col");
-  if (want("gather")) {
+  if (group("gather")) {
     double* big;
     const int64_t maxlen = 20000000;
     CK(cudaMalloc(&big, maxlen * 8));
@@ -833,6 +1358,222 @@ int main(int argc, char** argv) {
   run_wb(I256{}, B4{}, KT, 64, ce, V.dyg, col_bytes, "collong", true);
   run_wb(I256{}, B3{}, KT, 64, ce, V.dyg, col_bytes, "collong", true);
   run_wb(I512{}, B2{}, KT, 64, ce, V.dyg, col_bytes, "collong", true);
+  if (group("sgp")) {
+    for (int per : {4, 8}) {
+      const int grid = sms * per;
+      float us;
+      us = time_it([&] { stream_gather_probe<4><<<grid, 256>>>(KT.idx, KT.val, V.dyg, nnz, outp); }, reps);
+      std::printf("sgp col (dy 40MB) U=4 %d/SM: %.1f us = %.1f Gentry/s\n", per, us, nnz / us / 1e3);
+      us = time_it([&] { stream_gather_probe<8><<<grid, 256>>>(KT.idx, KT.val, V.dyg, nnz, outp); }, reps);
+      std::printf("sgp col (dy 40MB) U=8 %d/SM: %.1f us = %.1f Gentry/s\n", per, us, nnz / us / 1e3);
+      us = time_it([&] { stream_gather_probe<16><<<grid, 256>>>(KT.idx, KT.val, V.dyg, nnz, outp); }, reps);
+      std::printf("sgp col (dy 40MB) U=16 %d/SM: %.1f us = %.1f Gentry/s\n", per, us, nnz / us / 1e3);
+      us = time_it([&] { stream_gather_probe<8><<<grid, 256>>>(K.idx, K.val, V.xb, nnz, outp); }, reps);
+      std::printf("sgp row (xb 80MB) U=8 %d/SM: %.1f us = %.1f Gentry/s\n", per, us, nnz / us / 1e3);
+    }
+  }
+  auto run_seg = [&](auto tag_minb, const Csr& A, int span, auto epi, const double* v, double bytes,
+                     const char* nm, double* outv, double* refv) {
+    constexpr int MINB = decltype(tag_minb)::value;
+    char lb[160];
+    std::snprintf(lb, sizeof lb, "%s seg span=%d minb=%d", nm, span, MINB);
+    if (!want(lb)) return;
+    std::vector<int2> B;
+    int64_t slots = 0;
+    std::vector<int4> sp = build_spans(A.hstart, span, B, slots);
+    int4* d_s;
+    int2* d_b;
+    CK(cudaMalloc(&d_s, sp.size() * sizeof(int4) + 16));
+    CK(cudaMalloc(&d_b, B.size() * sizeof(int2) + 16));
+    CK(cudaMemcpy(d_s, sp.data(), sp.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_b, B.data(), B.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    double* part;
+    unsigned* cntp;
+    CK(cudaMalloc(&part, (slots + 1) * 8));
+    CK(cudaMalloc(&cntp, (slots + 1) * 4));
+    CK(cudaMemset(cntp, 0, (slots + 1) * 4));
+    auto k = seg_kernel<decltype(epi), MINB>;
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 256, 0));
+    const int grid = sms * per;
+    float us = time_it([&] { k<<<grid, 256>>>(d_s, d_b, (int64_t)sp.size(), A.start, A.idx, A.val, v, epi, part, cntp, outp); }, reps);
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "%s (%d/SM, %zu spans)", lb, per, sp.size());
+    report(buf, us, bytes);
+    if (refv != nullptr) {
+      double* mx;
+      CK(cudaMalloc(&mx, 8));
+      CK(cudaMemset(mx, 0, 8));
+      compare_kernel<<<1024, 256>>>(outv, refv, A.dim, mx);
+      double h = 0;
+      CK(cudaMemcpy(&h, mx, 8, cudaMemcpyDeviceToHost));
+      std::printf("   max rel diff vs vec kernel: %.3e\n", h);
+      cudaFree(mx);
+    }
+    cudaFree(d_s); cudaFree(d_b); cudaFree(part); cudaFree(cntp);
+  };
+  auto run_seg2 = [&](auto tag_u, auto tag_minb, const Csr& A, int span, auto epi, const double* v, double bytes,
+                      const char* nm, double* outv, double* refv) {
+    constexpr int U = decltype(tag_u)::value;
+    constexpr int MINB = decltype(tag_minb)::value;
+    char lb[160];
+    std::snprintf(lb, sizeof lb, "%s seg2 U=%d span=%d minb=%d", nm, U, span, MINB);
+    if (!want(lb)) return;
+    std::vector<int2> B;
+    int64_t slots = 0;
+    std::vector<int4> sp = build_spans(A.hstart, span, B, slots);
+    std::vector<int32_t> s0;
+    std::vector<uint32_t> M = build_masks(A.hstart, sp, U, s0);
+    int4* d_s;
+    int2* d_b;
+    int32_t* d_s0;
+    uint32_t* d_m;
+    CK(cudaMalloc(&d_s, sp.size() * sizeof(int4) + 16));
+    CK(cudaMalloc(&d_b, B.size() * sizeof(int2) + 16));
+    CK(cudaMalloc(&d_s0, s0.size() * 4 + 16));
+    CK(cudaMalloc(&d_m, M.size() * 4 + 16));
+    CK(cudaMemcpy(d_s, sp.data(), sp.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_b, B.data(), B.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_s0, s0.data(), s0.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_m, M.data(), M.size() * 4, cudaMemcpyHostToDevice));
+    double* part;
+    unsigned* cntp;
+    CK(cudaMalloc(&part, (slots + 1) * 8));
+    CK(cudaMalloc(&cntp, (slots + 1) * 4));
+    CK(cudaMemset(cntp, 0, (slots + 1) * 4));
+    auto k = seg2_kernel<U, decltype(epi), MINB>;
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 256, 0));
+    const int grid = sms * per;
+    float us = time_it([&] { k<<<grid, 256>>>(d_s, d_b, d_s0, d_m, (int64_t)sp.size(), A.idx, A.val, v, epi, part, cntp, outp); }, reps);
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "%s (%d/SM, %zu spans, masks %.0f MB)", lb, per, sp.size(), M.size() * 4 / 1e6);
+    report(buf, us, bytes);
+    if (refv != nullptr) {
+      double* mx;
+      CK(cudaMalloc(&mx, 8));
+      CK(cudaMemset(mx, 0, 8));
+      compare_kernel<<<1024, 256>>>(outv, refv, A.dim, mx);
+      double h = 0;
+      CK(cudaMemcpy(&h, mx, 8, cudaMemcpyDeviceToHost));
+      std::printf("   max rel diff vs vec kernel: %.3e\n", h);
+      cudaFree(mx);
+    }
+    cudaFree(d_s); cudaFree(d_b); cudaFree(d_s0); cudaFree(d_m); cudaFree(part); cudaFree(cntp);
+  };
+  using U4 = std::integral_constant<int, 4>;
+  using U8 = std::integral_constant<int, 8>;
+  using B5 = std::integral_constant<int, 5>;
+  using B6 = std::integral_constant<int, 6>;
+  auto run_seg3 = [&](auto tag_minb, const Csr& A, int span, auto epi, const double* v, double bytes,
+                      const char* nm, double* outv, double* refv) {
+    constexpr int MINB = decltype(tag_minb)::value;
+    char lb[160];
+    std::snprintf(lb, sizeof lb, "%s seg3 span=%d minb=%d", nm, span, MINB);
+    if (!want(lb)) return;
+    std::vector<int2> B;
+    int64_t slots = 0;
+    std::vector<int4> sp = build_spans(A.hstart, span, B, slots);
+    std::vector<int32_t> s0;
+    std::vector<uint32_t> M = build_masks3(A.hstart, sp, s0);
+    int4* d_s;
+    int2* d_b;
+    int32_t* d_s0;
+    uint32_t* d_m;
+    CK(cudaMalloc(&d_s, sp.size() * sizeof(int4) + 16));
+    CK(cudaMalloc(&d_b, B.size() * sizeof(int2) + 16));
+    CK(cudaMalloc(&d_s0, s0.size() * 4 + 16));
+    CK(cudaMalloc(&d_m, M.size() * 4 + 16));
+    CK(cudaMemcpy(d_s, sp.data(), sp.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_b, B.data(), B.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_s0, s0.data(), s0.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_m, M.data(), M.size() * 4, cudaMemcpyHostToDevice));
+    double* part;
+    unsigned* cntp;
+    CK(cudaMalloc(&part, (slots + 1) * 8));
+    CK(cudaMalloc(&cntp, (slots + 1) * 4));
+    CK(cudaMemset(cntp, 0, (slots + 1) * 4));
+    auto k = seg3_kernel<decltype(epi), MINB>;
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 256, 0));
+    const int grid = sms * per;
+    float us = time_it([&] { k<<<grid, 256>>>(d_s, d_b, d_s0, d_m, (int64_t)sp.size(), A.idx, A.val, v, epi, part, cntp, outp); }, reps);
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "%s (%d/SM, %zu spans, masks %.0f MB)", lb, per, sp.size(), M.size() * 4 / 1e6);
+    report(buf, us, bytes);
+    if (refv != nullptr) {
+      double* mx;
+      CK(cudaMalloc(&mx, 8));
+      CK(cudaMemset(mx, 0, 8));
+      compare_kernel<<<1024, 256>>>(outv, refv, A.dim, mx);
+      double h = 0;
+      CK(cudaMemcpy(&h, mx, 8, cudaMemcpyDeviceToHost));
+      std::printf("   max rel diff vs vec kernel: %.3e\n", h);
+      cudaFree(mx);
+    }
+    cudaFree(d_s); cudaFree(d_b); cudaFree(d_s0); cudaFree(d_m); cudaFree(part); cudaFree(cntp);
+  };
+  if (group("seg3")) {
+    double* ref_col;
+    CK(cudaMalloc(&ref_col, n * 8));
+    ColEpi ce2 = ce;
+    ce2.atyn = ref_col;
+    vec_kernel<32, ColEpi, 4><<<sms * 4, 256>>>(KT.dim, KT.start, KT.idx, KT.val, V.dyg, ce2, outp);
+    double* ref_row;
+    CK(cudaMalloc(&ref_row, m * 8));
+    RowEpi re2 = re;
+    re2.yn = ref_row;
+    vec_kernel<8, RowEpi, 4><<<sms * 4, 256>>>(K.dim, K.start, K.idx, K.val, V.xb, re2, outp);
+    CK(cudaDeviceSynchronize());
+    ColEpiNull cn{V.atyn};
+    run_seg3(B4{}, KT, 2048, cn, V.dyg, col_bytes, "colnull", nullptr, nullptr);
+    run_seg3(B5{}, KT, 2048, cn, V.dyg, col_bytes, "colnull", nullptr, nullptr);
+    for (int span : {1024, 2048, 4096}) {
+      run_seg3(B2{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg3(B3{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg3(B4{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg3(B5{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg3(B4{}, K, span, re, V.xb, row_bytes, "row", V.yn, ref_row);
+    }
+    cudaFree(ref_col); cudaFree(ref_row);
+  }
+  if (group("seg2")) {
+    double* ref_col;
+    CK(cudaMalloc(&ref_col, n * 8));
+    ColEpi ce2 = ce;
+    ce2.atyn = ref_col;
+    vec_kernel<32, ColEpi, 4><<<sms * 4, 256>>>(KT.dim, KT.start, KT.idx, KT.val, V.dyg, ce2, outp);
+    CK(cudaDeviceSynchronize());
+    for (int span : {1024, 2048}) {
+      run_seg2(U8{}, B3{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg2(U8{}, B4{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg2(U4{}, B4{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg2(U4{}, B5{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg2(U4{}, B6{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+    }
+    cudaFree(ref_col);
+  }
+  if (group("seg")) {
+    // reference outputs from the vec kernel (tree sums)
+    double* ref_col;
+    CK(cudaMalloc(&ref_col, n * 8));
+    ColEpi ce2 = ce;
+    ce2.atyn = ref_col;
+    vec_kernel<32, ColEpi, 4><<<sms * 4, 256>>>(KT.dim, KT.start, KT.idx, KT.val, V.dyg, ce2, outp);
+    double* ref_row;
+    CK(cudaMalloc(&ref_row, m * 8));
+    RowEpi re2 = re;
+    re2.yn = ref_row;
+    vec_kernel<8, RowEpi, 4><<<sms * 4, 256>>>(K.dim, K.start, K.idx, K.val, V.xb, re2, outp);
+    CK(cudaDeviceSynchronize());
+    for (int span : {1024, 2048, 4096}) {
+      run_seg(B2{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg(B3{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg(B4{}, KT, span, ce, V.dyg, col_bytes, "col", V.atyn, ref_col);
+      run_seg(B3{}, K, span, re, V.xb, row_bytes, "row", V.yn, ref_row);
+    }
+    cudaFree(ref_col); cudaFree(ref_row);
+  }
   // row pass over P column panels
   for (int P : {2, 3, 4, 6}) {
     {
