@@ -115,10 +115,25 @@ def same_bits(a, b) -> bool:
 
 
 def max_rel(a, b) -> float:
+    """Largest relative discrepancy between iterates: for each iterate (a row
+    of a 2-D array) ||a_k - b_k||_inf / max(||a_k||_inf, ||b_k||_inf) -- a
+    scale-free measure (no absolute floor); 0 when both are zero."""
+    a = np.atleast_2d(np.asarray(a, np.float64))
+    b = np.atleast_2d(np.asarray(b, np.float64))
+    if a.size == 0:
+        return 0.0
+    num = np.max(np.abs(a - b), axis=1)
+    den = np.maximum(np.max(np.abs(a), axis=1), np.max(np.abs(b), axis=1))
+    rel = np.where(den > 0.0, num / np.where(den > 0.0, den, 1.0), 0.0)
+    return float(np.max(rel))
+
+
+def max_rel_elem(a, b, floor: float = 0.0) -> float:
+    """Elementwise relative discrepancy |a-b| / max(|a|, |b|, floor)."""
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     if a.size == 0:
         return 0.0
-    den = np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-300)
-    d = np.abs(a - b) / np.maximum(den, 1.0)
+    den = np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)
+    d = np.where(den > 0.0, np.abs(a - b) / np.where(den > 0.0, den, 1.0), 0.0)
     return float(np.max(d))
