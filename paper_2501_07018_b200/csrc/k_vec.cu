@@ -147,6 +147,11 @@ __global__ void sub_kernel(const double* a, const double* b, double* out, int64_
   GRID_STRIDE(i, n) out[i] = a[i] - b[i];
 }
 
+__global__ void scale_div_kernel(const double* scale, const double* v, double* out, int64_t n) {
+  pdl_wait_cadence();
+  GRID_STRIDE(i, n) out[i] = v[i] / scale[i];
+}
+
 __global__ void scale_mul_kernel(const double* scale, const double* v, double* out, int64_t n) {
   pdl_wait_cadence();
   GRID_STRIDE(i, n) out[i] = scale[i] * v[i];
@@ -410,6 +415,11 @@ int pdlpk_sub(const double* a, const double* b, double* out, int64_t n, cudaStre
 int pdlpk_average_into(const pdlpk_step_state* st, const double* sum_x, const double* sum_y,
                        double* x, double* y, int64_t n, int64_t m, cudaStream_t s) {
   if (n + m > 0) launch_pdl(PDLPK_PDL_CADENCE, average_into_kernel, static_cast<unsigned>(ew_blocks(n + m)), kT, 0, s, st, sum_x, sum_y, x, y, n, m);
+  return ok();
+}
+
+int pdlpk_scale_div(const double* scale, const double* v, double* out, int64_t n, cudaStream_t s) {
+  if (n > 0) scale_div_kernel<<<ew_blocks(n), kT, 0, s>>>(scale, v, out, n);
   return ok();
 }
 

@@ -379,6 +379,8 @@ int pdlpk_sub(const double* a, const double* b, double* out, int64_t n, cudaStre
 int pdlpk_average_into(const pdlpk_step_state* st, const double* sum_x, const double* sum_y,
                        double* x, double* y, int64_t n, int64_t m, cudaStream_t s);
 /* out = scale .* v (unscale_primal / unscale_dual, rescaling.hpp:145-153). */
+/* out = v / scale (perf mode: an original-space product from a scaled one) */
+int pdlpk_scale_div(const double* scale, const double* v, double* out, int64_t n, cudaStream_t s);
 int pdlpk_scale_mul(const double* scale, const double* v, double* out, int64_t n,
                     cudaStream_t s);
 

@@ -778,6 +778,9 @@ struct Inner {  // InnerState (solver.hpp:135-193), vectors on device
   }
   int cur() const { return hs.cur; }
   int64_t k() const { return hs.k; }
+  // k at which the cadence last computed ax_cur = K x[cur] and aty[cur] =
+  // K' y[cur] afresh (-1: not current)
+  int64_t fresh_products_k = -1;
 };
 
 struct InnerCfg {  // InnerConfig (solver.hpp:114-133)
@@ -1614,7 +1617,19 @@ class Engine {
     const int c = D.cur();
     PDLP_LAUNCH(pdlpk_scale_mul(P.col_scale, D.x[c].get(), D.sol_x.get(), P.n, s()));
     PDLP_LAUNCH(pdlpk_scale_mul(P.row_scale, D.y[c].get(), D.sol_y.get(), P.m, s()));
-    D.sol_summary = original_kkt(P, D.sol_x.get(), D.sol_y.get(), cfg.rc_mode, D.sol_r.get(), D);
+    if (!parity_ && !dist() && &D == &main_ && D.fresh_products_k == D.k()) {
+      // Perf mode: the cadence has just computed K x and K' y for this
+      // iterate; with K = diag(1/row_scale) A diag(1/col_scale) and the
+      // unscaling x = col_scale x_s, y = row_scale y_s, the original-space
+      // products are A x = (K x_s) / row_scale and A' y = (K' y_s) / col_scale
+      // (two elementwise passes instead of two more products).
+      PDLP_LAUNCH(pdlpk_scale_div(P.row_scale, D.ax_cur.get(), D.prod_m.get(), P.m, s()));
+      PDLP_LAUNCH(pdlpk_scale_div(P.col_scale, D.aty[c].get(), D.prod_n.get(), P.n, s()));
+      D.sol_summary = screen(P, 1, D.sol_x.get(), D.sol_y.get(), D.prod_m.get(), D.prod_n.get(),
+                             cfg.rc_mode, D.sol_r.get());
+    } else {
+      D.sol_summary = original_kkt(P, D.sol_x.get(), D.sol_y.get(), cfg.rc_mode, D.sol_r.get(), D);
+    }
     D.have_sol = true;
   }
 
@@ -2149,7 +2164,12 @@ class Engine {
       const int32_t staged = q == 0 ? 0 : (q == np - 1 ? 4 : 1);
       const char* eb = std::getenv("PDLP_PANEL_BUDGET");
       const int32_t budget = pdlpk_stage_budget(eb != nullptr ? std::atoi(eb) : 2016);
-      build_schedule(st[q].data(), m, L, 64, budget, staged);
+      const char* es = std::getenv("PDLP_PANEL_SEG");
+      if (es != nullptr && es[0] == '1') {
+        build_seg_schedule(st[q].data(), m, L, 2048);
+      } else {
+        build_schedule(st[q].data(), m, L, 64, budget, staged);
+      }
       panels_.views[static_cast<size_t>(q)] = L.view;
     }
     panels_.carry.alloc(m);
@@ -2209,6 +2229,8 @@ class Engine {
   double cadence_seconds_ = 0.0;  // host time inside cadence blocks (incl. polishing)
   double polish_seconds_ = 0.0;
   double gap_seconds_ = 0.0;  // host time in normalized-gap evaluations (syncs included)
+  double cad_batch_seconds_ = 0.0;    // cadence: products, screens, ray tests up to the one sync
+  double cad_capture_seconds_ = 0.0;  // cadence: final original-space summary on a budget hit
   int64_t attempts_total_ = 0;
   bool profile_ = false;
   std::vector<cudaEvent_t> prof_ev_;
@@ -2346,6 +2368,7 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
       }
       product(P.K, 0, D.x[c].get(), D.ax_cur.get());
       product(P.KT, 0, D.y[c].get(), D.aty[c].get());
+      D.fresh_products_k = D.k();
       if (have_avg && !side) {
         product(P.K, 0, D.avg_x.get(), D.ax_avg.get());
         product(P.KT, 0, D.avg_y.get(), D.aty_avg.get());
@@ -2374,6 +2397,7 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
       }
       double h[kSlots];
       std::memcpy(h, read_slots(kSlots), sizeof(h));
+      cad_batch_seconds_ += std::chrono::duration<double>(Clock::now() - cad_t0).count();
       screen_cur = finish_summary(h[kSlotScrCur], h[kSlotScrCur + 1], h[kSlotScrCur + 2],
                                   -h[kSlotScrCur + 3]);
       if (screen_passes(cfg, screen_cur) &&
@@ -2431,6 +2455,7 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
             dev_copy(D.x[c].get(), D.avg_x.get(), P.n, s());
             dev_copy(D.y[c].get(), D.avg_y.get(), P.m, s());
             dev_copy(D.aty[c].get(), D.aty_avg.get(), P.n, s());
+            dev_copy(D.ax_cur.get(), D.ax_avg.get(), P.m, s());  // (fresh products follow)
           }
           dev_copy(D.ref_x.get(), D.x[c].get(), P.n, s());
           dev_copy(D.ref_y.get(), D.y[c].get(), P.m, s());
@@ -2468,7 +2493,10 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
         return kTimeLimit;
       }
       if (budget_hit) {
+        const auto tc = Clock::now();
         capture_current(P, cfg, D);
+        PDLP_CK(cudaStreamSynchronize(s()));
+        cad_capture_seconds_ += std::chrono::duration<double>(Clock::now() - tc).count();
         D.detail = "iteration limit reached";
         return kIterLimit;
       }
@@ -2696,10 +2724,11 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
     pdlpk_gap_window_stats(&wt, &wd);
     std::fprintf(stderr,
                  "phase=main event=timing solve=%.4f upload=%.4f precondition=%.4f loop=%.4f "
-                 "steps=%.4f cadence=%.4f gap=%.4f gap_windows=%lld/%lld polish=%.4f "
-                 "alloc=%.4f prep=%.4f results=%.4f\n",
+                 "steps=%.4f cadence=%.4f cad_batch=%.4f cad_capture=%.4f gap=%.4f "
+                 "gap_windows=%lld/%lld polish=%.4f alloc=%.4f prep=%.4f results=%.4f\n",
                  res->solve_seconds, res->upload_seconds, res->precondition_seconds,
-                 res->loop_seconds, res->step_seconds, E.cadence_seconds_, E.gap_seconds_,
+                 res->loop_seconds, res->step_seconds, E.cadence_seconds_, E.cad_batch_seconds_,
+                 E.cad_capture_seconds_, E.gap_seconds_,
                  static_cast<long long>(wd), static_cast<long long>(wt), E.polish_seconds_,
                  g_alloc_seconds, prep_seconds,
                  std::chrono::duration<double>(Clock::now() - results_t0).count());

@@ -146,10 +146,19 @@ __device__ __forceinline__ int warp_excl_scan_i(int v, int lane) {
   return x - v;
 }
 
+#ifndef PDLPK_SEG_EVICT_FIRST
+#define PDLPK_SEG_EVICT_FIRST 1 /* L2 evict_first hint on the spans' index/value streams */
+#endif
 template <class Epi>
 __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __restrict__ vals,
                                           const double* __restrict__ v, Epi& epi) {
   const int32_t* __restrict__ idx = A.index;
+#if PDLPK_SEG_EVICT_FIRST
+  const uint64_t pol = l2_first_policy();
+#define SEG_LD(p) ld_stream_ef(p, pol)
+#else
+#define SEG_LD(p) ld_stream(p)
+#endif
   const int lane = threadIdx.x & 31;
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -164,13 +173,13 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
       for (int64_t base = e0 & ~int64_t(7); base < e1; base += 256) {
         const int64_t k0 = base + 8 * lane;
         if (k0 + 8 > e0 && k0 < e1) {
-          const int4 i0 = ld_stream(reinterpret_cast<const int4*>(idx + k0));
-          const int4 i1 = ld_stream(reinterpret_cast<const int4*>(idx + k0 + 4));
+          const int4 i0 = SEG_LD(reinterpret_cast<const int4*>(idx + k0));
+          const int4 i1 = SEG_LD(reinterpret_cast<const int4*>(idx + k0 + 4));
           const int ci[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
           double a[8];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const double2 t = ld_stream(reinterpret_cast<const double2*>(vals + k0) + q);
+            const double2 t = SEG_LD(reinterpret_cast<const double2*>(vals + k0) + q);
             a[2 * q] = t.x;
             a[2 * q + 1] = t.y;
           }
@@ -217,12 +226,12 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
       const int64_t k0 = base + 8 * lane;
       double p[8];
       if (k0 + 8 > e0 && k0 < e1) {
-        const int4 i0 = ld_stream(reinterpret_cast<const int4*>(idx + k0));
-        const int4 i1 = ld_stream(reinterpret_cast<const int4*>(idx + k0 + 4));
+        const int4 i0 = SEG_LD(reinterpret_cast<const int4*>(idx + k0));
+        const int4 i1 = SEG_LD(reinterpret_cast<const int4*>(idx + k0 + 4));
         const int ci[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const double2 t = ld_stream(reinterpret_cast<const double2*>(vals + k0) + q);
+          const double2 t = SEG_LD(reinterpret_cast<const double2*>(vals + k0) + q);
           p[2 * q] = t.x;
           p[2 * q + 1] = t.y;
         }
@@ -273,6 +282,7 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
       rc += nend;
     }
   }
+#undef SEG_LD
 }
 
 // Segment mask of a layout: 1 chunks, 2 direct tiles, 4 staged tiles.
