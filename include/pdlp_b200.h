@@ -140,7 +140,7 @@ typedef struct pdlp_options {
   /* ---- B200 extensions (additive; the reference fields above are unchanged) */
   int32_t mode;   /* PDLP_MODE_PERF (default) or PDLP_MODE_PARITY */
   int32_t device; /* CUDA device ordinal */
-  int32_t use_graphs; /* capture the 64-step attempt block in a CUDA graph */
+  int32_t reserved0; /* reserved, must be 0 (keeps the struct layout) */
   int32_t profile_kernels; /* CUDA events around every step kernel (bench roofline) */
   /* Timed region of the main loop starts once this many iterations are done
    * (right after that cadence); see pdlp_result.timed_*.  0 = whole loop. */

@@ -98,7 +98,7 @@ class Options(C.Structure):
         ("observer_user", C.c_void_p),
         ("mode", C.c_int32),
         ("device", C.c_int32),
-        ("use_graphs", C.c_int32),
+        ("reserved0", C.c_int32),
         ("profile_kernels", C.c_int32),
         ("timing_warmup_iterations", C.c_int64),
     ]

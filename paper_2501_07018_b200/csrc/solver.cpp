@@ -2784,7 +2784,7 @@ void pdlp_default_options(pdlp_options* o) {
   o->restart_artificial = 0.5;
   o->mode = PDLP_MODE_PERF;
   o->device = 0;
-  o->use_graphs = 0;
+  o->reserved0 = 0;
 }
 
 int pdlp_solve(const pdlp_problem_view* problem, const pdlp_options* options,
