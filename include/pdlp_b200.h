@@ -325,6 +325,19 @@ int pdlp_solve_sharded(const pdlp_problem_view* problem, const pdlp_options* opt
 int pdlp_solve_sharded_emulated(const pdlp_problem_view* problem, const pdlp_options* options,
                                 int32_t world, pdlp_result* result);
 
+/* Shard-local ingest: each rank passes only its own shard (its rows in both
+ * layouts, its column block's objective and bounds; e.g. built by
+ * pdlp_gen_random_lp_shard), so no host ever holds the whole problem.
+ * The shard plan (rows, cols, row and column ranges) must be pdlp_shard_plan_for's for
+ * (rank, world).  Results as pdlp_solve_sharded (whole x, y, r per rank). */
+int pdlp_solve_sharded_local(const pdlp_shard_view* shard, const pdlp_options* options,
+                             int32_t rank, int32_t world, const unsigned char nccl_id[128],
+                             pdlp_result* result);
+/* The same with `world` ranks as threads on this process's GPU (tests). */
+int pdlp_solve_sharded_local_emulated(const pdlp_shard_view* const* shards,
+                                      const pdlp_options* options, int32_t world,
+                                      pdlp_result* result);
+
 /* ------------------------------------------------------ component entry --- *
  * Single-component entry points used by the parity tests (each runs the same
  * device kernels the solver uses; host arrays in, host arrays out). */

@@ -65,6 +65,22 @@ pdlp_instance* pdlp_gen_random_lp(const pdlp_gen_params* params);
  * counter-based streams, multi-threaded).  NULL on bad arguments. */
 pdlp_instance* pdlp_gen_random_lp_window(const pdlp_gen_params* params, int64_t r0, int64_t r1);
 
+/* One rank's shard of the counter-based instance pdlp_gen_random_lp_window
+ * (params, 0, rows) (every rank builds only its part):
+ * rows [r0, r1) in both layouts -- K_g with global column indices and K_g^T
+ * over all cols with local row indices, exactly the window's -- the row
+ * bounds, and for the column block [c0, c1) the variable bounds and the
+ * GLOBAL objective c = A'y* + r* (all rows of the block's columns).  With
+ * [r0,r1) x [c0,c1) from pdlp_shard_plan_for it equals pdlp_shard_extract of
+ * the whole instance.  NULL on bad ranges. */
+typedef struct pdlp_gen_shard pdlp_gen_shard;
+pdlp_gen_shard* pdlp_gen_random_lp_shard(const pdlp_gen_params* params, int64_t r0, int64_t r1,
+                                         int64_t c0, int64_t c1);
+/* The shard as the solver's pdlp_shard_view (plan.rank / world / blocks left
+ * 0 for the caller to fill; arrays owned by the shard). */
+void pdlp_gen_shard_view(const pdlp_gen_shard* shard, pdlp_shard_view* out);
+void pdlp_gen_shard_free(pdlp_gen_shard* shard);
+
 /* Transportation LP (C1): `sources` supply rows sum_d x_sd <= s_s (s integer
  * U[50,150]), `sinks` demand rows sum_s x_sd >= d_d (d scaled to 95 % of total
  * supply), n = sources*sinks flows x >= 0, all coefficients +1, costs U[1,100]. */

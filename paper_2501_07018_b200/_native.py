@@ -238,6 +238,11 @@ SOLVER_SIGNATURES = {
                                      C.c_int32, C.c_char_p, C.POINTER(Result)]),
     "pdlp_solve_sharded_emulated": (C.c_int, [C.POINTER(ProblemView), C.POINTER(Options),
                                               C.c_int32, C.POINTER(Result)]),
+    "pdlp_solve_sharded_local": (C.c_int, [C.POINTER(ShardView), C.POINTER(Options), C.c_int32,
+                                           C.c_int32, C.c_char_p, C.POINTER(Result)]),
+    "pdlp_solve_sharded_local_emulated": (C.c_int, [C.POINTER(C.POINTER(ShardView)),
+                                                    C.POINTER(Options), C.c_int32,
+                                                    C.POINTER(Result)]),
     "pdlp_pdhg_step": (C.c_int, [C.POINTER(ProblemView), c_double_p, c_double_p, C.c_double,
                                  C.c_double, C.c_int32, C.c_int32, c_double_p, c_double_p,
                                  c_int32_p]),
@@ -269,6 +274,10 @@ GEN_SIGNATURES = {
     "pdlp_instance_view": (None, [C.c_void_p, C.POINTER(ProblemView)]),
     "pdlp_instance_feasible_point": (c_double_p, [C.c_void_p]),
     "pdlp_instance_free": (None, [C.c_void_p]),
+    "pdlp_gen_random_lp_shard": (C.c_void_p, [C.POINTER(GenParams), C.c_int64, C.c_int64,
+                                               C.c_int64, C.c_int64]),
+    "pdlp_gen_shard_view": (None, [C.c_void_p, C.POINTER(ShardView)]),
+    "pdlp_gen_shard_free": (None, [C.c_void_p]),
 }
 
 

@@ -304,7 +304,17 @@ pdlp_instance* pdlp_gen_random_lp(const pdlp_gen_params* params) {
 // the sequential recipe per index; b = A_w x* and c = A_w' y*_w + r* are
 // formed over the window, so the window LP is feasible and bounded on its
 // own.  (Draws differ from pdlp_gen_random_lp's single sequential stream.)
+static pdlp_instance* random_lp_window(const pdlp_gen_params* params, int64_t r0, int64_t r1,
+                                       int64_t* entries_before);
+
 pdlp_instance* pdlp_gen_random_lp_window(const pdlp_gen_params* params, int64_t r0, int64_t r1) {
+  return random_lp_window(params, r0, r1, nullptr);
+}
+
+// entries_before (optional): entries of the whole instance in rows < r0, i.e.
+// the by_row position of the window's first entry.
+static pdlp_instance* random_lp_window(const pdlp_gen_params* params, int64_t r0, int64_t r1,
+                                       int64_t* entries_before) {
   const pdlp_gen_params& p = *params;
   if (p.rows < 1 || p.cols < 1 || r0 < 0 || r1 > p.rows || r0 >= r1) return nullptr;
   const int64_t m = p.rows, n = p.cols, mw = r1 - r0;
@@ -325,18 +335,32 @@ pdlp_instance* pdlp_gen_random_lp_window(const pdlp_gen_params* params, int64_t 
   };
   // Matrix: column streams, entries of the window kept (column-major order).
   std::vector<Triplets> part(static_cast<size_t>(T));
+  std::vector<int64_t> before(static_cast<size_t>(T), 0);
   parallel(n, [&](int t, int64_t lo, int64_t hi) {
     Triplets& tr = part[static_cast<size_t>(t)];
+    int64_t b = 0;
+    std::vector<int64_t> above;  // this column's rows < r0 (duplicates merge)
     for (int64_t c = lo; c < hi; ++c) {
       SplitMix rng = stream(1, c);
       const int64_t k = sample_count(rng, p);
+      above.clear();
       for (int64_t e = 0; e < k; ++e) {
         const int64_t row = rng.below(m);
         const double v = sample_value(rng, p);
         if (row >= r0 && row < r1) tr.push(row - r0, c, v);
+        if (entries_before != nullptr && row < r0) above.push_back(row);
+      }
+      if (!above.empty()) {
+        std::sort(above.begin(), above.end());
+        b += std::unique(above.begin(), above.end()) - above.begin();
       }
     }
+    before[static_cast<size_t>(t)] = b;
   });
+  if (entries_before != nullptr) {
+    *entries_before = 0;
+    for (int64_t b : before) *entries_before += b;
+  }
   Triplets all;
   size_t total = 0;
   for (const auto& tr : part) total += tr.v.size();
@@ -413,6 +437,136 @@ pdlp_instance* pdlp_gen_random_lp_window(const pdlp_gen_params* params, int64_t 
   inst->feasible_point = std::move(xs);
   return inst;
 }
+
+// One rank's shard of the counter-based instance (the window generator over
+// all m rows): rows [r0, r1) in both layouts exactly as the window generator
+// draws them, and for the column block [c0, c1) the bounds and the GLOBAL
+// objective c = A'y* + r* (every entry of the block's columns, all rows).
+// Work O(entries of the whole instance) for the matrix pass (each column's
+// stream is drawn to find its window rows) plus O(entries of the block) for
+// the objective; memory O(shard).
+struct pdlp_gen_shard {
+  pdlp_instance* win = nullptr;
+  int64_t rows = 0, cols = 0, r0 = 0, r1 = 0, c0 = 0, c1 = 0, entry_offset = 0;
+  std::vector<double> objective, var_lower, var_upper;
+  ~pdlp_gen_shard() { delete win; }
+};
+
+pdlp_gen_shard* pdlp_gen_random_lp_shard(const pdlp_gen_params* params, int64_t r0, int64_t r1,
+                                         int64_t c0, int64_t c1) {
+  const pdlp_gen_params& p = *params;
+  if (c0 < 0 || c1 > p.cols || c0 > c1) return nullptr;
+  auto* sh = new pdlp_gen_shard;
+  int64_t before = 0;
+  sh->win = random_lp_window(params, r0, r1, &before);
+  if (sh->win == nullptr) {
+    delete sh;
+    return nullptr;
+  }
+  sh->rows = p.rows;
+  sh->cols = p.cols;
+  sh->r0 = r0;
+  sh->r1 = r1;
+  sh->c0 = c0;
+  sh->c1 = c1;
+  sh->entry_offset = before;
+  const int64_t m = p.rows, nb = c1 - c0;
+  sh->var_lower.assign(sh->win->var_lower.begin() + c0, sh->win->var_lower.begin() + c1);
+  sh->var_upper.assign(sh->win->var_upper.begin() + c0, sh->win->var_upper.begin() + c1);
+  sh->objective.assign(static_cast<size_t>(nb), 0.0);
+  auto stream = [&](uint64_t kind, int64_t i) {
+    SplitMix h(p.seed ^ (kind * 0xd1b54a32d192ed03ull));
+    h.s += static_cast<uint64_t>(i) * 0x9e3779b97f4a7c15ull;
+    return SplitMix(h.next());
+  };
+  const int64_t n_eq_first = static_cast<int64_t>(std::llround(p.eq_frac * static_cast<double>(m)));
+  // y*_g from row g's stream, as the window generator draws it
+  auto ystar = [&](int64_t g) {
+    SplitMix rng = stream(3, g);
+    const bool eq = p.eq_rows_first ? (g < n_eq_first) : (rng.u01() < p.eq_frac);
+    if (eq) return rng.normal();
+    (void)rng.uniform(0.0, p.slack_hi);
+    return -std::fabs(rng.normal());
+  };
+  // r*_i from column i's bound stream
+  auto rstar = [&](int64_t i) {
+    SplitMix rng = stream(2, i);
+    int kind = 0;
+    if (p.bound_kind == 1) {
+      const double u = rng.u01();
+      kind = u < 0.6 ? 0 : (u < 0.9 ? 1 : 2);
+    }
+    if (kind == 0) {
+      (void)rng.uniform(0.0, p.box_hi);
+      return std::fabs(rng.normal());
+    }
+    if (kind == 1) {
+      const double l = rng.uniform(-p.box_hi, 0.0);
+      const double u = l + rng.uniform(1.0, 2.0 * p.box_hi);
+      (void)rng.uniform(l, u);
+      return rng.normal();
+    }
+    (void)rng.normal();
+    return 0.0;
+  };
+  const int T = static_cast<int>(std::max<unsigned>(1u, std::min(32u, std::thread::hardware_concurrency())));
+  std::vector<std::thread> th;
+  const int64_t per = (nb + T - 1) / T;
+  for (int t = 0; t < T; ++t) {
+    const int64_t lo = std::min(nb, per * t), hi = std::min(nb, lo + per);
+    th.emplace_back([&, lo, hi] {
+      std::vector<std::pair<int64_t, double>> col;
+      for (int64_t q = lo; q < hi; ++q) {
+        const int64_t c = c0 + q;
+        SplitMix rng = stream(1, c);
+        const int64_t k = sample_count(rng, p);
+        col.clear();
+        for (int64_t e = 0; e < k; ++e) {
+          const int64_t row = rng.below(m);
+          col.emplace_back(row, sample_value(rng, p));
+        }
+        // the column as build_layout stores it: rows ascending, duplicates
+        // summed in draw order; then the product in storage order
+        std::stable_sort(col.begin(), col.end(),
+                         [](const auto& a, const auto& b) { return a.first < b.first; });
+        double acc = 0.0;
+        for (size_t e = 0; e < col.size();) {
+          double v = col[e].second;
+          size_t f = e + 1;
+          while (f < col.size() && col[f].first == col[e].first) v += col[f++].second;
+          acc += v * ystar(col[e].first);
+          e = f;
+        }
+        sh->objective[static_cast<size_t>(q)] = acc + rstar(c);
+      }
+    });
+  }
+  for (auto& x : th) x.join();
+  return sh;
+}
+
+void pdlp_gen_shard_view(const pdlp_gen_shard* sh, pdlp_shard_view* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->plan.rows = sh->rows;
+  out->plan.cols = sh->cols;
+  out->plan.row_begin = sh->r0;
+  out->plan.row_end = sh->r1;
+  out->plan.col_begin = sh->c0;
+  out->plan.col_end = sh->c1;
+  const pdlp_instance* w = sh->win;
+  out->rows = {w->rows, static_cast<int64_t>(w->by_row.value.size()), w->by_row.start.data(),
+               w->by_row.index.data(), w->by_row.value.data()};
+  out->cols = {w->cols, static_cast<int64_t>(w->by_col.value.size()), w->by_col.start.data(),
+               w->by_col.index.data(), w->by_col.value.data()};
+  out->objective = sh->objective.data();
+  out->var_lower = sh->var_lower.data();
+  out->var_upper = sh->var_upper.data();
+  out->con_lower = w->con_lower.data();
+  out->con_upper = w->con_upper.data();
+  out->entry_offset = sh->entry_offset;
+}
+
+void pdlp_gen_shard_free(pdlp_gen_shard* sh) { delete sh; }
 
 pdlp_instance* pdlp_gen_transport(int64_t sources, int64_t sinks, uint64_t seed) {
   if (sources < 1 || sinks < 1) return nullptr;

@@ -834,8 +834,11 @@ class Engine {
   // comm != nullptr: one rank of a row-sharded solve; this
   // engine then holds rows [r0,r1) of A in both layouts and the column
   // block [c0,c1), and every product / reduction crosses ranks.
-  Engine(const pdlp_problem_view* p, const pdlp_options& o, Comm* comm = nullptr)
-      : opt_(o), comm_(comm) {
+  // shard != nullptr (with comm): this rank's shard as the caller built it
+  // (shard-local ingest, pdlp_solve_sharded_local); p is then unused.
+  Engine(const pdlp_problem_view* p, const pdlp_options& o, Comm* comm = nullptr,
+         const pdlp_shard_view* shard = nullptr)
+      : opt_(o), comm_(comm), shard_in_(shard) {
     parity_ = o.mode == PDLP_MODE_PARITY;
     shards_ = std::max(1, o.threads) * std::max(1, o.shards_per_thread);
     PDLP_CK(cudaSetDevice(o.device));
@@ -867,14 +870,16 @@ class Engine {
                  p->con_upper, p->var_lower, p->var_upper, 0, 0, 0);
     } else {
       // Every rank sees the whole problem, so structural errors throw on
-      // every rank alike before any collective.
+      // every rank alike before any collective.  (Shard-local ingest: each
+      // rank passes its own shard; the plan was checked against
+      // pdlp_shard_plan_for by the entry point.)
       ShardData sh;
-      extract_shard(*p, comm_->rank(), comm_->world(), sh);
+      if (shard_in_ == nullptr) extract_shard(*p, comm_->rank(), comm_->world(), sh);
+      const pdlp_shard_view& v = shard_in_ != nullptr ? *shard_in_ : sh.view;
       flag_.alloc(8);
-      plan_ = sh.view.plan;
-      m_glob_ = p->rows;
-      n_glob_ = p->cols;
-      const pdlp_shard_view& v = sh.view;
+      plan_ = v.plan;
+      m_glob_ = plan_.rows;
+      n_glob_ = plan_.cols;
       load_parts(v.rows, v.cols, plan_.row_end - plan_.row_begin, plan_.col_end - plan_.col_begin,
                  v.objective, v.con_lower, v.con_upper, v.var_lower, v.var_upper, plan_.row_begin,
                  plan_.col_begin, v.entry_offset);
@@ -2015,6 +2020,7 @@ class Engine {
   std::unique_ptr<AllocStreamScope> alloc_scope_;
   // sharded solve
   Comm* comm_ = nullptr;
+  const pdlp_shard_view* shard_in_ = nullptr;
   pdlp_shard_plan plan_{};
   int64_t m_glob_ = 0, n_glob_ = 0;
   pdlpk_red_log red_log_{};
@@ -2579,14 +2585,14 @@ int64_t inner_bytes(int64_t n, int64_t m) { return 8 * (24 * n + 17 * m) + 64 * 
 
 // comm != nullptr: this process/thread is one rank of a row-sharded solve.
 void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_result* res,
-           Comm* comm = nullptr) {
+           Comm* comm = nullptr, const pdlp_shard_view* shard = nullptr) {
   const auto t0 = Clock::now();
   // sharded: one log (rank 0); every rank computes the same trajectory
   pdlp_options local = *opts;
   if (comm != nullptr && comm->rank() != 0) local.logging = 0;
   const pdlp_options* o = &local;
   g_alloc_seconds = 0.0;
-  Engine E(problem, *o, comm);  // uploads and validates on device
+  Engine E(problem, *o, comm, shard);  // uploads and validates on device
   if (o->enable_scaling) E.precondition(o->ruiz_passes, o->pock_chambolle != 0);
   if (std::getenv("PDLP_NO_UNIFORM") == nullptr) E.detect_uniform();
   if (!E.dist()) {
@@ -2835,6 +2841,32 @@ int pdlp_nccl_unique_id(unsigned char out[128]) {
     g_last_error = why;
     return PDLP_ERR_CUDA;
   }
+  return PDLP_OK;
+}
+
+// A caller-built shard must be the one pdlp_shard_plan_for assigns to this
+// rank (equal blocks: the collectives exchange equal counts).
+static int check_shard_view(const pdlp_shard_view* v, int32_t rank, int32_t world,
+                            pdlp_shard_view* fixed) {
+  if (v == nullptr) {
+    g_last_error = "null shard";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  pdlp_shard_plan want{};
+  const int rc = pdlp_shard_plan_for(v->plan.rows, v->plan.cols, rank, world, &want);
+  if (rc != PDLP_OK) return rc;
+  if (want.row_begin != v->plan.row_begin || want.row_end != v->plan.row_end ||
+      want.col_begin != v->plan.col_begin || want.col_end != v->plan.col_end) {
+    g_last_error = "shard ranges differ from pdlp_shard_plan_for(rows, cols, rank, world)";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  if (v->rows.primary_dim != want.row_end - want.row_begin || v->cols.primary_dim != v->plan.cols ||
+      v->rows.nnz != v->cols.nnz) {
+    g_last_error = "invalid problem: row/column layouts disagree (index -1)";
+    return PDLP_ERR_INVALID_PROBLEM;
+  }
+  *fixed = *v;
+  fixed->plan = want;
   return PDLP_OK;
 }
 
@@ -3297,3 +3329,104 @@ int pdlp_step_size_rules(double movement, double curvature, double eta_bar, doub
 }
 
 }  // extern "C"
+
+// ------------------------------------------------ shard-local ingest ---
+// Every rank passes only its shard: nothing of the whole
+// problem is materialized on any host; x, y and the reduced costs are still
+// gathered to every rank's result (n- and m-length buffers).
+int pdlp_solve_sharded_local(const pdlp_shard_view* shard, const pdlp_options* options,
+                             int32_t rank, int32_t world, const unsigned char nccl_id[128],
+                             pdlp_result* result) {
+  pdlp_problem_view dummy{};
+  int rc = check_sharded_args(&dummy, options, rank, world, result);
+  if (rc != PDLP_OK) return rc;
+  pdlp_shard_view v{};
+  rc = check_shard_view(shard, rank, world, &v);
+  if (rc != PDLP_OK) return rc;
+  if (nccl_id == nullptr) {
+    g_last_error = "null nccl id";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&] {
+    std::unique_ptr<Comm> comm = make_nccl_comm(nccl_id, rank, world, options->device);
+    solve(nullptr, options, result, comm.get(), &v);
+  });
+}
+
+int pdlp_solve_sharded_local_emulated(const pdlp_shard_view* const* shards,
+                                      const pdlp_options* options, int32_t world,
+                                      pdlp_result* result) {
+  pdlp_problem_view dummy{};
+  int rc = check_sharded_args(&dummy, options, 0, world, result);
+  if (rc != PDLP_OK) return rc;
+  if (shards == nullptr) {
+    g_last_error = "null shards";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  std::vector<pdlp_shard_view> v(static_cast<size_t>(world));
+  for (int r = 0; r < world; ++r) {
+    rc = check_shard_view(shards[r], r, world, &v[static_cast<size_t>(r)]);
+    if (rc != PDLP_OK) return rc;
+  }
+  const size_t n = static_cast<size_t>(std::max<int64_t>(v[0].plan.cols, 0));
+  const size_t m = static_cast<size_t>(std::max<int64_t>(v[0].plan.rows, 0));
+  std::vector<pdlp_result> res(static_cast<size_t>(world));
+  struct Bufs {
+    std::vector<double> x, y, r, rx, ry, rr;
+  };
+  std::vector<Bufs> store(static_cast<size_t>(world));
+  for (int r = 0; r < world; ++r) {
+    if (r == 0) {
+      res[0] = *result;
+      continue;
+    }
+    Bufs& b = store[r];
+    for (auto* q : {&b.x, &b.r, &b.rx, &b.rr}) q->assign(n + 1, 0.0);
+    for (auto* q : {&b.y, &b.ry}) q->assign(m + 1, 0.0);
+    res[r] = pdlp_result{};
+    res[r].x = b.x.data();
+    res[r].y = b.y.data();
+    res[r].reduced_costs = b.r.data();
+    res[r].cert_ray_x = b.rx.data();
+    res[r].cert_ray_y = b.ry.data();
+    res[r].cert_ray_r = b.rr.data();
+  }
+  std::shared_ptr<ThreadHub> hub = make_thread_hub(world);
+  std::vector<int> codes(static_cast<size_t>(world), PDLP_OK);
+  std::vector<std::string> errs(static_cast<size_t>(world));
+  std::vector<std::thread> th;
+  for (int r = 0; r < world; ++r) {
+    th.emplace_back([&, r] {
+      codes[r] = guarded([&] {
+        std::unique_ptr<Comm> comm = make_thread_comm(hub, r);
+        solve(nullptr, options, &res[r], comm.get(), &v[static_cast<size_t>(r)]);
+      });
+      if (codes[r] != PDLP_OK) {
+        errs[r] = g_last_error;
+        abort_thread_hub(*hub);
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int r = 0; r < world; ++r) {
+    if (codes[r] != PDLP_OK && errs[r].find("another rank of the group failed") == std::string::npos) {
+      g_last_error = errs[r];
+      return codes[r];
+    }
+  }
+  for (int r = 0; r < world; ++r) {
+    if (codes[r] != PDLP_OK) {
+      g_last_error = errs[r];
+      return codes[r];
+    }
+  }
+  const pdlp_result user = *result;
+  *result = res[0];
+  result->x = user.x;
+  result->y = user.y;
+  result->reduced_costs = user.reduced_costs;
+  result->cert_ray_x = user.cert_ray_x;
+  result->cert_ray_y = user.cert_ray_y;
+  result->cert_ray_r = user.cert_ray_r;
+  return PDLP_OK;
+}

@@ -14,6 +14,13 @@ single-process (solver.hpp:535-608); this is the B200 extension of it.
         the same sharded program with `world` ranks as threads sharing this
         process's GPU (collectives = host barriers + device copies): checks
         the sharded path where fewer GPUs than ranks exist.
+
+Shard-local ingest (no host holds the whole problem):
+    generate_shard(config, seed, rank, world)   one rank's shard of the
+        counter-based random-LP instance (libpdlp_gen pdlp_gen_random_lp_shard)
+    solve_distributed_local(shard, options)     under torch.distributed
+    solve_sharded_local(shard, options, rank, world, nccl_id)
+    solve_sharded_local_emulated(shards, options)
 """
 from __future__ import annotations
 
@@ -132,3 +139,103 @@ def solve_distributed(problem: LpProblem, options: SolverOptions | None = None,
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return solve_sharded(problem, options, rank, world, obj[0])
+
+
+# ------------------------------------------------------ shard-local ingest ---
+class LocalShard:
+    """One rank's shard, owned by the generator library: K_g (global column
+    indices), K_g^T (all columns, local rows), the row bounds and the column
+    block's objective and bounds (kernels.h / pdlp_b200.h pdlp_shard_view)."""
+
+    def __init__(self, handle, plan: N.ShardPlan):
+        self._h = handle
+        self.view = N.ShardView()
+        N.gen().pdlp_gen_shard_view(handle, C.byref(self.view))
+        self.view.plan = plan
+        self.plan = _plan(plan)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.gen().pdlp_gen_shard_free(self._h)
+            self._h = None
+
+    def vectors(self) -> dict:
+        """Copies of the shard's vectors (no layouts)."""
+        v, pl = self.view, self.plan
+        ml, nl = pl.row_end - pl.row_begin, pl.col_end - pl.col_begin
+        return {"objective": _arr(v.objective, nl, np.float64),
+                "var_lower": _arr(v.var_lower, nl, np.float64),
+                "var_upper": _arr(v.var_upper, nl, np.float64),
+                "con_lower": _arr(v.con_lower, ml, np.float64),
+                "con_upper": _arr(v.con_upper, ml, np.float64)}
+
+    def as_dict(self) -> dict:
+        """Copies of the shard's arrays (the layout of extract_shard)."""
+        v, pl = self.view, self.plan
+        ml, nl = pl.row_end - pl.row_begin, pl.col_end - pl.col_begin
+
+        def csr(c):
+            return {"dim": c.primary_dim, "nnz": c.nnz,
+                    "start": _arr(c.start, c.primary_dim + 1, np.int64),
+                    "index": _arr(c.index, c.nnz, np.int64),
+                    "value": _arr(c.value, c.nnz, np.float64)}
+
+        return {"plan": pl, "rows": csr(v.rows), "cols": csr(v.cols),
+                "objective": _arr(v.objective, nl, np.float64),
+                "var_lower": _arr(v.var_lower, nl, np.float64),
+                "var_upper": _arr(v.var_upper, nl, np.float64),
+                "con_lower": _arr(v.con_lower, ml, np.float64),
+                "con_upper": _arr(v.con_upper, ml, np.float64),
+                "entry_offset": v.entry_offset}
+
+
+def generate_shard(config: str, seed: int, rank: int, world: int, **overrides) -> LocalShard:
+    """Rank `rank` of `world`'s shard of the counter-based instance
+    generate(config, seed, row_window=(0, rows), **overrides) -- built without
+    the rest of the instance (C0 / C2 / C4 recipes)."""
+    cfg = config.lower()
+    if cfg not in ("c0", "c2", "c4"):
+        raise ValueError("shard-local generation exists for the random-LP recipes c0, c2, c4")
+    prm = N.GenParams()
+    getattr(N.gen(), f"pdlp_gen_{cfg}_params")(C.byref(prm), seed)
+    for k, val in overrides.items():
+        setattr(prm, k, val)
+    plan = N.ShardPlan()
+    _check(N.lib().pdlp_shard_plan_for(prm.rows, prm.cols, rank, world, C.byref(plan)))
+    h = N.gen().pdlp_gen_random_lp_shard(C.byref(prm), plan.row_begin, plan.row_end,
+                                         plan.col_begin, plan.col_end)
+    if not h:
+        raise ValueError("bad shard ranges")
+    return LocalShard(h, plan)
+
+
+def solve_sharded_local(shard: LocalShard, options: SolverOptions | None, rank: int, world: int,
+                        nccl_id: bytes) -> SolveResult:
+    options = options or SolverOptions(mode="perf")
+    _quiet_nccl()
+    if len(nccl_id) != 128:
+        raise ValueError("nccl_id must be the 128-byte ncclUniqueId")
+    return run_solve(N.lib(), "pdlp_solve_sharded_local", None, options, to_c_options(options),
+                     extra=(rank, world, C.c_char_p(nccl_id)), first_arg=C.byref(shard.view),
+                     dims=(shard.plan.rows, shard.plan.cols))
+
+
+def solve_sharded_local_emulated(shards: list, options: SolverOptions | None) -> SolveResult:
+    options = options or SolverOptions(mode="perf")
+    arr = (C.POINTER(N.ShardView) * len(shards))(*[C.pointer(sh.view) for sh in shards])
+    return run_solve(N.lib(), "pdlp_solve_sharded_local_emulated", None, options,
+                     to_c_options(options), extra=(len(shards),), first_arg=arr,
+                     dims=(shards[0].plan.rows, shards[0].plan.cols))
+
+
+def solve_distributed_local(shard: LocalShard, options: SolverOptions | None = None,
+                            group=None) -> SolveResult:
+    """solve_distributed with each rank passing only its own shard."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    options = options or SolverOptions(mode="perf")
+    options.device = int(os.environ.get("LOCAL_RANK", options.device))
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return solve_sharded_local(shard, options, rank, world, obj[0])

@@ -212,13 +212,19 @@ def _check(rc: int) -> None:
     raise RuntimeError(f"pdlp error {rc}: {msg}")
 
 
-def run_solve(lib, fn_name: str, p: LpProblem, options: SolverOptions, c_opts: N.Options,
-              extra: tuple = ()) -> SolveResult:
+def run_solve(lib, fn_name: str, p: LpProblem | None, options: SolverOptions, c_opts: N.Options,
+              extra: tuple = (), first_arg=None, dims: tuple | None = None) -> SolveResult:
     """Shared marshalling for pdlp_solve, the sharded solves (extra = the
-    arguments between options and result) and the oracle's ref_solve."""
+    arguments between options and result) and the oracle's ref_solve.  The
+    shard-local solves pass no problem: first_arg is their shard argument
+    and dims = (rows, cols) of the whole problem."""
     t_prep = time.perf_counter()
-    view = p.view()
-    m, n = p.rows(), p.cols()
+    if p is not None:
+        view = p.view()
+        first_arg = C.byref(view)
+        m, n = p.rows(), p.cols()
+    else:
+        m, n = dims
     x = np.zeros(n)
     y = np.zeros(m)
     r = np.zeros(n)
@@ -233,7 +239,7 @@ def run_solve(lib, fn_name: str, p: LpProblem, options: SolverOptions, c_opts: N
         thunk = _observer_thunk(options.observer)
         c_opts.observer = thunk
     t_call = time.perf_counter()
-    rc = getattr(lib, fn_name)(C.byref(view), C.byref(c_opts), *extra, C.byref(res))
+    rc = getattr(lib, fn_name)(first_arg, C.byref(c_opts), *extra, C.byref(res))
     if os.environ.get("PDLP_TIMING"):
         print(f"phase=python event=timing call={time.perf_counter() - t_call:.4f} "
               f"native_solve={res.solve_seconds:.4f} prep={t_call - t_prep:.4f}", file=sys.stderr)

@@ -121,7 +121,8 @@ def test_c1_full_solve_to_1e4_parity(gpu, ref, c1):
 # --------------------------------------------------------------- C2 full ---
 @pytest.fixture(scope="module")
 def c2():
-    return P.generate("c2", 0)
+    # the benchmarked instance (bench.py WORKLOADS["c2"]: counter-based streams)
+    return P.generate("c2", 0, row_window=(0, 5_000_000))
 
 
 def test_c2_full_first_iterates_parity(gpu, ref, c2):

@@ -295,3 +295,46 @@ def test_peer_read_epilogue_matches_reduce_scatter(gpu, monkeypatch, world):
     # exchange (other worlds take other trajectories and may not polish)
     if world == 2:
         assert polished[1] > 0
+
+
+# -------------------------------------------------- shard-local ingest ---
+@pytest.mark.parametrize("cfg,kw", [("c2", {"rows": 3000, "cols": 7000, "kmax": 800}),
+                                    ("c0", {"rows": 500, "cols": 900})])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_generated_shards_equal_extracted_shards(cfg, kw, world):
+    """Each rank's shard built on its own (pdlp_gen_random_lp_shard: its rows,
+    its column block with the GLOBAL objective) equals the shard extracted
+    from the whole counter-based instance, array for array and bit for bit."""
+    full = P.generate(cfg, 3, row_window=(0, kw["rows"]), **kw)
+    for rank in range(world):
+        a = S.generate_shard(cfg, 3, rank, world, **kw).as_dict()
+        b = S.extract_shard(full, rank, world)
+        assert a["plan"] == b["plan"] and a["entry_offset"] == b["entry_offset"]
+        for key in ("objective", "var_lower", "var_upper", "con_lower", "con_upper"):
+            assert np.array_equal(a[key].view(np.int64), b[key].view(np.int64)), key
+        for lay in ("rows", "cols"):
+            for f in ("start", "index", "value"):
+                assert np.array_equal(a[lay][f], b[lay][f]), (lay, f)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_local_shards_solve_like_the_whole_problem(gpu, world):
+    """A sharded solve fed only the ranks' own shards is the sharded solve of
+    the whole instance, bit for bit (same partition, same kernels)."""
+    kw = {"rows": 2000, "cols": 4000, "kmax": 600}
+    full = P.generate("c2", 5, row_window=(0, kw["rows"]), **kw)
+    shards = [S.generate_shard("c2", 5, r, world, **kw) for r in range(world)]
+    o = _opts(iteration_limit=200, tolerances=P.TerminationTolerances(0.0, 0.0, 0.0))
+    a = S.solve_sharded_emulated(full, o, world)
+    b = S.solve_sharded_local_emulated(shards, o)
+    assert a.iterations == b.iterations == 200 and a.restarts == b.restarts
+    assert np.array_equal(a.x.view(np.int64), b.x.view(np.int64))
+    assert np.array_equal(a.y.view(np.int64), b.y.view(np.int64))
+
+
+@pytest.mark.gpu
+def test_local_shard_rejects_wrong_plan(gpu):
+    sh = S.generate_shard("c0", 1, 0, 2, rows=200, cols=300)
+    with pytest.raises(RuntimeError):  # a rank-0 shard claimed by rank 1
+        S.solve_sharded_local_emulated([sh, sh], _opts(iteration_limit=5))
