@@ -146,6 +146,9 @@ __device__ __forceinline__ int warp_excl_scan_i(int v, int lane) {
   return x - v;
 }
 
+#ifndef PDLPK_SEG_PREFETCH
+#define PDLPK_SEG_PREFETCH 0 /* warm a step's epilogue operands in L2 (measured: 18 us slower) */
+#endif
 #ifndef PDLPK_SEG_EVICT_FIRST
 #define PDLPK_SEG_EVICT_FIRST 1 /* L2 evict_first hint on the spans' index/value streams */
 #endif
@@ -249,7 +252,9 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
       const int nend_lane = __popc(eb);
       const int ends_before = warp_excl_scan_i(nend_lane, lane);
       const int nend = __shfl_sync(0xffffffffu, ends_before + nend_lane, 31);
+#if PDLPK_SEG_PREFETCH
       for (int j = lane; j < nend; j += 32) epi.prefetch(rc + j);
+#endif
       // the segment open at the lane's end, then the segmented scan of those
       // across lanes: what flows into each lane
       double tail = 0.0;
