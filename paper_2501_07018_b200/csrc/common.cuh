@@ -229,6 +229,17 @@ __device__ __forceinline__ double2 ld_stream_ef(const double2* p, uint64_t pol) 
                : "l"(p), "l"(pol));
   return v;
 }
+// Gather with an explicit L2 policy (pol from createpolicy).
+__device__ __forceinline__ double ld_gather_pol(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t l2_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ uint64_t l2_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));

@@ -580,7 +580,8 @@ int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t /*operand_l
              (10 * over256 >= nnz || static_cast<double>(maxlen) > 16.0 * mean);
   if (const char* e = std::getenv("PDLP_SEG")) seg = e[0] == '1';
   if (seg) {
-    build_seg_schedule(start, dim, L, 2048);
+    const char* es = std::getenv("PDLP_SEG_SPAN");
+    build_seg_schedule(start, dim, L, es != nullptr && std::atoi(es) >= 64 ? std::atoi(es) : 2048);
     return -1;
   }
   const char* env = std::getenv("PDLP_SHORT_MAX");

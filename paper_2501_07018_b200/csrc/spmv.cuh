@@ -149,6 +149,9 @@ __device__ __forceinline__ int warp_excl_scan_i(int v, int lane) {
 #ifndef PDLPK_SEG_PREFETCH
 #define PDLPK_SEG_PREFETCH 0 /* warm a step's epilogue operands in L2 (measured: 18 us slower) */
 #endif
+#ifndef PDLPK_SEG_GATHER_KEEP
+#define PDLPK_SEG_GATHER_KEEP 0 /* L2 evict_last hint on the gathers */
+#endif
 #ifndef PDLPK_SEG_EVICT_FIRST
 #define PDLPK_SEG_EVICT_FIRST 1 /* L2 evict_first hint on the spans' index/value streams */
 #endif
@@ -161,6 +164,12 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
 #define SEG_LD(p) ld_stream_ef(p, pol)
 #else
 #define SEG_LD(p) ld_stream(p)
+#endif
+#if PDLPK_SEG_GATHER_KEEP
+  const uint64_t gpol = l2_last_policy();
+#define SEG_G(p) ld_gather_pol(p, gpol)
+#else
+#define SEG_G(p) __ldg(p)
 #endif
   const int lane = threadIdx.x & 31;
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -188,7 +197,7 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
           }
           double g[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) g[u] = (k0 + u >= e0 && k0 + u < e1) ? __ldg(v + ci[u]) : 0.0;
+          for (int u = 0; u < 8; ++u) g[u] = (k0 + u >= e0 && k0 + u < e1) ? SEG_G(v + ci[u]) : 0.0;
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             if (k0 + u >= e0 && k0 + u < e1) acc = mac(acc, a[u], g[u]);
@@ -240,7 +249,7 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          p[u] = (k0 + u >= e0 && k0 + u < e1) ? p[u] * __ldg(v + ci[u]) : 0.0;
+          p[u] = (k0 + u >= e0 && k0 + u < e1) ? p[u] * SEG_G(v + ci[u]) : 0.0;
         }
       } else {
 #pragma unroll
@@ -288,6 +297,7 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
     }
   }
 #undef SEG_LD
+#undef SEG_G
 }
 
 // Segment mask of a layout: 1 chunks, 2 direct tiles, 4 staged tiles.
