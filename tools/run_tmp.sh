@@ -1,2 +1,1 @@
-python tools/c2_variants.py default tools/variants/gkeep/libpdlp_b200.so > gpurun_out/v7.jsonl 2> gpurun_out/v7.err
-bash tools/c2_prof.sh
+timeout 1200 compute-sanitizer --tool memcheck --leak-check no --print-limit 20 python tools/sanitize_small.py > gpurun_out/san_memcheck.log 2>&1; echo rc=$? >> gpurun_out/san_memcheck.log
