@@ -37,7 +37,7 @@ _DEFINES = os.environ.get("PDLP_DEFINES", "").split()
 CU_FLAGS += _DEFINES
 CXX_FLAGS += _DEFINES
 
-CU_SOURCES = ["k_step.cu", "k_vec.cu", "k_gap.cu", "k_scale.cu", "k_valid.cu", "k_feas.cu"]
+CU_SOURCES = ["k_step.cu", "k_vec.cu", "k_gap.cu", "k_scale.cu", "k_valid.cu", "k_feas.cu", "k_multi.cu"]
 CPP_SOURCES = ["solver.cpp", "host_stage.cpp", "comm.cpp", "shard.cpp", "mps.cpp"]
 HEADERS = ["common.cuh", "spmv.cuh", "reduce.cuh", "kernels.h", "device.hpp", "host_stage.hpp", "comm.hpp", "shard.hpp"]
 

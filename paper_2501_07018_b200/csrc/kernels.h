@@ -228,6 +228,16 @@ typedef struct pdlpk_panel_ptrs {
   double* val[PDLPK_MAX_ROW_PANELS];
 } pdlpk_panel_ptrs;
 int pdlpk_panel_scatter(const pdlpk_csr* K, const pdlpk_panel_ptrs* pp, cudaStream_t s);
+
+/* Multi-vector products on a segmented-span layout (k_multi.cu, perf mode):
+ * out.v[q] = A in.v[q] for q < vec (2 or 4) in one pass; pack = scratch of
+ * vec * operand_len doubles, part = scratch of vec * A->n_chunks doubles. */
+typedef struct pdlpk_multi_vecs {
+  double* v[4];
+} pdlpk_multi_vecs;
+int pdlpk_spmv_multi(const pdlpk_csr* A, int32_t orig, int32_t vec, const pdlpk_multi_vecs* in,
+                     int64_t operand_len, double* pack, const pdlpk_multi_vecs* out, double* part,
+                     cudaStream_t s);
 #define PDLPK_LINE_PARTIALS_MAX 262144
 
 /* Reduction context for cadence operations. */

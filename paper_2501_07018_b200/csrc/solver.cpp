@@ -956,6 +956,7 @@ class Engine {
     }
     upload_layout(by_row, n_glob_, bad.get(), prob_.row, s());
     g_interleave_warp_lines = false;
+    build_multi_row(by_row);
     const double t_row = lap();
     upload_layout(by_col, m, bad.get(), prob_.col, s());
     const double t_col = lap();
@@ -2199,6 +2200,67 @@ class Engine {
     return panels_.np >= 2 && P.K.index == prob_.row.view.index;
   }
 
+  // ---- multi-vector cadence products (k_multi.cu) ------------------------
+  // Perf mode, one GPU, layouts of >= 16M entries: the cadence's products
+  // of the current iterate, the window average and the ray candidates go
+  // through one pass per layout (2 operands through K, up to 4 through K').
+  // They need a segmented-span schedule on both layouts; the row layout
+  // keeps its tiles for the step and gets a second, span schedule here.
+  DevLayout mrow_;
+  bool mrow_ready_ = false;
+  DevBuf<double> multi_pack_, multi_part_, multi_prod_[2];
+  void build_multi_row(const pdlp_csr_view& v) {
+    mrow_ready_ = false;
+    const char* e = std::getenv("PDLP_MULTI");  // 0: off; 1: also below 16M entries
+    const bool force = e != nullptr && e[0] == '1';
+    if (parity_ || comm_ != nullptr || (e != nullptr && e[0] == '0') ||
+        (!force && prob_.row.view.nnz < (int64_t(16) << 20)) ||
+        !starts_valid(v.start, v.primary_dim, v.nnz)) {
+      return;
+    }
+    if (prob_.row.view.seg_mode) {  // the row layout's own schedule serves
+      mrow_ready_ = false;
+      multi_on_ = true;
+      return;
+    }
+    build_seg_schedule(v.start, v.primary_dim, mrow_, 2048);
+    const pdlpk_csr& R = prob_.row.view;
+    mrow_.view.dim = R.dim;
+    mrow_.view.nnz = R.nnz;
+    mrow_.view.start = R.start;
+    mrow_.view.wide = R.wide;
+    mrow_.view.index = R.index;
+    mrow_.view.value = R.value;
+    mrow_.view.value_orig = R.value_orig;
+    mrow_.view.dist_kind = R.dist_kind;
+    mrow_ready_ = true;
+    multi_on_ = true;
+  }
+  bool multi_on_ = false;  // multi products enabled for this problem
+  // the span-scheduled view of a layout used by the multi products, or null
+  const pdlpk_csr* multi_view(const pdlpk_csr& A) const {
+    if (!multi_on_) return nullptr;
+    if (A.seg_mode) return &A;
+    if (mrow_ready_ && A.index == prob_.row.view.index) return &mrow_.view;
+    return nullptr;
+  }
+  // out[q] = A in[q], q < k (k <= 4; padded to 2 or 4 with a scratch output)
+  void multi_product(const pdlpk_csr& A, int k, double* const* in, double* const* out,
+                     int64_t operand_len) {
+    const pdlpk_csr* V = multi_view(A);
+    const int vec = k <= 2 ? 2 : 4;
+    pdlpk_multi_vecs vi{}, vo{};
+    for (int q = 0; q < vec; ++q) {
+      vi.v[q] = in[q < k ? q : 0];
+      vo.v[q] = q < k ? out[q] : multi_prod_[1].get();
+    }
+    const size_t pack = static_cast<size_t>(vec) * static_cast<size_t>(std::max<int64_t>(operand_len, 1));
+    if (multi_pack_.size() < pack) multi_pack_.alloc(pack);
+    const size_t part = static_cast<size_t>(vec) * static_cast<size_t>(std::max<int64_t>(V->n_chunks, 1));
+    if (multi_part_.size() < part) multi_part_.alloc(part);
+    PDLP_LAUNCH(pdlpk_spmv_multi(V, 0, vec, &vi, operand_len, multi_pack_.get(), &vo,
+                                 multi_part_.get(), s()));
+  }
   DevBuf<double> side_prod_;  // the average ray's A^T product
   std::unique_ptr<Stream> gap_side_;  // second gap query's stream
   DevBuf<double> gap_scratch2_;
@@ -2336,7 +2398,11 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
       // distances) runs on the side stream with its own reduction scratch:
       // the same kernels on the same inputs, overlapped.
       const pdlpk_red rr = red();
-      const bool side = have_avg && !dist() && !gap_serial_;
+      // multi-vector products (perf mode, both layouts span-scheduled): the
+      // cadence's products in one pass per layout, all on the main stream
+      const bool multi = have_avg && !dist() && !parity_ && multi_view(P.K) != nullptr &&
+                         multi_view(P.KT) != nullptr;
+      const bool side = have_avg && !dist() && !gap_serial_ && !multi;
       cudaStream_t sa = s();
       pdlpk_red ra = rr;
       double* prod_a = D.prod_n.get();
@@ -2353,7 +2419,45 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
       }
       std::vector<RayCand> cands;
       if (cfg.detect_infeasibility) cands = ray_candidates(P, D, have_avg);
-      if (have_avg) {
+      std::vector<size_t> joint;  // ray candidates whose K' product joins the multi pass
+      if (multi) {
+        PDLP_LAUNCH(pdlpk_average_into(D.state.get(), D.sum_x.get(), D.sum_y.get(), D.avg_x.get(),
+                                       D.avg_y.get(), P.n, P.m, s()));
+        for (size_t q = 0; q < cands.size() && joint.size() < 2; ++q) {
+          if (cands[q].known_aty != D.aty[c].get()) joint.push_back(q);  // difference, average
+        }
+        for (size_t q : joint) {
+          PDLP_LAUNCH(pdlpk_ray_primal_prep(&P, 0, cands[q].y, D.ray_y[q].get(), &rr,
+                                            slot(kSlotRay + 8 * static_cast<int>(q)), s()));
+        }
+        for (auto& b : multi_prod_) {
+          if (b.size() < static_cast<size_t>(P.n)) b.alloc(P.n);
+        }
+        double* in_k[2] = {D.x[c].get(), D.avg_x.get()};
+        double* out_k[2] = {D.ax_cur.get(), D.ax_avg.get()};
+        multi_product(P.K, 2, in_k, out_k, P.n);
+        double* in_t[4] = {D.y[c].get(), D.avg_y.get(), nullptr, nullptr};
+        double* out_t[4] = {D.aty[c].get(), D.aty_avg.get(), nullptr, nullptr};
+        for (size_t j = 0; j < joint.size(); ++j) {
+          in_t[2 + j] = D.ray_y[joint[j]].get();
+          out_t[2 + j] = j == 0 ? D.prod_n.get() : multi_prod_[0].get();
+        }
+        multi_product(P.KT, 2 + static_cast<int>(joint.size()), in_t, out_t, P.m);
+        for (size_t j = 0; j < joint.size(); ++j) {
+          const size_t q = joint[j];
+          double* sl = slot(kSlotRay + 8 * static_cast<int>(q));
+          PDLP_LAUNCH(pdlpk_ray_primal_finish(&P, 0, D.ray_y[q].get(), out_t[2 + j], nullptr, sl + 1,
+                                              D.rhat[q].get(), &rr, sl + 2, s()));
+          PDLP_LAUNCH(pdlpk_ray_dual_prep(&P, 0, cands[q].x, &rr, sl + 4, s()));
+        }
+        PDLP_LAUNCH(pdlpk_screen(&P, 0, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
+                                 D.aty_avg.get(), cfg.rc_mode, &rr, D.rc_b.get(),
+                                 slot(kSlotScrAvg), s()));
+        if (want_restart) {
+          PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_x.get(), D.ref_x.get(), P.n, &rr, slot(kSlotDist + 2), s()));
+          PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_y.get(), D.ref_y.get(), P.m, &rr, slot(kSlotDist + 3), s()));
+        }
+      } else if (have_avg) {
         PDLP_LAUNCH(pdlpk_average_into(D.state.get(), D.sum_x.get(), D.sum_y.get(), D.avg_x.get(),
                                        D.avg_y.get(), P.n, P.m, sa));
         if (side) {
@@ -2373,27 +2477,35 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
           }
         }
       }
-      product(P.K, 0, D.x[c].get(), D.ax_cur.get());
-      product(P.KT, 0, D.y[c].get(), D.aty[c].get());
+      if (!multi) {
+        product(P.K, 0, D.x[c].get(), D.ax_cur.get());
+        product(P.KT, 0, D.y[c].get(), D.aty[c].get());
+      }
       D.fresh_products_k = D.k();
-      if (have_avg && !side) {
+      if (have_avg && !side && !multi) {
         product(P.K, 0, D.avg_x.get(), D.ax_avg.get());
         product(P.KT, 0, D.avg_y.get(), D.aty_avg.get());
       }
       PDLP_LAUNCH(pdlpk_screen(&P, 0, D.x[c].get(), D.y[c].get(), D.ax_cur.get(), D.aty[c].get(),
                                cfg.rc_mode, &rr, D.rc_a.get(), slot(kSlotScrCur), s()));
-      if (have_avg && !side) {
+      if (have_avg && !side && !multi) {
         PDLP_LAUNCH(pdlpk_screen(&P, 0, D.avg_x.get(), D.avg_y.get(), D.ax_avg.get(),
                                  D.aty_avg.get(), cfg.rc_mode, &rr, D.rc_b.get(),
                                  slot(kSlotScrAvg), s()));
       }
       if (cfg.detect_infeasibility) {
-        enqueue_rays(P, D, cands, 0, side ? cands.size() - 1 : cands.size());
+        if (multi) {
+          for (size_t q = 0; q < cands.size(); ++q) {  // the rest (the current iterate's ray)
+            if (std::find(joint.begin(), joint.end(), q) == joint.end()) enqueue_rays(P, D, cands, q, q + 1);
+          }
+        } else {
+          enqueue_rays(P, D, cands, 0, side ? cands.size() - 1 : cands.size());
+        }
       }
       if (want_restart) {
         PDLP_LAUNCH(pdlpk_diff_norm_sq(D.x[c].get(), D.ref_x.get(), P.n, &rr, slot(kSlotDist), s()));
         PDLP_LAUNCH(pdlpk_diff_norm_sq(D.y[c].get(), D.ref_y.get(), P.m, &rr, slot(kSlotDist + 1), s()));
-        if (have_avg && !side) {
+        if (have_avg && !side && !multi) {
           PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_x.get(), D.ref_x.get(), P.n, &rr, slot(kSlotDist + 2), s()));
           PDLP_LAUNCH(pdlpk_diff_norm_sq(D.avg_y.get(), D.ref_y.get(), P.m, &rr, slot(kSlotDist + 3), s()));
         }

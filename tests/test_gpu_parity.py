@@ -501,3 +501,22 @@ def test_row_panels_bit_identical(gpu, monkeypatch):
         b = P.solve(p, o)
         assert a.iterations == b.iterations and a.restarts == b.restarts
         assert same_bits(a.x, b.x) and same_bits(a.y, b.y), np_
+
+
+def test_multi_vector_cadence_products_bit_identical(gpu, monkeypatch):
+    # The cadence's products through one multi-vector pass per layout
+    # (k_multi.cu: current + average through K; current + average + the
+    # difference and average rays through K') equal the single-vector
+    # products on the same span schedules bit for bit, so whole solves are
+    # identical with and without them.
+    p = P.generate("c2", 3, rows=4000, cols=8000, kmax=3000)
+    tol = P.relative_tolerances(p)
+    o = P.SolverOptions(tolerances=P.TerminationTolerances(*tol), iteration_limit=700)
+    monkeypatch.setenv("PDLP_SEG", "1")
+    monkeypatch.setenv("PDLP_MULTI", "0")
+    a = P.solve(p, o)
+    monkeypatch.setenv("PDLP_MULTI", "1")
+    b = P.solve(p, o)
+    assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
+    assert same_bits(a.x, b.x) and same_bits(a.y, b.y)
+    assert a.restarts > 0  # the cadence (incl. restarts to the average) ran
