@@ -568,16 +568,20 @@ int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t /*operand_l
     return PDLPK_SHORT_MAX;
   }
   const int64_t nnz = L.view.nnz;
-  int64_t over64 = 0, over256 = 0, maxlen = 0;
+  int64_t over64 = 0, over256 = 0, maxlen = 0, empty = 0;
   for (int64_t r = 0; r < dim; ++r) {
     const int64_t len = start[r + 1] - start[r];
     if (len > 64) over64 += len;
     if (len > 256) over256 += len;
+    if (len == 0) ++empty;
     maxlen = std::max(maxlen, len);
   }
-  const double mean = dim > 0 ? static_cast<double>(nnz) / static_cast<double>(dim) : 0.0;
-  bool seg = nnz >= (int64_t(16) << 20) && !L.view.tile_direct &&
-             (10 * over256 >= nnz || static_cast<double>(maxlen) > 16.0 * mean);
+  // a heavy tail (lines beyond a warp line's 2,048 entries and a tenth of the
+  // entries in lines > 256: C2's power-law columns), and few empty lines
+  // (each is a span of its own).  Bimodal layouts such as C3's rows (2 and
+  // 1,000 entries) stay on tiles + warp lines.
+  bool seg = nnz >= (int64_t(16) << 20) && !L.view.tile_direct && maxlen > PDLPK_WARP_LINE_MAX &&
+             10 * over256 >= nnz && 100 * empty < dim;
   if (const char* e = std::getenv("PDLP_SEG")) seg = e[0] == '1';
   if (seg) {
     const char* es = std::getenv("PDLP_SEG_SPAN");
@@ -591,7 +595,20 @@ int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t /*operand_l
     return t;
   }
   const int64_t t = 3 * over64 >= nnz ? 256 : 64;
-  const int32_t budget = nnz >= (int64_t(16) << 20) ? pdlpk_stage_budget(2016) : 0;
+  // stage budget: the C1 sweep's 896-entry default for very short lines
+  // (C1's 2-entry columns, C3's 2-4-entry rows and columns); 2,016 entries
+  // for large layouts of longer short lines (C2's ~33-entry rows)
+  int64_t short_lines = 0, short_nnz = 0;
+  for (int64_t r = 0; r < dim; ++r) {
+    const int64_t len = start[r + 1] - start[r];
+    if (len <= t) {
+      ++short_lines;
+      short_nnz += len;
+    }
+  }
+  int32_t budget = (nnz >= (int64_t(16) << 20) && short_nnz >= 16 * short_lines)
+                       ? pdlpk_stage_budget(2016) : 0;
+  if (const char* eb = std::getenv("PDLP_STAGE_BUDGET")) budget = pdlpk_stage_budget(std::atoi(eb));
   build_schedule(start, dim, L, t, budget);
   return t;
 }
@@ -2107,7 +2124,7 @@ class Engine {
     DevBuf<double> carry;
   } panels_;
 
-  static int panel_count(int64_t n, int64_t nnz) {
+  static int panel_count(int64_t n, int64_t nnz, int64_t m) {
     if (const char* e = std::getenv("PDLP_ROW_PANELS")) {
       const int v = std::atoi(e);
       return v >= 2 ? std::min(v, PDLPK_MAX_ROW_PANELS) : 0;
@@ -2115,8 +2132,11 @@ class Engine {
     // x-bar above 48 MB and a matrix large enough for the gathers to
     // dominate; at most 4 panels (each launch re-reads the m-length row
     // pointers and carries)
+    // each launch re-reads the row pointers and the 8-byte carries (16 B per
+    // row and panel): only rows of >= 8 entries amortize that (C3's 2.5-entry
+    // rows measured 331 -> 807 us with 4 panels)
     const double mb = 8.0 * static_cast<double>(n) / 1048576.0;
-    if (mb <= 48.0 || nnz < (int64_t(16) << 20)) return 0;
+    if (mb <= 48.0 || nnz < (int64_t(16) << 20) || nnz < 8 * m) return 0;
     const int np = static_cast<int>(std::ceil(mb / 40.0));
     return np <= 4 ? np : 0;
   }
@@ -2126,7 +2146,7 @@ class Engine {
   void plan_panels(const pdlp_csr_view& v, int64_t n) {
     panels_ = Panels{};
     if (parity_ || comm_ != nullptr || v.primary_dim <= 0) return;
-    const int np = panel_count(n, v.nnz);
+    const int np = panel_count(n, v.nnz, v.primary_dim);
     if (np < 2) return;
     const int64_t m = v.primary_dim;
     const int64_t width = (n + np - 1) / np;

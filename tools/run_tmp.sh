@@ -1,3 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "multi or segmented or panels" > gpurun_out/t_multi.log 2>&1; echo rc=$? >> gpurun_out/t_multi.log
-python tools/cadence_c2.py > gpurun_out/cad3.log 2>&1
-PDLP_MULTI=0 python tools/cadence_c2.py > gpurun_out/cad3b.log 2>&1
+timeout 900 python tools/bench_configs.py c3 --steps 128 --warmup 8 --ttt-limit 30 > gpurun_out/cfg3.jsonl 2> gpurun_out/cfg3.err
+PDLP_STAGE_BUDGET=2016 timeout 900 python tools/bench_configs.py c3 --steps 128 --warmup 8 --ttt-limit 1 >> gpurun_out/cfg3.jsonl 2>> gpurun_out/cfg3.err
+PDLP_STAGE_BUDGET=1344 timeout 900 python tools/bench_configs.py c3 --steps 128 --warmup 8 --ttt-limit 1 >> gpurun_out/cfg3.jsonl 2>> gpurun_out/cfg3.err
+PDLP_SHORT_MAX=256 timeout 900 python tools/bench_configs.py c3 --steps 128 --warmup 8 --ttt-limit 1 >> gpurun_out/cfg3.jsonl 2>> gpurun_out/cfg3.err
