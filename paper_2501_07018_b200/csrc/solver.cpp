@@ -514,17 +514,24 @@ void build_seg_schedule(const int64_t* start, int64_t dim, DevLayout& L, int64_t
   }
   close();
   std::vector<uint32_t> masks(static_cast<size_t>(steps) * 16 + 16, 0u);
-  for (size_t i = 0; i < spans.size(); ++i) {
-    const int4 d = spans[i];
-    if (d.y <= 0) continue;
-    const int64_t e0 = static_cast<int64_t>(static_cast<uint32_t>(d.z)) | (static_cast<int64_t>(aux[i].w) << 32);
-    const int64_t b0 = e0 & ~int64_t(7);
-    for (int64_t r = d.x; r < static_cast<int64_t>(d.x) + d.y; ++r) {
-      const int64_t oh = start[r] - b0, oe = start[r + 1] - 1 - b0;
-      masks[static_cast<size_t>((step0[i] + oh / 256) * 16 + (oh % 256) / 32)] |= 1u << (oh % 32);
-      masks[static_cast<size_t>((step0[i] + oe / 256) * 16 + 8 + (oe % 256) / 32)] |= 1u << (oe % 32);
+  // spans own disjoint step ranges of the mask array: threads over spans
+  const int64_t nsp = static_cast<int64_t>(spans.size());
+  for_segments(nsp, static_cast<int>(std::clamp<int64_t>(nsp / 4096, 1, 16)),
+               [&](int, int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      const int4 d = spans[static_cast<size_t>(i)];
+      if (d.y <= 0) continue;
+      const int64_t e0 = static_cast<int64_t>(static_cast<uint32_t>(d.z)) |
+                         (static_cast<int64_t>(aux[static_cast<size_t>(i)].w) << 32);
+      const int64_t b0 = e0 & ~int64_t(7);
+      const int64_t s0 = step0[static_cast<size_t>(i)];
+      for (int64_t r = d.x; r < static_cast<int64_t>(d.x) + d.y; ++r) {
+        const int64_t oh = start[r] - b0, oe = start[r + 1] - 1 - b0;
+        masks[static_cast<size_t>((s0 + oh / 256) * 16 + (oh % 256) / 32)] |= 1u << (oh % 32);
+        masks[static_cast<size_t>((s0 + oe / 256) * 16 + 8 + (oe % 256) / 32)] |= 1u << (oe % 32);
+      }
     }
-  }
+  });
   upload_list(spans, L.seg_spans);
   upload_list(aux, L.seg_aux);
   upload_list(step0, L.seg_step0);
@@ -974,6 +981,7 @@ class Engine {
     upload_layout(by_row, n_glob_, bad.get(), prob_.row, s());
     g_interleave_warp_lines = false;
     build_multi_row(by_row);
+    start_panel_plan(by_row, n_glob_);
     const double t_row = lap();
     upload_layout(by_col, m, bad.get(), prob_.col, s());
     const double t_col = lap();
@@ -1069,6 +1077,8 @@ class Engine {
   }
 
   ~Engine() {
+    if (panel_thread_.t.joinable()) panel_thread_.t.join();
+    cudaStreamSynchronize(s());  // buffers on other streams (panels) free unordered with s()
     if (comm_ != nullptr) pdlpk_set_red_log(nullptr);
     if (peer_pbuf_ != nullptr) {
       cudaStreamSynchronize(s());
@@ -2116,6 +2126,9 @@ class Engine {
   // next to the pass's streams: the row layout is re-laid out as np CSR
   // matrices over consecutive column ranges of `width` columns, so each
   // launch of the row pass gathers from an x-bar range that stays in L2.
+  // The panel plan's own stream (created with the engine; declared before
+  // panels_ so the panel buffers, which free on it, go first).
+  std::unique_ptr<Stream> panel_stream_;
   struct Panels {
     int np = 0;
     int64_t width = 0;
@@ -2143,7 +2156,7 @@ class Engine {
 
   // Host part (structure and schedules) from the caller's row layout; the
   // device arrays are filled from the scaled values by fill_panels().
-  void plan_panels(const pdlp_csr_view& v, int64_t n) {
+  void plan_panels(const pdlp_csr_view& v, int64_t n, cudaStream_t ps) {
     panels_ = Panels{};
     if (parity_ || comm_ != nullptr || v.primary_dim <= 0) return;
     const int np = panel_count(n, v.nnz, v.primary_dim);
@@ -2176,8 +2189,8 @@ class Engine {
       const int64_t nz = st[q][m];
       L.start32.alloc(m + 1);
       std::vector<int32_t> s32(st[q].begin(), st[q].end());
-      PDLP_CK(cudaMemcpyAsync(L.start32.get(), s32.data(), (m + 1) * 4, cudaMemcpyHostToDevice, s()));
-      PDLP_CK(cudaStreamSynchronize(s()));
+      PDLP_CK(cudaMemcpyAsync(L.start32.get(), s32.data(), (m + 1) * 4, cudaMemcpyHostToDevice, ps));
+      PDLP_CK(cudaStreamSynchronize(ps));
       L.index.alloc(nz);
       L.value.alloc(nz);
       L.view.dim = m;
@@ -2201,6 +2214,40 @@ class Engine {
       panels_.views[static_cast<size_t>(q)] = L.view;
     }
     panels_.carry.alloc(m);
+  }
+
+  // The panels' host plan and schedules are built on a background thread
+  // while the column layout uploads (load_parts); joined before use.
+  struct Joiner {  // joins on every path, incl. a constructor that throws
+    std::thread t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } panel_thread_;
+  std::exception_ptr panel_err_;
+  void start_panel_plan(const pdlp_csr_view& v, int64_t n) {
+    if (parity_ || comm_ != nullptr || !starts_valid(v.start, v.primary_dim, v.nnz)) return;
+    const int dev = opt_.device;
+    if (!panel_stream_) panel_stream_ = std::make_unique<Stream>();
+    const cudaStream_t ps = panel_stream_->get();
+    panel_thread_.t = std::thread([this, v, n, dev, ps] {
+      try {
+        PDLP_CK(cudaSetDevice(dev));
+        AllocStreamScope scope(ps);  // the panel buffers live on (and free on) this stream
+        plan_panels(v, n, ps);
+        PDLP_CK(cudaStreamSynchronize(ps));
+      } catch (...) {
+        panel_err_ = std::current_exception();
+      }
+    });
+  }
+  void join_panels() {
+    if (panel_thread_.t.joinable()) panel_thread_.t.join();
+    if (panel_err_) {
+      std::exception_ptr e = panel_err_;
+      panel_err_ = nullptr;
+      std::rethrow_exception(e);
+    }
   }
 
   void fill_panels() {
@@ -2729,7 +2776,7 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
   if (o->enable_scaling) E.precondition(o->ruiz_passes, o->pock_chambolle != 0);
   if (std::getenv("PDLP_NO_UNIFORM") == nullptr) E.detect_uniform();
   if (!E.dist()) {
-    E.plan_panels(problem->by_row, problem->cols);
+    E.join_panels();
     E.fill_panels();
   }
   if (E.dist()) E.build_full_views();

@@ -1,4 +1,2 @@
-timeout 900 python tools/bench_configs.py c3 --steps 128 --warmup 8 --ttt-limit 30 > gpurun_out/cfg3.jsonl 2> gpurun_out/cfg3.err
-PDLP_STAGE_BUDGET=2016 timeout 900 python tools/bench_configs.py c3 --steps 128 --warmup 8 --ttt-limit 1 >> gpurun_out/cfg3.jsonl 2>> gpurun_out/cfg3.err
-PDLP_STAGE_BUDGET=1344 timeout 900 python tools/bench_configs.py c3 --steps 128 --warmup 8 --ttt-limit 1 >> gpurun_out/cfg3.jsonl 2>> gpurun_out/cfg3.err
-PDLP_SHORT_MAX=256 timeout 900 python tools/bench_configs.py c3 --steps 128 --warmup 8 --ttt-limit 1 >> gpurun_out/cfg3.jsonl 2>> gpurun_out/cfg3.err
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_schedule.py -q -m gpu -x > gpurun_out/t_e2e.log 2>&1; echo rc=$? >> gpurun_out/t_e2e.log
+python tools/e2e_c2.py > gpurun_out/e2e2.log 2>&1
