@@ -21,6 +21,7 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -623,10 +624,51 @@ int64_t autotune_schedule(const int64_t* start, int64_t dim, int64_t /*operand_l
 // Uploads one orientation; the raw int64 row pointers and indices are checked
 // on device before the int32 conversion (bad: device flag word, see
 // k_valid.cu).  bound = the secondary dimension.
+// A process-wide stream per device for schedule uploads built off the main
+// thread (never destroyed: the schedule buffers free on it).
+cudaStream_t schedule_stream() {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  int dev = 0;
+  PDLP_CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  cudaStream_t& st = streams[dev];
+  if (st == nullptr) PDLP_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  return st;
+}
+
 void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayout& L,
                    cudaStream_t s) {
   const int64_t dim = v.primary_dim, nnz = v.nnz;
   const bool wide = nnz >= (int64_t(1) << 31) - 1;
+  L.view.dim = dim;
+  L.view.nnz = nnz;
+  L.view.wide = wide ? 1 : 0;
+  // The schedule (a host pass over the line starts plus small uploads) is
+  // built on a second host thread while this one stages the layout's arrays.
+  const auto ts = std::chrono::steady_clock::now();
+  std::exception_ptr sched_err;
+  int dev = 0;
+  PDLP_CK(cudaGetDevice(&dev));
+  const bool interleave = g_interleave_warp_lines;
+  const cudaStream_t ss = schedule_stream();
+  std::thread sched([&, dev, interleave, ss] {
+    try {
+      PDLP_CK(cudaSetDevice(dev));
+      AllocStreamScope scope(ss);
+      g_interleave_warp_lines = interleave;
+      autotune_schedule(v.start, dim, bound, L, ss, bad);
+      PDLP_CK(cudaStreamSynchronize(ss));
+    } catch (...) {
+      sched_err = std::current_exception();
+    }
+  });
+  struct JoinOnExit {
+    std::thread& t;
+    ~JoinOnExit() {
+      if (t.joinable()) t.join();
+    }
+  } join_guard{sched};
   // start: 64-bit for wide layouts, else narrowed to 32 bits on the host
   // (saturating, so the range checks below still see a bad value)
   if (wide) {
@@ -650,20 +692,16 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
     stage_h2d(L.value_orig.get(), v.value, nnz * 8, s);
     PDLP_CK(cudaMemcpyAsync(L.value.get(), L.value_orig.get(), nnz * 8, cudaMemcpyDeviceToDevice, s));
   }
-  // (no sync: the host schedule build below overlaps the copies in flight)
-  L.view.dim = dim;
-  L.view.nnz = nnz;
-  L.view.wide = wide ? 1 : 0;
+  sched.join();
+  if (sched_err) std::rethrow_exception(sched_err);
   L.view.start = wide ? static_cast<const void*>(L.start64.get())
                       : static_cast<const void*>(L.start32.get());
   L.view.index = L.index.get();
   L.view.value = L.value.get();
   L.view.value_orig = L.value_orig.get();
-  const auto ts = std::chrono::steady_clock::now();
-  autotune_schedule(v.start, dim, bound, L, s, bad);
   if (std::getenv("PDLP_TIMING") != nullptr) {
     PDLP_CK(cudaStreamSynchronize(s));
-    std::fprintf(stderr, "phase=setup event=schedule lines=%lld nnz=%lld seconds=%.4f\n",
+    std::fprintf(stderr, "phase=setup event=layout lines=%lld nnz=%lld seconds=%.4f\n",
                  static_cast<long long>(dim), static_cast<long long>(nnz),
                  std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count());
   }
@@ -980,10 +1018,30 @@ class Engine {
     }
     upload_layout(by_row, n_glob_, bad.get(), prob_.row, s());
     g_interleave_warp_lines = false;
-    build_multi_row(by_row);
+    // the multi-product span schedule of the row layout: built on a second
+    // host thread while the column layout uploads
+    std::exception_ptr multi_err;
+    std::thread multi_thread([&, dev = opt_.device] {
+      try {
+        PDLP_CK(cudaSetDevice(dev));
+        AllocStreamScope scope(schedule_stream());
+        build_multi_row(by_row);
+        PDLP_CK(cudaStreamSynchronize(schedule_stream()));
+      } catch (...) {
+        multi_err = std::current_exception();
+      }
+    });
+    struct JoinOnExit {
+      std::thread& t;
+      ~JoinOnExit() {
+        if (t.joinable()) t.join();
+      }
+    } multi_guard{multi_thread};
     start_panel_plan(by_row, n_glob_);
     const double t_row = lap();
     upload_layout(by_col, m, bad.get(), prob_.col, s());
+    multi_thread.join();
+    if (multi_err) std::rethrow_exception(multi_err);
     const double t_col = lap();
     prob_.c_o = upload_vec(objective, n, s());
     prob_.lc_o = upload_vec(con_lower, m, s());
