@@ -238,7 +238,7 @@ typedef struct pdlpk_multi_vecs {
 int pdlpk_spmv_multi(const pdlpk_csr* A, int32_t orig, int32_t vec, const pdlpk_multi_vecs* in,
                      int64_t operand_len, double* pack, const pdlpk_multi_vecs* out, double* part,
                      cudaStream_t s);
-#define PDLPK_LINE_PARTIALS_MAX 262144
+#define PDLPK_LINE_PARTIALS_MAX 65536 /* the decision reads 2m terms serially in one CTA: bounded to 1 MB */
 
 /* Reduction context for cadence operations. */
 typedef struct pdlpk_red {

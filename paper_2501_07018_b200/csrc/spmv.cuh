@@ -149,6 +149,9 @@ __device__ __forceinline__ int warp_excl_scan_i(int v, int lane) {
 #ifndef PDLPK_SEG_PREFETCH
 #define PDLPK_SEG_PREFETCH 0 /* warm a step's epilogue operands in L2 (measured: 18 us slower) */
 #endif
+#ifndef PDLPK_SEG_PIPELINE
+#define PDLPK_SEG_PIPELINE 0 /* software-pipelined stream loads (one step ahead) */
+#endif
 #ifndef PDLPK_SEG_GATHER_KEEP
 #define PDLPK_SEG_GATHER_KEEP 0 /* L2 evict_last hint on the gathers */
 #endif
@@ -233,10 +236,49 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
     int64_t rc = d.x;
     double carry = 0.0;
     int64_t sid = A.seg_step0[it];
+#if PDLPK_SEG_PIPELINE
+    // the next step's index / value / mask loads are issued before this
+    // step's gathers: the stream latency overlaps the gather round trip
+    int4 ni0 = make_int4(0, 0, 0, 0), ni1 = make_int4(0, 0, 0, 0);
+    double2 nv[4];
+    uint32_t nmw = 0u;
+    auto fetch = [&](int64_t b, int64_t sidx) {
+      const int64_t kk = b + 8 * lane;
+      nmw = lane < 16 ? __ldg(A.seg_masks + sidx * 16 + lane) : 0u;
+      if (kk + 8 > e0 && kk < e1) {
+        ni0 = SEG_LD(reinterpret_cast<const int4*>(idx + kk));
+        ni1 = SEG_LD(reinterpret_cast<const int4*>(idx + kk + 4));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) nv[q] = SEG_LD(reinterpret_cast<const double2*>(vals + kk) + q);
+      }
+    };
+    fetch(e0 & ~int64_t(7), sid);
+#endif
     for (int64_t base = e0 & ~int64_t(7); base < e1; base += 256, ++sid) {
-      const uint32_t mw = lane < 16 ? __ldg(A.seg_masks + sid * 16 + lane) : 0u;
       const int64_t k0 = base + 8 * lane;
       double p[8];
+#if PDLPK_SEG_PIPELINE
+      const uint32_t mw = nmw;
+      const int4 i0 = ni0, i1 = ni1;
+      double a8[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a8[2 * q] = nv[q].x;
+        a8[2 * q + 1] = nv[q].y;
+      }
+      if (base + 256 < e1) fetch(base + 256, sid + 1);
+      if (k0 + 8 > e0 && k0 < e1) {
+        const int ci[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          p[u] = (k0 + u >= e0 && k0 + u < e1) ? a8[u] * SEG_G(v + ci[u]) : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = 0.0;
+      }
+#else
+      const uint32_t mw = lane < 16 ? __ldg(A.seg_masks + sid * 16 + lane) : 0u;
       if (k0 + 8 > e0 && k0 < e1) {
         const int4 i0 = SEG_LD(reinterpret_cast<const int4*>(idx + k0));
         const int4 i1 = SEG_LD(reinterpret_cast<const int4*>(idx + k0 + 4));
@@ -255,6 +297,7 @@ __device__ __forceinline__ void seg_spans(const pdlpk_csr& A, const double* __re
 #pragma unroll
         for (int u = 0; u < 8; ++u) p[u] = 0.0;
       }
+#endif
       const uint32_t hw = __shfl_sync(0xffffffffu, mw, lane >> 2);
       const uint32_t ew = __shfl_sync(0xffffffffu, mw, 8 + (lane >> 2));
       const uint32_t hb = (hw >> (8 * (lane & 3))) & 0xffu, eb = (ew >> (8 * (lane & 3))) & 0xffu;

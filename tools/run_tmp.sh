@@ -1,2 +1,2 @@
-timeout 1100 python -m pytest tests/ -q -m gpu -x -k "not scale" > gpurun_out/t_e2e.log 2>&1; echo rc=$? >> gpurun_out/t_e2e.log
-python tools/e2e_c2.py > gpurun_out/e2e2.log 2>&1
+timeout 1100 python -m pytest tests/ -q -m gpu -x -k "not scale" > gpurun_out/t_lp.log 2>&1; echo rc=$? >> gpurun_out/t_lp.log
+timeout 1500 python tools/c1_seeds.py > gpurun_out/c1_seeds.jsonl 2> gpurun_out/c1_seeds.err
