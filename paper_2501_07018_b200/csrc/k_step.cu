@@ -28,6 +28,9 @@ namespace pdlp {
 namespace {
 
 constexpr int kEwThreads = 256;
+#ifndef PDLPK_COL_SPLIT
+#define PDLPK_COL_SPLIT 1 /* segmented-span column pass as product + elementwise epilogue */
+#endif
 
 inline int ew_blocks(int64_t n) {
   int64_t b = (n + kEwThreads - 1) / kEwThreads;
@@ -401,19 +404,13 @@ struct ColEpi {
   }
 };
 
-template <class P, int Seg, bool Decide>
-__global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(pdlpk_step_args a) {
-  pdl_wait();
+// The column pass's tail: this CTA's partials of |dx|^2, dy'K dx and |x'|
+// into part3; with Decide, the last CTA combines every partial in a fixed
+// order and runs the accept/reject rule.  kt_slots: add the fixed slots of
+// K^T's multi-chunk lines (their epilogue terms live there).
+template <bool Decide>
+__device__ __forceinline__ void col_tail(const pdlpk_step_args& a, const ColEpi& e, bool kt_slots) {
   pdlpk_step_state* st = a.state;
-  if (st->halt) return;
-  const int cur = st->cur;
-  ColEpi e;
-  e.aty = a.aty[cur];
-  e.atyn = a.aty[cur ^ 1];
-  e.x = a.x[cur];
-  e.xn = a.x[cur ^ 1];
-  sched_spmv<P, Seg>(a.P.KT, a.P.KT.value, a.dy, e);
-  pdl_trigger();
   __shared__ double red[32];
   __shared__ bool last;
   const double s1 = block_sum(e.dx2, red);
@@ -469,15 +466,17 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(p
   }
   // then the fixed slots of multi-chunk lines (spmv.cuh), in slot order
   for (int64_t q = threadIdx.x; q < a.P.K.n_multi; q += blockDim.x) {
-    const double* s = a.P.K.line_acc + q * PDLPK_LINE_ACC;
-    dy2 += __ldcg(s);
-    infy = max_keep(infy, __ldcg(s + 1));
+    const double* sl = a.P.K.line_acc + q * PDLPK_LINE_ACC;
+    dy2 += __ldcg(sl);
+    infy = max_keep(infy, __ldcg(sl + 1));
   }
-  for (int64_t q = threadIdx.x; q < a.P.KT.n_multi; q += blockDim.x) {
-    const double* s = a.P.KT.line_acc + q * PDLPK_LINE_ACC;
-    dx2 += __ldcg(s);
-    curv += __ldcg(s + 1);
-    infx = max_keep(infx, __ldcg(s + 2));
+  if (kt_slots) {
+    for (int64_t q = threadIdx.x; q < a.P.KT.n_multi; q += blockDim.x) {
+      const double* sl = a.P.KT.line_acc + q * PDLPK_LINE_ACC;
+      dx2 += __ldcg(sl);
+      curv += __ldcg(sl + 1);
+      infx = max_keep(infx, __ldcg(sl + 2));
+    }
   }
   dy2 = block_sum(dy2, red);
   __syncthreads();
@@ -492,6 +491,69 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(p
     st->ticket = 0;
     decide(st, dx2, dy2, curv, infx, infy, a.f_down, a.f_up, a.table_len);
   }
+}
+
+template <class P, int Seg, bool Decide>
+__global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_pass(pdlpk_step_args a) {
+  pdl_wait();
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int cur = st->cur;
+  ColEpi e;
+  e.aty = a.aty[cur];
+  e.atyn = a.aty[cur ^ 1];
+  e.x = a.x[cur];
+  e.xn = a.x[cur ^ 1];
+  sched_spmv<P, Seg>(a.P.KT, a.P.KT.value, a.dy, e);
+  pdl_trigger();
+  col_tail<Decide>(a, e, true);
+}
+
+// Split column pass (segmented-span layouts): the product alone writes
+// d = K^T dy to aty_diff (one 8-byte store per line instead of the
+// epilogue's three loads and a store at scattered lanes), then a coalesced
+// elementwise pass runs the epilogue and the decision.
+struct DiffEpi {
+  double* __restrict__ out;
+  struct Pre {};
+  __device__ __forceinline__ Pre load(int64_t) const { return {}; }
+  __device__ __forceinline__ double init(const Pre&) const { return 0.0; }
+  __device__ __forceinline__ void prefetch(int64_t) const {}
+  static constexpr int kStaged = 0;
+  __device__ __forceinline__ const double* staged_src(int) const { return nullptr; }
+  __device__ __forceinline__ bool staged_reused(int) const { return false; }
+  __device__ __forceinline__ Pre from_stage(const double* const*, int) const { return {}; }
+  __device__ __forceinline__ void reset_acc() {}
+  __device__ __forceinline__ void export_acc(double*) const {}
+  __device__ __forceinline__ void line(int64_t r, double acc, const Pre&) { out[r] = acc; }
+};
+
+template <class P, int Seg>
+__global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) col_product(pdlpk_step_args a) {
+  pdl_wait();
+  if (a.state->halt) return;
+  DiffEpi e{a.aty_diff};
+  sched_spmv<P, Seg>(a.P.KT, a.P.KT.value, a.dy, e);
+  pdl_trigger();
+}
+
+__global__ void __launch_bounds__(kEwThreads) col_epi_decide(pdlpk_step_args a) {
+  pdl_wait();
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int cur = st->cur;
+  ColEpi e;
+  e.aty = a.aty[cur];
+  e.atyn = a.aty[cur ^ 1];
+  e.x = a.x[cur];
+  e.xn = a.x[cur ^ 1];
+  const int64_t n = a.P.n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    e.line(i, __ldcs(a.aty_diff + i), {__ldcs(e.aty + i), __ldcs(e.x + i), e.xn[i]});
+  }
+  pdl_trigger();
+  col_tail<true>(a, e, false);
 }
 
 // ------------------------------------------------------------ parity path ---
@@ -670,7 +732,11 @@ struct LaunchRowCol {
           launch_pdl(pdl, row_pass<P, Seg, 0>, gu, kSpmvThreads, smem, s, *a);
       }
     } else {
-      if (decide_here) {
+      if (decide_here && PDLPK_COL_SPLIT && A.seg_mode) {
+        launch_pdl(pdl, col_product<P, Seg>, gu, kSpmvThreads, smem, s, *a);
+        launch_pdl(pdl, col_epi_decide, static_cast<unsigned>(ew_blocks(a->P.n)), kEwThreads,
+                   static_cast<size_t>(0), s, *a);
+      } else if (decide_here) {
         allow_smem(col_pass<P, Seg, true>, smem);
         launch_pdl(pdl, col_pass<P, Seg, true>, gu, kSpmvThreads, smem, s, *a);
       } else {
@@ -841,6 +907,8 @@ using namespace pdlp;
 extern "C" int64_t pdlpk_step_partials(const pdlpk_problem* P) {
   const int64_t g2 = sched_blocks(P->K), g3 = sched_blocks(P->KT);
   int64_t need = 2 * g2 > 3 * g3 ? 2 * g2 : 3 * g3;
+  const int64_t ge = 3 * static_cast<int64_t>(ew_blocks(P->n));  // split column pass
+  if (P->KT.seg_mode && ge > need) need = ge;
   if (P->m <= PDLPK_LINE_PARTIALS_MAX && 2 * P->m > need) need = 2 * P->m;  // line_partials
   return need + 64;
 }
