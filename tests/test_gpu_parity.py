@@ -520,3 +520,24 @@ def test_multi_vector_cadence_products_bit_identical(gpu, monkeypatch):
     assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
     assert same_bits(a.x, b.x) and same_bits(a.y, b.y)
     assert a.restarts > 0  # the cadence (incl. restarts to the average) ran
+
+
+@pytest.mark.parametrize("knobs", [{"PDLP_ROW_PANELS": "2"}, {"PDLP_ROW_PANELS": "3", "PDLP_SEG": "1"},
+                                   {"PDLP_SEG": "1", "PDLP_MULTI": "1"}])
+def test_forced_schedules_on_ragged_problems(gpu, ref, monkeypatch, knobs):
+    # Column panels, segmented spans and multi-vector cadence products forced
+    # onto small ragged LPs (empty rows and columns, lines shorter and longer
+    # than the tiles): the solves reach the reference's outcome.
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(91)
+    cases = [random_box_lp(rng, 30 + rng.integers(40), 30 + rng.integers(60)) for _ in range(4)]
+    cases.append(P.generate("c2", 4, rows=1500, cols=3000, kmax=2500))
+    for p in cases:
+        tol = (1e-7, 1e-7, 1e-8)
+        o = P.SolverOptions(tolerances=P.TerminationTolerances(*tol), iteration_limit=20000)
+        g, r = P.solve(p, o), ref.solve(p, o)
+        assert g.status == r.status
+        if r.status == P.SolveStatus.OPTIMAL:
+            assert abs(g.summary.primal_objective - r.summary.primal_objective) <= 1e-5 * (
+                1.0 + abs(r.summary.primal_objective))
