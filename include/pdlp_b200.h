@@ -219,6 +219,14 @@ int pdlp_device_count(void);
  * pool and keep it between calls (no map/unmap per solve); this returns the
  * pool's unused memory on `device` to the driver.  0 or a negative error. */
 int pdlp_trim_device_memory(int device);
+/* B200 extension.  Counters of the sharded solves' distributed normalized
+ * gap (restarts.hpp:107-220 evaluated without gathering a vector, DESIGN.md
+ * §8): out[0..3] = evaluations, bracket-search rounds, events swept after
+ * the search, evaluations compared with the gathered one (PDLP_GAPD_CHECK=1);
+ * max_rel[0] / max_rel[1] = the largest relative difference seen there in
+ * the gap value / in lambda* (max_rel holds 2 doubles).  reset != 0 zeroes
+ * them after reading.  Process-wide. */
+void pdlp_gap_dist_stats(int64_t* out, double* max_rel, int32_t reset);
 
 /* Original-space re-verification of an infeasibility certificate (the `check`
  * command, tools/main.cpp:199-311 -> residuals.hpp:222-299): kind 0 tests a
@@ -269,14 +277,27 @@ int pdlp_mps_write(const pdlp_problem_view* problem, const char* name, int32_t m
                    char** text, size_t* len);
 void pdlp_mps_free_text(char* text);
 
-/* ------------------------------------------------- row-sharded solve --- *
+/* ----------------------------------------------------- sharded solve --- *
  * B200 extension (the reference solve is single-process).
- * `world` ranks, one GPU each: rank g owns rows [row_begin,row_end) of A in
- * both layouts (K_g and the matching entries of K^T) and the primal block
- * [col_begin,col_end).  Per PDHG attempt: x-bar all-gather, local K_g x-bar +
- * dual update, local partial K_g^T dy, reduce-scatter to the column owners,
- * and one all-gather of 5 step scalars; every rank takes the same decisions.
- * Blocks are equal-sized (NCCL all-gather / reduce-scatter); both are even. */
+ * `world` ranks, one GPU each.  Every rank owns a row block
+ * [row_begin,row_end) (y, A x, row bounds) and a column block
+ * [col_begin,col_end) (x, A'y, c, variable bounds); the matrix is cut one of
+ * two ways:
+ *   PDLP_CUT_ROWS  rank g holds its rows of A in both layouts: K_g (its
+ *                  rows, global column indices) and K_g^T (all n columns,
+ *                  its rows' entries).  Per attempt: x-bar all-gather, local
+ *                  K_g x-bar + dual update, partial K_g^T dy reduce-scattered
+ *                  to the column owners -- two n-vectors exchanged.
+ *   PDLP_CUT_COLS  rank g holds its columns of A in both layouts: K_g^T
+ *                  (its columns, global row indices) and K_g (all m rows,
+ *                  its columns' entries).  Per attempt: partial K_g x-bar
+ *                  reduce-scattered to the row owners + dual update, dy
+ *                  all-gathered, local K_g^T dy -- two m-vectors exchanged.
+ * plus one all-gather of 5 step scalars; every rank takes the same
+ * decisions.  Blocks are equal-sized (NCCL all-gather / reduce-scatter);
+ * both are even. */
+#define PDLP_CUT_ROWS 0
+#define PDLP_CUT_COLS 1
 typedef struct pdlp_shard_plan {
   int32_t rank;
   int32_t world;
@@ -284,11 +305,16 @@ typedef struct pdlp_shard_plan {
   int64_t row_block, col_block; /* mb, nb */
   int64_t row_begin, row_end;
   int64_t col_begin, col_end;
+  int32_t cut; /* PDLP_CUT_ROWS / PDLP_CUT_COLS */
+  int32_t _pad;
 } pdlp_shard_plan;
 
-/* One rank's shard, host side.  rows = K_g (lines local, global column
- * indices, pointing into the caller's by_row arrays); cols = K_g^T (all n
- * columns, local row indices, owned by the shard). */
+/* One rank's shard, host side.  PDLP_CUT_ROWS: rows = K_g (lines local,
+ * global column indices, pointing into the caller's by_row arrays), cols =
+ * K_g^T (all n columns, local row indices, owned by the shard).
+ * PDLP_CUT_COLS: rows = all m rows restricted to the column block (local
+ * column indices, owned by the shard), cols = the block's columns (global
+ * row indices, pointing into the caller's by_col arrays). */
 typedef struct pdlp_shard_view {
   pdlp_shard_plan plan;
   pdlp_csr_view rows;
@@ -298,15 +324,25 @@ typedef struct pdlp_shard_view {
   const double* var_upper;
   const double* con_lower; /* row_end - row_begin */
   const double* con_upper;
-  int64_t entry_offset; /* by_row position of K_g's first entry */
+  int64_t entry_offset; /* PDLP_CUT_ROWS: by_row position of K_g's first entry */
+  /* PDLP_CUT_COLS: per row r (m entries), by_row position of the row's first
+   * shard entry minus rows.start[r] (validation messages carry whole-problem
+   * entry indices); NULL when unknown (messages then carry shard indices). */
+  const int64_t* row_entry_offset;
 } pdlp_shard_view;
 
+/* The shard of `rank`: equal even blocks; the cut exchanges the smaller
+ * dimension (PDLP_CUT_COLS when rows < cols; PDLP_SHARD_CUT=rows|cols in the
+ * environment overrides). */
 int pdlp_shard_plan_for(int64_t rows, int64_t cols, int32_t rank, int32_t world,
                         pdlp_shard_plan* out);
 /* CPU only.  *owner keeps the shard's arrays alive; release with
  * pdlp_shard_free.  Structural layout errors -> PDLP_ERR_INVALID_PROBLEM. */
 int pdlp_shard_extract(const pdlp_problem_view* problem, int32_t rank, int32_t world,
                        pdlp_shard_view* out, void** owner);
+/* The same with an explicit cut (PDLP_CUT_ROWS / PDLP_CUT_COLS). */
+int pdlp_shard_extract_cut(const pdlp_problem_view* problem, int32_t rank, int32_t world,
+                           int32_t cut, pdlp_shard_view* out, void** owner);
 void pdlp_shard_free(void* owner);
 
 /* 128-byte ncclUniqueId for pdlp_solve_sharded (rank 0 creates it, the

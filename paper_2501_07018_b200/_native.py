@@ -186,6 +186,8 @@ class ShardPlan(C.Structure):
         ("row_end", C.c_int64),
         ("col_begin", C.c_int64),
         ("col_end", C.c_int64),
+        ("cut", C.c_int32),
+        ("_pad", C.c_int32),
     ]
 
 
@@ -200,6 +202,7 @@ class ShardView(C.Structure):
         ("con_lower", c_double_p),
         ("con_upper", c_double_p),
         ("entry_offset", C.c_int64),
+        ("row_entry_offset", C.POINTER(C.c_int64)),
     ]
 
 
@@ -211,10 +214,13 @@ SOLVER_SIGNATURES = {
     "pdlp_abi_version": (C.c_int, []),
     "pdlp_device_count": (C.c_int, []),
     "pdlp_trim_device_memory": (C.c_int, [C.c_int]),
+    "pdlp_gap_dist_stats": (None, [C.POINTER(C.c_int64), c_double_p, C.c_int32]),
     "pdlp_shard_plan_for": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32,
                                       C.POINTER(ShardPlan)]),
     "pdlp_shard_extract": (C.c_int, [C.POINTER(ProblemView), C.c_int32, C.c_int32,
                                      C.POINTER(ShardView), C.POINTER(C.c_void_p)]),
+    "pdlp_shard_extract_cut": (C.c_int, [C.POINTER(ProblemView), C.c_int32, C.c_int32, C.c_int32,
+                                         C.POINTER(ShardView), C.POINTER(C.c_void_p)]),
     "pdlp_shard_free": (None, [C.c_void_p]),
     "pdlp_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "pdlp_check_certificate": (C.c_int, [C.POINTER(ProblemView), C.c_int32, c_double_p, C.c_double,

@@ -85,7 +85,8 @@ def build(verbose: bool = False, force: bool = False) -> list[str]:
     if jobs or _mtime(LIB) < max(_mtime(o) for o in objs):
         _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs)
     gen_src = os.path.join(CSRC, "gen", "instances.cpp")
-    if _mtime(GEN_LIB) < max(_mtime(gen_src), _mtime(os.path.join(INCLUDE, "pdlp_gen.h"))):
+    if _mtime(GEN_LIB) < max(_mtime(gen_src), _mtime(os.path.join(INCLUDE, "pdlp_gen.h")),
+                             _mtime(os.path.join(INCLUDE, "pdlp_b200.h"))):
         _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-Wextra",
               f"-I{INCLUDE}", "-o", GEN_LIB, gen_src])
     return [LIB, GEN_LIB]

@@ -448,7 +448,9 @@ __global__ void finalize_perf_kernel(Work w, int64_t E, const double* r_slot, do
     }
     ls = clampd(ls, lam, hi);
   } else {
-    double c_sum = c0, b_sum = b0, hi = CUDART_INF;
+    // hi: the lambda of the last group above the sorted events (inf for a
+    // full sort; the bracket's upper neighbour for the distributed gap)
+    double c_sum = c0, b_sum = b0, hi = w.sc->base[2];
     if (E > 0) {
       c_sum = c0 + (w.cs[E - 1] + w.dc[w.vals_out[E - 1]]);
       b_sum = b0 + (w.bs[E - 1] + w.di[w.vals_out[E - 1]]);
@@ -486,6 +488,30 @@ __device__ __forceinline__ double cand_y(const GapIn& g, int64_t j, double lambd
     v = 0.0;
   }
   return cone_project(v, cone_of_bounds(g.lc[j], g.uc[j]));
+}
+
+// Coordinate t's term of gap_value_at (restarts.hpp:50-71): primal
+// coordinates first, then the dual ones.
+__device__ __forceinline__ double value_term(const GapIn& g, int64_t t, double lambda) {
+  if (t < g.n) {
+    const double xh = cand_x(g, t, lambda);
+    return g.cc(t) * (g.x[t] - xh) + g.aty[t] * xh;
+  }
+  const int64_t j = t - g.n;
+  const double yh = cand_y(g, j, lambda);
+  const double yj = g.y[j];
+  double d = -(yh * g.ax[j]);
+  if (yh > 0.0) {
+    d -= mul_zero_inf(-g.lc[j], yh);
+  } else if (yh < 0.0) {
+    d -= mul_zero_inf(-g.uc[j], yh);
+  }
+  if (yj > 0.0) {
+    d += mul_zero_inf(-g.lc[j], yj);
+  } else if (yj < 0.0) {
+    d += mul_zero_inf(-g.uc[j], yj);
+  }
+  return d;
 }
 
 // gap_value_at (restarts.hpp:50-71) in the reference's exact order.
@@ -730,27 +756,7 @@ extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const d
   launch_pdl(PDLPK_PDL_CADENCE, hit_fraction_kernel, static_cast<unsigned>(1), 1, 0, s, w, E, gap_slot + 2);
   const double* lam_star = &w.sc->lambda_star;
   auto fv = [g, lam_star] __device__(int64_t t, double* v) -> unsigned {
-    const double lambda = *lam_star;
-    if (t < g.n) {
-      const double xh = cand_x(g, t, lambda);
-      v[0] = g.cc(t) * (g.x[t] - xh) + g.aty[t] * xh;
-      return 1u;
-    }
-    const int64_t j = t - g.n;
-    const double yh = cand_y(g, j, lambda);
-    const double yj = g.y[j];
-    double d = -(yh * g.ax[j]);
-    if (yh > 0.0) {
-      d -= mul_zero_inf(-g.lc[j], yh);
-    } else if (yh < 0.0) {
-      d -= mul_zero_inf(-g.uc[j], yh);
-    }
-    if (yj > 0.0) {
-      d += mul_zero_inf(-g.lc[j], yj);
-    } else if (yj < 0.0) {
-      d += mul_zero_inf(-g.uc[j], yj);
-    }
-    v[0] = d;
+    v[0] = value_term(g, t, *lam_star);
     return 1u;
   };
   const int rc = multi_reduce<1>(fv, n + m, PDLPK_RED_TREE, red->shards, 0u, red->scratch,
@@ -758,4 +764,223 @@ extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const d
   if (rc != 0) return rc;
   launch_pdl(PDLPK_PDL_CADENCE, value_finish_kernel, static_cast<unsigned>(1), 1, 0, s, &w.sc->value, r_slot, r_value, gap_slot);
   return static_cast<int>(cudaGetLastError());
+}
+
+// ------------------------------------------- distributed gap ---
+// Row-sharded solves: each rank holds only its own column block (x, A'y, c,
+// bounds) and row block (y, A x, row bounds), so it builds the breakpoint
+// events of those coordinates (pdlpk_gap_prepare on the local views).  The
+// first crossing of the global descending order is located by a bracket
+// search that the host drives (solver.cpp Engine::gap_dist): at a sampled
+// key s every rank reduces, over its events inside the bracket, the masses
+// strictly above s and at-or-above s (TREE order) and the count below s;
+// the ranks' values are combined in rank order, phi(s) = C + B / lam(s)^2
+// says which side of s the crossing lies on, and each rank compacts its
+// bracket.  When the bracket is small its events are all-gathered, stably
+// sorted (rank order breaks key ties identically on every rank) and swept
+// with the single-GPU kernels, starting from the masses above the bracket.
+// No rank ever holds another rank's vectors.
+
+namespace pdlp {
+namespace {
+
+__global__ void gapd_stage_kernel(Work w, double* dst) {
+  dst[0] = w.sc->sums[0];
+  dst[1] = w.sc->sums[1];
+  dst[2] = static_cast<double>(w.sc->num_events);
+}
+
+__global__ void gapd_sample_kernel(const uint64_t* keys, int64_t A, int S, double* out) {
+  GRID_STRIDE(i, S) {
+    const int64_t k = A >= S ? (i * A) / S : i;
+    out[i] = __longlong_as_double(i < A ? static_cast<long long>(keys[k]) : 0ll);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[S] = static_cast<double>(A < S ? A : S);
+}
+
+__global__ void gapd_flag_kernel(Work w, const uint64_t* keys, int64_t A, uint64_t lo, uint64_t hi) {
+  GRID_STRIDE(e, A) {
+    const uint64_t k = keys[e];
+    w.flag[e] = (k >= lo && k <= hi) ? 1 : 0;
+  }
+}
+
+__global__ void gapd_pack_kernel(Work w, const uint64_t* keys, const int32_t* slots, int64_t A,
+                                 int64_t K, double* dst) {
+  GRID_STRIDE(e, K) {
+    const bool v = e < A;
+    dst[e] = __longlong_as_double(v ? static_cast<long long>(keys[e]) : 0ll);
+    dst[K + e] = v ? w.dc[slots[e]] : 0.0;
+    dst[2 * K + e] = v ? w.di[slots[e]] : 0.0;
+  }
+}
+
+struct GapdOffsets {
+  int world;
+  int64_t K;
+  int64_t off[PDLPK_GAPD_MAX_RANKS + 1];
+};
+
+// rank-ordered concatenation of the gathered brackets into slots 0..T-1
+__global__ void gapd_unpack_kernel(Work f, const double* all, GapdOffsets o) {
+  const int64_t T = o.off[o.world];
+  GRID_STRIDE(t, T) {
+    int r = 0;
+    while (t >= o.off[r + 1]) ++r;
+    const int64_t e = t - o.off[r];
+    const double* blk = all + static_cast<int64_t>(r) * 3 * o.K;
+    f.keys_in[t] = static_cast<uint64_t>(__double_as_longlong(blk[e]));
+    f.dc[t] = blk[o.K + e];
+    f.di[t] = blk[2 * o.K + e];
+    f.sel[t] = static_cast<int32_t>(t);
+  }
+}
+
+__global__ void gapd_base_kernel(Work f, double c0, double b0, double hi0) {
+  f.sc->base[0] = c0;
+  f.sc->base[1] = b0;
+  f.sc->base[2] = hi0;
+  f.sc->above_count = 0;
+}
+
+// The bracket's lowest group is known to cross (phi >= r^2 at its head, from
+// the search's reductions): if the sweep's own sums (scan order) put it just
+// below r^2, that group is the crossing.
+__global__ void gapd_force_last_kernel(Work f, int64_t T) {
+  if (f.sc->first != ~0ull || T <= 0) return;
+  int64_t h = T - 1;
+  const uint64_t k = f.keys_out[h];
+  while (h > 0 && f.keys_out[h - 1] == k) --h;
+  f.sc->first = static_cast<unsigned long long>(h);
+}
+
+}  // namespace
+}  // namespace pdlp
+
+extern "C" int pdlpk_gapd_lists(void* work, int64_t n, int64_t m, uint64_t** keys0, int32_t** slots0,
+                                uint64_t** keys1, int32_t** slots1) {
+  Work w = carve(work, n, m);
+  *keys0 = w.keys_in;
+  *slots0 = w.sel;
+  *keys1 = w.keys_out;
+  *slots1 = w.vals_out;
+  return 0;
+}
+
+extern "C" int pdlpk_gapd_stage(void* work, int64_t n, int64_t m, double* dst, cudaStream_t s) {
+  Work w = carve(work, n, m);
+  gapd_stage_kernel<<<1, 1, 0, s>>>(w, dst);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_gapd_keys(void* work, int64_t n, int64_t m, int64_t E, cudaStream_t s) {
+  Work w = carve(work, n, m);
+  if (E > 0) keys_kernel<<<ew_blocks(E), kT, 0, s>>>(w, E);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_gapd_sample(const uint64_t* keys, int64_t A, int S, double* out, cudaStream_t s) {
+  gapd_sample_kernel<<<ew_blocks(S), kT, 0, s>>>(keys, A, S, out);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_gapd_split(void* work, int64_t n, int64_t m, const uint64_t* keys,
+                                const int32_t* slots, int64_t A, uint64_t s_key,
+                                const pdlpk_red* red, double* out, cudaStream_t s) {
+  const Work w = carve(work, n, m);
+  auto f = [w, keys, slots, s_key] __device__(int64_t e, double* v) -> unsigned {
+    const uint64_t k = keys[e];
+    if (k < s_key) {
+      v[4] = 1.0;
+      return 16u;
+    }
+    const int32_t t = slots[e];
+    const double dc = w.dc[t], di = w.di[t];
+    v[2] = dc;
+    v[3] = di;
+    if (k == s_key) return 12u;
+    v[0] = dc;
+    v[1] = di;
+    return 15u;
+  };
+  return multi_reduce<5>(f, A, PDLPK_RED_TREE, red->shards, 0u, red->scratch, out, s);
+}
+
+extern "C" int pdlpk_gapd_compact(void* work, int64_t n, int64_t m, const uint64_t* keys_in,
+                                  const int32_t* slots_in, int64_t A, uint64_t lo, uint64_t hi,
+                                  uint64_t* keys_out, int32_t* slots_out, cudaStream_t s) {
+  Work w = carve(work, n, m);
+  if (A <= 0) return 0;
+  gapd_flag_kernel<<<ew_blocks(A), kT, 0, s>>>(w, keys_in, A, lo, hi);
+  size_t bytes = w.cub_bytes;
+  cudaError_t e = cub::DeviceSelect::Flagged(w.cub_tmp, bytes, keys_in, w.flag, keys_out,
+                                             &w.sc->num_high, static_cast<int>(A), s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  bytes = w.cub_bytes;
+  e = cub::DeviceSelect::Flagged(w.cub_tmp, bytes, slots_in, w.flag, slots_out, &w.sc->num_high,
+                                 static_cast<int>(A), s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_gapd_pack(void* work, int64_t n, int64_t m, const uint64_t* keys,
+                               const int32_t* slots, int64_t A, int64_t K, double* dst,
+                               cudaStream_t s) {
+  Work w = carve(work, n, m);
+  if (K > 0) gapd_pack_kernel<<<ew_blocks(K), kT, 0, s>>>(w, keys, slots, A, K, dst);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_gap_lambda_star(void* work, int64_t n, int64_t m, double* dst, cudaStream_t s) {
+  Work w = carve(work, n, m);
+  return static_cast<int>(cudaMemcpyAsync(dst, &w.sc->lambda_star, sizeof(double),
+                                          cudaMemcpyDeviceToDevice, s));
+}
+
+extern "C" size_t pdlpk_gapd_final_bytes(int64_t T) { return pdlpk_gap_work_bytes(T, 0); }
+
+extern "C" int pdlpk_gapd_final(void* fwork, int64_t cap, const double* all, int world, int64_t K,
+                                const int64_t* counts, double c0, double b0, double hi0,
+                                int lower_bounded, double r, double** lambda_star, cudaStream_t s) {
+  if (world < 1 || world > PDLPK_GAPD_MAX_RANKS) return static_cast<int>(cudaErrorInvalidValue);
+  Work f = carve(fwork, cap, 0);
+  GapdOffsets o{};
+  o.world = world;
+  o.K = K;
+  o.off[0] = 0;
+  for (int q = 0; q < world; ++q) o.off[q + 1] = o.off[q] + counts[q];
+  const int64_t T = o.off[world];
+  if (T > cap) return static_cast<int>(cudaErrorInvalidValue);
+  gapd_base_kernel<<<1, 1, 0, s>>>(f, c0, b0, hi0);
+  init_first_kernel<<<1, 1, 0, s>>>(f);
+  if (T > 0) {
+    gapd_unpack_kernel<<<ew_blocks(T), kT, 0, s>>>(f, all, o);
+    size_t bytes = f.cub_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(f.cub_tmp, bytes, f.keys_in, f.keys_out,
+                                                              f.sel, f.vals_out, static_cast<int>(T),
+                                                              0, 64, s);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    gather_masses_kernel<<<ew_blocks(T), kT, 0, s>>>(f, T);
+    bytes = f.cub_bytes;
+    cub::DeviceScan::ExclusiveSum(f.cub_tmp, bytes, f.cs, f.cs, static_cast<int>(T), s);
+    bytes = f.cub_bytes;
+    cub::DeviceScan::ExclusiveSum(f.cub_tmp, bytes, f.bs, f.bs, static_cast<int>(T), s);
+    first_hit_kernel<<<ew_blocks(T), kT, 0, s>>>(f, T, nullptr, r);
+    if (lower_bounded) gapd_force_last_kernel<<<1, 1, 0, s>>>(f, T);
+  }
+  finalize_perf_kernel<<<1, 1, 0, s>>>(f, T, nullptr, r);
+  *lambda_star = &f.sc->lambda_star;
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_gapd_value(const pdlpk_problem* P, const double* x, const double* y,
+                                const double* ax, const double* aty, double omega,
+                                const double* lambda_star, const pdlpk_red* red, double* out,
+                                cudaStream_t s) {
+  const GapIn g = make_in(P, x, y, ax, aty, omega);
+  auto fv = [g, lambda_star] __device__(int64_t t, double* v) -> unsigned {
+    v[0] = value_term(g, t, *lambda_star);
+    return 1u;
+  };
+  return multi_reduce<1>(fv, P->n + P->m, PDLPK_RED_TREE, red->shards, 0u, red->scratch, out, s);
 }

@@ -40,30 +40,62 @@ __global__ void mark_heads(const P* __restrict__ start, int64_t dim, int32_t* __
   }
 }
 
-// Each thread folds a contiguous chunk of kChunk entries with a running max
-// and flushes one atomic per line segment: a 2,000-entry line costs ~60
-// atomics instead of 2,000 on the same word.
-constexpr int kChunk = 32;
+// Line inf-norms, warp-coalesced: lane l of a warp takes entry base + l
+// (coalesced loads of the values and the line map), a segmented max over the
+// warp's 32 entries (a line is a run of equal line_of, which is
+// non-decreasing in k) leaves each run's max on its last lane, and that lane
+// does one atomicMax on the line's bits.  A 2,000-entry line costs ~63
+// atomics; order-free, so exact.
+__device__ __forceinline__ void seg_max_flush(int32_t line, unsigned long long a, bool valid,
+                                              unsigned long long* __restrict__ bits) {
+  const int lane = threadIdx.x & 31;
+  if (!valid) line = -1 - lane;  // never joins a run
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, a, o);
+    const int32_t tl = __shfl_up_sync(0xffffffffu, line, o);
+    if (lane >= o && tl == line) a = t > a ? t : a;
+  }
+  const int32_t next = __shfl_down_sync(0xffffffffu, line, 1);
+  if (valid && (lane == 31 || next != line)) atomicMax(bits + line, a);
+}
+
+__device__ __forceinline__ unsigned long long abs_bits(double v) {
+  return static_cast<unsigned long long>(__double_as_longlong(fabs(v)));
+}
+
+#define WARP_STRIDE(base, n)                                                                    \
+  for (int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~int64_t(31); \
+       base < (n); base += static_cast<int64_t>(gridDim.x) * blockDim.x)
 
 __global__ void absmax_kernel(const double* __restrict__ val, const int32_t* __restrict__ line_of,
                               int64_t nnz, unsigned long long* __restrict__ bits) {
-  const int64_t chunks = (nnz + kChunk - 1) / kChunk;
-  GRID_STRIDE(ch, chunks) {
-    const int64_t k0 = ch * kChunk;
-    const int64_t k1 = k0 + kChunk < nnz ? k0 + kChunk : nnz;
-    int32_t line = line_of[k0];
-    unsigned long long mx = 0;
-    for (int64_t k = k0; k < k1; ++k) {
-      const int32_t l = line_of[k];
-      const unsigned long long a = static_cast<unsigned long long>(__double_as_longlong(fabs(val[k])));
-      if (l != line) {
-        atomicMax(bits + line, mx);
-        line = l;
-        mx = 0;
-      }
-      mx = a > mx ? a : mx;
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(base, nnz) {
+    const int64_t k = base + lane;
+    const bool valid = k < nnz;
+    seg_max_flush(valid ? line_of[k] : 0, valid ? abs_bits(val[k]) : 0ull, valid, bits);
+  }
+}
+
+// One Ruiz pass's division (apply_elem) fused with the next pass's line
+// inf-norms of the result (bits_next != nullptr).
+__global__ void apply_max_kernel(double* __restrict__ val, const int32_t* __restrict__ idx,
+                                 const int32_t* __restrict__ line_of, int64_t nnz,
+                                 const double* __restrict__ fp, const double* __restrict__ fs,
+                                 unsigned long long* __restrict__ bits_next) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(base, nnz) {
+    const int64_t k = base + lane;
+    const bool valid = k < nnz;
+    int32_t line = 0;
+    double v = 0.0;
+    if (valid) {
+      line = line_of[k];
+      v = val[k] / (fp[line] * fs[idx[k]]);
+      val[k] = v;
     }
-    atomicMax(bits + line, mx);
+    if (bits_next != nullptr) seg_max_flush(line, valid ? abs_bits(v) : 0ull, valid, bits_next);
   }
 }
 
@@ -170,9 +202,38 @@ extern "C" int pdlpk_line_factors(const pdlpk_csr* A, const int32_t* line_of, in
   }
   cudaMemsetAsync(bits, 0, A->dim * sizeof(unsigned long long), s);
   if (A->nnz > 0) {
-    absmax_kernel<<<ew_blocks((A->nnz + kChunk - 1) / kChunk), kT, 0, s>>>(A->value, line_of, A->nnz, bits);
+    absmax_kernel<<<ew_blocks(A->nnz), kT, 0, s>>>(A->value, line_of, A->nnz, bits);
   }
   factor_from_bits<<<ew_blocks(A->dim), kT, 0, s>>>(bits, A->dim, f);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Ruiz on one GPU (Engine::precondition): the line inf-norms of both layouts
+// once, then per pass factors from the bits and the fused division + next
+// norms.  Same maxima, same divisions as line_factors + apply_factors.
+extern "C" int pdlpk_line_absmax(const pdlpk_csr* A, const int32_t* line_of,
+                                 unsigned long long* bits, cudaStream_t s) {
+  if (A->dim == 0) return 0;
+  cudaMemsetAsync(bits, 0, A->dim * sizeof(unsigned long long), s);
+  if (A->nnz > 0) absmax_kernel<<<ew_blocks(A->nnz), kT, 0, s>>>(A->value, line_of, A->nnz, bits);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_factors_from_bits(const unsigned long long* bits, int64_t dim, double* f,
+                                       cudaStream_t s) {
+  if (dim > 0) factor_from_bits<<<ew_blocks(dim), kT, 0, s>>>(bits, dim, f);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_apply_factors_max(const pdlpk_csr* A, const int32_t* line_of, double* value,
+                                       const double* f_primary, const double* f_secondary,
+                                       unsigned long long* bits_next, cudaStream_t s) {
+  if (bits_next != nullptr && A->dim > 0) {
+    cudaMemsetAsync(bits_next, 0, A->dim * sizeof(unsigned long long), s);
+  }
+  if (A->nnz == 0) return static_cast<int>(cudaGetLastError());
+  apply_max_kernel<<<ew_blocks(A->nnz), kT, 0, s>>>(value, A->index, line_of, A->nnz, f_primary,
+                                                   f_secondary, bits_next);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -200,7 +261,7 @@ extern "C" int pdlpk_line_norms(const pdlpk_csr* A, const int32_t* line_of, int3
   }
   cudaMemsetAsync(bits, 0, A->dim * sizeof(unsigned long long), s);
   if (A->nnz > 0) {
-    absmax_kernel<<<ew_blocks((A->nnz + kChunk - 1) / kChunk), kT, 0, s>>>(A->value, line_of, A->nnz, bits);
+    absmax_kernel<<<ew_blocks(A->nnz), kT, 0, s>>>(A->value, line_of, A->nnz, bits);
   }
   bits_to_norm<<<ew_blocks(A->dim), kT, 0, s>>>(bits, A->dim, norm);
   return static_cast<int>(cudaGetLastError());

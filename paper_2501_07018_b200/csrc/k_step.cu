@@ -732,7 +732,8 @@ struct LaunchRowCol {
           launch_pdl(pdl, row_pass<P, Seg, 0>, gu, kSpmvThreads, smem, s, *a);
       }
     } else {
-      if (decide_here && PDLPK_COL_SPLIT && A.seg_mode) {
+      if (decide_here && ((PDLPK_COL_SPLIT && A.seg_mode) || A.col_split)) {
+        allow_smem(col_product<P, Seg>, smem);
         launch_pdl(pdl, col_product<P, Seg>, gu, kSpmvThreads, smem, s, *a);
         launch_pdl(pdl, col_epi_decide, static_cast<unsigned>(ew_blocks(a->P.n)), kEwThreads,
                    static_cast<size_t>(0), s, *a);
@@ -908,7 +909,7 @@ extern "C" int64_t pdlpk_step_partials(const pdlpk_problem* P) {
   const int64_t g2 = sched_blocks(P->K), g3 = sched_blocks(P->KT);
   int64_t need = 2 * g2 > 3 * g3 ? 2 * g2 : 3 * g3;
   const int64_t ge = 3 * static_cast<int64_t>(ew_blocks(P->n));  // split column pass
-  if (P->KT.seg_mode && ge > need) need = ge;
+  if ((P->KT.seg_mode || P->KT.col_split) && ge > need) need = ge;
   if (P->m <= PDLPK_LINE_PARTIALS_MAX && 2 * P->m > need) need = 2 * P->m;  // line_partials
   return need + 64;
 }

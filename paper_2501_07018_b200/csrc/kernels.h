@@ -79,6 +79,11 @@ typedef struct pdlpk_csr {
   const int32_t* seg_step0;
   const uint32_t* seg_masks;
   int64_t n_seg_spans;
+  /* 1: a column pass over this layout (the dual polishing subproblem's K^T
+   * is the row layout) takes the split form, whose partials follow the line
+   * index: set on row layouts whose warp lines may run interleaved
+   * (solver.cpp build_schedule), so results do not depend on the order. */
+  int32_t col_split;
 } pdlpk_csr;
 
 #define PDLPK_DIST_NONE 0
@@ -441,6 +446,47 @@ int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const double* y, c
                      double qb, cudaStream_t s);
 /* Window sorts tried / decided on this host thread (cumulative). */
 void pdlpk_gap_window_stats(int64_t* tried, int64_t* decided);
+
+/* Distributed gap (row-sharded solves, k_gap.cu; the host drives the bracket
+ * search, solver.cpp Engine::gap_dist).  After pdlpk_gap_prepare on the
+ * rank's local views (work sized for the local n, m):
+ *   stage    dst[0..2] = local b_inf, c_inf, event count
+ *   keys     the E local events' order keys into list 0 (keys0 / slots0)
+ *   lists    the two ping-pong bracket lists (keys, event slots) inside work
+ *   sample   out[0..S) = S strided keys of a list (bit patterns), out[S] = taken
+ *   split    out[0..4] = masses (c, b) of list events with key > s_key, with
+ *            key >= s_key, and the count with key < s_key (TREE order)
+ *   compact  the list events with lo <= key <= hi into the other list
+ *   pack     dst[0..3K) = keys | d_const | d_inverse of a list, zero padded
+ *   final    rank-ordered concatenation of `world` packed blocks (counts[q]
+ *            events each), stable descending sort, sweep from the masses
+ *            (c0, b0) above the bracket and hi0 = lambda of the group above
+ *            it; lower_bounded: the bracket's lowest group is known to cross.
+ *            *lambda_star -> the device scalar.  fwork holds
+ *            pdlpk_gapd_final_bytes(cap) bytes, cap >= total events.
+ *   value    this rank's partial of gap_value_at at *lambda_star (TREE). */
+#define PDLPK_GAPD_MAX_RANKS 64
+int pdlpk_gapd_stage(void* work, int64_t n, int64_t m, double* dst, cudaStream_t s);
+int pdlpk_gapd_keys(void* work, int64_t n, int64_t m, int64_t E, cudaStream_t s);
+int pdlpk_gapd_lists(void* work, int64_t n, int64_t m, uint64_t** keys0, int32_t** slots0,
+                     uint64_t** keys1, int32_t** slots1);
+int pdlpk_gapd_sample(const uint64_t* keys, int64_t A, int S, double* out, cudaStream_t s);
+int pdlpk_gapd_split(void* work, int64_t n, int64_t m, const uint64_t* keys, const int32_t* slots,
+                     int64_t A, uint64_t s_key, const pdlpk_red* red, double* out, cudaStream_t s);
+int pdlpk_gapd_compact(void* work, int64_t n, int64_t m, const uint64_t* keys_in,
+                       const int32_t* slots_in, int64_t A, uint64_t lo, uint64_t hi,
+                       uint64_t* keys_out, int32_t* slots_out, cudaStream_t s);
+int pdlpk_gapd_pack(void* work, int64_t n, int64_t m, const uint64_t* keys, const int32_t* slots,
+                    int64_t A, int64_t K, double* dst, cudaStream_t s);
+size_t pdlpk_gapd_final_bytes(int64_t T);
+/* *dst (device) = lambda* of the last gap evaluated in `work` (checks). */
+int pdlpk_gap_lambda_star(void* work, int64_t n, int64_t m, double* dst, cudaStream_t s);
+int pdlpk_gapd_final(void* fwork, int64_t cap, const double* all, int world, int64_t K,
+                     const int64_t* counts, double c0, double b0, double hi0, int lower_bounded,
+                     double r, double** lambda_star, cudaStream_t s);
+int pdlpk_gapd_value(const pdlpk_problem* P, const double* x, const double* y, const double* ax,
+                     const double* aty, double omega, const double* lambda_star,
+                     const pdlpk_red* red, double* out, cudaStream_t s);
 /* slot = sqrt(omega*dx2 + dy2/omega) from two slots (restart_progress_metric). */
 int pdlpk_radius(const double* dx2, const double* dy2, double omega, double* out,
                  cudaStream_t s);
@@ -457,6 +503,16 @@ int pdlpk_line_factors(const pdlpk_csr* A, const int32_t* line_of, int32_t one_n
 /* value /= f_primary[line] * f_secondary[index] for one layout. */
 int pdlpk_apply_factors(const pdlpk_csr* A, const int32_t* line_of, double* value,
                         const double* f_primary, const double* f_secondary, cudaStream_t s);
+/* Ruiz passes on one GPU: bits[line] = max |v| of the layout's lines
+ * (order-free, exact); f = sqrt(max) or 1 from them; the division of
+ * apply_factors fused with the next pass's bits of the result
+ * (bits_next == NULL: the division alone). */
+int pdlpk_line_absmax(const pdlpk_csr* A, const int32_t* line_of, unsigned long long* bits,
+                      cudaStream_t s);
+int pdlpk_factors_from_bits(const unsigned long long* bits, int64_t dim, double* f, cudaStream_t s);
+int pdlpk_apply_factors_max(const pdlpk_csr* A, const int32_t* line_of, double* value,
+                            const double* f_primary, const double* f_secondary,
+                            unsigned long long* bits_next, cudaStream_t s);
 /* Vector part of apply_factors (rescaling.hpp:61-73). */
 int pdlpk_apply_vec_factors(double* lc, double* uc, double* row_scale, const double* fr,
                             int64_t m, double* c, double* lv, double* uv, double* col_scale,

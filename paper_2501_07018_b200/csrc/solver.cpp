@@ -165,6 +165,24 @@ bool direct_tiles(const int64_t* start, int64_t dim) {
 
 // Set around the row layout's upload (Engine::load_parts).
 thread_local bool g_interleave_warp_lines = false;
+// The row layout of a solve whose warp lines may be interleaved (whether or
+// not PDLP_NO_INTERLEAVE turns it off): column passes over it (the dual
+// polishing subproblem) take the split form in both cases.
+thread_local bool g_col_split_layout = false;
+
+// Distributed-gap counters (pdlp_gap_dist_stats): evaluations, bisection
+// rounds, events swept after the search, and -- with PDLP_GAPD_CHECK=1 --
+// the largest relative difference from the gathered evaluation.
+struct GapDistStats {
+  std::mutex mu;
+  int64_t evals = 0, rounds = 0, final_events = 0, checked = 0;
+  double max_rel = 0.0, max_rel_lambda = 0.0;
+};
+GapDistStats& gapd_stats() {
+  static GapDistStats g;
+  return g;
+}
+
 
 // Line segments of a schedule build: [lo, hi) line ranges built by host
 // threads (fixed boundaries, so the schedule is deterministic) and joined in
@@ -435,6 +453,7 @@ void build_schedule(const int64_t* start, int64_t dim, DevLayout& L,
   L.view.n_tiles = n_tiles;
   L.view.tile_direct = direct ? 1 : 0;
   L.view.seg_mode = 0;
+  L.view.col_split = g_col_split_layout ? 1 : 0;
   L.view.tile_lines_cap = static_cast<int32_t>(tile_rows);
   L.view.tile_nnz_cap = static_cast<int32_t>(tile_nnz);
   L.view.tile_stage_bytes = stage_bytes;
@@ -650,13 +669,14 @@ void upload_layout(const pdlp_csr_view& v, int64_t bound, unsigned* bad, DevLayo
   std::exception_ptr sched_err;
   int dev = 0;
   PDLP_CK(cudaGetDevice(&dev));
-  const bool interleave = g_interleave_warp_lines;
+  const bool interleave = g_interleave_warp_lines, col_split = g_col_split_layout;
   const cudaStream_t ss = schedule_stream();
-  std::thread sched([&, dev, interleave, ss] {
+  std::thread sched([&, dev, interleave, col_split, ss] {
     try {
       PDLP_CK(cudaSetDevice(dev));
       AllocStreamScope scope(ss);
       g_interleave_warp_lines = interleave;
+      g_col_split_layout = col_split;
       autotune_schedule(v.start, dim, bound, L, ss, bad);
       PDLP_CK(cudaStreamSynchronize(ss));
     } catch (...) {
@@ -937,28 +957,36 @@ class Engine {
       // rank passes its own shard; the plan was checked against
       // pdlp_shard_plan_for by the entry point.)
       ShardData sh;
-      if (shard_in_ == nullptr) extract_shard(*p, comm_->rank(), comm_->world(), sh);
+      if (shard_in_ == nullptr) {
+        extract_shard(*p, comm_->rank(), comm_->world(), auto_cut(p->rows, p->cols), sh);
+      }
       const pdlp_shard_view& v = shard_in_ != nullptr ? *shard_in_ : sh.view;
       flag_.alloc(8);
       plan_ = v.plan;
       m_glob_ = plan_.rows;
       n_glob_ = plan_.cols;
+      shard_rows_ = &v.rows;
+      shard_row_entry_offset_ = v.row_entry_offset;
       load_parts(v.rows, v.cols, plan_.row_end - plan_.row_begin, plan_.col_end - plan_.col_begin,
                  v.objective, v.con_lower, v.con_upper, v.var_lower, v.var_upper, plan_.row_begin,
                  plan_.col_begin, v.entry_offset);
-      prob_.row.view.dist_kind = PDLPK_DIST_GATHER;
-      prob_.col.view.dist_kind = PDLPK_DIST_PARTIAL;
-      gbuf_.alloc(full_cols());
-      pbuf_.alloc(full_cols());
-      dev_zero(gbuf_.get(), full_cols(), s());
-      dev_zero(pbuf_.get(), full_cols(), s());
+      shard_rows_ = nullptr;
+      // the row cut gathers x-bar (K_g) and reduce-scatters K_g^T's partial
+      // output; the column cut reduce-scatters K_g's partial row sums and
+      // gathers dy (K_g^T)
+      prob_.row.view.dist_kind = cols_cut() ? PDLPK_DIST_PARTIAL : PDLPK_DIST_GATHER;
+      prob_.col.view.dist_kind = cols_cut() ? PDLPK_DIST_GATHER : PDLPK_DIST_PARTIAL;
+      gbuf_.alloc(xch_full());
+      pbuf_.alloc(xch_full());
+      dev_zero(gbuf_.get(), xch_full(), s());
+      dev_zero(pbuf_.get(), xch_full(), s());
       const char* pe = std::getenv("PDLP_PEER_RS");
       const int w = comm_->world();
       if (w > 1 && w <= PDLPK_MAX_PEERS && !(pe != nullptr && pe[0] == '0')) {
-        peer_pbuf_ = comm_->alloc_peer_buffer(static_cast<size_t>(full_cols()));
-        peer_gather_ = comm_->alloc_peer_buffer(static_cast<size_t>(full_cols()));
-        dev_zero(peer_pbuf_, full_cols(), s());
-        dev_zero(peer_gather_, full_cols(), s());
+        peer_pbuf_ = comm_->alloc_peer_buffer(static_cast<size_t>(xch_full()));
+        peer_gather_ = comm_->alloc_peer_buffer(static_cast<size_t>(xch_full()));
+        dev_zero(peer_pbuf_, xch_full(), s());
+        dev_zero(peer_gather_, xch_full(), s());
         const std::vector<double*> ptrs = comm_->peer_pointers(peer_pbuf_, s());
         const std::vector<double*> gptrs = comm_->peer_pointers(peer_gather_, s());
         // every rank must take the same path: fall back together if any
@@ -974,7 +1002,7 @@ class Engine {
         } else {
           const int rank = comm_->rank();
           peers_.world = push_.world = w;
-          peers_.offset = push_.offset = plan_.col_block * rank;
+          peers_.offset = push_.offset = xch_block() * rank;
           for (int r = 0; r < w; ++r) {
             peers_.p[r] = ptrs[r];
             push_.p[r] = r == rank ? nullptr : gptrs[r];
@@ -1013,11 +1041,16 @@ class Engine {
     PDLP_CK(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned), s()));
     {
       const char* e = std::getenv("PDLP_NO_INTERLEAVE");
-      g_interleave_warp_lines = comm_ == nullptr && m <= PDLPK_LINE_PARTIALS_MAX &&
-                                line_partials_on_ && !(e != nullptr && e[0] == '1');
+      g_col_split_layout = comm_ == nullptr && m <= PDLPK_LINE_PARTIALS_MAX && line_partials_on_;
+      g_interleave_warp_lines = g_col_split_layout && !(e != nullptr && e[0] == '1');
     }
-    upload_layout(by_row, n_glob_, bad.get(), prob_.row, s());
+    // index bounds: the row layout indexes columns (all n, or the block's
+    // under the column cut), the column layout rows (the block's under the
+    // row cut, all m under the column cut)
+    const bool cc = comm_ != nullptr && cols_cut();
+    upload_layout(by_row, cc ? n : n_glob_, bad.get(), prob_.row, s());
     g_interleave_warp_lines = false;
+    g_col_split_layout = false;
     // the multi-product span schedule of the row layout: built on a second
     // host thread while the column layout uploads
     std::exception_ptr multi_err;
@@ -1039,7 +1072,7 @@ class Engine {
     } multi_guard{multi_thread};
     start_panel_plan(by_row, n_glob_);
     const double t_row = lap();
-    upload_layout(by_col, m, bad.get(), prob_.col, s());
+    upload_layout(by_col, cc ? m_glob_ : m, bad.get(), prob_.col, s());
     multi_thread.join();
     if (multi_err) std::rethrow_exception(multi_err);
     const double t_col = lap();
@@ -1060,7 +1093,10 @@ class Engine {
       PDLP_CK(cudaMemcpyAsync(hk, keys.get(), sizeof(hk), cudaMemcpyDeviceToHost, s()));
       PDLP_CK(cudaMemcpyAsync(&hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, s()));
       PDLP_CK(cudaStreamSynchronize(s()));
-      if (comm_ != nullptr) combine_validation(hk, hb, r0, c0, e0);
+      if (comm_ != nullptr) {
+        if (cc && hk[3] != ~0ull) hk[3] = col_cut_entry(hk[3]);
+        combine_validation(hk, hb, r0, c0, cc ? 0 : e0);
+      }
       static const char* var_msg[] = {"", "variable bound is NaN", "variable lower bound is +inf",
                                       "variable upper bound is -inf", "variable bounds crossed"};
       static const char* con_msg[] = {"", "constraint bound is NaN",
@@ -1082,7 +1118,7 @@ class Engine {
       DevBuf<char> work(work_bytes);
       PDLP_LAUNCH(pdlpk_line_of(&prob_.row.view, row_of_.get(), work.get(), work_bytes, s()));
       PDLP_LAUNCH(pdlpk_line_of(&prob_.col.view, col_of_.get(), work.get(), work_bytes, s()));
-      DevBuf<int> row_count(std::max<int64_t>(m, 1));
+      DevBuf<int> row_count(std::max<int64_t>(prob_.row.view.dim, 1));
       PDLP_LAUNCH(pdlpk_validate_consistency(&prob_.row.view, row_of_.get(), &prob_.col.view,
                                              col_of_.get(), row_count.get(), bad.get(), s()));
       unsigned hb = 0;
@@ -1111,7 +1147,10 @@ class Engine {
     // Two buffers let both gap queries of a cadence share one sync; above
     // 1 GB each (C4-shard sizes: 24 GB) one buffer is reused query by query.
     {
-      const size_t gw = std::max(pdlpk_gap_work_bytes(n_glob_, m_glob_), pdlpk_gap_work_bytes(m_glob_, n_glob_));
+      // whole-problem events on one GPU (and for the gathered evaluation);
+      // a sharded solve's distributed gap only holds the rank's blocks
+      const int64_t gn = gap_whole() ? n_glob_ : n, gm = gap_whole() ? m_glob_ : m;
+      const size_t gw = std::max(pdlpk_gap_work_bytes(gn, gm), pdlpk_gap_work_bytes(gm, gn));
       gap_shared_ = gw > (size_t(1) << 30);
       gap_work_[0].alloc(gw);
       if (!gap_shared_) gap_work_[1].alloc(gw);
@@ -1176,6 +1215,16 @@ class Engine {
   // ---- row-sharded plumbing (comm_ != nullptr) ---------------------------
   bool dist() const { return comm_ != nullptr; }
   int64_t full_cols() const { return plan_.col_block * comm_->world(); }
+  // The dimension a sharded attempt exchanges: columns for the row cut
+  // (x-bar gathered, K^T's output reduce-scattered), rows for the column cut
+  // (K's output reduce-scattered, dy gathered).  The dual polishing
+  // subproblem swaps the layouts' roles and exchanges the same dimension.
+  bool cols_cut() const { return plan_.cut == PDLP_CUT_COLS; }
+  int64_t xch_block() const { return cols_cut() ? plan_.row_block : plan_.col_block; }
+  int64_t xch_full() const { return xch_block() * comm_->world(); }
+  int64_t xch_local() const {
+    return cols_cut() ? plan_.row_end - plan_.row_begin : plan_.col_end - plan_.col_begin;
+  }
   int64_t full_rows() const { return plan_.row_block * comm_->world(); }
   int64_t full_len() const { return std::max<int64_t>(std::max(full_cols(), full_rows()), 1); }
 
@@ -1233,8 +1282,8 @@ class Engine {
       PDLP_LAUNCH(pdlpk_spmv(&L, orig, in, out, parity_, s()));
       return;
     }
-    const int64_t nb = plan_.col_block;
-    const int64_t nloc = plan_.col_end - plan_.col_begin;
+    const int64_t nb = xch_block();
+    const int64_t nloc = xch_local();
     if (L.dist_kind == PDLPK_DIST_GATHER) {
       gather(in, nloc, nb, gbuf_.get());
       PDLP_LAUNCH(pdlpk_spmv(&L, orig, gbuf_.get(), out, 0, s()));
@@ -1300,7 +1349,7 @@ class Engine {
   // collectives (K partial + RS, K^T gathered).
   void attempt_dist(const pdlpk_problem& P, Inner& D, const pdlpk_step_args& a) {
     const int rank = comm_->rank();
-    const int64_t nb = plan_.col_block;
+    const int64_t nb = xch_block();
     const bool kg = P.K.dist_kind == PDLPK_DIST_GATHER;
     const bool ktg = P.KT.dist_kind == PDLPK_DIST_GATHER;
     // x-bar is only read inside an attempt, so one peer-mappable gathered
@@ -1436,15 +1485,42 @@ class Engine {
   void precondition(int ruiz_passes, bool pock_chambolle) {
     const auto t0 = Clock::now();
     const int64_t m = prob_.m, n = prob_.n;
-    // fc spans every column of the layouts (all n when sharded)
-    DevBuf<double> fr(m), fc(n_glob_);
-    DevBuf<unsigned long long> bits(std::max<int64_t>(std::max(m, n_glob_), 1));
-    const int64_t c0 = dist() ? plan_.col_begin : 0;
+    // fc spans every column of the layouts (all n under the row cut), fr
+    // every row (all m under the column cut)
+    const bool cc = dist() && cols_cut();
+    const int64_t mr = cc ? m_glob_ : m, nc = cc ? n : n_glob_;
+    DevBuf<double> fr(std::max<int64_t>(mr, 1)), fc(std::max<int64_t>(nc, 1));
+    DevBuf<unsigned long long> bits(std::max<int64_t>(std::max(mr, nc), 1));
+    const int64_t c0 = dist() && !cc ? plan_.col_begin : 0;
+    const int64_t r0 = cc ? plan_.row_begin : 0;
     const int64_t nnz = prob_.row.view.nnz;
     (void)nnz;
     const DevBuf<int32_t>& row_of = row_of_;  // line maps built during validation
     const DevBuf<int32_t>& col_of = col_of_;
     auto pass = [&](int one_norm) {
+      if (cc) {
+        // column cut: the transpose of the row cut's combine -- a rank holds
+        // one consecutive run (its columns) of every row: row inf-norms
+        // max-combined, row 1-norms chained rank by rank, column norms local
+        PDLP_LAUNCH(pdlpk_line_factors(&prob_.col.view, col_of.get(), one_norm, fc.get(), bits.get(), s()));
+        if (one_norm == 0) {
+          PDLP_LAUNCH(pdlpk_line_norms(&prob_.row.view, row_of.get(), 0, fr.get(), bits.get(), s()));
+          comm_->allreduce(fr.get(), static_cast<size_t>(m_glob_), true, s());
+        } else {
+          dev_zero(fr.get(), m_glob_, s());
+          for (int r = 0; r < comm_->world(); ++r) {
+            if (r == comm_->rank()) PDLP_LAUNCH(pdlpk_line_onenorm_continue(&prob_.row.view, fr.get(), s()));
+            comm_->allreduce(fr.get(), static_cast<size_t>(m_glob_), true, s());
+          }
+        }
+        PDLP_LAUNCH(pdlpk_norm_to_factor(fr.get(), m_glob_, s()));
+        PDLP_LAUNCH(pdlpk_apply_factors(&prob_.row.view, row_of.get(), prob_.row.value.get(), fr.get(), fc.get(), s()));
+        PDLP_LAUNCH(pdlpk_apply_factors(&prob_.col.view, col_of.get(), prob_.col.value.get(), fc.get(), fr.get(), s()));
+        PDLP_LAUNCH(pdlpk_apply_vec_factors(prob_.lc.get(), prob_.uc.get(), prob_.row_scale.get(),
+                                            fr.get() + r0, m, prob_.c.get(), prob_.lv.get(),
+                                            prob_.uv.get(), prob_.col_scale.get(), fc.get(), n, s()));
+        return;
+      }
       PDLP_LAUNCH(pdlpk_line_factors(&prob_.row.view, row_of.get(), one_norm, fr.get(), bits.get(), s()));
       if (dist()) {
         // A rank holds one consecutive run (its rows) of every column.
@@ -1472,7 +1548,28 @@ class Engine {
                                           fr.get(), m, prob_.c.get(), prob_.lv.get(),
                                           prob_.uv.get(), prob_.col_scale.get(), fc.get() + c0, n, s()));
     };
-    for (int p = 0; p < ruiz_passes; ++p) pass(0);
+    if (!dist() && ruiz_passes > 0) {
+      // one GPU: both layouts' line inf-norms once, then each pass divides
+      // and takes the next pass's norms of the result in the same sweep
+      // (same maxima, same divisions as pass(0))
+      DevBuf<unsigned long long> bc(std::max<int64_t>(n, 1));
+      PDLP_LAUNCH(pdlpk_line_absmax(&prob_.row.view, row_of.get(), bits.get(), s()));
+      PDLP_LAUNCH(pdlpk_line_absmax(&prob_.col.view, col_of.get(), bc.get(), s()));
+      for (int p = 0; p < ruiz_passes; ++p) {
+        const bool more = p + 1 < ruiz_passes;
+        PDLP_LAUNCH(pdlpk_factors_from_bits(bits.get(), m, fr.get(), s()));
+        PDLP_LAUNCH(pdlpk_factors_from_bits(bc.get(), n, fc.get(), s()));
+        PDLP_LAUNCH(pdlpk_apply_factors_max(&prob_.row.view, row_of.get(), prob_.row.value.get(),
+                                            fr.get(), fc.get(), more ? bits.get() : nullptr, s()));
+        PDLP_LAUNCH(pdlpk_apply_factors_max(&prob_.col.view, col_of.get(), prob_.col.value.get(),
+                                            fc.get(), fr.get(), more ? bc.get() : nullptr, s()));
+        PDLP_LAUNCH(pdlpk_apply_vec_factors(prob_.lc.get(), prob_.uc.get(), prob_.row_scale.get(),
+                                            fr.get(), m, prob_.c.get(), prob_.lv.get(),
+                                            prob_.uv.get(), prob_.col_scale.get(), fc.get(), n, s()));
+      }
+    } else {
+      for (int p = 0; p < ruiz_passes; ++p) pass(0);
+    }
     if (pock_chambolle) pass(1);
     PDLP_CK(cudaStreamSynchronize(s()));
     precondition_seconds_ = std::chrono::duration<double>(Clock::now() - t0).count();
@@ -1574,7 +1671,7 @@ class Engine {
     }
     if (D.n != P.n || D.m != P.m || static_cast<int64_t>(D.part2.size()) < partials) {
       if (dist()) {
-        D.allocate(P.n, P.m, partials, shards_, full_cols(), plan_.col_block, comm_->world());
+        D.allocate(P.n, P.m, partials, shards_, xch_full(), xch_block(), comm_->world());
       } else {
         D.allocate(P.n, P.m, partials, shards_);
       }
@@ -1897,10 +1994,48 @@ class Engine {
       Clock::time_point t0;
       ~GapClock() { acc += std::chrono::duration<double>(Clock::now() - t0).count(); }
     } gap_clock{gap_seconds_, gap_t0};
+    if (dist() && !gap_gathered_) {
+      combine_logged();  // nothing may stay pending across the unlogged gap
+      pdlpk_set_red_log(nullptr);
+      for (int i = 0; i < count; ++i) out[i] = gap_dist(P, q[i], omega, i);
+      pdlpk_set_red_log(&red_log_);
+      if (gap_check_) {
+        // the same evaluations on gathered vectors: lambda* (which the
+        // crossing decides) and the gap value (a cancelling sum whose
+        // rounding follows the summation order)
+        double lam_d[2] = {gapd_lambda_[0], gapd_lambda_[1]}, ref[2], lam_g[2];
+        gaps_gathered(cfg, P, q, count, omega, ref);
+        for (int i = 0; i < count; ++i) {
+          void* w = gap_work_[gap_shared_ ? 0 : i].get();
+          PDLP_LAUNCH(pdlpk_gap_lambda_star(w, cfg.full->n, cfg.full->m, slot(kSlotGap + i), s()));
+        }
+        const double* hl = read_slots(kSlotGap + count);
+        for (int i = 0; i < count; ++i) lam_g[i] = hl[kSlotGap + i];
+        std::lock_guard<std::mutex> lk(gapd_stats().mu);
+        auto rel = [](double a, double b) {
+          return a == b ? 0.0 : std::fabs(a - b) / std::max(std::fabs(b), 1e-300);
+        };
+        for (int i = 0; i < count; ++i) {
+          gapd_stats().max_rel = std::max(gapd_stats().max_rel, rel(out[i], ref[i]));
+          gapd_stats().max_rel_lambda = std::max(gapd_stats().max_rel_lambda, rel(lam_d[i], lam_g[i]));
+          ++gapd_stats().checked;
+        }
+      }
+      return;
+    }
     if (dist()) {
-      // Sharded: every rank evaluates the same whole-problem gap on gathered
-      // vectors (identical inputs -> identical mu everywhere); the cadence
-      // runs it 2-3 times per 64 steps.
+      gaps_gathered(cfg, P, q, count, omega, out);
+      return;
+    }
+    gaps_local(P, q, count, omega, out);
+  }
+
+  // Sharded, PDLP_GAP_GATHERED=1 (and the PDLP_GAPD_CHECK comparison): every
+  // rank evaluates the same whole-problem gap on gathered vectors
+  // (identical inputs -> identical mu everywhere).
+  void gaps_gathered(const InnerCfg& cfg, const pdlpk_problem& P, const GapQuery* q, int count,
+                     double omega, double* out) {
+    {
       const int64_t nb = plan_.col_block, mb = plan_.row_block;
       const int64_t xb = cfg.swapped ? mb : nb, yb = cfg.swapped ? nb : mb;
       GapQuery g[2];
@@ -1915,9 +2050,182 @@ class Engine {
       pdlpk_set_red_log(nullptr);
       gaps_local(*cfg.full, g, count, omega, out);
       pdlpk_set_red_log(&red_log_);
-      return;
     }
-    gaps_local(P, q, count, omega, out);
+  }
+
+  // ---- distributed normalized gap ---------------------------
+  // normalized_duality_gap (restarts.hpp:107-220) over the row-sharded
+  // problem without gathering a vector: each rank builds the breakpoint
+  // events of its own column and row blocks; the reference's sequential
+  // sweep is replaced by a bracket search over the global descending order
+  // of the events.  A round picks a key s (weighted median of a strided key
+  // sample of every rank's bracket), every rank reduces the masses of its
+  // bracket events above / at-or-above s and counts those below, the ranks'
+  // values are added in rank order, and phi(s) = C + B / lam(s)^2 (the
+  // sweep's test at s) keeps the half that holds the first crossing: phi is
+  // monotone in lam, so phi(s) >= r^2 means the crossing is s or above it,
+  // else it is below s and the masses of [s, hi] join the base (C, B).  When
+  // the bracket is small its events are all-gathered and swept by the
+  // single-GPU kernels; lambda*, the candidate and the gap value follow from
+  // the local blocks and one more all-gather.  Every decision depends only
+  // on all-gathered values, so every rank takes the same branch and returns
+  // the same gap.  Communication per round: two all-gathers of 40 and 8
+  // doubles per rank.
+  static double host_key_value(uint64_t k) {
+    const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double d;
+    std::memcpy(&d, &b, sizeof(d));
+    return d;
+  }
+  static uint64_t bits_of(double d) {
+    uint64_t b;
+    std::memcpy(&b, &d, sizeof(b));
+    return b;
+  }
+  double* gapd_block(int64_t per_rank) {
+    const int64_t need = per_rank * comm_->world();
+    if (static_cast<int64_t>(gapd_buf_.size()) < need) gapd_buf_.alloc(need);
+    return gapd_buf_.get();
+  }
+  // all-gather blocks of `count` doubles of gapd_buf_ and read them back
+  const std::vector<double>& gapd_exchange(int64_t count) {
+    comm_->allgather(gapd_buf_.get(), static_cast<size_t>(count), s());
+    gapd_host_.resize(static_cast<size_t>(count * comm_->world()));
+    PDLP_CK(cudaMemcpyAsync(gapd_host_.data(), gapd_buf_.get(), gapd_host_.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));
+    return gapd_host_;
+  }
+
+  double gap_dist(const pdlpk_problem& P, const GapQuery& q, double omega, int qi) {
+    const int W = comm_->world(), R = comm_->rank();
+    const double radius = std::sqrt(omega * q.dx2 + q.dy2 / omega);
+    gapd_lambda_[qi] = 0.0;
+    if (!(radius > 0.0)) return 0.0;  // restarts.hpp:112
+    const double r2 = radius * radius;
+    const pdlpk_red rd = red();
+    void* work = gap_work_[0].get();
+    const int64_t n = P.n, m = P.m;
+    constexpr int kS = 32;     // sampled keys per rank and round
+    constexpr int kBlk = 40;   // doubles per rank of a sample exchange
+    PDLP_LAUNCH(pdlpk_gap_prepare(&P, q.x, q.y, q.ax, q.aty, omega, &rd, work, nullptr, s()));
+    double* blk = gapd_block(kBlk);
+    PDLP_LAUNCH(pdlpk_gapd_stage(work, n, m, blk + 8 * R, s()));
+    const std::vector<double>* h = &gapd_exchange(8);
+    double B = 0.0, C = 0.0;  // masses above the bracket (incl. lam -> inf)
+    std::vector<int64_t> A(W), An(W);
+    int64_t At = 0;
+    for (int r = 0; r < W; ++r) {
+      B += (*h)[8 * r];
+      C += (*h)[8 * r + 1];
+      A[r] = static_cast<int64_t>((*h)[8 * r + 2]);
+      At += A[r];
+    }
+    PDLP_LAUNCH(pdlpk_gapd_keys(work, n, m, A[R], s()));
+    uint64_t* lk[2];
+    int32_t* ls[2];
+    pdlpk_gapd_lists(work, n, m, &lk[0], &ls[0], &lk[1], &ls[1]);
+    int cur = 0;
+    uint64_t lo = 0, hi = ~0ull, above_min = ~0ull;
+    bool lower = false, above = false;
+    int stall = 0;
+    int64_t rounds = 0;
+    std::vector<std::pair<uint64_t, double>> smp;
+    while (At > gapd_final_ && stall < 3) {
+      ++rounds;
+      blk = gapd_block(kBlk);
+      PDLP_LAUNCH(pdlpk_gapd_sample(lk[cur], A[R], kS, blk + kBlk * R, s()));
+      h = &gapd_exchange(kBlk);
+      smp.clear();
+      for (int r = 0; r < W; ++r) {
+        const int taken = static_cast<int>((*h)[kBlk * r + kS]);
+        for (int i = 0; i < taken; ++i) {
+          smp.emplace_back(bits_of((*h)[kBlk * r + i]), static_cast<double>(A[r]) / taken);
+        }
+      }
+      std::sort(smp.begin(), smp.end(), [](const auto& a, const auto& b) {
+        return a.first > b.first || (a.first == b.first && a.second < b.second);
+      });
+      // weighted median from the top (a quarter after a round without
+      // progress: steps off a tie group at the bracket's bottom)
+      const double target = static_cast<double>(At) * (stall > 0 ? 0.25 : 0.5);
+      double acc = 0.0;
+      uint64_t s_key = smp.back().first;
+      for (const auto& e : smp) {
+        acc += e.second;
+        if (acc >= target) {
+          s_key = e.first;
+          break;
+        }
+      }
+      blk = gapd_block(kBlk);
+      PDLP_LAUNCH(pdlpk_gapd_split(work, n, m, lk[cur], ls[cur], A[R], s_key, &rd, blk + 8 * R, s()));
+      h = &gapd_exchange(8);
+      double cg = 0.0, bg = 0.0, ce = 0.0, be = 0.0;
+      for (int r = 0; r < W; ++r) {
+        cg += (*h)[8 * r];
+        bg += (*h)[8 * r + 1];
+        ce += (*h)[8 * r + 2];
+        be += (*h)[8 * r + 3];
+      }
+      const double lam = host_key_value(s_key);
+      const double c_sum = C + cg, b_sum = B + bg;
+      uint64_t nlo = lo, nhi = hi;
+      int64_t nt = 0;
+      if (c_sum + b_sum / (lam * lam) >= r2) {
+        nlo = s_key;  // the crossing is s or above it
+        lower = true;
+        for (int r = 0; r < W; ++r) An[r] = A[r] - static_cast<int64_t>((*h)[8 * r + 4]);
+      } else {
+        nhi = s_key - 1;  // below s: [s, hi] joins the masses above
+        C += ce;
+        B += be;
+        above = true;
+        above_min = s_key;
+        for (int r = 0; r < W; ++r) An[r] = static_cast<int64_t>((*h)[8 * r + 4]);
+      }
+      for (int r = 0; r < W; ++r) nt += An[r];
+      stall = nt == At ? stall + 1 : 0;
+      if (nt != At) {
+        PDLP_LAUNCH(pdlpk_gapd_compact(work, n, m, lk[cur], ls[cur], A[R], nlo, nhi, lk[cur ^ 1],
+                                       ls[cur ^ 1], s()));
+        cur ^= 1;
+      }
+      lo = nlo;
+      hi = nhi;
+      A.swap(An);
+      At = nt;
+    }
+    // the bracket's events, gathered in rank order, sorted and swept
+    int64_t K = 1;
+    for (int r = 0; r < W; ++r) K = std::max(K, A[r]);
+    blk = gapd_block(std::max<int64_t>(3 * K, kBlk));
+    PDLP_LAUNCH(pdlpk_gapd_pack(work, n, m, lk[cur], ls[cur], A[R], K, blk + 3 * K * R, s()));
+    comm_->allgather(blk, static_cast<size_t>(3 * K), s());
+    const int64_t cap = std::max<int64_t>(At, 1);
+    if (gapd_final_cap_ < cap) {
+      gapd_fwork_.alloc(pdlpk_gapd_final_bytes(cap));
+      gapd_final_cap_ = cap;
+    }
+    const double hi0 = above ? host_key_value(above_min) : std::numeric_limits<double>::infinity();
+    double* lam_star = nullptr;
+    PDLP_LAUNCH(pdlpk_gapd_final(gapd_fwork_.get(), gapd_final_cap_, blk, W, K, A.data(), C, B, hi0,
+                                 lower ? 1 : 0, radius, &lam_star, s()));
+    // (the value goes to block R after the final kernels read the blocks)
+    PDLP_LAUNCH(pdlpk_gapd_value(&P, q.x, q.y, q.ax, q.aty, omega, lam_star, &rd, blk + 8 * R, s()));
+    if (gap_check_) {
+      PDLP_CK(cudaMemcpyAsync(&gapd_lambda_[qi], lam_star, sizeof(double), cudaMemcpyDeviceToHost, s()));
+    }
+    h = &gapd_exchange(8);
+    double value = 0.0;
+    for (int r = 0; r < W; ++r) value += (*h)[8 * r];
+    {
+      std::lock_guard<std::mutex> lk(gapd_stats().mu);
+      ++gapd_stats().evals;
+      gapd_stats().rounds += rounds;
+      gapd_stats().final_events += At;
+    }
+    return (value > 0.0) ? value / radius : 0.0;
   }
 
   // Window of the next window sort for (subproblem, query): the last
@@ -2108,6 +2416,22 @@ class Engine {
   // sharded solve
   Comm* comm_ = nullptr;
   const pdlp_shard_view* shard_in_ = nullptr;
+  // column cut, during load: the shard's row layout and its by_row offsets
+  const pdlp_csr_view* shard_rows_ = nullptr;
+  const int64_t* shard_row_entry_offset_ = nullptr;
+  // first non-finite entry (code << 3 | kind) of the column cut's row
+  // layout -> its whole-problem by_row position (entries of a row keep
+  // their order, rows ascend: the first local one is the first global one)
+  unsigned long long col_cut_entry(unsigned long long key) const {
+    if (shard_rows_ == nullptr || shard_row_entry_offset_ == nullptr || shard_rows_->start == nullptr) {
+      return key;
+    }
+    const int64_t k = static_cast<int64_t>(key >> 3);
+    const int64_t* st = shard_rows_->start;
+    const int64_t r = std::upper_bound(st, st + shard_rows_->primary_dim + 1, k) - st - 1;
+    const int64_t g = k + shard_row_entry_offset_[r];
+    return (static_cast<unsigned long long>(g) << 3) | (key & 7ull);
+  }
   pdlp_shard_plan plan_{};
   int64_t m_glob_ = 0, n_glob_ = 0;
   pdlpk_red_log red_log_{};
@@ -2127,6 +2451,7 @@ class Engine {
   DevBuf<double> fc_c_, fc_lv_, fc_uv_, fc_zero_, fr_lc_, fr_uc_, fr_zero_;
   DevBuf<double> fs_lc_, fs_uc_, fs_lv_, fs_uv_;
   DevBuf<double> gq_[2][4];
+  DevBuf<double> rows_full_;  // a sharded result's gathered row-side vector
   pdlpk_problem full_main_{}, full_primal_{}, full_dual_{};
   DevProblem prob_;
   DevBuf<double> slots_;
@@ -2134,6 +2459,24 @@ class Engine {
   DevBuf<double> red_scratch_;
   DevBuf<char> gap_work_[2];
   bool gap_shared_ = false;  // one gap buffer, queries evaluated one at a time
+  // distributed gap (sharded solves): PDLP_GAP_GATHERED=1 restores the
+  // gathered evaluation, PDLP_GAPD_CHECK=1 runs both and records the
+  // difference, PDLP_GAPD_FINAL = bracket size swept after the search
+  bool gap_gathered_ = std::getenv("PDLP_GAP_GATHERED") != nullptr &&
+                       std::getenv("PDLP_GAP_GATHERED")[0] == '1';
+  bool gap_check_ = std::getenv("PDLP_GAPD_CHECK") != nullptr &&
+                    std::getenv("PDLP_GAPD_CHECK")[0] == '1';
+  int64_t gapd_final_ = [] {
+    const char* e = std::getenv("PDLP_GAPD_FINAL");
+    const long long v = e != nullptr ? std::atoll(e) : 0;
+    return v > 0 ? static_cast<int64_t>(v) : int64_t(1) << 15;
+  }();
+  DevBuf<double> gapd_buf_;
+  DevBuf<char> gapd_fwork_;
+  int64_t gapd_final_cap_ = 0;
+  std::vector<double> gapd_host_;
+  double gapd_lambda_[2] = {0.0, 0.0};  // lambda* of the last evaluations (checks)
+  bool gap_whole() const { return !dist() || gap_gathered_ || gap_check_; }
   std::map<std::pair<const void*, int>, GapWindow> gap_windows_;
   // The cadence's side stream (the window average's share, the second gap
   // query), created on first use: the engine's device is current then.
@@ -2837,7 +3180,7 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
     E.join_panels();
     E.fill_panels();
   }
-  if (E.dist()) E.build_full_views();
+  if (E.dist() && E.gap_whole()) E.build_full_views();
   if (o->enable_polish) {
     // The polishing subproblems' states are allocated mid-loop, the first
     // time polishing triggers.  Growing the pool then costs 10-300 ms of
@@ -2913,7 +3256,10 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
       copy_to_host(host, dev, col_side ? P.n : P.m, E.s());
       return;
     }
-    double* full = col_side ? E.gbuf_.get() : E.gq_[0][0].get();
+    if (!col_side && E.rows_full_.size() < static_cast<size_t>(E.full_rows())) {
+      E.rows_full_.alloc(E.full_rows());
+    }
+    double* full = col_side ? E.gbuf_.get() : E.rows_full_.get();
     E.gather(dev, col_side ? P.n : P.m, col_side ? E.plan_.col_block : E.plan_.row_block, full);
     copy_to_host(host, full, col_side ? E.n_glob_ : E.m_glob_, E.s());
     PDLP_CK(cudaStreamSynchronize(E.s()));
@@ -3048,23 +3394,33 @@ int pdlp_shard_plan_for(int64_t rows, int64_t cols, int32_t rank, int32_t world,
     g_last_error = "invalid shard request";
     return PDLP_ERR_INVALID_ARGUMENT;
   }
-  *out = shard_plan(rows, cols, rank, world);
+  *out = shard_plan(rows, cols, rank, world, auto_cut(rows, cols));
   return PDLP_OK;
 }
 
-int pdlp_shard_extract(const pdlp_problem_view* problem, int32_t rank, int32_t world,
-                       pdlp_shard_view* out, void** owner) {
+int pdlp_shard_extract_cut(const pdlp_problem_view* problem, int32_t rank, int32_t world,
+                           int32_t cut, pdlp_shard_view* out, void** owner) {
   if (problem == nullptr || out == nullptr || owner == nullptr || world < 1 || rank < 0 ||
-      rank >= world) {
+      rank >= world || (cut != PDLP_CUT_ROWS && cut != PDLP_CUT_COLS)) {
     g_last_error = "invalid shard request";
     return PDLP_ERR_INVALID_ARGUMENT;
   }
   return guarded([&] {
     auto d = std::make_unique<ShardData>();
-    extract_shard(*problem, rank, world, *d);
+    extract_shard(*problem, rank, world, cut, *d);
     *out = d->view;
     *owner = d.release();
   });
+}
+
+int pdlp_shard_extract(const pdlp_problem_view* problem, int32_t rank, int32_t world,
+                       pdlp_shard_view* out, void** owner) {
+  if (problem == nullptr) {
+    g_last_error = "invalid shard request";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  return pdlp_shard_extract_cut(problem, rank, world, auto_cut(problem->rows, problem->cols), out,
+                                owner);
 }
 
 void pdlp_shard_free(void* owner) { delete static_cast<ShardData*>(owner); }
@@ -3090,15 +3446,23 @@ static int check_shard_view(const pdlp_shard_view* v, int32_t rank, int32_t worl
     g_last_error = "null shard";
     return PDLP_ERR_INVALID_ARGUMENT;
   }
-  pdlp_shard_plan want{};
-  const int rc = pdlp_shard_plan_for(v->plan.rows, v->plan.cols, rank, world, &want);
-  if (rc != PDLP_OK) return rc;
+  if (world < 1 || rank < 0 || rank >= world || v->plan.rows < 0 || v->plan.cols < 0 ||
+      (v->plan.cut != PDLP_CUT_ROWS && v->plan.cut != PDLP_CUT_COLS)) {
+    g_last_error = "invalid shard request";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  // the shard's own cut (a caller may build either); the ranges must be
+  // the equal blocks of pdlp_shard_plan_for
+  const pdlp_shard_plan want = shard_plan(v->plan.rows, v->plan.cols, rank, world, v->plan.cut);
   if (want.row_begin != v->plan.row_begin || want.row_end != v->plan.row_end ||
       want.col_begin != v->plan.col_begin || want.col_end != v->plan.col_end) {
     g_last_error = "shard ranges differ from pdlp_shard_plan_for(rows, cols, rank, world)";
     return PDLP_ERR_INVALID_ARGUMENT;
   }
-  if (v->rows.primary_dim != want.row_end - want.row_begin || v->cols.primary_dim != v->plan.cols ||
+  const bool cols_cut = want.cut == PDLP_CUT_COLS;
+  const int64_t rows_dim = cols_cut ? v->plan.rows : want.row_end - want.row_begin;
+  const int64_t cols_dim = cols_cut ? want.col_end - want.col_begin : v->plan.cols;
+  if (v->rows.primary_dim != rows_dim || v->cols.primary_dim != cols_dim ||
       v->rows.nnz != v->cols.nnz) {
     g_last_error = "invalid problem: row/column layouts disagree (index -1)";
     return PDLP_ERR_INVALID_PROBLEM;
@@ -3223,6 +3587,26 @@ int pdlp_trim_device_memory(int device) {
     PDLP_CK(cudaDeviceGetDefaultMemPool(&pool, device));
     PDLP_CK(cudaMemPoolTrimTo(pool, 0));
   });
+}
+
+void pdlp_gap_dist_stats(int64_t* out, double* max_rel, int32_t reset) {
+  /* max_rel[0]: the gap values, max_rel[1]: lambda* */
+  auto& g = pdlp_host::gapd_stats();
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (out != nullptr) {
+    out[0] = g.evals;
+    out[1] = g.rounds;
+    out[2] = g.final_events;
+    out[3] = g.checked;
+  }
+  if (max_rel != nullptr) {
+    max_rel[0] = g.max_rel;
+    max_rel[1] = g.max_rel_lambda;
+  }
+  if (reset) {
+    g.evals = g.rounds = g.final_events = g.checked = 0;
+    g.max_rel = g.max_rel_lambda = 0.0;
+  }
 }
 
 int pdlp_abi_version(void) { return PDLP_ABI_VERSION; }

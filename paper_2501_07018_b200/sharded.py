@@ -47,11 +47,15 @@ class ShardPlan:
     row_end: int
     col_begin: int
     col_end: int
+    cut: str = "rows"  # "rows": K_g = the rank's rows; "cols": its columns
+
+
+CUTS = {"rows": 0, "cols": 1}
 
 
 def _plan(p: N.ShardPlan) -> ShardPlan:
     return ShardPlan(p.rank, p.world, p.rows, p.cols, p.row_block, p.col_block, p.row_begin,
-                     p.row_end, p.col_begin, p.col_end)
+                     p.row_end, p.col_begin, p.col_end, "cols" if p.cut == 1 else "rows")
 
 
 def shard_plan(rows: int, cols: int, rank: int, world: int) -> ShardPlan:
@@ -66,13 +70,18 @@ def _arr(ptr, n: int, dtype) -> np.ndarray:
     return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
 
 
-def extract_shard(problem: LpProblem, rank: int, world: int) -> dict:
-    """Host-side shard of one rank (copies): K_g and K_g^T in CSR form plus
-    the rank's vector blocks.  CPU only."""
+def extract_shard(problem: LpProblem, rank: int, world: int, cut: str | None = None) -> dict:
+    """Host-side shard of one rank (copies): the rows / cols layouts in CSR
+    form plus the rank's vector blocks; cut "rows" / "cols" (default: the
+    one pdlp_shard_plan_for picks).  CPU only."""
     view = problem.view()
     out = N.ShardView()
     owner = C.c_void_p()
-    _check(N.lib().pdlp_shard_extract(C.byref(view), rank, world, C.byref(out), C.byref(owner)))
+    if cut is None:
+        _check(N.lib().pdlp_shard_extract(C.byref(view), rank, world, C.byref(out), C.byref(owner)))
+    else:
+        _check(N.lib().pdlp_shard_extract_cut(C.byref(view), rank, world, CUTS[cut], C.byref(out),
+                                              C.byref(owner)))
     try:
         pl = _plan(out.plan)
         ml, nl = pl.row_end - pl.row_begin, pl.col_end - pl.col_begin
@@ -89,7 +98,9 @@ def extract_shard(problem: LpProblem, rank: int, world: int) -> dict:
                 "var_upper": _arr(out.var_upper, nl, np.float64),
                 "con_lower": _arr(out.con_lower, ml, np.float64),
                 "con_upper": _arr(out.con_upper, ml, np.float64),
-                "entry_offset": out.entry_offset}
+                "entry_offset": out.entry_offset,
+                "row_entry_offset": _arr(out.row_entry_offset,
+                                         out.rows.primary_dim if pl.cut == "cols" else 0, np.int64)}
     finally:
         N.lib().pdlp_shard_free(owner)
 
@@ -124,6 +135,18 @@ def solve_sharded_emulated(problem: LpProblem, options: SolverOptions | None,
     options = options or SolverOptions(mode="perf")
     return run_solve(N.lib(), "pdlp_solve_sharded_emulated", problem, options,
                      to_c_options(options), extra=(world,))
+
+
+def gap_dist_stats(reset: bool = False) -> dict:
+    """Counters of the distributed normalized gap (process-wide): evaluations,
+    bracket-search rounds, events swept after the search, evaluations
+    compared with the gathered gap (PDLP_GAPD_CHECK=1) and the largest
+    relative difference seen there."""
+    out = (C.c_int64 * 4)()
+    mx = (C.c_double * 2)()
+    N.lib().pdlp_gap_dist_stats(out, mx, 1 if reset else 0)
+    return {"evals": out[0], "rounds": out[1], "final_events": out[2], "checked": out[3],
+            "max_rel": mx[0], "max_rel_lambda": mx[1]}
 
 
 def solve_distributed(problem: LpProblem, options: SolverOptions | None = None,
@@ -202,6 +225,7 @@ def generate_shard(config: str, seed: int, rank: int, world: int, **overrides) -
         setattr(prm, k, val)
     plan = N.ShardPlan()
     _check(N.lib().pdlp_shard_plan_for(prm.rows, prm.cols, rank, world, C.byref(plan)))
+    plan.cut = CUTS["rows"]  # the generator builds row-cut shards
     h = N.gen().pdlp_gen_random_lp_shard(C.byref(prm), plan.row_begin, plan.row_end,
                                          plan.col_begin, plan.col_end)
     if not h:

@@ -1,8 +1,10 @@
-"""Row-sharded solve.
+"""Sharded solve: the row cut and the column cut.
 
-CPU: the shard plan and the host-side shard extraction, and a world_size-2
-gloo run of the per-step exchange schedule (x-bar all-gather, partial K^T dy
-reduced to the column owners) on extracted shards.  GPU: the sharded solve
+CPU: the shard plan and the host-side shard extraction (both cuts), and
+world_size-2 gloo runs of the per-step exchange schedules on extracted
+shards (row cut: x-bar all-gather, partial K^T dy reduced to the column
+owners; column cut: partial K x-bar reduced to the row owners, dy
+all-gathered).  GPU: the sharded solve
 with threads-emulated ranks on one GPU (collectives = host barriers + device
 copies, no cross-kernel waits) and the NCCL communicator at world 1, both
 against the single-GPU solve.
@@ -65,7 +67,7 @@ def test_extract_shard_reassembles_matrix(world):
     aty = np.zeros(n)
     seen = 0
     for r in range(world):
-        sh = S.extract_shard(p, r, world)
+        sh = S.extract_shard(p, r, world, cut="rows")
         pl = sh["plan"]
         kg, kgt = _dense_shard(sh, n)
         np.testing.assert_array_equal(kg, a[pl.row_begin:pl.row_end])
@@ -80,6 +82,67 @@ def test_extract_shard_reassembles_matrix(world):
     assert seen == p.a.nonzeros()
     np.testing.assert_allclose(ax, a @ x, rtol=1e-13, atol=1e-13)
     np.testing.assert_allclose(aty, a.T @ y, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_extract_column_cut_reassembles_matrix(world):
+    """PDLP_CUT_COLS: the rows layout is every row restricted to the rank's
+    columns (local column indices), the cols layout the rank's columns
+    (global rows); row_entry_offset maps a shard entry to its by_row
+    position."""
+    rng = np.random.default_rng(10 + world)
+    p = random_box_lp(rng, 13, 29)
+    a = dense(p)
+    m, n = a.shape
+    x = rng.uniform(-1, 1, n)
+    y = rng.uniform(-1, 1, m)
+    ax = np.zeros(m)
+    aty = np.zeros(n)
+    seen = 0
+    for r in range(world):
+        sh = S.extract_shard(p, r, world, cut="cols")
+        pl = sh["plan"]
+        assert pl.cut == "cols"
+        c0, c1 = pl.col_begin, pl.col_end
+        rows, cols = sh["rows"], sh["cols"]
+        assert rows["dim"] == m and cols["dim"] == c1 - c0
+        kg = np.zeros((m, c1 - c0))
+        for i in range(m):
+            for k in range(rows["start"][i], rows["start"][i + 1]):
+                kg[i, rows["index"][k]] += rows["value"][k]
+                g = k + sh["row_entry_offset"][i]  # whole-problem by_row position
+                assert p.a.by_row.index[g] == rows["index"][k] + c0
+                assert p.a.by_row.value[g] == rows["value"][k]
+        kgt = np.zeros((c1 - c0, m))
+        for j in range(c1 - c0):
+            for k in range(cols["start"][j], cols["start"][j + 1]):
+                kgt[j, cols["index"][k]] += cols["value"][k]
+        np.testing.assert_array_equal(kg, a[:, c0:c1])
+        np.testing.assert_array_equal(kgt, a[:, c0:c1].T)
+        np.testing.assert_array_equal(sh["objective"], p.objective[c0:c1])
+        np.testing.assert_array_equal(sh["con_lower"], p.con_lower[pl.row_begin:pl.row_end])
+        ax += kg @ x[c0:c1]                  # partial K x, summed over ranks
+        aty[c0:c1] = kgt @ y                 # K^T y stays local
+        seen += rows["nnz"]
+        assert cols["nnz"] == rows["nnz"]
+    assert seen == p.a.nonzeros()
+    np.testing.assert_allclose(ax, a @ x, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(aty, a.T @ y, rtol=1e-13, atol=1e-13)
+
+
+def test_shard_plan_picks_the_cheaper_exchange(monkeypatch):
+    """The cut exchanges the smaller dimension: columns are cut when m < n
+    (dy and the partial row sums are m-vectors), rows otherwise;
+    PDLP_SHARD_CUT overrides."""
+    monkeypatch.setenv("PDLP_SHARD_CUT", "auto")
+    assert S.shard_plan(4000, 4_000_000, 0, 8).cut == "cols"
+    assert S.shard_plan(5_000_000, 10_000_000, 1, 8).cut == "cols"
+    assert S.shard_plan(1000, 1000, 0, 2).cut == "rows"
+    assert S.shard_plan(2000, 1000, 0, 2).cut == "rows"
+    monkeypatch.setenv("PDLP_SHARD_CUT", "rows")
+    assert S.shard_plan(4000, 4_000_000, 0, 8).cut == "rows"
+    monkeypatch.setenv("PDLP_SHARD_CUT", "cols")
+    assert S.shard_plan(2000, 1000, 0, 2).cut == "cols"
 
 
 def test_extract_shard_rejects_broken_layout():
@@ -113,7 +176,7 @@ def _exchange_worker(rank, world, port, out):
     try:
         p = P.generate("c0", 3, rows=60, cols=90)
         m, n = p.rows(), p.cols()
-        sh = S.extract_shard(p, rank, world)
+        sh = S.extract_shard(p, rank, world, cut="rows")
         pl = sh["plan"]
         kg, kgt = _dense_shard(sh, n)
         rng = np.random.default_rng(7)
@@ -141,6 +204,69 @@ def _exchange_worker(rank, world, port, out):
                      float(np.max(np.abs(mine - (a.T @ full_dy)[c0:c1]), initial=0.0)))
     finally:
         dist.destroy_process_group()
+
+
+def _exchange_worker_cols(rank, world, port, out):
+    """The column cut's step on CPU: local x-bar block -> partial K_g x-bar
+    over all m rows -> reduction to the row owners (all-reduce, keep the own
+    block) -> local dual update -> dy all-gather (equal padded blocks) ->
+    local K_g^T dy on the rank's columns."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = P.generate("c0", 4, rows=60, cols=90)
+        m, n = p.rows(), p.cols()
+        sh = S.extract_shard(p, rank, world, cut="cols")
+        pl = sh["plan"]
+        c0, c1, r0, r1 = pl.col_begin, pl.col_end, pl.row_begin, pl.row_end
+        rows, cols = sh["rows"], sh["cols"]
+        kg = np.zeros((m, c1 - c0))
+        for i in range(m):
+            for k in range(rows["start"][i], rows["start"][i + 1]):
+                kg[i, rows["index"][k]] += rows["value"][k]
+        kgt = np.zeros((c1 - c0, m))
+        for j in range(c1 - c0):
+            for k in range(cols["start"][j], cols["start"][j + 1]):
+                kgt[j, cols["index"][k]] += cols["value"][k]
+        rng = np.random.default_rng(7)
+        x = rng.uniform(-1, 1, n)
+        xn = rng.uniform(-1, 1, n)
+        y = rng.uniform(-1, 1, m)
+        mb = pl.row_block
+        part = np.zeros(mb * world)
+        part[:m] = kg @ (2 * xn[c0:c1] - x[c0:c1])          # partial K x-bar, all rows
+        t = torch.from_numpy(part)
+        dist.all_reduce(t)
+        ax = t.numpy()[r0:r1]                                # my rows' sums
+        blk = np.zeros(mb)
+        blk[: r1 - r0] = -0.5 * ax + 0.25 * y[r0:r1]        # a local dual update
+        parts = [torch.zeros(mb, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(blk))
+        dy = torch.cat(parts).numpy()[:m]
+        mine = kgt @ dy                                      # K^T dy on my columns
+        a = dense(p)
+        full_ax = a @ (2 * xn - x)
+        full_dy = -0.5 * full_ax + 0.25 * y
+        out[rank] = (float(np.max(np.abs(ax - full_ax[r0:r1]), initial=0.0)),
+                     float(np.max(np.abs(mine - (a.T @ full_dy)[c0:c1]), initial=0.0)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_schedule_gloo_world2_column_cut():
+    import torch.multiprocessing as mp
+
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_exchange_worker_cols, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert sorted(out.keys()) == [0, 1]
+    for r in range(world):
+        assert out[r][0] < 1e-11 and out[r][1] < 1e-11, out[r]
 
 
 def test_exchange_schedule_gloo_world2():
@@ -308,7 +434,7 @@ def test_generated_shards_equal_extracted_shards(cfg, kw, world):
     full = P.generate(cfg, 3, row_window=(0, kw["rows"]), **kw)
     for rank in range(world):
         a = S.generate_shard(cfg, 3, rank, world, **kw).as_dict()
-        b = S.extract_shard(full, rank, world)
+        b = S.extract_shard(full, rank, world, cut="rows")
         assert a["plan"] == b["plan"] and a["entry_offset"] == b["entry_offset"]
         for key in ("objective", "var_lower", "var_upper", "con_lower", "con_upper"):
             assert np.array_equal(a[key].view(np.int64), b[key].view(np.int64)), key
@@ -338,3 +464,55 @@ def test_local_shard_rejects_wrong_plan(gpu):
     sh = S.generate_shard("c0", 1, 0, 2, rows=200, cols=300)
     with pytest.raises(RuntimeError):  # a rank-0 shard claimed by rank 1
         S.solve_sharded_local_emulated([sh, sh], _opts(iteration_limit=5))
+
+
+# ---------------------------------------------------- distributed gap ---
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_distributed_gap_matches_gathered(gpu, monkeypatch, world):
+    """The sharded solves' normalized duality gap (restarts.hpp:107-220) is
+    evaluated without gathering a vector: a bracket search over the global
+    event order (rank-local reductions at a sampled key, combined in rank
+    order), then the bracket's events gathered and swept.  With
+    PDLP_GAPD_CHECK=1 every evaluation is also run on gathered vectors:
+    lambda* (which the located crossing decides) agrees to 1e-9 relative; the
+    gap value is a cancelling sum added in another order (per rank, then
+    across ranks), so it agrees to rounding of its terms (1e-6 relative here).
+    PDLP_GAPD_FINAL=8 forces the search down to eight events, so the
+    bisection rounds run on these small instances."""
+    monkeypatch.setenv("PDLP_GAPD_CHECK", "1")
+    monkeypatch.setenv("PDLP_GAPD_FINAL", "8")
+    S.gap_dist_stats(reset=True)
+    cases = [P.generate("c0", 0), P.generate("c1", 1, sources=50, sinks=70),
+             P.generate("c2", 2, rows=800, cols=1600, kmax=600)]
+    for p in cases:
+        tol = P.relative_tolerances(p, 1e-4)
+        o = _opts(tolerances=P.TerminationTolerances(*tol), iteration_limit=3000)
+        b = S.solve_sharded_emulated(p, o, world)
+        assert b.status in (P.SolveStatus.OPTIMAL, P.SolveStatus.ITERATION_LIMIT)
+    st = S.gap_dist_stats(reset=True)
+    assert st["evals"] > 0 and st["checked"] == st["evals"]
+    assert st["rounds"] >= st["evals"]  # every evaluation bisected at least once
+    assert st["max_rel_lambda"] <= 1e-9, st
+    assert st["max_rel"] <= 1e-6, st
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_gap_solves_match_gathered_gap_solves(gpu, monkeypatch, world):
+    """Whole sharded solves with the distributed gap (default) and with the
+    gathered one (PDLP_GAP_GATHERED=1) reach the same status, restarts and
+    optimum: the gaps agree to rounding, so the restart decisions do."""
+    for p in (P.generate("c0", 0), P.generate("c1", 0, sources=60, sinks=60)):
+        tol = P.relative_tolerances(p, 1e-4)
+        o = _opts(tolerances=P.TerminationTolerances(*tol))
+        monkeypatch.setenv("PDLP_GAP_GATHERED", "1")
+        a = S.solve_sharded_emulated(p, o, world)
+        monkeypatch.delenv("PDLP_GAP_GATHERED")
+        S.gap_dist_stats(reset=True)
+        b = S.solve_sharded_emulated(p, o, world)
+        assert S.gap_dist_stats()["evals"] > 0
+        assert a.status == b.status == P.SolveStatus.OPTIMAL
+        assert abs(b.summary.primal_objective - a.summary.primal_objective) <= \
+            2e-4 * abs(a.summary.primal_objective)
+        assert b.summary.primal_residual_inf <= tol[0] and b.summary.dual_residual_inf <= tol[1]

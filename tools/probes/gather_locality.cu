@@ -1,0 +1,166 @@
+// Probe (measurement, not product code): does ordering C2's columns by
+// degree make the row pass's x-bar gathers cheaper?  The row layout's column
+// indices follow the column-degree distribution (power law, alpha = 2 on
+// [2, 1e4], BASELINE configs[2]); with columns numbered by descending degree
+// the popular ones share cache lines and stay in L1/L2.
+//   * pure gathers v[random % len] for len from L1- to HBM-sized vectors
+//   * stream + gather (acc += val[k] * v[idx[k]], coalesced idx/val) with
+//     idx drawn uniform, power-law with degree-sorted numbering, and
+//     power-law with the same degrees under a random-looking bijection
+// nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o gather_locality gather_locality.cu
+#include <cuda_runtime.h>
+#include <thrust/device_ptr.h>
+#include <thrust/scan.h>
+#include <thrust/sort.h>
+#include <thrust/functional.h>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { std::printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+__device__ __forceinline__ uint32_t hash32(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
+  return static_cast<uint32_t>(x);
+}
+__device__ __forceinline__ double u01(uint64_t x) { return (hash32(x) + 0.5) * (1.0 / 4294967296.0); }
+
+__global__ void degrees(int32_t* deg, int64_t n) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    // alpha = 2 on [2, 1e4]: inverse CDF of p(k) ~ k^-2 truncated
+    const double u = u01(j * 7919 + 1);
+    const double a = 1.0 / 2.0, b = 1.0 / 1e4;
+    double k = 1.0 / (a - u * (a - b));
+    int32_t d = static_cast<int32_t>(k);
+    deg[j] = d < 2 ? 2 : (d > 10000 ? 10000 : d);
+  }
+}
+__global__ void draw(const int64_t* cdf, int64_t n, int64_t nnz, int32_t* idx_sorted, int32_t* idx_perm,
+                     int32_t* idx_unif, double* val) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = static_cast<int64_t>(u01(k * 31 + 7) * nnz);
+    int64_t lo = 0, hi = n - 1;  // first j with cdf[j] > t
+    while (lo < hi) { const int64_t mid = (lo + hi) / 2; if (cdf[mid] > t) hi = mid; else lo = mid + 1; }
+    idx_sorted[k] = static_cast<int32_t>(lo);
+    idx_perm[k] = static_cast<int32_t>((static_cast<uint64_t>(lo) * 2654435761ull + 12345) % n);
+    idx_unif[k] = static_cast<int32_t>(u01(k * 131 + 3) * n);
+    val[k] = u01(k) - 0.5;
+  }
+}
+template <int U>
+__global__ void __launch_bounds__(256) gather_probe(const double* __restrict__ v, int64_t len, int64_t count, double* out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int64_t b = tid * U; b < count; b += nt * U) {
+    double g[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) g[u] = __ldg(v + (hash32(b + u) % static_cast<uint32_t>(len)));
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += g[u];
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+template <int U>
+__global__ void __launch_bounds__(256) stream_gather(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                                     const double* __restrict__ v, int64_t nnz, double* out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int64_t b = tid; b < nnz; b += nt * U) {
+    int32_t ci[U]; double a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) { const int64_t k = b + u * nt; ci[u] = k < nnz ? __ldcs(idx + k) : 0; a[u] = k < nnz ? __ldcs(val + k) : 0.0; }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += a[u] * __ldg(v + ci[u]);
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+// Hot columns (the H most popular, numbered [0, H) in the degree-sorted
+// draw) read through L1; every other gather skips L1 allocation, so the hot
+// lines are not evicted by the cold stream.
+__device__ __forceinline__ double ld_na(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+template <int U, int MODE>
+__global__ void __launch_bounds__(256) stream_gather_hot(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                                         const double* __restrict__ v, int64_t nnz, int32_t H, double* out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int64_t b = tid; b < nnz; b += nt * U) {
+    int32_t ci[U]; double a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) { const int64_t k = b + u * nt; ci[u] = k < nnz ? __ldcs(idx + k) : 0; a[u] = k < nnz ? __ldcs(val + k) : 0.0; }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double g;
+      if (MODE == 0) g = ld_na(v + ci[u]);
+      else g = ci[u] < H ? __ldg(v + ci[u]) : ld_na(v + ci[u]);
+      acc += a[u] * g;
+    }
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+template <class F> float time_it(F f, int reps) {
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  f(); cudaDeviceSynchronize();
+  cudaEventRecord(a); for (int i = 0; i < reps; ++i) f(); cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b); return ms * 1000.f / reps;
+}
+int main() {
+  int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t n = 10000000;
+  int32_t* deg; CK(cudaMalloc(&deg, n * 4));
+  degrees<<<2048, 256>>>(deg, n);
+  thrust::device_ptr<int32_t> dp(deg);
+  thrust::sort(dp, dp + n, thrust::greater<int32_t>());
+  int64_t* cdf; CK(cudaMalloc(&cdf, n * 8));
+  thrust::device_ptr<int64_t> cp(cdf);
+  thrust::inclusive_scan(dp, dp + n, cp);
+  int64_t nnz = 0; CK(cudaMemcpy(&nnz, cdf + n - 1, 8, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> hd(8); CK(cudaMemcpy(hd.data(), deg, 32, cudaMemcpyDeviceToHost));
+  std::printf("n=%lld nnz=%lld (mean %.2f), top degrees %d %d %d\n", (long long)n, (long long)nnz, (double)nnz / n, hd[0], hd[1], hd[2]);
+  // share of entries in the top-K columns
+  for (int64_t K : {4096LL, 16384LL, 65536LL, 262144LL}) {
+    int64_t c; CK(cudaMemcpy(&c, cdf + K - 1, 8, cudaMemcpyDeviceToHost));
+    std::printf("  top %lld columns (%lld KB of x): %.1f %% of entries\n", (long long)K, (long long)K * 8 / 1024, 100.0 * c / nnz);
+  }
+  int32_t *is, *ip, *iu; double *val, *v, *out;
+  CK(cudaMalloc(&is, nnz * 4)); CK(cudaMalloc(&ip, nnz * 4)); CK(cudaMalloc(&iu, nnz * 4));
+  CK(cudaMalloc(&val, nnz * 8)); CK(cudaMalloc(&v, n * 8)); CK(cudaMalloc(&out, 8));
+  CK(cudaMemset(v, 0, n * 8));
+  draw<<<4096, 256>>>(cdf, n, nnz, is, ip, iu, val);
+  CK(cudaDeviceSynchronize());
+  const int reps = 10;
+  for (int64_t len : {2048LL, 8192LL, 16384LL, 65536LL, 524288LL, 5000000LL, 10000000LL}) {
+    for (int per : {4, 8}) {
+      const float us = time_it([&] { gather_probe<8><<<sms * per, 256>>>(v, len, nnz, out); }, reps);
+      std::printf("gather len=%8lld (%7.0f KB) %d CTA/SM: %8.1f us  %6.1f G/s\n", (long long)len, len * 8 / 1024.0, per, us, nnz / us / 1e3);
+    }
+  }
+  const char* names[3] = {"uniform", "powerlaw degree-sorted", "powerlaw permuted"};
+  int32_t* ids[3] = {iu, is, ip};
+  for (int q = 0; q < 3; ++q) {
+    for (int per : {4, 8}) {
+      const float us = time_it([&] { stream_gather<4><<<sms * per, 256>>>(ids[q], val, v, nnz, out); }, reps);
+      std::printf("stream+gather %-24s %d CTA/SM: %8.1f us  %6.1f G entries/s  (%.0f GB/s of idx+val)\n", names[q], per, us,
+                  nnz / us / 1e3, nnz * 12.0 / us / 1e3);
+    }
+  }
+  // L1 isolation of the hot columns (degree-sorted draw)
+  for (int smem_kb : {0, 100}) {
+    // emulate a kernel that also holds smem_kb of shared memory per CTA (2 CTAs/SM)
+    for (int per : {2, 4}) {
+      const size_t sm = static_cast<size_t>(smem_kb) * 1024 / 2;
+      cudaFuncSetAttribute(stream_gather_hot<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      cudaFuncSetAttribute(stream_gather_hot<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+      float us = time_it([&] { stream_gather_hot<4, 0><<<sms * per, 256, sm>>>(is, val, v, nnz, 0, out); }, reps);
+      std::printf("smem %3d KB/SM %d CTA/SM  sorted, all no_allocate         : %8.1f us\n", smem_kb, per, us);
+      for (int H : {4096, 8192, 12288, 16384, 24576}) {
+        us = time_it([&] { stream_gather_hot<4, 1><<<sms * per, 256, sm>>>(is, val, v, nnz, H, out); }, reps);
+        std::printf("smem %3d KB/SM %d CTA/SM  sorted, hot H=%5d via L1 (%3d KB): %8.1f us\n", smem_kb, per, H, H * 8 / 1024, us);
+      }
+    }
+  }
+  return 0;
+}
