@@ -76,8 +76,17 @@ pdlp_instance* pdlp_gen_random_lp_window(const pdlp_gen_params* params, int64_t 
 typedef struct pdlp_gen_shard pdlp_gen_shard;
 pdlp_gen_shard* pdlp_gen_random_lp_shard(const pdlp_gen_params* params, int64_t r0, int64_t r1,
                                          int64_t c0, int64_t c1);
+/* The same instance's shard under PDLP_CUT_COLS: the block's columns
+ * [c0, c1) in both layouts -- K_g^T with global row indices, exactly the
+ * instance's columns, and K_g over all rows with local column indices --
+ * their variable bounds and objective, and the row bounds of [r0, r1) (from
+ * the row window, which draws every column's stream once).  Equals
+ * pdlp_shard_extract_cut(..., PDLP_CUT_COLS) of the whole instance except
+ * row_entry_offset (NULL: not known without the rest of the rows). */
+pdlp_gen_shard* pdlp_gen_random_lp_colshard(const pdlp_gen_params* params, int64_t r0, int64_t r1,
+                                            int64_t c0, int64_t c1);
 /* The shard as the solver's pdlp_shard_view (plan.rank / world / blocks left
- * 0 for the caller to fill; arrays owned by the shard). */
+ * 0 for the caller to fill; plan.cut set; arrays owned by the shard). */
 void pdlp_gen_shard_view(const pdlp_gen_shard* shard, pdlp_shard_view* out);
 void pdlp_gen_shard_free(pdlp_gen_shard* shard);
 

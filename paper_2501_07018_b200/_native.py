@@ -282,6 +282,8 @@ GEN_SIGNATURES = {
     "pdlp_instance_free": (None, [C.c_void_p]),
     "pdlp_gen_random_lp_shard": (C.c_void_p, [C.POINTER(GenParams), C.c_int64, C.c_int64,
                                                C.c_int64, C.c_int64]),
+    "pdlp_gen_random_lp_colshard": (C.c_void_p, [C.POINTER(GenParams), C.c_int64, C.c_int64,
+                                               C.c_int64, C.c_int64]),
     "pdlp_gen_shard_view": (None, [C.c_void_p, C.POINTER(ShardView)]),
     "pdlp_gen_shard_free": (None, [C.c_void_p]),
 }

@@ -449,14 +449,27 @@ struct pdlp_gen_shard {
   pdlp_instance* win = nullptr;
   int64_t rows = 0, cols = 0, r0 = 0, r1 = 0, c0 = 0, c1 = 0, entry_offset = 0;
   std::vector<double> objective, var_lower, var_upper;
+  // column cut: the block's layouts and the window rows' bounds
+  int32_t cut = 0;
+  std::vector<int64_t> rstart, rindex, cstart, cindex;
+  std::vector<double> rvalue, cvalue, con_lower, con_upper;
   ~pdlp_gen_shard() { delete win; }
 };
 
+static pdlp_gen_shard* build_shard(const pdlp_gen_params* params, int64_t r0, int64_t r1,
+                                   int64_t c0, int64_t c1, int32_t cut);
+
 pdlp_gen_shard* pdlp_gen_random_lp_shard(const pdlp_gen_params* params, int64_t r0, int64_t r1,
                                          int64_t c0, int64_t c1) {
+  return build_shard(params, r0, r1, c0, c1, 0);
+}
+
+static pdlp_gen_shard* build_shard(const pdlp_gen_params* params, int64_t r0, int64_t r1,
+                                   int64_t c0, int64_t c1, int32_t cut) {
   const pdlp_gen_params& p = *params;
   if (c0 < 0 || c1 > p.cols || c0 > c1) return nullptr;
   auto* sh = new pdlp_gen_shard;
+  sh->cut = cut;
   int64_t before = 0;
   sh->win = random_lp_window(params, r0, r1, &before);
   if (sh->win == nullptr) {
@@ -512,9 +525,13 @@ pdlp_gen_shard* pdlp_gen_random_lp_shard(const pdlp_gen_params* params, int64_t 
   const int T = static_cast<int>(std::max<unsigned>(1u, std::min(32u, std::thread::hardware_concurrency())));
   std::vector<std::thread> th;
   const int64_t per = (nb + T - 1) / T;
+  // column cut: the block's columns as stored (per thread, joined below)
+  std::vector<std::vector<int64_t>> t_len(static_cast<size_t>(T)), t_row(static_cast<size_t>(T));
+  std::vector<std::vector<double>> t_val(static_cast<size_t>(T));
+  const bool keep = sh->cut == 1;
   for (int t = 0; t < T; ++t) {
     const int64_t lo = std::min(nb, per * t), hi = std::min(nb, lo + per);
-    th.emplace_back([&, lo, hi] {
+    th.emplace_back([&, t, lo, hi] {
       std::vector<std::pair<int64_t, double>> col;
       for (int64_t q = lo; q < hi; ++q) {
         const int64_t c = c0 + q;
@@ -530,19 +547,62 @@ pdlp_gen_shard* pdlp_gen_random_lp_shard(const pdlp_gen_params* params, int64_t 
         std::stable_sort(col.begin(), col.end(),
                          [](const auto& a, const auto& b) { return a.first < b.first; });
         double acc = 0.0;
+        int64_t len = 0;
         for (size_t e = 0; e < col.size();) {
           double v = col[e].second;
           size_t f = e + 1;
           while (f < col.size() && col[f].first == col[e].first) v += col[f++].second;
           acc += v * ystar(col[e].first);
+          if (keep) {
+            t_row[static_cast<size_t>(t)].push_back(col[e].first);
+            t_val[static_cast<size_t>(t)].push_back(v);
+            ++len;
+          }
           e = f;
         }
+        if (keep) t_len[static_cast<size_t>(t)].push_back(len);
         sh->objective[static_cast<size_t>(q)] = acc + rstar(c);
       }
     });
   }
   for (auto& x : th) x.join();
+  if (keep) {
+    // K_g^T: the block's columns in order; K_g: its transpose over all rows
+    // (a counting sort keeps columns ascending within each row)
+    sh->cstart.assign(1, 0);
+    for (int t = 0; t < T; ++t) {
+      for (int64_t len : t_len[static_cast<size_t>(t)]) sh->cstart.push_back(sh->cstart.back() + len);
+      sh->cindex.insert(sh->cindex.end(), t_row[static_cast<size_t>(t)].begin(), t_row[static_cast<size_t>(t)].end());
+      sh->cvalue.insert(sh->cvalue.end(), t_val[static_cast<size_t>(t)].begin(), t_val[static_cast<size_t>(t)].end());
+      t_row[static_cast<size_t>(t)] = {};
+      t_val[static_cast<size_t>(t)] = {};
+    }
+    const int64_t nnz = static_cast<int64_t>(sh->cindex.size());
+    sh->rstart.assign(static_cast<size_t>(m + 1), 0);
+    for (int64_t r : sh->cindex) ++sh->rstart[static_cast<size_t>(r + 1)];
+    for (int64_t r = 0; r < m; ++r) sh->rstart[static_cast<size_t>(r + 1)] += sh->rstart[static_cast<size_t>(r)];
+    sh->rindex.resize(static_cast<size_t>(nnz));
+    sh->rvalue.resize(static_cast<size_t>(nnz));
+    std::vector<int64_t> fill(sh->rstart.begin(), sh->rstart.end() - 1);
+    for (int64_t q = 0; q < nb; ++q) {
+      for (int64_t k = sh->cstart[static_cast<size_t>(q)]; k < sh->cstart[static_cast<size_t>(q + 1)]; ++k) {
+        const int64_t o = fill[static_cast<size_t>(sh->cindex[static_cast<size_t>(k)])]++;
+        sh->rindex[static_cast<size_t>(o)] = q;
+        sh->rvalue[static_cast<size_t>(o)] = sh->cvalue[static_cast<size_t>(k)];
+      }
+    }
+    // only the window rows' bounds are kept from the window
+    sh->con_lower = sh->win->con_lower;
+    sh->con_upper = sh->win->con_upper;
+    delete sh->win;
+    sh->win = nullptr;
+  }
   return sh;
+}
+
+pdlp_gen_shard* pdlp_gen_random_lp_colshard(const pdlp_gen_params* params, int64_t r0, int64_t r1,
+                                            int64_t c0, int64_t c1) {
+  return build_shard(params, r0, r1, c0, c1, 1);
 }
 
 void pdlp_gen_shard_view(const pdlp_gen_shard* sh, pdlp_shard_view* out) {
@@ -553,6 +613,21 @@ void pdlp_gen_shard_view(const pdlp_gen_shard* sh, pdlp_shard_view* out) {
   out->plan.row_end = sh->r1;
   out->plan.col_begin = sh->c0;
   out->plan.col_end = sh->c1;
+  out->plan.cut = sh->cut;
+  if (sh->cut == 1) {
+    out->rows = {sh->rows, static_cast<int64_t>(sh->rvalue.size()), sh->rstart.data(),
+                 sh->rindex.data(), sh->rvalue.data()};
+    out->cols = {sh->c1 - sh->c0, static_cast<int64_t>(sh->cvalue.size()), sh->cstart.data(),
+                 sh->cindex.data(), sh->cvalue.data()};
+    out->objective = sh->objective.data();
+    out->var_lower = sh->var_lower.data();
+    out->var_upper = sh->var_upper.data();
+    out->con_lower = sh->con_lower.data();
+    out->con_upper = sh->con_upper.data();
+    out->entry_offset = 0;
+    out->row_entry_offset = nullptr;
+    return;
+  }
   const pdlp_instance* w = sh->win;
   out->rows = {w->rows, static_cast<int64_t>(w->by_row.value.size()), w->by_row.start.data(),
                w->by_row.index.data(), w->by_row.value.data()};

@@ -53,7 +53,7 @@ void parallel_lines(int64_t dim, F f) {
 
 }  // namespace
 
-static const bool g_auto_cols = false;  // (bring-up: PDLP_SHARD_CUT=cols)
+static const bool g_auto_cols = true;
 
 int auto_cut(int64_t m, int64_t n) {
   if (const char* e = std::getenv("PDLP_SHARD_CUT")) {

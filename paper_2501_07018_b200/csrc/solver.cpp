@@ -2451,7 +2451,7 @@ class Engine {
   DevBuf<double> fc_c_, fc_lv_, fc_uv_, fc_zero_, fr_lc_, fr_uc_, fr_zero_;
   DevBuf<double> fs_lc_, fs_uc_, fs_lv_, fs_uv_;
   DevBuf<double> gq_[2][4];
-  DevBuf<double> rows_full_;  // a sharded result's gathered row-side vector
+  DevBuf<double> rows_full_;  // a sharded result's gathered vector
   pdlpk_problem full_main_{}, full_primal_{}, full_dual_{};
   DevProblem prob_;
   DevBuf<double> slots_;
@@ -3256,10 +3256,9 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
       copy_to_host(host, dev, col_side ? P.n : P.m, E.s());
       return;
     }
-    if (!col_side && E.rows_full_.size() < static_cast<size_t>(E.full_rows())) {
-      E.rows_full_.alloc(E.full_rows());
-    }
-    double* full = col_side ? E.gbuf_.get() : E.rows_full_.get();
+    const int64_t need = col_side ? E.full_cols() : E.full_rows();
+    if (E.rows_full_.size() < static_cast<size_t>(need)) E.rows_full_.alloc(need);
+    double* full = E.rows_full_.get();
     E.gather(dev, col_side ? P.n : P.m, col_side ? E.plan_.col_block : E.plan_.row_block, full);
     copy_to_host(host, full, col_side ? E.n_glob_ : E.m_glob_, E.s());
     PDLP_CK(cudaStreamSynchronize(E.s()));

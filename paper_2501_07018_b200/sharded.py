@@ -212,10 +212,12 @@ class LocalShard:
                 "entry_offset": v.entry_offset}
 
 
-def generate_shard(config: str, seed: int, rank: int, world: int, **overrides) -> LocalShard:
+def generate_shard(config: str, seed: int, rank: int, world: int, cut: str = "rows",
+                   **overrides) -> LocalShard:
     """Rank `rank` of `world`'s shard of the counter-based instance
     generate(config, seed, row_window=(0, rows), **overrides) -- built without
-    the rest of the instance (C0 / C2 / C4 recipes)."""
+    the rest of the instance (C0 / C2 / C4 recipes); cut "rows" (K_g = the
+    rank's rows) or "cols" (the rank's columns), "auto" = pdlp_shard_plan_for's."""
     cfg = config.lower()
     if cfg not in ("c0", "c2", "c4"):
         raise ValueError("shard-local generation exists for the random-LP recipes c0, c2, c4")
@@ -225,9 +227,11 @@ def generate_shard(config: str, seed: int, rank: int, world: int, **overrides) -
         setattr(prm, k, val)
     plan = N.ShardPlan()
     _check(N.lib().pdlp_shard_plan_for(prm.rows, prm.cols, rank, world, C.byref(plan)))
-    plan.cut = CUTS["rows"]  # the generator builds row-cut shards
-    h = N.gen().pdlp_gen_random_lp_shard(C.byref(prm), plan.row_begin, plan.row_end,
-                                         plan.col_begin, plan.col_end)
+    if cut != "auto":
+        plan.cut = CUTS[cut]
+    fn = N.gen().pdlp_gen_random_lp_colshard if plan.cut == CUTS["cols"] else \
+        N.gen().pdlp_gen_random_lp_shard
+    h = fn(C.byref(prm), plan.row_begin, plan.row_end, plan.col_begin, plan.col_end)
     if not h:
         raise ValueError("bad shard ranges")
     return LocalShard(h, plan)

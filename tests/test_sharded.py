@@ -295,7 +295,8 @@ def _rel(a, b):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
-def test_sharded_first_100_iterates_track_single_gpu(gpu, world):
+@pytest.mark.parametrize("cut", ["rows", "cols"])
+def test_sharded_first_100_iterates_track_single_gpu(gpu, monkeypatch, world, cut):
     """iterates within 1e-9 relative over the first 100 steps.
 
     The sharded solve scales the problem bit-identically (max-norms are
@@ -307,6 +308,7 @@ def test_sharded_first_100_iterates_track_single_gpu(gpu, world):
     reference's gap takes 7324.19 vs 6524.97 on average-iterate inputs that
     agree to 1e-12.  So the restart-free power-law case runs
     with restarts off; the others exercise the whole cadence."""
+    monkeypatch.setenv("PDLP_SHARD_CUT", cut)
     cases = [(P.generate("c0", 0), {}), (P.generate("c1", 1, sources=50, sinks=70), {}),
              (P.generate("c2", 2, rows=800, cols=1600, kmax=600), {"enable_restarts": False})]
     for p, kw in cases:
@@ -320,7 +322,9 @@ def test_sharded_first_100_iterates_track_single_gpu(gpu, world):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_solve_reaches_the_same_optimum(gpu, ref, world):
+@pytest.mark.parametrize("cut", ["rows", "cols"])
+def test_sharded_solve_reaches_the_same_optimum(gpu, ref, monkeypatch, world, cut):
+    monkeypatch.setenv("PDLP_SHARD_CUT", cut)
     for p in (P.generate("c0", 0), P.generate("c1", 0, sources=60, sinks=60)):
         tol = P.relative_tolerances(p, 1e-4)
         o = _opts(tolerances=P.TerminationTolerances(*tol))
@@ -395,11 +399,13 @@ def test_nccl_world1_matches_emulated(gpu):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_peer_read_epilogue_matches_reduce_scatter(gpu, monkeypatch, world):
+@pytest.mark.parametrize("cut", ["rows", "cols"])
+def test_peer_read_epilogue_matches_reduce_scatter(gpu, monkeypatch, world, cut):
     """The reduce-scatter folded into the epilogue (owners read every rank's
     partial product over P2P and sum in rank order) gives the same bits as
     the collective path it replaces, over whole solves: attempts, cadence
     products, both polishing subproblems and the final verification."""
+    monkeypatch.setenv("PDLP_SHARD_CUT", cut)
     cases = [(P.generate("c0", 3), {}), (P.generate("c1", 3, sources=45, sinks=55), {}),
              (P.generate("c0", 4), {"enable_polish": False, "iteration_limit": 700})]
     polished = []
@@ -416,10 +422,11 @@ def test_peer_read_epilogue_matches_reduce_scatter(gpu, monkeypatch, world):
         np.testing.assert_array_equal(a.x, b.x)
         np.testing.assert_array_equal(a.y, b.y)
         polished.append(b.polish_iterations)
-    # at world 2 the transport case polishes: both subproblems (the dual one
-    # reads the partial products in its row epilogue) ran over the peer
-    # exchange (other worlds take other trajectories and may not polish)
-    if world == 2:
+    # at world 2 the transport case polishes under the row cut: both
+    # subproblems (the dual one reads the partial products in its row
+    # epilogue) ran over the peer exchange (other worlds and the column cut
+    # take other trajectories and may not polish)
+    if world == 2 and cut == "rows":
         assert polished[1] > 0
 
 
@@ -427,14 +434,16 @@ def test_peer_read_epilogue_matches_reduce_scatter(gpu, monkeypatch, world):
 @pytest.mark.parametrize("cfg,kw", [("c2", {"rows": 3000, "cols": 7000, "kmax": 800}),
                                     ("c0", {"rows": 500, "cols": 900})])
 @pytest.mark.parametrize("world", [1, 2, 3])
-def test_generated_shards_equal_extracted_shards(cfg, kw, world):
+@pytest.mark.parametrize("cut", ["rows", "cols"])
+def test_generated_shards_equal_extracted_shards(cfg, kw, world, cut):
     """Each rank's shard built on its own (pdlp_gen_random_lp_shard: its rows,
-    its column block with the GLOBAL objective) equals the shard extracted
-    from the whole counter-based instance, array for array and bit for bit."""
+    its column block with the GLOBAL objective; pdlp_gen_random_lp_colshard:
+    its columns, its rows' bounds) equals the shard extracted from the whole
+    counter-based instance, array for array and bit for bit."""
     full = P.generate(cfg, 3, row_window=(0, kw["rows"]), **kw)
     for rank in range(world):
-        a = S.generate_shard(cfg, 3, rank, world, **kw).as_dict()
-        b = S.extract_shard(full, rank, world, cut="rows")
+        a = S.generate_shard(cfg, 3, rank, world, cut=cut, **kw).as_dict()
+        b = S.extract_shard(full, rank, world, cut=cut)
         assert a["plan"] == b["plan"] and a["entry_offset"] == b["entry_offset"]
         for key in ("objective", "var_lower", "var_upper", "con_lower", "con_upper"):
             assert np.array_equal(a[key].view(np.int64), b[key].view(np.int64)), key
@@ -445,12 +454,15 @@ def test_generated_shards_equal_extracted_shards(cfg, kw, world):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [1, 2, 3])
-def test_local_shards_solve_like_the_whole_problem(gpu, world):
+@pytest.mark.parametrize("cut", ["rows", "cols"])
+def test_local_shards_solve_like_the_whole_problem(gpu, monkeypatch, world, cut):
     """A sharded solve fed only the ranks' own shards is the sharded solve of
-    the whole instance, bit for bit (same partition, same kernels)."""
+    the whole instance, bit for bit (same partition, same kernels), for the
+    row cut and the column cut."""
+    monkeypatch.setenv("PDLP_SHARD_CUT", cut)
     kw = {"rows": 2000, "cols": 4000, "kmax": 600}
     full = P.generate("c2", 5, row_window=(0, kw["rows"]), **kw)
-    shards = [S.generate_shard("c2", 5, r, world, **kw) for r in range(world)]
+    shards = [S.generate_shard("c2", 5, r, world, cut=cut, **kw) for r in range(world)]
     o = _opts(iteration_limit=200, tolerances=P.TerminationTolerances(0.0, 0.0, 0.0))
     a = S.solve_sharded_emulated(full, o, world)
     b = S.solve_sharded_local_emulated(shards, o)
@@ -469,7 +481,8 @@ def test_local_shard_rejects_wrong_plan(gpu):
 # ---------------------------------------------------- distributed gap ---
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_distributed_gap_matches_gathered(gpu, monkeypatch, world):
+@pytest.mark.parametrize("cut", ["rows", "cols"])
+def test_distributed_gap_matches_gathered(gpu, monkeypatch, world, cut):
     """The sharded solves' normalized duality gap (restarts.hpp:107-220) is
     evaluated without gathering a vector: a bracket search over the global
     event order (rank-local reductions at a sampled key, combined in rank
@@ -480,6 +493,7 @@ def test_distributed_gap_matches_gathered(gpu, monkeypatch, world):
     across ranks), so it agrees to rounding of its terms (1e-6 relative here).
     PDLP_GAPD_FINAL=8 forces the search down to eight events, so the
     bisection rounds run on these small instances."""
+    monkeypatch.setenv("PDLP_SHARD_CUT", cut)
     monkeypatch.setenv("PDLP_GAPD_CHECK", "1")
     monkeypatch.setenv("PDLP_GAPD_FINAL", "8")
     S.gap_dist_stats(reset=True)
