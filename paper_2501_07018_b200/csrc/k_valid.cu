@@ -14,7 +14,15 @@
 //     equal value (binary search), and each row receives exactly as many
 //     column entries as it holds.
 // Together these make the column entries a bijection onto the row entries,
-// which is what the rebuild comparison asserts.
+// which is what the rebuild comparison asserts.  Large layouts take the
+// rebuild itself instead: a stable radix sort of the column entries by row
+// (the column layout lists columns in ascending order, so each row's entries
+// come out in ascending column order -- the row form) compared entry by
+// entry with the row layout: the same rows, columns and values, position for
+// position.  (Sort passes instead of a dependent binary search per entry:
+// C2, 165.7M entries, 21 -> ~5 ms.)
+
+#include <cub/cub.cuh>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -117,6 +125,25 @@ __global__ void match_kernel(const P* __restrict__ rstart, const int32_t* __rest
   }
 }
 
+__global__ void iota_kernel(int32_t* v, int64_t n) {
+  GRID_STRIDE(k, n) v[k] = static_cast<int32_t>(k);
+}
+
+// Position q of the rebuilt row form: row skeys[q], column col_of[k], value
+// cval[k] (k = the column-layout position) against the row layout's entry q.
+__global__ void rebuilt_match_kernel(const int32_t* __restrict__ skeys,
+                                     const int32_t* __restrict__ svals,
+                                     const int32_t* __restrict__ row_of,
+                                     const int32_t* __restrict__ ridx,
+                                     const double* __restrict__ rval,
+                                     const int32_t* __restrict__ col_of,
+                                     const double* __restrict__ cval, int64_t nnz, unsigned* bad) {
+  GRID_STRIDE(q, nnz) {
+    const int32_t k = svals[q];
+    if (skeys[q] != row_of[q] || ridx[q] != col_of[k] || !(rval[q] == cval[k])) atomicOr(bad, 8u);
+  }
+}
+
 template <class P>
 __global__ void count_check_kernel(const P* __restrict__ rstart, int64_t dim,
                                    const int* __restrict__ row_count, unsigned* bad) {
@@ -161,6 +188,34 @@ extern "C" int pdlpk_validate_consistency(const pdlpk_csr* R, const int32_t* row
                                           int* row_count, unsigned* bad, cudaStream_t s) {
   const int64_t nnz = R->nnz;
   if (nnz > 1) sorted_check_kernel<<<ew_blocks(nnz - 1), kT, 0, s>>>(R->index, row_of, nnz, bad);
+  if (nnz >= (int64_t(1) << 20) && nnz < (int64_t(1) << 31)) {
+    int end_bit = 1;
+    while (end_bit < 31 && (int64_t(1) << end_bit) < R->dim) ++end_bit;
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, static_cast<const int32_t*>(nullptr),
+                                    static_cast<int32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
+                                    static_cast<int32_t*>(nullptr), static_cast<int>(nnz), 0, end_bit, s);
+    char* buf = nullptr;
+    const size_t arr = (static_cast<size_t>(nnz) * 4 + 255) & ~size_t(255);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&buf), 3 * arr + tmp_bytes, s) == cudaSuccess) {
+      int32_t* skeys = reinterpret_cast<int32_t*>(buf);
+      int32_t* vin = reinterpret_cast<int32_t*>(buf + arr);
+      int32_t* svals = reinterpret_cast<int32_t*>(buf + 2 * arr);
+      iota_kernel<<<ew_blocks(nnz), kT, 0, s>>>(vin, nnz);
+      const cudaError_t e = cub::DeviceRadixSort::SortPairs(buf + 3 * arr, tmp_bytes, Cl->index, skeys,
+                                                           vin, svals, static_cast<int>(nnz), 0,
+                                                           end_bit, s);
+      if (e == cudaSuccess) {
+        rebuilt_match_kernel<<<ew_blocks(nnz), kT, 0, s>>>(skeys, svals, row_of, R->index,
+                                                           R->value_orig, col_of, Cl->value_orig,
+                                                           nnz, bad);
+      }
+      cudaFreeAsync(buf, s);
+      if (e != cudaSuccess) return static_cast<int>(e);
+      return static_cast<int>(cudaGetLastError());
+    }
+    cudaGetLastError();  // out of memory: the binary-search form below
+  }
   cudaMemsetAsync(row_count, 0, (R->dim > 0 ? R->dim : 1) * sizeof(int), s);
   if (nnz > 0) {
     if (R->wide) {

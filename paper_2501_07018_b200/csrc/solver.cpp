@@ -3181,11 +3181,17 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
     E.fill_panels();
   }
   if (E.dist() && E.gap_whole()) E.build_full_views();
-  if (o->enable_polish) {
+  // Polishing is only considered at a cadence point k >= 100 below the
+  // iteration budget (solver.hpp:395-401; the first trigger is 100).
+  const int64_t ci = o->check_interval > 0 ? o->check_interval : 64;
+  const int64_t first_polish_k = (100 + ci - 1) / ci * ci;
+  if (o->enable_polish && first_polish_k < o->iteration_limit) {
     // The polishing subproblems' states are allocated mid-loop, the first
     // time polishing triggers.  Growing the pool then costs 10-300 ms of
     // driver time; reserve it now (freed blocks stay in the retaining pool
-    // and are sub-allocated later).
+    // and are sub-allocated later).  (A solve whose budget ends before the
+    // first possible trigger skips it: the 4.7 GB reserve of C2 costs
+    // 40-55 ms even on a warm pool.)
     const int64_t nl = E.problem().n, ml = E.problem().m;
     DevBuf<char> reserve(static_cast<size_t>(inner_bytes(nl, ml) + inner_bytes(ml, nl)));
   }

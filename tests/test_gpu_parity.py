@@ -412,6 +412,32 @@ def test_validation_messages_match_reference(gpu, ref, kind):
     assert str(ours.value) == str(theirs.value)
 
 
+@pytest.mark.parametrize("kind", ["value", "row_swap", "dup_row", "none"])
+def test_layout_consistency_rebuild_on_large_layouts(gpu, kind):
+    """Layouts of >= 2^20 entries are checked by rebuilding the row form from
+    the column form (stable radix sort by row) and comparing position by
+    position: a changed value, two rows exchanged inside a column, or a
+    column listing one row twice are rejected with the reference's message;
+    consistent layouts solve."""
+    p = P.generate("c2", 1, rows=100000, cols=200000)
+    assert p.a.nonzeros() >= 1 << 20
+    C = p.a.by_col
+    j = next(j for j in range(p.cols()) if C.start[j + 1] - C.start[j] >= 3)
+    k = C.start[j]
+    if kind == "value":
+        C.value[k + 1] *= 1.0 + 2.0 ** -40
+    elif kind == "row_swap":  # two entries of the column trade rows
+        C.index[k], C.index[k + 1] = C.index[k + 1], C.index[k]
+    elif kind == "dup_row":
+        C.index[k + 1] = C.index[k]
+    o = P.SolverOptions(mode="perf", iteration_limit=2)
+    if kind == "none":
+        assert P.solve(p, o).iterations == 2
+        return
+    with pytest.raises(ValueError, match="row/column layouts disagree"):
+        P.solve(p, o)
+
+
 @pytest.mark.parametrize("kind", ["index_wraps", "index_huge", "index_negative", "start_wraps",
                                   "index_wraps_staged"])
 def test_out_of_range_layout_values_are_rejected(gpu, ref, kind):

@@ -8,7 +8,10 @@ traffic (bench.py reads profiles/ncu_traffic.json as roofline.traffic).
 
 The row pass of a layout with column panels is several launches
 (row_pass<..., 1> first panel, <..., 2> middle, <..., 3> last): their traffic
-is summed into `row_pass`, whose algorithmic bytes are the whole pass's.
+is summed into `row_pass`, whose algorithmic bytes are the whole pass's.  A
+split column pass (segmented-span layouts: `col_product` writes d = K'dy,
+`col_epi_decide` runs the epilogue and the decision) is summed into
+`col_pass` the same way.
 """
 import argparse
 import csv
@@ -59,11 +62,13 @@ def main() -> None:
     for d in data:
         k = short(d[idx["Kernel Name"]])
         base = k.split("<")[0]
+        if base in ("col_product", "col_epi_decide"):
+            base = "col_pass"
         rd, wr = val(d, "dram__bytes_read.sum"), val(d, "dram__bytes_write.sum")
         traffic[base] = traffic.get(base, 0.0) + rd + wr
         lines.append(
             f"| `{k}` | {val(d, 'gpu__time_duration.sum') * 1e6:.1f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} | "
-            f"{alg.get(base, 0) / 1e6:.1f}{' (whole pass)' if base == 'row_pass' and re.search(r', [123]>$', k) else ''} | "
+            f"{alg.get(base, 0) / 1e6:.1f}{' (whole pass)' if (base == 'row_pass' and re.search(r', [123]>$', k)) or k.startswith(('col_product', 'col_epi')) else ''} | "
             f"{val(d, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
             f"{val(d, 'lts__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
             f"{val(d, 'l1tex__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
