@@ -219,6 +219,18 @@ int pdlp_device_count(void);
  * pool and keep it between calls (no map/unmap per solve); this returns the
  * pool's unused memory on `device` to the driver.  0 or a negative error. */
 int pdlp_trim_device_memory(int device);
+/* B200 extension.  Page-lock caller memory (cudaHostRegister, portable) for
+ * the solves that read or write it: a problem's arrays registered this way
+ * upload with one DMA each (64-bit indices narrowed on the device) instead of
+ * through the pinned staging ring's host copies; registered result buffers
+ * are filled by DMA.  Unregister before freeing the memory. */
+int pdlp_host_register(void* ptr, size_t bytes);
+int pdlp_host_unregister(void* ptr);
+/* B200 extension.  Page-locked host allocation (cudaHostAlloc, portable) for
+ * a caller that builds its problem or result buffers in pinned memory
+ * directly (where registering existing pages is not permitted). */
+int pdlp_host_alloc(size_t bytes, void** out);
+int pdlp_host_free(void* ptr);
 /* B200 extension.  Counters of the sharded solves' distributed normalized
  * gap (restarts.hpp:107-220 evaluated without gathering a vector, DESIGN.md
  * §8): out[0..3] = evaluations, bracket-search rounds, events swept after

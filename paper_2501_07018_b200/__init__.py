@@ -9,7 +9,9 @@ from .problem import (CompressedLayout, LpProblem, SparseMatrix, generate, gener
 from .solver import (CertificateKind, InfeasibilityCertificate, IterationRecord, ResidualSummary,
                      RestartThresholds, SolveResult, SolverOptions, SolveStatus,
                      TerminationTolerances, adaptive_step, apply_rescaling, device_count,
-                     kkt_residuals, normalized_duality_gap, pdhg_step, solve, solve_status_name,
+                     kkt_residuals, normalized_duality_gap, pdhg_step, pinned, pinned_copy,
+                     pinned_empty, solve,
+                     solve_status_name,
                      spmv, spmv_transpose, step_size_rules)
 
 from .mps import MpsModel, parse_mps, read_mps, write_mps, write_mps_file

@@ -214,6 +214,10 @@ SOLVER_SIGNATURES = {
     "pdlp_abi_version": (C.c_int, []),
     "pdlp_device_count": (C.c_int, []),
     "pdlp_trim_device_memory": (C.c_int, [C.c_int]),
+    "pdlp_host_register": (C.c_int, [C.c_void_p, C.c_size_t]),
+    "pdlp_host_unregister": (C.c_int, [C.c_void_p]),
+    "pdlp_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "pdlp_host_free": (C.c_int, [C.c_void_p]),
     "pdlp_gap_dist_stats": (None, [C.POINTER(C.c_int64), c_double_p, C.c_int32]),
     "pdlp_shard_plan_for": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32,
                                       C.POINTER(ShardPlan)]),

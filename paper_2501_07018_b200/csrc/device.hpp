@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <map>
+#include <mutex>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstddef>
@@ -54,6 +57,92 @@ inline void retain_pool_memory(int device) {
   done[device] = true;
 }
 
+// Exact-size cache of stream-ordered blocks across solves (a caching layer
+// over the pool): a released buffer goes into it with an event recorded on
+// its stream; a later allocation of the same byte size on the same device
+// takes it back after the allocating stream waits for that event.  Repeated
+// solves of one problem then allocate nothing -- the pool's own reuse of
+// blocks freed on another (since destroyed) stream still mapped memory,
+// 2-5 ms per large buffer.  Bounded (PDLP_BLOCK_CACHE_MB, default 49152;
+// 0 disables it); pdlp_trim_device_memory empties it; an allocation that
+// fails empties it and retries.
+class BlockCache {
+ public:
+  static BlockCache& get() {
+    static BlockCache* c = new BlockCache();  // leaked: outlives static teardown
+    return *c;
+  }
+  void* take(size_t bytes, cudaStream_t s) {
+    if (cap_ == 0) return nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = free_.find(std::make_pair(dev, bytes));
+    if (it == free_.end() || it->second.empty()) return nullptr;
+    Block b = it->second.back();
+    it->second.pop_back();
+    held_ -= bytes;
+    cudaStreamWaitEvent(s, b.ev, 0);
+    cudaEventDestroy(b.ev);  // released once the wait is satisfied
+    return b.p;
+  }
+  bool give(void* p, size_t bytes, cudaStream_t s) {
+    if (cap_ == 0) return false;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    std::lock_guard<std::mutex> g(mu_);
+    if (held_ + bytes > cap_) return false;
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (cudaEventRecord(ev, s) != cudaSuccess) {
+      cudaGetLastError();
+      cudaEventDestroy(ev);
+      return false;
+    }
+    free_[std::make_pair(dev, bytes)].push_back(Block{p, ev});
+    held_ += bytes;
+    return true;
+  }
+  // Frees every cached block of `device` (-1: all devices).
+  void trim(int device) {
+    std::lock_guard<std::mutex> g(mu_);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto it = free_.begin(); it != free_.end();) {
+      if (device >= 0 && it->first.first != device) {
+        ++it;
+        continue;
+      }
+      cudaSetDevice(it->first.first);
+      for (Block& b : it->second) {
+        cudaEventSynchronize(b.ev);
+        cudaEventDestroy(b.ev);
+        cudaFree(b.p);
+        held_ -= it->first.second;
+      }
+      it = free_.erase(it);
+    }
+    cudaSetDevice(cur);
+  }
+
+ private:
+  BlockCache() {
+    const char* e = std::getenv("PDLP_BLOCK_CACHE_MB");
+    const long long mb = e != nullptr ? std::atoll(e) : 49152;
+    cap_ = mb > 0 ? static_cast<size_t>(mb) << 20 : 0;
+  }
+  struct Block {
+    void* p;
+    cudaEvent_t ev;
+  };
+  std::mutex mu_;
+  std::map<std::pair<int, size_t>, std::vector<Block>> free_;
+  size_t held_ = 0, cap_ = 0;
+};
+
 class AllocStreamScope {
  public:
   explicit AllocStreamScope(cudaStream_t s) : prev_(g_alloc_stream) { g_alloc_stream = s; }
@@ -99,7 +188,13 @@ class DevBuf {
     s_ = g_alloc_stream;
     const auto t0 = std::chrono::steady_clock::now();
     if (s_ != nullptr) {
-      PDLP_CK(cudaMallocAsync(&p, n * sizeof(T) + 64, s_));
+      const size_t bytes = n * sizeof(T) + 64;
+      p = BlockCache::get().take(bytes, s_);
+      if (p == nullptr && cudaMallocAsync(&p, bytes, s_) != cudaSuccess) {
+        cudaGetLastError();  // out of memory: return the cached blocks, retry
+        BlockCache::get().trim(-1);
+        PDLP_CK(cudaMallocAsync(&p, bytes, s_));
+      }
     } else {
       PDLP_CK(cudaMalloc(&p, n * sizeof(T) + 64));
     }
@@ -114,7 +209,7 @@ class DevBuf {
   void release() {
     if (p_ != nullptr) {
       if (s_ != nullptr) {
-        cudaFreeAsync(p_, s_);
+        if (!BlockCache::get().give(p_, n_ * sizeof(T) + 64, s_)) cudaFreeAsync(p_, s_);
       } else {
         cudaFree(p_);
       }

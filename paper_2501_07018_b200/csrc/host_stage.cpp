@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "device.hpp"
+#include "kernels.h"
 
 namespace pdlp_host {
 namespace {
@@ -224,9 +225,21 @@ void stage_report(double* wait_s, double* copy_s, double* mbytes) {
   g_wait_s = g_copy_s = g_bytes = 0.0;
 }
 
+// Page-locked host memory (cudaHostAlloc'd or registered, e.g. through
+// pdlp_host_register): the copy engine reads it directly, so uploads from it
+// skip the ring's host copies.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 void stage_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return;
-  if (bytes <= kDirectMax || !ring().ok) {
+  if (bytes <= kDirectMax || !ring().ok || is_pinned(src)) {
     PDLP_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return;
   }
@@ -235,6 +248,24 @@ void stage_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 
 void stage_h2d_narrow(int32_t* dst, const int64_t* src, size_t count, cudaStream_t s) {
   if (count == 0) return;
+  if (count * 8 > kDirectMax && is_pinned(src)) {
+    // pinned source: DMA the 64-bit values into a device chunk, narrow there
+    // (same saturation as the host path); stream order reuses the chunk
+    const size_t chunk = std::min(count, size_t(32) << 20);
+    int64_t* tmp = nullptr;  // allocated and freed on s: ordered after its last use
+    PDLP_CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), chunk * 8, s));
+    cudaError_t err = cudaSuccess;
+    for (size_t off = 0; off < count && err == cudaSuccess; off += chunk) {
+      const size_t n = std::min(chunk, count - off);
+      err = cudaMemcpyAsync(tmp, src + off, n * 8, cudaMemcpyHostToDevice, s);
+      if (err == cudaSuccess) {
+        err = static_cast<cudaError_t>(pdlpk_narrow_i64(tmp, dst + off, static_cast<int64_t>(n), s));
+      }
+    }
+    cudaFreeAsync(tmp, s);
+    PDLP_CK(err);
+    return;
+  }
   if (!ring().ok || count * 8 <= kDirectMax) {
     // small: narrow on the host into a temporary, one pageable copy
     std::vector<int32_t> tmp(count);
@@ -252,7 +283,7 @@ void stage_h2d_narrow(int32_t* dst, const int64_t* src, size_t count, cudaStream
 void stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return;
   Ring& R = ring();
-  if (bytes <= kDirectMax || !R.ok) {
+  if (bytes <= kDirectMax || !R.ok || is_pinned(dst)) {
     PDLP_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
     PDLP_CK(cudaStreamSynchronize(s));
     return;

@@ -33,6 +33,10 @@ void stage_h2d_narrow(int32_t* dst, const int64_t* src, size_t count, cudaStream
 // pageable cudaMemcpy).
 void stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
+// Whether p is page-locked host memory (uploads from / downloads into it
+// bypass the ring: one DMA, indices narrowed on the device).
+bool is_pinned(const void* p);
+
 // Staged upload time since the last call: waiting for ring slots (DMA-bound)
 // vs host copies into them (copy-bound), and the bytes staged.
 void stage_report(double* wait_s, double* copy_s, double* mbytes);

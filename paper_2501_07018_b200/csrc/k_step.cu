@@ -938,6 +938,42 @@ static pdlpk_step_args launch_row(const pdlpk_step_args* a, cudaStream_t s, bool
   return b;
 }
 
+// PDLP_DY_PERSIST=1 (measurement knob, perf mode): the column pass's gathers
+// of dy go through a persisting L2 access-policy window (dy stays resident
+// while the matrix streams pass with evict_first).
+static bool dy_persist_on(const pdlpk_step_args* a) {
+  static const int on = [] {
+    const char* e = std::getenv("PDLP_DY_PERSIST");
+    return e != nullptr && e[0] == '1' ? 1 : 0;
+  }();
+  if (!on || a->dy == nullptr || a->P.m <= 0) return false;
+  static int limit_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (limit_dev != dev) {
+    size_t want = static_cast<size_t>(a->P.m) * 8;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    cudaGetLastError();
+    limit_dev = dev;
+  }
+  return true;
+}
+
+static void dy_window(cudaStream_t s, const pdlpk_step_args* a, bool set) {
+  cudaStreamAttrValue v{};
+  if (set) {
+    v.accessPolicyWindow.base_ptr = const_cast<double*>(a->dy);
+    v.accessPolicyWindow.num_bytes = static_cast<size_t>(a->P.m) * 8;
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  } else {
+    v.accessPolicyWindow.num_bytes = 0;
+  }
+  cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();
+}
+
 extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
   const bool pdl = a->mode == 0;  // perf mode: the three kernels chain with PDL
   launch_pdl(pdl, primal_pass<false>, static_cast<unsigned>(ew_blocks(a->P.n)), kEwThreads, 0, s,
@@ -946,7 +982,10 @@ extern "C" int pdlpk_attempt(const pdlpk_step_args* a, cudaStream_t s) {
     // Degenerate shapes (an empty side) still need the decision, which the
     // column pass performs: it always has >= 1 CTA (short_blocks >= 1).
     const pdlpk_step_args c = launch_row(a, s, true);
+    const bool persist = dy_persist_on(a);
+    if (persist) dy_window(s, a, true);
     dispatch_p(c.P.KT, LaunchRowCol{&c, s, false, true, true});
+    if (persist) dy_window(s, a, false);
   } else {
     const int gm = ew_blocks(a->P.m), gn = ew_blocks(a->P.n);
     if (a->P.K.wide) {
@@ -970,7 +1009,10 @@ extern "C" int pdlpk_attempt_timed(const pdlpk_step_args* a, cudaEvent_t* ev, cu
   if (a->mode == 0) {
     const pdlpk_step_args c = launch_row(a, s, false);
     cudaEventRecord(ev[2], s);
+    const bool persist = dy_persist_on(a);
+    if (persist) dy_window(s, a, true);
     dispatch_p(c.P.KT, LaunchRowCol{&c, s, false});
+    if (persist) dy_window(s, a, false);
   } else {
     const int gm = ew_blocks(a->P.m), gn = ew_blocks(a->P.n);
     if (a->P.K.wide) {

@@ -125,6 +125,13 @@ __global__ void match_kernel(const P* __restrict__ rstart, const int32_t* __rest
   }
 }
 
+__global__ void narrow_kernel(const int64_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n) {
+  GRID_STRIDE(k, n) {
+    const int64_t x = src[k];
+    dst[k] = x < 0 ? -1 : (x > INT32_MAX ? INT32_MAX : static_cast<int32_t>(x));
+  }
+}
+
 __global__ void iota_kernel(int32_t* v, int64_t n) {
   GRID_STRIDE(k, n) v[k] = static_cast<int32_t>(k);
 }
@@ -180,6 +187,11 @@ extern "C" int pdlpk_validate_raw_layout32(const int32_t* start, int64_t dim, co
                                            unsigned* bad, cudaStream_t s) {
   if (start != nullptr) ptr_check_kernel<<<ew_blocks(dim + 1), kT, 0, s>>>(start, dim, nnz, bad);
   if (idx != nullptr && count > 0) index_range_kernel<<<ew_blocks(count), kT, 0, s>>>(idx, count, bound, bad);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_narrow_i64(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s) {
+  if (n > 0) narrow_kernel<<<ew_blocks(n), kT, 0, s>>>(src, dst, n);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -492,6 +492,9 @@ int pdlpk_radius(const double* dx2, const double* dy2, double omega, double* out
                  cudaStream_t s);
 
 /* ------------------------------------------------------- preconditioning --- */
+/* dst[k] = src[k] narrowed to int32 with the host stager's saturation
+ * (x < 0 -> -1, x > INT32_MAX -> INT32_MAX), for uploads from pinned memory. */
+int pdlpk_narrow_i64(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t s);
 /* line_of[k] = line owning entry k (max-scan over line heads; k_scale.cu). */
 size_t pdlpk_line_of_work_bytes(int64_t nnz);
 int pdlpk_line_of(const pdlpk_csr* A, int32_t* line_of, void* work, size_t work_bytes,

@@ -3192,8 +3192,18 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
     // and are sub-allocated later).  (A solve whose budget ends before the
     // first possible trigger skips it: the 4.7 GB reserve of C2 costs
     // 40-55 ms even on a warm pool.)
+    // (Straight to the pool: through DevBuf the block would park in the
+    // block cache instead of growing the pool.)
     const int64_t nl = E.problem().n, ml = E.problem().m;
-    DevBuf<char> reserve(static_cast<size_t>(inner_bytes(nl, ml) + inner_bytes(ml, nl)));
+    void* reserve = nullptr;
+    const size_t rb = static_cast<size_t>(inner_bytes(nl, ml) + inner_bytes(ml, nl));
+    const auto tr = std::chrono::steady_clock::now();
+    if (cudaMallocAsync(&reserve, rb, E.s()) == cudaSuccess) {
+      cudaFreeAsync(reserve, E.s());
+    } else {
+      cudaGetLastError();
+    }
+    g_alloc_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - tr).count();
   }
   const pdlpk_problem P = E.problem().view();
 
@@ -3584,11 +3594,37 @@ int pdlp_solve_sharded_emulated(const pdlp_problem_view* problem, const pdlp_opt
   return PDLP_OK;
 }
 
+int pdlp_host_register(void* ptr, size_t bytes) {
+  if (ptr == nullptr || bytes == 0) return PDLP_OK;
+  return guarded([&] { PDLP_CK(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable)); });
+}
+
+int pdlp_host_unregister(void* ptr) {
+  if (ptr == nullptr) return PDLP_OK;
+  return guarded([&] { PDLP_CK(cudaHostUnregister(ptr)); });
+}
+
+int pdlp_host_alloc(size_t bytes, void** out) {
+  if (out == nullptr) {
+    g_last_error = "null argument";
+    return PDLP_ERR_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  if (bytes == 0) return PDLP_OK;
+  return guarded([&] { PDLP_CK(cudaHostAlloc(out, bytes, cudaHostAllocPortable)); });
+}
+
+int pdlp_host_free(void* ptr) {
+  if (ptr == nullptr) return PDLP_OK;
+  return guarded([&] { PDLP_CK(cudaFreeHost(ptr)); });
+}
+
 int pdlp_trim_device_memory(int device) {
   return guarded([&] {
     cudaMemPool_t pool;
     PDLP_CK(cudaSetDevice(device));
     PDLP_CK(cudaDeviceSynchronize());
+    BlockCache::get().trim(device);
     PDLP_CK(cudaDeviceGetDefaultMemPool(&pool, device));
     PDLP_CK(cudaMemPoolTrimTo(pool, 0));
   });

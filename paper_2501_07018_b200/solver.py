@@ -213,11 +213,14 @@ def _check(rc: int) -> None:
 
 
 def run_solve(lib, fn_name: str, p: LpProblem | None, options: SolverOptions, c_opts: N.Options,
-              extra: tuple = (), first_arg=None, dims: tuple | None = None) -> SolveResult:
+              extra: tuple = (), first_arg=None, dims: tuple | None = None,
+              out: dict | None = None) -> SolveResult:
     """Shared marshalling for pdlp_solve, the sharded solves (extra = the
     arguments between options and result) and the oracle's ref_solve.  The
     shard-local solves pass no problem: first_arg is their shard argument
-    and dims = (rows, cols) of the whole problem."""
+    and dims = (rows, cols) of the whole problem.  out: caller buffers for
+    x / y / reduced_costs (float64, contiguous; e.g. registered with
+    `pinned`, so the results come back by DMA)."""
     t_prep = time.perf_counter()
     if p is not None:
         view = p.view()
@@ -225,9 +228,19 @@ def run_solve(lib, fn_name: str, p: LpProblem | None, options: SolverOptions, c_
         m, n = p.rows(), p.cols()
     else:
         m, n = dims
-    x = np.zeros(n)
-    y = np.zeros(m)
-    r = np.zeros(n)
+
+    def buf(name, size):
+        a = (out or {}).get(name)
+        if a is None:
+            return np.zeros(size)
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+                and a.shape == (size,)):
+            raise ValueError(f"out[{name!r}] must be a contiguous float64 array of {size}")
+        return a
+
+    x = buf("x", n)
+    y = buf("y", m)
+    r = buf("reduced_costs", n)
     rx = np.zeros(n)
     ry = np.zeros(m)
     rr = np.zeros(n)
@@ -275,10 +288,94 @@ def run_solve(lib, fn_name: str, p: LpProblem | None, options: SolverOptions, c_
         kernel_seconds=list(res.kernel_seconds), kernel_launches=list(res.kernel_launches))
 
 
-def solve(problem: LpProblem, options: SolverOptions | None = None) -> SolveResult:
-    """pdhglp::solve on the GPU (solver.hpp:535-608)."""
+def solve(problem: LpProblem, options: SolverOptions | None = None,
+          out: dict | None = None) -> SolveResult:
+    """pdhglp::solve on the GPU (solver.hpp:535-608).  out: optional caller
+    buffers {"x", "y", "reduced_costs"} the result is written into."""
     options = options or SolverOptions()
-    return run_solve(N.lib(), "pdlp_solve", problem, options, to_c_options(options))
+    return run_solve(N.lib(), "pdlp_solve", problem, options, to_c_options(options), out=out)
+
+
+class _PinnedBlock:
+    """One pdlp_host_alloc block; freed when the last array over it dies."""
+
+    def __init__(self, nbytes: int):
+        self.ptr = C.c_void_p()
+        _check(N.lib().pdlp_host_alloc(max(int(nbytes), 1), C.byref(self.ptr)))
+
+    def __del__(self):
+        if getattr(self, "ptr", None) is not None and self.ptr.value:
+            N.lib().pdlp_host_free(self.ptr)
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """An uninitialised numpy array in page-locked host memory
+    (pdlp_host_alloc): solves read it / write it by DMA."""
+    dt = np.dtype(dtype)
+    count = int(np.prod(shape)) if np.ndim(shape) else int(shape)
+    blk = _PinnedBlock(count * dt.itemsize)
+    buf = (C.c_char * max(count * dt.itemsize, 1)).from_address(blk.ptr.value)
+    buf._pinned_block = blk  # the array keeps buf alive, buf keeps the block
+    return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
+
+
+def pinned_copy(problem: LpProblem) -> LpProblem:
+    """The same LP with every array copied into page-locked host memory:
+    solves of the copy upload by DMA (64-bit indices narrowed on the
+    device) instead of through the pinned staging ring's host copies."""
+    from .problem import CompressedLayout, SparseMatrix
+
+    def cp(a):
+        out = pinned_empty(a.shape, a.dtype)
+        np.copyto(out, a)
+        return out
+
+    a = problem.a
+    lay = lambda L: CompressedLayout(cp(L.start), cp(L.index), cp(L.value))  # noqa: E731
+    problem.view()  # normalises the vectors to contiguous float64 first
+    return LpProblem(SparseMatrix(a.rows, a.cols, lay(a.by_row), lay(a.by_col)),
+                     cp(problem.objective), cp(problem.con_lower), cp(problem.con_upper),
+                     cp(problem.var_lower), cp(problem.var_upper))
+
+
+class pinned:
+    """Page-lock host arrays for the solves inside the block (B200 extension,
+    pdlp_host_register): a problem registered this way uploads with one DMA
+    per array (64-bit indices narrowed on the device) instead of through the
+    pinned staging ring's host copies, and registered result buffers (solve's
+    `out`) are filled by DMA.  Accepts LpProblem and numpy arrays.
+
+        with P.pinned(problem, x, y, r):
+            P.solve(problem, options, out={"x": x, "y": y, "reduced_costs": r})
+    """
+
+    def __init__(self, *objs):
+        self._arrays = []
+        for o in objs:
+            if isinstance(o, LpProblem):
+                for lay in (o.a.by_row, o.a.by_col):
+                    self._arrays += [lay.start, lay.index, lay.value]
+                o.view()  # normalises the vectors to contiguous float64 first
+                self._arrays += [o.objective, o.con_lower, o.con_upper, o.var_lower, o.var_upper]
+            else:
+                self._arrays.append(o)
+        self._done = []
+
+    def __enter__(self):
+        lib = N.lib()
+        for a in self._arrays:
+            if isinstance(a, np.ndarray) and a.nbytes > 0 and a.flags.c_contiguous:
+                _check(lib.pdlp_host_register(a.ctypes.data, a.nbytes))
+                self._done.append(a)
+        return self
+
+    def __exit__(self, *exc):
+        lib = N.lib()
+        for a in self._done:
+            lib.pdlp_host_unregister(a.ctypes.data)
+        self._done = []
+        return False
 
 
 # ------------------------------------------------------ component entries ---

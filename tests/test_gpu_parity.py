@@ -567,3 +567,21 @@ def test_forced_schedules_on_ragged_problems(gpu, ref, monkeypatch, knobs):
         if r.status == P.SolveStatus.OPTIMAL:
             assert abs(g.summary.primal_objective - r.summary.primal_objective) <= 1e-5 * (
                 1.0 + abs(r.summary.primal_objective))
+
+
+def test_pinned_problem_and_outputs_solve_identically(gpu):
+    """A problem held in page-locked memory (pinned_copy) uploads by DMA with
+    its 64-bit indices narrowed on the device, and page-locked result buffers
+    are filled by DMA: the solve is the pageable one bit for bit."""
+    p = P.generate("c2", 3, rows=60000, cols=120000)  # layouts above the 1 MB direct-copy size
+    o = P.SolverOptions(mode="perf", iteration_limit=40,
+                        tolerances=P.TerminationTolerances(0.0, 0.0, 0.0))
+    a = P.solve(p, o)
+    pp = P.pinned_copy(p)
+    out = {"x": P.pinned_empty(p.cols()), "y": P.pinned_empty(p.rows()),
+           "reduced_costs": P.pinned_empty(p.cols())}
+    b = P.solve(pp, o, out=out)
+    assert b.x is out["x"]
+    assert a.iterations == b.iterations == 40
+    assert same_bits(a.x, b.x) and same_bits(a.y, b.y)
+    assert same_bits(a.reduced_costs, b.reduced_costs)
