@@ -62,6 +62,7 @@ struct GapScalars {
   unsigned long long above_min;       // smallest key above the window
   unsigned long long above_count;     // events above the window
   double above[2];                    // their masses (c, b), tree order
+  int est_ra, est_rb;                 // estimated window: sample ranks (rb < 0: to the bottom)
 };
 
 struct Work {
@@ -73,6 +74,8 @@ struct Work {
   double *cs, *bs;  // sorted masses (perf scans)
   int32_t* hsel;    // partial sort: slots of the selected (top) events
   uint64_t *samp_in, *samp_out;  // partial sort: key sample and its sort
+  int32_t *sidx_in, *sidx_out;    // estimated window: sample ranks through the sort
+  double *sdc, *sdi;              // ... and the sampled events' masses
   GapScalars* sc;
   void* cub_tmp;
   size_t cub_bytes;
@@ -93,13 +96,17 @@ size_t cub_bytes_for(int64_t N) {
   cub::DeviceSelect::Flagged(nullptr, c, thrust::counting_iterator<int32_t>(0),
                              static_cast<uint8_t*>(nullptr), static_cast<int32_t*>(nullptr),
                              static_cast<int*>(nullptr), static_cast<int>(N));
-  size_t d = 0, e = 0;
+  size_t d = 0, e = 0, f = 0;
   cub::DeviceSelect::Flagged(nullptr, d, static_cast<uint64_t*>(nullptr),
                              static_cast<uint8_t*>(nullptr), static_cast<uint64_t*>(nullptr),
                              static_cast<int*>(nullptr), static_cast<int>(N));
   cub::DeviceRadixSort::SortKeysDescending(nullptr, e, static_cast<uint64_t*>(nullptr),
                                            static_cast<uint64_t*>(nullptr), kGapSample);
-  return std::max(std::max(a, std::max(b, c)), std::max(d, e));
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, f, static_cast<uint64_t*>(nullptr),
+                                            static_cast<uint64_t*>(nullptr),
+                                            static_cast<int32_t*>(nullptr),
+                                            static_cast<int32_t*>(nullptr), kGapSample);
+  return std::max(std::max(std::max(a, f), std::max(b, c)), std::max(d, e));
 }
 
 Work carve(void* base, int64_t n, int64_t m) {
@@ -124,6 +131,10 @@ Work carve(void* base, int64_t n, int64_t m) {
   w.hsel = reinterpret_cast<int32_t*>(take(4 * N));
   w.samp_in = reinterpret_cast<uint64_t*>(take(8 * kGapSample));
   w.samp_out = reinterpret_cast<uint64_t*>(take(8 * kGapSample));
+  w.sidx_in = reinterpret_cast<int32_t*>(take(4 * kGapSample));
+  w.sidx_out = reinterpret_cast<int32_t*>(take(4 * kGapSample));
+  w.sdc = reinterpret_cast<double*>(take(8 * kGapSample));
+  w.sdi = reinterpret_cast<double*>(take(8 * kGapSample));
   w.sc = reinterpret_cast<GapScalars*>(take(sizeof(GapScalars)));
   w.cub_bytes = cub_bytes_for(N);
   w.cub_tmp = take(w.cub_bytes);
@@ -356,6 +367,76 @@ __global__ void base_full_kernel(Work w) {
   w.sc->above_count = 0;
 }
 
+// First evaluation of a (subproblem, query) -- no previous crossing depth to
+// place a window: the strided sample carries its events' masses, is sorted,
+// and one CTA scans it with the masses scaled by E / S to estimate where
+// phi first reaches r^2; the window is the sample ranks around it.  A miss
+// falls back to the full sort (gap_window returns 0), so the estimate only
+// decides the cost, never the value.
+__global__ void sample_masses_kernel(Work w, int64_t E) {
+  pdl_wait_cadence();
+  GRID_STRIDE(i, kGapSample) {
+    const int64_t pos = (i * E) / kGapSample;
+    const int32_t t = w.sel[pos];
+    w.samp_in[i] = w.keys_in[pos];
+    w.sidx_in[i] = static_cast<int32_t>(i);
+    w.sdc[i] = w.dc[t];
+    w.sdi[i] = w.di[t];
+  }
+}
+
+constexpr int kEstThreads = 1024;
+constexpr int kEstPer = kGapSample / kEstThreads;
+__global__ void __launch_bounds__(kEstThreads) estimate_window_kernel(Work w, int64_t E, double r,
+                                                                      int margin) {
+  pdl_wait_cadence();
+  const double scale = static_cast<double>(E) / kGapSample;
+  const double r2 = r * r;
+  const int j0 = threadIdx.x * kEstPer;
+  double c = 0.0, b = 0.0;
+  for (int j = j0; j < j0 + kEstPer; ++j) {
+    const int32_t q = w.sidx_out[j];
+    c += w.sdc[q];
+    b += w.sdi[q];
+  }
+  using Scan = cub::BlockScan<double, kEstThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  double cx, bx;
+  Scan(tmp).ExclusiveSum(c, cx);
+  __syncthreads();
+  Scan(tmp).ExclusiveSum(b, bx);
+  __shared__ int hit;
+  if (threadIdx.x == 0) hit = kGapSample;
+  __syncthreads();
+  double cs = cx, bs = bx;  // sample masses above rank j
+  for (int j = j0; j < j0 + kEstPer; ++j) {
+    const double lam = key_value(w.samp_out[j]);
+    const double phi = (w.sc->sums[1] + scale * cs) + (w.sc->sums[0] + scale * bs) / (lam * lam);
+    if (phi >= r2) {
+      atomicMin(&hit, j);
+      break;
+    }
+    const int32_t q = w.sidx_out[j];
+    cs += w.sdc[q];
+    bs += w.sdi[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int h = hit;
+    w.sc->est_ra = h - margin > 0 ? h - margin : 0;
+    w.sc->est_rb = h + margin < kGapSample - 1 ? h + margin : -1;
+  }
+}
+
+__global__ void window_keys_est_kernel(Work w) {
+  pdl_wait_cadence();
+  const int ra = w.sc->est_ra, rb = w.sc->est_rb;
+  w.sc->hi_key = ra > 0 ? w.samp_out[ra] : ~0ull;
+  w.sc->lo_key = rb >= 0 ? w.samp_out[rb] : 0ull;
+  w.sc->above_min = ~0ull;
+  w.sc->above_count = 0;
+}
+
 // Window [lo_key, hi_key] between sample ranks ra (0: no events above) and rb.
 __global__ void window_keys_kernel(Work w, int ra, int rb) {
   pdl_wait_cadence();
@@ -570,6 +651,7 @@ extern "C" size_t pdlpk_gap_work_bytes(int64_t n, int64_t m) {
   const int64_t N = n + 2 * m;
   return align_up(N) + align_up(8 * N) * 3 + align_up(4 * N) + align_up(8 * N) * 2 +
          align_up(4 * N) + align_up(8 * N) * 2 + align_up(4 * N) + 2 * align_up(8 * kGapSample) +
+         2 * align_up(4 * kGapSample) + 2 * align_up(8 * kGapSample) +
          align_up(sizeof(GapScalars)) + align_up(cub_bytes_for(N)) + 256;
 }
 
@@ -634,19 +716,36 @@ thread_local int64_t g_window_stats[2] = {0, 0};  // windows tried, decided
 // with events above, or no hit above the bottom, returns 0 and the full sort
 // runs.  Returns the window's event count when it decided.  Two host syncs
 // (the window count, the hit).
+// qa == -2: the estimated window (first evaluation, see estimate_window_kernel).
 static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const pdlpk_red* red,
                           const double* r_slot, double r_value, cudaStream_t s) {
+  const bool est = qa == -2.0;
+  if (est && r_slot != nullptr) return 0;  // the estimate needs the radius on the host
   launch_pdl(PDLPK_PDL_CADENCE, keys_kernel, static_cast<unsigned>(ew_blocks(E)), kT, 0, s, w, E);
-  launch_pdl(PDLPK_PDL_CADENCE, sample_keys_kernel, static_cast<unsigned>(ew_blocks(kGapSample)), kT, 0, s, w, E);
   size_t bytes = w.cub_bytes;
-  if (cub::DeviceRadixSort::SortKeysDescending(w.cub_tmp, bytes, w.samp_in, w.samp_out, kGapSample,
-                                               0, 64, s) != cudaSuccess) {
-    return -1;
+  int ra = 0, rb = -1;
+  bool to_bottom = true;
+  if (est) {
+    launch_pdl(PDLPK_PDL_CADENCE, sample_masses_kernel, static_cast<unsigned>(ew_blocks(kGapSample)), kT, 0, s, w, E);
+    if (cub::DeviceRadixSort::SortPairsDescending(w.cub_tmp, bytes, w.samp_in, w.samp_out, w.sidx_in,
+                                                  w.sidx_out, kGapSample, 0, 64, s) != cudaSuccess) {
+      return -1;
+    }
+    const int margin = static_cast<int>(0.05 * kGapSample);
+    estimate_window_kernel<<<1, kEstThreads, 0, s>>>(w, E, r_value, margin);
+    launch_pdl(PDLPK_PDL_CADENCE, window_keys_est_kernel, static_cast<unsigned>(1), 1, 0, s, w);
+    ra = 1;  // (unknown on the host: the above-mass reduction always runs)
+  } else {
+    launch_pdl(PDLPK_PDL_CADENCE, sample_keys_kernel, static_cast<unsigned>(ew_blocks(kGapSample)), kT, 0, s, w, E);
+    if (cub::DeviceRadixSort::SortKeysDescending(w.cub_tmp, bytes, w.samp_in, w.samp_out, kGapSample,
+                                                 0, 64, s) != cudaSuccess) {
+      return -1;
+    }
+    ra = qa <= 0.0 ? 0 : std::min(kGapSample - 1, static_cast<int>(qa * kGapSample));
+    to_bottom = qb >= 1.0;
+    rb = to_bottom ? -1 : std::min(kGapSample - 1, static_cast<int>(qb * kGapSample));
+    launch_pdl(PDLPK_PDL_CADENCE, window_keys_kernel, static_cast<unsigned>(1), 1, 0, s, w, ra, rb);
   }
-  const int ra = qa <= 0.0 ? 0 : std::min(kGapSample - 1, static_cast<int>(qa * kGapSample));
-  const bool to_bottom = qb >= 1.0;
-  const int rb = to_bottom ? -1 : std::min(kGapSample - 1, static_cast<int>(qb * kGapSample));
-  launch_pdl(PDLPK_PDL_CADENCE, window_keys_kernel, static_cast<unsigned>(1), 1, 0, s, w, ra, rb);
   launch_pdl(PDLPK_PDL_CADENCE, window_flags_kernel, static_cast<unsigned>(ew_blocks(E)), kT, 0, s, w, E);
   if (ra > 0) {
     const Work wc = w;
@@ -675,9 +774,11 @@ static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const 
                                  static_cast<int>(E), s) != cudaSuccess) {
     return -1;
   }
-  int eh = 0;
+  int eh = 0, est_rb = -1;
   cudaMemcpyAsync(&eh, &w.sc->num_high, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (est) cudaMemcpyAsync(&est_rb, &w.sc->est_rb, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+  if (est) to_bottom = est_rb < 0;
   if (eh <= 0 || eh >= E) return 0;
   bytes = w.cub_bytes;
   if (cub::DeviceRadixSort::SortPairsDescending(w.cub_tmp, bytes, keys_h, w.keys_out, w.hsel,
@@ -718,7 +819,8 @@ extern "C" int pdlpk_gap_finish(const pdlpk_problem* P, const double* x, const d
   const bool parity = red->parity != 0;
   bool decided = false;
   int64_t E_fin = E;  // events the finalize reads (the window's when it decided)
-  if (!parity && qa >= 0.0 && qb > qa && qb - qa < 0.5 && E > (int64_t(1) << 20)) {
+  if (!parity && ((qa >= 0.0 && qb > qa && qb - qa < 0.5) || qa == -2.0) &&
+      E > (int64_t(1) << 20)) {
     const int64_t pr = gap_window(w, E, qa, qb, red, r_slot, r_value, s);
     if (pr < 0) return static_cast<int>(cudaGetLastError());
     decided = pr > 0;

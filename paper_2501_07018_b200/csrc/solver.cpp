@@ -1986,8 +1986,10 @@ class Engine {
     const double *x, *y, *ax, *aty;
     double dx2, dy2;
   };
+  // key0: the window-history slot of q[0] (0 current iterate, 1 window
+  // average; the restart candidate's re-evaluation passes its own)
   void gaps(const InnerCfg& cfg, const pdlpk_problem& P, const GapQuery* q, int count,
-            double omega, double* out) {
+            double omega, double* out, int key0 = 0) {
     const auto gap_t0 = Clock::now();
     struct GapClock {
       double& acc;
@@ -2027,7 +2029,7 @@ class Engine {
       gaps_gathered(cfg, P, q, count, omega, out);
       return;
     }
-    gaps_local(P, q, count, omega, out);
+    gaps_local(P, q, count, omega, out, key0);
   }
 
   // Sharded, PDLP_GAP_GATHERED=1 (and the PDLP_GAPD_CHECK comparison): every
@@ -2238,9 +2240,10 @@ class Engine {
     return gap_windows_[std::make_pair(static_cast<const void*>(P.c), i)];
   }
 
-  void gaps_local(const pdlpk_problem& P, const GapQuery* q, int count, double omega, double* out) {
+  void gaps_local(const pdlpk_problem& P, const GapQuery* q, int count, double omega, double* out,
+                  int key0 = 0) {
     if (gap_shared_ && count > 1) {
-      for (int i = 0; i < count; ++i) gaps_local(P, q + i, 1, omega, out + i);
+      for (int i = 0; i < count; ++i) gaps_local(P, q + i, 1, omega, out + i, key0 + i);
       return;
     }
     const pdlpk_red r = red();
@@ -2280,14 +2283,22 @@ class Engine {
     const auto t_fin = Clock::now();
     double qa[2] = {-1.0, -1.0}, qb[2] = {-1.0, -1.0};
     for (int i = 0; i < count; ++i) {
-      const GapWindow& gw = gap_window_for(P, i);
-      // Default: windows from the top only, whose gap is bit-identical to
-      // the full sort's (nothing is summed outside the sorted order), so the
-      // gap stays a function of its inputs.  PDLP_GAP_WINDOWS=any also
-      // places windows mid-depth and at the bottom (faster for deep or
-      // absent crossings; the masses above such a window are tree-summed,
-      // which changes the gap's last bits).
-      if (!gap_partial_off_ && gw.depth >= 1.0 && gap_any_window_) {
+      const GapWindow& gw = gap_window_for(P, key0 + i);
+      // Windows of the sorted breakpoints around the expected crossing: the
+      // previous evaluation's depth, or, for the first evaluation of a
+      // (subproblem, query), an estimate from a mass-carrying key sample
+      // (qa = qb = -2).  The masses above a window are tree-summed, so the
+      // gap's last bits differ from a full sort's; it stays a function of
+      // its inputs (deterministic), and a window that misses the crossing
+      // falls back to the full sort.  PDLP_GAP_WINDOWS=top keeps windows at
+      // the top of the order (bit-identical to the full sort, rarely
+      // smaller).
+      if (!gap_partial_off_ && gap_any_window_) {
+        // the sample estimate: the previous depth misleads after a restart
+        // or an omega update (measured on C2: history windows missed 4 of
+        // 8 evaluations in a 64-iteration solve, the estimate none)
+        qa[i] = qb[i] = -2.0;
+      } else if (!gap_partial_off_ && gw.depth >= 1.0 && gap_any_window_) {
         qa[i] = 0.9995;  // no crossing last time: only the last ~0.05 % sorted
         qb[i] = 1.0;
       } else if (!gap_partial_off_ && gw.depth >= 0.0 && gw.depth < 1.0) {
@@ -2321,7 +2332,7 @@ class Engine {
                      1e6 * std::chrono::duration<double>(t_end - t_fin).count(), 1e3 * gpu_prep,
                      1e3 * gpu_fin);
       }
-      GapWindow& gw = gap_window_for(P, i);
+      GapWindow& gw = gap_window_for(P, key0 + i);
       if (qb[i] > qa[i] && hit < 1.0 && qa[i] < 0.999) {  // did the crossing fall inside?
         const bool inside = hit >= qa[i] && hit <= qb[i];
         gw.half = inside ? std::max(0.02, 0.75 * gw.half) : std::min(0.24, 2.0 * gw.half);
@@ -2746,7 +2757,7 @@ class Engine {
   }();
   bool gap_any_window_ = [] {
     const char* e = std::getenv("PDLP_GAP_WINDOWS");
-    return e != nullptr && std::strcmp(e, "any") == 0;
+    return !(e != nullptr && std::strcmp(e, "top") == 0);
   }();
   bool gap_partial_off_ = [] {
     const char* e = std::getenv("PDLP_GAP_PARTIAL");
@@ -3037,7 +3048,7 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
             // diff_norm_sq(candidate, ref) is exactly the metric's distance
             D.omega = update_primal_weight(std::sqrt(cq.dx2), std::sqrt(cq.dy2), D.omega);
           }
-          gaps(cfg, P, &cq, 1, D.omega, &D.mu_last);
+          gaps(cfg, P, &cq, 1, D.omega, &D.mu_last, use_current ? 0 : 1);
           if (!use_current) {
             dev_copy(D.x[c].get(), D.avg_x.get(), P.n, s());
             dev_copy(D.y[c].get(), D.avg_y.get(), P.m, s());

@@ -5,7 +5,8 @@ lambda to the first crossing.  k_gap.cu's window path sorts only the events at
 depth fractions [qa, qb] and enters the sweep with the summed masses of the
 events above; it either decides (crossing inside) or falls back to the full
 sort.  Either way the value must equal the full sort's to rounding: the only
-difference is the summation order of the masses above the window.
+difference is the summation order of the masses above the window.  The same
+holds for the estimated window of a first evaluation.
 """
 from __future__ import annotations
 
@@ -14,8 +15,10 @@ import pytest
 
 import paper_2501_07018_b200 as P
 
+# (-2, -2): the window estimated from a mass-carrying key sample (the first
+# evaluation of a restart query)
 WINDOWS = [(0.0, 0.1), (0.0, 0.45), (0.05, 0.3), (0.25, 0.5), (0.4, 0.6), (0.45, 0.55),
-           (0.55, 0.8), (0.7, 0.99), (0.6, 1.0), (0.9995, 1.0)]
+           (0.55, 0.8), (0.7, 0.99), (0.6, 1.0), (0.9995, 1.0), (-2.0, -2.0)]
 
 
 @pytest.mark.gpu
