@@ -25,6 +25,8 @@
 // Translation unit compiled with -fmad=false (see common.cuh).
 
 #include <cub/cub.cuh>
+#include <cstdio>
+#include <cstdlib>
 #include <thrust/iterator/counting_iterator.h>
 
 #include "common.cuh"
@@ -733,8 +735,15 @@ static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const 
     }
     const int margin = static_cast<int>(0.05 * kGapSample);
     estimate_window_kernel<<<1, kEstThreads, 0, s>>>(w, E, r_value, margin);
+    // A deep estimate (or none) comes from a sample that missed a few heavy
+    // breakpoints (C2: estimated depth >= 0.88 for crossings at 0.11-0.63):
+    // go straight to the full sort instead of a window that would miss.
+    int est_h[2] = {0, 0};
+    cudaMemcpyAsync(est_h, &w.sc->est_ra, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+    if (est_h[1] < 0 || est_h[0] > (3 * kGapSample) / 4) return 0;
     launch_pdl(PDLPK_PDL_CADENCE, window_keys_est_kernel, static_cast<unsigned>(1), 1, 0, s, w);
-    ra = 1;  // (unknown on the host: the above-mass reduction always runs)
+    ra = est_h[0];
   } else {
     launch_pdl(PDLPK_PDL_CADENCE, sample_keys_kernel, static_cast<unsigned>(ew_blocks(kGapSample)), kT, 0, s, w, E);
     if (cub::DeviceRadixSort::SortKeysDescending(w.cub_tmp, bytes, w.samp_in, w.samp_out, kGapSample,
@@ -798,6 +807,13 @@ static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const 
   cudaMemcpyAsync(&h.first, &w.sc->first, sizeof(h.first), cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(&h.above, &w.sc->above_count, sizeof(h.above), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+  static const bool dbg = std::getenv("PDLP_GAP_DEBUG") != nullptr;
+  if (dbg && est) {
+    int ra_h = 0;
+    cudaMemcpy(&ra_h, &w.sc->est_ra, sizeof(int), cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "gap window est: ranks [%d, %d] of %d, window events %d, first %lld, above %llu\n",
+                 ra_h, est_rb, kGapSample, eh, static_cast<long long>(h.first), h.above);
+  }
   if (h.first == ~0ull) return to_bottom ? eh : 0;
   if (h.first == 0 && h.above > 0) return 0;
   return eh;
