@@ -548,6 +548,31 @@ def test_multi_vector_cadence_products_bit_identical(gpu, monkeypatch):
     assert a.restarts > 0  # the cadence (incl. restarts to the average) ran
 
 
+@pytest.mark.parametrize("mode", ["perf", "parity"])
+def test_side_stream_cadence_on_multi_chunk_lines(gpu, monkeypatch, mode):
+    # The cadence's window-average share runs on a side stream with its own
+    # chunk scratch (chunk partials, arrival counters, line accumulators)
+    # while the main stream runs the same kernels on the same layouts.  On
+    # a layout with lines cut into several CTA chunks (> 2,048 entries) the
+    # overlapped cadence must give the bits of the serial one
+    # (PDLP_GAP_SERIAL=1), restart decisions included.
+    p = P.generate("c2", 5, rows=5000, cols=6000, kmax=5000)
+    assert np.diff(p.a.by_col.start).max() > 2048
+    tol = P.relative_tolerances(p)
+    o = P.SolverOptions(tolerances=P.TerminationTolerances(*tol), iteration_limit=1500)
+    o.mode = mode
+    monkeypatch.setenv("PDLP_SEG", "0")    # tile schedule with chunked lines
+    monkeypatch.setenv("PDLP_MULTI", "0")  # single-vector cadence products: the side stream is used
+    monkeypatch.setenv("PDLP_GAP_SERIAL", "1")
+    a = P.solve(p, o)
+    monkeypatch.setenv("PDLP_GAP_SERIAL", "0")
+    for _ in range(3):
+        b = P.solve(p, o)
+        assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
+        assert same_bits(a.x, b.x) and same_bits(a.y, b.y)
+    assert a.restarts > 0
+
+
 @pytest.mark.parametrize("knobs", [{"PDLP_ROW_PANELS": "2"}, {"PDLP_ROW_PANELS": "3", "PDLP_SEG": "1"},
                                    {"PDLP_SEG": "1", "PDLP_MULTI": "1"}])
 def test_forced_schedules_on_ragged_problems(gpu, ref, monkeypatch, knobs):

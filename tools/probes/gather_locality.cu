@@ -101,6 +101,26 @@ __global__ void __launch_bounds__(256) stream_gather_hot(const int32_t* __restri
   }
   if (acc == 12345.678) out[0] = acc;
 }
+// Hot columns held in shared memory: a 1,024-thread CTA per SM copies
+// v[0, H) into shared memory once and serves gathers of columns < H from
+// there (bank-conflicted but off the L1 tag stage); the rest go to L1/L2.
+template <int U>
+__global__ void __launch_bounds__(1024) stream_gather_smem(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                                          const double* __restrict__ v, int64_t nnz, int32_t H, double* out) {
+  extern __shared__ double hot[];
+  for (int32_t j = threadIdx.x; j < H; j += blockDim.x) hot[j] = v[j];
+  __syncthreads();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int64_t b = tid; b < nnz; b += nt * U) {
+    int32_t ci[U]; double a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) { const int64_t k = b + u * nt; ci[u] = k < nnz ? __ldcs(idx + k) : 0; a[u] = k < nnz ? __ldcs(val + k) : 0.0; }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += a[u] * (ci[u] < H ? hot[ci[u]] : __ldg(v + ci[u]));
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
 template <class F> float time_it(F f, int reps) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   f(); cudaDeviceSynchronize();
@@ -161,6 +181,15 @@ int main() {
         std::printf("smem %3d KB/SM %d CTA/SM  sorted, hot H=%5d via L1 (%3d KB): %8.1f us\n", smem_kb, per, H, H * 8 / 1024, us);
       }
     }
+  }
+  // hot columns in shared memory (degree-sorted draw), one 1,024-thread CTA per SM
+  cudaFuncSetAttribute(stream_gather_smem<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(stream_gather_smem<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int H : {0, 4096, 8192, 16384, 24576}) {
+    const size_t sm = static_cast<size_t>(H) * 8;
+    float us4 = time_it([&] { stream_gather_smem<4><<<sms, 1024, sm>>>(is, val, v, nnz, H, out); }, reps);
+    float us8 = time_it([&] { stream_gather_smem<8><<<sms, 1024, sm>>>(is, val, v, nnz, H, out); }, reps);
+    std::printf("hot H=%5d in shared memory (%3d KB), 1 x 1024 threads/SM: U=4 %8.1f us  U=8 %8.1f us\n", H, H * 8 / 1024, us4, us8);
   }
   return 0;
 }
