@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <map>
@@ -268,4 +269,16 @@ inline double elapsed_seconds(const Event& a, const Event& b) {
   return static_cast<double>(ms) * 1e-3;
 }
 
+}  // namespace pdlp_host
+
+// NVTX phase ranges (tracing): upload / precondition / attempts /
+// cadence / gap / polish.  nvtx3 is header-only and inert unless a profiler
+// injects itself (ncu --nvtx, Nsight Systems); no library is linked.
+namespace pdlp_host {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 }  // namespace pdlp_host

@@ -387,6 +387,18 @@ __global__ void sample_masses_kernel(Work w, int64_t E) {
   }
 }
 
+// The sample's masses in sorted order (w.cs / w.bs are free until the window
+// is selected), so the one-CTA scan below reads them with independent,
+// pipelined loads instead of a dependent gather per sample rank.
+__global__ void sorted_masses_kernel(Work w) {
+  pdl_wait_cadence();
+  GRID_STRIDE(j, kGapSample) {
+    const int32_t q = w.sidx_out[j];
+    w.cs[j] = w.sdc[q];
+    w.bs[j] = w.sdi[q];
+  }
+}
+
 constexpr int kEstThreads = 1024;
 constexpr int kEstPer = kGapSample / kEstThreads;
 __global__ void __launch_bounds__(kEstThreads) estimate_window_kernel(Work w, int64_t E, double r,
@@ -396,10 +408,10 @@ __global__ void __launch_bounds__(kEstThreads) estimate_window_kernel(Work w, in
   const double r2 = r * r;
   const int j0 = threadIdx.x * kEstPer;
   double c = 0.0, b = 0.0;
+#pragma unroll 16
   for (int j = j0; j < j0 + kEstPer; ++j) {
-    const int32_t q = w.sidx_out[j];
-    c += w.sdc[q];
-    b += w.sdi[q];
+    c += w.cs[j];
+    b += w.bs[j];
   }
   using Scan = cub::BlockScan<double, kEstThreads>;
   __shared__ typename Scan::TempStorage tmp;
@@ -411,17 +423,17 @@ __global__ void __launch_bounds__(kEstThreads) estimate_window_kernel(Work w, in
   if (threadIdx.x == 0) hit = kGapSample;
   __syncthreads();
   double cs = cx, bs = bx;  // sample masses above rank j
+  const double s0 = w.sc->sums[0], s1 = w.sc->sums[1];
+  int first = kGapSample;   // this thread's first rank with phi >= r^2 (no early exit: loads stay independent)
+#pragma unroll 8
   for (int j = j0; j < j0 + kEstPer; ++j) {
     const double lam = key_value(w.samp_out[j]);
-    const double phi = (w.sc->sums[1] + scale * cs) + (w.sc->sums[0] + scale * bs) / (lam * lam);
-    if (phi >= r2) {
-      atomicMin(&hit, j);
-      break;
-    }
-    const int32_t q = w.sidx_out[j];
-    cs += w.sdc[q];
-    bs += w.sdi[q];
+    const double phi = (s1 + scale * cs) + (s0 + scale * bs) / (lam * lam);
+    if (phi >= r2 && first == kGapSample) first = j;
+    cs += w.cs[j];
+    bs += w.bs[j];
   }
+  if (first < kGapSample) atomicMin(&hit, first);
   __syncthreads();
   if (threadIdx.x == 0) {
     const int h = hit;
@@ -734,6 +746,7 @@ static int64_t gap_window(const Work& w, int64_t E, double qa, double qb, const 
       return -1;
     }
     const int margin = static_cast<int>(0.05 * kGapSample);
+    launch_pdl(PDLPK_PDL_CADENCE, sorted_masses_kernel, static_cast<unsigned>(ew_blocks(kGapSample)), kT, 0, s, w);
     estimate_window_kernel<<<1, kEstThreads, 0, s>>>(w, E, r_value, margin);
     // A deep estimate (or none) comes from a sample that missed a few heavy
     // breakpoints (C2: estimated depth >= 0.88 for crossings at 0.11-0.63):

@@ -941,6 +941,7 @@ class Engine {
 
   // ---- setup -------------------------------------------------------------
   void load(const pdlp_problem_view* p) {
+    NvtxRange nvtx("pdlp:upload");
     const auto t0 = Clock::now();
     if (comm_ == nullptr) {
       m_glob_ = p->rows;
@@ -1483,6 +1484,7 @@ class Engine {
 
   // apply_rescaling (rescaling.hpp:137-143) on device, both layouts in place.
   void precondition(int ruiz_passes, bool pock_chambolle) {
+    NvtxRange nvtx("pdlp:precondition");
     const auto t0 = Clock::now();
     const int64_t m = prob_.m, n = prob_.n;
     // fc spans every column of the layouts (all n under the row cut), fr
@@ -1706,6 +1708,7 @@ class Engine {
 
   // Runs step attempts until k reaches target or the controller halts.
   void run_steps(const pdlpk_problem& P, Inner& D, int64_t target) {
+    NvtxRange nvtx("pdlp:attempts");
     ensure_table(target + 1);
     pdlpk_step_args a = step_args(P, D);
     PDLP_LAUNCH(pdlpk_arm(D.state.get(), target, s()));
@@ -1990,6 +1993,7 @@ class Engine {
   // average; the restart candidate's re-evaluation passes its own)
   void gaps(const InnerCfg& cfg, const pdlpk_problem& P, const GapQuery* q, int count,
             double omega, double* out, int key0 = 0) {
+    NvtxRange nvtx("pdlp:gap");
     const auto gap_t0 = Clock::now();
     struct GapClock {
       double& acc;
@@ -2793,6 +2797,7 @@ class Engine {
 
 bool Engine::attempt_polish(const pdlpk_problem& P, const InnerCfg& cfg, Inner& D) {
   // solver.hpp:290-348
+  NvtxRange nvtx("pdlp:polish");
   const auto pol_t0 = Clock::now();
   struct PolishClock {
     double& acc;
@@ -2858,6 +2863,7 @@ int Engine::run_inner(const pdlpk_problem& P, const pdlpk_problem&, const InnerC
     const bool budget_hit = D.k() >= cfg.budget;
     const bool at_cadence = budget_hit || (D.k() % cfg.check_interval == 0);
     if (at_cadence) {
+      NvtxRange nvtx("pdlp:cadence");
       const auto cad_t0 = Clock::now();
       struct CadenceClock {  // adds the cadence's host time on every exit
         double& acc;
