@@ -146,6 +146,20 @@ def test_c2_full_first_iterates_perf(gpu, ref, c2):
 
 
 # ------------------------------------------------------ C2 / C3 mid-size ---
+def test_c2_full_perf_mode_is_deterministic(gpu, c2):
+    """on layouts of >= 16M entries the schedule is a
+    function of the line lengths (no timed autotuning), the step reductions
+    combine in a fixed order and the gap's window placement is a function of
+    its inputs -- two perf solves of the headline instance across a 64-step
+    cadence (screens, ray tests, gap evaluations, a restart decision) give
+    the same bits."""
+    o = _opts(70)
+    a, b = P.solve(c2, o), P.solve(c2, o)
+    assert (a.iterations, a.restarts, a.step_retries) == (b.iterations, b.restarts, b.step_retries)
+    assert a.final_step_size == b.final_step_size and a.final_primal_weight == b.final_primal_weight
+    assert same_bits(a.x, b.x) and same_bits(a.y, b.y)
+
+
 @pytest.mark.parametrize("force", [None, "seg", "panels"])
 def test_c2_mid_first_100_iterates_perf(gpu, ref, monkeypatch, force):
     """C2 recipe at 200k x 400k: first 100 iterates, with the default
