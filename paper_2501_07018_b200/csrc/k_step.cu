@@ -20,6 +20,8 @@
 //
 // Translation unit compiled with -fmad=false (see common.cuh).
 
+#include <cub/device/device_scan.cuh>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "spmv.cuh"
@@ -359,6 +361,123 @@ __global__ void __launch_bounds__(kSpmvThreads, spmv_min_blocks(Seg)) row_pass(p
   if (threadIdx.x == 0) {
     a.part2[blockIdx.x] = s1;
     a.part2[gridDim.x + blockIdx.x] = s2;
+  }
+}
+
+// ------------------------------------------- sliced-ELL row pass (knob) ---
+// PDLP_ROW_SELL=1: the row pass over the SELL-32 copy of the row layout
+// (kernels.h pdlpk_step_args::sell).  One warp per slice of 32 rows, lane =
+// row; index and value loads are coalesced straight from global memory, each
+// lane adds its row's products in storage order (the sums of the tile path's
+// storage-order lines), the dual update runs in the same lane.
+#ifndef PDLPK_SELL_UNROLL
+#define PDLPK_SELL_UNROLL 8
+#endif
+#ifndef PDLPK_SELL_MINB
+#define PDLPK_SELL_MINB 4
+#endif
+constexpr int kSellUnroll = PDLPK_SELL_UNROLL;
+template <class P>
+__global__ void __launch_bounds__(kSpmvThreads, PDLPK_SELL_MINB) row_pass_sell(pdlpk_step_args a) {
+  pdl_wait();
+  pdlpk_step_state* st = a.state;
+  if (st->halt) return;
+  const int cur = st->cur;
+  RowEpiT<false> e;
+  e.y = a.y[cur];
+  e.yn = a.y[cur ^ 1];
+  e.dy = a.dy;
+  e.lc = a.P.lc;
+  e.uc = a.P.uc;
+  e.sy = a.sum_y;
+  e.sigma = st->eta * st->omega;
+  e.pend = st->avg_pending != 0;
+  e.w = st->avg_w;
+  if (a.line_partials) {
+    e.lp = a.part2;
+    e.lm = a.P.m;
+  }
+  const P* __restrict__ start = static_cast<const P*>(a.P.K.start);
+  const double* __restrict__ v = a.xbar;
+  const int64_t m = a.P.K.dim;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t g = w0; g < a.sell.ng; g += nw) {
+    const int64_t r = g * 32 + lane;
+    const bool live = r < m;
+    const int32_t n = live ? static_cast<int32_t>(start[r + 1] - start[r]) : 0;
+    const int64_t o = a.sell.off[g];
+    const int32_t w = static_cast<int32_t>((a.sell.off[g + 1] - o) >> 5);
+    RowEpiT<false>::Pre pre{};
+    if (live) pre = e.load(r);
+    const int32_t* __restrict__ pi = a.sell.sidx + o + lane;
+    const double* __restrict__ pv = a.sell.sval + o + lane;
+    double acc = 0.0;
+    for (int32_t k = 0; k < w; k += kSellUnroll) {
+      int32_t c[kSellUnroll];
+      double x[kSellUnroll], t[kSellUnroll];
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) {
+        const bool on = k + u < n;
+        c[u] = on ? ld_stream(pi + 32 * (k + u)) : 0;
+        x[u] = on ? ld_stream(pv + 32 * (k + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) t[u] = (k + u < n) ? __ldg(v + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kSellUnroll; ++u) {
+        if (k + u < n) acc = mac(acc, x[u], t[u]);
+      }
+    }
+    if (live) e.line(r, acc, pre);
+  }
+  pdl_trigger();
+  if (a.line_partials) return;
+  __shared__ double red[32];
+  const double s1 = block_sum(e.dy2, red);
+  __syncthreads();
+  const double s2 = block_max(e.infy, red);
+  if (threadIdx.x == 0) {
+    a.part2[blockIdx.x] = s1;
+    a.part2[gridDim.x + blockIdx.x] = s2;
+  }
+}
+
+// SELL build: 32 x the longest line of each slice, and the scatter of the
+// row layout's entries to their slots (padding slots are never read).
+template <class P>
+__global__ void sell_width_kernel(const P* __restrict__ start, int64_t m, int64_t ng,
+                                  int64_t* __restrict__ w32) {
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < ng;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t w = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int64_t r = g * 32 + l;
+      if (r < m) {
+        const int64_t len = static_cast<int64_t>(start[r + 1] - start[r]);
+        w = len > w ? len : w;
+      }
+    }
+    w32[g] = 32 * w;
+  }
+}
+template <class P>
+__global__ void sell_fill_kernel(const P* __restrict__ start, const int32_t* __restrict__ idx,
+                                 const double* __restrict__ val, int64_t m,
+                                 const int64_t* __restrict__ off, int32_t* __restrict__ sidx,
+                                 double* __restrict__ sval) {
+  // one warp per row: coalesced reads of the row, 128-byte-strided writes
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = w0; r < m; r += nw) {
+    const int64_t b = static_cast<int64_t>(start[r]), e = static_cast<int64_t>(start[r + 1]);
+    const int64_t base = off[r >> 5] + (r & 31);
+    for (int64_t k = b + lane; k < e; k += 32) {
+      sidx[base + 32 * (k - b)] = idx[k];
+      sval[base + 32 * (k - b)] = val[k];
+    }
   }
 }
 
@@ -914,6 +1033,41 @@ extern "C" int64_t pdlpk_step_partials(const pdlpk_problem* P) {
   return need + 64;
 }
 
+extern "C" int pdlpk_sell_plan(const pdlpk_csr* K, int64_t* w32, int64_t* off, void* tmp,
+                               size_t* tmp_bytes, cudaStream_t s) {
+  const int64_t ng = (K->dim + 31) / 32;
+  if (tmp == nullptr) {
+    *tmp_bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, *tmp_bytes, w32, off + 1, static_cast<int>(ng), s);
+    return static_cast<int>(cudaGetLastError());
+  }
+  if (ng <= 0) return 0;
+  const unsigned g = static_cast<unsigned>(std::min<int64_t>((ng + 255) / 256, 148 * 8));
+  if (K->wide) {
+    sell_width_kernel<<<g, 256, 0, s>>>(static_cast<const int64_t*>(K->start), K->dim, ng, w32);
+  } else {
+    sell_width_kernel<<<g, 256, 0, s>>>(static_cast<const int32_t*>(K->start), K->dim, ng, w32);
+  }
+  cudaMemsetAsync(off, 0, sizeof(int64_t), s);
+  size_t bytes = *tmp_bytes;
+  cub::DeviceScan::InclusiveSum(tmp, bytes, w32, off + 1, static_cast<int>(ng), s);
+  return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int pdlpk_sell_fill(const pdlpk_csr* K, const int64_t* off, int32_t* sidx, double* sval,
+                               cudaStream_t s) {
+  if (K->dim <= 0) return 0;
+  const unsigned g = 148 * 16;
+  if (K->wide) {
+    sell_fill_kernel<<<g, 256, 0, s>>>(static_cast<const int64_t*>(K->start), K->index, K->value,
+                                       K->dim, off, sidx, sval);
+  } else {
+    sell_fill_kernel<<<g, 256, 0, s>>>(static_cast<const int32_t*>(K->start), K->index, K->value,
+                                       K->dim, off, sidx, sval);
+  }
+  return static_cast<int>(cudaGetLastError());
+}
+
 extern "C" int pdlpk_arm(pdlpk_step_state* st, int64_t k_target, cudaStream_t s) {
   arm_kernel<<<1, 1, 0, s>>>(st, k_target);
   return static_cast<int>(cudaGetLastError());
@@ -923,6 +1077,21 @@ extern "C" int pdlpk_arm(pdlpk_step_state* st, int64_t k_target, cudaStream_t s)
 // returned args are the column pass's: with panels its decision reads the
 // last panel launch's partials, so P.K is that layout.
 static pdlpk_step_args launch_row(const pdlpk_step_args* a, cudaStream_t s, bool pdl) {
+  if (a->sell.off != nullptr) {
+    const unsigned g = static_cast<unsigned>(a->sell.blocks);
+    if (a->P.K.wide) {
+      launch_pdl(pdl, row_pass_sell<int64_t>, g, kSpmvThreads, static_cast<size_t>(0), s, *a);
+    } else {
+      launch_pdl(pdl, row_pass_sell<int32_t>, g, kSpmvThreads, static_cast<size_t>(0), s, *a);
+    }
+    // the decision reads this pass's per-CTA partials: a layout view that
+    // only says how many there are (sched_blocks) and has no line slots
+    pdlpk_step_args b = *a;
+    b.P.K.seg_mode = 1;
+    b.P.K.tile_blocks = a->sell.blocks;
+    b.P.K.n_multi = 0;
+    return b;
+  }
   if (a->n_row_panels < 2 || a->row_panels == nullptr) {
     dispatch_p(a->P.K, LaunchRowCol{a, s, true, true, pdl});
     return *a;

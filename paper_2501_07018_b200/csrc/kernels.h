@@ -221,7 +221,27 @@ typedef struct pdlpk_step_args {
   int32_t _pad_panel;
   const pdlpk_csr* row_panels; /* host pointer: read by the launch code only */
   double* carry;               /* m */
+  /* Sliced-ELL copy of the row layout (measurement knob PDLP_ROW_SELL=1,
+   * perf mode, one GPU): rows in slices of 32 in their natural order, entry
+   * k of the slice's lane l at off[g] + 32 k + l, so a warp's index and value
+   * loads are coalesced without staging and each lane sums its own row in
+   * storage order.  off == NULL: not built.  blocks = CTAs of the pass (its
+   * per-CTA partials). */
+  struct {
+    const int64_t* off; /* ng + 1 */
+    const int32_t* sidx;
+    const double* sval;
+    int64_t ng;
+    int32_t blocks;
+    int32_t _pad;
+  } sell;
 } pdlpk_step_args;
+
+/* SELL build (k_step.cu): slice offsets from the row layout's line lengths
+ * (tmp == NULL: only *tmp_bytes is set), then the scatter of its entries. */
+int pdlpk_sell_plan(const pdlpk_csr* K, int64_t* w32, int64_t* off, void* tmp, size_t* tmp_bytes,
+                    cudaStream_t s);
+int pdlpk_sell_fill(const pdlpk_csr* K, const int64_t* off, int32_t* sidx, double* sval, cudaStream_t s);
 #define PDLPK_MAX_ROW_PANELS 8
 
 /* Device pointers of the column panels (k_vec.cu pdlpk_panel_scatter). */

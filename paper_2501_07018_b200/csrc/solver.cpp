@@ -1640,6 +1640,13 @@ class Engine {
     a.shard_part = D.shard_part.get();
     a.line_partials = (!parity_ && !dist() && P.m <= PDLPK_LINE_PARTIALS_MAX && line_partials_on_)
                           ? 1 : 0;
+    if (!parity_ && uses_sell(P)) {
+      a.sell.off = sell_off_.get();
+      a.sell.sidx = sell_idx_.get();
+      a.sell.sval = sell_val_.get();
+      a.sell.ng = sell_ng_;
+      a.sell.blocks = sell_blocks_;
+    }
     if (!parity_ && uses_panels(P)) {
       a.n_row_panels = panels_.np;
       a.row_panels = panels_.views.data();
@@ -1668,6 +1675,7 @@ class Engine {
       Q.K = panels_.views.back();
       partials = std::max(partials, pdlpk_step_partials(&Q));
     }
+    if (uses_sell(P)) partials = std::max<int64_t>(partials, 2 * static_cast<int64_t>(sell_blocks_) + 64);
     if (dist()) {
       partials = std::max<int64_t>(partials, 3 * pdlpk_dist_ew_grid(std::max(P.n, P.m)) + 64);
     }
@@ -2680,7 +2688,55 @@ class Engine {
   }
 
   bool uses_panels(const pdlpk_problem& P) const {
-    return panels_.np >= 2 && P.K.index == prob_.row.view.index;
+    return panels_.np >= 2 && P.K.index == prob_.row.view.index && !sell_ready_;
+  }
+
+  // ---- sliced-ELL row pass (measurement knob PDLP_ROW_SELL=1) -------------
+  // Perf mode, one GPU: a SELL-32 copy of the scaled row layout (kernels.h
+  // pdlpk_step_args::sell) built after preconditioning; the step's row pass
+  // then runs row_pass_sell on the main problem and the primal polishing
+  // subproblem (the same K).  Lab numbers and why it is off: DESIGN section 4.
+  DevBuf<int64_t> sell_off_, sell_w32_;
+  DevBuf<int32_t> sell_idx_;
+  DevBuf<double> sell_val_;
+  DevBuf<unsigned char> sell_tmp_;
+  int64_t sell_ng_ = 0;
+  int32_t sell_blocks_ = 0;
+  bool sell_ready_ = false;
+  void build_sell() {
+    sell_ready_ = false;
+    const char* e = std::getenv("PDLP_ROW_SELL");
+    if (e == nullptr || e[0] != '1' || parity_ || comm_ != nullptr) return;
+    const pdlpk_csr& K = prob_.row.view;
+    if (K.dim <= 0 || K.nnz <= 0) return;
+    sell_ng_ = (K.dim + 31) / 32;
+    sell_off_.alloc(static_cast<size_t>(sell_ng_ + 1));
+    sell_w32_.alloc(static_cast<size_t>(sell_ng_));
+    size_t tb = 0;
+    PDLP_LAUNCH(pdlpk_sell_plan(&K, sell_w32_.get(), sell_off_.get(), nullptr, &tb, s()));
+    sell_tmp_.alloc(tb + 16);
+    PDLP_LAUNCH(pdlpk_sell_plan(&K, sell_w32_.get(), sell_off_.get(), sell_tmp_.get(), &tb, s()));
+    int64_t slots = 0;
+    PDLP_CK(cudaMemcpyAsync(&slots, sell_off_.get() + sell_ng_, sizeof(int64_t), cudaMemcpyDeviceToHost, s()));
+    PDLP_CK(cudaStreamSynchronize(s()));
+    if (slots <= 0 || slots > 4 * K.nnz + 32 * sell_ng_) return;  // padding out of hand: keep the tiles
+    sell_idx_.alloc(static_cast<size_t>(slots));
+    sell_val_.alloc(static_cast<size_t>(slots));
+    PDLP_LAUNCH(pdlpk_sell_fill(&K, sell_off_.get(), sell_idx_.get(), sell_val_.get(), s()));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt_.device);
+    int per_sm = 4;  // PDLP_SELL_CTAS: CTAs per SM of the pass (measurement)
+    if (const char* c = std::getenv("PDLP_SELL_CTAS")) per_sm = std::max(1, std::atoi(c));
+    sell_blocks_ = static_cast<int32_t>(std::min<int64_t>(static_cast<int64_t>(per_sm) * sms, (sell_ng_ + 7) / 8));
+    sell_ready_ = true;
+    if (opt_.logging) {
+      std::fprintf(stderr, "phase=setup event=row_sell slices=%lld slots=%lld padding=%.3f\n",
+                   static_cast<long long>(sell_ng_), static_cast<long long>(slots),
+                   static_cast<double>(slots) / static_cast<double>(K.nnz));
+    }
+  }
+  bool uses_sell(const pdlpk_problem& P) const {
+    return sell_ready_ && P.K.index == prob_.row.view.index && P.K.value == prob_.row.view.value;
   }
 
   // ---- multi-vector cadence products (k_multi.cu) ------------------------
@@ -3196,6 +3252,7 @@ void solve(const pdlp_problem_view* problem, const pdlp_options* opts, pdlp_resu
   if (!E.dist()) {
     E.join_panels();
     E.fill_panels();
+    E.build_sell();
   }
   if (E.dist() && E.gap_whole()) E.build_full_views();
   // Polishing is only considered at a cadence point k >= 100 below the

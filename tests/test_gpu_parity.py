@@ -529,6 +529,25 @@ def test_row_panels_bit_identical(gpu, monkeypatch):
         assert same_bits(a.x, b.x) and same_bits(a.y, b.y), np_
 
 
+def test_row_sell_bit_identical(gpu, monkeypatch):
+    # The sliced-ELL row pass (PDLP_ROW_SELL=1: lane per row, coalesced
+    # slice-column-major streams) adds each row's products in storage order,
+    # like the tile path's short lines, and the step's row-pass reductions are
+    # per line here (m <= PDLPK_LINE_PARTIALS_MAX): bit-identical iterates,
+    # across cadences, restarts and polishing attempts.
+    p = P.generate("c2", 2, rows=20000, cols=40000, kmax=400)
+    assert np.diff(p.a.by_row.start).max() <= 64  # every row in the storage-order tile path
+    tol = P.relative_tolerances(p)
+    o = P.SolverOptions(tolerances=P.TerminationTolerances(*tol), iteration_limit=600)
+    monkeypatch.setenv("PDLP_ROW_PANELS", "0")
+    a = P.solve(p, o)
+    monkeypatch.setenv("PDLP_ROW_SELL", "1")
+    b = P.solve(p, o)
+    assert (a.status, a.iterations, a.restarts) == (b.status, b.iterations, b.restarts)
+    assert same_bits(a.x, b.x) and same_bits(a.y, b.y)
+    assert a.iterations == 600 or a.status == P.SolveStatus.OPTIMAL
+
+
 def test_multi_vector_cadence_products_bit_identical(gpu, monkeypatch):
     # The cadence's products through one multi-vector pass per layout
     # (k_multi.cu: current + average through K; current + average + the
@@ -574,7 +593,7 @@ def test_side_stream_cadence_on_multi_chunk_lines(gpu, monkeypatch, mode):
 
 
 @pytest.mark.parametrize("knobs", [{"PDLP_ROW_PANELS": "2"}, {"PDLP_ROW_PANELS": "3", "PDLP_SEG": "1"},
-                                   {"PDLP_SEG": "1", "PDLP_MULTI": "1"}])
+                                   {"PDLP_SEG": "1", "PDLP_MULTI": "1"}, {"PDLP_ROW_SELL": "1"}])
 def test_forced_schedules_on_ragged_problems(gpu, ref, monkeypatch, knobs):
     # Column panels, segmented spans and multi-vector cadence products forced
     # onto small ragged LPs (empty rows and columns, lines shorter and longer
