@@ -104,7 +104,9 @@ def test_c1_full_solve_to_1e4(gpu, ref, c1):
     across its own shard plans (x1.5 margin)."""
     tol = P.relative_tolerances(c1)
     r4 = ref.solve(c1, _opts(200000, spt=4, tol=tol))
-    r1 = ref.solve(c1, _opts(200000, spt=1, tol=tol))
+    # a second shard plan of the reference (~45 s of host time) only on request:
+    # its spread is recorded over 5 seeds in profiles/r2_c1_seeds_vs_reference.jsonl
+    r1 = ref.solve(c1, _opts(200000, spt=1, tol=tol)) if os.environ.get("PDLP_LONG_TESTS") == "1" else r4
     g = P.solve(c1, _opts(200000, tol=tol))
     assert g.status == r4.status == r1.status == P.SolveStatus.OPTIMAL
     s = g.summary
@@ -114,7 +116,7 @@ def test_c1_full_solve_to_1e4(gpu, ref, c1):
     lo = min(r4.iterations, r1.iterations)
     hi = max(r4.iterations, r1.iterations)
     print(f"C1 1e-4: gpu perf {g.iterations} it ({g.restarts} restarts), reference "
-          f"{r4.iterations} (S=4x{THREADS}) / {r1.iterations} (S=1x{THREADS})")
+          f"{r4.iterations} (S=4x{THREADS})" + (f" / {r1.iterations} (S=1x{THREADS})" if r1 is not r4 else ""))
     assert lo / 1.5 <= g.iterations <= hi * 1.5
 
 
